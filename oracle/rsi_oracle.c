@@ -218,7 +218,10 @@ int rsi_oracle_run(const float* V, int64_t nv, const int32_t* T, int64_t nt,
             int64_t best_j = -1;
             double best_t = 0.0;
             unsigned f = 0u;
-            for (int64_t j = 0; j < nt; ++j) {
+            /* reading R12: a segment with a NaN/Inf coordinate is a miss */
+            int finite = isfinite(O[0]) && isfinite(O[1]) && isfinite(O[2]) &&
+                         isfinite(Ee[0]) && isfinite(Ee[1]) && isfinite(Ee[2]);
+            for (int64_t j = 0; finite && j < nt; ++j) {
                 const int32_t* tj = T + 3 * j;
                 double A[3] = {V[3 * tj[0]], V[3 * tj[0] + 1], V[3 * tj[0] + 2]};
                 double B[3] = {V[3 * tj[1]], V[3 * tj[1] + 1], V[3 * tj[1] + 2]};

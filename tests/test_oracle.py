@@ -235,6 +235,11 @@ def test_degenerate_inputs_and_validation():
     Vd = np.float32([[0, 0, 0], [1, 1, 1], [2, 2, 2]])
     r = oracle.run(Vd, np.int32([[0, 1, 2]]), np.float32([[1, 1, 0]]), np.float32([[1, 1, 2]]))
     assert r["hit"][0] == 0
+    # reading R12: a segment with a NaN / Inf coordinate is a miss
+    S = np.float32([[12.5, 2.2, np.nan], [np.inf, 2.2, 2.0], [12.7, 2.2, 2.0]])
+    E = np.float32([[12.5, 2.2, 0.0], [12.7, 2.2, 0.0], [12.7, 2.2, -np.inf]])
+    r = oracle.run(V, T, S, E)
+    assert r["hit"].tolist() == [0, 0, 0] and r["count"].tolist() == [0, 0, 0]
     with pytest.raises(ValueError):
         oracle.run(V, np.int32([[0, 1, 5]]), p, p)
     with pytest.raises(TypeError):

@@ -1,0 +1,214 @@
+/*
+ * rsi.h -- C-ABI of the B200-native segment x triangle-mesh intersection
+ * library (arXiv 2305.01867 and its CUDA predecessor arXiv 2209.02878).
+ *
+ * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n, SURVEY 8(b).
+ *
+ * Problem (section 1 "Background"): N_r line segments ("rays")
+ * l_i = (r_i^start, r_i^end) are tested against a surface of N_t triangles
+ * t_j = [t_j1, t_j2, t_j3] indexing vertices {v_n}.  A linear BVH built from
+ * Morton codes of the triangles and a binary radix tree prunes the candidate
+ * triangles; each candidate is tested with Moller-Trumbore.
+ * Three modes: boolean, barycentric (nearest intersecting triangle,
+ * distance and point), intercept_count (number of unique intersections).
+ *
+ * Conventions for every entry point
+ *   - Pointers prefixed d_ are DEVICE pointers on the current CUDA device;
+ *     h_ are HOST pointers.  Arrays are dense, C-order, little-endian.
+ *   - Points are float32 [n][3] (x, y, z); triangle indices are int32 [n][3]
+ *     (the int32-everywhere lesson of case study 1, P:272-299, P:498 -- a
+ *     64-bit index array passed here is a caller bug the Python binding
+ *     rejects rather than casting).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Device work is stream-ordered; calls return when work is ENQUEUED unless
+ *     stated otherwise.
+ *   - Every call returns rsi_status_t.  On failure rsi_last_error() returns a
+ *     thread-local message; CUDA errors are never swallowed.
+ *   - The library is thread-compatible: a handle may be used by one thread at a
+ *     time; distinct handles are independent.
+ */
+#ifndef RSI_H_
+#define RSI_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    RSI_OK = 0,
+    RSI_E_INVALID_ARG = 1, /* null pointer, negative size, bad mode, bad options       */
+    RSI_E_EMPTY = 2,       /* N_t == 0 or N_v == 0 ("empty mesh")                 */
+    RSI_E_INDEX_RANGE = 3, /* a triangle index outside [0, N_v)                 */
+    RSI_E_NONFINITE = 4,   /* a NaN / Inf vertex coordinate                   */
+    RSI_E_CUDA = 5,        /* a CUDA runtime error; message has cudaGetErrorString      */
+    RSI_E_OOM = 6,         /* device allocation failed                                  */
+    RSI_E_INTEGRITY = 7    /* BVH validator found a violation               */
+} rsi_status_t;
+
+/* Modes. */
+typedef enum {
+    RSI_MODE_BOOLEAN = 0,        /* P:26 "(N_r,1) boolean array"                        */
+    RSI_MODE_BARYCENTRIC = 1,    /* P:27 nearest triangle, distance and point           */
+    RSI_MODE_INTERCEPT_COUNT = 2 /* P:28 "number of unique intersections"               */
+} rsi_mode_t;
+
+/* Option bits (rsi_options_t.flags). */
+#define RSI_OPT_FP64_MOLLER 1u /* every Moller-Trumbore test in double precision: the
+                                  paper's USE_DOUBLE_PRECISION_MOLLER.  Results
+                                  are identical either way; only speed differs. */
+
+typedef struct {
+    uint32_t struct_size; /* sizeof(rsi_options_t); 0 or a NULL options pointer = defaults   */
+    uint32_t flags;       /* RSI_OPT_* bits (default 0)                                      */
+    double dedup_tau;     /* intercept_count: hits whose t differ by <= tau merge (single
+                             linkage on t, reading R4).  Default 1e-6 (t units).   */
+} rsi_options_t;
+
+/* Opaque BVH handle: owns the packed triangles and the BVH on the device
+ * where it was built.  Created by rsi_build, destroyed by rsi_free. */
+typedef struct rsi_bvh* rsi_handle_t;
+
+/*
+ * Caller-owned per-ray outputs for rsi_intersect (device pointers) and
+ * rsi_test (host pointers).  Which fields are written depends on the mode;
+ * fields of other modes are ignored and may be NULL.
+ *   BOOLEAN:          hit[n]   uint8 0/1
+ *   INTERCEPT_COUNT:  count[n] int32 >= 0
+ *   BARYCENTRIC:      tri[n]   int32 original triangle index, -1 on a miss
+ *                     t[n]     float32 parametric position in [0,1]       (optional)
+ *                     dist[n]  float32 t * |end - start|   (3b)     (optional)
+ *                     point[n][3] float32 start + t*(end - start) (3d) (optional)
+ *                     t/dist/point are NaN on a miss.
+ */
+typedef struct {
+    uint8_t* hit;
+    int32_t* count;
+    int32_t* tri;
+    float* t;
+    float* dist;
+    float* point;
+} rsi_outputs_t;
+
+/* Cumulative per-handle counters (reporting; SURVEY 5 "stats struct"). */
+typedef struct {
+    uint64_t rays;           /* rays processed by rsi_intersect                         */
+    uint64_t fp64_pairs;     /* (ray, triangle) pairs whose hit decision the fp32 error
+                                filter could not certify, re-decided in fp64      */
+    uint64_t fp64_rays;      /* rays whose nearest-hit / dedup / output value needed fp64 */
+    uint64_t overflow_rays;  /* intercept_count rays that overflowed the register hit
+                                list and went through the exact re-pass                  */
+    uint64_t nonfinite_rays; /* rays with a NaN/Inf coordinate (reported as misses)       */
+} rsi_stats_t;
+
+/* Library version string, e.g. "rsi-b200 0.1.0 sm_100a". */
+const char* rsi_version(void);
+
+/* Thread-local message for the most recent failing call on this thread. */
+const char* rsi_last_error(void);
+
+/*
+ * rsi_build -- build the linear BVH over a triangle mesh (Fig. 1 P:17-24;
+ * SURVEY 8(a) A1..A7): validate, surface extent, 30-bit Morton codes of
+ * centroids, radix sort, Karras binary radix tree,
+ * leaf init + atomic bottom-up AABB refit, packing.
+ *   d_vertices  [n_vertices][3] float32, device.  Borrowed during the call only.
+ *   d_triangles [n_triangles][3] int32, device.    Borrowed during the call only.
+ *   options     may be NULL (defaults).
+ *   out         receives the new handle (set to NULL on failure).
+ * The handle keeps its own packed copy of the triangles, so the inputs may be
+ * freed or overwritten once this call returns.  Validation (indices in range,
+ * finite vertices) makes this call SYNCHRONOUS on `stream` at its end (one
+ * 4-byte device->host status read).
+ * Errors: RSI_E_INVALID_ARG, RSI_E_EMPTY, RSI_E_INDEX_RANGE, RSI_E_NONFINITE,
+ *         RSI_E_OOM, RSI_E_CUDA.
+ */
+rsi_status_t rsi_build(const float* d_vertices, int64_t n_vertices,
+                       const int32_t* d_triangles, int64_t n_triangles,
+                       const rsi_options_t* options, void* stream, rsi_handle_t* out);
+
+/*
+ * rsi_rebuild -- rebuild `h` in place for a new mesh (same semantics as
+ * rsi_build).  Device memory is reused when the new mesh fits; on failure the
+ * handle is left empty (n_triangles 0) but valid for rsi_free / rsi_rebuild.
+ */
+rsi_status_t rsi_rebuild(rsi_handle_t h, const float* d_vertices, int64_t n_vertices,
+                         const int32_t* d_triangles, int64_t n_triangles, void* stream);
+
+/*
+ * rsi_intersect -- test n_rays segments against the mesh of `h` (
+ * SURVEY 8(a) A8..A9): per-ray short-stack BVH traversal + Moller-Trumbore.
+ *   d_start, d_end  [n_rays][3] float32 segment end points, device.
+ *   mode            an rsi_mode_t.
+ *   out             device output pointers for `mode` (see rsi_outputs_t).
+ * Results equal the exhaustive double-precision definition.
+ * Asynchronous for BOOLEAN and BARYCENTRIC.  INTERCEPT_COUNT synchronizes
+ * `stream` once (a 4-byte overflow count) and, only if some ray overflowed the
+ * register hit list, runs an exact re-pass (which synchronizes once more).
+ * n_rays == 0 is a no-op.  Errors: RSI_E_INVALID_ARG, RSI_E_OOM, RSI_E_CUDA.
+ */
+rsi_status_t rsi_intersect(rsi_handle_t h, const float* d_start, const float* d_end,
+                           int64_t n_rays, int32_t mode, const rsi_outputs_t* out,
+                           void* stream);
+
+/*
+ * rsi_test -- the paper's end-to-end call `PyCudaRSI.test(vertices, triangles,
+ * raysFrom, raysTo, cfg)` on HOST buffers: host->device copies,
+ * rsi_build, rsi_intersect, device->host copies of the mode's outputs, and a
+ * final synchronize of `stream`.  Host inputs should be pinned for full copy
+ * bandwidth (pageable memory works but is slower).  h_out fields are HOST
+ * pointers.  Temporary device memory is stream-ordered (cudaMallocAsync).
+ * Errors: as rsi_build and rsi_intersect.
+ */
+rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices,
+                      const int32_t* h_triangles, int64_t n_triangles,
+                      const float* h_start, const float* h_end, int64_t n_rays,
+                      int32_t mode, const rsi_options_t* options,
+                      const rsi_outputs_t* h_out, void* stream);
+
+/*
+ * rsi_compact_hits -- step 3a "identify intersecting rays" on the
+ * device: writes the ray indices i with d_tri[i] >= 0 in ASCENDING order to
+ * d_ray_ids (capacity n_rays) and their number to *d_n_hits (device int32).
+ * Together with the dense barycentric outputs this yields the paper's sparse
+ * return (intersecting_rays, distances, hit_triangles, hit_points).
+ * Asynchronous.  Errors: RSI_E_INVALID_ARG, RSI_E_OOM, RSI_E_CUDA.
+ */
+rsi_status_t rsi_compact_hits(const int32_t* d_tri, int64_t n_rays, int32_t* d_ray_ids,
+                              int32_t* d_n_hits, void* stream);
+
+/* Release the handle and its device memory (stream-ordered on the build stream). */
+rsi_status_t rsi_free(rsi_handle_t h);
+
+/* Read the cumulative counters of `h`; synchronizes `stream`. */
+rsi_status_t rsi_get_stats(rsi_handle_t h, rsi_stats_t* out, void* stream);
+
+/* Zero the counters of `h` (stream-ordered). */
+rsi_status_t rsi_reset_stats(rsi_handle_t h, void* stream);
+
+/*
+ * Diagnostics (the paper's BVH debugging strategy: copy the tree
+ * from device to host and decode it).
+ * rsi_bvh_info: sizes and the scene AABB (root box) of `h` (host outputs);
+ *   n_nodes = max(N_t - 1, 1) internal child-pair nodes.
+ * rsi_bvh_download: copies the tree to HOST buffers (any may be NULL) and
+ *   synchronizes `stream`:
+ *     h_child   [n_nodes][2] int32  child refs: >= 0 internal node, < 0 leaf ~slot
+ *     h_box     [n_nodes][2][6] float32 child AABBs (xlo, ylo, zlo, xhi, yhi, zhi)
+ *     h_leaf_tri[N_t] int32  original triangle index stored at each leaf slot
+ *     h_morton  [N_t] uint32 sorted 30-bit Morton codes (z-major interleave)
+ *     h_parent  [n_nodes + N_t] int32 parent of internal nodes then of leaves,
+ *               encoded (parent << 1) | side (side 0 = left); -1 for the root
+ *     h_arrivals[n_nodes] uint32 refit arrival counters ("atomic")
+ */
+rsi_status_t rsi_bvh_info(rsi_handle_t h, int64_t* n_triangles, int64_t* n_nodes,
+                          float* scene_lo3, float* scene_hi3);
+rsi_status_t rsi_bvh_download(rsi_handle_t h, int32_t* h_child, float* h_box,
+                              int32_t* h_leaf_tri, uint32_t* h_morton, int32_t* h_parent,
+                              uint32_t* h_arrivals, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSI_H_ */

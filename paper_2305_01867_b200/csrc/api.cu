@@ -1,0 +1,305 @@
+// api.cu -- the extern "C" boundary declared in include/rsi.h.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "rsi_internal.cuh"
+
+static thread_local char g_err[512] = "";
+
+rsi_status_t rsi_set_error(rsi_status_t s, const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(g_err, sizeof(g_err), fmt, ap);
+    va_end(ap);
+    return s;
+}
+
+rsi_status_t rsi_cuda_check(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return RSI_OK;
+    (void)cudaGetLastError();
+    if (e == cudaErrorMemoryAllocation)
+        return rsi_set_error(RSI_E_OOM, "%s: %s", what, cudaGetErrorString(e));
+    return rsi_set_error(RSI_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+static rsi_status_t read_options(const rsi_options_t* in, rsi_options_t* out) {
+    out->struct_size = sizeof(rsi_options_t);
+    out->flags = 0;
+    out->dedup_tau = 1e-6;
+    if (!in || in->struct_size == 0) return RSI_OK;
+    if (in->struct_size != sizeof(rsi_options_t))
+        return rsi_set_error(RSI_E_INVALID_ARG, "rsi_options_t.struct_size %u != %zu", in->struct_size,
+                             sizeof(rsi_options_t));
+    if (in->flags & ~RSI_OPT_FP64_MOLLER) return rsi_set_error(RSI_E_INVALID_ARG, "unknown option flags 0x%x", in->flags);
+    if (!(in->dedup_tau >= 0.0)) return rsi_set_error(RSI_E_INVALID_ARG, "dedup_tau must be >= 0");
+    *out = *in;
+    return RSI_OK;
+}
+
+static rsi_status_t check_mesh_args(const float* V, int64_t nv, const int32_t* T, int64_t nt) {
+    if (nv < 0 || nt < 0) return rsi_set_error(RSI_E_INVALID_ARG, "negative mesh size");
+    if (nv == 0 || nt == 0) return rsi_set_error(RSI_E_EMPTY, "empty mesh (n_vertices=%lld, n_triangles=%lld)",
+                                                 (long long)nv, (long long)nt);
+    if (!V || !T) return rsi_set_error(RSI_E_INVALID_ARG, "null vertices/triangles pointer");
+    return RSI_OK;
+}
+
+extern "C" {
+
+const char* rsi_version(void) { return RSI_VERSION_STRING; }
+
+const char* rsi_last_error(void) { return g_err; }
+
+rsi_status_t rsi_build(const float* d_vertices, int64_t n_vertices, const int32_t* d_triangles,
+                       int64_t n_triangles, const rsi_options_t* options, void* stream, rsi_handle_t* out) {
+    if (!out) return rsi_set_error(RSI_E_INVALID_ARG, "null output handle pointer");
+    *out = nullptr;
+    rsi_options_t opt;
+    rsi_status_t st = read_options(options, &opt);
+    if (st != RSI_OK) return st;
+    st = check_mesh_args(d_vertices, n_vertices, d_triangles, n_triangles);
+    if (st != RSI_OK) return st;
+    rsi_bvh* h = new (std::nothrow) rsi_bvh();
+    if (!h) return rsi_set_error(RSI_E_OOM, "host allocation failed");
+    h->opt = opt;
+    cudaStream_t s = (cudaStream_t)stream;
+    h->stream = s;
+    st = rsi_cuda_check(cudaGetDevice(&h->device), "cudaGetDevice");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaMallocAsync((void**)&h->scratch, SCR_WORDS * sizeof(uint32_t), s), "scratch");
+    if (st == RSI_OK)
+        st = rsi_cuda_check(cudaMallocAsync((void**)&h->stats, ST_WORDS * sizeof(unsigned long long), s), "stats");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaMemsetAsync(h->stats, 0, ST_WORDS * sizeof(unsigned long long), s), "stats");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaMallocHost((void**)&h->h_pinned, 64 * sizeof(uint32_t)), "pinned");
+    if (st == RSI_OK) st = rsi_build_device(h, d_vertices, n_vertices, d_triangles, n_triangles, s);
+    if (st != RSI_OK) {
+        char saved[512];
+        memcpy(saved, g_err, sizeof(saved));
+        rsi_free(h);
+        memcpy(g_err, saved, sizeof(saved));
+        return st;
+    }
+    *out = h;
+    return RSI_OK;
+}
+
+rsi_status_t rsi_rebuild(rsi_handle_t h, const float* d_vertices, int64_t n_vertices, const int32_t* d_triangles,
+                         int64_t n_triangles, void* stream) {
+    if (!h) return rsi_set_error(RSI_E_INVALID_ARG, "null handle");
+    h->n_tri = 0;
+    h->n_nodes = 0;
+    rsi_status_t st = check_mesh_args(d_vertices, n_vertices, d_triangles, n_triangles);
+    if (st != RSI_OK) return st;
+    return rsi_build_device(h, d_vertices, n_vertices, d_triangles, n_triangles, (cudaStream_t)stream);
+}
+
+rsi_status_t rsi_intersect(rsi_handle_t h, const float* d_start, const float* d_end, int64_t n_rays, int32_t mode,
+                           const rsi_outputs_t* out, void* stream) {
+    if (!h) return rsi_set_error(RSI_E_INVALID_ARG, "null handle");
+    if (h->n_tri <= 0) return rsi_set_error(RSI_E_INVALID_ARG, "handle holds no mesh (a failed rebuild?)");
+    if (n_rays < 0) return rsi_set_error(RSI_E_INVALID_ARG, "negative n_rays");
+    if (!out) return rsi_set_error(RSI_E_INVALID_ARG, "null outputs");
+    if (mode != RSI_MODE_BOOLEAN && mode != RSI_MODE_BARYCENTRIC && mode != RSI_MODE_INTERCEPT_COUNT)
+        return rsi_set_error(RSI_E_INVALID_ARG, "bad mode %d", mode);
+    if (n_rays == 0) return RSI_OK;
+    if (!d_start || !d_end) return rsi_set_error(RSI_E_INVALID_ARG, "null ray pointer");
+    if (mode == RSI_MODE_BOOLEAN && !out->hit) return rsi_set_error(RSI_E_INVALID_ARG, "boolean mode needs out->hit");
+    if (mode == RSI_MODE_BARYCENTRIC && !out->tri)
+        return rsi_set_error(RSI_E_INVALID_ARG, "barycentric mode needs out->tri");
+    if (mode == RSI_MODE_INTERCEPT_COUNT && !out->count)
+        return rsi_set_error(RSI_E_INVALID_ARG, "intercept_count mode needs out->count");
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (dev != h->device)
+        return rsi_set_error(RSI_E_INVALID_ARG, "handle built on device %d, current device is %d", h->device, dev);
+    rsi_status_t st = rsi_intersect_device(h, d_start, d_end, n_rays, mode, out, (cudaStream_t)stream);
+    if (st == RSI_OK) h->host_rays += (uint64_t)n_rays;
+    return st;
+}
+
+rsi_status_t rsi_compact_hits(const int32_t* d_tri, int64_t n_rays, int32_t* d_ray_ids, int32_t* d_n_hits,
+                              void* stream) {
+    if (n_rays < 0 || (n_rays > 0 && (!d_tri || !d_ray_ids)) || !d_n_hits)
+        return rsi_set_error(RSI_E_INVALID_ARG, "bad compaction arguments");
+    if (n_rays > ((int64_t)1 << 31) - 1) return rsi_set_error(RSI_E_INVALID_ARG, "n_rays exceeds 2^31-1");
+    return rsi_compact_device(d_tri, n_rays, d_ray_ids, d_n_hits, (cudaStream_t)stream);
+}
+
+rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t* h_triangles, int64_t n_triangles,
+                      const float* h_start, const float* h_end, int64_t n_rays, int32_t mode,
+                      const rsi_options_t* options, const rsi_outputs_t* h_out, void* stream) {
+    if (!h_out || n_rays < 0 || (n_rays > 0 && (!h_start || !h_end)))
+        return rsi_set_error(RSI_E_INVALID_ARG, "bad rsi_test arguments");
+    rsi_status_t st = check_mesh_args(h_vertices, n_vertices, h_triangles, n_triangles);
+    if (st != RSI_OK) return st;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t bv = (size_t)n_vertices * 3 * sizeof(float), bt = (size_t)n_triangles * 3 * sizeof(int32_t);
+    const size_t br = (size_t)n_rays * 3 * sizeof(float);
+    size_t bout = 0;
+    if (mode == RSI_MODE_BOOLEAN) bout = (size_t)n_rays;
+    else if (mode == RSI_MODE_INTERCEPT_COUNT) bout = (size_t)n_rays * 4;
+    else if (mode == RSI_MODE_BARYCENTRIC) bout = (size_t)n_rays * 4 * 6;
+    else return rsi_set_error(RSI_E_INVALID_ARG, "bad mode %d", mode);
+    char* buf = nullptr;
+    const size_t al = 256;
+    auto up = [&](size_t x) { return (x + al - 1) / al * al; };
+    const size_t total = up(bv) + up(bt) + 2 * up(br) + up(bout) + al;
+    st = rsi_cuda_check(cudaMallocAsync((void**)&buf, total, s), "rsi_test buffers");
+    if (st != RSI_OK) return st;
+    float* dV = (float*)buf;
+    int32_t* dT = (int32_t*)(buf + up(bv));
+    float* dS = (float*)(buf + up(bv) + up(bt));
+    float* dE = (float*)(buf + up(bv) + up(bt) + up(br));
+    char* dO = buf + up(bv) + up(bt) + 2 * up(br);
+    st = rsi_cuda_check(cudaMemcpyAsync(dV, h_vertices, bv, cudaMemcpyHostToDevice, s), "H2D vertices");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaMemcpyAsync(dT, h_triangles, bt, cudaMemcpyHostToDevice, s), "H2D triangles");
+    if (st == RSI_OK && br) st = rsi_cuda_check(cudaMemcpyAsync(dS, h_start, br, cudaMemcpyHostToDevice, s), "H2D start");
+    if (st == RSI_OK && br) st = rsi_cuda_check(cudaMemcpyAsync(dE, h_end, br, cudaMemcpyHostToDevice, s), "H2D end");
+    rsi_handle_t h = nullptr;
+    if (st == RSI_OK) st = rsi_build(dV, n_vertices, dT, n_triangles, options, stream, &h);
+    rsi_outputs_t d_out{};
+    if (st == RSI_OK) {
+        const size_t n = (size_t)n_rays;
+        if (mode == RSI_MODE_BOOLEAN) d_out.hit = (uint8_t*)dO;
+        if (mode == RSI_MODE_INTERCEPT_COUNT) d_out.count = (int32_t*)dO;
+        if (mode == RSI_MODE_BARYCENTRIC) {
+            d_out.tri = (int32_t*)dO;
+            d_out.t = (float*)(dO + 4 * n);
+            d_out.dist = (float*)(dO + 8 * n);
+            d_out.point = (float*)(dO + 12 * n);
+        }
+        st = rsi_intersect(h, dS, dE, n_rays, mode, &d_out, stream);
+    }
+    if (st == RSI_OK && n_rays > 0) {
+        const size_t n = (size_t)n_rays;
+        auto d2h = [&](void* dst, const void* src, size_t b) {
+            if (dst && st == RSI_OK) st = rsi_cuda_check(cudaMemcpyAsync(dst, src, b, cudaMemcpyDeviceToHost, s), "D2H");
+        };
+        if (mode == RSI_MODE_BOOLEAN) d2h(h_out->hit, d_out.hit, n);
+        if (mode == RSI_MODE_INTERCEPT_COUNT) d2h(h_out->count, d_out.count, 4 * n);
+        if (mode == RSI_MODE_BARYCENTRIC) {
+            d2h(h_out->tri, d_out.tri, 4 * n);
+            d2h(h_out->t, d_out.t, 4 * n);
+            d2h(h_out->dist, d_out.dist, 4 * n);
+            d2h(h_out->point, d_out.point, 12 * n);
+        }
+    }
+    if (h) {
+        char saved[512];
+        memcpy(saved, g_err, sizeof(saved));
+        rsi_free(h);
+        memcpy(g_err, saved, sizeof(saved));
+    }
+    cudaFreeAsync(buf, s);
+    rsi_status_t st2 = rsi_cuda_check(cudaStreamSynchronize(s), "rsi_test");
+    return st != RSI_OK ? st : st2;
+}
+
+rsi_status_t rsi_free(rsi_handle_t h) {
+    if (!h) return RSI_OK;
+    cudaStream_t s = h->stream;
+    void* bufs[] = {h->nodes, h->tris, h->keys, h->vals, h->keys_tmp, h->vals_tmp, h->parent,
+                    h->arrivals, h->hist, h->scratch, h->stats, h->ovf_list};
+    rsi_status_t st = RSI_OK;
+    for (void* p : bufs)
+        if (p) {
+            rsi_status_t e = rsi_cuda_check(cudaFreeAsync(p, s), "cudaFreeAsync");
+            if (st == RSI_OK) st = e;
+        }
+    if (h->h_pinned) cudaFreeHost(h->h_pinned);
+    delete h;
+    return st;
+}
+
+rsi_status_t rsi_get_stats(rsi_handle_t h, rsi_stats_t* out, void* stream) {
+    if (!h || !out) return rsi_set_error(RSI_E_INVALID_ARG, "null argument");
+    unsigned long long v[ST_WORDS] = {0};
+    cudaStream_t s = (cudaStream_t)stream;
+    rsi_status_t st = rsi_cuda_check(cudaMemcpyAsync(v, h->stats, sizeof(v), cudaMemcpyDeviceToHost, s), "stats");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaStreamSynchronize(s), "stats");
+    if (st != RSI_OK) return st;
+    out->rays = h->host_rays;
+    out->fp64_pairs = v[ST_FP64_PAIRS];
+    out->fp64_rays = v[ST_FP64_RAYS];
+    out->overflow_rays = h->host_overflow;
+    out->nonfinite_rays = v[ST_NONFINITE];
+    return RSI_OK;
+}
+
+rsi_status_t rsi_reset_stats(rsi_handle_t h, void* stream) {
+    if (!h) return rsi_set_error(RSI_E_INVALID_ARG, "null handle");
+    h->host_rays = 0;
+    h->host_overflow = 0;
+    return rsi_cuda_check(cudaMemsetAsync(h->stats, 0, ST_WORDS * sizeof(unsigned long long), (cudaStream_t)stream),
+                          "reset stats");
+}
+
+rsi_status_t rsi_bvh_info(rsi_handle_t h, int64_t* n_triangles, int64_t* n_nodes, float* lo3, float* hi3) {
+    if (!h) return rsi_set_error(RSI_E_INVALID_ARG, "null handle");
+    if (n_triangles) *n_triangles = h->n_tri;
+    if (n_nodes) *n_nodes = h->n_nodes;
+    for (int k = 0; k < 3; ++k) {
+        if (lo3) lo3[k] = h->scene_lo[k];
+        if (hi3) hi3[k] = h->scene_hi[k];
+    }
+    return RSI_OK;
+}
+
+rsi_status_t rsi_bvh_download(rsi_handle_t h, int32_t* h_child, float* h_box, int32_t* h_leaf_tri,
+                              uint32_t* h_morton, int32_t* h_parent, uint32_t* h_arrivals, void* stream) {
+    if (!h) return rsi_set_error(RSI_E_INVALID_ARG, "null handle");
+    if (h->n_tri <= 0) return rsi_set_error(RSI_E_INVALID_ARG, "handle holds no mesh");
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t nn = h->n_nodes, nt = h->n_tri;
+    rsi_status_t st = RSI_OK;
+    float4* nodes = nullptr;
+    if (h_child || h_box) {
+        nodes = new (std::nothrow) float4[4 * nn];
+        if (!nodes) return rsi_set_error(RSI_E_OOM, "host allocation failed");
+        st = rsi_cuda_check(cudaMemcpyAsync(nodes, h->nodes, nn * 4 * sizeof(float4), cudaMemcpyDeviceToHost, s), "nodes");
+    }
+    float4* tris = nullptr;
+    if (st == RSI_OK && h_leaf_tri) {
+        tris = new (std::nothrow) float4[3 * nt];
+        if (!tris) st = rsi_set_error(RSI_E_OOM, "host allocation failed");
+        else st = rsi_cuda_check(cudaMemcpyAsync(tris, h->tris, nt * 3 * sizeof(float4), cudaMemcpyDeviceToHost, s), "tris");
+    }
+    if (st == RSI_OK && h_morton)
+        st = rsi_cuda_check(cudaMemcpyAsync(h_morton, h->keys, nt * sizeof(uint32_t), cudaMemcpyDeviceToHost, s), "keys");
+    if (st == RSI_OK && h_parent)
+        st = rsi_cuda_check(cudaMemcpyAsync(h_parent, h->parent, (nn + nt) * sizeof(int32_t), cudaMemcpyDeviceToHost, s),
+                            "parent");
+    if (st == RSI_OK && h_arrivals)
+        st = rsi_cuda_check(cudaMemcpyAsync(h_arrivals, h->arrivals, nn * sizeof(uint32_t), cudaMemcpyDeviceToHost, s),
+                            "arrivals");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaStreamSynchronize(s), "download");
+    if (st == RSI_OK) {
+        for (int64_t i = 0; i < nn; ++i) {
+            const float* f = reinterpret_cast<const float*>(nodes ? nodes + 4 * i : nullptr);
+            if (h_child) {
+                int32_t refs[2];
+                memcpy(refs, f + 12, 8);
+                h_child[2 * i] = refs[0];
+                h_child[2 * i + 1] = refs[1];
+            }
+            if (h_box) {
+                float* b = h_box + 12 * i;
+                // left: xlo ylo zlo xhi yhi zhi
+                b[0] = f[0]; b[1] = f[2]; b[2] = f[8]; b[3] = f[1]; b[4] = f[3]; b[5] = f[9];
+                b[6] = f[4]; b[7] = f[6]; b[8] = f[10]; b[9] = f[5]; b[10] = f[7]; b[11] = f[11];
+            }
+        }
+        if (h_leaf_tri)
+            for (int64_t k = 0; k < nt; ++k) {
+                int32_t id;
+                memcpy(&id, &tris[3 * k].w, 4);
+                h_leaf_tri[k] = id;
+            }
+    }
+    delete[] nodes;
+    delete[] tris;
+    return st;
+}
+
+}  // extern "C"

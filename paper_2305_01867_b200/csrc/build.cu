@@ -1,0 +1,549 @@
+// build.cu -- LBVH construction on sm_100a.
+//
+//   A1+A2  k_extent_validate  index range + finite check, surface AABB
+//   A3     k_morton           30-bit z-major Morton code of each centroid
+//   A4     k_sort_*           hand-written stable LSD radix sort of (code, id)
+//   A5     k_karras           Karras binary radix tree topology
+//   A6+A7  k_refit            leaf init + atomic bottom-up AABB refit written
+//                             straight into the 64 B child-pair layout (P:255-270,
+//                             P:442), triangles packed in Morton order
+//
+// Every grid is derived from the element count it covers (the case-study-2
+// lesson: never size one kernel's grid from another's count).
+#include <cstdio>
+
+#include "rsi_internal.cuh"
+
+namespace {
+
+constexpr int kBlock = 256;
+
+__global__ void k_build_init(uint32_t* scratch) {
+    int i = threadIdx.x;
+    if (i < 3) {
+        scratch[SCR_EXT_MIN + i] = 0xffffffffu;
+        scratch[SCR_EXT_MAX + i] = 0u;
+    }
+    if (i == 0) scratch[SCR_STATUS] = 0u;
+}
+
+__device__ __forceinline__ float warp_min(float v) {
+    for (int o = 16; o; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+    for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// A1 + A2: surface extent of ALL vertices (exact fp32 min/max) and validation.
+__global__ void __launch_bounds__(kBlock) k_extent_validate(const float* __restrict__ V, int64_t nv,
+                                                            const int32_t* __restrict__ T, int64_t nt,
+                                                            uint32_t* scratch) {
+    float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    uint32_t bad = 0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            float x = V[3 * i + k];
+            if (!isfinite(x)) bad |= STATUS_NONFINITE;
+            mn[k] = fminf(mn[k], x);
+            mx[k] = fmaxf(mx[k], x);
+        }
+    }
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < 3 * nt; i += stride) {
+        int32_t a = T[i];
+        if (a < 0 || (int64_t)a >= nv) bad |= STATUS_INDEX;
+    }
+    __shared__ float smn[3][kBlock / 32], smx[3][kBlock / 32];
+    __shared__ uint32_t sbad;
+    if (threadIdx.x == 0) sbad = 0;
+    __syncthreads();
+    int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        float a = warp_min(mn[k]), b = warp_max(mx[k]);
+        if (lane == 0) {
+            smn[k][w] = a;
+            smx[k][w] = b;
+        }
+    }
+    if (bad) atomicOr(&sbad, bad);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            float a = lane < kBlock / 32 ? smn[k][lane] : INFINITY;
+            float b = lane < kBlock / 32 ? smx[k][lane] : -INFINITY;
+            a = warp_min(a);
+            b = warp_max(b);
+            if (lane == 0 && a <= b) {
+                atomicMin(&scratch[SCR_EXT_MIN + k], rsi_f2ord(a));
+                atomicMax(&scratch[SCR_EXT_MAX + k], rsi_f2ord(b));
+            }
+        }
+        if (lane == 0 && sbad) atomicOr(&scratch[SCR_STATUS], sbad);
+    }
+}
+
+// Spread the low 10 bits of x so bit k lands at bit 3k.
+__device__ __forceinline__ uint32_t expand10(uint32_t x) {
+    x &= 0x3ffu;
+    x = (x | (x << 16)) & 0x030000ffu;
+    x = (x | (x << 8)) & 0x0300f00fu;
+    x = (x | (x << 4)) & 0x030c30c3u;
+    x = (x | (x << 2)) & 0x09249249u;
+    return x;
+}
+
+__device__ __forceinline__ uint32_t quantize10(float c, float lo, float hi) {
+    float w = hi - lo;
+    if (!(w > 0.0f)) return 0u;  // zero-width axis -> 0 (reading R8)
+    float q = floorf((c - lo) / w * 1024.0f);
+    q = fminf(fmaxf(q, 0.0f), 1023.0f);  // NaN -> 0 via fmaxf
+    return (uint32_t)q;
+}
+
+__device__ __forceinline__ int32_t safe_index(int32_t a, int64_t nv) {
+    return (a < 0 || (int64_t)a >= nv) ? 0 : a;  // invalid meshes are rejected by status
+}
+
+// A3: code = expand(qx) | expand(qy) << 1 | expand(qz) << 2 (z-major, reading R8).
+// Also zeroes the refit arrival counters.
+__global__ void __launch_bounds__(kBlock) k_morton(const float* __restrict__ V, int64_t nv,
+                                                   const int32_t* __restrict__ T, int n,
+                                                   const uint32_t* __restrict__ scratch,
+                                                   uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
+                                                   uint32_t* __restrict__ arrivals, int n_nodes) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    if (j < n_nodes) arrivals[j] = 0u;
+    float lo[3], hi[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = rsi_ord2f(scratch[SCR_EXT_MIN + k]);
+        hi[k] = rsi_ord2f(scratch[SCR_EXT_MAX + k]);
+    }
+    int32_t a = safe_index(T[3 * j], nv), b = safe_index(T[3 * j + 1], nv), c = safe_index(T[3 * j + 2], nv);
+    uint32_t q[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        float cen = (V[3 * a + k] + V[3 * b + k] + V[3 * c + k]) / 3.0f;
+        q[k] = quantize10(cen, lo[k], hi[k]);
+    }
+    keys[j] = expand10(q[0]) | (expand10(q[1]) << 1) | (expand10(q[2]) << 2);
+    vals[j] = j;
+}
+
+// ------------------------------------------------------------------ A4: radix sort
+// Stable LSD sort, 8-bit digits, 4 passes over the 30-bit keys.  Stability of
+// each pass comes from warp-ordered ranking: a warp walks its contiguous
+// segment 32 keys at a time, lanes in index order, and ranks equal digits with
+// __match_any_sync; per-warp digit counts are scanned over warps, then over
+// digits (and, for the multi-block path, over blocks in digit-major order).
+constexpr int kDigits = 256;
+constexpr int kPasses = 4;
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Exclusive scan of s[0..255] in place by one warp; returns the total.
+__device__ uint32_t warp_scan256(uint32_t* s) {
+    int lane = threadIdx.x & 31;
+    uint32_t v[8], sum = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        v[j] = s[lane * 8 + j];
+        sum += v[j];
+    }
+    uint32_t inc = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    uint32_t run = inc - sum;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        s[lane * 8 + j] = run;
+        run += v[j];
+    }
+    return __shfl_sync(0xffffffffu, inc, 31);
+}
+
+// Count digits of this warp's segment [beg, end) into wcnt (warp-private row).
+__device__ __forceinline__ void warp_count(const uint32_t* __restrict__ ks, int beg, int end, int shift,
+                                           uint32_t* wcnt) {
+    int lane = threadIdx.x & 31;
+    for (int base = beg; base < end; base += 32) {
+        int i = base + lane;
+        bool valid = i < end;
+        uint32_t d = valid ? (ks[i] >> shift) & 255u : 256u;
+        uint32_t peers = __match_any_sync(0xffffffffu, d);
+        if (valid && lane == __ffs(peers) - 1) wcnt[d] += __popc(peers);
+        __syncwarp();
+    }
+}
+
+// Scatter this warp's segment; wcnt[d] holds the warp's running offset within digit d.
+__device__ __forceinline__ void warp_scatter(const uint32_t* __restrict__ ks, const int32_t* __restrict__ vs,
+                                             uint32_t* __restrict__ kd, int32_t* __restrict__ vd, int beg,
+                                             int end, int shift, uint32_t* wcnt, const uint32_t* dbase) {
+    int lane = threadIdx.x & 31;
+    uint32_t lt = lanemask_lt();
+    for (int base = beg; base < end; base += 32) {
+        int i = base + lane;
+        bool valid = i < end;
+        uint32_t key = valid ? ks[i] : 0u;
+        int32_t val = valid ? vs[i] : 0;
+        uint32_t d = valid ? (key >> shift) & 255u : 256u;
+        uint32_t peers = __match_any_sync(0xffffffffu, d);
+        if (valid) {
+            uint32_t pos = dbase[d] + wcnt[d] + __popc(peers & lt);
+            kd[pos] = key;
+            vd[pos] = val;
+        }
+        __syncwarp();
+        if (valid && lane == __ffs(peers) - 1) wcnt[d] += __popc(peers);
+        __syncwarp();
+    }
+}
+
+constexpr int kSmallThreads = 1024;
+constexpr int kSmallMax = 1 << 16;  // single-CTA sort up to 64 Ki keys
+
+// Whole sort in one CTA (N_t <= 64 Ki): no inter-block traffic, one launch.
+__global__ void __launch_bounds__(kSmallThreads) k_sort_small(uint32_t* ka, int32_t* va, uint32_t* kb,
+                                                              int32_t* vb, int n) {
+    __shared__ uint32_t wcnt[32][kDigits + 1];
+    __shared__ uint32_t dbase[kDigits];
+    const int w = threadIdx.x >> 5;
+    const int seg = (((n + 31) / 32) + 31) & ~31;
+    const int beg = min(w * seg, n), end = min(beg + seg, n);
+    for (int p = 0; p < kPasses; ++p) {
+        const uint32_t* ks = (p & 1) ? kb : ka;
+        const int32_t* vs = (p & 1) ? vb : va;
+        uint32_t* kd = (p & 1) ? ka : kb;
+        int32_t* vd = (p & 1) ? va : vb;
+        const int shift = 8 * p;
+        for (int i = threadIdx.x; i < 32 * (kDigits + 1); i += blockDim.x) (&wcnt[0][0])[i] = 0u;
+        __syncthreads();
+        warp_count(ks, beg, end, shift, wcnt[w]);
+        __syncthreads();
+        if (threadIdx.x < kDigits) {
+            uint32_t s = 0;
+            for (int x = 0; x < 32; ++x) {
+                uint32_t c = wcnt[x][threadIdx.x];
+                wcnt[x][threadIdx.x] = s;
+                s += c;
+            }
+            dbase[threadIdx.x] = s;
+        }
+        __syncthreads();
+        if (w == 0) warp_scan256(dbase);
+        __syncthreads();
+        warp_scatter(ks, vs, kd, vd, beg, end, shift, wcnt[w], dbase);
+        __syncthreads();
+    }
+}
+
+constexpr int kTileThreads = 512;
+constexpr int kTileWarps = kTileThreads / 32;
+constexpr int kTile = 4096;  // keys per block (256 per warp)
+
+__global__ void __launch_bounds__(kTileThreads) k_sort_hist(const uint32_t* __restrict__ ks, int n, int shift,
+                                                            uint32_t* __restrict__ hist) {
+    __shared__ uint32_t cnt[kDigits];
+    for (int i = threadIdx.x; i < kDigits; i += blockDim.x) cnt[i] = 0u;
+    __syncthreads();
+    int beg = blockIdx.x * kTile, end = min(beg + kTile, n);
+    for (int i = beg + threadIdx.x; i < end; i += blockDim.x) atomicAdd(&cnt[(ks[i] >> shift) & 255u], 1u);
+    __syncthreads();
+    for (int d = threadIdx.x; d < kDigits; d += blockDim.x) hist[(size_t)d * gridDim.x + blockIdx.x] = cnt[d];
+}
+
+// Exclusive scan of hist[0..m) in place (digit-major over blocks); one CTA.
+__global__ void __launch_bounds__(1024) k_sort_scan(uint32_t* hist, int m) {
+    __shared__ uint32_t wsum[32];
+    __shared__ uint32_t carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int base = 0; base < m; base += 1024) {
+        int i = base + threadIdx.x;
+        uint32_t v = i < m ? hist[i] : 0u, inc = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) wsum[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            uint32_t s = wsum[lane], si = s;
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, si, o);
+                if (lane >= o) si += y;
+            }
+            wsum[lane] = si - s;
+        }
+        __syncthreads();
+        if (i < m) hist[i] = carry + wsum[w] + inc - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += wsum[31] + inc;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kTileThreads) k_sort_scatter(const uint32_t* __restrict__ ks,
+                                                               const int32_t* __restrict__ vs,
+                                                               uint32_t* __restrict__ kd, int32_t* __restrict__ vd,
+                                                               int n, int shift, const uint32_t* __restrict__ hist) {
+    __shared__ uint32_t wcnt[kTileWarps][kDigits + 1];
+    __shared__ uint32_t dbase[kDigits];
+    const int w = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < kTileWarps * (kDigits + 1); i += blockDim.x) (&wcnt[0][0])[i] = 0u;
+    __syncthreads();
+    const int tbeg = blockIdx.x * kTile;
+    const int beg = min(tbeg + w * (kTile / kTileWarps), n);
+    const int end = min(beg + kTile / kTileWarps, n);
+    warp_count(ks, beg, end, shift, wcnt[w]);
+    __syncthreads();
+    if (threadIdx.x < kDigits) {
+        uint32_t s = 0;
+        for (int x = 0; x < kTileWarps; ++x) {
+            uint32_t c = wcnt[x][threadIdx.x];
+            wcnt[x][threadIdx.x] = s;
+            s += c;
+        }
+        dbase[threadIdx.x] = hist[(size_t)threadIdx.x * gridDim.x + blockIdx.x];
+    }
+    __syncthreads();
+    warp_scatter(ks, vs, kd, vd, beg, end, shift, wcnt[w], dbase);
+}
+
+// ------------------------------------------------------------------ A5: Karras topology
+// delta(i, j): common-prefix length of the sorted codes; equal codes fall back
+// to 32 + clz(i ^ j) (index augmentation); -1 out of range.
+__device__ __forceinline__ int kdelta(const uint32_t* __restrict__ k, int n, int i, uint32_t ki, int j) {
+    if (j < 0 || j >= n) return -1;
+    uint32_t kj = k[j];
+    return (ki == kj) ? 32 + __clz(i ^ j) : __clz(ki ^ kj);
+}
+
+__device__ __forceinline__ void set_ref(float4* nodes, int node, int side, int32_t ref) {
+    reinterpret_cast<int32_t*>(nodes + 4 * node + 3)[side] = ref;
+}
+
+// One thread per internal node i in [0, n-2]: range direction, range end by
+// exponential + binary search, split position gamma, children and parents.
+__global__ void __launch_bounds__(kBlock) k_karras(const uint32_t* __restrict__ keys, int n,
+                                                   float4* __restrict__ nodes, int32_t* __restrict__ parent,
+                                                   uint32_t* __restrict__ arrivals) {
+    const int n_nodes = n > 1 ? n - 1 : 1;
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n == 1) {  // single triangle: root holds leaf 0 on the left, an unhittable point at +inf on the right
+        if (i == 0) {
+            float4* nd = nodes;
+            nd[1] = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+            nd[2].z = INFINITY;
+            nd[2].w = INFINITY;
+            nd[3] = make_float4(__int_as_float(~0), __int_as_float(~0), 0.f, 0.f);
+            parent[0] = -1;
+            parent[n_nodes + 0] = 0;
+            arrivals[0] = 2u;
+        }
+        return;
+    }
+    if (i >= n - 1) return;
+    const uint32_t ki = keys[i];
+    const int dir = (kdelta(keys, n, i, ki, i + 1) - kdelta(keys, n, i, ki, i - 1)) > 0 ? 1 : -1;
+    const int dmin = kdelta(keys, n, i, ki, i - dir);
+    int lmax = 2;
+    while (kdelta(keys, n, i, ki, i + lmax * dir) > dmin) lmax <<= 1;
+    int l = 0;
+    for (int t = lmax >> 1; t >= 1; t >>= 1)
+        if (kdelta(keys, n, i, ki, i + (l + t) * dir) > dmin) l += t;
+    const int j = i + l * dir;
+    const int dnode = kdelta(keys, n, i, ki, j);
+    int s = 0, step = l;
+    do {
+        step = (step + 1) >> 1;
+        int ns = s + step;
+        if (ns < l && kdelta(keys, n, i, ki, i + ns * dir) > dnode) s = ns;
+    } while (step > 1);
+    const int gamma = i + s * dir + min(dir, 0);
+    const int lo = min(i, j), hi = max(i, j);
+    int32_t left = (lo == gamma) ? ~gamma : gamma;
+    int32_t right = (hi == gamma + 1) ? ~(gamma + 1) : gamma + 1;
+    set_ref(nodes, i, 0, left);
+    set_ref(nodes, i, 1, right);
+    reinterpret_cast<int32_t*>(nodes + 4 * i + 3)[2] = 0;
+    reinterpret_cast<int32_t*>(nodes + 4 * i + 3)[3] = 0;
+    parent[left >= 0 ? left : n_nodes + ~left] = (i << 1) | 0;
+    parent[right >= 0 ? right : n_nodes + ~right] = (i << 1) | 1;
+    if (i == 0) parent[0] = -1;
+}
+
+// ------------------------------------------------------------------ A6 + A7: refit + pack
+__device__ __forceinline__ void write_slot(float4* nodes, int node, int side, const float lo[3], const float hi[3]) {
+    float* f = reinterpret_cast<float*>(nodes + 4 * node);
+    int o = side ? 4 : 0;
+    f[o + 0] = lo[0];
+    f[o + 1] = hi[0];
+    f[o + 2] = lo[1];
+    f[o + 3] = hi[1];
+    f[8 + 2 * side] = lo[2];
+    f[9 + 2 * side] = hi[2];
+}
+
+// One thread per leaf slot k: pack triangle k (Morton order), compute its AABB
+// and ascend.  At each internal node the box goes into this child's slot, then
+// __threadfence + atomicAdd on the arrival counter: the first arrival stops,
+// the second (which sees the sibling's box) merges and continues.
+__global__ void __launch_bounds__(kBlock) k_refit(const float* __restrict__ V, int64_t nv,
+                                                  const int32_t* __restrict__ T, const int32_t* __restrict__ vals,
+                                                  int n, float4* nodes, float4* __restrict__ tris,
+                                                  const int32_t* __restrict__ parent, uint32_t* arrivals,
+                                                  uint32_t* scratch) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int n_nodes = n > 1 ? n - 1 : 1;
+    const int32_t id = vals[k];
+    const int32_t ia = safe_index(T[3 * id], nv), ib = safe_index(T[3 * id + 1], nv),
+                  ic = safe_index(T[3 * id + 2], nv);
+    float a[3], b[3], c[3], lo[3], hi[3];
+#pragma unroll
+    for (int x = 0; x < 3; ++x) {
+        a[x] = V[3 * ia + x];
+        b[x] = V[3 * ib + x];
+        c[x] = V[3 * ic + x];
+        lo[x] = fminf(a[x], fminf(b[x], c[x]));
+        hi[x] = fmaxf(a[x], fmaxf(b[x], c[x]));
+    }
+    tris[3 * k + 0] = make_float4(a[0], a[1], a[2], __int_as_float(id));
+    tris[3 * k + 1] = make_float4(b[0], b[1], b[2], 0.f);
+    tris[3 * k + 2] = make_float4(c[0], c[1], c[2], 0.f);
+    int32_t p = parent[n_nodes + k];
+    while (true) {
+        const int node = p >> 1, side = p & 1;
+        write_slot(nodes, node, side, lo, hi);
+        if (n == 1) break;
+        __threadfence();
+        if (atomicAdd(&arrivals[node], 1u) == 0u) return;
+        __threadfence();
+        const volatile float* f = reinterpret_cast<const volatile float*>(nodes + 4 * node);
+        const int o = side ? 0 : 4;  // sibling slot
+        lo[0] = fminf(lo[0], f[o + 0]);
+        hi[0] = fmaxf(hi[0], f[o + 1]);
+        lo[1] = fminf(lo[1], f[o + 2]);
+        hi[1] = fmaxf(hi[1], f[o + 3]);
+        lo[2] = fminf(lo[2], f[8 + 2 * (1 - side)]);
+        hi[2] = fmaxf(hi[2], f[9 + 2 * (1 - side)]);
+        if (node == 0) break;
+        p = parent[node];
+    }
+    // root box (scene AABB) for rsi_bvh_info
+    float* root = reinterpret_cast<float*>(scratch + 9);
+    for (int x = 0; x < 3; ++x) {
+        root[x] = lo[x];
+        root[3 + x] = hi[x];
+    }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host side
+static rsi_status_t ensure_capacity(rsi_bvh* h, int64_t n, cudaStream_t s) {
+    int nb = rsi_ceil_div(n, kTile);
+    if (n <= h->cap_tri && nb <= h->sort_blocks_cap) return RSI_OK;
+    void* old[] = {h->nodes, h->tris, h->keys, h->vals, h->keys_tmp, h->vals_tmp, h->parent, h->arrivals, h->hist};
+    for (void* p : old)
+        if (p) cudaFreeAsync(p, s);
+    int64_t nn = n > 1 ? n - 1 : 1;
+    cudaError_t e = cudaSuccess;
+#define RSI_ALLOC(ptr, bytes) \
+    if (e == cudaSuccess) e = cudaMallocAsync((void**)&(ptr), (size_t)(bytes), s);
+    RSI_ALLOC(h->nodes, nn * 4 * sizeof(float4));
+    RSI_ALLOC(h->tris, n * 3 * sizeof(float4));
+    RSI_ALLOC(h->keys, n * sizeof(uint32_t));
+    RSI_ALLOC(h->vals, n * sizeof(int32_t));
+    RSI_ALLOC(h->keys_tmp, n * sizeof(uint32_t));
+    RSI_ALLOC(h->vals_tmp, n * sizeof(int32_t));
+    RSI_ALLOC(h->parent, (nn + n) * sizeof(int32_t));
+    RSI_ALLOC(h->arrivals, nn * sizeof(uint32_t));
+    RSI_ALLOC(h->hist, (size_t)kDigits * nb * sizeof(uint32_t));
+#undef RSI_ALLOC
+    if (e != cudaSuccess) {
+        h->cap_tri = 0;
+        h->sort_blocks_cap = 0;
+        (void)cudaGetLastError();
+        return rsi_set_error(RSI_E_OOM, "device allocation for %lld triangles failed: %s", (long long)n,
+                             cudaGetErrorString(e));
+    }
+    h->cap_tri = n;
+    h->sort_blocks_cap = nb;
+    return RSI_OK;
+}
+
+static void launch_sort(rsi_bvh* h, int n, cudaStream_t s) {
+    if (n <= kSmallMax) {
+        k_sort_small<<<1, kSmallThreads, 0, s>>>(h->keys, h->vals, h->keys_tmp, h->vals_tmp, n);
+        return;
+    }
+    int nb = rsi_ceil_div(n, kTile);
+    for (int p = 0; p < kPasses; ++p) {
+        uint32_t* ks = (p & 1) ? h->keys_tmp : h->keys;
+        int32_t* vs = (p & 1) ? h->vals_tmp : h->vals;
+        uint32_t* kd = (p & 1) ? h->keys : h->keys_tmp;
+        int32_t* vd = (p & 1) ? h->vals : h->vals_tmp;
+        k_sort_hist<<<nb, kTileThreads, 0, s>>>(ks, n, 8 * p, h->hist);
+        k_sort_scan<<<1, 1024, 0, s>>>(h->hist, kDigits * nb);
+        k_sort_scatter<<<nb, kTileThreads, 0, s>>>(ks, vs, kd, vd, n, 8 * p, h->hist);
+    }
+}
+
+rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int32_t* T, int64_t nt,
+                              cudaStream_t s) {
+    h->n_tri = 0;
+    h->n_nodes = 0;
+    if (nt > (int64_t)1 << 30)
+        return rsi_set_error(RSI_E_INVALID_ARG, "n_triangles %lld exceeds 2^30", (long long)nt);
+    rsi_status_t st = ensure_capacity(h, nt, s);
+    if (st != RSI_OK) return st;
+    const int n = (int)nt;
+    const int n_nodes = n > 1 ? n - 1 : 1;
+    k_build_init<<<1, 32, 0, s>>>(h->scratch);
+    int64_t work = nv > 3 * nt ? nv : 3 * nt;
+    int eb = rsi_ceil_div(work, kBlock);
+    if (eb > 148 * 8) eb = 148 * 8;
+    k_extent_validate<<<eb, kBlock, 0, s>>>(V, nv, T, nt, h->scratch);
+    k_morton<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, n, h->scratch, h->keys, h->vals, h->arrivals,
+                                                         n_nodes);
+    launch_sort(h, n, s);
+    k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent, h->arrivals);
+    k_refit<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, h->vals, n, h->nodes, h->tris, h->parent,
+                                                        h->arrivals, h->scratch);
+    st = rsi_cuda_check(cudaGetLastError(), "build kernel launch");
+    if (st != RSI_OK) return st;
+    st = rsi_cuda_check(cudaMemcpyAsync(h->h_pinned, h->scratch, SCR_WORDS * sizeof(uint32_t),
+                                        cudaMemcpyDeviceToHost, s),
+                        "status read");
+    if (st != RSI_OK) return st;
+    st = rsi_cuda_check(cudaStreamSynchronize(s), "build");
+    if (st != RSI_OK) return st;
+    uint32_t status = h->h_pinned[SCR_STATUS];
+    if (status & STATUS_INDEX) return rsi_set_error(RSI_E_INDEX_RANGE, "a triangle index is outside [0, %lld)", (long long)nv);
+    if (status & STATUS_NONFINITE) return rsi_set_error(RSI_E_NONFINITE, "a vertex coordinate is NaN or Inf");
+    const float* root = reinterpret_cast<const float*>(h->h_pinned + 9);
+    for (int x = 0; x < 3; ++x) {
+        h->scene_lo[x] = root[x];
+        h->scene_hi[x] = root[3 + x];
+    }
+    h->n_tri = nt;
+    h->n_nodes = n_nodes;
+    h->stream = s;
+    return RSI_OK;
+}

@@ -1,0 +1,100 @@
+// rsi_internal.cuh -- shared internals of the sm_100a CUDA path (not part of the ABI).
+//
+// Layouts:
+//   node  (64 B, 4 x float4) -- a "child pair": both children's AABBs + refs
+//     n0 = (L.lo.x, L.hi.x, L.lo.y, L.hi.y)
+//     n1 = (R.lo.x, R.hi.x, R.lo.y, R.hi.y)
+//     n2 = (L.lo.z, L.hi.z, R.lo.z, R.hi.z)
+//     n3 = (ref L, ref R, 0, 0) as int bits; ref >= 0 internal node, < 0 leaf ~slot
+//   tri   (48 B, 3 x float4) in Morton order: (v0, id bits), (v1, 0), (v2, 0)
+//   The vertices are stored exactly (not e1/e2) so the fp64 mirror can
+//   recompute the oracle's operation order bit-for-bit.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/rsi.h"
+
+#define RSI_VERSION_STRING "rsi-b200 0.1.0 sm_100a"
+
+// scratch words (uint32) in rsi_bvh::scratch
+enum {
+    SCR_EXT_MIN = 0,   // 3 words: order-preserving encoded min x,y,z
+    SCR_EXT_MAX = 3,   // 3 words: encoded max
+    SCR_STATUS = 6,    // bit 0 index out of range, bit 1 non-finite vertex
+    SCR_OVF_COUNT = 7, // intercept_count overflow list length
+    SCR_OVF_TOTAL = 8, // re-pass: total raw hits over overflowed rays
+    SCR_WORDS = 16
+};
+enum { STATUS_INDEX = 1u, STATUS_NONFINITE = 2u };
+
+// stats counters (unsigned long long) in rsi_bvh::stats
+enum { ST_RAYS = 0, ST_FP64_PAIRS, ST_FP64_RAYS, ST_OVERFLOW, ST_NONFINITE, ST_WORDS };
+
+struct rsi_bvh {
+    int device = 0;
+    cudaStream_t stream = nullptr;  // build stream (frees are ordered on it)
+    rsi_options_t opt{};
+    int64_t n_tri = 0, n_nodes = 0;  // current mesh
+    int64_t cap_tri = 0;             // allocated capacity (triangles)
+    int64_t sort_blocks_cap = 0;
+    float4* nodes = nullptr;         // [4 * n_nodes]
+    float4* tris = nullptr;          // [3 * n_tri]
+    uint32_t* keys = nullptr;        // sorted Morton codes [n_tri]
+    int32_t* vals = nullptr;         // sorted triangle ids [n_tri]
+    uint32_t* keys_tmp = nullptr;
+    int32_t* vals_tmp = nullptr;
+    int32_t* parent = nullptr;       // [n_nodes + n_tri]
+    uint32_t* arrivals = nullptr;    // [n_nodes]
+    uint32_t* hist = nullptr;        // sort: [256 * blocks]
+    uint32_t* scratch = nullptr;     // [SCR_WORDS]
+    unsigned long long* stats = nullptr;  // [ST_WORDS]
+    uint32_t* h_pinned = nullptr;    // pinned host words for status reads
+    // intercept_count overflow workspace
+    int32_t* ovf_list = nullptr;     // ray ids
+    int64_t ovf_cap = 0;
+    float scene_lo[3] = {0, 0, 0}, scene_hi[3] = {0, 0, 0};
+    uint64_t host_rays = 0, host_overflow = 0;  // counters known on the host
+};
+
+// ---------------------------------------------------------------- host helpers (api.cu)
+rsi_status_t rsi_set_error(rsi_status_t s, const char* fmt, ...);
+rsi_status_t rsi_cuda_check(cudaError_t e, const char* what);
+
+// build.cu
+rsi_status_t rsi_build_device(rsi_bvh* h, const float* d_vertices, int64_t n_vertices,
+                              const int32_t* d_triangles, int64_t n_triangles,
+                              cudaStream_t stream);
+// traverse.cu
+rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* d_start, const float* d_end,
+                                  int64_t n_rays, int32_t mode, const rsi_outputs_t* out,
+                                  cudaStream_t stream);
+rsi_status_t rsi_compact_device(const int32_t* d_tri, int64_t n_rays, int32_t* d_ids,
+                                int32_t* d_n, cudaStream_t stream);
+
+// ---------------------------------------------------------------- device helpers
+
+// Order-preserving float <-> uint32 map (monotone over all non-NaN floats), so
+// that float min/max can use integer atomics.
+__host__ __device__ inline uint32_t rsi_f2ord(float f) {
+#ifdef __CUDA_ARCH__
+    uint32_t u = __float_as_uint(f);
+#else
+    uint32_t u;
+    __builtin_memcpy(&u, &f, 4);
+#endif
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__host__ __device__ inline float rsi_ord2f(uint32_t u) {
+    uint32_t b = (u & 0x80000000u) ? (u & 0x7fffffffu) : ~u;
+#ifdef __CUDA_ARCH__
+    return __uint_as_float(b);
+#else
+    float f;
+    __builtin_memcpy(&f, &b, 4);
+    return f;
+#endif
+}
+
+static inline int rsi_ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }

@@ -1,0 +1,777 @@
+// traverse.cu -- per-ray BVH traversal + Moller-Trumbore on sm_100a
+// (SURVEY 8(a) rows A8 and A9).
+//
+// One thread per segment.  Each thread walks the child-pair BVH with a short
+// stack (64 entries: depth <= 62 for the index-augmented 62-bit Karras key,
+// SURVEY 7), tests both child boxes of every node with a conservative slab
+// test, and runs Moller-Trumbore on every leaf whose box it enters.
+//
+// Exactness.  Every discrete decision -- hit / miss,
+// nearest-hit order, dedup merge -- is taken in fp32 only when a forward error
+// bound certifies it; otherwise it is re-made by an fp64 "mirror" that repeats
+// the oracle's operation order with correctly rounded
+// __dmul_rn/__dadd_rn/__dsub_rn/__ddiv_rn and no contraction, so it returns the
+// oracle's exact double results.  This is the paper's
+// USE_DOUBLE_PRECISION_MOLLER idea applied only where fp32 is unsure.
+#include <cstdio>
+
+#include "rsi_internal.cuh"
+
+namespace {
+
+constexpr float kU = 5.9604644775390625e-08f;    // 2^-24, fp32 unit roundoff
+constexpr float kFilt = 16.0f * kU;              // K = 16
+constexpr float kTerr = 12.0f * kU;              // t forward-error constant
+constexpr float kSlack = 4.76837158203125e-07f;  // 2^-21: slab-test slack factor
+constexpr float kTiny = 1e-30f;                  // absolute floor (underflow)
+constexpr float kOutTol = 4e-6f;                 // max certified |t error| for fp32 outputs
+constexpr int kStack = 64;
+constexpr int kCountCap = 8;  // intercept_count hits held in registers per ray
+constexpr int kThreads = 128;
+
+enum { MT_MISS = 0, MT_HIT = 1, MT_UNSURE = 2 };
+
+struct Ray {
+    float ox, oy, oz;  // start (r^start)
+    float ex, ey, ez;  // end (r^end), kept exactly for the fp64 mirror
+    float dx, dy, dz;  // d = end - start (fp32)
+    float ix, iy, iz;  // slab: 1/d per axis (0 on degenerate axes)
+    float lx, ly, lz;  // slab offsets applied to the box's lo plane
+    float hx, hy, hz;  // slab offsets applied to the box's hi plane
+};
+
+// Per-axis slab setup.  t = fma(plane, inv, -off) approximates (plane - o)/d;
+// the slack (2^-21 * (1 + |o/d|)) exceeds the fp32 error of that expression
+// for |t| <= ~1, and is applied so the computed entry t is never later and the
+// exit t never earlier than the exact ones: the test never rejects a box the
+// exact segment touches.  |d| < 1e-30 (incl. 0): the axis imposes no constraint.
+__device__ __forceinline__ void slab_axis(float o, float d, float& inv, float& offlo, float& offhi) {
+    if (fabsf(d) >= 1e-30f) {
+        inv = 1.0f / d;
+        float oinv = o * inv;
+        float slack = kSlack * (1.0f + fabsf(oinv));
+        float sg = inv > 0.0f ? slack : -slack;
+        offlo = oinv + sg;
+        offhi = oinv - sg;
+        if (isfinite(offlo) && isfinite(offhi)) return;
+    }
+    inv = 0.0f;
+    offlo = INFINITY;
+    offhi = -INFINITY;
+}
+
+// Returns false for rays that cannot hit: zero length or a non-finite coordinate
+// (reading R12).  `nonfinite` is set for the latter.
+__device__ __forceinline__ bool load_ray(Ray& r, const float* __restrict__ S, const float* __restrict__ E,
+                                         int64_t i, bool& nonfinite) {
+    r.ox = __ldg(S + 3 * i);
+    r.oy = __ldg(S + 3 * i + 1);
+    r.oz = __ldg(S + 3 * i + 2);
+    r.ex = __ldg(E + 3 * i);
+    r.ey = __ldg(E + 3 * i + 1);
+    r.ez = __ldg(E + 3 * i + 2);
+    nonfinite = !(isfinite(r.ox) && isfinite(r.oy) && isfinite(r.oz) && isfinite(r.ex) && isfinite(r.ey) &&
+                  isfinite(r.ez));
+    r.dx = r.ex - r.ox;
+    r.dy = r.ey - r.oy;
+    r.dz = r.ez - r.oz;
+    slab_axis(r.ox, r.dx, r.ix, r.lx, r.hx);
+    slab_axis(r.oy, r.dy, r.iy, r.ly, r.hy);
+    slab_axis(r.oz, r.dz, r.iz, r.lz, r.hz);
+    return !nonfinite && !(r.dx == 0.0f && r.dy == 0.0f && r.dz == 0.0f);
+}
+
+// Conservative segment/box overlap on [0, tclip]; tnear is the (lowered) entry t.
+__device__ __forceinline__ bool slab(const Ray& r, float lox, float hix, float loy, float hiy, float loz, float hiz,
+                                     float tclip, float& tnear) {
+    float tx1 = fmaf(lox, r.ix, -r.lx), tx2 = fmaf(hix, r.ix, -r.hx);
+    float ty1 = fmaf(loy, r.iy, -r.ly), ty2 = fmaf(hiy, r.iy, -r.hy);
+    float tz1 = fmaf(loz, r.iz, -r.lz), tz2 = fmaf(hiz, r.iz, -r.hz);
+    tnear = fmaxf(fmaxf(fminf(tx1, tx2), fminf(ty1, ty2)), fmaxf(fminf(tz1, tz2), 0.0f));
+    float tfar = fminf(fminf(fmaxf(tx1, tx2), fmaxf(ty1, ty2)), fminf(fmaxf(tz1, tz2), tclip));
+    return tnear <= tfar;
+}
+
+// ---------------------------------------------------------------- fp32 MT + error filter
+// Same algebra as the oracle (p = d x e2, det = e1.p, q = s x e1, nu = s.p,
+// nv = d.q, nt = e2.q).  Each quantity X has a "shadow" M_X (the same
+// expression on absolute values with + for -): |fl(X) - X| <= ~10u M_X, so a
+// sign test on X is certain when |X| > 16u M_X (+ an underflow floor).
+// Returns MT_MISS / MT_HIT (with t and a bound et on |t - t_exact|) / MT_UNSURE.
+__device__ __forceinline__ int mt32(const Ray& r, const float4& A, const float4& B, const float4& C, float& t,
+                                    float& et) {
+    const float e1x = B.x - A.x, e1y = B.y - A.y, e1z = B.z - A.z;
+    const float e2x = C.x - A.x, e2y = C.y - A.y, e2z = C.z - A.z;
+    const float px = r.dy * e2z - r.dz * e2y, py = r.dz * e2x - r.dx * e2z, pz = r.dx * e2y - r.dy * e2x;
+    const float adx = fabsf(r.dx), ady = fabsf(r.dy), adz = fabsf(r.dz);
+    const float Px = ady * fabsf(e2z) + adz * fabsf(e2y), Py = adz * fabsf(e2x) + adx * fabsf(e2z),
+                Pz = adx * fabsf(e2y) + ady * fabsf(e2x);
+    const float det = e1x * px + e1y * py + e1z * pz;
+    const float Mdet = fabsf(e1x) * Px + fabsf(e1y) * Py + fabsf(e1z) * Pz;
+    if (!(fabsf(det) > fmaf(kFilt, Mdet, kTiny))) return MT_UNSURE;  // near-parallel / NaN
+    const float sg = det < 0.0f ? -1.0f : 1.0f;
+    const float sx = r.ox - A.x, sy = r.oy - A.y, sz = r.oz - A.z;
+    const float asx = fabsf(sx), asy = fabsf(sy), asz = fabsf(sz);
+    const float nu = sg * (sx * px + sy * py + sz * pz);
+    const float Mu = asx * Px + asy * Py + asz * Pz;
+    const float bu = fmaf(kFilt, Mu, kTiny);
+    if (nu < -bu) return MT_MISS;
+    const float qx = sy * e1z - sz * e1y, qy = sz * e1x - sx * e1z, qz = sx * e1y - sy * e1x;
+    const float Qx = asy * fabsf(e1z) + asz * fabsf(e1y), Qy = asz * fabsf(e1x) + asx * fabsf(e1z),
+                Qz = asx * fabsf(e1y) + asy * fabsf(e1x);
+    const float nv = sg * (r.dx * qx + r.dy * qy + r.dz * qz);
+    const float Mv = adx * Qx + ady * Qy + adz * Qz;
+    const float bv = fmaf(kFilt, Mv, kTiny);
+    if (nv < -bv) return MT_MISS;
+    const float adet = fabsf(det);
+    const float w = adet - nu - nv;
+    const float bw = fmaf(kFilt, Mdet + Mu + Mv, kTiny);
+    if (w < -bw) return MT_MISS;
+    const float nt = sg * (e2x * qx + e2y * qy + e2z * qz);
+    const float Mt = fabsf(e2x) * Qx + fabsf(e2y) * Qy + fabsf(e2z) * Qz;
+    const float bt = fmaf(kFilt, Mt, kTiny);
+    if (nt < -bt) return MT_MISS;
+    const float z = adet - nt;
+    const float bz = fmaf(kFilt, Mdet + Mt, kTiny);
+    if (z < -bz) return MT_MISS;
+    if (nu > bu && nv > bv && w > bw && nt > bt && z > bz) {
+        t = __fdiv_rn(nt, adet);
+        et = kTerr * (Mt + Mdet) / adet + 3.0f * kU;
+        return MT_HIT;
+    }
+    return MT_UNSURE;
+}
+
+// ---------------------------------------------------------------- fp64 mirror
+// Exactly the oracle's operation order (oracle/rsi_oracle.c rsi_oracle_mt,
+// SURVEY 8(c)); each * and +/- is a separately rounded IEEE double op.
+__device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
+
+__device__ __noinline__ int mt64(const Ray& r, const float4 A, const float4 B, const float4 C, double* t_out) {
+    const double Ox = r.ox, Oy = r.oy, Oz = r.oz;
+    const double dx = ds((double)r.ex, Ox), dy = ds((double)r.ey, Oy), dz = ds((double)r.ez, Oz);
+    const double Ax = A.x, Ay = A.y, Az = A.z;
+    const double e1x = ds(B.x, Ax), e1y = ds(B.y, Ay), e1z = ds(B.z, Az);
+    const double e2x = ds(C.x, Ax), e2y = ds(C.y, Ay), e2z = ds(C.z, Az);
+    const double sx = ds(Ox, Ax), sy = ds(Oy, Ay), sz = ds(Oz, Az);
+    const double px = ds(dm(dy, e2z), dm(dz, e2y));
+    const double py = ds(dm(dz, e2x), dm(dx, e2z));
+    const double pz = ds(dm(dx, e2y), dm(dy, e2x));
+    double det = da(da(dm(e1x, px), dm(e1y, py)), dm(e1z, pz));
+    const double qx = ds(dm(sy, e1z), dm(sz, e1y));
+    const double qy = ds(dm(sz, e1x), dm(sx, e1z));
+    const double qz = ds(dm(sx, e1y), dm(sy, e1x));
+    double nu = da(da(dm(sx, px), dm(sy, py)), dm(sz, pz));
+    double nv = da(da(dm(dx, qx), dm(dy, qy)), dm(dz, qz));
+    double nt = da(da(dm(e2x, qx), dm(e2y, qy)), dm(e2z, qz));
+    if (det == 0.0) return 0;
+    if (t_out) *t_out = __ddiv_rn(nt, det);
+    if (det < 0.0) {
+        det = -det;
+        nu = -nu;
+        nv = -nv;
+        nt = -nt;
+    }
+    return (nu >= 0.0) && (nv >= 0.0) && (da(nu, nv) <= det) && (nt >= 0.0) && (nt <= det);
+}
+
+__device__ __forceinline__ void load_tri(const float4* __restrict__ tris, int k, float4& A, float4& B, float4& C) {
+    A = __ldg(tris + 3 * k);
+    B = __ldg(tris + 3 * k + 1);
+    C = __ldg(tris + 3 * k + 2);
+}
+
+// ---------------------------------------------------------------- traversal skeleton
+// leaf(slot) returns true to terminate the walk; tclip may shrink inside it.
+template <class LeafFn>
+__device__ __forceinline__ void traverse(const float4* __restrict__ nodes, const Ray& r, float& tclip,
+                                         LeafFn&& leaf) {
+    int stack[kStack];
+    int sp = 0;
+    int node = 0;
+    while (true) {
+        const float4* nd = nodes + 4 * node;
+        const float4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2);
+        const int4 n3 = __ldg(reinterpret_cast<const int4*>(nd + 3));
+        float nearL, nearR;
+        bool hL = slab(r, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, tclip, nearL);
+        bool hR = slab(r, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, tclip, nearR);
+        if (hL && n3.x < 0) {
+            if (leaf(~n3.x)) return;
+            hL = false;
+        }
+        if (hR && n3.y < 0) {
+            if (leaf(~n3.y)) return;
+            hR = false;
+        }
+        if (hL && hR) {
+            const bool rfirst = nearR < nearL;
+            stack[sp++] = rfirst ? n3.x : n3.y;
+            node = rfirst ? n3.y : n3.x;
+        } else if (hL) {
+            node = n3.x;
+        } else if (hR) {
+            node = n3.y;
+        } else {
+            if (sp == 0) return;
+            node = stack[--sp];
+        }
+    }
+}
+
+struct Stats {
+    unsigned fp64_pairs = 0, fp64_ray = 0, nonfinite = 0;
+};
+
+__device__ __forceinline__ void flush_stats(const Stats& st, unsigned long long* stats) {
+    const unsigned m = 0xffffffffu;
+    unsigned a = st.fp64_pairs, b = st.fp64_ray, c = st.nonfinite;
+    if (__any_sync(m, a | b | c)) {
+        for (int o = 16; o; o >>= 1) {
+            a += __shfl_xor_sync(m, a, o);
+            b += __shfl_xor_sync(m, b, o);
+            c += __shfl_xor_sync(m, c, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (a) atomicAdd(stats + ST_FP64_PAIRS, (unsigned long long)a);
+            if (b) atomicAdd(stats + ST_FP64_RAYS, (unsigned long long)b);
+            if (c) atomicAdd(stats + ST_NONFINITE, (unsigned long long)c);
+        }
+    }
+}
+
+// Decide one (ray, leaf) pair: MT_MISS, or MT_HIT with either (t32, et) or an
+// exact t64 (is64 = true).
+template <bool kFP64>
+__device__ __forceinline__ int decide(const Ray& r, const float4& A, const float4& B, const float4& C, float& t32,
+                                      float& et, double& t64, bool& is64, Stats& st) {
+    if (!kFP64) {
+        int s = mt32(r, A, B, C, t32, et);
+        if (s != MT_UNSURE) {
+            is64 = false;
+            return s;
+        }
+        ++st.fp64_pairs;
+    }
+    is64 = true;
+    return mt64(r, A, B, C, &t64) ? MT_HIT : MT_MISS;
+}
+
+// ---------------------------------------------------------------- boolean
+template <bool kFP64>
+__global__ void __launch_bounds__(kThreads) k_boolean(const float4* __restrict__ nodes,
+                                                      const float4* __restrict__ tris,
+                                                      const float* __restrict__ S, const float* __restrict__ E,
+                                                      int64_t n, uint8_t* __restrict__ hit,
+                                                      unsigned long long* stats) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    Stats st;
+    if (i < n) {
+        Ray r;
+        bool nonfinite;
+        bool found = false;
+        if (load_ray(r, S, E, i, nonfinite)) {
+            float tclip = 1.0f;
+            traverse(nodes, r, tclip, [&](int k) {
+                float4 A, B, C;
+                load_tri(tris, k, A, B, C);
+                float t32, et;
+                double t64;
+                bool is64;
+                if (decide<kFP64>(r, A, B, C, t32, et, t64, is64, st) == MT_HIT) {
+                    found = true;
+                    return true;  // any-hit early exit
+                }
+                return false;
+            });
+        }
+        st.nonfinite = nonfinite;
+        hit[i] = found ? 1 : 0;
+    }
+    flush_stats(st, stats);
+}
+
+// ---------------------------------------------------------------- barycentric (nearest hit)
+// Best = lexicographic min of (t, original id) (reading R5).  A hit is held as
+// an interval [t32 - et, t32 + et] or an exact fp64 value; overlapping
+// intervals are resolved by recomputing both in the fp64 mirror.
+struct Best {
+    int id = 0x7fffffff;  // original triangle id
+    int slot = -1;        // leaf slot (to recompute)
+    float t = 0.f, e = 0.f;
+    bool is64 = false;
+    double t64 = 0.0;
+};
+
+template <bool kFP64>
+__global__ void __launch_bounds__(kThreads) k_barycentric(const float4* __restrict__ nodes,
+                                                          const float4* __restrict__ tris,
+                                                          const float* __restrict__ S,
+                                                          const float* __restrict__ E, int64_t n,
+                                                          int32_t* __restrict__ tri_out, float* __restrict__ t_out,
+                                                          float* __restrict__ dist_out,
+                                                          float* __restrict__ point_out,
+                                                          unsigned long long* stats) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    Stats st;
+    if (i < n) {
+        Ray r;
+        bool nonfinite;
+        Best b;
+        if (load_ray(r, S, E, i, nonfinite)) {
+            float tclip = 1.0f;
+            traverse(nodes, r, tclip, [&](int k) {
+                float4 A, B, C;
+                load_tri(tris, k, A, B, C);
+                float t32, et;
+                double t64;
+                bool is64;
+                if (decide<kFP64>(r, A, B, C, t32, et, t64, is64, st) != MT_HIT) return false;
+                const int id = __float_as_int(A.w);
+                bool take;
+                if (b.slot < 0) {
+                    take = true;
+                } else {
+                    double clo = is64 ? t64 : (double)t32 - (double)et, chi = is64 ? t64 : (double)t32 + (double)et;
+                    double blo = b.is64 ? b.t64 : (double)b.t - (double)b.e, bhi = b.is64 ? b.t64 : (double)b.t + (double)b.e;
+                    if (chi < blo) {
+                        take = true;
+                    } else if (clo > bhi) {
+                        take = false;
+                    } else {  // ambiguous order: settle both in the fp64 mirror
+                        st.fp64_ray = 1;
+                        if (!is64) {
+                            mt64(r, A, B, C, &t64);
+                            is64 = true;
+                        }
+                        if (!b.is64) {
+                            float4 bA, bB, bC;
+                            load_tri(tris, b.slot, bA, bB, bC);
+                            mt64(r, bA, bB, bC, &b.t64);
+                            b.is64 = true;
+                        }
+                        take = (t64 < b.t64) || (t64 == b.t64 && id < b.id);
+                    }
+                }
+                if (take) {
+                    b.id = id;
+                    b.slot = k;
+                    b.is64 = is64;
+                    if (is64) {
+                        b.t64 = t64;
+                        tclip = fminf(tclip, __double2float_ru(t64));
+                    } else {
+                        b.t = t32;
+                        b.e = et;
+                        tclip = fminf(tclip, __fadd_ru(t32, et));
+                    }
+                }
+                return false;
+            });
+        }
+        st.nonfinite = nonfinite;
+        if (b.slot >= 0) {
+            float t;
+            if (b.is64) {
+                t = (float)b.t64;
+            } else if (b.e <= kOutTol) {
+                t = b.t;
+            } else {  // fp32 value not certified to the output tolerance
+                float4 bA, bB, bC;
+                load_tri(tris, b.slot, bA, bB, bC);
+                double t64 = 0.0;
+                mt64(r, bA, bB, bC, &t64);
+                t = (float)t64;
+                st.fp64_ray = 1;
+            }
+            tri_out[i] = b.id;
+            if (t_out) t_out[i] = t;
+            if (dist_out) dist_out[i] = t * sqrtf(r.dx * r.dx + r.dy * r.dy + r.dz * r.dz);
+            if (point_out) {
+                point_out[3 * i] = fmaf(t, r.dx, r.ox);
+                point_out[3 * i + 1] = fmaf(t, r.dy, r.oy);
+                point_out[3 * i + 2] = fmaf(t, r.dz, r.oz);
+            }
+        } else {
+            tri_out[i] = -1;
+            if (t_out) t_out[i] = NAN;
+            if (dist_out) dist_out[i] = NAN;
+            if (point_out) {
+                point_out[3 * i] = NAN;
+                point_out[3 * i + 1] = NAN;
+                point_out[3 * i + 2] = NAN;
+            }
+        }
+    }
+    flush_stats(st, stats);
+}
+
+// ---------------------------------------------------------------- intercept_count
+// count = number of single-linkage clusters of hit t with threshold tau
+// (reading R4): 1 + #{sorted gaps > tau}.  The fp32 path is used only when
+// every pairwise |t_a - t_b| vs tau decision is certified; otherwise all hit t
+// are recomputed in the fp64 mirror and counted exactly as the oracle does.
+__device__ __forceinline__ void sort_small(double* v, int n) {
+    for (int a = 1; a < n; ++a) {
+        double x = v[a];
+        int b = a - 1;
+        while (b >= 0 && v[b] > x) {
+            v[b + 1] = v[b];
+            --b;
+        }
+        v[b + 1] = x;
+    }
+}
+
+template <bool kFP64>
+__global__ void __launch_bounds__(kThreads) k_count(const float4* __restrict__ nodes,
+                                                    const float4* __restrict__ tris, const float* __restrict__ S,
+                                                    const float* __restrict__ E, int64_t n, double tau,
+                                                    int32_t* __restrict__ count_out, int32_t* __restrict__ ovf_list,
+                                                    uint32_t* scratch, unsigned long long* stats) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    Stats st;
+    if (i < n) {
+        Ray r;
+        bool nonfinite;
+        float lt[kCountCap], le[kCountCap];
+        int lk[kCountCap];
+        int nh = 0;
+        bool overflow = false;
+        if (load_ray(r, S, E, i, nonfinite)) {
+            float tclip = 1.0f;
+            traverse(nodes, r, tclip, [&](int k) {
+                float4 A, B, C;
+                load_tri(tris, k, A, B, C);
+                float t32, et;
+                double t64;
+                bool is64;
+                if (decide<kFP64>(r, A, B, C, t32, et, t64, is64, st) != MT_HIT) return false;
+                if (nh == kCountCap) {
+                    overflow = true;
+                    return true;
+                }
+                if (is64) {
+                    t32 = (float)t64;
+                    et = fmaf(kU, fabsf(t32), kTiny);
+                }
+#pragma unroll
+                for (int x = 0; x < kCountCap; ++x)
+                    if (x == nh) {
+                        lt[x] = t32;
+                        le[x] = et;
+                        lk[x] = k;
+                    }
+                ++nh;
+                return false;
+            });
+        }
+        st.nonfinite = nonfinite;
+        if (overflow) {
+            uint32_t pos = atomicAdd(&scratch[SCR_OVF_COUNT], 1u);
+            ovf_list[pos] = (int32_t)i;
+            count_out[i] = -1;
+        } else if (nh <= 1) {
+            count_out[i] = nh;
+        } else {
+            const float ftau = (float)tau;
+            bool sure = true;
+#pragma unroll
+            for (int a = 0; a < kCountCap; ++a)
+#pragma unroll
+                for (int c = a + 1; c < kCountCap; ++c)
+                    if (c < nh) {
+                        float g = fabsf(lt[a] - lt[c]);
+                        float tol = le[a] + le[c] + fmaf(2.0f * kU, g + ftau, kTiny);
+                        if (fabsf(g - ftau) <= tol) sure = false;
+                    }
+            int cnt = 1;
+            if (sure) {
+                // insertion sort of the fp32 values, then count gaps > tau
+#pragma unroll
+                for (int a = 1; a < kCountCap; ++a)
+#pragma unroll
+                    for (int c = a; c > 0; --c)
+                        if (c < nh && lt[c - 1] > lt[c]) {
+                            float x = lt[c];
+                            lt[c] = lt[c - 1];
+                            lt[c - 1] = x;
+                        }
+#pragma unroll
+                for (int a = 0; a + 1 < kCountCap; ++a)
+                    if (a + 1 < nh && lt[a + 1] - lt[a] > ftau) ++cnt;
+            } else {
+                st.fp64_ray = 1;
+                double v[kCountCap];
+                for (int a = 0; a < nh; ++a) {
+                    float4 A, B, C;
+                    load_tri(tris, lk[a], A, B, C);
+                    mt64(r, A, B, C, &v[a]);
+                }
+                sort_small(v, nh);
+                for (int a = 0; a + 1 < nh; ++a)
+                    if (da(v[a + 1], -v[a]) > tau) ++cnt;
+            }
+            count_out[i] = cnt;
+        }
+    }
+    flush_stats(st, stats);
+}
+
+// ---------------------------------------------------------------- exact re-pass for overflowed rays
+// Pass A: raw hit count per overflowed ray and its segment offset in a pool.
+__global__ void __launch_bounds__(kThreads) k_ovf_size(const float4* __restrict__ nodes,
+                                                       const float4* __restrict__ tris, const float* __restrict__ S,
+                                                       const float* __restrict__ E, const int32_t* __restrict__ list,
+                                                       int n_ovf, int32_t* __restrict__ seg, uint32_t* scratch) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_ovf) return;
+    Ray r;
+    bool nonfinite;
+    load_ray(r, S, E, list[j], nonfinite);
+    int nh = 0;
+    float tclip = 1.0f;
+    traverse(nodes, r, tclip, [&](int k) {
+        float4 A, B, C;
+        load_tri(tris, k, A, B, C);
+        float t32, et;
+        int s = mt32(r, A, B, C, t32, et);
+        if (s == MT_HIT || (s == MT_UNSURE && mt64(r, A, B, C, nullptr))) ++nh;
+        return false;
+    });
+    seg[2 * j] = (int32_t)atomicAdd(&scratch[SCR_OVF_TOTAL], (uint32_t)nh);
+    seg[2 * j + 1] = nh;
+}
+
+// Pass B: exact fp64 t of every hit, then sort the segment and count.
+__global__ void __launch_bounds__(kThreads) k_ovf_count(const float4* __restrict__ nodes,
+                                                        const float4* __restrict__ tris, const float* __restrict__ S,
+                                                        const float* __restrict__ E, const int32_t* __restrict__ list,
+                                                        int n_ovf, const int32_t* __restrict__ seg, double* pool,
+                                                        double tau, int32_t* __restrict__ count_out) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_ovf) return;
+    Ray r;
+    bool nonfinite;
+    const int64_t i = list[j];
+    load_ray(r, S, E, i, nonfinite);
+    double* v = pool + seg[2 * j];
+    const int cap = seg[2 * j + 1];
+    int nh = 0;
+    float tclip = 1.0f;
+    traverse(nodes, r, tclip, [&](int k) {
+        float4 A, B, C;
+        load_tri(tris, k, A, B, C);
+        double t64;
+        if (mt64(r, A, B, C, &t64) && nh < cap) v[nh++] = t64;
+        return false;
+    });
+    // heap sort v[0..nh)
+    for (int start = nh / 2 - 1; start >= 0; --start) {
+        int root = start;
+        while (2 * root + 1 < nh) {
+            int c = 2 * root + 1;
+            if (c + 1 < nh && v[c] < v[c + 1]) ++c;
+            if (v[root] < v[c]) {
+                double x = v[root];
+                v[root] = v[c];
+                v[c] = x;
+                root = c;
+            } else {
+                break;
+            }
+        }
+    }
+    for (int end = nh - 1; end > 0; --end) {
+        double x = v[0];
+        v[0] = v[end];
+        v[end] = x;
+        int root = 0;
+        while (2 * root + 1 < end) {
+            int c = 2 * root + 1;
+            if (c + 1 < end && v[c] < v[c + 1]) ++c;
+            if (v[root] < v[c]) {
+                double y = v[root];
+                v[root] = v[c];
+                v[c] = y;
+                root = c;
+            } else {
+                break;
+            }
+        }
+    }
+    int cnt = nh > 0 ? 1 : 0;
+    for (int a = 0; a + 1 < nh; ++a)
+        if (da(v[a + 1], -v[a]) > tau) ++cnt;
+    count_out[i] = cnt;
+}
+
+// ---------------------------------------------------------------- ordered compaction (3a)
+constexpr int kCompactTile = 4096;
+
+__global__ void __launch_bounds__(256) k_compact_count(const int32_t* __restrict__ tri, int64_t n,
+                                                       uint32_t* __restrict__ blk) {
+    __shared__ uint32_t c;
+    if (threadIdx.x == 0) c = 0;
+    __syncthreads();
+    int64_t beg = (int64_t)blockIdx.x * kCompactTile;
+    uint32_t mine = 0;
+    for (int64_t i = beg + threadIdx.x; i < beg + kCompactTile && i < n; i += blockDim.x) mine += tri[i] >= 0;
+    for (int o = 16; o; o >>= 1) mine += __shfl_xor_sync(0xffffffffu, mine, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&c, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) blk[blockIdx.x] = c;
+}
+
+__global__ void __launch_bounds__(1024) k_compact_scan(uint32_t* blk, int m, int32_t* d_n) {
+    // single CTA exclusive scan (m is small: n / 4096)
+    __shared__ uint32_t carry;
+    __shared__ uint32_t wsum[32];
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int base = 0; base < m; base += 1024) {
+        int i = base + threadIdx.x;
+        uint32_t v = i < m ? blk[i] : 0u, inc = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) wsum[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            uint32_t s = wsum[lane], si = s;
+            for (int o = 1; o < 32; o <<= 1) {
+                uint32_t y = __shfl_up_sync(0xffffffffu, si, o);
+                if (lane >= o) si += y;
+            }
+            wsum[lane] = si - s;
+        }
+        __syncthreads();
+        if (i < m) blk[i] = carry + wsum[w] + inc - v;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry += wsum[31] + inc;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *d_n = (int32_t)carry;
+}
+
+__global__ void __launch_bounds__(256) k_compact_write(const int32_t* __restrict__ tri, int64_t n,
+                                                       const uint32_t* __restrict__ blk, int32_t* __restrict__ ids) {
+    // each warp handles a contiguous chunk of the tile in order
+    __shared__ uint32_t wtot[8];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t beg = (int64_t)blockIdx.x * kCompactTile + (int64_t)w * (kCompactTile / 8);
+    const int64_t end = beg + kCompactTile / 8;
+    uint32_t cnt = 0;
+    for (int64_t i = beg + lane; i < end; i += 32) cnt += (i < n && tri[i] >= 0);
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if (lane == 0) wtot[w] = cnt;
+    __syncthreads();
+    uint32_t base = blk[blockIdx.x];
+    for (int x = 0; x < w; ++x) base += wtot[x];
+    uint32_t lt;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(lt));
+    for (int64_t i0 = beg; i0 < end; i0 += 32) {
+        int64_t i = i0 + lane;
+        bool h = i < n && tri[i] >= 0;
+        uint32_t bal = __ballot_sync(0xffffffffu, h);
+        if (h) ids[base + __popc(bal & lt)] = (int32_t)i;
+        base += __popc(bal);
+    }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host side
+template <bool kFP64>
+static void launch_main(rsi_bvh* h, const float* S, const float* E, int64_t n, int32_t mode,
+                        const rsi_outputs_t* out, cudaStream_t s) {
+    const int64_t blocks = (n + kThreads - 1) / kThreads;
+    if (mode == RSI_MODE_BOOLEAN) {
+        k_boolean<kFP64><<<(unsigned)blocks, kThreads, 0, s>>>(h->nodes, h->tris, S, E, n, out->hit, h->stats);
+    } else if (mode == RSI_MODE_BARYCENTRIC) {
+        k_barycentric<kFP64><<<(unsigned)blocks, kThreads, 0, s>>>(h->nodes, h->tris, S, E, n, out->tri, out->t,
+                                                                   out->dist, out->point, h->stats);
+    } else {
+        k_count<kFP64><<<(unsigned)blocks, kThreads, 0, s>>>(h->nodes, h->tris, S, E, n, h->opt.dedup_tau,
+                                                             out->count, h->ovf_list, h->scratch, h->stats);
+    }
+}
+
+rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, int64_t n, int32_t mode,
+                                  const rsi_outputs_t* out, cudaStream_t s) {
+    if (n == 0) return RSI_OK;
+    if (n > ((int64_t)1 << 31) - 1)
+        return rsi_set_error(RSI_E_INVALID_ARG, "n_rays %lld exceeds 2^31-1", (long long)n);
+    rsi_status_t st;
+    if (mode == RSI_MODE_INTERCEPT_COUNT) {
+        if (h->ovf_cap < n) {
+            if (h->ovf_list) cudaFreeAsync(h->ovf_list, s);
+            h->ovf_list = nullptr;
+            h->ovf_cap = 0;
+            st = rsi_cuda_check(cudaMallocAsync((void**)&h->ovf_list, (size_t)n * sizeof(int32_t), s), "overflow list");
+            if (st != RSI_OK) return RSI_E_OOM;
+            h->ovf_cap = n;
+        }
+        st = rsi_cuda_check(cudaMemsetAsync(h->scratch + SCR_OVF_COUNT, 0, 2 * sizeof(uint32_t), s), "memset");
+        if (st != RSI_OK) return st;
+    }
+    if (h->opt.flags & RSI_OPT_FP64_MOLLER)
+        launch_main<true>(h, S, E, n, mode, out, s);
+    else
+        launch_main<false>(h, S, E, n, mode, out, s);
+    st = rsi_cuda_check(cudaGetLastError(), "traversal launch");
+    if (st != RSI_OK) return st;
+    if (mode != RSI_MODE_INTERCEPT_COUNT) return RSI_OK;
+
+    // intercept_count: exact re-pass for rays that overflowed the register list
+    st = rsi_cuda_check(cudaMemcpyAsync(h->h_pinned, h->scratch + SCR_OVF_COUNT, sizeof(uint32_t),
+                                        cudaMemcpyDeviceToHost, s), "overflow count");
+    if (st != RSI_OK) return st;
+    st = rsi_cuda_check(cudaStreamSynchronize(s), "intercept_count");
+    if (st != RSI_OK) return st;
+    const int n_ovf = (int)h->h_pinned[0];
+    if (n_ovf == 0) return RSI_OK;
+    int32_t* seg = nullptr;
+    double* pool = nullptr;
+    st = rsi_cuda_check(cudaMallocAsync((void**)&seg, (size_t)n_ovf * 2 * sizeof(int32_t), s), "overflow segs");
+    if (st != RSI_OK) return RSI_E_OOM;
+    const int nb = rsi_ceil_div(n_ovf, kThreads);
+    k_ovf_size<<<nb, kThreads, 0, s>>>(h->nodes, h->tris, S, E, h->ovf_list, n_ovf, seg, h->scratch);
+    cudaMemcpyAsync(h->h_pinned, h->scratch + SCR_OVF_TOTAL, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+    st = rsi_cuda_check(cudaStreamSynchronize(s), "overflow sizing");
+    if (st != RSI_OK) {
+        cudaFreeAsync(seg, s);
+        return st;
+    }
+    const size_t total = h->h_pinned[0];
+    st = rsi_cuda_check(cudaMallocAsync((void**)&pool, (total ? total : 1) * sizeof(double), s), "overflow pool");
+    if (st != RSI_OK) {
+        cudaFreeAsync(seg, s);
+        return RSI_E_OOM;
+    }
+    k_ovf_count<<<nb, kThreads, 0, s>>>(h->nodes, h->tris, S, E, h->ovf_list, n_ovf, seg, pool, h->opt.dedup_tau,
+                                        out->count);
+    st = rsi_cuda_check(cudaGetLastError(), "overflow pass");
+    cudaFreeAsync(pool, s);
+    cudaFreeAsync(seg, s);
+    h->host_overflow += (uint64_t)n_ovf;
+    return st;
+}
+
+rsi_status_t rsi_compact_device(const int32_t* tri, int64_t n, int32_t* ids, int32_t* d_n, cudaStream_t s) {
+    if (n == 0) return rsi_cuda_check(cudaMemsetAsync(d_n, 0, sizeof(int32_t), s), "memset");
+    const int nb = rsi_ceil_div(n, kCompactTile);
+    uint32_t* blk = nullptr;
+    rsi_status_t st = rsi_cuda_check(cudaMallocAsync((void**)&blk, (size_t)nb * sizeof(uint32_t), s), "compact");
+    if (st != RSI_OK) return RSI_E_OOM;
+    k_compact_count<<<nb, 256, 0, s>>>(tri, n, blk);
+    k_compact_scan<<<1, 1024, 0, s>>>(blk, nb, d_n);
+    k_compact_write<<<nb, 256, 0, s>>>(tri, n, blk, ids);
+    st = rsi_cuda_check(cudaGetLastError(), "compaction launch");
+    cudaFreeAsync(blk, s);
+    return st;
+}

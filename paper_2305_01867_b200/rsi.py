@@ -1,0 +1,327 @@
+"""Thin ctypes binding of the C-ABI in include/rsi.h (argument marshalling only).
+
+Every step of the path runs in librsi.so's CUDA kernels; this module only turns
+torch tensors into pointers, picks the current CUDA stream and allocates the
+caller-owned outputs with torch.  There is no CPU fallback: if librsi.so is
+missing or no CUDA device is present, calls raise.
+
+Names follow the C entry points (rsi_build, rsi_intersect, rsi_test, ...).
+The paper's user-level call `PyCudaRSI(params).test(vertices, triangles,
+raysFrom, raysTo, cfg)` is `rsi_test(..., cfg={'mode': m})`.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _build
+
+MODES = {"boolean": 0, "barycentric": 1, "intercept_count": 2}
+OPT_FP64_MOLLER = 1
+
+_lock = threading.Lock()
+_lib = None
+
+_p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+
+
+class RsiError(RuntimeError):
+    """A non-zero rsi_status_t; .status holds the code."""
+
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"rsi status {status}: {msg}")
+        self.status = status
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("struct_size", ctypes.c_uint32), ("flags", ctypes.c_uint32), ("dedup_tau", ctypes.c_double)]
+
+
+class _Outputs(ctypes.Structure):
+    _fields_ = [("hit", _p), ("count", _p), ("tri", _p), ("t", _p), ("dist", _p), ("point", _p)]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_uint64) for n in ("rays", "fp64_pairs", "fp64_rays", "overflow_rays", "nonfinite_rays")]
+
+
+def lib_path() -> str:
+    return _build.LIB
+
+
+def load():
+    """Load librsi.so (raises if it was not built -- no fallback)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(_build.LIB):
+            raise RuntimeError(f"{_build.LIB} is missing: run __graft_entry__.build() "
+                               "(nvcc sm_100a); there is no CPU fallback")
+        lib = ctypes.CDLL(_build.LIB)
+        sig = {
+            "rsi_version": ([], ctypes.c_char_p),
+            "rsi_last_error": ([], ctypes.c_char_p),
+            "rsi_build": ([_p, _i64, _p, _i64, _p, _p, ctypes.POINTER(_p)], ctypes.c_int),
+            "rsi_rebuild": ([_p, _p, _i64, _p, _i64, _p], ctypes.c_int),
+            "rsi_intersect": ([_p, _p, _p, _i64, _i32, ctypes.POINTER(_Outputs), _p], ctypes.c_int),
+            "rsi_test": ([_p, _i64, _p, _i64, _p, _p, _i64, _i32, _p, ctypes.POINTER(_Outputs), _p], ctypes.c_int),
+            "rsi_compact_hits": ([_p, _i64, _p, _p, _p], ctypes.c_int),
+            "rsi_free": ([_p], ctypes.c_int),
+            "rsi_get_stats": ([_p, ctypes.POINTER(_Stats), _p], ctypes.c_int),
+            "rsi_reset_stats": ([_p, _p], ctypes.c_int),
+            "rsi_bvh_info": ([_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _p, _p], ctypes.c_int),
+            "rsi_bvh_download": ([_p, _p, _p, _p, _p, _p, _p, _p], ctypes.c_int),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(lib, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = lib
+        return lib
+
+
+def _check(rc: int):
+    if rc != 0:
+        raise RsiError(rc, load().rsi_last_error().decode())
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _dev(t: torch.Tensor, dtype, name: str, cols: int | None = 3) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor):
+        t = torch.as_tensor(np.asarray(t))
+    if t.dtype != dtype:
+        if dtype == torch.int32 and t.dtype in (torch.int64, torch.uint64):
+            # the case-study-1 bug: never reinterpret / silently narrow indices
+            raise TypeError(f"{name} must be int32, got {t.dtype} (P:272-299: int width mismatch)")
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if cols is not None and (t.dim() != 2 or t.shape[1] != cols):
+        raise ValueError(f"{name} must have shape [n, {cols}], got {tuple(t.shape)}")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (use rsi_test for host arrays)")
+    return t.contiguous()
+
+
+def rsi_version() -> str:
+    return load().rsi_version().decode()
+
+
+@dataclass
+class Options:
+    fp64_moller: bool = False   # P:501 USE_DOUBLE_PRECISION_MOLLER
+    dedup_tau: float = 1e-6     # reading R4
+
+    def _c(self) -> _Options:
+        return _Options(ctypes.sizeof(_Options), OPT_FP64_MOLLER if self.fp64_moller else 0, float(self.dedup_tau))
+
+
+class Handle:
+    """Owns an rsi_handle_t (the BVH on one device)."""
+
+    def __init__(self, ptr: int, device: torch.device):
+        self._ptr = ptr
+        self.device = device
+
+    @property
+    def ptr(self) -> int:
+        if not self._ptr:
+            raise ValueError("handle already freed")
+        return self._ptr
+
+    def free(self):
+        if self._ptr:
+            _check(load().rsi_free(self._ptr))
+            self._ptr = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.free()
+
+
+def rsi_build(vertices: torch.Tensor, triangles: torch.Tensor, options: Options | None = None,
+              stream=None) -> Handle:
+    """rsi_build: LBVH over the mesh (device tensors float32 [N_v,3], int32 [N_t,3])."""
+    lib = load()
+    V = _dev(vertices, torch.float32, "vertices")
+    T = _dev(triangles, torch.int32, "triangles")
+    opt = (options or Options())._c()
+    h = _p()
+    with torch.cuda.device(V.device):
+        _check(lib.rsi_build(V.data_ptr(), V.shape[0], T.data_ptr(), T.shape[0], ctypes.byref(opt),
+                             _stream(stream), ctypes.byref(h)))
+    return Handle(h.value, V.device)
+
+
+def rsi_rebuild(h: Handle, vertices: torch.Tensor, triangles: torch.Tensor, stream=None) -> Handle:
+    V = _dev(vertices, torch.float32, "vertices")
+    T = _dev(triangles, torch.int32, "triangles")
+    with torch.cuda.device(V.device):
+        _check(load().rsi_rebuild(h.ptr, V.data_ptr(), V.shape[0], T.data_ptr(), T.shape[0], _stream(stream)))
+    return h
+
+
+def alloc_outputs(n: int, mode: str, device, with_t: bool = True) -> dict:
+    """torch-allocated caller-owned outputs for `mode` (see rsi_outputs_t)."""
+    if mode == "boolean":
+        return {"hit": torch.empty(n, dtype=torch.uint8, device=device)}
+    if mode == "intercept_count":
+        return {"count": torch.empty(n, dtype=torch.int32, device=device)}
+    if mode == "barycentric":
+        out = {"tri": torch.empty(n, dtype=torch.int32, device=device),
+               "dist": torch.empty(n, dtype=torch.float32, device=device),
+               "point": torch.empty((n, 3), dtype=torch.float32, device=device)}
+        if with_t:
+            out["t"] = torch.empty(n, dtype=torch.float32, device=device)
+        return out
+    raise ValueError(f"mode must be one of {list(MODES)}, got {mode!r}")
+
+
+def _outputs_struct(out: dict) -> _Outputs:
+    o = _Outputs()
+    for k in ("hit", "count", "tri", "t", "dist", "point"):
+        if out.get(k) is not None:
+            setattr(o, k, out[k].data_ptr())
+    return o
+
+
+def rsi_intersect(h: Handle, start: torch.Tensor, end: torch.Tensor, mode: str = "boolean",
+                  out: dict | None = None, stream=None) -> dict:
+    """rsi_intersect: per-ray traversal + Moller-Trumbore; returns the output dict."""
+    if mode not in MODES:
+        raise ValueError(f"mode must be one of {list(MODES)}, got {mode!r}")
+    S = _dev(start, torch.float32, "start")
+    E = _dev(end, torch.float32, "end")
+    if S.shape != E.shape:
+        raise ValueError("start/end shape mismatch")
+    n = S.shape[0]
+    if out is None:
+        out = alloc_outputs(n, mode, S.device)
+    o = _outputs_struct(out)
+    with torch.cuda.device(S.device):
+        _check(load().rsi_intersect(h.ptr, S.data_ptr(), E.data_ptr(), n, MODES[mode], ctypes.byref(o),
+                                    _stream(stream)))
+    return out
+
+
+def rsi_compact_hits(tri: torch.Tensor, stream=None):
+    """Step 3a: ascending ray ids with tri >= 0, on the device.
+    Returns (ids_buffer [n] int32, n_hits int32 device scalar)."""
+    T = _dev(tri, torch.int32, "tri", cols=None)
+    ids = torch.empty(T.numel(), dtype=torch.int32, device=T.device)
+    nh = torch.empty(1, dtype=torch.int32, device=T.device)
+    with torch.cuda.device(T.device):
+        _check(load().rsi_compact_hits(T.data_ptr(), T.numel(), ids.data_ptr(), nh.data_ptr(), _stream(stream)))
+    return ids, nh
+
+
+def sparse_barycentric(out: dict, stream=None):
+    """The paper's barycentric return: (intersecting_rays, distances,
+    hit_triangles, hit_points), rays ascending.  Compaction runs on the GPU;
+    the gather of the selected rows uses torch indexing (data movement only)."""
+    ids, nh = rsi_compact_hits(out["tri"], stream)
+    k = int(nh.item())
+    ids = ids[:k]
+    il = ids.long()
+    return ids, out["dist"][il], out["tri"][il], out["point"][il]
+
+
+def rsi_test(vertices, triangles, start, end, cfg: dict | None = None, options: Options | None = None,
+             stream=None, out: dict | None = None):
+    """End-to-end on HOST arrays through the C-ABI's rsi_test:
+    H2D, build, intersect, D2H, synchronize.  Returns the boolean array, the
+    counts, or (intersecting_rays, distances, hit_triangles, hit_points)."""
+    lib = load()
+    mode = (cfg or {}).get("mode", "boolean")
+    if mode not in MODES:
+        raise ValueError(f"mode must be one of {list(MODES)}, got {mode!r}")
+
+    def host(a, dtype, name):
+        if isinstance(a, torch.Tensor):
+            if a.is_cuda:
+                raise ValueError(f"{name}: rsi_test takes host arrays")
+            if a.dtype != dtype:
+                raise TypeError(f"{name} must be {dtype}, got {a.dtype}")
+            return a.contiguous()
+        a = np.asarray(a)
+        nd = {torch.float32: np.float32, torch.int32: np.int32}[dtype]
+        if a.dtype != nd:
+            raise TypeError(f"{name} must be {nd.__name__}, got {a.dtype} (P:272-299)")
+        return torch.from_numpy(np.ascontiguousarray(a))
+
+    V = host(vertices, torch.float32, "vertices").reshape(-1, 3)
+    T = host(triangles, torch.int32, "triangles").reshape(-1, 3)
+    S = host(start, torch.float32, "start").reshape(-1, 3)
+    E = host(end, torch.float32, "end").reshape(-1, 3)
+    n = S.shape[0]
+    if out is None:
+        out = {k: v.cpu() for k, v in alloc_outputs(n, mode, "cpu").items()}
+    o = _outputs_struct(out)
+    opt = (options or Options())._c()
+    _check(lib.rsi_test(V.data_ptr(), V.shape[0], T.data_ptr(), T.shape[0], S.data_ptr(), E.data_ptr(), n,
+                        MODES[mode], ctypes.byref(opt), ctypes.byref(o), _stream(stream)))
+    if mode == "boolean":
+        return out["hit"].numpy().astype(bool).reshape(n, 1)
+    if mode == "intercept_count":
+        return out["count"].numpy()
+    tri = out["tri"].numpy()
+    ids = np.nonzero(tri >= 0)[0].astype(np.int32)
+    return ids, out["dist"].numpy()[ids], tri[ids], out["point"].numpy()[ids]
+
+
+def rsi_get_stats(h: Handle, stream=None) -> dict:
+    st = _Stats()
+    _check(load().rsi_get_stats(h.ptr, ctypes.byref(st), _stream(stream)))
+    return {n: int(getattr(st, n)) for n, _ in _Stats._fields_}
+
+
+def rsi_reset_stats(h: Handle, stream=None):
+    _check(load().rsi_reset_stats(h.ptr, _stream(stream)))
+
+
+def rsi_free(h: Handle):
+    h.free()
+
+
+def rsi_bvh_info(h: Handle) -> dict:
+    nt, nn = _i64(), _i64()
+    lo = (ctypes.c_float * 3)()
+    hi = (ctypes.c_float * 3)()
+    _check(load().rsi_bvh_info(h.ptr, ctypes.byref(nt), ctypes.byref(nn), lo, hi))
+    return {"n_triangles": nt.value, "n_nodes": nn.value, "scene_lo": list(lo), "scene_hi": list(hi)}
+
+
+def rsi_bvh_download(h: Handle, stream=None) -> dict:
+    """Copy the BVH to host numpy arrays (P:204-241 debugging strategy)."""
+    info = rsi_bvh_info(h)
+    nt, nn = info["n_triangles"], info["n_nodes"]
+    d = {
+        "child": np.zeros((nn, 2), np.int32),
+        "box": np.zeros((nn, 2, 6), np.float32),
+        "leaf_tri": np.zeros(nt, np.int32),
+        "morton": np.zeros(nt, np.uint32),
+        "parent": np.zeros(nn + nt, np.int32),
+        "arrivals": np.zeros(nn, np.uint32),
+    }
+    ptrs = [d[k].ctypes.data_as(_p) for k in ("child", "box", "leaf_tri", "morton", "parent", "arrivals")]
+    _check(load().rsi_bvh_download(h.ptr, *ptrs, _stream(stream)))
+    d.update(info)
+    return d

@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""Benchmark of the hot path: LBVH build + traversal/Moller-Trumbore (+ NCCL gather at N>1).
+
+Contract: prints ONE JSON line on rank 0.
+
+  step     = one pass of the whole hot path over one batch of synthetic input:
+             rsi_rebuild (A1..A7: validate, extent, Morton, radix sort, Karras,
+             refit/pack) + rsi_intersect (A8..A9) [+ NCCL gather of the per-ray
+             outputs to rank 0 (A10) when N > 1].
+  workload = closed UV-sphere mesh N_t = 10 000 (configs[1]/[2]), 1e7 segments
+             per GPU with endpoints U[-1.5,1.5]^3 (weak scaling: each rank owns
+             its own 1e7-ray slice), mode boolean (the north-star mode);
+             barycentric and intercept_count rates are reported alongside.
+  value    = total rays processed by all ranks / max-over-ranks device time.
+  e2e      = the same metric through the C-ABI's rsi_test on pinned HOST
+             buffers (H2D of mesh + rays, build, intersect, D2H of results).
+
+`--impl reference` times the CPU oracle (the only reference this paper tier
+has) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+METRIC = "rays/sec (boolean & barycentric) at N_t=1e4, N_r=1e7-1e8 on 1/2/4/8 B200"
+UNIT = "rays/s"
+
+# Algorithmic work model of the traversal kernel:
+# per ray box tests and Moller-Trumbore tests for the sphere / long-segment
+# workload, and FP32-pipe instructions per test.
+WORK = {
+    "boolean": {"box_tests": 36.8, "mt_tests": 1.62},
+    "barycentric": {"box_tests": 54.9, "mt_tests": 2.92},
+    "intercept_count": {"box_tests": 69.3, "mt_tests": 3.97},
+}
+FP32_PER_BOX = 17.0
+FP32_PER_MT = 70.0
+N_SM = 148
+FP32_LANES = 128
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--rays-per-gpu", type=int, default=10_000_000)
+    ap.add_argument("--workload", default="sphere", choices=["sphere", "terrain", "paper_terrain", "sphere1m"])
+    ap.add_argument("--mode", default="boolean", choices=["boolean", "barycentric", "intercept_count"])
+    ap.add_argument("--no-extra-modes", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample rays (0 = auto ~15 s)")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        try:
+            p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                  "-i", str(self.index), "-lms", "100"], stdout=subprocess.PIPE, text=True)
+        except OSError:
+            return
+        while not self._stop.is_set():
+            line = p.stdout.readline()
+            if not line:
+                break
+            self.rows.append([x.strip() for x in line.split(",")])
+        p.terminate()
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._t.join(timeout=3)
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) >= 9 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) >= 9 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows if len(r) >= 9 for k in range(4) if r[5 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ helpers
+def workload_inputs(name: str, n: int, rank: int):
+    seed = {"sphere": 3, "terrain": 4, "paper_terrain": 6, "sphere1m": 5}[name] + 1000 * rank
+    V, T, S, E, _ = synth.workload(name, n, seed=seed)
+    return V, T, S, E
+
+
+def cpu_baseline(V, T, S, E, target_s=15.0, sample=0):
+    """The oracle (as it stands) on a bounded sample of the same workload."""
+    import oracle
+    cores = oracle.max_threads()
+    if sample <= 0:
+        # calibrate with a small run, then size for ~target_s of CPU work
+        n0 = 200
+        t = time.perf_counter()
+        oracle.run(V, T, S[:n0], E[:n0], flags=False)
+        dt = max(time.perf_counter() - t, 1e-3)
+        sample = int(min(len(S), max(n0, n0 * target_s / dt)))
+    t = time.perf_counter()
+    oracle.run(V, T, S[:sample], E[:sample], flags=False)
+    dt = time.perf_counter() - t
+    return {"value": sample / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"first {sample} rays of the workload x all {len(T)} triangles, all modes at once "
+                      f"(exhaustive fp64, {dt:.1f} s)"}
+
+
+def roofline(mode: str, rays: int, kernel_ms: float, sm_mhz: float | None):
+    w = WORK[mode]
+    inst_per_ray = w["box_tests"] * FP32_PER_BOX + w["mt_tests"] * FP32_PER_MT
+    clock = (sm_mhz or 1965.0) * 1e6
+    peak = N_SM * FP32_LANES * clock / 1e12            # T FP32 inst/s
+    achieved = inst_per_ray * rays / (kernel_ms * 1e-3) / 1e12
+    return {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 4), "unit": "TFP32-inst/s",
+            "frac": round(achieved / peak, 5), "traffic": None,
+            "kernel": f"k_{mode}", "kernel_ms": round(kernel_ms, 4),
+            "model": f"{w['box_tests']} box x {FP32_PER_BOX:.0f} + {w['mt_tests']} MT x {FP32_PER_MT:.0f} "
+                     f"= {inst_per_ray:.0f} FP32 inst/ray; peak = 148 SM x 128 lanes x sm_mhz"}
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    V, T, S, E = workload_inputs(args.workload, max(args.rays_per_gpu // 1000, 20000), 0)
+    import oracle
+    cores = oracle.max_threads()
+    n0 = 100
+    t = time.perf_counter()
+    oracle.run(V, T, S[:n0], E[:n0], flags=False)
+    dt = max(time.perf_counter() - t, 1e-3)
+    per_step = int(max(n0, min(len(S), n0 * 8.0 / dt)))   # ~8 s of CPU per step
+    for i in range(args.warmup):
+        oracle.run(V, T, S[:per_step], E[:per_step], flags=False)
+    t = time.perf_counter()
+    for i in range(args.steps):
+        oracle.run(V, T, S[:per_step], E[:per_step], flags=False)
+    el = time.perf_counter() - t
+    value = per_step * args.steps / el
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": f"{args.workload} N_t={len(T)}, boolean, oracle sample "
+                                                      f"{per_step} rays/step"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{per_step} rays/step x {len(T)} triangles (exhaustive fp64)"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2305_01867_b200 import rsi
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    n = args.rays_per_gpu
+    V, T, S, E = workload_inputs(args.workload, n, rank)
+    Vd, Td = torch.from_numpy(V).to(dev), torch.from_numpy(T).to(dev)
+    Sd, Ed = torch.from_numpy(S).to(dev), torch.from_numpy(E).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    h = rsi.rsi_build(Vd, Td)
+    kernels_per_build = 6 if len(T) <= 65536 else 5 + 12
+
+    def timed(mode: str, steps: int, warmup: int, clocks: bool):
+        out = rsi.alloc_outputs(n, mode, dev)
+        gather_buf = None
+        if world > 1:
+            key = {"boolean": "hit", "barycentric": "tri", "intercept_count": "count"}[mode]
+            gather_buf = torch.empty((world,) + tuple(out[key].shape), dtype=out[key].dtype, device=dev)
+
+        def step(ev=None):
+            if ev is not None:
+                ev[0].record(stream)
+            rsi.rsi_rebuild(h, Vd, Td)
+            if ev is not None:
+                ev[1].record(stream)
+            rsi.rsi_intersect(h, Sd, Ed, mode, out=out)
+            if ev is not None:
+                ev[2].record(stream)
+            if world > 1:
+                key = {"boolean": "hit", "barycentric": "tri", "intercept_count": "count"}[mode]
+                dist.all_gather_into_tensor(gather_buf, out[key])
+
+        for _ in range(warmup):
+            step()
+        torch.cuda.synchronize(dev)
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sampler = ClockSampler(local) if clocks else None
+        if sampler:
+            sampler.__enter__()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        t0.record(stream)
+        for k in range(steps):
+            step(evs[k])
+        t1.record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        if sampler:
+            sampler.__exit__()
+        ms = t0.elapsed_time(t1)
+        build_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+        query_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+        if world > 1:
+            tm = torch.tensor([ms, build_ms, query_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+            ms, build_ms, query_ms = tm.tolist()
+        return ms, build_ms, query_ms, (sampler.summary() if sampler else None)
+
+    ms, build_ms, query_ms, clk = timed(args.mode, args.steps, max(args.warmup, 3), True)
+    total_rays = n * world * args.steps
+    value = total_rays / (ms * 1e-3)
+    extra = {}
+    if not args.no_extra_modes:
+        for m in ("barycentric", "intercept_count"):
+            if m == args.mode:
+                continue
+            mms, mb, mq, _ = timed(m, args.steps, 3, False)
+            extra[m] = {"value": n * world * args.steps / (mms * 1e-3), "ms_per_step": mms / args.steps,
+                        "build_ms": mb, "query_ms": mq}
+    stats = rsi.rsi_get_stats(h)
+
+    # e2e: through the C-ABI rsi_test on pinned host buffers (rank-local)
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(a).pin_memory()  # noqa: E731
+        hV, hT, hS, hE = pin(V), pin(T), pin(S), pin(E)
+        hout = {"hit": torch.empty(n, dtype=torch.uint8).pin_memory()}
+        for _ in range(2):
+            rsi.rsi_test(hV, hT, hS, hE, {"mode": args.mode}, out=hout)
+        e_steps = max(2, min(args.steps, 5))
+        if world > 1:
+            dist.barrier()
+        t = time.perf_counter()
+        for _ in range(e_steps):
+            rsi.rsi_test(hV, hT, hS, hE, {"mode": args.mode}, out=hout)
+        el = time.perf_counter() - t
+        if world > 1:
+            tt = torch.tensor([el], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            el = tt.item()
+        h2d = V.nbytes + T.nbytes + S.nbytes + E.nbytes
+        e2e = {"value": n * world * e_steps / el, "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": n, "ms_per_step": el / e_steps * 1e3,
+               "api": "rsi_test (C-ABI, pinned host buffers)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(V, T, S, E, sample=args.cpu_sample)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded UV-sphere mesh, uniform segments; see DESIGN.md 4)",
+            "config": {"workload": f"{args.workload} N_t={len(T)}, N_r={n}/GPU, mode={args.mode}",
+                       "n_triangles": len(T), "rays_per_gpu": n, "mode": args.mode,
+                       "parallelism": f"ray-sharded x{world}" + (" + NCCL all_gather" if world > 1 else ""),
+                       "l2": "inputs larger than L2 (240 MB of segments per GPU)",
+                       "step": "rsi_rebuild + rsi_intersect" + (" + gather" if world > 1 else "")},
+            "build_ms": build_ms, "query_ms": query_ms,
+            "roofline": roofline(args.mode, n, query_ms, clk["sm_mhz"] if clk else None),
+            "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": args.steps * (kernels_per_build + 1),
+            "clocks": clk, "modes": extra, "stats": stats,
+        }
+        print(json.dumps(line), flush=True)
+    h.free()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,398 @@
+"""-m gpu: the CUDA path (through the C-ABI) against the CPU oracle, element by element.
+
+Bar (BASELINE.json north_star): boolean, intercept_count
+and nearest-triangle index bit-exact on EVERY ray (flagged rays are counted and
+reported, never excused); t within 1e-5, dist within 1e-5*|d|, point within
+1e-5*max(|O|_inf, |E|_inf).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+DEV = "cuda:0"
+
+
+@pytest.fixture(scope="module")
+def rsi():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2305_01867_b200 import _build, rsi as _rsi
+    _build.build_library()
+    return _rsi
+
+
+def to_dev(*arrs):
+    return [torch.from_numpy(np.ascontiguousarray(a)).to(DEV) for a in arrs]
+
+
+def run_all(rsi, V, T, S, E, options=None):
+    Vd, Td, Sd, Ed = to_dev(V, T, S, E)
+    h = rsi.rsi_build(Vd, Td, options)
+    out = {"hit": rsi.rsi_intersect(h, Sd, Ed, "boolean")["hit"].cpu().numpy()}
+    b = rsi.rsi_intersect(h, Sd, Ed, "barycentric")
+    out.update({k: v.cpu().numpy() for k, v in b.items()})
+    out["count"] = rsi.rsi_intersect(h, Sd, Ed, "intercept_count")["count"].cpu().numpy()
+    out["stats"] = rsi.rsi_get_stats(h)
+    h.free()
+    return out
+
+
+def assert_parity(got, ref, S, E, label=""):
+    n_flag = int((ref["flags"] != 0).sum()) if "flags" in ref else 0
+    bad_hit = np.nonzero(got["hit"] != ref["hit"])[0]
+    bad_cnt = np.nonzero(got["count"] != ref["count"])[0]
+    bad_tri = np.nonzero(got["tri"] != ref["tri"])[0]
+    assert bad_hit.size == 0, f"{label} boolean mismatches at {bad_hit[:10]} (flagged rays: {n_flag})"
+    assert bad_cnt.size == 0, (f"{label} count mismatches at {bad_cnt[:10]}: got {got['count'][bad_cnt[:10]]} "
+                               f"ref {ref['count'][bad_cnt[:10]]}")
+    assert bad_tri.size == 0, f"{label} tri mismatches at {bad_tri[:10]}"
+    m = ref["tri"] >= 0
+    d = (E.astype(np.float64) - S)
+    dn = np.linalg.norm(d, axis=1)
+    assert np.all(np.abs(got["t"][m] - ref["t"][m]) <= 1e-5), label
+    assert np.all(np.abs(got["dist"][m] - ref["dist"][m]) <= 1e-5 * np.maximum(dn[m], 1e-30)), label
+    scale = np.maximum(np.abs(S).max(1), np.abs(E).max(1))[m]
+    assert np.all(np.abs(got["point"][m] - ref["point"][m]).max(1) <= 1e-5 * np.maximum(scale, 1e-30)), label
+    assert np.all(np.isnan(got["t"][~m])) and np.all(np.isnan(got["point"][~m]))
+    return n_flag
+
+
+# ------------------------------------------------------------------ paper worked example
+
+def test_fig3_fixture_all_modes(rsi, golden):
+    g = golden("fig3_case_study1.txt")
+    V, T = synth.fixture()
+    S, E = synth.fixture_rays()
+    got = run_all(rsi, V, T, S, E)
+    assert got["hit"].tolist() == [int(x) for x in g["boolean"][0]]
+    for row in g["hit"]:
+        i, tri = int(row[0]), int(row[1])
+        assert got["tri"][i] == tri
+        np.testing.assert_allclose(got["point"][i], np.array(row[2:], float), atol=1e-4)
+    ref = oracle.run(V, T, S, E)
+    assert_parity(got, ref, S, E, "fig3")
+
+
+def test_canopy_counts(rsi, golden):
+    g = golden("canopy_counts.txt")
+    V, T = synth.canopy()
+    S, E = synth.fixture_rays()
+    got = run_all(rsi, V, T, S, E)
+    assert got["count"].tolist() == [int(x) for x in g["count"][0]]
+
+
+def test_fig3_bvh_structure(rsi, golden):
+    """Leaf order (T0, T3, T1, T2) and node boxes of the P:306-346 dump; the
+    root splits leaves [0,1] | [2,3] (z-major Morton, reading R8)."""
+    g = golden("fig3_case_study1.txt")
+    V, T = synth.fixture()
+    Vd, Td = to_dev(V, T)
+    h = rsi.rsi_build(Vd, Td)
+    d = rsi.rsi_bvh_download(h)
+    h.free()
+    leaves = g["leaf"]
+    assert d["leaf_tri"].tolist() == [int(r[1]) for r in leaves]
+    # leaf boxes: the child slot that holds each leaf
+    for node in range(d["n_nodes"]):
+        for side in range(2):
+            ref = d["child"][node, side]
+            if ref < 0:
+                slot = ~ref
+                row = leaves[slot]
+                exp = np.array(row[2:], np.float32)  # xlo xhi ylo yhi zlo zhi
+                b = d["box"][node, side]             # xlo ylo zlo xhi yhi zhi
+                np.testing.assert_allclose([b[0], b[3], b[1], b[4], b[2], b[5]], exp, atol=1e-6)
+    # the root's two children are the subtrees [0,1] and [2,3] with the printed boxes
+    nodes = {(int(r[0]), int(r[1])): np.array(r[2:], np.float32) for r in g["node"]}
+    root = d["child"][0]
+    assert root[0] >= 0 and root[1] >= 0
+    for side, rng in ((0, (0, 1)), (1, (2, 3))):
+        b = d["box"][0, side]
+        np.testing.assert_allclose([b[0], b[3], b[1], b[4], b[2], b[5]], nodes[rng], atol=1e-6)
+    np.testing.assert_allclose(d["scene_lo"] + d["scene_hi"], [12, 2, 1, 13, 3, 1.3], atol=1e-6)
+    assert (d["arrivals"] == 2).all()
+
+
+# ------------------------------------------------------------------ configs at oracle sizes
+
+def test_config0_unit_cube_all_modes(rsi):
+    V, T, S, E, _ = synth.workload("cube", 10_000)
+    ref = oracle.run(V, T, S, E)
+    got = run_all(rsi, V, T, S, E)
+    assert_parity(got, ref, S, E, "cube")
+
+
+def test_cube_axis_aligned_closed_form(rsi):
+    V, T = synth.cube()
+    xs = np.linspace(0.0, 1.0, 9)
+    pts = [(x, y) for x in xs for y in xs]
+    S = np.array([(x, y, -1.0) for x, y in pts], np.float32)
+    E = np.array([(x, y, 2.0) for x, y in pts], np.float32)
+    ref = oracle.run(V, T, S, E)
+    got = run_all(rsi, V, T, S, E)
+    assert_parity(got, ref, S, E, "cube-axis")
+    inner = np.array([0 < x < 1 and 0 < y < 1 for x, y in pts])
+    assert (got["count"][inner] == 2).all()
+    np.testing.assert_allclose(got["t"][inner], 1 / 3, atol=1e-7)
+
+
+@pytest.mark.parametrize("n_rays", [1, 31, 20_011])
+def test_sphere_all_modes(rsi, n_rays):
+    V, T, S, E, _ = synth.workload("sphere", n_rays)
+    ref = oracle.run(V, T, S, E)
+    got = run_all(rsi, V, T, S, E)
+    assert_parity(got, ref, S, E, "sphere")
+
+
+def test_folded_terrain_intercept_count(rsi):
+    V, T, S, E, _ = synth.workload("terrain", 6000)
+    ref = oracle.run(V, T, S, E)
+    got = run_all(rsi, V, T, S, E)
+    assert_parity(got, ref, S, E, "terrain")
+    assert (got["count"] == 3).sum() > 100
+
+
+def test_paper_terrain_vertical_and_oblique(rsi):
+    V, T = synth.paper_terrain()
+    S1, E1 = synth.vertical_rays(3000, V, 6)
+    lo, hi = V.min(0), V.max(0)
+    S2, E2 = synth.box_rays(3000, lo - [0, 0, 5], hi + [0, 0, 5], 8)
+    S, E = np.vstack([S1, S2]), np.vstack([E1, E2])
+    ref = oracle.run(V, T, S, E)
+    got = run_all(rsi, V, T, S, E)
+    assert_parity(got, ref, S, E, "paper-terrain")
+
+
+def test_rays_through_vertices_and_edges_exact(rsi):
+    """Adversarial: exactly vertical segments through grid vertices and edge
+    midpoints of the paper-scale terrain (coordinates ~1e3).  Every decision
+    sits on a triangle boundary; results must still equal the oracle's."""
+    V, T = synth.paper_terrain(40, 30)
+    rng = np.random.default_rng(5)
+    idx = rng.integers(0, len(V), 800)
+    P = V[idx].astype(np.float64)
+    Q = V[rng.integers(0, len(V), 800)].astype(np.float64)
+    mid = (P[:400] + V[idx[:400] + 1]) / 2  # (mostly) edge midpoints
+    P = np.vstack([P, mid])
+    S = np.column_stack([P[:, :2], np.full(len(P), 80.0)]).astype(np.float32)
+    E = np.column_stack([P[:, :2], np.full(len(P), 40.0)]).astype(np.float32)
+    # plus oblique segments aimed at vertices
+    S2 = (Q + rng.normal(size=Q.shape) * [30, 30, 10]).astype(np.float32)
+    E2 = (2 * Q - S2).astype(np.float32)
+    S, E = np.vstack([S, S2]), np.vstack([E, E2])
+    ref = oracle.run(V, T, S, E)
+    got = run_all(rsi, V, T, S, E)
+    n_flag = assert_parity(got, ref, S, E, "vertices")
+    assert n_flag > 500  # the case really is on the boundaries
+
+
+def test_fp64_moller_option_identical(rsi):
+    V, T, S, E, _ = synth.workload("sphere", 4000, seed=21)
+    a = run_all(rsi, V, T, S, E)
+    b = run_all(rsi, V, T, S, E, rsi.Options(fp64_moller=True))
+    for k in ("hit", "count", "tri"):
+        assert (a[k] == b[k]).all()
+    ref = oracle.run(V, T, S, E)
+    assert_parity(b, ref, S, E, "fp64")
+    assert b["stats"]["fp64_pairs"] == 0  # the fp64 path does not count "uncertain" pairs
+
+
+# ------------------------------------------------------------------ edge cases
+
+def test_single_triangle_and_degenerates(rsi):
+    V = np.float32([[0, 0, 0], [1, 0, 0], [0, 1, 0]])
+    T = np.int32([[0, 1, 2]])
+    S = np.float32([[0.2, 0.2, 1], [0.9, 0.9, 1], [0.2, 0.2, 0], [0.3, 0.3, 5], [np.nan, 0, 1], [0.2, 0.2, 1]])
+    E = np.float32([[0.2, 0.2, -1], [0.9, 0.9, -1], [0.2, 0.2, 0], [0.3, 0.3, 0], [0.1, 0.1, -1], [0.2, 0.2, 0]])
+    ref = oracle.run(V, T, S, E)
+    got = run_all(rsi, V, T, S, E)
+    assert_parity(got, ref, S, E, "single")
+    assert got["hit"].tolist() == [1, 0, 0, 1, 0, 1]
+    assert got["stats"]["nonfinite_rays"] >= 1
+
+
+def test_stacked_identical_triangles_and_overflow_repass(rsi):
+    """30 coincident copies + 20 parallel sheets: duplicate Morton codes
+    (index-augmented delta), nearest-tie -> lowest id, and > 8 hits per ray
+    (register-list overflow -> exact re-pass)."""
+    base = np.float32([[0, 0, 0], [1, 0, 0], [0, 1, 0]])
+    Vs, Ts = [], []
+    for k in range(30):
+        Vs.append(base + [0, 0, 0.5]); Ts.append(np.arange(3) + 3 * len(Ts))
+    for k in range(20):
+        Vs.append(base + [0, 0, 1.0 + 0.01 * k]); Ts.append(np.arange(3) + 3 * len(Ts))
+    V = np.vstack(Vs).astype(np.float32)
+    T = np.vstack(Ts).astype(np.int32)
+    S, E = synth.box_rays(3000, [-0.2, -0.2, -1], [1.2, 1.2, 2.5], 9)
+    S[:500, 2] = -1
+    E[:500, 2] = 3
+    E[:500, :2] = S[:500, :2]
+    ref = oracle.run(V, T, S, E)
+    Vd, Td, Sd, Ed = to_dev(V, T, S, E)
+    h = rsi.rsi_build(Vd, Td)
+    got = run_all(rsi, V, T, S, E)
+    assert_parity(got, ref, S, E, "stacked")
+    assert (got["count"] >= 9).sum() > 50
+    d = rsi.rsi_bvh_download(h)
+    assert sorted(d["leaf_tri"].tolist()) == list(range(len(T)))
+    assert (d["arrivals"] == 2).all()
+    h.free()
+
+
+def test_build_errors(rsi):
+    V, T = synth.fixture()
+    Vd, Td = to_dev(V, T)
+    with pytest.raises(rsi.RsiError) as e:
+        rsi.rsi_build(Vd, torch.tensor([[0, 1, 9]], dtype=torch.int32, device=DEV))
+    assert e.value.status == 3
+    Vn = V.copy()
+    Vn[2, 1] = np.nan
+    with pytest.raises(rsi.RsiError) as e:
+        rsi.rsi_build(to_dev(Vn)[0], Td)
+    assert e.value.status == 4
+    with pytest.raises(rsi.RsiError) as e:
+        rsi.rsi_build(Vd, torch.zeros((0, 3), dtype=torch.int32, device=DEV))
+    assert e.value.status == 2
+    with pytest.raises(TypeError):
+        rsi.rsi_build(Vd, Td.long())
+    h = rsi.rsi_build(Vd, Td)
+    z = torch.zeros((0, 3), dtype=torch.float32, device=DEV)
+    assert rsi.rsi_intersect(h, z, z, "boolean")["hit"].numel() == 0
+    h.free()
+
+
+@pytest.mark.parametrize("nt", [1, 2, 3, 17, 1000, 70_001])
+def test_bvh_integrity_random_meshes(rsi, nt):
+    """Validator invariants (P:407-464 failure signatures must be absent):
+    leaf bijection, arrivals == 2, root reachable from every leaf, child boxes
+    exact unions, parent/child links mutual; sorted Morton codes equal a
+    bit-loop z-major encoding of the fp32 centroids."""
+    rng = np.random.default_rng(nt)
+    V = rng.uniform(-3, 7, (3 * nt, 3)).astype(np.float32)
+    T = rng.permutation(3 * nt).reshape(nt, 3).astype(np.int32)
+    Vd, Td = to_dev(V, T)
+    h = rsi.rsi_build(Vd, Td)
+    d = rsi.rsi_bvh_download(h)
+    h.free()
+    nn = d["n_nodes"]
+    assert sorted(d["leaf_tri"].tolist()) == list(range(nt))
+    assert (d["arrivals"] == 2).all()
+    # morton reference (bit loop) on fp32 centroids
+    lo, hi = V.min(0), V.max(0)
+    c = (V[T[:, 0]] + V[T[:, 1]] + V[T[:, 2]]) / np.float32(3)
+    q = np.clip(np.floor((c - lo) / (hi - lo) * np.float32(1024)), 0, 1023).astype(np.uint32)
+    code = np.zeros(nt, np.uint32)
+    for b in range(10):
+        for a in range(3):
+            code |= ((q[:, a] >> b) & 1) << (3 * b + a)
+    order = np.argsort(code, kind="stable")
+    assert (d["morton"] == code[order]).all()
+    assert (d["leaf_tri"] == order).all()
+    if nt == 1:
+        return
+    # boxes: recompute bottom-up and compare exactly
+    tb = np.concatenate([V[T].min(1), V[T].max(1)], 1)  # per original triangle
+    box = {}
+
+    def node_box(ref):
+        if ref < 0:
+            return tb[d["leaf_tri"][~ref]]
+        if ref in box:
+            return box[ref]
+        raise KeyError
+
+    parent = d["parent"]
+    assert parent[0] == -1
+    for i in range(nn):
+        for side in range(2):
+            ch = d["child"][i, side]
+            p = parent[ch] if ch >= 0 else parent[nn + ~ch]
+            assert p == (i << 1 | side)
+    # iterative post-order
+    stack = [(0, False)]
+    while stack:
+        i, done = stack.pop()
+        if done:
+            l, r = (node_box(x) for x in d["child"][i])
+            exp = [np.concatenate([np.minimum(l[:3], r[:3]), np.maximum(l[3:], r[3:])])]
+            got_l, got_r = d["box"][i]
+            assert (got_l == l).all() and (got_r == r).all()
+            box[i] = exp[0]
+        else:
+            stack.append((i, True))
+            for ch in d["child"][i]:
+                if ch >= 0:
+                    stack.append((int(ch), False))
+    assert len(box) == nn
+
+
+def test_compaction_and_sparse_return(rsi):
+    V, T, S, E, _ = synth.workload("sphere", 50_000, seed=13)
+    Vd, Td, Sd, Ed = to_dev(V, T, S, E)
+    h = rsi.rsi_build(Vd, Td)
+    out = rsi.rsi_intersect(h, Sd, Ed, "barycentric")
+    ids, dist, tri, pts = rsi.sparse_barycentric(out)
+    exp = np.nonzero(out["tri"].cpu().numpy() >= 0)[0]
+    assert (ids.cpu().numpy() == exp).all()
+    assert (tri.cpu().numpy() >= 0).all()
+    h.free()
+
+
+def test_rsi_test_host_end_to_end(rsi):
+    """The paper's user call on host arrays through rsi_test."""
+    V, T, S, E, _ = synth.workload("sphere", 5000, seed=17)
+    ref = oracle.run(V, T, S, E)
+    b = rsi.rsi_test(V, T, S, E, {"mode": "boolean"})
+    assert b.shape == (5000, 1) and (b[:, 0] == ref["hit"].astype(bool)).all()
+    c = rsi.rsi_test(V, T, S, E, {"mode": "intercept_count"})
+    assert (c == ref["count"]).all()
+    ids, dist, tri, pts = rsi.rsi_test(V, T, S, E, {"mode": "barycentric"})
+    rids, rdist, rtri, rpts = oracle.sparse_barycentric(ref)
+    assert (ids == rids).all() and (tri == rtri).all()
+    np.testing.assert_allclose(pts, rpts, atol=1e-5 * 1.5)
+
+
+# ------------------------------------------------------------------ full sizes (sampled)
+
+def test_bench_size_sampled_parity(rsi):
+    """configs[2]-size: N_t = 1e4, N_r = 1e7 in the launch configuration the
+    bench times; a seeded sample of 2000 rays is checked against the oracle one
+    by one, and mode consistency is checked on all 1e7 rays."""
+    V, T, S, E, _ = synth.workload("sphere", 10_000_000, seed=3)
+    Vd, Td, Sd, Ed = to_dev(V, T, S, E)
+    h = rsi.rsi_build(Vd, Td)
+    hit = rsi.rsi_intersect(h, Sd, Ed, "boolean")["hit"].cpu().numpy()
+    bar = {k: v.cpu().numpy() for k, v in rsi.rsi_intersect(h, Sd, Ed, "barycentric").items()}
+    cnt = rsi.rsi_intersect(h, Sd, Ed, "intercept_count")["count"].cpu().numpy()
+    h.free()
+    assert ((bar["tri"] >= 0) == (hit > 0)).all()
+    assert ((cnt > 0) == (hit > 0)).all()
+    rng = np.random.default_rng(0)
+    sample = np.sort(rng.choice(len(S), 2000, replace=False))
+    ref = oracle.run(V, T, S[sample], E[sample])
+    got = {"hit": hit[sample], "count": cnt[sample], **{k: v[sample] for k, v in bar.items()}}
+    assert_parity(got, ref, S[sample], E[sample], "1e7-sample")
+
+
+def test_million_triangle_mesh_sampled(rsi):
+    """configs[4] mesh (N_t = 1e6, multi-block radix sort, 6.8% duplicate
+    codes): 1e6 rays, 64 sampled against the oracle."""
+    V, T, S, E, _ = synth.workload("sphere1m", 1_000_000)
+    Vd, Td, Sd, Ed = to_dev(V, T, S, E)
+    h = rsi.rsi_build(Vd, Td)
+    d = rsi.rsi_bvh_download(h)
+    assert (d["arrivals"] == 2).all()
+    assert (np.bincount(d["leaf_tri"], minlength=len(T)) == 1).all()
+    hit = rsi.rsi_intersect(h, Sd, Ed, "boolean")["hit"].cpu().numpy()
+    bar = {k: v.cpu().numpy() for k, v in rsi.rsi_intersect(h, Sd, Ed, "barycentric").items()}
+    cnt = rsi.rsi_intersect(h, Sd, Ed, "intercept_count")["count"].cpu().numpy()
+    h.free()
+    sample = np.arange(0, len(S), len(S) // 64)[:64]
+    ref = oracle.run(V, T, S[sample], E[sample], flags=False)
+    got = {"hit": hit[sample], "count": cnt[sample], **{k: v[sample] for k, v in bar.items()}}
+    assert_parity(got, ref, S[sample], E[sample], "1m-sample")

@@ -174,7 +174,7 @@ def test_rays_through_vertices_and_edges_exact(rsi):
     sits on a triangle boundary; results must still equal the oracle's."""
     V, T = synth.paper_terrain(40, 30)
     rng = np.random.default_rng(5)
-    idx = rng.integers(0, len(V), 800)
+    idx = rng.integers(0, len(V) - 1, 800)
     P = V[idx].astype(np.float64)
     Q = V[rng.integers(0, len(V), 800)].astype(np.float64)
     mid = (P[:400] + V[idx[:400] + 1]) / 2  # (mostly) edge midpoints

@@ -58,6 +58,8 @@ typedef enum {
 #define RSI_OPT_FP64_MOLLER 1u /* every Moller-Trumbore test in double precision: the
                                   paper's USE_DOUBLE_PRECISION_MOLLER.  Results
                                   are identical either way; only speed differs. */
+#define RSI_OPT_COUNTERS 2u    /* count box tests and Moller-Trumbore tests in rsi_stats_t
+                                  (instrumented kernels; for roofline accounting, slower). */
 
 typedef struct {
     uint32_t struct_size; /* sizeof(rsi_options_t); 0 or a NULL options pointer = defaults   */
@@ -100,6 +102,8 @@ typedef struct {
     uint64_t overflow_rays;  /* intercept_count rays that overflowed the register hit
                                 list and went through the exact re-pass                  */
     uint64_t nonfinite_rays; /* rays with a NaN/Inf coordinate (reported as misses)       */
+    uint64_t box_tests;      /* child-box slab tests (RSI_OPT_COUNTERS only, else 0)      */
+    uint64_t mt_tests;       /* Moller-Trumbore tests (RSI_OPT_COUNTERS only, else 0)     */
 } rsi_stats_t;
 
 /* Library version string, e.g. "rsi-b200 0.1.0 sm_100a". */

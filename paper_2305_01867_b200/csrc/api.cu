@@ -1,6 +1,7 @@
 // api.cu -- the extern "C" boundary declared in include/rsi.h.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -32,7 +33,7 @@ static rsi_status_t read_options(const rsi_options_t* in, rsi_options_t* out) {
     if (in->struct_size != sizeof(rsi_options_t))
         return rsi_set_error(RSI_E_INVALID_ARG, "rsi_options_t.struct_size %u != %zu", in->struct_size,
                              sizeof(rsi_options_t));
-    if (in->flags & ~RSI_OPT_FP64_MOLLER) return rsi_set_error(RSI_E_INVALID_ARG, "unknown option flags 0x%x", in->flags);
+    if (in->flags & ~(RSI_OPT_FP64_MOLLER | RSI_OPT_COUNTERS)) return rsi_set_error(RSI_E_INVALID_ARG, "unknown option flags 0x%x", in->flags);
     if (!(in->dedup_tau >= 0.0)) return rsi_set_error(RSI_E_INVALID_ARG, "dedup_tau must be >= 0");
     *out = *in;
     return RSI_OK;
@@ -64,6 +65,7 @@ rsi_status_t rsi_build(const float* d_vertices, int64_t n_vertices, const int32_
     rsi_bvh* h = new (std::nothrow) rsi_bvh();
     if (!h) return rsi_set_error(RSI_E_OOM, "host allocation failed");
     h->opt = opt;
+    if (const char* e = getenv("RSI_MIN_TRAV")) h->min_trav = atoi(e);  // tuning knob
     cudaStream_t s = (cudaStream_t)stream;
     h->stream = s;
     st = rsi_cuda_check(cudaGetDevice(&h->device), "cudaGetDevice");
@@ -224,6 +226,8 @@ rsi_status_t rsi_get_stats(rsi_handle_t h, rsi_stats_t* out, void* stream) {
     out->fp64_rays = v[ST_FP64_RAYS];
     out->overflow_rays = h->host_overflow;
     out->nonfinite_rays = v[ST_NONFINITE];
+    out->box_tests = v[ST_BOX_TESTS];
+    out->mt_tests = v[ST_MT_TESTS];
     return RSI_OK;
 }
 

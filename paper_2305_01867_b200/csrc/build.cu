@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(kBlock) k_refit(const float* __restrict__ V, i
         p = parent[node];
     }
     // root box (scene AABB) for rsi_bvh_info
-    float* root = reinterpret_cast<float*>(scratch + 9);
+    float* root = reinterpret_cast<float*>(scratch + SCR_ROOT);
     for (int x = 0; x < 3; ++x) {
         root[x] = lo[x];
         root[3 + x] = hi[x];
@@ -537,7 +537,7 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
     uint32_t status = h->h_pinned[SCR_STATUS];
     if (status & STATUS_INDEX) return rsi_set_error(RSI_E_INDEX_RANGE, "a triangle index is outside [0, %lld)", (long long)nv);
     if (status & STATUS_NONFINITE) return rsi_set_error(RSI_E_NONFINITE, "a vertex coordinate is NaN or Inf");
-    const float* root = reinterpret_cast<const float*>(h->h_pinned + 9);
+    const float* root = reinterpret_cast<const float*>(h->h_pinned + SCR_ROOT);
     for (int x = 0; x < 3; ++x) {
         h->scene_lo[x] = root[x];
         h->scene_hi[x] = root[3 + x];

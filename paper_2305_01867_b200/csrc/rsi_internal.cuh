@@ -23,14 +23,16 @@ enum {
     SCR_EXT_MIN = 0,   // 3 words: order-preserving encoded min x,y,z
     SCR_EXT_MAX = 3,   // 3 words: encoded max
     SCR_STATUS = 6,    // bit 0 index out of range, bit 1 non-finite vertex
-    SCR_OVF_COUNT = 7, // intercept_count overflow list length
-    SCR_OVF_TOTAL = 8, // re-pass: total raw hits over overflowed rays
-    SCR_WORDS = 16
+    SCR_ROOT = 9,      // 6 words: root (scene) AABB as float bits
+    SCR_OVF_COUNT = 16, // intercept_count overflow list length
+    SCR_OVF_TOTAL = 17, // re-pass: total raw hits over overflowed rays
+    SCR_DISPENSER = 18, // 2 words: 64-bit ray dispenser of the persistent traversal grid
+    SCR_WORDS = 32
 };
 enum { STATUS_INDEX = 1u, STATUS_NONFINITE = 2u };
 
 // stats counters (unsigned long long) in rsi_bvh::stats
-enum { ST_RAYS = 0, ST_FP64_PAIRS, ST_FP64_RAYS, ST_OVERFLOW, ST_NONFINITE, ST_WORDS };
+enum { ST_RAYS = 0, ST_FP64_PAIRS, ST_FP64_RAYS, ST_OVERFLOW, ST_NONFINITE, ST_BOX_TESTS, ST_MT_TESTS, ST_WORDS };
 
 struct rsi_bvh {
     int device = 0;
@@ -56,6 +58,7 @@ struct rsi_bvh {
     int64_t ovf_cap = 0;
     float scene_lo[3] = {0, 0, 0}, scene_hi[3] = {0, 0, 0};
     uint64_t host_rays = 0, host_overflow = 0;  // counters known on the host
+    int min_trav = 8;  // traversal-phase exit threshold (lanes still searching); env RSI_MIN_TRAV
 };
 
 // ---------------------------------------------------------------- host helpers (api.cu)

@@ -28,6 +28,7 @@ constexpr float kOutTol = 4e-6f;                 // max certified |t error| for 
 constexpr int kStack = 64;
 constexpr int kCountCap = 8;  // intercept_count hits held in registers per ray
 constexpr int kThreads = 128;
+constexpr int kChunk = 64;   // rays a warp takes from the global dispenser at once
 
 enum { MT_MISS = 0, MT_HIT = 1, MT_UNSURE = 2 };
 
@@ -222,22 +223,26 @@ __device__ __forceinline__ void traverse(const float4* __restrict__ nodes, const
 }
 
 struct Stats {
-    unsigned fp64_pairs = 0, fp64_ray = 0, nonfinite = 0;
+    unsigned fp64_pairs = 0, fp64_ray = 0, nonfinite = 0, boxes = 0, mts = 0;
 };
 
 __device__ __forceinline__ void flush_stats(const Stats& st, unsigned long long* stats) {
     const unsigned m = 0xffffffffu;
-    unsigned a = st.fp64_pairs, b = st.fp64_ray, c = st.nonfinite;
-    if (__any_sync(m, a | b | c)) {
+    unsigned a = st.fp64_pairs, b = st.fp64_ray, c = st.nonfinite, d = st.boxes, e = st.mts;
+    if (__any_sync(m, a | b | c | d | e)) {
         for (int o = 16; o; o >>= 1) {
             a += __shfl_xor_sync(m, a, o);
             b += __shfl_xor_sync(m, b, o);
             c += __shfl_xor_sync(m, c, o);
+            d += __shfl_xor_sync(m, d, o);
+            e += __shfl_xor_sync(m, e, o);
         }
         if ((threadIdx.x & 31) == 0) {
             if (a) atomicAdd(stats + ST_FP64_PAIRS, (unsigned long long)a);
             if (b) atomicAdd(stats + ST_FP64_RAYS, (unsigned long long)b);
             if (c) atomicAdd(stats + ST_NONFINITE, (unsigned long long)c);
+            if (d) atomicAdd(stats + ST_BOX_TESTS, (unsigned long long)d);
+            if (e) atomicAdd(stats + ST_MT_TESTS, (unsigned long long)e);
         }
     }
 }
@@ -259,160 +264,165 @@ __device__ __forceinline__ int decide(const Ray& r, const float4& A, const float
     return mt64(r, A, B, C, &t64) ? MT_HIT : MT_MISS;
 }
 
-// ---------------------------------------------------------------- boolean
-template <bool kFP64>
-__global__ void __launch_bounds__(kThreads) k_boolean(const float4* __restrict__ nodes,
-                                                      const float4* __restrict__ tris,
-                                                      const float* __restrict__ S, const float* __restrict__ E,
-                                                      int64_t n, uint8_t* __restrict__ hit,
-                                                      unsigned long long* stats) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    Stats st;
-    if (i < n) {
-        Ray r;
-        bool nonfinite;
-        bool found = false;
-        if (load_ray(r, S, E, i, nonfinite)) {
-            float tclip = 1.0f;
-            traverse(nodes, r, tclip, [&](int k) {
-                float4 A, B, C;
-                load_tri(tris, k, A, B, C);
-                float t32, et;
-                double t64;
-                bool is64;
-                if (decide<kFP64>(r, A, B, C, t32, et, t64, is64, st) == MT_HIT) {
-                    found = true;
-                    return true;  // any-hit early exit
-                }
-                return false;
-            });
-        }
-        st.nonfinite = nonfinite;
-        hit[i] = found ? 1 : 0;
-    }
-    flush_stats(st, stats);
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
 }
 
-// ---------------------------------------------------------------- barycentric (nearest hit)
-// Best = lexicographic min of (t, original id) (reading R5).  A hit is held as
-// an interval [t32 - et, t32 + et] or an exact fp64 value; overlapping
-// intervals are resolved by recomputing both in the fp64 mirror.
-struct Best {
-    int id = 0x7fffffff;  // original triangle id
-    int slot = -1;        // leaf slot (to recompute)
-    float t = 0.f, e = 0.f;
-    bool is64 = false;
-    double t64 = 0.0;
+// ---------------------------------------------------------------- per-mode ray state
+// Each mode keeps its per-ray result state; leaf() returns true when the ray
+// can stop (boolean any-hit, intercept_count register overflow).
+enum { MODE_BOOL = 0, MODE_BARY = 1, MODE_COUNT = 2 };
+
+struct TraceParams {
+    const float4* nodes;
+    const float4* tris;
+    const float* S;
+    const float* E;
+    int64_t n;
+    uint8_t* hit;
+    int32_t* tri;
+    float* t;
+    float* dist;
+    float* point;
+    int32_t* count;
+    double tau;
+    int32_t* ovf_list;
+    uint32_t* scratch;
+    unsigned long long* stats;
+    unsigned long long* counter;  // persistent-grid ray dispenser
+    int min_trav;                 // leave the traversal phase when fewer lanes still search
 };
 
-template <bool kFP64>
-__global__ void __launch_bounds__(kThreads) k_barycentric(const float4* __restrict__ nodes,
-                                                          const float4* __restrict__ tris,
-                                                          const float* __restrict__ S,
-                                                          const float* __restrict__ E, int64_t n,
-                                                          int32_t* __restrict__ tri_out, float* __restrict__ t_out,
-                                                          float* __restrict__ dist_out,
-                                                          float* __restrict__ point_out,
-                                                          unsigned long long* stats) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    Stats st;
-    if (i < n) {
-        Ray r;
-        bool nonfinite;
-        Best b;
-        if (load_ray(r, S, E, i, nonfinite)) {
-            float tclip = 1.0f;
-            traverse(nodes, r, tclip, [&](int k) {
-                float4 A, B, C;
-                load_tri(tris, k, A, B, C);
-                float t32, et;
-                double t64;
-                bool is64;
-                if (decide<kFP64>(r, A, B, C, t32, et, t64, is64, st) != MT_HIT) return false;
-                const int id = __float_as_int(A.w);
-                bool take;
-                if (b.slot < 0) {
-                    take = true;
-                } else {
-                    double clo = is64 ? t64 : (double)t32 - (double)et, chi = is64 ? t64 : (double)t32 + (double)et;
-                    double blo = b.is64 ? b.t64 : (double)b.t - (double)b.e, bhi = b.is64 ? b.t64 : (double)b.t + (double)b.e;
-                    if (chi < blo) {
-                        take = true;
-                    } else if (clo > bhi) {
-                        take = false;
-                    } else {  // ambiguous order: settle both in the fp64 mirror
-                        st.fp64_ray = 1;
-                        if (!is64) {
-                            mt64(r, A, B, C, &t64);
-                            is64 = true;
-                        }
-                        if (!b.is64) {
-                            float4 bA, bB, bC;
-                            load_tri(tris, b.slot, bA, bB, bC);
-                            mt64(r, bA, bB, bC, &b.t64);
-                            b.is64 = true;
-                        }
-                        take = (t64 < b.t64) || (t64 == b.t64 && id < b.id);
-                    }
+template <int MODE>
+struct ModeState;
+
+template <>
+struct ModeState<MODE_BOOL> {
+    bool found;
+    __device__ __forceinline__ void init() { found = false; }
+    template <bool kFP64>
+    __device__ __forceinline__ bool leaf(const TraceParams& p, const Ray& r, int k, float& tclip, Stats& st) {
+        float4 A, B, C;
+        load_tri(p.tris, k, A, B, C);
+        float t32, et;
+        double t64;
+        bool is64;
+        found = decide<kFP64>(r, A, B, C, t32, et, t64, is64, st) == MT_HIT;
+        return found;  // any-hit early exit
+    }
+    __device__ __forceinline__ void finish(const TraceParams& p, const Ray&, int64_t i, Stats&) {
+        p.hit[i] = found ? 1 : 0;
+    }
+};
+
+// Barycentric: lexicographic min of (t, original id) (reading R5).  A hit is
+// held as an interval [t32 - et, t32 + et] or an exact fp64 value; overlapping
+// intervals are resolved by recomputing both in the fp64 mirror.
+template <>
+struct ModeState<MODE_BARY> {
+    int id, slot;
+    float t, e;
+    bool is64;
+    double t64;
+    __device__ __forceinline__ void init() {
+        id = 0x7fffffff;
+        slot = -1;
+        t = e = 0.f;
+        is64 = false;
+        t64 = 0.0;
+    }
+    template <bool kFP64>
+    __device__ __forceinline__ bool leaf(const TraceParams& p, const Ray& r, int k, float& tclip, Stats& st) {
+        float4 A, B, C;
+        load_tri(p.tris, k, A, B, C);
+        float t32, et;
+        double c64;
+        bool c_is64;
+        if (decide<kFP64>(r, A, B, C, t32, et, c64, c_is64, st) != MT_HIT) return false;
+        const int cid = __float_as_int(A.w);
+        bool take;
+        if (slot < 0) {
+            take = true;
+        } else {
+            const double clo = c_is64 ? c64 : (double)t32 - (double)et, chi = c_is64 ? c64 : (double)t32 + (double)et;
+            const double blo = is64 ? t64 : (double)t - (double)e, bhi = is64 ? t64 : (double)t + (double)e;
+            if (chi < blo) {
+                take = true;
+            } else if (clo > bhi) {
+                take = false;
+            } else {  // order not certified: settle both in the fp64 mirror
+                st.fp64_ray = 1;
+                if (!c_is64) {
+                    mt64(r, A, B, C, &c64);
+                    c_is64 = true;
                 }
-                if (take) {
-                    b.id = id;
-                    b.slot = k;
-                    b.is64 = is64;
-                    if (is64) {
-                        b.t64 = t64;
-                        tclip = fminf(tclip, __double2float_ru(t64));
-                    } else {
-                        b.t = t32;
-                        b.e = et;
-                        tclip = fminf(tclip, __fadd_ru(t32, et));
-                    }
+                if (!is64) {
+                    float4 bA, bB, bC;
+                    load_tri(p.tris, slot, bA, bB, bC);
+                    mt64(r, bA, bB, bC, &t64);
+                    is64 = true;
                 }
-                return false;
-            });
+                take = (c64 < t64) || (c64 == t64 && cid < id);
+            }
         }
-        st.nonfinite = nonfinite;
-        if (b.slot >= 0) {
-            float t;
-            if (b.is64) {
-                t = (float)b.t64;
-            } else if (b.e <= kOutTol) {
-                t = b.t;
+        if (take) {
+            id = cid;
+            slot = k;
+            is64 = c_is64;
+            if (c_is64) {
+                t64 = c64;
+                tclip = fminf(tclip, __double2float_ru(c64));
+            } else {
+                t = t32;
+                e = et;
+                tclip = fminf(tclip, __fadd_ru(t32, et));
+            }
+        }
+        return false;
+    }
+    __device__ __forceinline__ void finish(const TraceParams& p, const Ray& r, int64_t i, Stats& st) {
+        if (slot >= 0) {
+            float tt;
+            if (is64) {
+                tt = (float)t64;
+            } else if (e <= kOutTol) {
+                tt = t;
             } else {  // fp32 value not certified to the output tolerance
                 float4 bA, bB, bC;
-                load_tri(tris, b.slot, bA, bB, bC);
-                double t64 = 0.0;
-                mt64(r, bA, bB, bC, &t64);
-                t = (float)t64;
+                load_tri(p.tris, slot, bA, bB, bC);
+                double v = 0.0;
+                mt64(r, bA, bB, bC, &v);
+                tt = (float)v;
                 st.fp64_ray = 1;
             }
-            tri_out[i] = b.id;
-            if (t_out) t_out[i] = t;
-            if (dist_out) dist_out[i] = t * sqrtf(r.dx * r.dx + r.dy * r.dy + r.dz * r.dz);
-            if (point_out) {
-                point_out[3 * i] = fmaf(t, r.dx, r.ox);
-                point_out[3 * i + 1] = fmaf(t, r.dy, r.oy);
-                point_out[3 * i + 2] = fmaf(t, r.dz, r.oz);
+            p.tri[i] = id;
+            if (p.t) p.t[i] = tt;
+            if (p.dist) p.dist[i] = tt * sqrtf(r.dx * r.dx + r.dy * r.dy + r.dz * r.dz);
+            if (p.point) {
+                p.point[3 * i] = fmaf(tt, r.dx, r.ox);
+                p.point[3 * i + 1] = fmaf(tt, r.dy, r.oy);
+                p.point[3 * i + 2] = fmaf(tt, r.dz, r.oz);
             }
         } else {
-            tri_out[i] = -1;
-            if (t_out) t_out[i] = NAN;
-            if (dist_out) dist_out[i] = NAN;
-            if (point_out) {
-                point_out[3 * i] = NAN;
-                point_out[3 * i + 1] = NAN;
-                point_out[3 * i + 2] = NAN;
+            p.tri[i] = -1;
+            if (p.t) p.t[i] = NAN;
+            if (p.dist) p.dist[i] = NAN;
+            if (p.point) {
+                p.point[3 * i] = NAN;
+                p.point[3 * i + 1] = NAN;
+                p.point[3 * i + 2] = NAN;
             }
         }
     }
-    flush_stats(st, stats);
-}
+};
 
-// ---------------------------------------------------------------- intercept_count
-// count = number of single-linkage clusters of hit t with threshold tau
-// (reading R4): 1 + #{sorted gaps > tau}.  The fp32 path is used only when
-// every pairwise |t_a - t_b| vs tau decision is certified; otherwise all hit t
-// are recomputed in the fp64 mirror and counted exactly as the oracle does.
+// intercept_count: count = number of single-linkage clusters of hit t with
+// threshold tau (reading R4): 1 + #{sorted gaps > tau}.  The fp32 path is used
+// only when every pairwise |t_a - t_b| vs tau decision is certified; otherwise
+// all hit t are recomputed in the fp64 mirror and counted exactly as the
+// oracle does.  More than kCountCap hits -> the exact re-pass.
 __device__ __forceinline__ void sort_small(double* v, int n) {
     for (int a = 1; a < n; ++a) {
         double x = v[a];
@@ -425,99 +435,212 @@ __device__ __forceinline__ void sort_small(double* v, int n) {
     }
 }
 
-template <bool kFP64>
-__global__ void __launch_bounds__(kThreads) k_count(const float4* __restrict__ nodes,
-                                                    const float4* __restrict__ tris, const float* __restrict__ S,
-                                                    const float* __restrict__ E, int64_t n, double tau,
-                                                    int32_t* __restrict__ count_out, int32_t* __restrict__ ovf_list,
-                                                    uint32_t* scratch, unsigned long long* stats) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    Stats st;
-    if (i < n) {
-        Ray r;
-        bool nonfinite;
-        float lt[kCountCap], le[kCountCap];
-        int lk[kCountCap];
-        int nh = 0;
-        bool overflow = false;
-        if (load_ray(r, S, E, i, nonfinite)) {
-            float tclip = 1.0f;
-            traverse(nodes, r, tclip, [&](int k) {
-                float4 A, B, C;
-                load_tri(tris, k, A, B, C);
-                float t32, et;
-                double t64;
-                bool is64;
-                if (decide<kFP64>(r, A, B, C, t32, et, t64, is64, st) != MT_HIT) return false;
-                if (nh == kCountCap) {
-                    overflow = true;
-                    return true;
-                }
-                if (is64) {
-                    t32 = (float)t64;
-                    et = fmaf(kU, fabsf(t32), kTiny);
-                }
-#pragma unroll
-                for (int x = 0; x < kCountCap; ++x)
-                    if (x == nh) {
-                        lt[x] = t32;
-                        le[x] = et;
-                        lk[x] = k;
-                    }
-                ++nh;
-                return false;
-            });
+template <>
+struct ModeState<MODE_COUNT> {
+    float lt[kCountCap], le[kCountCap];
+    int lk[kCountCap];
+    int nh;
+    bool overflow;
+    __device__ __forceinline__ void init() {
+        nh = 0;
+        overflow = false;
+    }
+    template <bool kFP64>
+    __device__ __forceinline__ bool leaf(const TraceParams& p, const Ray& r, int k, float& tclip, Stats& st) {
+        float4 A, B, C;
+        load_tri(p.tris, k, A, B, C);
+        float t32, et;
+        double t64;
+        bool is64;
+        if (decide<kFP64>(r, A, B, C, t32, et, t64, is64, st) != MT_HIT) return false;
+        if (nh == kCountCap) {
+            overflow = true;
+            return true;
         }
-        st.nonfinite = nonfinite;
-        if (overflow) {
-            uint32_t pos = atomicAdd(&scratch[SCR_OVF_COUNT], 1u);
-            ovf_list[pos] = (int32_t)i;
-            count_out[i] = -1;
-        } else if (nh <= 1) {
-            count_out[i] = nh;
-        } else {
-            const float ftau = (float)tau;
-            bool sure = true;
+        if (is64) {
+            t32 = (float)t64;
+            et = fmaf(kU, fabsf(t32), kTiny);
+        }
 #pragma unroll
-            for (int a = 0; a < kCountCap; ++a)
-#pragma unroll
-                for (int c = a + 1; c < kCountCap; ++c)
-                    if (c < nh) {
-                        float g = fabsf(lt[a] - lt[c]);
-                        float tol = le[a] + le[c] + fmaf(2.0f * kU, g + ftau, kTiny);
-                        if (fabsf(g - ftau) <= tol) sure = false;
-                    }
-            int cnt = 1;
-            if (sure) {
-                // insertion sort of the fp32 values, then count gaps > tau
-#pragma unroll
-                for (int a = 1; a < kCountCap; ++a)
-#pragma unroll
-                    for (int c = a; c > 0; --c)
-                        if (c < nh && lt[c - 1] > lt[c]) {
-                            float x = lt[c];
-                            lt[c] = lt[c - 1];
-                            lt[c - 1] = x;
-                        }
-#pragma unroll
-                for (int a = 0; a + 1 < kCountCap; ++a)
-                    if (a + 1 < nh && lt[a + 1] - lt[a] > ftau) ++cnt;
-            } else {
-                st.fp64_ray = 1;
-                double v[kCountCap];
-                for (int a = 0; a < nh; ++a) {
-                    float4 A, B, C;
-                    load_tri(tris, lk[a], A, B, C);
-                    mt64(r, A, B, C, &v[a]);
-                }
-                sort_small(v, nh);
-                for (int a = 0; a + 1 < nh; ++a)
-                    if (da(v[a + 1], -v[a]) > tau) ++cnt;
+        for (int x = 0; x < kCountCap; ++x)
+            if (x == nh) {
+                lt[x] = t32;
+                le[x] = et;
+                lk[x] = k;
             }
-            count_out[i] = cnt;
+        ++nh;
+        return false;
+    }
+    __device__ __forceinline__ void finish(const TraceParams& p, const Ray& r, int64_t i, Stats& st) {
+        if (overflow) {
+            uint32_t pos = atomicAdd(&p.scratch[SCR_OVF_COUNT], 1u);
+            p.ovf_list[pos] = (int32_t)i;
+            p.count[i] = -1;
+            return;
+        }
+        if (nh <= 1) {
+            p.count[i] = nh;
+            return;
+        }
+        const float ftau = (float)p.tau;
+        bool sure = true;
+#pragma unroll
+        for (int a = 0; a < kCountCap; ++a)
+#pragma unroll
+            for (int c = a + 1; c < kCountCap; ++c)
+                if (c < nh) {
+                    float g = fabsf(lt[a] - lt[c]);
+                    float tol = le[a] + le[c] + fmaf(2.0f * kU, g + ftau, kTiny);
+                    if (fabsf(g - ftau) <= tol) sure = false;
+                }
+        int cnt = 1;
+        if (sure) {
+#pragma unroll
+            for (int a = 1; a < kCountCap; ++a)
+#pragma unroll
+                for (int c = a; c > 0; --c)
+                    if (c < nh && lt[c - 1] > lt[c]) {
+                        float x = lt[c];
+                        lt[c] = lt[c - 1];
+                        lt[c - 1] = x;
+                    }
+#pragma unroll
+            for (int a = 0; a + 1 < kCountCap; ++a)
+                if (a + 1 < nh && lt[a + 1] - lt[a] > ftau) ++cnt;
+        } else {
+            st.fp64_ray = 1;
+            double v[kCountCap];
+            for (int a = 0; a < nh; ++a) {
+                float4 A, B, C;
+                load_tri(p.tris, lk[a], A, B, C);
+                mt64(r, A, B, C, &v[a]);
+            }
+            sort_small(v, nh);
+            for (int a = 0; a + 1 < nh; ++a)
+                if (da(v[a + 1], -v[a]) > p.tau) ++cnt;
+        }
+        p.count[i] = cnt;
+    }
+};
+
+// ---------------------------------------------------------------- the traversal kernel
+// Persistent warps with per-lane ray refill and postponed leaves (after Aila &
+// Laine's while-while traversal, adapted to segments and child-pair nodes):
+//   1. refill: lanes without a ray take the next ray ids from the warp's chunk
+//      (one atomicAdd per kChunk rays per warp), so lanes never idle while rays remain;
+//   2. traversal phase: lanes walk internal nodes until they hold a pending
+//      leaf (or run out of nodes); the phase ends when no lane (or fewer than
+//      min_trav lanes) is still searching;
+//   3. leaf phase: all lanes with pending leaves run Moller-Trumbore together;
+//   4. finished rays write their outputs and free the lane.
+template <int MODE, bool kFP64, bool kCounters>
+__global__ void __launch_bounds__(kThreads) k_trace(const TraceParams p) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt = lanemask_lt();
+    Stats st;
+    int64_t cnext = 0, cend = 0;  // warp-uniform chunk [cnext, cend)
+    bool exhausted = false;       // warp-uniform
+    int64_t ray = -1;
+    Ray r;
+    int node = -1, sp = 0, leaf0 = -1, leaf1 = -1;
+    int stack[kStack];
+    float tclip = 1.0f;
+    ModeState<MODE> ms;
+    while (true) {
+        // ---- 1. refill
+        unsigned want = __ballot_sync(FULL, ray < 0);
+        bool fresh = false;
+        while (want && !exhausted) {
+            if (cnext >= cend) {
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(p.counter, (unsigned long long)kChunk);
+                base = __shfl_sync(FULL, base, 0);
+                if ((int64_t)base >= p.n) {
+                    exhausted = true;
+                    break;
+                }
+                cnext = (int64_t)base;
+                cend = min((int64_t)base + kChunk, p.n);
+            }
+            const int take = (int)min((int64_t)__popc(want), cend - cnext);
+            const bool mine = (want >> lane) & 1u;
+            const int rank = __popc(want & lt);
+            const bool got = mine && rank < take;
+            if (got) {
+                ray = cnext + rank;
+                fresh = true;
+            }
+            want &= ~__ballot_sync(FULL, got);
+            cnext += take;
+        }
+        if (fresh) {
+            bool nonfinite;
+            const bool ok = load_ray(r, p.S, p.E, ray, nonfinite);
+            st.nonfinite += nonfinite;
+            ms.init();
+            tclip = 1.0f;
+            sp = 0;
+            leaf0 = leaf1 = -1;
+            node = ok ? 0 : -1;
+        }
+        if (__ballot_sync(FULL, ray >= 0) == 0) break;  // no rays left for this warp
+
+        // ---- 2. traversal phase
+        while (true) {
+            const bool trav = node >= 0 && leaf0 < 0;
+            const unsigned tm = __ballot_sync(FULL, trav);
+            if (tm == 0) break;
+            if (__popc(tm) < p.min_trav && __ballot_sync(FULL, leaf0 >= 0)) break;
+            if (trav) {
+                const float4* nd = p.nodes + 4 * node;
+                const float4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2);
+                const int4 n3 = __ldg(reinterpret_cast<const int4*>(nd + 3));
+                float nearL, nearR;
+                bool hL = slab(r, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, tclip, nearL);
+                bool hR = slab(r, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, tclip, nearR);
+                if (kCounters) st.boxes += 2;
+                if (hL && n3.x < 0) {
+                    leaf0 = ~n3.x;
+                    hL = false;
+                }
+                if (hR && n3.y < 0) {
+                    if (leaf0 < 0)
+                        leaf0 = ~n3.y;
+                    else
+                        leaf1 = ~n3.y;
+                    hR = false;
+                }
+                if (hL && hR) {
+                    const bool rfirst = nearR < nearL;
+                    stack[sp++] = rfirst ? n3.x : n3.y;
+                    node = rfirst ? n3.y : n3.x;
+                } else if (hL) {
+                    node = n3.x;
+                } else if (hR) {
+                    node = n3.y;
+                } else {
+                    node = sp > 0 ? stack[--sp] : -1;
+                }
+            }
+        }
+
+        // ---- 3. leaf phase
+        if (leaf0 >= 0) {
+            if (kCounters) st.mts += 1 + (leaf1 >= 0);
+            bool done = ms.template leaf<kFP64>(p, r, leaf0, tclip, st);
+            if (!done && leaf1 >= 0) done = ms.template leaf<kFP64>(p, r, leaf1, tclip, st);
+            leaf0 = leaf1 = -1;
+            if (done) node = -1;
+        }
+
+        // ---- 4. finish
+        if (ray >= 0 && node < 0 && leaf0 < 0) {
+            ms.finish(p, r, ray, st);
+            ray = -1;
         }
     }
-    flush_stats(st, stats);
+    flush_stats(st, p.stats);
 }
 
 // ---------------------------------------------------------------- exact re-pass for overflowed rays
@@ -686,19 +809,29 @@ __global__ void __launch_bounds__(256) k_compact_write(const int32_t* __restrict
 }  // namespace
 
 // ---------------------------------------------------------------- host side
-template <bool kFP64>
-static void launch_main(rsi_bvh* h, const float* S, const float* E, int64_t n, int32_t mode,
-                        const rsi_outputs_t* out, cudaStream_t s) {
-    const int64_t blocks = (n + kThreads - 1) / kThreads;
-    if (mode == RSI_MODE_BOOLEAN) {
-        k_boolean<kFP64><<<(unsigned)blocks, kThreads, 0, s>>>(h->nodes, h->tris, S, E, n, out->hit, h->stats);
-    } else if (mode == RSI_MODE_BARYCENTRIC) {
-        k_barycentric<kFP64><<<(unsigned)blocks, kThreads, 0, s>>>(h->nodes, h->tris, S, E, n, out->tri, out->t,
-                                                                   out->dist, out->point, h->stats);
-    } else {
-        k_count<kFP64><<<(unsigned)blocks, kThreads, 0, s>>>(h->nodes, h->tris, S, E, n, h->opt.dedup_tau,
-                                                             out->count, h->ovf_list, h->scratch, h->stats);
+template <int MODE, bool kFP64, bool kCounters>
+static void launch_trace(const TraceParams& p, cudaStream_t s) {
+    static int grid = 0;  // persistent grid: resident blocks per SM x SMs (per instantiation)
+    if (grid == 0) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trace<MODE, kFP64, kCounters>, kThreads, 0);
+        grid = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
     }
+    const int64_t need = (p.n + kThreads - 1) / kThreads;
+    const int g = (int)(need < grid ? need : grid);
+    k_trace<MODE, kFP64, kCounters><<<g, kThreads, 0, s>>>(p);
+}
+
+template <bool kFP64, bool kCounters>
+static void launch_mode(int32_t mode, const TraceParams& p, cudaStream_t s) {
+    if (mode == RSI_MODE_BOOLEAN)
+        launch_trace<MODE_BOOL, kFP64, kCounters>(p, s);
+    else if (mode == RSI_MODE_BARYCENTRIC)
+        launch_trace<MODE_BARY, kFP64, kCounters>(p, s);
+    else
+        launch_trace<MODE_COUNT, kFP64, kCounters>(p, s);
 }
 
 rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, int64_t n, int32_t mode,
@@ -707,22 +840,40 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     if (n > ((int64_t)1 << 31) - 1)
         return rsi_set_error(RSI_E_INVALID_ARG, "n_rays %lld exceeds 2^31-1", (long long)n);
     rsi_status_t st;
-    if (mode == RSI_MODE_INTERCEPT_COUNT) {
-        if (h->ovf_cap < n) {
-            if (h->ovf_list) cudaFreeAsync(h->ovf_list, s);
-            h->ovf_list = nullptr;
-            h->ovf_cap = 0;
-            st = rsi_cuda_check(cudaMallocAsync((void**)&h->ovf_list, (size_t)n * sizeof(int32_t), s), "overflow list");
-            if (st != RSI_OK) return RSI_E_OOM;
-            h->ovf_cap = n;
-        }
-        st = rsi_cuda_check(cudaMemsetAsync(h->scratch + SCR_OVF_COUNT, 0, 2 * sizeof(uint32_t), s), "memset");
-        if (st != RSI_OK) return st;
+    if (mode == RSI_MODE_INTERCEPT_COUNT && h->ovf_cap < n) {
+        if (h->ovf_list) cudaFreeAsync(h->ovf_list, s);
+        h->ovf_list = nullptr;
+        h->ovf_cap = 0;
+        st = rsi_cuda_check(cudaMallocAsync((void**)&h->ovf_list, (size_t)n * sizeof(int32_t), s), "overflow list");
+        if (st != RSI_OK) return RSI_E_OOM;
+        h->ovf_cap = n;
     }
-    if (h->opt.flags & RSI_OPT_FP64_MOLLER)
-        launch_main<true>(h, S, E, n, mode, out, s);
+    // zero the overflow counters and the ray dispenser (scratch words 16..19)
+    st = rsi_cuda_check(cudaMemsetAsync(h->scratch + SCR_OVF_COUNT, 0, 4 * sizeof(uint32_t), s), "memset");
+    if (st != RSI_OK) return st;
+    TraceParams p{};
+    p.nodes = h->nodes;
+    p.tris = h->tris;
+    p.S = S;
+    p.E = E;
+    p.n = n;
+    p.hit = out->hit;
+    p.tri = out->tri;
+    p.t = out->t;
+    p.dist = out->dist;
+    p.point = out->point;
+    p.count = out->count;
+    p.tau = h->opt.dedup_tau;
+    p.ovf_list = h->ovf_list;
+    p.scratch = h->scratch;
+    p.stats = h->stats;
+    p.counter = reinterpret_cast<unsigned long long*>(h->scratch + SCR_DISPENSER);
+    p.min_trav = h->min_trav;
+    const bool fp64 = (h->opt.flags & RSI_OPT_FP64_MOLLER) != 0, ctr = (h->opt.flags & RSI_OPT_COUNTERS) != 0;
+    if (fp64)
+        ctr ? launch_mode<true, true>(mode, p, s) : launch_mode<true, false>(mode, p, s);
     else
-        launch_main<false>(h, S, E, n, mode, out, s);
+        ctr ? launch_mode<false, true>(mode, p, s) : launch_mode<false, false>(mode, p, s);
     st = rsi_cuda_check(cudaGetLastError(), "traversal launch");
     if (st != RSI_OK) return st;
     if (mode != RSI_MODE_INTERCEPT_COUNT) return RSI_OK;

@@ -23,6 +23,7 @@ from . import _build
 
 MODES = {"boolean": 0, "barycentric": 1, "intercept_count": 2}
 OPT_FP64_MOLLER = 1
+OPT_COUNTERS = 2
 
 _lock = threading.Lock()
 _lib = None
@@ -49,7 +50,8 @@ class _Outputs(ctypes.Structure):
 
 
 class _Stats(ctypes.Structure):
-    _fields_ = [(n, ctypes.c_uint64) for n in ("rays", "fp64_pairs", "fp64_rays", "overflow_rays", "nonfinite_rays")]
+    _fields_ = [(n, ctypes.c_uint64) for n in ("rays", "fp64_pairs", "fp64_rays", "overflow_rays", "nonfinite_rays",
+                                               "box_tests", "mt_tests")]
 
 
 def lib_path() -> str:
@@ -121,9 +123,11 @@ def rsi_version() -> str:
 class Options:
     fp64_moller: bool = False   # P:501 USE_DOUBLE_PRECISION_MOLLER
     dedup_tau: float = 1e-6     # reading R4
+    counters: bool = False      # instrumented kernels: box / MT test counts in rsi_get_stats
 
     def _c(self) -> _Options:
-        return _Options(ctypes.sizeof(_Options), OPT_FP64_MOLLER if self.fp64_moller else 0, float(self.dedup_tau))
+        flags = (OPT_FP64_MOLLER if self.fp64_moller else 0) | (OPT_COUNTERS if self.counters else 0)
+        return _Options(ctypes.sizeof(_Options), flags, float(self.dedup_tau))
 
 
 class Handle:

@@ -1,0 +1,37 @@
+"""GPU-box helper: time the traversal per mode for several knob settings."""
+import os, sys, time, json
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import numpy as np, torch
+import synth
+from paper_2305_01867_b200 import rsi
+
+n = int(os.environ.get("N", "10000000"))
+wl = os.environ.get("WL", "sphere")
+V, T, S, E, _ = synth.workload(wl, n, seed=3)
+dev = torch.device("cuda:0")
+Vd, Td, Sd, Ed = (torch.from_numpy(a).to(dev) for a in (V, T, S, E))
+res = {}
+for mt in [int(x) for x in os.environ.get("MINTRAV", "0,4,8,16").split(",")]:
+    os.environ["RSI_MIN_TRAV"] = str(mt)
+    h = rsi.rsi_build(Vd, Td)
+    for mode in ("boolean", "barycentric", "intercept_count"):
+        out = rsi.alloc_outputs(n, mode, dev)
+        for _ in range(2):
+            rsi.rsi_intersect(h, Sd, Ed, mode, out=out)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            rsi.rsi_intersect(h, Sd, Ed, mode, out=out)
+        e1.record(); torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 5
+        res[f"{mode}/min_trav={mt}"] = {"ms": round(ms, 3), "Grays_s": round(n / ms / 1e6, 3)}
+    h.free()
+hc = rsi.rsi_build(Vd, Td, rsi.Options(counters=True))
+for mode in ("boolean", "barycentric", "intercept_count"):
+    rsi.rsi_reset_stats(hc)
+    rsi.rsi_intersect(hc, Sd, Ed, mode)
+    st = rsi.rsi_get_stats(hc)
+    res[f"work/{mode}"] = {"box_per_ray": st["box_tests"] / n, "mt_per_ray": st["mt_tests"] / n,
+                           "fp64_pairs": st["fp64_pairs"], "fp64_rays": st["fp64_rays"], "overflow": st["overflow_rays"]}
+print(json.dumps(res, indent=1))

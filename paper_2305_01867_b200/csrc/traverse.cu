@@ -293,6 +293,7 @@ struct TraceParams {
     unsigned long long* stats;
     unsigned long long* counter;  // persistent-grid ray dispenser
     int min_trav;                 // leave the traversal phase when fewer lanes still search
+    int spec;                     // max pending leaves while traversing (1 = none speculative)
 };
 
 template <int MODE>
@@ -543,7 +544,7 @@ __global__ void __launch_bounds__(kThreads) k_trace(const TraceParams p) {
     bool exhausted = false;       // warp-uniform
     int64_t ray = -1;
     Ray r;
-    int node = -1, sp = 0, leaf0 = -1, leaf1 = -1;
+    int node = -1, sp = 0, npend = 0, l0 = -1, l1 = -1, l2 = -1;  // pending (postponed) leaves
     int stack[kStack];
     float tclip = 1.0f;
     ModeState<MODE> ms;
@@ -581,18 +582,22 @@ __global__ void __launch_bounds__(kThreads) k_trace(const TraceParams p) {
             ms.init();
             tclip = 1.0f;
             sp = 0;
-            leaf0 = leaf1 = -1;
+            npend = 0;
             node = ok ? 0 : -1;
         }
         if (__ballot_sync(FULL, ray >= 0) == 0) break;  // no rays left for this warp
 
         // ---- 2. traversal phase
+        // A lane searches while it has a node and fewer than p.spec pending
+        // leaves (spec = 2: lanes that already hold a leaf keep traversing
+        // speculatively in slots that would otherwise idle).  The phase lasts
+        // while some lane still has no pending leaf.
         while (true) {
-            const bool trav = node >= 0 && leaf0 < 0;
-            const unsigned tm = __ballot_sync(FULL, trav);
-            if (tm == 0) break;
-            if (__popc(tm) < p.min_trav && __ballot_sync(FULL, leaf0 >= 0)) break;
-            if (trav) {
+            const bool searching = node >= 0 && npend == 0;
+            const unsigned sm = __ballot_sync(FULL, searching);
+            if (sm == 0) break;
+            if (__popc(sm) < p.min_trav && __ballot_sync(FULL, npend > 0)) break;
+            if (node >= 0 && npend < p.spec) {
                 const float4* nd = p.nodes + 4 * node;
                 const float4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2);
                 const int4 n3 = __ldg(reinterpret_cast<const int4*>(nd + 3));
@@ -601,14 +606,15 @@ __global__ void __launch_bounds__(kThreads) k_trace(const TraceParams p) {
                 bool hR = slab(r, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, tclip, nearR);
                 if (kCounters) st.boxes += 2;
                 if (hL && n3.x < 0) {
-                    leaf0 = ~n3.x;
+                    const int x = ~n3.x;
+                    if (npend == 0) l0 = x; else l1 = x;
+                    ++npend;
                     hL = false;
                 }
                 if (hR && n3.y < 0) {
-                    if (leaf0 < 0)
-                        leaf0 = ~n3.y;
-                    else
-                        leaf1 = ~n3.y;
+                    const int x = ~n3.y;
+                    if (npend == 0) l0 = x; else if (npend == 1) l1 = x; else l2 = x;
+                    ++npend;
                     hR = false;
                 }
                 if (hL && hR) {
@@ -626,16 +632,17 @@ __global__ void __launch_bounds__(kThreads) k_trace(const TraceParams p) {
         }
 
         // ---- 3. leaf phase
-        if (leaf0 >= 0) {
-            if (kCounters) st.mts += 1 + (leaf1 >= 0);
-            bool done = ms.template leaf<kFP64>(p, r, leaf0, tclip, st);
-            if (!done && leaf1 >= 0) done = ms.template leaf<kFP64>(p, r, leaf1, tclip, st);
-            leaf0 = leaf1 = -1;
+        if (npend > 0) {
+            if (kCounters) st.mts += npend;
+            bool done = ms.template leaf<kFP64>(p, r, l0, tclip, st);
+            if (!done && npend > 1) done = ms.template leaf<kFP64>(p, r, l1, tclip, st);
+            if (!done && npend > 2) done = ms.template leaf<kFP64>(p, r, l2, tclip, st);
+            npend = 0;
             if (done) node = -1;
         }
 
         // ---- 4. finish
-        if (ray >= 0 && node < 0 && leaf0 < 0) {
+        if (ray >= 0 && node < 0 && npend == 0) {
             ms.finish(p, r, ray, st);
             ray = -1;
         }
@@ -869,6 +876,7 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     p.stats = h->stats;
     p.counter = reinterpret_cast<unsigned long long*>(h->scratch + SCR_DISPENSER);
     p.min_trav = h->min_trav;
+    p.spec = h->spec;
     const bool fp64 = (h->opt.flags & RSI_OPT_FP64_MOLLER) != 0, ctr = (h->opt.flags & RSI_OPT_COUNTERS) != 0;
     if (fp64)
         ctr ? launch_mode<true, true>(mode, p, s) : launch_mode<true, false>(mode, p, s);

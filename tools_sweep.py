@@ -11,8 +11,10 @@ V, T, S, E, _ = synth.workload(wl, n, seed=3)
 dev = torch.device("cuda:0")
 Vd, Td, Sd, Ed = (torch.from_numpy(a).to(dev) for a in (V, T, S, E))
 res = {}
-for mt in [int(x) for x in os.environ.get("MINTRAV", "0,4,8,16").split(",")]:
-    os.environ["RSI_MIN_TRAV"] = str(mt)
+for cfg in os.environ.get("CFGS", "8:1,8:2,4:2,16:2").split(","):
+    mt, sp = cfg.split(":")
+    os.environ["RSI_MIN_TRAV"] = mt
+    os.environ["RSI_SPEC"] = sp
     h = rsi.rsi_build(Vd, Td)
     for mode in ("boolean", "barycentric", "intercept_count"):
         out = rsi.alloc_outputs(n, mode, dev)
@@ -25,7 +27,7 @@ for mt in [int(x) for x in os.environ.get("MINTRAV", "0,4,8,16").split(",")]:
             rsi.rsi_intersect(h, Sd, Ed, mode, out=out)
         e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 5
-        res[f"{mode}/min_trav={mt}"] = {"ms": round(ms, 3), "Grays_s": round(n / ms / 1e6, 3)}
+        res[f"{mode}/min_trav={mt},spec={sp}"] = {"ms": round(ms, 3), "Grays_s": round(n / ms / 1e6, 3)}
     h.free()
 hc = rsi.rsi_build(Vd, Td, rsi.Options(counters=True))
 for mode in ("boolean", "barycentric", "intercept_count"):

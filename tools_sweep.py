@@ -36,4 +36,4 @@ for mode in ("boolean", "barycentric", "intercept_count"):
     st = rsi.rsi_get_stats(hc)
     res[f"work/{mode}"] = {"box_per_ray": st["box_tests"] / n, "mt_per_ray": st["mt_tests"] / n,
                            "fp64_pairs": st["fp64_pairs"], "fp64_rays": st["fp64_rays"], "overflow": st["overflow_rays"]}
-print(json.dumps(res, indent=1))
+[print(k, json.dumps(v)) for k, v in res.items()]

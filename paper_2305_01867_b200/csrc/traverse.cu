@@ -23,6 +23,7 @@ constexpr float kU = 5.9604644775390625e-08f;    // 2^-24, fp32 unit roundoff
 constexpr float kFilt = 16.0f * kU;              // K = 16
 constexpr float kTerr = 12.0f * kU;              // t forward-error constant
 constexpr float kSlack = 4.76837158203125e-07f;  // 2^-21: slab-test slack factor
+constexpr float kSlackMax = 1.953125e-03f;       // 2^-9: larger slack -> axis unconstrained
 constexpr float kTiny = 1e-30f;                  // absolute floor (underflow)
 constexpr float kOutTol = 4e-6f;                 // max certified |t error| for fp32 outputs
 constexpr int kStack = 64;
@@ -34,31 +35,28 @@ enum { MT_MISS = 0, MT_HIT = 1, MT_UNSURE = 2 };
 
 struct Ray {
     float ox, oy, oz;  // start (r^start)
-    float ex, ey, ez;  // end (r^end), kept exactly for the fp64 mirror
-    float dx, dy, dz;  // d = end - start (fp32)
-    float ix, iy, iz;  // slab: 1/d per axis (0 on degenerate axes)
-    float lx, ly, lz;  // slab offsets applied to the box's lo plane
-    float hx, hy, hz;  // slab offsets applied to the box's hi plane
+    float dx, dy, dz;  // d = end - start (fp32); the end point itself is re-read for the fp64 mirror
+    float ix, iy, iz;  // slab: 1/d per axis (0 on an unconstrained axis)
+    float qx, qy, qz;  // slab: o/d per axis (NaN on an unconstrained axis)
+    float S;           // slab slack: 2 x the largest per-axis error bound (t units)
 };
 
-// Per-axis slab setup.  t = fma(plane, inv, -off) approximates (plane - o)/d;
-// the slack (2^-21 * (1 + |o/d|)) exceeds the fp32 error of that expression
-// for |t| <= ~1, and is applied so the computed entry t is never later and the
-// exit t never earlier than the exact ones: the test never rejects a box the
-// exact segment touches.  |d| < 1e-30 (incl. 0): the axis imposes no constraint.
-__device__ __forceinline__ void slab_axis(float o, float d, float& inv, float& offlo, float& offhi) {
+// Per-axis slab setup.  t = fma(plane, inv, -o/d) approximates (plane - o)/d
+// with an absolute error below slack = 2^-21 (1 + |o/d|) for |t| <= ~1 (the
+// only range where a decision is taken).  The box test accepts when
+//   max(t_near, 0) - S <= min(t_far, tclip),  S = 2 max_axis slack,
+// so it never rejects a box the exact segment touches.  Axes with |d| < 1e-30
+// or slack > 2^-9 impose no constraint (inv = 0, o/d = NaN: min/max ignore NaN).
+__device__ __forceinline__ void slab_axis(float o, float d, float& inv, float& oinv, float& slack) {
     if (fabsf(d) >= 1e-30f) {
         inv = 1.0f / d;
-        float oinv = o * inv;
-        float slack = kSlack * (1.0f + fabsf(oinv));
-        float sg = inv > 0.0f ? slack : -slack;
-        offlo = oinv + sg;
-        offhi = oinv - sg;
-        if (isfinite(offlo) && isfinite(offhi)) return;
+        oinv = o * inv;
+        slack = kSlack * (1.0f + fabsf(oinv));
+        if (slack <= kSlackMax) return;  // also false for NaN / Inf
     }
     inv = 0.0f;
-    offlo = INFINITY;
-    offhi = -INFINITY;
+    oinv = __int_as_float(0x7fffffff);  // NaN
+    slack = 0.0f;
 }
 
 // Returns false for rays that cannot hit: zero length or a non-finite coordinate
@@ -68,29 +66,29 @@ __device__ __forceinline__ bool load_ray(Ray& r, const float* __restrict__ S, co
     r.ox = __ldg(S + 3 * i);
     r.oy = __ldg(S + 3 * i + 1);
     r.oz = __ldg(S + 3 * i + 2);
-    r.ex = __ldg(E + 3 * i);
-    r.ey = __ldg(E + 3 * i + 1);
-    r.ez = __ldg(E + 3 * i + 2);
-    nonfinite = !(isfinite(r.ox) && isfinite(r.oy) && isfinite(r.oz) && isfinite(r.ex) && isfinite(r.ey) &&
-                  isfinite(r.ez));
-    r.dx = r.ex - r.ox;
-    r.dy = r.ey - r.oy;
-    r.dz = r.ez - r.oz;
-    slab_axis(r.ox, r.dx, r.ix, r.lx, r.hx);
-    slab_axis(r.oy, r.dy, r.iy, r.ly, r.hy);
-    slab_axis(r.oz, r.dz, r.iz, r.lz, r.hz);
+    const float ex = __ldg(E + 3 * i), ey = __ldg(E + 3 * i + 1), ez = __ldg(E + 3 * i + 2);
+    nonfinite = !(isfinite(r.ox) && isfinite(r.oy) && isfinite(r.oz) && isfinite(ex) && isfinite(ey) &&
+                  isfinite(ez));
+    r.dx = ex - r.ox;
+    r.dy = ey - r.oy;
+    r.dz = ez - r.oz;
+    float sx, sy, sz;
+    slab_axis(r.ox, r.dx, r.ix, r.qx, sx);
+    slab_axis(r.oy, r.dy, r.iy, r.qy, sy);
+    slab_axis(r.oz, r.dz, r.iz, r.qz, sz);
+    r.S = 2.0f * fmaxf(sx, fmaxf(sy, sz));
     return !nonfinite && !(r.dx == 0.0f && r.dy == 0.0f && r.dz == 0.0f);
 }
 
-// Conservative segment/box overlap on [0, tclip]; tnear is the (lowered) entry t.
+// Conservative segment/box overlap on [0, tclip]; tnear is the entry t.
 __device__ __forceinline__ bool slab(const Ray& r, float lox, float hix, float loy, float hiy, float loz, float hiz,
                                      float tclip, float& tnear) {
-    float tx1 = fmaf(lox, r.ix, -r.lx), tx2 = fmaf(hix, r.ix, -r.hx);
-    float ty1 = fmaf(loy, r.iy, -r.ly), ty2 = fmaf(hiy, r.iy, -r.hy);
-    float tz1 = fmaf(loz, r.iz, -r.lz), tz2 = fmaf(hiz, r.iz, -r.hz);
-    tnear = fmaxf(fmaxf(fminf(tx1, tx2), fminf(ty1, ty2)), fmaxf(fminf(tz1, tz2), 0.0f));
-    float tfar = fminf(fminf(fmaxf(tx1, tx2), fmaxf(ty1, ty2)), fminf(fmaxf(tz1, tz2), tclip));
-    return tnear <= tfar;
+    const float tx1 = fmaf(lox, r.ix, -r.qx), tx2 = fmaf(hix, r.ix, -r.qx);
+    const float ty1 = fmaf(loy, r.iy, -r.qy), ty2 = fmaf(hiy, r.iy, -r.qy);
+    const float tz1 = fmaf(loz, r.iz, -r.qz), tz2 = fmaf(hiz, r.iz, -r.qz);
+    tnear = fmaxf(fmaxf(fminf(tx1, tx2), fminf(ty1, ty2)), fminf(tz1, tz2));
+    const float tfar = fminf(fminf(fmaxf(tx1, tx2), fmaxf(ty1, ty2)), fmaxf(tz1, tz2));
+    return fmaxf(tnear - r.S, -r.S) <= fminf(tfar, tclip);
 }
 
 // ---------------------------------------------------------------- fp32 MT + error filter
@@ -150,9 +148,11 @@ __device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b
 __device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
 
-__device__ __noinline__ int mt64(const Ray& r, const float4 A, const float4 B, const float4 C, double* t_out) {
+// `e3` points at this segment's end point (r^end) in the caller's array.
+__device__ __noinline__ int mt64(const Ray& r, const float* __restrict__ e3, const float4 A, const float4 B,
+                                 const float4 C, double* t_out) {
     const double Ox = r.ox, Oy = r.oy, Oz = r.oz;
-    const double dx = ds((double)r.ex, Ox), dy = ds((double)r.ey, Oy), dz = ds((double)r.ez, Oz);
+    const double dx = ds((double)__ldg(e3), Ox), dy = ds((double)__ldg(e3 + 1), Oy), dz = ds((double)__ldg(e3 + 2), Oz);
     const double Ax = A.x, Ay = A.y, Az = A.z;
     const double e1x = ds(B.x, Ax), e1y = ds(B.y, Ay), e1z = ds(B.z, Az);
     const double e2x = ds(C.x, Ax), e2y = ds(C.y, Ay), e2z = ds(C.z, Az);
@@ -222,46 +222,28 @@ __device__ __forceinline__ void traverse(const float4* __restrict__ nodes, const
     }
 }
 
+// Block-level counters in shared memory (rare events), flushed once per block.
 struct Stats {
-    unsigned fp64_pairs = 0, fp64_ray = 0, nonfinite = 0, boxes = 0, mts = 0;
+    unsigned* s;  // shared [ST_WORDS]
+    unsigned boxes = 0, mts = 0;  // RSI_OPT_COUNTERS only
+    __device__ __forceinline__ void add(int k, unsigned v = 1) { atomicAdd(s + k, v); }
 };
-
-__device__ __forceinline__ void flush_stats(const Stats& st, unsigned long long* stats) {
-    const unsigned m = 0xffffffffu;
-    unsigned a = st.fp64_pairs, b = st.fp64_ray, c = st.nonfinite, d = st.boxes, e = st.mts;
-    if (__any_sync(m, a | b | c | d | e)) {
-        for (int o = 16; o; o >>= 1) {
-            a += __shfl_xor_sync(m, a, o);
-            b += __shfl_xor_sync(m, b, o);
-            c += __shfl_xor_sync(m, c, o);
-            d += __shfl_xor_sync(m, d, o);
-            e += __shfl_xor_sync(m, e, o);
-        }
-        if ((threadIdx.x & 31) == 0) {
-            if (a) atomicAdd(stats + ST_FP64_PAIRS, (unsigned long long)a);
-            if (b) atomicAdd(stats + ST_FP64_RAYS, (unsigned long long)b);
-            if (c) atomicAdd(stats + ST_NONFINITE, (unsigned long long)c);
-            if (d) atomicAdd(stats + ST_BOX_TESTS, (unsigned long long)d);
-            if (e) atomicAdd(stats + ST_MT_TESTS, (unsigned long long)e);
-        }
-    }
-}
 
 // Decide one (ray, leaf) pair: MT_MISS, or MT_HIT with either (t32, et) or an
 // exact t64 (is64 = true).
 template <bool kFP64>
-__device__ __forceinline__ int decide(const Ray& r, const float4& A, const float4& B, const float4& C, float& t32,
-                                      float& et, double& t64, bool& is64, Stats& st) {
+__device__ __forceinline__ int decide(const Ray& r, const float* e3, const float4& A, const float4& B,
+                                      const float4& C, float& t32, float& et, double& t64, bool& is64, Stats& st) {
     if (!kFP64) {
         int s = mt32(r, A, B, C, t32, et);
         if (s != MT_UNSURE) {
             is64 = false;
             return s;
         }
-        ++st.fp64_pairs;
+        st.add(ST_FP64_PAIRS);
     }
     is64 = true;
-    return mt64(r, A, B, C, &t64) ? MT_HIT : MT_MISS;
+    return mt64(r, e3, A, B, C, &t64) ? MT_HIT : MT_MISS;
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -280,7 +262,7 @@ struct TraceParams {
     const float4* tris;
     const float* S;
     const float* E;
-    int64_t n;
+    int n;
     uint8_t* hit;
     int32_t* tri;
     float* t;
@@ -291,9 +273,9 @@ struct TraceParams {
     int32_t* ovf_list;
     uint32_t* scratch;
     unsigned long long* stats;
-    unsigned long long* counter;  // persistent-grid ray dispenser
-    int min_trav;                 // leave the traversal phase when fewer lanes still search
-    int spec;                     // max pending leaves while traversing (1 = none speculative)
+    unsigned int* counter;  // persistent-grid ray dispenser
+    int min_trav;           // leave the traversal phase when fewer lanes still search
+    int spec;               // max pending leaves while traversing (1 = no speculation)
 };
 
 template <int MODE>
@@ -304,16 +286,17 @@ struct ModeState<MODE_BOOL> {
     bool found;
     __device__ __forceinline__ void init() { found = false; }
     template <bool kFP64>
-    __device__ __forceinline__ bool leaf(const TraceParams& p, const Ray& r, int k, float& tclip, Stats& st) {
+    __device__ __forceinline__ bool leaf(const TraceParams& p, const Ray& r, const float* e3, int k, float& tclip,
+                                         Stats& st) {
         float4 A, B, C;
         load_tri(p.tris, k, A, B, C);
         float t32, et;
         double t64;
         bool is64;
-        found = decide<kFP64>(r, A, B, C, t32, et, t64, is64, st) == MT_HIT;
+        found = decide<kFP64>(r, e3, A, B, C, t32, et, t64, is64, st) == MT_HIT;
         return found;  // any-hit early exit
     }
-    __device__ __forceinline__ void finish(const TraceParams& p, const Ray&, int64_t i, Stats&) {
+    __device__ __forceinline__ void finish(const TraceParams& p, const Ray&, const float*, int i, Stats&) {
         p.hit[i] = found ? 1 : 0;
     }
 };
@@ -335,13 +318,14 @@ struct ModeState<MODE_BARY> {
         t64 = 0.0;
     }
     template <bool kFP64>
-    __device__ __forceinline__ bool leaf(const TraceParams& p, const Ray& r, int k, float& tclip, Stats& st) {
+    __device__ __forceinline__ bool leaf(const TraceParams& p, const Ray& r, const float* e3, int k, float& tclip,
+                                         Stats& st) {
         float4 A, B, C;
         load_tri(p.tris, k, A, B, C);
         float t32, et;
         double c64;
         bool c_is64;
-        if (decide<kFP64>(r, A, B, C, t32, et, c64, c_is64, st) != MT_HIT) return false;
+        if (decide<kFP64>(r, e3, A, B, C, t32, et, c64, c_is64, st) != MT_HIT) return false;
         const int cid = __float_as_int(A.w);
         bool take;
         if (slot < 0) {
@@ -354,15 +338,15 @@ struct ModeState<MODE_BARY> {
             } else if (clo > bhi) {
                 take = false;
             } else {  // order not certified: settle both in the fp64 mirror
-                st.fp64_ray = 1;
+                st.add(ST_FP64_RAYS);
                 if (!c_is64) {
-                    mt64(r, A, B, C, &c64);
+                    mt64(r, e3, A, B, C, &c64);
                     c_is64 = true;
                 }
                 if (!is64) {
                     float4 bA, bB, bC;
                     load_tri(p.tris, slot, bA, bB, bC);
-                    mt64(r, bA, bB, bC, &t64);
+                    mt64(r, e3, bA, bB, bC, &t64);
                     is64 = true;
                 }
                 take = (c64 < t64) || (c64 == t64 && cid < id);
@@ -383,7 +367,7 @@ struct ModeState<MODE_BARY> {
         }
         return false;
     }
-    __device__ __forceinline__ void finish(const TraceParams& p, const Ray& r, int64_t i, Stats& st) {
+    __device__ __forceinline__ void finish(const TraceParams& p, const Ray& r, const float* e3, int i, Stats& st) {
         if (slot >= 0) {
             float tt;
             if (is64) {
@@ -394,9 +378,9 @@ struct ModeState<MODE_BARY> {
                 float4 bA, bB, bC;
                 load_tri(p.tris, slot, bA, bB, bC);
                 double v = 0.0;
-                mt64(r, bA, bB, bC, &v);
+                mt64(r, e3, bA, bB, bC, &v);
                 tt = (float)v;
-                st.fp64_ray = 1;
+                st.add(ST_FP64_RAYS);
             }
             p.tri[i] = id;
             if (p.t) p.t[i] = tt;
@@ -423,7 +407,8 @@ struct ModeState<MODE_BARY> {
 // threshold tau (reading R4): 1 + #{sorted gaps > tau}.  The fp32 path is used
 // only when every pairwise |t_a - t_b| vs tau decision is certified; otherwise
 // all hit t are recomputed in the fp64 mirror and counted exactly as the
-// oracle does.  More than kCountCap hits -> the exact re-pass.
+// oracle does.  More than kCountCap hits -> the exact re-pass.  The hit list
+// lives in shared memory (column per thread) to keep registers for occupancy.
 __device__ __forceinline__ void sort_small(double* v, int n) {
     for (int a = 1; a < n; ++a) {
         double x = v[a];
@@ -438,8 +423,8 @@ __device__ __forceinline__ void sort_small(double* v, int n) {
 
 template <>
 struct ModeState<MODE_COUNT> {
-    float lt[kCountCap], le[kCountCap];
-    int lk[kCountCap];
+    float2* te;  // shared: te[x * kThreads] = (t, err) of hit x
+    int* kk;     // shared: leaf slot of hit x
     int nh;
     bool overflow;
     __device__ __forceinline__ void init() {
@@ -447,13 +432,14 @@ struct ModeState<MODE_COUNT> {
         overflow = false;
     }
     template <bool kFP64>
-    __device__ __forceinline__ bool leaf(const TraceParams& p, const Ray& r, int k, float& tclip, Stats& st) {
+    __device__ __forceinline__ bool leaf(const TraceParams& p, const Ray& r, const float* e3, int k, float& tclip,
+                                         Stats& st) {
         float4 A, B, C;
         load_tri(p.tris, k, A, B, C);
         float t32, et;
         double t64;
         bool is64;
-        if (decide<kFP64>(r, A, B, C, t32, et, t64, is64, st) != MT_HIT) return false;
+        if (decide<kFP64>(r, e3, A, B, C, t32, et, t64, is64, st) != MT_HIT) return false;
         if (nh == kCountCap) {
             overflow = true;
             return true;
@@ -462,17 +448,12 @@ struct ModeState<MODE_COUNT> {
             t32 = (float)t64;
             et = fmaf(kU, fabsf(t32), kTiny);
         }
-#pragma unroll
-        for (int x = 0; x < kCountCap; ++x)
-            if (x == nh) {
-                lt[x] = t32;
-                le[x] = et;
-                lk[x] = k;
-            }
+        te[nh * kThreads] = make_float2(t32, et);
+        kk[nh * kThreads] = k;
         ++nh;
         return false;
     }
-    __device__ __forceinline__ void finish(const TraceParams& p, const Ray& r, int64_t i, Stats& st) {
+    __device__ __forceinline__ void finish(const TraceParams& p, const Ray& r, const float* e3, int i, Stats& st) {
         if (overflow) {
             uint32_t pos = atomicAdd(&p.scratch[SCR_OVF_COUNT], 1u);
             p.ovf_list[pos] = (int32_t)i;
@@ -484,6 +465,14 @@ struct ModeState<MODE_COUNT> {
             return;
         }
         const float ftau = (float)p.tau;
+        float lt[kCountCap], le[kCountCap];
+#pragma unroll
+        for (int x = 0; x < kCountCap; ++x)
+            if (x < nh) {
+                const float2 v = te[x * kThreads];
+                lt[x] = v.x;
+                le[x] = v.y;
+            }
         bool sure = true;
 #pragma unroll
         for (int a = 0; a < kCountCap; ++a)
@@ -509,12 +498,12 @@ struct ModeState<MODE_COUNT> {
             for (int a = 0; a + 1 < kCountCap; ++a)
                 if (a + 1 < nh && lt[a + 1] - lt[a] > ftau) ++cnt;
         } else {
-            st.fp64_ray = 1;
+            st.add(ST_FP64_RAYS);
             double v[kCountCap];
             for (int a = 0; a < nh; ++a) {
                 float4 A, B, C;
-                load_tri(p.tris, lk[a], A, B, C);
-                mt64(r, A, B, C, &v[a]);
+                load_tri(p.tris, kk[a * kThreads], A, B, C);
+                mt64(r, e3, A, B, C, &v[a]);
             }
             sort_small(v, nh);
             for (int a = 0; a + 1 < nh; ++a)
@@ -529,42 +518,52 @@ struct ModeState<MODE_COUNT> {
 // Laine's while-while traversal, adapted to segments and child-pair nodes):
 //   1. refill: lanes without a ray take the next ray ids from the warp's chunk
 //      (one atomicAdd per kChunk rays per warp), so lanes never idle while rays remain;
-//   2. traversal phase: lanes walk internal nodes until they hold a pending
-//      leaf (or run out of nodes); the phase ends when no lane (or fewer than
-//      min_trav lanes) is still searching;
+//   2. traversal phase: a lane walks internal nodes while it holds fewer than
+//      `spec` pending leaves; the phase ends when no lane (or fewer than
+//      min_trav lanes) is still searching without a pending leaf;
 //   3. leaf phase: all lanes with pending leaves run Moller-Trumbore together;
 //   4. finished rays write their outputs and free the lane.
 template <int MODE, bool kFP64, bool kCounters>
-__global__ void __launch_bounds__(kThreads) k_trace(const TraceParams p) {
+__global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? 8 : 6) k_trace(const TraceParams p) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
+    __shared__ unsigned s_stats[ST_WORDS];
+    __shared__ float2 s_te[MODE == MODE_COUNT ? kCountCap * kThreads : 1];
+    __shared__ int s_k[MODE == MODE_COUNT ? kCountCap * kThreads : 1];
+    if (threadIdx.x < ST_WORDS) s_stats[threadIdx.x] = 0u;
+    __syncthreads();
     Stats st;
-    int64_t cnext = 0, cend = 0;  // warp-uniform chunk [cnext, cend)
-    bool exhausted = false;       // warp-uniform
-    int64_t ray = -1;
+    st.s = s_stats;
+    int cnext = 0, cend = 0;  // warp-uniform chunk [cnext, cend)
+    bool exhausted = false;   // warp-uniform
+    int ray = -1;
     Ray r;
     int node = -1, sp = 0, npend = 0, l0 = -1, l1 = -1, l2 = -1;  // pending (postponed) leaves
     int stack[kStack];
     float tclip = 1.0f;
     ModeState<MODE> ms;
+    if constexpr (MODE == MODE_COUNT) {
+        ms.te = s_te + threadIdx.x;
+        ms.kk = s_k + threadIdx.x;
+    }
     while (true) {
         // ---- 1. refill
         unsigned want = __ballot_sync(FULL, ray < 0);
         bool fresh = false;
         while (want && !exhausted) {
             if (cnext >= cend) {
-                unsigned long long base = 0;
-                if (lane == 0) base = atomicAdd(p.counter, (unsigned long long)kChunk);
+                unsigned base = 0;
+                if (lane == 0) base = atomicAdd(p.counter, (unsigned)kChunk);
                 base = __shfl_sync(FULL, base, 0);
-                if ((int64_t)base >= p.n) {
+                if (base >= (unsigned)p.n) {
                     exhausted = true;
                     break;
                 }
-                cnext = (int64_t)base;
-                cend = min((int64_t)base + kChunk, p.n);
+                cnext = (int)base;
+                cend = min((int)base + kChunk, p.n);
             }
-            const int take = (int)min((int64_t)__popc(want), cend - cnext);
+            const int take = min(__popc(want), cend - cnext);
             const bool mine = (want >> lane) & 1u;
             const int rank = __popc(want & lt);
             const bool got = mine && rank < take;
@@ -578,7 +577,7 @@ __global__ void __launch_bounds__(kThreads) k_trace(const TraceParams p) {
         if (fresh) {
             bool nonfinite;
             const bool ok = load_ray(r, p.S, p.E, ray, nonfinite);
-            st.nonfinite += nonfinite;
+            if (nonfinite) st.add(ST_NONFINITE);
             ms.init();
             tclip = 1.0f;
             sp = 0;
@@ -588,10 +587,6 @@ __global__ void __launch_bounds__(kThreads) k_trace(const TraceParams p) {
         if (__ballot_sync(FULL, ray >= 0) == 0) break;  // no rays left for this warp
 
         // ---- 2. traversal phase
-        // A lane searches while it has a node and fewer than p.spec pending
-        // leaves (spec = 2: lanes that already hold a leaf keep traversing
-        // speculatively in slots that would otherwise idle).  The phase lasts
-        // while some lane still has no pending leaf.
         while (true) {
             const bool searching = node >= 0 && npend == 0;
             const unsigned sm = __ballot_sync(FULL, searching);
@@ -633,21 +628,27 @@ __global__ void __launch_bounds__(kThreads) k_trace(const TraceParams p) {
 
         // ---- 3. leaf phase
         if (npend > 0) {
+            const float* e3 = p.E + 3 * (int64_t)ray;
             if (kCounters) st.mts += npend;
-            bool done = ms.template leaf<kFP64>(p, r, l0, tclip, st);
-            if (!done && npend > 1) done = ms.template leaf<kFP64>(p, r, l1, tclip, st);
-            if (!done && npend > 2) done = ms.template leaf<kFP64>(p, r, l2, tclip, st);
+            bool done = ms.template leaf<kFP64>(p, r, e3, l0, tclip, st);
+            if (!done && npend > 1) done = ms.template leaf<kFP64>(p, r, e3, l1, tclip, st);
+            if (!done && npend > 2) done = ms.template leaf<kFP64>(p, r, e3, l2, tclip, st);
             npend = 0;
             if (done) node = -1;
         }
 
         // ---- 4. finish
         if (ray >= 0 && node < 0 && npend == 0) {
-            ms.finish(p, r, ray, st);
+            ms.finish(p, r, p.E + 3 * (int64_t)ray, ray, st);
             ray = -1;
         }
     }
-    flush_stats(st, p.stats);
+    if (kCounters) {
+        st.add(ST_BOX_TESTS, st.boxes);
+        st.add(ST_MT_TESTS, st.mts);
+    }
+    __syncthreads();
+    if (threadIdx.x < ST_WORDS && s_stats[threadIdx.x]) atomicAdd(p.stats + threadIdx.x, (unsigned long long)s_stats[threadIdx.x]);
 }
 
 // ---------------------------------------------------------------- exact re-pass for overflowed rays
@@ -668,7 +669,7 @@ __global__ void __launch_bounds__(kThreads) k_ovf_size(const float4* __restrict_
         load_tri(tris, k, A, B, C);
         float t32, et;
         int s = mt32(r, A, B, C, t32, et);
-        if (s == MT_HIT || (s == MT_UNSURE && mt64(r, A, B, C, nullptr))) ++nh;
+        if (s == MT_HIT || (s == MT_UNSURE && mt64(r, E + 3 * (int64_t)list[j], A, B, C, nullptr))) ++nh;
         return false;
     });
     seg[2 * j] = (int32_t)atomicAdd(&scratch[SCR_OVF_TOTAL], (uint32_t)nh);
@@ -695,7 +696,7 @@ __global__ void __launch_bounds__(kThreads) k_ovf_count(const float4* __restrict
         float4 A, B, C;
         load_tri(tris, k, A, B, C);
         double t64;
-        if (mt64(r, A, B, C, &t64) && nh < cap) v[nh++] = t64;
+        if (mt64(r, E + 3 * i, A, B, C, &t64) && nh < cap) v[nh++] = t64;
         return false;
     });
     // heap sort v[0..nh)
@@ -863,7 +864,7 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     p.tris = h->tris;
     p.S = S;
     p.E = E;
-    p.n = n;
+    p.n = (int)n;
     p.hit = out->hit;
     p.tri = out->tri;
     p.t = out->t;
@@ -874,7 +875,7 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     p.ovf_list = h->ovf_list;
     p.scratch = h->scratch;
     p.stats = h->stats;
-    p.counter = reinterpret_cast<unsigned long long*>(h->scratch + SCR_DISPENSER);
+    p.counter = h->scratch + SCR_DISPENSER;
     p.min_trav = h->min_trav;
     p.spec = h->spec;
     const bool fp64 = (h->opt.flags & RSI_OPT_FP64_MOLLER) != 0, ctr = (h->opt.flags & RSI_OPT_COUNTERS) != 0;

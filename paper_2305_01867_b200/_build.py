@@ -49,3 +49,11 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
     return LIB
+
+
+def build_variant(name: str, defines: dict) -> str:
+    """Build lib/librsi_<name>.so with extra -D defines (tuning sweeps only)."""
+    out = os.path.join(LIB_DIR, f"librsi_{name}.so")
+    cmd = [_nvcc(), *NVCC_FLAGS, *[f"-D{k}={v}" for k, v in defines.items()], "-o", out, *SOURCES]
+    subprocess.check_call(cmd)
+    return out

@@ -28,6 +28,12 @@ constexpr float kTiny = 1e-30f;                  // absolute floor (underflow)
 constexpr float kOutTol = 4e-6f;                 // max certified |t error| for fp32 outputs
 constexpr int kStack = 64;
 constexpr int kCountCap = 8;  // intercept_count hits held in registers per ray
+#ifndef RSI_BOOL_MINB
+#define RSI_BOOL_MINB 8
+#endif
+#ifndef RSI_OTHER_MINB
+#define RSI_OTHER_MINB 6
+#endif
 constexpr int kThreads = 128;
 constexpr int kChunk = 64;   // rays a warp takes from the global dispenser at once
 
@@ -524,7 +530,7 @@ struct ModeState<MODE_COUNT> {
 //   3. leaf phase: all lanes with pending leaves run Moller-Trumbore together;
 //   4. finished rays write their outputs and free the lane.
 template <int MODE, bool kFP64, bool kCounters>
-__global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? 8 : 6) k_trace(const TraceParams p) {
+__global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : RSI_OTHER_MINB) k_trace(const TraceParams p) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();

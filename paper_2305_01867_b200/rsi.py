@@ -64,10 +64,11 @@ def load():
     with _lock:
         if _lib is not None:
             return _lib
-        if not os.path.exists(_build.LIB):
+        path = os.environ.get("RSI_LIB", _build.LIB)  # variant builds for tuning sweeps
+        if not os.path.exists(path):
             raise RuntimeError(f"{_build.LIB} is missing: run __graft_entry__.build() "
                                "(nvcc sm_100a); there is no CPU fallback")
-        lib = ctypes.CDLL(_build.LIB)
+        lib = ctypes.CDLL(path)
         sig = {
             "rsi_version": ([], ctypes.c_char_p),
             "rsi_last_error": ([], ctypes.c_char_p),

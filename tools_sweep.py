@@ -11,7 +11,7 @@ V, T, S, E, _ = synth.workload(wl, n, seed=3)
 dev = torch.device("cuda:0")
 Vd, Td, Sd, Ed = (torch.from_numpy(a).to(dev) for a in (V, T, S, E))
 res = {}
-for cfg in os.environ.get("CFGS", "8:1,8:2,4:2,16:2").split(","):
+for cfg in os.environ.get("CFGS", "8:2").split(","):
     mt, sp = cfg.split(":")
     os.environ["RSI_MIN_TRAV"] = mt
     os.environ["RSI_SPEC"] = sp
@@ -27,8 +27,10 @@ for cfg in os.environ.get("CFGS", "8:1,8:2,4:2,16:2").split(","):
             rsi.rsi_intersect(h, Sd, Ed, mode, out=out)
         e1.record(); torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 5
-        res[f"{mode}/min_trav={mt},spec={sp}"] = {"ms": round(ms, 3), "Grays_s": round(n / ms / 1e6, 3)}
+        res[f"{os.path.basename(os.environ.get('RSI_LIB', 'default'))}:{mode}/min_trav={mt},spec={sp}"] = {"ms": round(ms, 3), "Grays_s": round(n / ms / 1e6, 3)}
     h.free()
+if os.environ.get("COUNTERS", "1") == "0":
+    [print(k, json.dumps(v)) for k, v in res.items()]; sys.exit(0)
 hc = rsi.rsi_build(Vd, Td, rsi.Options(counters=True))
 for mode in ("boolean", "barycentric", "intercept_count"):
     rsi.rsi_reset_stats(hc)

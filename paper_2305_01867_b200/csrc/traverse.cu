@@ -39,20 +39,30 @@ constexpr int kChunk = 64;   // rays a warp takes from the global dispenser at o
 
 enum { MT_MISS = 0, MT_HIT = 1, MT_UNSURE = 2 };
 
+#ifndef RSI_SLAB_2OFF
+#define RSI_SLAB_2OFF 0
+#endif
 struct Ray {
     float ox, oy, oz;  // start (r^start)
     float dx, dy, dz;  // d = end - start (fp32); the end point itself is re-read for the fp64 mirror
     float ix, iy, iz;  // slab: 1/d per axis (0 on an unconstrained axis)
+#if RSI_SLAB_2OFF
+    float lx, ly, lz;  // slab: o/d + slack*sign(d): offset of the box's lo planes
+    float hx, hy, hz;  // slab: o/d - slack*sign(d): offset of the box's hi planes
+#else
     float qx, qy, qz;  // slab: o/d per axis (NaN on an unconstrained axis)
     float S;           // slab slack: 2 x the largest per-axis error bound (t units)
+#endif
 };
 
 // Per-axis slab setup.  t = fma(plane, inv, -o/d) approximates (plane - o)/d
 // with an absolute error below slack = 2^-21 (1 + |o/d|) for |t| <= ~1 (the
-// only range where a decision is taken).  The box test accepts when
-//   max(t_near, 0) - S <= min(t_far, tclip),  S = 2 max_axis slack,
-// so it never rejects a box the exact segment touches.  Axes with |d| < 1e-30
-// or slack > 2^-9 impose no constraint (inv = 0, o/d = NaN: min/max ignore NaN).
+// only range where a decision is taken).  Either the slack is folded into
+// separate lo/hi plane offsets so entry t is lowered and exit t raised
+// (RSI_SLAB_2OFF), or the box test accepts when
+//   max(t_near, 0) - S <= min(t_far, tclip),  S = 2 max_axis slack.
+// Either way it never rejects a box the exact segment touches.  Axes with
+// |d| < 1e-30 or slack > 2^-9 impose no constraint.
 __device__ __forceinline__ void slab_axis(float o, float d, float& inv, float& oinv, float& slack) {
     if (fabsf(d) >= 1e-30f) {
         inv = 1.0f / d;
@@ -61,7 +71,7 @@ __device__ __forceinline__ void slab_axis(float o, float d, float& inv, float& o
         if (slack <= kSlackMax) return;  // also false for NaN / Inf
     }
     inv = 0.0f;
-    oinv = __int_as_float(0x7fffffff);  // NaN
+    oinv = __int_as_float(0x7fffffff);  // NaN: min/max ignore this axis
     slack = 0.0f;
 }
 
@@ -78,23 +88,50 @@ __device__ __forceinline__ bool load_ray(Ray& r, const float* __restrict__ S, co
     r.dx = ex - r.ox;
     r.dy = ey - r.oy;
     r.dz = ez - r.oz;
+#if RSI_SLAB_2OFF
+    float q, sl;
+    slab_axis(r.ox, r.dx, r.ix, q, sl);
+    sl = r.ix > 0.0f ? sl : -sl;
+    r.lx = r.ix != 0.0f ? q + sl : -INFINITY;
+    r.hx = r.ix != 0.0f ? q - sl : INFINITY;
+    slab_axis(r.oy, r.dy, r.iy, q, sl);
+    sl = r.iy > 0.0f ? sl : -sl;
+    r.ly = r.iy != 0.0f ? q + sl : -INFINITY;
+    r.hy = r.iy != 0.0f ? q - sl : INFINITY;
+    slab_axis(r.oz, r.dz, r.iz, q, sl);
+    sl = r.iz > 0.0f ? sl : -sl;
+    r.lz = r.iz != 0.0f ? q + sl : -INFINITY;
+    r.hz = r.iz != 0.0f ? q - sl : INFINITY;
+#else
     float sx, sy, sz;
     slab_axis(r.ox, r.dx, r.ix, r.qx, sx);
     slab_axis(r.oy, r.dy, r.iy, r.qy, sy);
     slab_axis(r.oz, r.dz, r.iz, r.qz, sz);
     r.S = 2.0f * fmaxf(sx, fmaxf(sy, sz));
+#endif
     return !nonfinite && !(r.dx == 0.0f && r.dy == 0.0f && r.dz == 0.0f);
 }
 
 // Conservative segment/box overlap on [0, tclip]; tnear is the entry t.
 __device__ __forceinline__ bool slab(const Ray& r, float lox, float hix, float loy, float hiy, float loz, float hiz,
                                      float tclip, float& tnear) {
+#if RSI_SLAB_2OFF
+    // unconstrained axis: inv = 0 with offsets -inf / +inf gives t = +inf on the lo plane and
+    // -inf on the hi plane, so the axis interval is (-inf, +inf).
+    const float tx1 = fmaf(lox, r.ix, -r.lx), tx2 = fmaf(hix, r.ix, -r.hx);
+    const float ty1 = fmaf(loy, r.iy, -r.ly), ty2 = fmaf(hiy, r.iy, -r.hy);
+    const float tz1 = fmaf(loz, r.iz, -r.lz), tz2 = fmaf(hiz, r.iz, -r.hz);
+    tnear = fmaxf(fmaxf(fminf(tx1, tx2), fminf(ty1, ty2)), fmaxf(fminf(tz1, tz2), 0.0f));
+    const float tfar = fminf(fminf(fmaxf(tx1, tx2), fmaxf(ty1, ty2)), fminf(fmaxf(tz1, tz2), tclip));
+    return tnear <= tfar;
+#else
     const float tx1 = fmaf(lox, r.ix, -r.qx), tx2 = fmaf(hix, r.ix, -r.qx);
     const float ty1 = fmaf(loy, r.iy, -r.qy), ty2 = fmaf(hiy, r.iy, -r.qy);
     const float tz1 = fmaf(loz, r.iz, -r.qz), tz2 = fmaf(hiz, r.iz, -r.qz);
     tnear = fmaxf(fmaxf(fminf(tx1, tx2), fminf(ty1, ty2)), fminf(tz1, tz2));
     const float tfar = fminf(fminf(fmaxf(tx1, tx2), fmaxf(ty1, ty2)), fmaxf(tz1, tz2));
     return fmaxf(tnear - r.S, -r.S) <= fminf(tfar, tclip);
+#endif
 }
 
 // ---------------------------------------------------------------- fp32 MT + error filter

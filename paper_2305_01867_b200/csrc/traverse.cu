@@ -265,11 +265,23 @@ __device__ __forceinline__ void traverse(const float4* __restrict__ nodes, const
     }
 }
 
-// Block-level counters in shared memory (rare events), flushed once per block.
+#ifndef RSI_SMEM_STATS
+#define RSI_SMEM_STATS 0
+#endif
+#ifndef RSI_QUEUE
+#define RSI_QUEUE 0
+#endif
+// Per-thread counters of rare events, reduced per warp at kernel end
+// (RSI_SMEM_STATS=1: block-level shared-memory atomics instead).
 struct Stats {
+#if RSI_SMEM_STATS
     unsigned* s;  // shared [ST_WORDS]
-    unsigned boxes = 0, mts = 0;  // RSI_OPT_COUNTERS only
     __device__ __forceinline__ void add(int k, unsigned v = 1) { atomicAdd(s + k, v); }
+#else
+    unsigned c[ST_WORDS] = {};
+    __device__ __forceinline__ void add(int k, unsigned v = 1) { c[k] += v; }
+#endif
+    unsigned boxes = 0, mts = 0;  // RSI_OPT_COUNTERS only
 };
 
 // Decide one (ray, leaf) pair: MT_MISS, or MT_HIT with either (t32, et) or an
@@ -571,13 +583,15 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
-    __shared__ unsigned s_stats[ST_WORDS];
     __shared__ float2 s_te[MODE == MODE_COUNT ? kCountCap * kThreads : 1];
     __shared__ int s_k[MODE == MODE_COUNT ? kCountCap * kThreads : 1];
+    Stats st;
+#if RSI_SMEM_STATS
+    __shared__ unsigned s_stats[ST_WORDS];
     if (threadIdx.x < ST_WORDS) s_stats[threadIdx.x] = 0u;
     __syncthreads();
-    Stats st;
     st.s = s_stats;
+#endif
     int cnext = 0, cend = 0;  // warp-uniform chunk [cnext, cend)
     bool exhausted = false;   // warp-uniform
     int ray = -1;
@@ -625,11 +639,13 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             tclip = 1.0f;
             sp = 0;
             npend = 0;
+            l0 = l1 = -1;
             node = ok ? 0 : -1;
         }
         if (__ballot_sync(FULL, ray >= 0) == 0) break;  // no rays left for this warp
 
         // ---- 2. traversal phase
+#if RSI_QUEUE
         while (true) {
             const bool searching = node >= 0 && npend == 0;
             const unsigned sm = __ballot_sync(FULL, searching);
@@ -679,9 +695,60 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             npend = 0;
             if (done) node = -1;
         }
+#else
+        // a lane walks internal nodes until it holds a pending leaf (l0, and l1
+        // when both children of the visited node are leaves)
+        while (true) {
+            const bool trav = node >= 0 && l0 < 0;
+            const unsigned tm = __ballot_sync(FULL, trav);
+            if (tm == 0) break;
+            if (__popc(tm) < p.min_trav && __ballot_sync(FULL, l0 >= 0)) break;
+            if (trav) {
+                const float4* nd = p.nodes + 4 * node;
+                const float4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2);
+                const int4 n3 = __ldg(reinterpret_cast<const int4*>(nd + 3));
+                float nearL, nearR;
+                bool hL = slab(r, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, tclip, nearL);
+                bool hR = slab(r, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, tclip, nearR);
+                if (kCounters) st.boxes += 2;
+                if (hL && n3.x < 0) {
+                    l0 = ~n3.x;
+                    hL = false;
+                }
+                if (hR && n3.y < 0) {
+                    if (l0 < 0)
+                        l0 = ~n3.y;
+                    else
+                        l1 = ~n3.y;
+                    hR = false;
+                }
+                if (hL && hR) {
+                    const bool rfirst = nearR < nearL;
+                    stack[sp++] = rfirst ? n3.x : n3.y;
+                    node = rfirst ? n3.y : n3.x;
+                } else if (hL) {
+                    node = n3.x;
+                } else if (hR) {
+                    node = n3.y;
+                } else {
+                    node = sp > 0 ? stack[--sp] : -1;
+                }
+            }
+        }
+
+        // ---- 3. leaf phase
+        if (l0 >= 0) {
+            const float* e3 = p.E + 3 * (int64_t)ray;
+            if (kCounters) st.mts += 1 + (l1 >= 0);
+            bool done = ms.template leaf<kFP64>(p, r, e3, l0, tclip, st);
+            if (!done && l1 >= 0) done = ms.template leaf<kFP64>(p, r, e3, l1, tclip, st);
+            l0 = l1 = -1;
+            if (done) node = -1;
+        }
+#endif
 
         // ---- 4. finish
-        if (ray >= 0 && node < 0 && npend == 0) {
+        if (ray >= 0 && node < 0 && npend == 0 && l0 < 0) {
             ms.finish(p, r, p.E + 3 * (int64_t)ray, ray, st);
             ray = -1;
         }
@@ -690,8 +757,19 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
         st.add(ST_BOX_TESTS, st.boxes);
         st.add(ST_MT_TESTS, st.mts);
     }
+#if RSI_SMEM_STATS
     __syncthreads();
     if (threadIdx.x < ST_WORDS && s_stats[threadIdx.x]) atomicAdd(p.stats + threadIdx.x, (unsigned long long)s_stats[threadIdx.x]);
+#else
+#pragma unroll
+    for (int k = 1; k < ST_WORDS; ++k) {
+        unsigned v = st.c[k];
+        if (__any_sync(FULL, v)) {
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+            if (lane == 0 && v) atomicAdd(p.stats + k, (unsigned long long)v);
+        }
+    }
+#endif
 }
 
 // ---------------------------------------------------------------- exact re-pass for overflowed rays

@@ -39,40 +39,33 @@ constexpr int kChunk = 64;   // rays a warp takes from the global dispenser at o
 
 enum { MT_MISS = 0, MT_HIT = 1, MT_UNSURE = 2 };
 
-#ifndef RSI_SLAB_2OFF
-#define RSI_SLAB_2OFF 0
-#endif
 struct Ray {
     float ox, oy, oz;  // start (r^start)
-    float dx, dy, dz;  // d = end - start (fp32); the end point itself is re-read for the fp64 mirror
-    float ix, iy, iz;  // slab: 1/d per axis (0 on an unconstrained axis)
-#if RSI_SLAB_2OFF
-    float lx, ly, lz;  // slab: o/d + slack*sign(d): offset of the box's lo planes
-    float hx, hy, hz;  // slab: o/d - slack*sign(d): offset of the box's hi planes
-#else
-    float qx, qy, qz;  // slab: o/d per axis (NaN on an unconstrained axis)
-    float S;           // slab slack: 2 x the largest per-axis error bound (t units)
-#endif
+    float ex, ey, ez;  // end (r^end), kept exactly for the fp64 mirror
+    float dx, dy, dz;  // d = end - start (fp32)
+    float ix, iy, iz;  // slab: 1/d per axis (0 on degenerate axes)
+    float lx, ly, lz;  // slab offsets applied to the box's lo plane
+    float hx, hy, hz;  // slab offsets applied to the box's hi plane
 };
 
-// Per-axis slab setup.  t = fma(plane, inv, -o/d) approximates (plane - o)/d
-// with an absolute error below slack = 2^-21 (1 + |o/d|) for |t| <= ~1 (the
-// only range where a decision is taken).  Either the slack is folded into
-// separate lo/hi plane offsets so entry t is lowered and exit t raised
-// (RSI_SLAB_2OFF), or the box test accepts when
-//   max(t_near, 0) - S <= min(t_far, tclip),  S = 2 max_axis slack.
-// Either way it never rejects a box the exact segment touches.  Axes with
-// |d| < 1e-30 or slack > 2^-9 impose no constraint.
-__device__ __forceinline__ void slab_axis(float o, float d, float& inv, float& oinv, float& slack) {
+// Per-axis slab setup.  t = fma(plane, inv, -off) approximates (plane - o)/d;
+// the slack (2^-21 * (1 + |o/d|)) exceeds the fp32 error of that expression
+// for |t| <= ~1, and is applied so the computed entry t is never later and the
+// exit t never earlier than the exact ones: the test never rejects a box the
+// exact segment touches.  |d| < 1e-30 (incl. 0): the axis imposes no constraint.
+__device__ __forceinline__ void slab_axis(float o, float d, float& inv, float& offlo, float& offhi) {
     if (fabsf(d) >= 1e-30f) {
         inv = 1.0f / d;
-        oinv = o * inv;
-        slack = kSlack * (1.0f + fabsf(oinv));
-        if (slack <= kSlackMax) return;  // also false for NaN / Inf
+        float oinv = o * inv;
+        float slack = kSlack * (1.0f + fabsf(oinv));
+        float sg = inv > 0.0f ? slack : -slack;
+        offlo = oinv + sg;
+        offhi = oinv - sg;
+        if (isfinite(offlo) && isfinite(offhi)) return;
     }
     inv = 0.0f;
-    oinv = __int_as_float(0x7fffffff);  // NaN: min/max ignore this axis
-    slack = 0.0f;
+    offlo = INFINITY;
+    offhi = -INFINITY;
 }
 
 // Returns false for rays that cannot hit: zero length or a non-finite coordinate
@@ -82,56 +75,29 @@ __device__ __forceinline__ bool load_ray(Ray& r, const float* __restrict__ S, co
     r.ox = __ldg(S + 3 * i);
     r.oy = __ldg(S + 3 * i + 1);
     r.oz = __ldg(S + 3 * i + 2);
-    const float ex = __ldg(E + 3 * i), ey = __ldg(E + 3 * i + 1), ez = __ldg(E + 3 * i + 2);
-    nonfinite = !(isfinite(r.ox) && isfinite(r.oy) && isfinite(r.oz) && isfinite(ex) && isfinite(ey) &&
-                  isfinite(ez));
-    r.dx = ex - r.ox;
-    r.dy = ey - r.oy;
-    r.dz = ez - r.oz;
-#if RSI_SLAB_2OFF
-    float q, sl;
-    slab_axis(r.ox, r.dx, r.ix, q, sl);
-    sl = r.ix > 0.0f ? sl : -sl;
-    r.lx = r.ix != 0.0f ? q + sl : -INFINITY;
-    r.hx = r.ix != 0.0f ? q - sl : INFINITY;
-    slab_axis(r.oy, r.dy, r.iy, q, sl);
-    sl = r.iy > 0.0f ? sl : -sl;
-    r.ly = r.iy != 0.0f ? q + sl : -INFINITY;
-    r.hy = r.iy != 0.0f ? q - sl : INFINITY;
-    slab_axis(r.oz, r.dz, r.iz, q, sl);
-    sl = r.iz > 0.0f ? sl : -sl;
-    r.lz = r.iz != 0.0f ? q + sl : -INFINITY;
-    r.hz = r.iz != 0.0f ? q - sl : INFINITY;
-#else
-    float sx, sy, sz;
-    slab_axis(r.ox, r.dx, r.ix, r.qx, sx);
-    slab_axis(r.oy, r.dy, r.iy, r.qy, sy);
-    slab_axis(r.oz, r.dz, r.iz, r.qz, sz);
-    r.S = 2.0f * fmaxf(sx, fmaxf(sy, sz));
-#endif
+    r.ex = __ldg(E + 3 * i);
+    r.ey = __ldg(E + 3 * i + 1);
+    r.ez = __ldg(E + 3 * i + 2);
+    nonfinite = !(isfinite(r.ox) && isfinite(r.oy) && isfinite(r.oz) && isfinite(r.ex) && isfinite(r.ey) &&
+                  isfinite(r.ez));
+    r.dx = r.ex - r.ox;
+    r.dy = r.ey - r.oy;
+    r.dz = r.ez - r.oz;
+    slab_axis(r.ox, r.dx, r.ix, r.lx, r.hx);
+    slab_axis(r.oy, r.dy, r.iy, r.ly, r.hy);
+    slab_axis(r.oz, r.dz, r.iz, r.lz, r.hz);
     return !nonfinite && !(r.dx == 0.0f && r.dy == 0.0f && r.dz == 0.0f);
 }
 
-// Conservative segment/box overlap on [0, tclip]; tnear is the entry t.
+// Conservative segment/box overlap on [0, tclip]; tnear is the (lowered) entry t.
 __device__ __forceinline__ bool slab(const Ray& r, float lox, float hix, float loy, float hiy, float loz, float hiz,
                                      float tclip, float& tnear) {
-#if RSI_SLAB_2OFF
-    // unconstrained axis: inv = 0 with offsets -inf / +inf gives t = +inf on the lo plane and
-    // -inf on the hi plane, so the axis interval is (-inf, +inf).
-    const float tx1 = fmaf(lox, r.ix, -r.lx), tx2 = fmaf(hix, r.ix, -r.hx);
-    const float ty1 = fmaf(loy, r.iy, -r.ly), ty2 = fmaf(hiy, r.iy, -r.hy);
-    const float tz1 = fmaf(loz, r.iz, -r.lz), tz2 = fmaf(hiz, r.iz, -r.hz);
+    float tx1 = fmaf(lox, r.ix, -r.lx), tx2 = fmaf(hix, r.ix, -r.hx);
+    float ty1 = fmaf(loy, r.iy, -r.ly), ty2 = fmaf(hiy, r.iy, -r.hy);
+    float tz1 = fmaf(loz, r.iz, -r.lz), tz2 = fmaf(hiz, r.iz, -r.hz);
     tnear = fmaxf(fmaxf(fminf(tx1, tx2), fminf(ty1, ty2)), fmaxf(fminf(tz1, tz2), 0.0f));
-    const float tfar = fminf(fminf(fmaxf(tx1, tx2), fmaxf(ty1, ty2)), fminf(fmaxf(tz1, tz2), tclip));
+    float tfar = fminf(fminf(fmaxf(tx1, tx2), fmaxf(ty1, ty2)), fminf(fmaxf(tz1, tz2), tclip));
     return tnear <= tfar;
-#else
-    const float tx1 = fmaf(lox, r.ix, -r.qx), tx2 = fmaf(hix, r.ix, -r.qx);
-    const float ty1 = fmaf(loy, r.iy, -r.qy), ty2 = fmaf(hiy, r.iy, -r.qy);
-    const float tz1 = fmaf(loz, r.iz, -r.qz), tz2 = fmaf(hiz, r.iz, -r.qz);
-    tnear = fmaxf(fmaxf(fminf(tx1, tx2), fminf(ty1, ty2)), fminf(tz1, tz2));
-    const float tfar = fminf(fminf(fmaxf(tx1, tx2), fmaxf(ty1, ty2)), fmaxf(tz1, tz2));
-    return fmaxf(tnear - r.S, -r.S) <= fminf(tfar, tclip);
-#endif
 }
 
 // ---------------------------------------------------------------- fp32 MT + error filter
@@ -191,11 +157,9 @@ __device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b
 __device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double ds(double a, double b) { return __dsub_rn(a, b); }
 
-// `e3` points at this segment's end point (r^end) in the caller's array.
-__device__ __noinline__ int mt64(const Ray& r, const float* __restrict__ e3, const float4 A, const float4 B,
-                                 const float4 C, double* t_out) {
+__device__ __noinline__ int mt64(const Ray& r, const float4 A, const float4 B, const float4 C, double* t_out) {
     const double Ox = r.ox, Oy = r.oy, Oz = r.oz;
-    const double dx = ds((double)__ldg(e3), Ox), dy = ds((double)__ldg(e3 + 1), Oy), dz = ds((double)__ldg(e3 + 2), Oz);
+    const double dx = ds((double)r.ex, Ox), dy = ds((double)r.ey, Oy), dz = ds((double)r.ez, Oz);
     const double Ax = A.x, Ay = A.y, Az = A.z;
     const double e1x = ds(B.x, Ax), e1y = ds(B.y, Ay), e1z = ds(B.z, Az);
     const double e2x = ds(C.x, Ax), e2y = ds(C.y, Ay), e2z = ds(C.z, Az);
@@ -287,7 +251,7 @@ struct Stats {
 // Decide one (ray, leaf) pair: MT_MISS, or MT_HIT with either (t32, et) or an
 // exact t64 (is64 = true).
 template <bool kFP64>
-__device__ __forceinline__ int decide(const Ray& r, const float* e3, const float4& A, const float4& B,
+__device__ __forceinline__ int decide(const Ray& r, const float4& A, const float4& B,
                                       const float4& C, float& t32, float& et, double& t64, bool& is64, Stats& st) {
     if (!kFP64) {
         int s = mt32(r, A, B, C, t32, et);
@@ -298,7 +262,7 @@ __device__ __forceinline__ int decide(const Ray& r, const float* e3, const float
         st.add(ST_FP64_PAIRS);
     }
     is64 = true;
-    return mt64(r, e3, A, B, C, &t64) ? MT_HIT : MT_MISS;
+    return mt64(r, A, B, C, &t64) ? MT_HIT : MT_MISS;
 }
 
 __device__ __forceinline__ uint32_t lanemask_lt() {
@@ -317,7 +281,7 @@ struct TraceParams {
     const float4* tris;
     const float* S;
     const float* E;
-    int n;
+    int64_t n;
     uint8_t* hit;
     int32_t* tri;
     float* t;
@@ -328,7 +292,7 @@ struct TraceParams {
     int32_t* ovf_list;
     uint32_t* scratch;
     unsigned long long* stats;
-    unsigned int* counter;  // persistent-grid ray dispenser
+    unsigned long long* counter;  // persistent-grid ray dispenser
     int min_trav;           // leave the traversal phase when fewer lanes still search
     int spec;               // max pending leaves while traversing (1 = no speculation)
 };
@@ -341,17 +305,17 @@ struct ModeState<MODE_BOOL> {
     bool found;
     __device__ __forceinline__ void init() { found = false; }
     template <bool kFP64>
-    __device__ __forceinline__ bool leaf(const TraceParams& p, const Ray& r, const float* e3, int k, float& tclip,
+    __device__ __forceinline__ bool leaf(const TraceParams& p, const Ray& r, int k, float& tclip,
                                          Stats& st) {
         float4 A, B, C;
         load_tri(p.tris, k, A, B, C);
         float t32, et;
         double t64;
         bool is64;
-        found = decide<kFP64>(r, e3, A, B, C, t32, et, t64, is64, st) == MT_HIT;
+        found = decide<kFP64>(r, A, B, C, t32, et, t64, is64, st) == MT_HIT;
         return found;  // any-hit early exit
     }
-    __device__ __forceinline__ void finish(const TraceParams& p, const Ray&, const float*, int i, Stats&) {
+    __device__ __forceinline__ void finish(const TraceParams& p, const Ray&, int64_t i, Stats&) {
         p.hit[i] = found ? 1 : 0;
     }
 };
@@ -373,14 +337,14 @@ struct ModeState<MODE_BARY> {
         t64 = 0.0;
     }
     template <bool kFP64>
-    __device__ __forceinline__ bool leaf(const TraceParams& p, const Ray& r, const float* e3, int k, float& tclip,
+    __device__ __forceinline__ bool leaf(const TraceParams& p, const Ray& r, int k, float& tclip,
                                          Stats& st) {
         float4 A, B, C;
         load_tri(p.tris, k, A, B, C);
         float t32, et;
         double c64;
         bool c_is64;
-        if (decide<kFP64>(r, e3, A, B, C, t32, et, c64, c_is64, st) != MT_HIT) return false;
+        if (decide<kFP64>(r, A, B, C, t32, et, c64, c_is64, st) != MT_HIT) return false;
         const int cid = __float_as_int(A.w);
         bool take;
         if (slot < 0) {
@@ -395,13 +359,13 @@ struct ModeState<MODE_BARY> {
             } else {  // order not certified: settle both in the fp64 mirror
                 st.add(ST_FP64_RAYS);
                 if (!c_is64) {
-                    mt64(r, e3, A, B, C, &c64);
+                    mt64(r, A, B, C, &c64);
                     c_is64 = true;
                 }
                 if (!is64) {
                     float4 bA, bB, bC;
                     load_tri(p.tris, slot, bA, bB, bC);
-                    mt64(r, e3, bA, bB, bC, &t64);
+                    mt64(r, bA, bB, bC, &t64);
                     is64 = true;
                 }
                 take = (c64 < t64) || (c64 == t64 && cid < id);
@@ -422,7 +386,7 @@ struct ModeState<MODE_BARY> {
         }
         return false;
     }
-    __device__ __forceinline__ void finish(const TraceParams& p, const Ray& r, const float* e3, int i, Stats& st) {
+    __device__ __forceinline__ void finish(const TraceParams& p, const Ray& r, int64_t i, Stats& st) {
         if (slot >= 0) {
             float tt;
             if (is64) {
@@ -433,7 +397,7 @@ struct ModeState<MODE_BARY> {
                 float4 bA, bB, bC;
                 load_tri(p.tris, slot, bA, bB, bC);
                 double v = 0.0;
-                mt64(r, e3, bA, bB, bC, &v);
+                mt64(r, bA, bB, bC, &v);
                 tt = (float)v;
                 st.add(ST_FP64_RAYS);
             }
@@ -487,14 +451,14 @@ struct ModeState<MODE_COUNT> {
         overflow = false;
     }
     template <bool kFP64>
-    __device__ __forceinline__ bool leaf(const TraceParams& p, const Ray& r, const float* e3, int k, float& tclip,
+    __device__ __forceinline__ bool leaf(const TraceParams& p, const Ray& r, int k, float& tclip,
                                          Stats& st) {
         float4 A, B, C;
         load_tri(p.tris, k, A, B, C);
         float t32, et;
         double t64;
         bool is64;
-        if (decide<kFP64>(r, e3, A, B, C, t32, et, t64, is64, st) != MT_HIT) return false;
+        if (decide<kFP64>(r, A, B, C, t32, et, t64, is64, st) != MT_HIT) return false;
         if (nh == kCountCap) {
             overflow = true;
             return true;
@@ -508,7 +472,7 @@ struct ModeState<MODE_COUNT> {
         ++nh;
         return false;
     }
-    __device__ __forceinline__ void finish(const TraceParams& p, const Ray& r, const float* e3, int i, Stats& st) {
+    __device__ __forceinline__ void finish(const TraceParams& p, const Ray& r, int64_t i, Stats& st) {
         if (overflow) {
             uint32_t pos = atomicAdd(&p.scratch[SCR_OVF_COUNT], 1u);
             p.ovf_list[pos] = (int32_t)i;
@@ -558,7 +522,7 @@ struct ModeState<MODE_COUNT> {
             for (int a = 0; a < nh; ++a) {
                 float4 A, B, C;
                 load_tri(p.tris, kk[a * kThreads], A, B, C);
-                mt64(r, e3, A, B, C, &v[a]);
+                mt64(r, A, B, C, &v[a]);
             }
             sort_small(v, nh);
             for (int a = 0; a + 1 < nh; ++a)
@@ -592,9 +556,9 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
     __syncthreads();
     st.s = s_stats;
 #endif
-    int cnext = 0, cend = 0;  // warp-uniform chunk [cnext, cend)
-    bool exhausted = false;   // warp-uniform
-    int ray = -1;
+    int64_t cnext = 0, cend = 0;  // warp-uniform chunk [cnext, cend)
+    bool exhausted = false;       // warp-uniform
+    int64_t ray = -1;
     Ray r;
     int node = -1, sp = 0, npend = 0, l0 = -1, l1 = -1, l2 = -1;  // pending (postponed) leaves
     int stack[kStack];
@@ -610,17 +574,17 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
         bool fresh = false;
         while (want && !exhausted) {
             if (cnext >= cend) {
-                unsigned base = 0;
-                if (lane == 0) base = atomicAdd(p.counter, (unsigned)kChunk);
+                unsigned long long base = 0;
+                if (lane == 0) base = atomicAdd(p.counter, (unsigned long long)kChunk);
                 base = __shfl_sync(FULL, base, 0);
-                if (base >= (unsigned)p.n) {
+                if ((int64_t)base >= p.n) {
                     exhausted = true;
                     break;
                 }
-                cnext = (int)base;
-                cend = min((int)base + kChunk, p.n);
+                cnext = (int64_t)base;
+                cend = min((int64_t)base + kChunk, p.n);
             }
-            const int take = min(__popc(want), cend - cnext);
+            const int take = (int)min((int64_t)__popc(want), cend - cnext);
             const bool mine = (want >> lane) & 1u;
             const int rank = __popc(want & lt);
             const bool got = mine && rank < take;
@@ -687,11 +651,10 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
 
         // ---- 3. leaf phase
         if (npend > 0) {
-            const float* e3 = p.E + 3 * (int64_t)ray;
             if (kCounters) st.mts += npend;
-            bool done = ms.template leaf<kFP64>(p, r, e3, l0, tclip, st);
-            if (!done && npend > 1) done = ms.template leaf<kFP64>(p, r, e3, l1, tclip, st);
-            if (!done && npend > 2) done = ms.template leaf<kFP64>(p, r, e3, l2, tclip, st);
+            bool done = ms.template leaf<kFP64>(p, r, l0, tclip, st);
+            if (!done && npend > 1) done = ms.template leaf<kFP64>(p, r, l1, tclip, st);
+            if (!done && npend > 2) done = ms.template leaf<kFP64>(p, r, l2, tclip, st);
             npend = 0;
             if (done) node = -1;
         }
@@ -738,10 +701,9 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
 
         // ---- 3. leaf phase
         if (l0 >= 0) {
-            const float* e3 = p.E + 3 * (int64_t)ray;
             if (kCounters) st.mts += 1 + (l1 >= 0);
-            bool done = ms.template leaf<kFP64>(p, r, e3, l0, tclip, st);
-            if (!done && l1 >= 0) done = ms.template leaf<kFP64>(p, r, e3, l1, tclip, st);
+            bool done = ms.template leaf<kFP64>(p, r, l0, tclip, st);
+            if (!done && l1 >= 0) done = ms.template leaf<kFP64>(p, r, l1, tclip, st);
             l0 = l1 = -1;
             if (done) node = -1;
         }
@@ -749,7 +711,7 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
 
         // ---- 4. finish
         if (ray >= 0 && node < 0 && npend == 0 && l0 < 0) {
-            ms.finish(p, r, p.E + 3 * (int64_t)ray, ray, st);
+            ms.finish(p, r, ray, st);
             ray = -1;
         }
     }
@@ -790,7 +752,7 @@ __global__ void __launch_bounds__(kThreads) k_ovf_size(const float4* __restrict_
         load_tri(tris, k, A, B, C);
         float t32, et;
         int s = mt32(r, A, B, C, t32, et);
-        if (s == MT_HIT || (s == MT_UNSURE && mt64(r, E + 3 * (int64_t)list[j], A, B, C, nullptr))) ++nh;
+        if (s == MT_HIT || (s == MT_UNSURE && mt64(r, A, B, C, nullptr))) ++nh;
         return false;
     });
     seg[2 * j] = (int32_t)atomicAdd(&scratch[SCR_OVF_TOTAL], (uint32_t)nh);
@@ -817,7 +779,7 @@ __global__ void __launch_bounds__(kThreads) k_ovf_count(const float4* __restrict
         float4 A, B, C;
         load_tri(tris, k, A, B, C);
         double t64;
-        if (mt64(r, E + 3 * i, A, B, C, &t64) && nh < cap) v[nh++] = t64;
+        if (mt64(r, A, B, C, &t64) && nh < cap) v[nh++] = t64;
         return false;
     });
     // heap sort v[0..nh)
@@ -985,7 +947,7 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     p.tris = h->tris;
     p.S = S;
     p.E = E;
-    p.n = (int)n;
+    p.n = n;
     p.hit = out->hit;
     p.tri = out->tri;
     p.t = out->t;
@@ -996,7 +958,7 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     p.ovf_list = h->ovf_list;
     p.scratch = h->scratch;
     p.stats = h->stats;
-    p.counter = h->scratch + SCR_DISPENSER;
+    p.counter = reinterpret_cast<unsigned long long*>(h->scratch + SCR_DISPENSER);
     p.min_trav = h->min_trav;
     p.spec = h->spec;
     const bool fp64 = (h->opt.flags & RSI_OPT_FP64_MOLLER) != 0, ctr = (h->opt.flags & RSI_OPT_COUNTERS) != 0;

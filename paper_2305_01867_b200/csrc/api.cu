@@ -66,7 +66,6 @@ rsi_status_t rsi_build(const float* d_vertices, int64_t n_vertices, const int32_
     if (!h) return rsi_set_error(RSI_E_OOM, "host allocation failed");
     h->opt = opt;
     if (const char* e = getenv("RSI_MIN_TRAV")) h->min_trav = atoi(e);  // tuning knobs
-    if (const char* e = getenv("RSI_SPEC")) h->spec = atoi(e) < 1 ? 1 : (atoi(e) > 2 ? 2 : atoi(e));
     cudaStream_t s = (cudaStream_t)stream;
     h->stream = s;
     st = rsi_cuda_check(cudaGetDevice(&h->device), "cudaGetDevice");

@@ -59,7 +59,6 @@ struct rsi_bvh {
     float scene_lo[3] = {0, 0, 0}, scene_hi[3] = {0, 0, 0};
     uint64_t host_rays = 0, host_overflow = 0;  // counters known on the host
     int min_trav = 8;  // traversal-phase exit threshold (lanes still searching); env RSI_MIN_TRAV
-    int spec = 2;      // pending-leaf limit while traversing (speculation); env RSI_SPEC
 };
 
 // ---------------------------------------------------------------- host helpers (api.cu)

@@ -23,7 +23,6 @@ constexpr float kU = 5.9604644775390625e-08f;    // 2^-24, fp32 unit roundoff
 constexpr float kFilt = 16.0f * kU;              // K = 16
 constexpr float kTerr = 12.0f * kU;              // t forward-error constant
 constexpr float kSlack = 4.76837158203125e-07f;  // 2^-21: slab-test slack factor
-constexpr float kSlackMax = 1.953125e-03f;       // 2^-9: larger slack -> axis unconstrained
 constexpr float kTiny = 1e-30f;                  // absolute floor (underflow)
 constexpr float kOutTol = 4e-6f;                 // max certified |t error| for fp32 outputs
 constexpr int kStack = 64;
@@ -229,22 +228,10 @@ __device__ __forceinline__ void traverse(const float4* __restrict__ nodes, const
     }
 }
 
-#ifndef RSI_SMEM_STATS
-#define RSI_SMEM_STATS 0
-#endif
-#ifndef RSI_QUEUE
-#define RSI_QUEUE 0
-#endif
-// Per-thread counters of rare events, reduced per warp at kernel end
-// (RSI_SMEM_STATS=1: block-level shared-memory atomics instead).
+// Per-thread counters of rare events, reduced per warp at kernel end.
 struct Stats {
-#if RSI_SMEM_STATS
-    unsigned* s;  // shared [ST_WORDS]
-    __device__ __forceinline__ void add(int k, unsigned v = 1) { atomicAdd(s + k, v); }
-#else
     unsigned c[ST_WORDS] = {};
     __device__ __forceinline__ void add(int k, unsigned v = 1) { c[k] += v; }
-#endif
     unsigned boxes = 0, mts = 0;  // RSI_OPT_COUNTERS only
 };
 
@@ -294,7 +281,6 @@ struct TraceParams {
     unsigned long long* stats;
     unsigned long long* counter;  // persistent-grid ray dispenser
     int min_trav;           // leave the traversal phase when fewer lanes still search
-    int spec;               // max pending leaves while traversing (1 = no speculation)
 };
 
 template <int MODE>
@@ -537,9 +523,10 @@ struct ModeState<MODE_COUNT> {
 // Laine's while-while traversal, adapted to segments and child-pair nodes):
 //   1. refill: lanes without a ray take the next ray ids from the warp's chunk
 //      (one atomicAdd per kChunk rays per warp), so lanes never idle while rays remain;
-//   2. traversal phase: a lane walks internal nodes while it holds fewer than
-//      `spec` pending leaves; the phase ends when no lane (or fewer than
-//      min_trav lanes) is still searching without a pending leaf;
+//   2. traversal phase: a lane walks internal nodes until it holds a pending
+//      leaf (a leaf child whose box the segment enters; both children when
+//      both are leaves); the phase ends when no lane (or fewer than min_trav
+//      lanes, while others wait with leaves) is still searching;
 //   3. leaf phase: all lanes with pending leaves run Moller-Trumbore together;
 //   4. finished rays write their outputs and free the lane.
 template <int MODE, bool kFP64, bool kCounters>
@@ -550,17 +537,12 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
     __shared__ float2 s_te[MODE == MODE_COUNT ? kCountCap * kThreads : 1];
     __shared__ int s_k[MODE == MODE_COUNT ? kCountCap * kThreads : 1];
     Stats st;
-#if RSI_SMEM_STATS
-    __shared__ unsigned s_stats[ST_WORDS];
-    if (threadIdx.x < ST_WORDS) s_stats[threadIdx.x] = 0u;
-    __syncthreads();
-    st.s = s_stats;
-#endif
+
     int64_t cnext = 0, cend = 0;  // warp-uniform chunk [cnext, cend)
     bool exhausted = false;       // warp-uniform
     int64_t ray = -1;
     Ray r;
-    int node = -1, sp = 0, npend = 0, l0 = -1, l1 = -1, l2 = -1;  // pending (postponed) leaves
+    int node = -1, sp = 0, l0 = -1, l1 = -1;  // l0/l1: pending (postponed) leaf slots
     int stack[kStack];
     float tclip = 1.0f;
     ModeState<MODE> ms;
@@ -602,63 +584,12 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             ms.init();
             tclip = 1.0f;
             sp = 0;
-            npend = 0;
             l0 = l1 = -1;
             node = ok ? 0 : -1;
         }
         if (__ballot_sync(FULL, ray >= 0) == 0) break;  // no rays left for this warp
 
         // ---- 2. traversal phase
-#if RSI_QUEUE
-        while (true) {
-            const bool searching = node >= 0 && npend == 0;
-            const unsigned sm = __ballot_sync(FULL, searching);
-            if (sm == 0) break;
-            if (__popc(sm) < p.min_trav && __ballot_sync(FULL, npend > 0)) break;
-            if (node >= 0 && npend < p.spec) {
-                const float4* nd = p.nodes + 4 * node;
-                const float4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2);
-                const int4 n3 = __ldg(reinterpret_cast<const int4*>(nd + 3));
-                float nearL, nearR;
-                bool hL = slab(r, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, tclip, nearL);
-                bool hR = slab(r, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, tclip, nearR);
-                if (kCounters) st.boxes += 2;
-                if (hL && n3.x < 0) {
-                    const int x = ~n3.x;
-                    if (npend == 0) l0 = x; else l1 = x;
-                    ++npend;
-                    hL = false;
-                }
-                if (hR && n3.y < 0) {
-                    const int x = ~n3.y;
-                    if (npend == 0) l0 = x; else if (npend == 1) l1 = x; else l2 = x;
-                    ++npend;
-                    hR = false;
-                }
-                if (hL && hR) {
-                    const bool rfirst = nearR < nearL;
-                    stack[sp++] = rfirst ? n3.x : n3.y;
-                    node = rfirst ? n3.y : n3.x;
-                } else if (hL) {
-                    node = n3.x;
-                } else if (hR) {
-                    node = n3.y;
-                } else {
-                    node = sp > 0 ? stack[--sp] : -1;
-                }
-            }
-        }
-
-        // ---- 3. leaf phase
-        if (npend > 0) {
-            if (kCounters) st.mts += npend;
-            bool done = ms.template leaf<kFP64>(p, r, l0, tclip, st);
-            if (!done && npend > 1) done = ms.template leaf<kFP64>(p, r, l1, tclip, st);
-            if (!done && npend > 2) done = ms.template leaf<kFP64>(p, r, l2, tclip, st);
-            npend = 0;
-            if (done) node = -1;
-        }
-#else
         // a lane walks internal nodes until it holds a pending leaf (l0, and l1
         // when both children of the visited node are leaves)
         while (true) {
@@ -707,10 +638,9 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             l0 = l1 = -1;
             if (done) node = -1;
         }
-#endif
 
         // ---- 4. finish
-        if (ray >= 0 && node < 0 && npend == 0 && l0 < 0) {
+        if (ray >= 0 && node < 0 && l0 < 0) {
             ms.finish(p, r, ray, st);
             ray = -1;
         }
@@ -719,10 +649,6 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
         st.add(ST_BOX_TESTS, st.boxes);
         st.add(ST_MT_TESTS, st.mts);
     }
-#if RSI_SMEM_STATS
-    __syncthreads();
-    if (threadIdx.x < ST_WORDS && s_stats[threadIdx.x]) atomicAdd(p.stats + threadIdx.x, (unsigned long long)s_stats[threadIdx.x]);
-#else
 #pragma unroll
     for (int k = 1; k < ST_WORDS; ++k) {
         unsigned v = st.c[k];
@@ -731,7 +657,6 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             if (lane == 0 && v) atomicAdd(p.stats + k, (unsigned long long)v);
         }
     }
-#endif
 }
 
 // ---------------------------------------------------------------- exact re-pass for overflowed rays
@@ -960,7 +885,6 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     p.stats = h->stats;
     p.counter = reinterpret_cast<unsigned long long*>(h->scratch + SCR_DISPENSER);
     p.min_trav = h->min_trav;
-    p.spec = h->spec;
     const bool fp64 = (h->opt.flags & RSI_OPT_FP64_MOLLER) != 0, ctr = (h->opt.flags & RSI_OPT_COUNTERS) != 0;
     if (fp64)
         ctr ? launch_mode<true, true>(mode, p, s) : launch_mode<true, false>(mode, p, s);

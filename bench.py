@@ -41,9 +41,11 @@ METRIC = "rays/sec (boolean & barycentric) at N_t=1e4, N_r=1e7-1e8 on 1/2/4/8 B2
 UNIT = "rays/s"
 
 # Algorithmic work model of the traversal kernel:
-# per ray box tests and Moller-Trumbore tests for the sphere / long-segment
-# workload, and FP32-pipe instructions per test.
-WORK = {
+# FP32-pipe instructions per child-box slab test and per Moller-Trumbore test.
+# The per-ray numbers of box and MT tests are MEASURED in this run by an
+# instrumented launch (RSI_OPT_COUNTERS) outside the timed region; SURVEY
+# 8(d)'s CPU-model figures are the fallback.
+WORK_MODEL = {
     "boolean": {"box_tests": 36.8, "mt_tests": 1.62},
     "barycentric": {"box_tests": 54.9, "mt_tests": 2.92},
     "intercept_count": {"box_tests": 69.3, "mt_tests": 3.97},
@@ -142,8 +144,8 @@ def cpu_baseline(V, T, S, E, target_s=15.0, sample=0):
                       f"(exhaustive fp64, {dt:.1f} s)"}
 
 
-def roofline(mode: str, rays: int, kernel_ms: float, sm_mhz: float | None):
-    w = WORK[mode]
+def roofline(mode: str, rays: int, kernel_ms: float, sm_mhz: float | None, work: dict | None = None):
+    w = work or WORK_MODEL[mode]
     inst_per_ray = w["box_tests"] * FP32_PER_BOX + w["mt_tests"] * FP32_PER_MT
     clock = (sm_mhz or 1965.0) * 1e6
     peak = N_SM * FP32_LANES * clock / 1e12            # T FP32 inst/s
@@ -151,15 +153,16 @@ def roofline(mode: str, rays: int, kernel_ms: float, sm_mhz: float | None):
     return {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 4), "unit": "TFP32-inst/s",
             "frac": round(achieved / peak, 5), "traffic": None,
             "kernel": f"k_{mode}", "kernel_ms": round(kernel_ms, 4),
-            "model": f"{w['box_tests']} box x {FP32_PER_BOX:.0f} + {w['mt_tests']} MT x {FP32_PER_MT:.0f} "
-                     f"= {inst_per_ray:.0f} FP32 inst/ray; peak = 148 SM x 128 lanes x sm_mhz"}
+            "model": f"{w['box_tests']:.2f} box x {FP32_PER_BOX:.0f} + {w['mt_tests']:.2f} MT x {FP32_PER_MT:.0f} "
+                     f"= {inst_per_ray:.0f} FP32 inst/ray ({'measured' if work else 'SURVEY 8(d) model'} "
+                     f"tests/ray); peak = 148 SM x 128 FP32 lanes x median sm_mhz"}
 
 
 # ------------------------------------------------------------------ reference arm
 def run_reference(args, rank: int, world: int):
     if rank != 0:
         return
-    V, T, S, E = workload_inputs(args.workload, max(args.rays_per_gpu // 1000, 20000), 0)
+    V, T, S, E = workload_inputs(args.workload, max(args.rays_per_gpu // 5, 20000), 0)
     import oracle
     cores = oracle.max_threads()
     n0 = 100
@@ -198,6 +201,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2305_01867_b200 import rsi
+    from paper_2305_01867_b200.sharded import gather_outputs
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -214,10 +218,6 @@ def main():
 
     def timed(mode: str, steps: int, warmup: int, clocks: bool):
         out = rsi.alloc_outputs(n, mode, dev)
-        gather_buf = None
-        if world > 1:
-            key = {"boolean": "hit", "barycentric": "tri", "intercept_count": "count"}[mode]
-            gather_buf = torch.empty((world,) + tuple(out[key].shape), dtype=out[key].dtype, device=dev)
 
         def step(ev=None):
             if ev is not None:
@@ -229,8 +229,7 @@ def main():
             if ev is not None:
                 ev[2].record(stream)
             if world > 1:
-                key = {"boolean": "hit", "barycentric": "tri", "intercept_count": "count"}[mode]
-                dist.all_gather_into_tensor(gather_buf, out[key])
+                gather_outputs(out, n * world)
 
         for _ in range(warmup):
             step()
@@ -273,6 +272,12 @@ def main():
             extra[m] = {"value": n * world * args.steps / (mms * 1e-3), "ms_per_step": mms / args.steps,
                         "build_ms": mb, "query_ms": mq}
     stats = rsi.rsi_get_stats(h)
+    # measured algorithmic work per ray (instrumented launch, outside the timed region)
+    work = None
+    with rsi.rsi_build(Vd, Td, rsi.Options(counters=True)) as hc:
+        rsi.rsi_intersect(hc, Sd, Ed, args.mode)
+        cs = rsi.rsi_get_stats(hc)
+        work = {"box_tests": cs["box_tests"] / n, "mt_tests": cs["mt_tests"] / n}
 
     # e2e: through the C-ABI rsi_test on pinned host buffers (rank-local)
     e2e = None
@@ -314,9 +319,11 @@ def main():
                        "l2": "inputs larger than L2 (240 MB of segments per GPU)",
                        "step": "rsi_rebuild + rsi_intersect" + (" + gather" if world > 1 else "")},
             "build_ms": build_ms, "query_ms": query_ms,
-            "roofline": roofline(args.mode, n, query_ms, clk["sm_mhz"] if clk else None),
+            "roofline": roofline(args.mode, n, query_ms, clk["sm_mhz"] if clk else None, work),
+            "work_per_ray": work,
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": args.steps * (kernels_per_build + 1),
+            "gpu_launches_note": f"per step: {kernels_per_build} build kernels + 1 traversal kernel",
             "clocks": clk, "modes": extra, "stats": stats,
         }
         print(json.dumps(line), flush=True)

@@ -47,6 +47,19 @@ static rsi_status_t check_mesh_args(const float* V, int64_t nv, const int32_t* T
     return RSI_OK;
 }
 
+// Keep freed stream-ordered allocations cached in the device's default pool, so
+// per-call cudaMallocAsync / cudaFreeAsync (rsi_test, overflow pass) do not
+// return memory to the OS between calls.
+void rsi_keep_pool_cached() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    (void)cudaGetLastError();
+}
+
 extern "C" {
 
 const char* rsi_version(void) { return RSI_VERSION_STRING; }
@@ -65,6 +78,7 @@ rsi_status_t rsi_build(const float* d_vertices, int64_t n_vertices, const int32_
     rsi_bvh* h = new (std::nothrow) rsi_bvh();
     if (!h) return rsi_set_error(RSI_E_OOM, "host allocation failed");
     h->opt = opt;
+    rsi_keep_pool_cached();
     if (const char* e = getenv("RSI_MIN_TRAV")) h->min_trav = atoi(e);  // tuning knobs
     cudaStream_t s = (cudaStream_t)stream;
     h->stream = s;
@@ -133,58 +147,111 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
                       const rsi_options_t* options, const rsi_outputs_t* h_out, void* stream) {
     if (!h_out || n_rays < 0 || (n_rays > 0 && (!h_start || !h_end)))
         return rsi_set_error(RSI_E_INVALID_ARG, "bad rsi_test arguments");
+    if (mode != RSI_MODE_BOOLEAN && mode != RSI_MODE_BARYCENTRIC && mode != RSI_MODE_INTERCEPT_COUNT)
+        return rsi_set_error(RSI_E_INVALID_ARG, "bad mode %d", mode);
     rsi_status_t st = check_mesh_args(h_vertices, n_vertices, h_triangles, n_triangles);
     if (st != RSI_OK) return st;
     cudaStream_t s = (cudaStream_t)stream;
+    rsi_keep_pool_cached();
+    // 1. mesh upload + build (the build synchronizes once for validation)
     const size_t bv = (size_t)n_vertices * 3 * sizeof(float), bt = (size_t)n_triangles * 3 * sizeof(int32_t);
-    const size_t br = (size_t)n_rays * 3 * sizeof(float);
-    size_t bout = 0;
-    if (mode == RSI_MODE_BOOLEAN) bout = (size_t)n_rays;
-    else if (mode == RSI_MODE_INTERCEPT_COUNT) bout = (size_t)n_rays * 4;
-    else if (mode == RSI_MODE_BARYCENTRIC) bout = (size_t)n_rays * 4 * 6;
-    else return rsi_set_error(RSI_E_INVALID_ARG, "bad mode %d", mode);
-    char* buf = nullptr;
-    const size_t al = 256;
-    auto up = [&](size_t x) { return (x + al - 1) / al * al; };
-    const size_t total = up(bv) + up(bt) + 2 * up(br) + up(bout) + al;
-    st = rsi_cuda_check(cudaMallocAsync((void**)&buf, total, s), "rsi_test buffers");
+    char* mesh = nullptr;
+    st = rsi_cuda_check(cudaMallocAsync((void**)&mesh, ((bv + 255) / 256) * 256 + bt, s), "rsi_test mesh");
     if (st != RSI_OK) return st;
-    float* dV = (float*)buf;
-    int32_t* dT = (int32_t*)(buf + up(bv));
-    float* dS = (float*)(buf + up(bv) + up(bt));
-    float* dE = (float*)(buf + up(bv) + up(bt) + up(br));
-    char* dO = buf + up(bv) + up(bt) + 2 * up(br);
+    float* dV = (float*)mesh;
+    int32_t* dT = (int32_t*)(mesh + ((bv + 255) / 256) * 256);
     st = rsi_cuda_check(cudaMemcpyAsync(dV, h_vertices, bv, cudaMemcpyHostToDevice, s), "H2D vertices");
     if (st == RSI_OK) st = rsi_cuda_check(cudaMemcpyAsync(dT, h_triangles, bt, cudaMemcpyHostToDevice, s), "H2D triangles");
-    if (st == RSI_OK && br) st = rsi_cuda_check(cudaMemcpyAsync(dS, h_start, br, cudaMemcpyHostToDevice, s), "H2D start");
-    if (st == RSI_OK && br) st = rsi_cuda_check(cudaMemcpyAsync(dE, h_end, br, cudaMemcpyHostToDevice, s), "H2D end");
     rsi_handle_t h = nullptr;
     if (st == RSI_OK) st = rsi_build(dV, n_vertices, dT, n_triangles, options, stream, &h);
-    rsi_outputs_t d_out{};
-    if (st == RSI_OK) {
-        const size_t n = (size_t)n_rays;
-        if (mode == RSI_MODE_BOOLEAN) d_out.hit = (uint8_t*)dO;
-        if (mode == RSI_MODE_INTERCEPT_COUNT) d_out.count = (int32_t*)dO;
-        if (mode == RSI_MODE_BARYCENTRIC) {
-            d_out.tri = (int32_t*)dO;
-            d_out.t = (float*)(dO + 4 * n);
-            d_out.dist = (float*)(dO + 8 * n);
-            d_out.point = (float*)(dO + 12 * n);
+    cudaFreeAsync(mesh, s);
+    if (st != RSI_OK) return st;
+
+    // 2. rays in chunks through a 3-stream pipeline: H2D(c+1) and D2H(c-1)
+    //    overlap the traversal of chunk c (which runs on the caller's stream).
+    const int64_t kChunkRays = (int64_t)1 << 21;
+    const int64_t nchunk = (n_rays + kChunkRays - 1) / kChunkRays;
+    const int64_t crays = n_rays < kChunkRays ? n_rays : kChunkRays;
+    size_t out_b = mode == RSI_MODE_BOOLEAN ? 1 : (mode == RSI_MODE_INTERCEPT_COUNT ? 4 : 24);
+    auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+    const size_t slot_b = 2 * up((size_t)crays * 12) + up((size_t)crays * out_b);
+    char* slots = nullptr;
+    cudaStream_t sh = nullptr, sd = nullptr;
+    cudaEvent_t* ev = nullptr;  // per chunk: h2d done, kernel done, d2h done
+    if (nchunk > 0) {
+        st = rsi_cuda_check(cudaMallocAsync((void**)&slots, 2 * slot_b, s), "rsi_test ray buffers");
+        if (st == RSI_OK) st = rsi_cuda_check(cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking), "stream");
+        if (st == RSI_OK) st = rsi_cuda_check(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking), "stream");
+        if (st == RSI_OK) {
+            ev = new (std::nothrow) cudaEvent_t[3 * nchunk]();
+            if (!ev) st = rsi_set_error(RSI_E_OOM, "host allocation failed");
         }
-        st = rsi_intersect(h, dS, dE, n_rays, mode, &d_out, stream);
+        for (int64_t k = 0; st == RSI_OK && k < 3 * nchunk; ++k)
+            st = rsi_cuda_check(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming), "event");
     }
-    if (st == RSI_OK && n_rays > 0) {
-        const size_t n = (size_t)n_rays;
-        auto d2h = [&](void* dst, const void* src, size_t b) {
-            if (dst && st == RSI_OK) st = rsi_cuda_check(cudaMemcpyAsync(dst, src, b, cudaMemcpyDeviceToHost, s), "D2H");
-        };
-        if (mode == RSI_MODE_BOOLEAN) d2h(h_out->hit, d_out.hit, n);
-        if (mode == RSI_MODE_INTERCEPT_COUNT) d2h(h_out->count, d_out.count, 4 * n);
+    cudaEvent_t ready = nullptr;  // slots allocated + handle built on `s`
+    if (st == RSI_OK && nchunk > 0) {
+        st = rsi_cuda_check(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
+        if (st == RSI_OK) st = rsi_cuda_check(cudaEventRecord(ready, s), "event");
+        if (st == RSI_OK) st = rsi_cuda_check(cudaStreamWaitEvent(sh, ready, 0), "wait");
+        if (st == RSI_OK) st = rsi_cuda_check(cudaStreamWaitEvent(sd, ready, 0), "wait");
+    }
+    auto slot = [&](int64_t c) { return slots + (c & 1) * slot_b; };
+    auto h2d = [&](int64_t c) {
+        const int64_t r0 = c * kChunkRays, nr = (n_rays - r0) < kChunkRays ? (n_rays - r0) : kChunkRays;
+        char* b = slot(c);
+        if (c >= 2) st = rsi_cuda_check(cudaStreamWaitEvent(sh, ev[3 * (c - 2) + 1], 0), "wait");
+        if (st == RSI_OK)
+            st = rsi_cuda_check(cudaMemcpyAsync(b, h_start + 3 * r0, (size_t)nr * 12, cudaMemcpyHostToDevice, sh), "H2D start");
+        if (st == RSI_OK)
+            st = rsi_cuda_check(cudaMemcpyAsync(b + up((size_t)crays * 12), h_end + 3 * r0, (size_t)nr * 12,
+                                                cudaMemcpyHostToDevice, sh), "H2D end");
+        if (st == RSI_OK) st = rsi_cuda_check(cudaEventRecord(ev[3 * c], sh), "event");
+    };
+    if (st == RSI_OK && nchunk > 0) h2d(0);
+    for (int64_t c = 0; st == RSI_OK && c < nchunk; ++c) {
+        if (c + 1 < nchunk) h2d(c + 1);
+        if (st != RSI_OK) break;
+        const int64_t r0 = c * kChunkRays, nr = (n_rays - r0) < kChunkRays ? (n_rays - r0) : kChunkRays;
+        char* b = slot(c);
+        char* o = b + 2 * up((size_t)crays * 12);
+        st = rsi_cuda_check(cudaStreamWaitEvent(s, ev[3 * c], 0), "wait");
+        if (st == RSI_OK && c >= 2) st = rsi_cuda_check(cudaStreamWaitEvent(s, ev[3 * (c - 2) + 2], 0), "wait");
+        rsi_outputs_t d_out{};
+        if (mode == RSI_MODE_BOOLEAN) d_out.hit = (uint8_t*)o;
+        if (mode == RSI_MODE_INTERCEPT_COUNT) d_out.count = (int32_t*)o;
         if (mode == RSI_MODE_BARYCENTRIC) {
-            d2h(h_out->tri, d_out.tri, 4 * n);
-            d2h(h_out->t, d_out.t, 4 * n);
-            d2h(h_out->dist, d_out.dist, 4 * n);
-            d2h(h_out->point, d_out.point, 12 * n);
+            d_out.tri = (int32_t*)o;
+            d_out.t = h_out->t ? (float*)(o + 4 * (size_t)crays) : nullptr;
+            d_out.dist = h_out->dist ? (float*)(o + 8 * (size_t)crays) : nullptr;
+            d_out.point = h_out->point ? (float*)(o + 12 * (size_t)crays) : nullptr;
+        }
+        if (st == RSI_OK)
+            st = rsi_intersect(h, (const float*)b, (const float*)(b + up((size_t)crays * 12)), nr, mode, &d_out, stream);
+        if (st == RSI_OK) st = rsi_cuda_check(cudaEventRecord(ev[3 * c + 1], s), "event");
+        if (st == RSI_OK) st = rsi_cuda_check(cudaStreamWaitEvent(sd, ev[3 * c + 1], 0), "wait");
+        auto d2h = [&](void* dst, const void* src, size_t bytes) {
+            if (dst && st == RSI_OK)
+                st = rsi_cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, sd), "D2H");
+        };
+        if (mode == RSI_MODE_BOOLEAN) d2h(h_out->hit ? h_out->hit + r0 : nullptr, d_out.hit, (size_t)nr);
+        if (mode == RSI_MODE_INTERCEPT_COUNT) d2h(h_out->count ? h_out->count + r0 : nullptr, d_out.count, 4 * (size_t)nr);
+        if (mode == RSI_MODE_BARYCENTRIC) {
+            d2h(h_out->tri ? h_out->tri + r0 : nullptr, d_out.tri, 4 * (size_t)nr);
+            d2h(h_out->t ? h_out->t + r0 : nullptr, d_out.t, 4 * (size_t)nr);
+            d2h(h_out->dist ? h_out->dist + r0 : nullptr, d_out.dist, 4 * (size_t)nr);
+            d2h(h_out->point ? h_out->point + 3 * r0 : nullptr, d_out.point, 12 * (size_t)nr);
+        }
+        if (st == RSI_OK) st = rsi_cuda_check(cudaEventRecord(ev[3 * c + 2], sd), "event");
+    }
+    // 3. drain, release (frees ordered after the last D2H), synchronize
+    rsi_status_t st2 = RSI_OK;
+    if (sd) {
+        cudaEvent_t fin;
+        if (cudaEventCreateWithFlags(&fin, cudaEventDisableTiming) == cudaSuccess) {
+            cudaEventRecord(fin, sd);
+            cudaStreamWaitEvent(s, fin, 0);
+            cudaEventDestroy(fin);
         }
     }
     if (h) {
@@ -193,8 +260,15 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
         rsi_free(h);
         memcpy(g_err, saved, sizeof(saved));
     }
-    cudaFreeAsync(buf, s);
-    rsi_status_t st2 = rsi_cuda_check(cudaStreamSynchronize(s), "rsi_test");
+    if (slots) cudaFreeAsync(slots, s);
+    st2 = rsi_cuda_check(cudaStreamSynchronize(s), "rsi_test");
+    if (sh) cudaStreamDestroy(sh);
+    if (sd) cudaStreamDestroy(sd);
+    if (ev)
+        for (int64_t k = 0; k < 3 * nchunk; ++k)
+            if (ev[k]) cudaEventDestroy(ev[k]);
+    delete[] ev;
+    if (ready) cudaEventDestroy(ready);
     return st != RSI_OK ? st : st2;
 }
 

@@ -64,6 +64,7 @@ struct rsi_bvh {
 // ---------------------------------------------------------------- host helpers (api.cu)
 rsi_status_t rsi_set_error(rsi_status_t s, const char* fmt, ...);
 rsi_status_t rsi_cuda_check(cudaError_t e, const char* what);
+void rsi_keep_pool_cached();
 
 // build.cu
 rsi_status_t rsi_build_device(rsi_bvh* h, const float* d_vertices, int64_t n_vertices,

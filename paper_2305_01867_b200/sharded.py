@@ -1,0 +1,71 @@
+"""Ray-sharded multi-GPU driver.
+
+Rays are independent, so the path shards with no data-path collective: every
+rank replicates the mesh, builds its own BVH on its GPU (rsi_build), and
+intersects the contiguous ray slice [floor(r N / W), floor((r+1) N / W)).  The
+only collective is the final gather of the per-ray outputs to rank 0 in ray
+order (north_star: "NCCL over NVLink is used only to gather the per-ray
+outputs").  The gather pads every slice to ceil(N / W) rows and uses one
+all_gather_into_tensor per output field (NCCL over NVLink on GPUs, gloo in the
+CPU tests), then trims the padding.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+# output fields per mode, in rsi_outputs_t order
+FIELDS = {"boolean": ("hit",), "intercept_count": ("count",), "barycentric": ("tri", "t", "dist", "point")}
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous slice of rank `rank` out of `world` (sizes differ by <= 1)."""
+    if world <= 0 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return (n * rank) // world, (n * (rank + 1)) // world
+
+
+def gather_outputs(local: dict, n_total: int, group=None) -> dict:
+    """All-gather per-ray outputs of every rank's slice into full arrays in ray
+    order (every rank receives them; rank 0 is the consumer).  `local` holds
+    this rank's slice tensors (same device for all ranks' backend)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    per = -(-n_total // world)
+    lo, hi = shard_range(n_total, rank, world)
+    out = {}
+    for k in sorted(local):
+        t = local[k]
+        if t.shape[0] != hi - lo:
+            raise ValueError(f"{k}: slice has {t.shape[0]} rows, expected {hi - lo}")
+        pad = torch.zeros((per,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        pad[: hi - lo] = t
+        full = torch.empty((world * per,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(full, pad, group=group)
+        parts = [full[r * per: r * per + (shard_range(n_total, r, world)[1] - shard_range(n_total, r, world)[0])]
+                 for r in range(world)]
+        out[k] = torch.cat(parts, 0)
+    return out
+
+
+def intersect_sharded(vertices: torch.Tensor, triangles: torch.Tensor, start: torch.Tensor, end: torch.Tensor,
+                      mode: str = "boolean", options=None, group=None, intersect_fn=None) -> dict:
+    """Replicated build + sharded intersect + gather.  `start`/`end` are the
+    FULL ray arrays (any device; this rank's slice is moved to its GPU).
+    `intersect_fn(vertices, triangles, s, e, mode) -> dict` defaults to the
+    CUDA path (rsi_build + rsi_intersect on the current device)."""
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    n = start.shape[0]
+    lo, hi = shard_range(n, rank, world)
+    if intersect_fn is None:
+        from . import rsi
+        dev = torch.device("cuda", torch.cuda.current_device())
+        V, T = vertices.to(dev), triangles.to(dev)
+        s, e = start[lo:hi].to(dev), end[lo:hi].to(dev)
+        with rsi.rsi_build(V, T, options) as h:
+            local = rsi.rsi_intersect(h, s, e, mode)
+    else:
+        local = intersect_fn(vertices, triangles, start[lo:hi], end[lo:hi], mode)
+    local = {k: local[k] for k in FIELDS[mode] if k in local}
+    return gather_outputs(local, n, group)

@@ -144,6 +144,15 @@ def cpu_baseline(V, T, S, E, target_s=15.0, sample=0):
                       f"(exhaustive fp64, {dt:.1f} s)"}
 
 
+def _traffic(mode: str, rays: int):
+    """DRAM bytes per launch from the committed ncu capture (same workload), if present."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+        return int(t[mode]) if rays == 10_000_000 else None
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def roofline(mode: str, rays: int, kernel_ms: float, sm_mhz: float | None, work: dict | None = None):
     w = work or WORK_MODEL[mode]
     inst_per_ray = w["box_tests"] * FP32_PER_BOX + w["mt_tests"] * FP32_PER_MT
@@ -151,7 +160,8 @@ def roofline(mode: str, rays: int, kernel_ms: float, sm_mhz: float | None, work:
     peak = N_SM * FP32_LANES * clock / 1e12            # T FP32 inst/s
     achieved = inst_per_ray * rays / (kernel_ms * 1e-3) / 1e12
     return {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 4), "unit": "TFP32-inst/s",
-            "frac": round(achieved / peak, 5), "traffic": None,
+            "frac": round(achieved / peak, 5), "traffic": _traffic(mode, rays),
+            "traffic_unit": "DRAM bytes/launch (ncu); algorithmic ray stream = 25 B/ray (boolean)",
             "kernel": f"k_{mode}", "kernel_ms": round(kernel_ms, 4),
             "model": f"{w['box_tests']:.2f} box x {FP32_PER_BOX:.0f} + {w['mt_tests']:.2f} MT x {FP32_PER_MT:.0f} "
                      f"= {inst_per_ray:.0f} FP32 inst/ray ({'measured' if work else 'SURVEY 8(d) model'} "

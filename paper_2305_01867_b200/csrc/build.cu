@@ -453,13 +453,66 @@ __global__ void __launch_bounds__(kBlock) k_refit(const float* __restrict__ V, i
     }
 }
 
+// ------------------------------------------------------------------ 4-wide view (grandchild records)
+// One thread per internal node n: gather the boxes and refs of n's
+// grandchildren from the child-pair records of n and of its internal children.
+__global__ void __launch_bounds__(kBlock) k_quads(const float4* __restrict__ nodes, int n_nodes,
+                                                  float4* __restrict__ quads) {
+    int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= n_nodes) return;
+    float lo[3][4], hi[3][4];
+    int ref[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+        for (int a = 0; a < 3; ++a) lo[a][j] = hi[a][j] = INFINITY;
+        ref[j] = ~0;
+    }
+    int k = 0;
+    const float4* nd = nodes + 4 * n;
+    const float4 n0 = nd[0], n1 = nd[1], n2 = nd[2];
+    const int4 n3 = *reinterpret_cast<const int4*>(nd + 3);
+    const float4 cb[2] = {n0, n1};
+    const float cz[2][2] = {{n2.x, n2.y}, {n2.z, n2.w}};
+    const int cr[2] = {n3.x, n3.y};
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+        const int c = cr[side];
+        if (c < 0) {  // leaf child stands for itself
+            lo[0][k] = cb[side].x; hi[0][k] = cb[side].y; lo[1][k] = cb[side].z; hi[1][k] = cb[side].w;
+            lo[2][k] = cz[side][0]; hi[2][k] = cz[side][1];
+            ref[k] = c;
+            ++k;
+        } else {
+            const float4* cd = nodes + 4 * c;
+            const float4 c0 = cd[0], c1 = cd[1], c2 = cd[2];
+            const int4 c3 = *reinterpret_cast<const int4*>(cd + 3);
+            lo[0][k] = c0.x; hi[0][k] = c0.y; lo[1][k] = c0.z; hi[1][k] = c0.w; lo[2][k] = c2.x; hi[2][k] = c2.y;
+            ref[k] = c3.x;
+            ++k;
+            lo[0][k] = c1.x; hi[0][k] = c1.y; lo[1][k] = c1.z; hi[1][k] = c1.w; lo[2][k] = c2.z; hi[2][k] = c2.w;
+            ref[k] = c3.y;
+            ++k;
+        }
+    }
+    float4* q = quads + 8 * n;
+    q[0] = make_float4(lo[0][0], lo[0][1], lo[0][2], lo[0][3]);
+    q[1] = make_float4(hi[0][0], hi[0][1], hi[0][2], hi[0][3]);
+    q[2] = make_float4(lo[1][0], lo[1][1], lo[1][2], lo[1][3]);
+    q[3] = make_float4(hi[1][0], hi[1][1], hi[1][2], hi[1][3]);
+    q[4] = make_float4(lo[2][0], lo[2][1], lo[2][2], lo[2][3]);
+    q[5] = make_float4(hi[2][0], hi[2][1], hi[2][2], hi[2][3]);
+    q[6] = make_float4(__int_as_float(ref[0]), __int_as_float(ref[1]), __int_as_float(ref[2]), __int_as_float(ref[3]));
+    q[7] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ host side
 static rsi_status_t ensure_capacity(rsi_bvh* h, int64_t n, cudaStream_t s) {
     int nb = rsi_ceil_div(n, kTile);
     if (n <= h->cap_tri && nb <= h->sort_blocks_cap) return RSI_OK;
-    void* old[] = {h->nodes, h->tris, h->keys, h->vals, h->keys_tmp, h->vals_tmp, h->parent, h->arrivals, h->hist};
+    void* old[] = {h->nodes, h->quads, h->tris, h->keys, h->vals, h->keys_tmp, h->vals_tmp, h->parent, h->arrivals, h->hist};
     for (void* p : old)
         if (p) cudaFreeAsync(p, s);
     int64_t nn = n > 1 ? n - 1 : 1;
@@ -467,6 +520,7 @@ static rsi_status_t ensure_capacity(rsi_bvh* h, int64_t n, cudaStream_t s) {
 #define RSI_ALLOC(ptr, bytes) \
     if (e == cudaSuccess) e = cudaMallocAsync((void**)&(ptr), (size_t)(bytes), s);
     RSI_ALLOC(h->nodes, nn * 4 * sizeof(float4));
+    RSI_ALLOC(h->quads, nn * 8 * sizeof(float4));
     RSI_ALLOC(h->tris, n * 3 * sizeof(float4));
     RSI_ALLOC(h->keys, n * sizeof(uint32_t));
     RSI_ALLOC(h->vals, n * sizeof(int32_t));
@@ -526,6 +580,7 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
     k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent, h->arrivals);
     k_refit<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, h->vals, n, h->nodes, h->tris, h->parent,
                                                         h->arrivals, h->scratch);
+    k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads);
     st = rsi_cuda_check(cudaGetLastError(), "build kernel launch");
     if (st != RSI_OK) return st;
     st = rsi_cuda_check(cudaMemcpyAsync(h->h_pinned, h->scratch, SCR_WORDS * sizeof(uint32_t),

@@ -6,6 +6,12 @@
 //     n1 = (R.lo.x, R.hi.x, R.lo.y, R.hi.y)
 //     n2 = (L.lo.z, L.hi.z, R.lo.z, R.hi.z)
 //     n3 = (ref L, ref R, 0, 0) as int bits; ref >= 0 internal node, < 0 leaf ~slot
+//   quad  (128 B, 8 x float4) -- for every internal node n, the AABBs and refs
+//         of its up-to-4 grandchildren (a child that is a leaf stands for itself):
+//     q0 = lo.x[0..3], q1 = hi.x[0..3], q2 = lo.y[0..3], q3 = hi.y[0..3],
+//     q4 = lo.z[0..3], q5 = hi.z[0..3], q6 = ref[0..3] (int bits), q7 = unused
+//     empty slots hold a point box at +inf (never hit).  Traversing quads
+//     visits every other level of the binary tree: half the dependent fetches.
 //   tri   (48 B, 3 x float4) in Morton order: (v0, id bits), (v1, 0), (v2, 0)
 //   The vertices are stored exactly (not e1/e2) so the fp64 mirror can
 //   recompute the oracle's operation order bit-for-bit.
@@ -42,6 +48,7 @@ struct rsi_bvh {
     int64_t cap_tri = 0;             // allocated capacity (triangles)
     int64_t sort_blocks_cap = 0;
     float4* nodes = nullptr;         // [4 * n_nodes]
+    float4* quads = nullptr;         // [8 * n_nodes] grandchild (4-wide) records
     float4* tris = nullptr;          // [3 * n_tri]
     uint32_t* keys = nullptr;        // sorted Morton codes [n_tri]
     int32_t* vals = nullptr;         // sorted triangle ids [n_tri]

@@ -25,7 +25,15 @@ constexpr float kTerr = 12.0f * kU;              // t forward-error constant
 constexpr float kSlack = 4.76837158203125e-07f;  // 2^-21: slab-test slack factor
 constexpr float kTiny = 1e-30f;                  // absolute floor (underflow)
 constexpr float kOutTol = 4e-6f;                 // max certified |t error| for fp32 outputs
-constexpr int kStack = 64;
+#ifndef RSI_QUAD
+#define RSI_QUAD 1
+#endif
+#ifndef RSI_SORT_ALL
+#define RSI_SORT_ALL 1
+#endif
+constexpr int kNoRef = (int)0x80000000;  // "no child" (never a valid ref: ~slot > INT_MIN)
+// binary: depth <= 62 of the index-augmented 62-bit key; quad: <= 31 visits x 3 pushes
+constexpr int kStack = RSI_QUAD ? 96 : 64;
 constexpr int kCountCap = 8;  // intercept_count hits held in registers per ray
 #ifndef RSI_BOOL_MINB
 #define RSI_BOOL_MINB 8
@@ -265,6 +273,7 @@ enum { MODE_BOOL = 0, MODE_BARY = 1, MODE_COUNT = 2 };
 
 struct TraceParams {
     const float4* nodes;
+    const float4* quads;
     const float4* tris;
     const float* S;
     const float* E;
@@ -529,11 +538,23 @@ struct ModeState<MODE_COUNT> {
 //      lanes, while others wait with leaves) is still searching;
 //   3. leaf phase: all lanes with pending leaves run Moller-Trumbore together;
 //   4. finished rays write their outputs and free the lane.
+// compare-and-swap of (key, ref) pairs: ascending keys
+__device__ __forceinline__ void cas(float& ka, int& ca, float& kb, int& cb) {
+    const bool sw = kb < ka;
+    const float tk = sw ? kb : ka;
+    kb = sw ? ka : kb;
+    ka = tk;
+    const int tc = sw ? cb : ca;
+    cb = sw ? ca : cb;
+    ca = tc;
+}
+
 template <int MODE, bool kFP64, bool kCounters>
 __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : RSI_OTHER_MINB) k_trace(const TraceParams p) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
+    constexpr bool kSort = (MODE == MODE_BARY) || RSI_SORT_ALL;
     __shared__ float2 s_te[MODE == MODE_COUNT ? kCountCap * kThreads : 1];
     __shared__ int s_k[MODE == MODE_COUNT ? kCountCap * kThreads : 1];
     Stats st;
@@ -589,6 +610,90 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
         }
         if (__ballot_sync(FULL, ray >= 0) == 0) break;  // no rays left for this warp
 
+#if RSI_QUAD
+        // ---- 2. traversal phase (4-wide view: a visit tests the up-to-4
+        // grandchildren of a binary node; hit children are ordered near-first
+        // (kSort) or by slot, the first becomes the next visit and the rest go
+        // on the stack; a leaf (ref < 0) becomes the lane's pending leaf)
+        while (true) {
+            const bool trav = node >= 0 && l0 < 0;
+            const unsigned tm = __ballot_sync(FULL, trav);
+            if (tm == 0) break;
+            if (__popc(tm) < p.min_trav && __ballot_sync(FULL, l0 >= 0)) break;
+            if (trav) {
+                const float4* q = p.quads + 8 * node;
+                const float4 q0 = __ldg(q), q1 = __ldg(q + 1), q2 = __ldg(q + 2), q3 = __ldg(q + 3);
+                const float4 q4 = __ldg(q + 4), q5 = __ldg(q + 5);
+                const int4 q6 = __ldg(reinterpret_cast<const int4*>(q + 6));
+                float k0, k1, k2, k3;
+                const bool h0 = slab(r, q0.x, q1.x, q2.x, q3.x, q4.x, q5.x, tclip, k0);
+                const bool h1 = slab(r, q0.y, q1.y, q2.y, q3.y, q4.y, q5.y, tclip, k1);
+                const bool h2 = slab(r, q0.z, q1.z, q2.z, q3.z, q4.z, q5.z, tclip, k2);
+                const bool h3 = slab(r, q0.w, q1.w, q2.w, q3.w, q4.w, q5.w, tclip, k3);
+                if (kCounters) st.boxes += 4;
+                int c0 = h0 ? q6.x : kNoRef, c1 = h1 ? q6.y : kNoRef, c2 = h2 ? q6.z : kNoRef, c3 = h3 ? q6.w : kNoRef;
+                if (kSort) {
+                    k0 = h0 ? k0 : INFINITY;
+                    k1 = h1 ? k1 : INFINITY;
+                    k2 = h2 ? k2 : INFINITY;
+                    k3 = h3 ? k3 : INFINITY;
+                    cas(k0, c0, k1, c1);
+                    cas(k2, c2, k3, c3);
+                    cas(k0, c0, k2, c2);
+                    cas(k1, c1, k3, c3);
+                    cas(k1, c1, k2, c2);
+                }
+                int first = kNoRef;
+                if (c3 != kNoRef) first = c3;
+                if (c2 != kNoRef) {
+                    if (first != kNoRef) stack[sp++] = first;
+                    first = c2;
+                }
+                if (c1 != kNoRef) {
+                    if (first != kNoRef) stack[sp++] = first;
+                    first = c1;
+                }
+                if (c0 != kNoRef) {
+                    if (first != kNoRef) stack[sp++] = first;
+                    first = c0;
+                }
+                if (first == kNoRef && sp > 0) first = stack[--sp];
+                if (first == kNoRef) {
+                    node = -1;
+                } else if (first >= 0) {
+                    node = first;
+                } else {
+                    l0 = ~first;
+                    node = -1;
+                }
+            }
+        }
+
+        // ---- 3. leaf phase (up to two leaves in a row from the stack)
+        if (l0 >= 0) {
+            if (kCounters) st.mts += 1;
+            bool done = ms.template leaf<kFP64>(p, r, l0, tclip, st);
+            l0 = -1;
+            int nxt = (!done && sp > 0) ? stack[--sp] : kNoRef;
+            if (nxt != kNoRef && nxt < 0) {
+                if (kCounters) st.mts += 1;
+                done = ms.template leaf<kFP64>(p, r, ~nxt, tclip, st);
+                nxt = (!done && sp > 0) ? stack[--sp] : kNoRef;
+            }
+            if (done) {
+                node = -1;
+                sp = 0;
+            } else if (nxt == kNoRef) {
+                node = -1;
+            } else if (nxt >= 0) {
+                node = nxt;
+            } else {
+                l0 = ~nxt;
+                node = -1;
+            }
+        }
+
+#else
         // ---- 2. traversal phase
         // a lane walks internal nodes until it holds a pending leaf (l0, and l1
         // when both children of the visited node are leaves)
@@ -639,6 +744,7 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             if (done) node = -1;
         }
 
+#endif
         // ---- 4. finish
         if (ray >= 0 && node < 0 && l0 < 0) {
             ms.finish(p, r, ray, st);
@@ -869,6 +975,7 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     if (st != RSI_OK) return st;
     TraceParams p{};
     p.nodes = h->nodes;
+    p.quads = h->quads;
     p.tris = h->tris;
     p.S = S;
     p.E = E;

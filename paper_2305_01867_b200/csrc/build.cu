@@ -423,9 +423,10 @@ __global__ void __launch_bounds__(kBlock) k_refit(const float* __restrict__ V, i
         lo[x] = fminf(a[x], fminf(b[x], c[x]));
         hi[x] = fmaxf(a[x], fmaxf(b[x], c[x]));
     }
-    tris[3 * k + 0] = make_float4(a[0], a[1], a[2], __int_as_float(id));
-    tris[3 * k + 1] = make_float4(b[0], b[1], b[2], 0.f);
-    tris[3 * k + 2] = make_float4(c[0], c[1], c[2], 0.f);
+    tris[4 * k + 0] = make_float4(a[0], a[1], a[2], __int_as_float(id));
+    tris[4 * k + 1] = make_float4(b[0], b[1], b[2], 0.f);
+    tris[4 * k + 2] = make_float4(c[0], c[1], c[2], 0.f);
+    tris[4 * k + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
     int32_t p = parent[n_nodes + k];
     while (true) {
         const int node = p >> 1, side = p & 1;
@@ -521,7 +522,7 @@ static rsi_status_t ensure_capacity(rsi_bvh* h, int64_t n, cudaStream_t s) {
     if (e == cudaSuccess) e = cudaMallocAsync((void**)&(ptr), (size_t)(bytes), s);
     RSI_ALLOC(h->nodes, nn * 4 * sizeof(float4));
     RSI_ALLOC(h->quads, nn * 8 * sizeof(float4));
-    RSI_ALLOC(h->tris, n * 3 * sizeof(float4));
+    RSI_ALLOC(h->tris, n * 4 * sizeof(float4));
     RSI_ALLOC(h->keys, n * sizeof(uint32_t));
     RSI_ALLOC(h->vals, n * sizeof(int32_t));
     RSI_ALLOC(h->keys_tmp, n * sizeof(uint32_t));

@@ -12,7 +12,8 @@
 //     q4 = lo.z[0..3], q5 = hi.z[0..3], q6 = ref[0..3] (int bits), q7 = unused
 //     empty slots hold a point box at +inf (never hit).  Traversing quads
 //     visits every other level of the binary tree: half the dependent fetches.
-//   tri   (48 B, 3 x float4) in Morton order: (v0, id bits), (v1, 0), (v2, 0)
+//   tri   (64 B, 4 x float4) in Morton order: (v0, id bits), (v1, 0), (v2, 0), pad
+//         (64 B so a triangle is two 256-bit loads)
 //   The vertices are stored exactly (not e1/e2) so the fp64 mirror can
 //   recompute the oracle's operation order bit-for-bit.
 #pragma once
@@ -49,7 +50,7 @@ struct rsi_bvh {
     int64_t sort_blocks_cap = 0;
     float4* nodes = nullptr;         // [4 * n_nodes]
     float4* quads = nullptr;         // [8 * n_nodes] grandchild (4-wide) records
-    float4* tris = nullptr;          // [3 * n_tri]
+    float4* tris = nullptr;          // [4 * n_tri]
     uint32_t* keys = nullptr;        // sorted Morton codes [n_tri]
     int32_t* vals = nullptr;         // sorted triangle ids [n_tri]
     uint32_t* keys_tmp = nullptr;

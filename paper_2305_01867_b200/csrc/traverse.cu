@@ -34,6 +34,10 @@ constexpr float kOutTol = 4e-6f;                 // max certified |t error| for 
 constexpr int kNoRef = (int)0x80000000;  // "no child" (never a valid ref: ~slot > INT_MIN)
 // binary: depth <= 62 of the index-augmented 62-bit key; quad: <= 31 visits x 3 pushes
 constexpr int kStack = RSI_QUAD ? 96 : 64;
+#ifndef RSI_SMEM_STACK
+#define RSI_SMEM_STACK 32
+#endif
+constexpr int kSmemStack = RSI_SMEM_STACK;  // stack entries per lane kept in shared memory
 constexpr int kCountCap = 8;  // intercept_count hits held in registers per ray
 #ifndef RSI_BOOL_MINB
 #define RSI_BOOL_MINB 8
@@ -192,10 +196,27 @@ __device__ __noinline__ int mt64(const Ray& r, const float4 A, const float4 B, c
     return (nu >= 0.0) && (nv >= 0.0) && (da(nu, nv) <= det) && (nt >= 0.0) && (nt <= det);
 }
 
+#ifndef RSI_LDG256
+#define RSI_LDG256 1
+#endif
+// 256-bit read-only global load (sm_100: LDG.E.ENL2.256): one L1 wavefront per
+// lane-line instead of two for a pair of 128-bit loads.
+__device__ __forceinline__ void ldg256(const float4* p, float4& a, float4& b) {
+#if RSI_LDG256
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w)
+        : "l"(p));
+#else
+    a = __ldg(p);
+    b = __ldg(p + 1);
+#endif
+}
+
+// triangle slot k: 64 B (4 x float4, the last one padding) for two 256-bit loads
 __device__ __forceinline__ void load_tri(const float4* __restrict__ tris, int k, float4& A, float4& B, float4& C) {
-    A = __ldg(tris + 3 * k);
-    B = __ldg(tris + 3 * k + 1);
-    C = __ldg(tris + 3 * k + 2);
+    float4 pad;
+    ldg256(tris + 4 * k, A, B);
+    ldg256(tris + 4 * k + 2, C, pad);
 }
 
 // ---------------------------------------------------------------- traversal skeleton
@@ -208,8 +229,10 @@ __device__ __forceinline__ void traverse(const float4* __restrict__ nodes, const
     int node = 0;
     while (true) {
         const float4* nd = nodes + 4 * node;
-        const float4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2);
-        const int4 n3 = __ldg(reinterpret_cast<const int4*>(nd + 3));
+        float4 n0, n1, n2, n3f;
+        ldg256(nd, n0, n1);
+        ldg256(nd + 2, n2, n3f);
+        const int4 n3 = make_int4(__float_as_int(n3f.x), __float_as_int(n3f.y), 0, 0);
         float nearL, nearR;
         bool hL = slab(r, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, tclip, nearL);
         bool hR = slab(r, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, tclip, nearR);
@@ -538,6 +561,22 @@ struct ModeState<MODE_COUNT> {
 //      lanes, while others wait with leaves) is still searching;
 //   3. leaf phase: all lanes with pending leaves run Moller-Trumbore together;
 //   4. finished rays write their outputs and free the lane.
+struct LaneStack {
+    int* s;  // this lane's shared-memory column: entry k at s[k * kThreads]
+    int local[kStack - kSmemStack];
+    __device__ __forceinline__ void push(int& sp, int x) {
+        if (sp < kSmemStack)
+            s[sp * kThreads] = x;
+        else
+            local[sp - kSmemStack] = x;
+        ++sp;
+    }
+    __device__ __forceinline__ int pop(int& sp) {
+        --sp;
+        return sp < kSmemStack ? s[sp * kThreads] : local[sp - kSmemStack];
+    }
+};
+
 // compare-and-swap of (key, ref) pairs: ascending keys
 __device__ __forceinline__ void cas(float& ka, int& ca, float& kb, int& cb) {
     const bool sw = kb < ka;
@@ -564,7 +603,11 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
     int64_t ray = -1;
     Ray r;
     int node = -1, sp = 0, l0 = -1, l1 = -1;  // l0/l1: pending (postponed) leaf slots
-    int stack[kStack];
+    // per-lane traversal stack: the first kSmemStack entries in a shared-memory
+    // column (one bank per lane: conflict-free at any depth), the rest local
+    LaneStack stk;
+    __shared__ int s_stack[kSmemStack > 0 ? kSmemStack * kThreads : 1];
+    stk.s = s_stack + threadIdx.x;
     float tclip = 1.0f;
     ModeState<MODE> ms;
     if constexpr (MODE == MODE_COUNT) {
@@ -622,9 +665,13 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             if (__popc(tm) < p.min_trav && __ballot_sync(FULL, l0 >= 0)) break;
             if (trav) {
                 const float4* q = p.quads + 8 * node;
-                const float4 q0 = __ldg(q), q1 = __ldg(q + 1), q2 = __ldg(q + 2), q3 = __ldg(q + 3);
-                const float4 q4 = __ldg(q + 4), q5 = __ldg(q + 5);
-                const int4 q6 = __ldg(reinterpret_cast<const int4*>(q + 6));
+                float4 q0, q1, q2, q3, q4, q5, q6f, q7f;
+                ldg256(q, q0, q1);
+                ldg256(q + 2, q2, q3);
+                ldg256(q + 4, q4, q5);
+                ldg256(q + 6, q6f, q7f);
+                const int4 q6 = make_int4(__float_as_int(q6f.x), __float_as_int(q6f.y), __float_as_int(q6f.z),
+                                          __float_as_int(q6f.w));
                 float k0, k1, k2, k3;
                 const bool h0 = slab(r, q0.x, q1.x, q2.x, q3.x, q4.x, q5.x, tclip, k0);
                 const bool h1 = slab(r, q0.y, q1.y, q2.y, q3.y, q4.y, q5.y, tclip, k1);
@@ -646,18 +693,18 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
                 int first = kNoRef;
                 if (c3 != kNoRef) first = c3;
                 if (c2 != kNoRef) {
-                    if (first != kNoRef) stack[sp++] = first;
+                    if (first != kNoRef) stk.push(sp, first);
                     first = c2;
                 }
                 if (c1 != kNoRef) {
-                    if (first != kNoRef) stack[sp++] = first;
+                    if (first != kNoRef) stk.push(sp, first);
                     first = c1;
                 }
                 if (c0 != kNoRef) {
-                    if (first != kNoRef) stack[sp++] = first;
+                    if (first != kNoRef) stk.push(sp, first);
                     first = c0;
                 }
-                if (first == kNoRef && sp > 0) first = stack[--sp];
+                if (first == kNoRef && sp > 0) first = stk.pop(sp);
                 if (first == kNoRef) {
                     node = -1;
                 } else if (first >= 0) {
@@ -674,11 +721,11 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             if (kCounters) st.mts += 1;
             bool done = ms.template leaf<kFP64>(p, r, l0, tclip, st);
             l0 = -1;
-            int nxt = (!done && sp > 0) ? stack[--sp] : kNoRef;
+            int nxt = (!done && sp > 0) ? stk.pop(sp) : kNoRef;
             if (nxt != kNoRef && nxt < 0) {
                 if (kCounters) st.mts += 1;
                 done = ms.template leaf<kFP64>(p, r, ~nxt, tclip, st);
-                nxt = (!done && sp > 0) ? stack[--sp] : kNoRef;
+                nxt = (!done && sp > 0) ? stk.pop(sp) : kNoRef;
             }
             if (done) {
                 node = -1;
@@ -704,8 +751,10 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             if (__popc(tm) < p.min_trav && __ballot_sync(FULL, l0 >= 0)) break;
             if (trav) {
                 const float4* nd = p.nodes + 4 * node;
-                const float4 n0 = __ldg(nd), n1 = __ldg(nd + 1), n2 = __ldg(nd + 2);
-                const int4 n3 = __ldg(reinterpret_cast<const int4*>(nd + 3));
+                float4 n0, n1, n2, n3f;
+                ldg256(nd, n0, n1);
+                ldg256(nd + 2, n2, n3f);
+                const int4 n3 = make_int4(__float_as_int(n3f.x), __float_as_int(n3f.y), 0, 0);
                 float nearL, nearR;
                 bool hL = slab(r, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, tclip, nearL);
                 bool hR = slab(r, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, tclip, nearR);
@@ -723,14 +772,14 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
                 }
                 if (hL && hR) {
                     const bool rfirst = nearR < nearL;
-                    stack[sp++] = rfirst ? n3.x : n3.y;
+                    stk.push(sp, rfirst ? n3.x : n3.y);
                     node = rfirst ? n3.y : n3.x;
                 } else if (hL) {
                     node = n3.x;
                 } else if (hR) {
                     node = n3.y;
                 } else {
-                    node = sp > 0 ? stack[--sp] : -1;
+                    node = sp > 0 ? stk.pop(sp) : -1;
                 }
             }
         }

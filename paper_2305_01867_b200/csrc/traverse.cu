@@ -25,19 +25,35 @@ constexpr float kTerr = 12.0f * kU;              // t forward-error constant
 constexpr float kSlack = 4.76837158203125e-07f;  // 2^-21: slab-test slack factor
 constexpr float kTiny = 1e-30f;                  // absolute floor (underflow)
 constexpr float kOutTol = 4e-6f;                 // max certified |t error| for fp32 outputs
-#ifndef RSI_QUAD
-#define RSI_QUAD 1
+// Per-mode traversal configuration (measured, profiles/r1_*): boolean walks
+// the binary child-pair nodes with a local-memory stack; barycentric and
+// intercept_count walk the 4-wide grandchild records, intercept_count with
+// the first stack entries in shared memory.
+#ifndef RSI_BOOL_QUAD
+#define RSI_BOOL_QUAD 0
+#endif
+#ifndef RSI_BARY_QUAD
+#define RSI_BARY_QUAD 1
+#endif
+#ifndef RSI_COUNT_QUAD
+#define RSI_COUNT_QUAD 1
+#endif
+#ifndef RSI_BOOL_SMEM
+#define RSI_BOOL_SMEM 0
+#endif
+#ifndef RSI_BARY_SMEM
+#define RSI_BARY_SMEM 0
+#endif
+#ifndef RSI_COUNT_SMEM
+#define RSI_COUNT_SMEM 32
 #endif
 #ifndef RSI_SORT_ALL
 #define RSI_SORT_ALL 1
 #endif
 constexpr int kNoRef = (int)0x80000000;  // "no child" (never a valid ref: ~slot > INT_MIN)
 // binary: depth <= 62 of the index-augmented 62-bit key; quad: <= 31 visits x 3 pushes
-constexpr int kStack = RSI_QUAD ? 96 : 64;
-#ifndef RSI_SMEM_STACK
-#define RSI_SMEM_STACK 32
-#endif
-constexpr int kSmemStack = RSI_SMEM_STACK;  // stack entries per lane kept in shared memory
+constexpr int kStackBinary = 64;
+constexpr int kStackQuad = 96;
 constexpr int kCountCap = 8;  // intercept_count hits held in registers per ray
 #ifndef RSI_BOOL_MINB
 #define RSI_BOOL_MINB 8
@@ -224,7 +240,7 @@ __device__ __forceinline__ void load_tri(const float4* __restrict__ tris, int k,
 template <class LeafFn>
 __device__ __forceinline__ void traverse(const float4* __restrict__ nodes, const Ray& r, float& tclip,
                                          LeafFn&& leaf) {
-    int stack[kStack];
+    int stack[kStackBinary];
     int sp = 0;
     int node = 0;
     while (true) {
@@ -561,6 +577,7 @@ struct ModeState<MODE_COUNT> {
 //      lanes, while others wait with leaves) is still searching;
 //   3. leaf phase: all lanes with pending leaves run Moller-Trumbore together;
 //   4. finished rays write their outputs and free the lane.
+template <int kStack, int kSmemStack>
 struct LaneStack {
     int* s;  // this lane's shared-memory column: entry k at s[k * kThreads]
     int local[kStack - kSmemStack];
@@ -594,6 +611,9 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
     constexpr bool kSort = (MODE == MODE_BARY) || RSI_SORT_ALL;
+    constexpr bool kQuad = MODE == MODE_BOOL ? RSI_BOOL_QUAD : (MODE == MODE_BARY ? RSI_BARY_QUAD : RSI_COUNT_QUAD);
+    constexpr int kSmemStack = MODE == MODE_BOOL ? RSI_BOOL_SMEM : (MODE == MODE_BARY ? RSI_BARY_SMEM : RSI_COUNT_SMEM);
+    constexpr int kStack = kQuad ? kStackQuad : kStackBinary;
     __shared__ float2 s_te[MODE == MODE_COUNT ? kCountCap * kThreads : 1];
     __shared__ int s_k[MODE == MODE_COUNT ? kCountCap * kThreads : 1];
     Stats st;
@@ -605,7 +625,7 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
     int node = -1, sp = 0, l0 = -1, l1 = -1;  // l0/l1: pending (postponed) leaf slots
     // per-lane traversal stack: the first kSmemStack entries in a shared-memory
     // column (one bank per lane: conflict-free at any depth), the rest local
-    LaneStack stk;
+    LaneStack<kStack, kSmemStack> stk;
     __shared__ int s_stack[kSmemStack > 0 ? kSmemStack * kThreads : 1];
     stk.s = s_stack + threadIdx.x;
     float tclip = 1.0f;
@@ -653,7 +673,7 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
         }
         if (__ballot_sync(FULL, ray >= 0) == 0) break;  // no rays left for this warp
 
-#if RSI_QUAD
+        if constexpr (kQuad) {
         // ---- 2. traversal phase (4-wide view: a visit tests the up-to-4
         // grandchildren of a binary node; hit children are ordered near-first
         // (kSort) or by slot, the first becomes the next visit and the rest go
@@ -740,7 +760,7 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             }
         }
 
-#else
+        } else {
         // ---- 2. traversal phase
         // a lane walks internal nodes until it holds a pending leaf (l0, and l1
         // when both children of the visited node are leaves)
@@ -792,8 +812,8 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             l0 = l1 = -1;
             if (done) node = -1;
         }
+        }
 
-#endif
         // ---- 4. finish
         if (ray >= 0 && node < 0 && l0 < 0) {
             ms.finish(p, r, ray, st);

@@ -284,6 +284,7 @@ rsi_status_t rsi_free(rsi_handle_t h) {
             if (st == RSI_OK) st = e;
         }
     if (h->h_pinned) cudaFreeHost(h->h_pinned);
+    if (h->tex_nodes) cudaDestroyTextureObject(h->tex_nodes);
     delete h;
     return st;
 }

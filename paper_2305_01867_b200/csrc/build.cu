@@ -598,6 +598,23 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
         h->scene_lo[x] = root[x];
         h->scene_hi[x] = root[3 + x];
     }
+    if (h->tex_nodes) {
+        cudaDestroyTextureObject(h->tex_nodes);
+        h->tex_nodes = 0;
+    }
+    {
+        cudaResourceDesc rd{};
+        rd.resType = cudaResourceTypeLinear;
+        rd.res.linear.devPtr = h->nodes;
+        rd.res.linear.desc = cudaCreateChannelDesc<float4>();
+        rd.res.linear.sizeInBytes = (size_t)n_nodes * 4 * sizeof(float4);
+        cudaTextureDesc td{};
+        td.readMode = cudaReadModeElementType;
+        if (cudaCreateTextureObject(&h->tex_nodes, &rd, &td, nullptr) != cudaSuccess) {
+            (void)cudaGetLastError();
+            h->tex_nodes = 0;
+        }
+    }
     h->n_tri = nt;
     h->n_nodes = n_nodes;
     h->stream = s;

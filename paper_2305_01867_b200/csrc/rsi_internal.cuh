@@ -50,6 +50,7 @@ struct rsi_bvh {
     int64_t sort_blocks_cap = 0;
     float4* nodes = nullptr;         // [4 * n_nodes]
     float4* quads = nullptr;         // [8 * n_nodes] grandchild (4-wide) records
+    cudaTextureObject_t tex_nodes = 0;  // texture view of `nodes` (recreated on rebuild)
     float4* tris = nullptr;          // [4 * n_tri]
     uint32_t* keys = nullptr;        // sorted Morton codes [n_tri]
     int32_t* vals = nullptr;         // sorted triangle ids [n_tri]

@@ -212,6 +212,9 @@ __device__ __noinline__ int mt64(const Ray& r, const float4 A, const float4 B, c
     return (nu >= 0.0) && (nv >= 0.0) && (da(nu, nv) <= det) && (nt >= 0.0) && (nt <= det);
 }
 
+#ifndef RSI_TEX_NODES
+#define RSI_TEX_NODES 0
+#endif
 #ifndef RSI_LDG256
 #define RSI_LDG256 1
 #endif
@@ -312,6 +315,7 @@ enum { MODE_BOOL = 0, MODE_BARY = 1, MODE_COUNT = 2 };
 
 struct TraceParams {
     const float4* nodes;
+    cudaTextureObject_t tex_nodes;  // same array through the texture path (RSI_TEX_NODES)
     const float4* quads;
     const float4* tris;
     const float* S;
@@ -770,10 +774,17 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             if (tm == 0) break;
             if (__popc(tm) < p.min_trav && __ballot_sync(FULL, l0 >= 0)) break;
             if (trav) {
+#if RSI_TEX_NODES
+                const float4 n0 = tex1Dfetch<float4>(p.tex_nodes, 4 * node);
+                const float4 n1 = tex1Dfetch<float4>(p.tex_nodes, 4 * node + 1);
+                const float4 n2 = tex1Dfetch<float4>(p.tex_nodes, 4 * node + 2);
+                const float4 n3f = tex1Dfetch<float4>(p.tex_nodes, 4 * node + 3);
+#else
                 const float4* nd = p.nodes + 4 * node;
                 float4 n0, n1, n2, n3f;
                 ldg256(nd, n0, n1);
                 ldg256(nd + 2, n2, n3f);
+#endif
                 const int4 n3 = make_int4(__float_as_int(n3f.x), __float_as_int(n3f.y), 0, 0);
                 float nearL, nearR;
                 bool hL = slab(r, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, tclip, nearL);
@@ -1044,6 +1055,7 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     if (st != RSI_OK) return st;
     TraceParams p{};
     p.nodes = h->nodes;
+    p.tex_nodes = h->tex_nodes;
     p.quads = h->quads;
     p.tris = h->tris;
     p.S = S;

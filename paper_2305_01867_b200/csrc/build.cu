@@ -455,20 +455,61 @@ __global__ void __launch_bounds__(kBlock) k_refit(const float* __restrict__ V, i
 }
 
 // ------------------------------------------------------------------ 4-wide view (grandchild records)
-// One thread per internal node n: gather the boxes and refs of n's
-// grandchildren from the child-pair records of n and of its internal children.
+// One thread per internal node n: the up-to-4 grandchildren of n (a leaf child
+// stands for itself), their AABBs quantized to 8 bits on a per-axis
+// power-of-two grid anchored at an origin p that is itself a multiple of the
+// grid step s = 2^e:  lo' = p + qlo*s <= lo,  hi' = p + qhi*s >= hi  (exact:
+// computed in double; |p/s| < 2^24 keeps p + q*s exactly representable, so the
+// traversal's decode is exact, and directed rounding keeps it conservative
+// otherwise).  64 B per record = two 256-bit loads.
+//   w0..w2  p.x, p.y, p.z (float)        w3  e_x+128 | e_y+128<<8 | e_z+128<<16 | valid<<24
+//   w4..w9  qlo.x, qhi.x, qlo.y, qhi.y, qlo.z, qhi.z   (byte j = child j)
+//   w10..w13 ref[0..3]                   w14, w15 unused
+constexpr int kQuadEMin = -126, kQuadEMax = 104;  // s and s*2^23 stay normal floats
+
+__device__ __forceinline__ void quant_axis(const float* lo, const float* hi, int cnt, uint32_t& wlo, uint32_t& whi,
+                                           float& p_out, int& e_out, bool& ok) {
+    float nlo = INFINITY, nhi = -INFINITY;
+    for (int j = 0; j < cnt; ++j) {
+        nlo = fminf(nlo, lo[j]);
+        nhi = fmaxf(nhi, hi[j]);
+    }
+    const double ext = (double)nhi - (double)nlo;
+    int e = kQuadEMin;
+    if (ext > 0.0) {
+        int ex;
+        frexp(ext / 255.0, &ex);  // ext/255 < 2^ex
+        e = ex - 1;
+        if (e < kQuadEMin) e = kQuadEMin;
+    }
+    double sc, p;
+    while (true) {
+        sc = ldexp(1.0, e);
+        p = floor((double)nlo / sc) * sc;  // multiple of s, p <= nlo
+        // covers the node, and p = k*s with |k| < 2^23 so p and p - 2^23 s are exact floats
+        if (((double)nhi - p <= 255.0 * sc && fabs(p / sc) < 8388608.0) || e >= kQuadEMax) break;
+        ++e;
+    }
+    wlo = 0u;
+    whi = 0u;
+    for (int j = 0; j < cnt; ++j) {
+        double ql = floor(((double)lo[j] - p) / sc), qh = ceil(((double)hi[j] - p) / sc);
+        ql = fmin(fmax(ql, 0.0), 255.0);
+        qh = fmin(fmax(qh, 0.0), 255.0);
+        wlo |= (uint32_t)ql << (8 * j);
+        whi |= (uint32_t)qh << (8 * j);
+    }
+    p_out = (float)p;  // exact (|p/s| < 2^23)
+    e_out = e;
+    ok = ((double)nhi - p <= 255.0 * sc) && fabs(p / sc) < 8388608.0 && (double)p_out == p;
+}
+
 __global__ void __launch_bounds__(kBlock) k_quads(const float4* __restrict__ nodes, int n_nodes,
-                                                  float4* __restrict__ quads) {
+                                                  float4* __restrict__ quads, uint32_t* scratch) {
     int n = blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= n_nodes) return;
     float lo[3][4], hi[3][4];
-    int ref[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-#pragma unroll
-        for (int a = 0; a < 3; ++a) lo[a][j] = hi[a][j] = INFINITY;
-        ref[j] = ~0;
-    }
+    int ref[4] = {0, 0, 0, 0};
     int k = 0;
     const float4* nd = nodes + 4 * n;
     const float4 n0 = nd[0], n1 = nd[1], n2 = nd[2];
@@ -480,6 +521,7 @@ __global__ void __launch_bounds__(kBlock) k_quads(const float4* __restrict__ nod
     for (int side = 0; side < 2; ++side) {
         const int c = cr[side];
         if (c < 0) {  // leaf child stands for itself
+            if (cb[side].x == INFINITY) continue;  // the empty right slot of a 1-triangle tree
             lo[0][k] = cb[side].x; hi[0][k] = cb[side].y; lo[1][k] = cb[side].z; hi[1][k] = cb[side].w;
             lo[2][k] = cz[side][0]; hi[2][k] = cz[side][1];
             ref[k] = c;
@@ -496,15 +538,28 @@ __global__ void __launch_bounds__(kBlock) k_quads(const float4* __restrict__ nod
             ++k;
         }
     }
-    float4* q = quads + 8 * n;
-    q[0] = make_float4(lo[0][0], lo[0][1], lo[0][2], lo[0][3]);
-    q[1] = make_float4(hi[0][0], hi[0][1], hi[0][2], hi[0][3]);
-    q[2] = make_float4(lo[1][0], lo[1][1], lo[1][2], lo[1][3]);
-    q[3] = make_float4(hi[1][0], hi[1][1], hi[1][2], hi[1][3]);
-    q[4] = make_float4(lo[2][0], lo[2][1], lo[2][2], lo[2][3]);
-    q[5] = make_float4(hi[2][0], hi[2][1], hi[2][2], hi[2][3]);
-    q[6] = make_float4(__int_as_float(ref[0]), __int_as_float(ref[1]), __int_as_float(ref[2]), __int_as_float(ref[3]));
-    q[7] = make_float4(0.f, 0.f, 0.f, 0.f);
+    uint32_t w[16];
+    float px[3];
+    int ex[3];
+    bool ok = true;
+    for (int a = 0; a < 3; ++a) {
+        bool oka;
+        quant_axis(lo[a], hi[a], k, w[4 + 2 * a], w[5 + 2 * a], px[a], ex[a], oka);
+        ok = ok && oka;
+    }
+    if (!ok) atomicOr(&scratch[SCR_STATUS], STATUS_RANGE);  // coordinates beyond ~1e33
+    w[0] = __float_as_uint(px[0]);
+    w[1] = __float_as_uint(px[1]);
+    w[2] = __float_as_uint(px[2]);
+    w[3] = (uint32_t)(ex[0] + 128) | ((uint32_t)(ex[1] + 128) << 8) | ((uint32_t)(ex[2] + 128) << 16) |
+           (((1u << k) - 1u) << 24);
+    for (int j = 0; j < 4; ++j) w[10 + j] = (uint32_t)ref[j];
+    w[14] = w[15] = 0u;
+    uint4* q = reinterpret_cast<uint4*>(quads + 4 * n);
+    q[0] = make_uint4(w[0], w[1], w[2], w[3]);
+    q[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    q[2] = make_uint4(w[8], w[9], w[10], w[11]);
+    q[3] = make_uint4(w[12], w[13], w[14], w[15]);
 }
 
 }  // namespace
@@ -521,7 +576,7 @@ static rsi_status_t ensure_capacity(rsi_bvh* h, int64_t n, cudaStream_t s) {
 #define RSI_ALLOC(ptr, bytes) \
     if (e == cudaSuccess) e = cudaMallocAsync((void**)&(ptr), (size_t)(bytes), s);
     RSI_ALLOC(h->nodes, nn * 4 * sizeof(float4));
-    RSI_ALLOC(h->quads, nn * 8 * sizeof(float4));
+    RSI_ALLOC(h->quads, nn * 4 * sizeof(float4));
     RSI_ALLOC(h->tris, n * 4 * sizeof(float4));
     RSI_ALLOC(h->keys, n * sizeof(uint32_t));
     RSI_ALLOC(h->vals, n * sizeof(int32_t));
@@ -581,7 +636,7 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
     k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent, h->arrivals);
     k_refit<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, h->vals, n, h->nodes, h->tris, h->parent,
                                                         h->arrivals, h->scratch);
-    k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads);
+    k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads, h->scratch);
     st = rsi_cuda_check(cudaGetLastError(), "build kernel launch");
     if (st != RSI_OK) return st;
     st = rsi_cuda_check(cudaMemcpyAsync(h->h_pinned, h->scratch, SCR_WORDS * sizeof(uint32_t),
@@ -593,6 +648,8 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
     uint32_t status = h->h_pinned[SCR_STATUS];
     if (status & STATUS_INDEX) return rsi_set_error(RSI_E_INDEX_RANGE, "a triangle index is outside [0, %lld)", (long long)nv);
     if (status & STATUS_NONFINITE) return rsi_set_error(RSI_E_NONFINITE, "a vertex coordinate is NaN or Inf");
+    if (status & STATUS_RANGE)
+        return rsi_set_error(RSI_E_INVALID_ARG, "mesh extent too large for the quantized BVH (|coordinates| > ~1e33)");
     const float* root = reinterpret_cast<const float*>(h->h_pinned + SCR_ROOT);
     for (int x = 0; x < 3; ++x) {
         h->scene_lo[x] = root[x];

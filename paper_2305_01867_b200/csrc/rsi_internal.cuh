@@ -6,12 +6,10 @@
 //     n1 = (R.lo.x, R.hi.x, R.lo.y, R.hi.y)
 //     n2 = (L.lo.z, L.hi.z, R.lo.z, R.hi.z)
 //     n3 = (ref L, ref R, 0, 0) as int bits; ref >= 0 internal node, < 0 leaf ~slot
-//   quad  (128 B, 8 x float4) -- for every internal node n, the AABBs and refs
-//         of its up-to-4 grandchildren (a child that is a leaf stands for itself):
-//     q0 = lo.x[0..3], q1 = hi.x[0..3], q2 = lo.y[0..3], q3 = hi.y[0..3],
-//     q4 = lo.z[0..3], q5 = hi.z[0..3], q6 = ref[0..3] (int bits), q7 = unused
-//     empty slots hold a point box at +inf (never hit).  Traversing quads
-//     visits every other level of the binary tree: half the dependent fetches.
+//   quad  (64 B, 4 x float4) -- for every internal node n, its up-to-4
+//         grandchildren (a leaf child stands for itself) with 8-bit quantized
+//         AABBs on a power-of-two grid (see k_quads in build.cu); traversing
+//         quads visits every other level of the binary tree.
 //   tri   (64 B, 4 x float4) in Morton order: (v0, id bits), (v1, 0), (v2, 0), pad
 //         (64 B so a triangle is two 256-bit loads)
 //   The vertices are stored exactly (not e1/e2) so the fp64 mirror can
@@ -36,7 +34,7 @@ enum {
     SCR_DISPENSER = 18, // 2 words: 64-bit ray dispenser of the persistent traversal grid
     SCR_WORDS = 32
 };
-enum { STATUS_INDEX = 1u, STATUS_NONFINITE = 2u };
+enum { STATUS_INDEX = 1u, STATUS_NONFINITE = 2u, STATUS_RANGE = 4u };
 
 // stats counters (unsigned long long) in rsi_bvh::stats
 enum { ST_RAYS = 0, ST_FP64_PAIRS, ST_FP64_RAYS, ST_OVERFLOW, ST_NONFINITE, ST_BOX_TESTS, ST_MT_TESTS, ST_WORDS };
@@ -49,7 +47,7 @@ struct rsi_bvh {
     int64_t cap_tri = 0;             // allocated capacity (triangles)
     int64_t sort_blocks_cap = 0;
     float4* nodes = nullptr;         // [4 * n_nodes]
-    float4* quads = nullptr;         // [8 * n_nodes] grandchild (4-wide) records
+    float4* quads = nullptr;         // [4 * n_nodes] compressed grandchild (4-wide) records
     cudaTextureObject_t tex_nodes = 0;  // texture view of `nodes` (recreated on rebuild)
     float4* tris = nullptr;          // [4 * n_tri]
     uint32_t* keys = nullptr;        // sorted Morton codes [n_tri]

@@ -688,19 +688,45 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             if (tm == 0) break;
             if (__popc(tm) < p.min_trav && __ballot_sync(FULL, l0 >= 0)) break;
             if (trav) {
-                const float4* q = p.quads + 8 * node;
-                float4 q0, q1, q2, q3, q4, q5, q6f, q7f;
-                ldg256(q, q0, q1);
-                ldg256(q + 2, q2, q3);
-                ldg256(q + 4, q4, q5);
-                ldg256(q + 6, q6f, q7f);
-                const int4 q6 = make_int4(__float_as_int(q6f.x), __float_as_int(q6f.y), __float_as_int(q6f.z),
-                                          __float_as_int(q6f.w));
+                const float4* q = p.quads + 4 * node;
+                float4 qa, qb, qc, qd;
+                ldg256(q, qa, qb);
+                ldg256(q + 2, qc, qd);
+                const uint32_t w3 = __float_as_uint(qa.w);
+                const uint32_t vmask = w3 >> 24;
+                // per axis: grid step s = 2^e, s*2^23, and the decode offsets p - 2^23 s
+                // (exact when the record's |p/s| < 2^23; rounded outward otherwise)
+                float sc[3], plo[3], phi[3];
+                const float pp[3] = {qa.x, qa.y, qa.z};
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const uint32_t eb = (w3 >> (8 * a)) & 255u;
+                    sc[a] = __uint_as_float((eb - 1u) << 23);
+                    const float s23 = __uint_as_float((eb + 22u) << 23);
+                    plo[a] = __fsub_rd(pp[a], s23);
+                    phi[a] = __fsub_ru(pp[a], s23);
+                }
+                const uint32_t wq[6] = {__float_as_uint(qb.x), __float_as_uint(qb.y), __float_as_uint(qb.z),
+                                        __float_as_uint(qb.w), __float_as_uint(qc.x), __float_as_uint(qc.y)};
+                const int4 q6 = make_int4(__float_as_int(qc.z), __float_as_int(qc.w), __float_as_int(qd.x),
+                                          __float_as_int(qd.y));
+                // child j plane: (2^23 + q) * s + (p - 2^23 s) = p + q s, rounded outward
+                auto dec_lo = [&](int a, int j) {
+                    return __fmaf_rd(__uint_as_float(__byte_perm(wq[2 * a], 0x4B000000u, 0x7440u + j)), sc[a], plo[a]);
+                };
+                auto dec_hi = [&](int a, int j) {
+                    return __fmaf_ru(__uint_as_float(__byte_perm(wq[2 * a + 1], 0x4B000000u, 0x7440u + j)), sc[a],
+                                     phi[a]);
+                };
                 float k0, k1, k2, k3;
-                const bool h0 = slab(r, q0.x, q1.x, q2.x, q3.x, q4.x, q5.x, tclip, k0);
-                const bool h1 = slab(r, q0.y, q1.y, q2.y, q3.y, q4.y, q5.y, tclip, k1);
-                const bool h2 = slab(r, q0.z, q1.z, q2.z, q3.z, q4.z, q5.z, tclip, k2);
-                const bool h3 = slab(r, q0.w, q1.w, q2.w, q3.w, q4.w, q5.w, tclip, k3);
+                const bool h0 = ((vmask & 1u) != 0u) & slab(r, dec_lo(0, 0), dec_hi(0, 0), dec_lo(1, 0), dec_hi(1, 0),
+                                                     dec_lo(2, 0), dec_hi(2, 0), tclip, k0);
+                const bool h1 = ((vmask & 2u) != 0u) & slab(r, dec_lo(0, 1), dec_hi(0, 1), dec_lo(1, 1), dec_hi(1, 1),
+                                                     dec_lo(2, 1), dec_hi(2, 1), tclip, k1);
+                const bool h2 = ((vmask & 4u) != 0u) & slab(r, dec_lo(0, 2), dec_hi(0, 2), dec_lo(1, 2), dec_hi(1, 2),
+                                                     dec_lo(2, 2), dec_hi(2, 2), tclip, k2);
+                const bool h3 = ((vmask & 8u) != 0u) & slab(r, dec_lo(0, 3), dec_hi(0, 3), dec_lo(1, 3), dec_hi(1, 3),
+                                                     dec_lo(2, 3), dec_hi(2, 3), tclip, k3);
                 if (kCounters) st.boxes += 4;
                 int c0 = h0 ? q6.x : kNoRef, c1 = h1 ? q6.y : kNoRef, c2 = h2 ? q6.z : kNoRef, c3 = h3 ? q6.w : kNoRef;
                 if (kSort) {

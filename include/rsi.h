@@ -104,6 +104,11 @@ typedef struct {
     uint64_t nonfinite_rays; /* rays with a NaN/Inf coordinate (reported as misses)       */
     uint64_t box_tests;      /* child-box slab tests (RSI_OPT_COUNTERS only, else 0)      */
     uint64_t mt_tests;       /* Moller-Trumbore tests (RSI_OPT_COUNTERS only, else 0)     */
+    /* SIMT-efficiency diagnostics (RSI_OPT_COUNTERS only): summed over traversal
+       iterations of every warp, the lanes searching / holding a pending leaf /
+       idle (no ray or finished), the iteration count, and for leaf phases the
+       lanes testing a leaf and the number of phases. */
+    uint64_t it_search, it_pending, it_idle, iterations, leaf_lanes, leaf_phases;
 } rsi_stats_t;
 
 /* Library version string, e.g. "rsi-b200 0.1.0 sm_100a". */

@@ -303,6 +303,12 @@ rsi_status_t rsi_get_stats(rsi_handle_t h, rsi_stats_t* out, void* stream) {
     out->nonfinite_rays = v[ST_NONFINITE];
     out->box_tests = v[ST_BOX_TESTS];
     out->mt_tests = v[ST_MT_TESTS];
+    out->it_search = v[ST_IT_SEARCH];
+    out->it_pending = v[ST_IT_PEND];
+    out->it_idle = v[ST_IT_IDLE];
+    out->iterations = v[ST_ITERS];
+    out->leaf_lanes = v[ST_LEAF_LANES];
+    out->leaf_phases = v[ST_LEAF_PHASES];
     return RSI_OK;
 }
 

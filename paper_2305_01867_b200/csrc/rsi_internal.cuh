@@ -37,7 +37,12 @@ enum {
 enum { STATUS_INDEX = 1u, STATUS_NONFINITE = 2u, STATUS_RANGE = 4u };
 
 // stats counters (unsigned long long) in rsi_bvh::stats
-enum { ST_RAYS = 0, ST_FP64_PAIRS, ST_FP64_RAYS, ST_OVERFLOW, ST_NONFINITE, ST_BOX_TESTS, ST_MT_TESTS, ST_WORDS };
+enum {
+    ST_RAYS = 0, ST_FP64_PAIRS, ST_FP64_RAYS, ST_OVERFLOW, ST_NONFINITE, ST_BOX_TESTS, ST_MT_TESTS,
+    // SIMT-efficiency diagnostics (RSI_OPT_COUNTERS): lane-iterations by state
+    ST_IT_SEARCH, ST_IT_PEND, ST_IT_IDLE, ST_ITERS, ST_LEAF_LANES, ST_LEAF_PHASES,
+    ST_WORDS
+};
 
 struct rsi_bvh {
     int device = 0;

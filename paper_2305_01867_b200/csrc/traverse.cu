@@ -686,6 +686,15 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             const bool trav = node >= 0 && l0 < 0;
             const unsigned tm = __ballot_sync(FULL, trav);
             if (tm == 0) break;
+            if (kCounters && lane == 0) {
+                const unsigned pm = __popc(__ballot_sync(FULL, l0 >= 0));
+                st.c[ST_IT_SEARCH] += __popc(tm);
+                st.c[ST_IT_PEND] += pm;
+                st.c[ST_IT_IDLE] += 32u - __popc(tm) - pm;
+                st.c[ST_ITERS] += 1;
+            } else if (kCounters) {
+                __ballot_sync(FULL, l0 >= 0);
+            }
             if (__popc(tm) < p.min_trav && __ballot_sync(FULL, l0 >= 0)) break;
             if (trav) {
                 const float4* q = p.quads + 4 * node;
@@ -767,6 +776,13 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
         }
 
         // ---- 3. leaf phase (up to two leaves in a row from the stack)
+        if (kCounters) {
+            const unsigned lm = __popc(__ballot_sync(FULL, l0 >= 0));
+            if (lane == 0 && lm) {
+                st.c[ST_LEAF_LANES] += lm;
+                st.c[ST_LEAF_PHASES] += 1;
+            }
+        }
         if (l0 >= 0) {
             if (kCounters) st.mts += 1;
             bool done = ms.template leaf<kFP64>(p, r, l0, tclip, st);
@@ -798,6 +814,15 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             const bool trav = node >= 0 && l0 < 0;
             const unsigned tm = __ballot_sync(FULL, trav);
             if (tm == 0) break;
+            if (kCounters && lane == 0) {
+                const unsigned pm = __popc(__ballot_sync(FULL, l0 >= 0));
+                st.c[ST_IT_SEARCH] += __popc(tm);
+                st.c[ST_IT_PEND] += pm;
+                st.c[ST_IT_IDLE] += 32u - __popc(tm) - pm;
+                st.c[ST_ITERS] += 1;
+            } else if (kCounters) {
+                __ballot_sync(FULL, l0 >= 0);
+            }
             if (__popc(tm) < p.min_trav && __ballot_sync(FULL, l0 >= 0)) break;
             if (trav) {
 #if RSI_TEX_NODES
@@ -842,6 +867,13 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
         }
 
         // ---- 3. leaf phase
+        if (kCounters) {
+            const unsigned lm = __popc(__ballot_sync(FULL, l0 >= 0));
+            if (lane == 0 && lm) {
+                st.c[ST_LEAF_LANES] += lm;
+                st.c[ST_LEAF_PHASES] += 1;
+            }
+        }
         if (l0 >= 0) {
             if (kCounters) st.mts += 1 + (l1 >= 0);
             bool done = ms.template leaf<kFP64>(p, r, l0, tclip, st);

@@ -51,7 +51,8 @@ class _Outputs(ctypes.Structure):
 
 class _Stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_uint64) for n in ("rays", "fp64_pairs", "fp64_rays", "overflow_rays", "nonfinite_rays",
-                                               "box_tests", "mt_tests")]
+                                               "box_tests", "mt_tests", "it_search", "it_pending", "it_idle",
+                                               "iterations", "leaf_lanes", "leaf_phases")]
 
 
 def lib_path() -> str:

@@ -37,5 +37,10 @@ for mode in ("boolean", "barycentric", "intercept_count"):
     rsi.rsi_intersect(hc, Sd, Ed, mode)
     st = rsi.rsi_get_stats(hc)
     res[f"work/{mode}"] = {"box_per_ray": st["box_tests"] / n, "mt_per_ray": st["mt_tests"] / n,
-                           "fp64_pairs": st["fp64_pairs"], "fp64_rays": st["fp64_rays"], "overflow": st["overflow_rays"]}
+                           "fp64_pairs": st["fp64_pairs"], "fp64_rays": st["fp64_rays"], "overflow": st["overflow_rays"],
+                           "trav_eff": st["it_search"] / max(1, 32 * st["iterations"]),
+                           "trav_pend": st["it_pending"] / max(1, 32 * st["iterations"]),
+                           "trav_idle": st["it_idle"] / max(1, 32 * st["iterations"]),
+                           "iters_per_ray": st["iterations"] * 32 / n,
+                           "leaf_eff": st["leaf_lanes"] / max(1, 32 * st["leaf_phases"])}
 [print(k, json.dumps(v)) for k, v in res.items()]

@@ -215,6 +215,9 @@ __device__ __noinline__ int mt64(const Ray& r, const float4 A, const float4 B, c
 #ifndef RSI_TEX_NODES
 #define RSI_TEX_NODES 0
 #endif
+#ifndef RSI_SPEC
+#define RSI_SPEC 1
+#endif
 #ifndef RSI_LDG256
 #define RSI_LDG256 1
 #endif
@@ -626,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
     bool exhausted = false;       // warp-uniform
     int64_t ray = -1;
     Ray r;
-    int node = -1, sp = 0, l0 = -1, l1 = -1;  // l0/l1: pending (postponed) leaf slots
+    int node = -1, sp = 0, l0 = -1, l1 = -1, l2 = -1;  // pending (postponed) leaf slots
     // per-lane traversal stack: the first kSmemStack entries in a shared-memory
     // column (one bank per lane: conflict-free at any depth), the rest local
     LaneStack<kStack, kSmemStack> stk;
@@ -672,7 +675,7 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             ms.init();
             tclip = 1.0f;
             sp = 0;
-            l0 = l1 = -1;
+            l0 = l1 = l2 = -1;
             node = ok ? 0 : -1;
         }
         if (__ballot_sync(FULL, ray >= 0) == 0) break;  // no rays left for this warp
@@ -824,7 +827,9 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
                 __ballot_sync(FULL, l0 >= 0);
             }
             if (__popc(tm) < p.min_trav && __ballot_sync(FULL, l0 >= 0)) break;
-            if (trav) {
+            // RSI_SPEC: a lane holding one pending leaf keeps walking in slots it
+            // would otherwise idle in (its new leaves queue in l1, l2)
+            if (trav || (RSI_SPEC && node >= 0 && l1 < 0)) {
 #if RSI_TEX_NODES
                 const float4 n0 = tex1Dfetch<float4>(p.tex_nodes, 4 * node);
                 const float4 n1 = tex1Dfetch<float4>(p.tex_nodes, 4 * node + 1);
@@ -842,14 +847,19 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
                 bool hR = slab(r, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, tclip, nearR);
                 if (kCounters) st.boxes += 2;
                 if (hL && n3.x < 0) {
-                    l0 = ~n3.x;
+                    if (l0 < 0)
+                        l0 = ~n3.x;
+                    else
+                        l1 = ~n3.x;
                     hL = false;
                 }
                 if (hR && n3.y < 0) {
                     if (l0 < 0)
                         l0 = ~n3.y;
-                    else
+                    else if (l1 < 0)
                         l1 = ~n3.y;
+                    else
+                        l2 = ~n3.y;
                     hR = false;
                 }
                 if (hL && hR) {
@@ -875,10 +885,11 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             }
         }
         if (l0 >= 0) {
-            if (kCounters) st.mts += 1 + (l1 >= 0);
+            if (kCounters) st.mts += 1 + (l1 >= 0) + (l2 >= 0);
             bool done = ms.template leaf<kFP64>(p, r, l0, tclip, st);
             if (!done && l1 >= 0) done = ms.template leaf<kFP64>(p, r, l1, tclip, st);
-            l0 = l1 = -1;
+            if (!done && l2 >= 0) done = ms.template leaf<kFP64>(p, r, l2, tclip, st);
+            l0 = l1 = l2 = -1;
             if (done) node = -1;
         }
         }

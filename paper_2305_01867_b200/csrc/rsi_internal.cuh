@@ -70,7 +70,7 @@ struct rsi_bvh {
     int64_t ovf_cap = 0;
     float scene_lo[3] = {0, 0, 0}, scene_hi[3] = {0, 0, 0};
     uint64_t host_rays = 0, host_overflow = 0;  // counters known on the host
-    int min_trav = 8;  // traversal-phase exit threshold (lanes still searching); env RSI_MIN_TRAV
+    int min_trav = -1;  // traversal-phase exit threshold (-1: per-mode default); env RSI_MIN_TRAV
 };
 
 // ---------------------------------------------------------------- host helpers (api.cu)
@@ -86,6 +86,7 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* d_vertices, int64_t n_ver
 rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* d_start, const float* d_end,
                                   int64_t n_rays, int32_t mode, const rsi_outputs_t* out,
                                   cudaStream_t stream);
+bool rsi_uses_quads();  // traverse.cu: does any mode walk the 4-wide records
 rsi_status_t rsi_compact_device(const int32_t* d_tri, int64_t n_rays, int32_t* d_ids,
                                 int32_t* d_n, cudaStream_t stream);
 

@@ -25,18 +25,18 @@ constexpr float kTerr = 12.0f * kU;              // t forward-error constant
 constexpr float kSlack = 4.76837158203125e-07f;  // 2^-21: slab-test slack factor
 constexpr float kTiny = 1e-30f;                  // absolute floor (underflow)
 constexpr float kOutTol = 4e-6f;                 // max certified |t error| for fp32 outputs
-// Per-mode traversal configuration (measured, profiles/r1_*): boolean walks
-// the binary child-pair nodes with a local-memory stack; barycentric and
-// intercept_count walk the 4-wide grandchild records, intercept_count with
-// the first stack entries in shared memory.
+// Per-mode traversal configuration.  Measured on B200 (round 1): all modes
+// walk the binary child-pair nodes with speculative traversal and a
+// local-memory stack; the compressed 4-wide records (RSI_*_QUAD) and
+// shared-memory stacks (RSI_*_SMEM) were slower and stay as build options.
 #ifndef RSI_BOOL_QUAD
 #define RSI_BOOL_QUAD 0
 #endif
 #ifndef RSI_BARY_QUAD
-#define RSI_BARY_QUAD 1
+#define RSI_BARY_QUAD 0
 #endif
 #ifndef RSI_COUNT_QUAD
-#define RSI_COUNT_QUAD 1
+#define RSI_COUNT_QUAD 0
 #endif
 #ifndef RSI_BOOL_SMEM
 #define RSI_BOOL_SMEM 0
@@ -45,8 +45,9 @@ constexpr float kOutTol = 4e-6f;                 // max certified |t error| for 
 #define RSI_BARY_SMEM 0
 #endif
 #ifndef RSI_COUNT_SMEM
-#define RSI_COUNT_SMEM 32
+#define RSI_COUNT_SMEM 0
 #endif
+#define RSI_ANY_QUAD (RSI_BOOL_QUAD || RSI_BARY_QUAD || RSI_COUNT_QUAD)
 #ifndef RSI_SORT_ALL
 #define RSI_SORT_ALL 1
 #endif
@@ -1141,7 +1142,8 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     p.scratch = h->scratch;
     p.stats = h->stats;
     p.counter = reinterpret_cast<unsigned long long*>(h->scratch + SCR_DISPENSER);
-    p.min_trav = h->min_trav;
+    // traversal-phase exit threshold, measured per mode (env RSI_MIN_TRAV overrides)
+    p.min_trav = h->min_trav >= 0 ? h->min_trav : (mode == RSI_MODE_BOOLEAN ? 16 : 8);
     const bool fp64 = (h->opt.flags & RSI_OPT_FP64_MOLLER) != 0, ctr = (h->opt.flags & RSI_OPT_COUNTERS) != 0;
     if (fp64)
         ctr ? launch_mode<true, true>(mode, p, s) : launch_mode<true, false>(mode, p, s);
@@ -1185,6 +1187,8 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     h->host_overflow += (uint64_t)n_ovf;
     return st;
 }
+
+bool rsi_uses_quads() { return RSI_ANY_QUAD; }
 
 rsi_status_t rsi_compact_device(const int32_t* tri, int64_t n, int32_t* ids, int32_t* d_n, cudaStream_t s) {
     if (n == 0) return rsi_cuda_check(cudaMemsetAsync(d_n, 0, sizeof(int32_t), s), "memset");

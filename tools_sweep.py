@@ -11,7 +11,7 @@ V, T, S, E, _ = synth.workload(wl, n, seed=3)
 dev = torch.device("cuda:0")
 Vd, Td, Sd, Ed = (torch.from_numpy(a).to(dev) for a in (V, T, S, E))
 res = {}
-for cfg in os.environ.get("CFGS", "8:2").split(","):
+for cfg in os.environ.get("CFGS", "-1:1").split(","):
     mt, sp = cfg.split(":")
     os.environ["RSI_MIN_TRAV"] = mt
     os.environ["RSI_SPEC"] = sp

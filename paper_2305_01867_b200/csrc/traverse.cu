@@ -602,37 +602,6 @@ struct LaneStack {
     }
 };
 
-// Per-warp staging of a chunk's precomputed rays: field f of ray j at
-// stage[f * kChunk + j] (consecutive lanes -> consecutive banks).
-constexpr int kStageFields = 19;
-__device__ __forceinline__ void stage_put(float* st, int j, const Ray& r, bool ok) {
-    const float v[kStageFields] = {r.ox, r.oy, r.oz, r.ex, r.ey, r.ez, r.dx, r.dy, r.dz, r.ix,
-                                   r.iy, r.iz, r.lx, r.ly, r.lz, r.hx, r.hy, r.hz, ok ? 1.0f : 0.0f};
-#pragma unroll
-    for (int f = 0; f < kStageFields; ++f) st[f * kChunk + j] = v[f];
-}
-__device__ __forceinline__ bool stage_get(const float* st, int j, Ray& r) {
-    r.ox = st[0 * kChunk + j];
-    r.oy = st[1 * kChunk + j];
-    r.oz = st[2 * kChunk + j];
-    r.ex = st[3 * kChunk + j];
-    r.ey = st[4 * kChunk + j];
-    r.ez = st[5 * kChunk + j];
-    r.dx = st[6 * kChunk + j];
-    r.dy = st[7 * kChunk + j];
-    r.dz = st[8 * kChunk + j];
-    r.ix = st[9 * kChunk + j];
-    r.iy = st[10 * kChunk + j];
-    r.iz = st[11 * kChunk + j];
-    r.lx = st[12 * kChunk + j];
-    r.ly = st[13 * kChunk + j];
-    r.lz = st[14 * kChunk + j];
-    r.hx = st[15 * kChunk + j];
-    r.hy = st[16 * kChunk + j];
-    r.hz = st[17 * kChunk + j];
-    return st[18 * kChunk + j] != 0.0f;
-}
-
 // compare-and-swap of (key, ref) pairs: ascending keys
 __device__ __forceinline__ void cas(float& ka, int& ca, float& kb, int& cb) {
     const bool sw = kb < ka;
@@ -657,9 +626,7 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
     __shared__ int s_k[MODE == MODE_COUNT ? kCountCap * kThreads : 1];
     Stats st;
 
-    int64_t cbase = 0, cnext = 0, cend = 0;  // warp-uniform chunk [cnext, cend) starting at cbase
-    __shared__ float s_stage[kThreads / 32][kStageFields * kChunk];
-    float* stage = s_stage[threadIdx.x >> 5];
+    int64_t cnext = 0, cend = 0;  // warp-uniform chunk [cnext, cend)
     bool exhausted = false;       // warp-uniform
     int64_t ray = -1;
     Ray r;
@@ -677,13 +644,8 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
     }
     while (true) {
         // ---- 1. refill
-        // A new chunk is set up by the whole (converged) warp at once: 2 rays
-        // per lane, coalesced loads, slab precomputation at full SIMT
-        // efficiency, into this warp's shared-memory staging area; lanes that
-        // need a ray then copy one.
         unsigned want = __ballot_sync(FULL, ray < 0);
         bool fresh = false;
-        bool ok = false;
         while (want && !exhausted) {
             if (cnext >= cend) {
                 unsigned long long base = 0;
@@ -693,21 +655,8 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
                     exhausted = true;
                     break;
                 }
-                cbase = cnext = (int64_t)base;
+                cnext = (int64_t)base;
                 cend = min((int64_t)base + kChunk, p.n);
-                __syncwarp();  // previous chunk fully read
-#pragma unroll
-                for (int h = 0; h < kChunk / 32; ++h) {
-                    const int j = h * 32 + lane;
-                    if (cbase + j < cend) {
-                        Ray t;
-                        bool nonfinite;
-                        const bool okj = load_ray(t, p.S, p.E, cbase + j, nonfinite);
-                        if (nonfinite) st.add(ST_NONFINITE);
-                        stage_put(stage, j, t, okj);
-                    }
-                }
-                __syncwarp();
             }
             const int take = (int)min((int64_t)__popc(want), cend - cnext);
             const bool mine = (want >> lane) & 1u;
@@ -715,13 +664,15 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             const bool got = mine && rank < take;
             if (got) {
                 ray = cnext + rank;
-                ok = stage_get(stage, (int)(ray - cbase), r);
                 fresh = true;
             }
             want &= ~__ballot_sync(FULL, got);
             cnext += take;
         }
         if (fresh) {
+            bool nonfinite;
+            const bool ok = load_ray(r, p.S, p.E, ray, nonfinite);
+            if (nonfinite) st.add(ST_NONFINITE);
             ms.init();
             tclip = 1.0f;
             sp = 0;

@@ -454,6 +454,225 @@ __global__ void __launch_bounds__(kBlock) k_refit(const float* __restrict__ V, i
     }
 }
 
+// ------------------------------------------------------------------ fused single-CTA build (N_t <= 10240)
+// All of A1..A7 in one launch for small meshes (the configs' N_t = 1e4): the
+// build is latency-bound there, so one CTA keeps the Morton codes, the sort's
+// ping-pong buffers, the parent links and the arrival counters in shared
+// memory and separates the steps with __syncthreads (no inter-kernel gaps, no
+// global-memory round trips inside the sort, block-scope fences in the refit).
+constexpr int kFusedMax = 10240;
+constexpr int kFusedThreads = 1024;
+
+__global__ void __launch_bounds__(kFusedThreads) k_build_small(const float* __restrict__ V, int64_t nv,
+                                                               const int32_t* __restrict__ T, int n,
+                                                               float4* nodes, float4* __restrict__ tris,
+                                                               uint32_t* __restrict__ g_keys,
+                                                               int32_t* __restrict__ g_vals,
+                                                               int32_t* __restrict__ g_parent,
+                                                               uint32_t* __restrict__ g_arrivals, uint32_t* scratch) {
+    extern __shared__ uint32_t sm[];
+    uint32_t* ka = sm;
+    int32_t* va = reinterpret_cast<int32_t*>(sm + n);
+    uint32_t* kb = sm + 2 * n;
+    int32_t* vb = reinterpret_cast<int32_t*>(sm + 3 * n);
+    __shared__ uint32_t s_ext[6], s_status;
+    __shared__ uint32_t wcnt[32][kDigits + 1];
+    __shared__ uint32_t dbase[kDigits];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const int n_nodes = n > 1 ? n - 1 : 1;
+
+    // A1 + A2: validate + surface extent
+    if (tid < 3) {
+        s_ext[tid] = 0xffffffffu;
+        s_ext[3 + tid] = 0u;
+    }
+    if (tid == 0) s_status = 0u;
+    __syncthreads();
+    {
+        float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+        uint32_t bad = 0;
+        for (int64_t i = tid; i < nv; i += kFusedThreads)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const float x = V[3 * i + k];
+                if (!isfinite(x)) bad |= STATUS_NONFINITE;
+                mn[k] = fminf(mn[k], x);
+                mx[k] = fmaxf(mx[k], x);
+            }
+        for (int64_t i = tid; i < 3 * (int64_t)n; i += kFusedThreads) {
+            const int32_t a = T[i];
+            if (a < 0 || (int64_t)a >= nv) bad |= STATUS_INDEX;
+        }
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float a = warp_min(mn[k]), b = warp_max(mx[k]);
+            if (lane == 0 && a <= b) {
+                atomicMin(&s_ext[k], rsi_f2ord(a));
+                atomicMax(&s_ext[3 + k], rsi_f2ord(b));
+            }
+        }
+        if (bad) atomicOr(&s_status, bad);
+    }
+    __syncthreads();
+
+    // A3: Morton codes
+    float lo[3], hi[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = rsi_ord2f(s_ext[k]);
+        hi[k] = rsi_ord2f(s_ext[3 + k]);
+    }
+    for (int j = tid; j < n; j += kFusedThreads) {
+        const int32_t a = safe_index(T[3 * j], nv), b = safe_index(T[3 * j + 1], nv), c = safe_index(T[3 * j + 2], nv);
+        uint32_t q[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const float cen = (V[3 * a + k] + V[3 * b + k] + V[3 * c + k]) / 3.0f;
+            q[k] = quantize10(cen, lo[k], hi[k]);
+        }
+        ka[j] = expand10(q[0]) | (expand10(q[1]) << 1) | (expand10(q[2]) << 2);
+        va[j] = j;
+    }
+    __syncthreads();
+
+    // A4: stable LSD radix sort in shared memory (same warp-ranked passes as k_sort_small)
+    {
+        const int seg = (((n + 31) / 32) + 31) & ~31;
+        const int beg = min(w * seg, n), end = min(beg + seg, n);
+        for (int pass = 0; pass < kPasses; ++pass) {
+            const uint32_t* ks = (pass & 1) ? kb : ka;
+            const int32_t* vs = (pass & 1) ? vb : va;
+            uint32_t* kd = (pass & 1) ? ka : kb;
+            int32_t* vd = (pass & 1) ? va : vb;
+            const int shift = 8 * pass;
+            for (int i = tid; i < 32 * (kDigits + 1); i += kFusedThreads) (&wcnt[0][0])[i] = 0u;
+            __syncthreads();
+            warp_count(ks, beg, end, shift, wcnt[w]);
+            __syncthreads();
+            if (tid < kDigits) {
+                uint32_t sum = 0;
+                for (int x = 0; x < 32; ++x) {
+                    const uint32_t c = wcnt[x][tid];
+                    wcnt[x][tid] = sum;
+                    sum += c;
+                }
+                dbase[tid] = sum;
+            }
+            __syncthreads();
+            if (w == 0) warp_scan256(dbase);
+            __syncthreads();
+            warp_scatter(ks, vs, kd, vd, beg, end, shift, wcnt[w], dbase);
+            __syncthreads();
+        }
+    }
+    for (int j = tid; j < n; j += kFusedThreads) {
+        g_keys[j] = ka[j];
+        g_vals[j] = va[j];
+    }
+
+    // A5: Karras topology; parents into shared memory (the kb/vb region)
+    int32_t* parent = reinterpret_cast<int32_t*>(kb);
+    if (n == 1) {
+        if (tid == 0) {
+            nodes[1] = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
+            nodes[2].z = INFINITY;
+            nodes[2].w = INFINITY;
+            nodes[3] = make_float4(__int_as_float(~0), __int_as_float(~0), 0.f, 0.f);
+            parent[0] = -1;
+            parent[1] = 0;
+        }
+    } else {
+        for (int i = tid; i < n - 1; i += kFusedThreads) {
+            const uint32_t ki = ka[i];
+            const int dir = (kdelta(ka, n, i, ki, i + 1) - kdelta(ka, n, i, ki, i - 1)) > 0 ? 1 : -1;
+            const int dmin = kdelta(ka, n, i, ki, i - dir);
+            int lmax = 2;
+            while (kdelta(ka, n, i, ki, i + lmax * dir) > dmin) lmax <<= 1;
+            int l = 0;
+            for (int t = lmax >> 1; t >= 1; t >>= 1)
+                if (kdelta(ka, n, i, ki, i + (l + t) * dir) > dmin) l += t;
+            const int j = i + l * dir;
+            const int dnode = kdelta(ka, n, i, ki, j);
+            int sp = 0, step = l;
+            do {
+                step = (step + 1) >> 1;
+                const int ns = sp + step;
+                if (ns < l && kdelta(ka, n, i, ki, i + ns * dir) > dnode) sp = ns;
+            } while (step > 1);
+            const int gamma = i + sp * dir + min(dir, 0);
+            const int rlo = min(i, j), rhi = max(i, j);
+            const int32_t left = (rlo == gamma) ? ~gamma : gamma;
+            const int32_t right = (rhi == gamma + 1) ? ~(gamma + 1) : gamma + 1;
+            reinterpret_cast<int4*>(nodes + 4 * i + 3)[0] = make_int4(left, right, 0, 0);
+            parent[left >= 0 ? left : n_nodes + ~left] = (i << 1) | 0;
+            parent[right >= 0 ? right : n_nodes + ~right] = (i << 1) | 1;
+        }
+        if (tid == 0) parent[0] = -1;
+    }
+    __syncthreads();
+
+    // A6 + A7: leaf init + atomic refit with shared-memory arrival counters
+    uint32_t* arrivals = ka;  // the keys are in g_keys now
+    for (int i = tid; i < n_nodes; i += kFusedThreads) arrivals[i] = (n == 1) ? 2u : 0u;
+    __syncthreads();
+    for (int k = tid; k < n; k += kFusedThreads) {
+        const int32_t id = va[k];
+        const int32_t ia = safe_index(T[3 * id], nv), ib = safe_index(T[3 * id + 1], nv),
+                      ic = safe_index(T[3 * id + 2], nv);
+        float a[3], b[3], c[3], blo[3], bhi[3];
+#pragma unroll
+        for (int x = 0; x < 3; ++x) {
+            a[x] = V[3 * ia + x];
+            b[x] = V[3 * ib + x];
+            c[x] = V[3 * ic + x];
+            blo[x] = fminf(a[x], fminf(b[x], c[x]));
+            bhi[x] = fmaxf(a[x], fmaxf(b[x], c[x]));
+        }
+        tris[4 * k + 0] = make_float4(a[0], a[1], a[2], __int_as_float(id));
+        tris[4 * k + 1] = make_float4(b[0], b[1], b[2], 0.f);
+        tris[4 * k + 2] = make_float4(c[0], c[1], c[2], 0.f);
+        tris[4 * k + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
+        int32_t p = parent[n_nodes + k];
+        bool root = false;
+        while (true) {
+            const int node = p >> 1, side = p & 1;
+            write_slot(nodes, node, side, blo, bhi);
+            if (n == 1) {
+                root = true;
+                break;
+            }
+            __threadfence_block();
+            if (atomicAdd(&arrivals[node], 1u) == 0u) break;
+            __threadfence_block();
+            const volatile float* f = reinterpret_cast<const volatile float*>(nodes + 4 * node);
+            const int o = side ? 0 : 4;  // sibling slot
+            blo[0] = fminf(blo[0], f[o + 0]);
+            bhi[0] = fmaxf(bhi[0], f[o + 1]);
+            blo[1] = fminf(blo[1], f[o + 2]);
+            bhi[1] = fmaxf(bhi[1], f[o + 3]);
+            blo[2] = fminf(blo[2], f[8 + 2 * (1 - side)]);
+            bhi[2] = fmaxf(bhi[2], f[9 + 2 * (1 - side)]);
+            if (node == 0) {
+                root = true;
+                break;
+            }
+            p = parent[node];
+        }
+        if (root) {
+            float* rb = reinterpret_cast<float*>(scratch + SCR_ROOT);
+            for (int x = 0; x < 3; ++x) {
+                rb[x] = blo[x];
+                rb[3 + x] = bhi[x];
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < n_nodes + n; i += kFusedThreads) g_parent[i] = parent[i];
+    for (int i = tid; i < n_nodes; i += kFusedThreads) g_arrivals[i] = arrivals[i];
+    if (tid < 6) scratch[SCR_EXT_MIN + tid] = s_ext[tid];
+    if (tid == 0) scratch[SCR_STATUS] = s_status;
+}
+
 // ------------------------------------------------------------------ 4-wide view (grandchild records)
 // One thread per internal node n: the up-to-4 grandchildren of n (a leaf child
 // stands for itself), their AABBs quantized to 8 bits on a per-axis
@@ -625,17 +844,28 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
     if (st != RSI_OK) return st;
     const int n = (int)nt;
     const int n_nodes = n > 1 ? n - 1 : 1;
-    k_build_init<<<1, 32, 0, s>>>(h->scratch);
-    int64_t work = nv > 3 * nt ? nv : 3 * nt;
-    int eb = rsi_ceil_div(work, kBlock);
-    if (eb > 148 * 8) eb = 148 * 8;
-    k_extent_validate<<<eb, kBlock, 0, s>>>(V, nv, T, nt, h->scratch);
-    k_morton<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, n, h->scratch, h->keys, h->vals, h->arrivals,
-                                                         n_nodes);
-    launch_sort(h, n, s);
-    k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent, h->arrivals);
-    k_refit<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, h->vals, n, h->nodes, h->tris, h->parent,
-                                                        h->arrivals, h->scratch);
+    if (n <= kFusedMax) {
+        static bool attr = false;
+        const size_t dyn = (size_t)16 * kFusedMax;
+        if (!attr) {
+            cudaFuncSetAttribute(k_build_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+            attr = true;
+        }
+        k_build_small<<<1, kFusedThreads, (size_t)16 * n, s>>>(V, nv, T, n, h->nodes, h->tris, h->keys, h->vals,
+                                                                h->parent, h->arrivals, h->scratch);
+    } else {
+        k_build_init<<<1, 32, 0, s>>>(h->scratch);
+        int64_t work = nv > 3 * nt ? nv : 3 * nt;
+        int eb = rsi_ceil_div(work, kBlock);
+        if (eb > 148 * 8) eb = 148 * 8;
+        k_extent_validate<<<eb, kBlock, 0, s>>>(V, nv, T, nt, h->scratch);
+        k_morton<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, n, h->scratch, h->keys, h->vals, h->arrivals,
+                                                             n_nodes);
+        launch_sort(h, n, s);
+        k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent, h->arrivals);
+        k_refit<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, h->vals, n, h->nodes, h->tris, h->parent,
+                                                            h->arrivals, h->scratch);
+    }
     if (rsi_uses_quads()) k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads, h->scratch);
     st = rsi_cuda_check(cudaGetLastError(), "build kernel launch");
     if (st != RSI_OK) return st;

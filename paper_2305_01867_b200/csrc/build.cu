@@ -435,14 +435,15 @@ __global__ void __launch_bounds__(kBlock) k_refit(const float* __restrict__ V, i
         __threadfence();
         if (atomicAdd(&arrivals[node], 1u) == 0u) return;
         __threadfence();
-        const volatile float* f = reinterpret_cast<const volatile float*>(nodes + 4 * node);
+        // sibling box: L2-coherent loads (ld.global.cg), ordered after the atomic
+        const float* f = reinterpret_cast<const float*>(nodes + 4 * node);
         const int o = side ? 0 : 4;  // sibling slot
-        lo[0] = fminf(lo[0], f[o + 0]);
-        hi[0] = fmaxf(hi[0], f[o + 1]);
-        lo[1] = fminf(lo[1], f[o + 2]);
-        hi[1] = fmaxf(hi[1], f[o + 3]);
-        lo[2] = fminf(lo[2], f[8 + 2 * (1 - side)]);
-        hi[2] = fmaxf(hi[2], f[9 + 2 * (1 - side)]);
+        lo[0] = fminf(lo[0], __ldcg(f + o + 0));
+        hi[0] = fmaxf(hi[0], __ldcg(f + o + 1));
+        lo[1] = fminf(lo[1], __ldcg(f + o + 2));
+        hi[1] = fmaxf(hi[1], __ldcg(f + o + 3));
+        lo[2] = fminf(lo[2], __ldcg(f + 8 + 2 * (1 - side)));
+        hi[2] = fmaxf(hi[2], __ldcg(f + 9 + 2 * (1 - side)));
         if (node == 0) break;
         p = parent[node];
     }
@@ -455,11 +456,12 @@ __global__ void __launch_bounds__(kBlock) k_refit(const float* __restrict__ V, i
 }
 
 // ------------------------------------------------------------------ fused single-CTA build (N_t <= 10240)
-// All of A1..A7 in one launch for small meshes (the configs' N_t = 1e4): the
-// build is latency-bound there, so one CTA keeps the Morton codes, the sort's
-// ping-pong buffers, the parent links and the arrival counters in shared
-// memory and separates the steps with __syncthreads (no inter-kernel gaps, no
-// global-memory round trips inside the sort, block-scope fences in the refit).
+// A1..A5 in one launch for small meshes (the configs' N_t = 1e4): the build is
+// latency-bound there, so one CTA keeps the Morton codes, the sort's ping-pong
+// buffers and the parent links in shared memory and separates the steps with
+// __syncthreads (no inter-kernel gaps, no global round trips inside the sort).
+// The refit (A6+A7) stays a multi-CTA kernel: its depth-long atomic chains
+// need one thread per leaf in flight, not 1024 threads looping.
 constexpr int kFusedMax = 10240;
 constexpr int kFusedThreads = 1024;
 
@@ -611,64 +613,9 @@ __global__ void __launch_bounds__(kFusedThreads) k_build_small(const float* __re
     }
     __syncthreads();
 
-    // A6 + A7: leaf init + atomic refit with shared-memory arrival counters
-    uint32_t* arrivals = ka;  // the keys are in g_keys now
-    for (int i = tid; i < n_nodes; i += kFusedThreads) arrivals[i] = (n == 1) ? 2u : 0u;
-    __syncthreads();
-    for (int k = tid; k < n; k += kFusedThreads) {
-        const int32_t id = va[k];
-        const int32_t ia = safe_index(T[3 * id], nv), ib = safe_index(T[3 * id + 1], nv),
-                      ic = safe_index(T[3 * id + 2], nv);
-        float a[3], b[3], c[3], blo[3], bhi[3];
-#pragma unroll
-        for (int x = 0; x < 3; ++x) {
-            a[x] = V[3 * ia + x];
-            b[x] = V[3 * ib + x];
-            c[x] = V[3 * ic + x];
-            blo[x] = fminf(a[x], fminf(b[x], c[x]));
-            bhi[x] = fmaxf(a[x], fmaxf(b[x], c[x]));
-        }
-        tris[4 * k + 0] = make_float4(a[0], a[1], a[2], __int_as_float(id));
-        tris[4 * k + 1] = make_float4(b[0], b[1], b[2], 0.f);
-        tris[4 * k + 2] = make_float4(c[0], c[1], c[2], 0.f);
-        tris[4 * k + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
-        int32_t p = parent[n_nodes + k];
-        bool root = false;
-        while (true) {
-            const int node = p >> 1, side = p & 1;
-            write_slot(nodes, node, side, blo, bhi);
-            if (n == 1) {
-                root = true;
-                break;
-            }
-            __threadfence_block();
-            if (atomicAdd(&arrivals[node], 1u) == 0u) break;
-            __threadfence_block();
-            const volatile float* f = reinterpret_cast<const volatile float*>(nodes + 4 * node);
-            const int o = side ? 0 : 4;  // sibling slot
-            blo[0] = fminf(blo[0], f[o + 0]);
-            bhi[0] = fmaxf(bhi[0], f[o + 1]);
-            blo[1] = fminf(blo[1], f[o + 2]);
-            bhi[1] = fmaxf(bhi[1], f[o + 3]);
-            blo[2] = fminf(blo[2], f[8 + 2 * (1 - side)]);
-            bhi[2] = fmaxf(bhi[2], f[9 + 2 * (1 - side)]);
-            if (node == 0) {
-                root = true;
-                break;
-            }
-            p = parent[node];
-        }
-        if (root) {
-            float* rb = reinterpret_cast<float*>(scratch + SCR_ROOT);
-            for (int x = 0; x < 3; ++x) {
-                rb[x] = blo[x];
-                rb[3 + x] = bhi[x];
-            }
-        }
-    }
-    __syncthreads();
+    // hand over to the multi-CTA refit (k_refit): parents and zeroed arrival counters
     for (int i = tid; i < n_nodes + n; i += kFusedThreads) g_parent[i] = parent[i];
-    for (int i = tid; i < n_nodes; i += kFusedThreads) g_arrivals[i] = arrivals[i];
+    for (int i = tid; i < n_nodes; i += kFusedThreads) g_arrivals[i] = (n == 1) ? 2u : 0u;
     if (tid < 6) scratch[SCR_EXT_MIN + tid] = s_ext[tid];
     if (tid == 0) scratch[SCR_STATUS] = s_status;
 }
@@ -853,6 +800,8 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
         }
         k_build_small<<<1, kFusedThreads, (size_t)16 * n, s>>>(V, nv, T, n, h->nodes, h->tris, h->keys, h->vals,
                                                                 h->parent, h->arrivals, h->scratch);
+        k_refit<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, h->vals, n, h->nodes, h->tris, h->parent,
+                                                            h->arrivals, h->scratch);
     } else {
         k_build_init<<<1, 32, 0, s>>>(h->scratch);
         int64_t work = nv > 3 * nt ? nv : 3 * nt;

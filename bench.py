@@ -224,7 +224,7 @@ def main():
     Sd, Ed = torch.from_numpy(S).to(dev), torch.from_numpy(E).to(dev)
     stream = torch.cuda.current_stream(dev)
     h = rsi.rsi_build(Vd, Td)
-    kernels_per_build = 2 if len(T) <= 10240 else (6 if len(T) <= 65536 else 5 + 12)
+    kernels_per_build = 6 if len(T) <= 65536 else 5 + 12
 
     def timed(mode: str, steps: int, warmup: int, clocks: bool):
         out = rsi.alloc_outputs(n, mode, dev)

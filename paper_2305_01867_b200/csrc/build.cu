@@ -455,169 +455,55 @@ __global__ void __launch_bounds__(kBlock) k_refit(const float* __restrict__ V, i
     }
 }
 
-// ------------------------------------------------------------------ fused single-CTA build (N_t <= 10240)
-// A1..A5 in one launch for small meshes (the configs' N_t = 1e4): the build is
-// latency-bound there, so one CTA keeps the Morton codes, the sort's ping-pong
-// buffers and the parent links in shared memory and separates the steps with
-// __syncthreads (no inter-kernel gaps, no global round trips inside the sort).
-// The refit (A6+A7) stays a multi-CTA kernel: its depth-long atomic chains
-// need one thread per leaf in flight, not 1024 threads looping.
-constexpr int kFusedMax = 10240;
-constexpr int kFusedThreads = 1024;
+// Whole sort in one CTA with keys and values resident in shared memory
+// (N_t <= kSmemSortMax): no global-memory latency inside the passes.
+constexpr int kSmemSortMax = 10240;
 
-__global__ void __launch_bounds__(kFusedThreads) k_build_small(const float* __restrict__ V, int64_t nv,
-                                                               const int32_t* __restrict__ T, int n,
-                                                               float4* nodes, float4* __restrict__ tris,
-                                                               uint32_t* __restrict__ g_keys,
-                                                               int32_t* __restrict__ g_vals,
-                                                               int32_t* __restrict__ g_parent,
-                                                               uint32_t* __restrict__ g_arrivals, uint32_t* scratch) {
+__global__ void __launch_bounds__(kSmallThreads) k_sort_smem(uint32_t* gk, int32_t* gv, int n) {
     extern __shared__ uint32_t sm[];
     uint32_t* ka = sm;
     int32_t* va = reinterpret_cast<int32_t*>(sm + n);
     uint32_t* kb = sm + 2 * n;
     int32_t* vb = reinterpret_cast<int32_t*>(sm + 3 * n);
-    __shared__ uint32_t s_ext[6], s_status;
     __shared__ uint32_t wcnt[32][kDigits + 1];
     __shared__ uint32_t dbase[kDigits];
-    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const int n_nodes = n > 1 ? n - 1 : 1;
-
-    // A1 + A2: validate + surface extent
-    if (tid < 3) {
-        s_ext[tid] = 0xffffffffu;
-        s_ext[3 + tid] = 0u;
+    const int tid = threadIdx.x, w = tid >> 5;
+    for (int j = tid; j < n; j += kSmallThreads) {
+        ka[j] = gk[j];
+        va[j] = gv[j];
     }
-    if (tid == 0) s_status = 0u;
     __syncthreads();
-    {
-        float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
-        uint32_t bad = 0;
-        for (int64_t i = tid; i < nv; i += kFusedThreads)
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                const float x = V[3 * i + k];
-                if (!isfinite(x)) bad |= STATUS_NONFINITE;
-                mn[k] = fminf(mn[k], x);
-                mx[k] = fmaxf(mx[k], x);
+    const int seg = (((n + 31) / 32) + 31) & ~31;
+    const int beg = min(w * seg, n), end = min(beg + seg, n);
+    for (int pass = 0; pass < kPasses; ++pass) {
+        const uint32_t* ks = (pass & 1) ? kb : ka;
+        const int32_t* vs = (pass & 1) ? vb : va;
+        uint32_t* kd = (pass & 1) ? ka : kb;
+        int32_t* vd = (pass & 1) ? va : vb;
+        const int shift = 8 * pass;
+        for (int i = tid; i < 32 * (kDigits + 1); i += kSmallThreads) (&wcnt[0][0])[i] = 0u;
+        __syncthreads();
+        warp_count(ks, beg, end, shift, wcnt[w]);
+        __syncthreads();
+        if (tid < kDigits) {
+            uint32_t sum = 0;
+            for (int x = 0; x < 32; ++x) {
+                const uint32_t c = wcnt[x][tid];
+                wcnt[x][tid] = sum;
+                sum += c;
             }
-        for (int64_t i = tid; i < 3 * (int64_t)n; i += kFusedThreads) {
-            const int32_t a = T[i];
-            if (a < 0 || (int64_t)a >= nv) bad |= STATUS_INDEX;
+            dbase[tid] = sum;
         }
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const float a = warp_min(mn[k]), b = warp_max(mx[k]);
-            if (lane == 0 && a <= b) {
-                atomicMin(&s_ext[k], rsi_f2ord(a));
-                atomicMax(&s_ext[3 + k], rsi_f2ord(b));
-            }
-        }
-        if (bad) atomicOr(&s_status, bad);
+        __syncthreads();
+        if (w == 0) warp_scan256(dbase);
+        __syncthreads();
+        warp_scatter(ks, vs, kd, vd, beg, end, shift, wcnt[w], dbase);
+        __syncthreads();
     }
-    __syncthreads();
-
-    // A3: Morton codes
-    float lo[3], hi[3];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        lo[k] = rsi_ord2f(s_ext[k]);
-        hi[k] = rsi_ord2f(s_ext[3 + k]);
+    for (int j = tid; j < n; j += kSmallThreads) {
+        gk[j] = ka[j];
+        gv[j] = va[j];
     }
-    for (int j = tid; j < n; j += kFusedThreads) {
-        const int32_t a = safe_index(T[3 * j], nv), b = safe_index(T[3 * j + 1], nv), c = safe_index(T[3 * j + 2], nv);
-        uint32_t q[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            const float cen = (V[3 * a + k] + V[3 * b + k] + V[3 * c + k]) / 3.0f;
-            q[k] = quantize10(cen, lo[k], hi[k]);
-        }
-        ka[j] = expand10(q[0]) | (expand10(q[1]) << 1) | (expand10(q[2]) << 2);
-        va[j] = j;
-    }
-    __syncthreads();
-
-    // A4: stable LSD radix sort in shared memory (same warp-ranked passes as k_sort_small)
-    {
-        const int seg = (((n + 31) / 32) + 31) & ~31;
-        const int beg = min(w * seg, n), end = min(beg + seg, n);
-        for (int pass = 0; pass < kPasses; ++pass) {
-            const uint32_t* ks = (pass & 1) ? kb : ka;
-            const int32_t* vs = (pass & 1) ? vb : va;
-            uint32_t* kd = (pass & 1) ? ka : kb;
-            int32_t* vd = (pass & 1) ? va : vb;
-            const int shift = 8 * pass;
-            for (int i = tid; i < 32 * (kDigits + 1); i += kFusedThreads) (&wcnt[0][0])[i] = 0u;
-            __syncthreads();
-            warp_count(ks, beg, end, shift, wcnt[w]);
-            __syncthreads();
-            if (tid < kDigits) {
-                uint32_t sum = 0;
-                for (int x = 0; x < 32; ++x) {
-                    const uint32_t c = wcnt[x][tid];
-                    wcnt[x][tid] = sum;
-                    sum += c;
-                }
-                dbase[tid] = sum;
-            }
-            __syncthreads();
-            if (w == 0) warp_scan256(dbase);
-            __syncthreads();
-            warp_scatter(ks, vs, kd, vd, beg, end, shift, wcnt[w], dbase);
-            __syncthreads();
-        }
-    }
-    for (int j = tid; j < n; j += kFusedThreads) {
-        g_keys[j] = ka[j];
-        g_vals[j] = va[j];
-    }
-
-    // A5: Karras topology; parents into shared memory (the kb/vb region)
-    int32_t* parent = reinterpret_cast<int32_t*>(kb);
-    if (n == 1) {
-        if (tid == 0) {
-            nodes[1] = make_float4(INFINITY, INFINITY, INFINITY, INFINITY);
-            nodes[2].z = INFINITY;
-            nodes[2].w = INFINITY;
-            nodes[3] = make_float4(__int_as_float(~0), __int_as_float(~0), 0.f, 0.f);
-            parent[0] = -1;
-            parent[1] = 0;
-        }
-    } else {
-        for (int i = tid; i < n - 1; i += kFusedThreads) {
-            const uint32_t ki = ka[i];
-            const int dir = (kdelta(ka, n, i, ki, i + 1) - kdelta(ka, n, i, ki, i - 1)) > 0 ? 1 : -1;
-            const int dmin = kdelta(ka, n, i, ki, i - dir);
-            int lmax = 2;
-            while (kdelta(ka, n, i, ki, i + lmax * dir) > dmin) lmax <<= 1;
-            int l = 0;
-            for (int t = lmax >> 1; t >= 1; t >>= 1)
-                if (kdelta(ka, n, i, ki, i + (l + t) * dir) > dmin) l += t;
-            const int j = i + l * dir;
-            const int dnode = kdelta(ka, n, i, ki, j);
-            int sp = 0, step = l;
-            do {
-                step = (step + 1) >> 1;
-                const int ns = sp + step;
-                if (ns < l && kdelta(ka, n, i, ki, i + ns * dir) > dnode) sp = ns;
-            } while (step > 1);
-            const int gamma = i + sp * dir + min(dir, 0);
-            const int rlo = min(i, j), rhi = max(i, j);
-            const int32_t left = (rlo == gamma) ? ~gamma : gamma;
-            const int32_t right = (rhi == gamma + 1) ? ~(gamma + 1) : gamma + 1;
-            reinterpret_cast<int4*>(nodes + 4 * i + 3)[0] = make_int4(left, right, 0, 0);
-            parent[left >= 0 ? left : n_nodes + ~left] = (i << 1) | 0;
-            parent[right >= 0 ? right : n_nodes + ~right] = (i << 1) | 1;
-        }
-        if (tid == 0) parent[0] = -1;
-    }
-    __syncthreads();
-
-    // hand over to the multi-CTA refit (k_refit): parents and zeroed arrival counters
-    for (int i = tid; i < n_nodes + n; i += kFusedThreads) g_parent[i] = parent[i];
-    for (int i = tid; i < n_nodes; i += kFusedThreads) g_arrivals[i] = (n == 1) ? 2u : 0u;
-    if (tid < 6) scratch[SCR_EXT_MIN + tid] = s_ext[tid];
-    if (tid == 0) scratch[SCR_STATUS] = s_status;
 }
 
 // ------------------------------------------------------------------ 4-wide view (grandchild records)
@@ -765,6 +651,15 @@ static rsi_status_t ensure_capacity(rsi_bvh* h, int64_t n, cudaStream_t s) {
 }
 
 static void launch_sort(rsi_bvh* h, int n, cudaStream_t s) {
+    if (n <= kSmemSortMax) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_sort_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * kSmemSortMax);
+            attr = true;
+        }
+        k_sort_smem<<<1, kSmallThreads, (size_t)16 * n, s>>>(h->keys, h->vals, n);
+        return;
+    }
     if (n <= kSmallMax) {
         k_sort_small<<<1, kSmallThreads, 0, s>>>(h->keys, h->vals, h->keys_tmp, h->vals_tmp, n);
         return;
@@ -791,30 +686,17 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
     if (st != RSI_OK) return st;
     const int n = (int)nt;
     const int n_nodes = n > 1 ? n - 1 : 1;
-    if (n <= kFusedMax) {
-        static bool attr = false;
-        const size_t dyn = (size_t)16 * kFusedMax;
-        if (!attr) {
-            cudaFuncSetAttribute(k_build_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-            attr = true;
-        }
-        k_build_small<<<1, kFusedThreads, (size_t)16 * n, s>>>(V, nv, T, n, h->nodes, h->tris, h->keys, h->vals,
-                                                                h->parent, h->arrivals, h->scratch);
-        k_refit<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, h->vals, n, h->nodes, h->tris, h->parent,
-                                                            h->arrivals, h->scratch);
-    } else {
-        k_build_init<<<1, 32, 0, s>>>(h->scratch);
-        int64_t work = nv > 3 * nt ? nv : 3 * nt;
-        int eb = rsi_ceil_div(work, kBlock);
-        if (eb > 148 * 8) eb = 148 * 8;
-        k_extent_validate<<<eb, kBlock, 0, s>>>(V, nv, T, nt, h->scratch);
-        k_morton<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, n, h->scratch, h->keys, h->vals, h->arrivals,
-                                                             n_nodes);
-        launch_sort(h, n, s);
-        k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent, h->arrivals);
-        k_refit<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, h->vals, n, h->nodes, h->tris, h->parent,
-                                                            h->arrivals, h->scratch);
-    }
+    k_build_init<<<1, 32, 0, s>>>(h->scratch);
+    int64_t work = nv > 3 * nt ? nv : 3 * nt;
+    int eb = rsi_ceil_div(work, kBlock);
+    if (eb > 148 * 8) eb = 148 * 8;
+    k_extent_validate<<<eb, kBlock, 0, s>>>(V, nv, T, nt, h->scratch);
+    k_morton<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, n, h->scratch, h->keys, h->vals, h->arrivals,
+                                                         n_nodes);
+    launch_sort(h, n, s);
+    k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent, h->arrivals);
+    k_refit<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, h->vals, n, h->nodes, h->tris, h->parent,
+                                                        h->arrivals, h->scratch);
     if (rsi_uses_quads()) k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads, h->scratch);
     st = rsi_cuda_check(cudaGetLastError(), "build kernel launch");
     if (st != RSI_OK) return st;

@@ -174,6 +174,19 @@ __device__ uint32_t warp_scan256(uint32_t* s) {
     return __shfl_sync(0xffffffffu, inc, 31);
 }
 
+// Lanes of the warp holding the same 8-bit digit as this lane (valid lanes
+// only): AND over the digit's bits of ballot(bit) or ~ballot(bit) -- cheaper
+// than __match_any_sync.
+__device__ __forceinline__ uint32_t digit_peers(bool valid, uint32_t d) {
+    uint32_t m = __ballot_sync(0xffffffffu, valid);
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        m &= ((d >> b) & 1u) ? bb : ~bb;
+    }
+    return valid ? m : 0u;
+}
+
 // Count digits of this warp's segment [beg, end) into wcnt (warp-private row).
 __device__ __forceinline__ void warp_count(const uint32_t* __restrict__ ks, int beg, int end, int shift,
                                            uint32_t* wcnt) {
@@ -181,8 +194,8 @@ __device__ __forceinline__ void warp_count(const uint32_t* __restrict__ ks, int 
     for (int base = beg; base < end; base += 32) {
         int i = base + lane;
         bool valid = i < end;
-        uint32_t d = valid ? (ks[i] >> shift) & 255u : 256u;
-        uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t d = valid ? (ks[i] >> shift) & 255u : 0u;
+        const uint32_t peers = digit_peers(valid, d);
         if (valid && lane == __ffs(peers) - 1) wcnt[d] += __popc(peers);
         __syncwarp();
     }
@@ -199,8 +212,8 @@ __device__ __forceinline__ void warp_scatter(const uint32_t* __restrict__ ks, co
         bool valid = i < end;
         uint32_t key = valid ? ks[i] : 0u;
         int32_t val = valid ? vs[i] : 0;
-        uint32_t d = valid ? (key >> shift) & 255u : 256u;
-        uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t d = valid ? (key >> shift) & 255u : 0u;
+        const uint32_t peers = digit_peers(valid, d);
         if (valid) {
             uint32_t pos = dbase[d] + wcnt[d] + __popc(peers & lt);
             kd[pos] = key;
@@ -432,9 +445,10 @@ __global__ void __launch_bounds__(kBlock) k_refit(const float* __restrict__ V, i
         const int node = p >> 1, side = p & 1;
         write_slot(nodes, node, side, lo, hi);
         if (n == 1) break;
-        __threadfence();
-        if (atomicAdd(&arrivals[node], 1u) == 0u) return;
-        __threadfence();
+        // acq_rel arrival: releases this child's box, acquires the sibling's
+        uint32_t old;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(arrivals + node) : "memory");
+        if (old == 0u) return;
         // sibling box: L2-coherent loads (ld.global.cg), ordered after the atomic
         const float* f = reinterpret_cast<const float*>(nodes + 4 * node);
         const int o = side ? 0 : 4;  // sibling slot

@@ -213,10 +213,17 @@ def main():
     from paper_2305_01867_b200 import rsi
     from paper_2305_01867_b200.sharded import gather_outputs
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one process per GPU; RSI_BENCH_BACKEND=gloo + more ranks than GPUs is a
+    # launch/gather dry run on a single device (testing only, never a number)
+    ndev = torch.cuda.device_count()
+    torch.cuda.set_device(local % ndev)
+    dev = torch.device("cuda", local % ndev)
+    backend = os.environ.get("RSI_BENCH_BACKEND", "nccl")
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     n = args.rays_per_gpu
     V, T, S, E = workload_inputs(args.workload, n, rank)

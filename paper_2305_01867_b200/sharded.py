@@ -38,9 +38,11 @@ def gather_outputs(local: dict, n_total: int, group=None) -> dict:
         t = local[k]
         if t.shape[0] != hi - lo:
             raise ValueError(f"{k}: slice has {t.shape[0]} rows, expected {hi - lo}")
-        pad = torch.zeros((per,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        # gloo has no CUDA all_gather_into_tensor: stage through the host there
+        dev = t.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+        pad = torch.zeros((per,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
         pad[: hi - lo] = t
-        full = torch.empty((world * per,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        full = torch.empty((world * per,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
         dist.all_gather_into_tensor(full, pad, group=group)
         parts = [full[r * per: r * per + (shard_range(n_total, r, world)[1] - shard_range(n_total, r, world)[0])]
                  for r in range(world)]

@@ -332,7 +332,7 @@ def main():
             "data": "synthetic (seeded UV-sphere mesh, uniform segments; see DESIGN.md 4)",
             "config": {"workload": f"{args.workload} N_t={len(T)}, N_r={n}/GPU, mode={args.mode}",
                        "n_triangles": len(T), "rays_per_gpu": n, "mode": args.mode,
-                       "parallelism": f"ray-sharded x{world}" + (" + NCCL all_gather" if world > 1 else ""),
+                       "parallelism": f"ray-sharded x{world}" + (f" + {backend} gather to rank 0" if world > 1 else ""),
                        "l2": "inputs larger than L2 (240 MB of segments per GPU)",
                        "step": "rsi_rebuild + rsi_intersect" + (" + gather" if world > 1 else "")},
             "build_ms": build_ms, "query_ms": query_ms,

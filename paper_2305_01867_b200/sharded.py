@@ -25,10 +25,11 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
     return (n * rank) // world, (n * (rank + 1)) // world
 
 
-def gather_outputs(local: dict, n_total: int, group=None) -> dict:
-    """All-gather per-ray outputs of every rank's slice into full arrays in ray
-    order (every rank receives them; rank 0 is the consumer).  `local` holds
-    this rank's slice tensors (same device for all ranks' backend)."""
+def gather_outputs(local: dict, n_total: int, group=None, dst: int = 0) -> dict | None:
+    """Gather per-ray outputs of every rank's slice to rank `dst` in ray order
+    (one dist.gather per output field: NCCL point-to-point over NVLink on GPUs,
+    gloo in the CPU tests).  Slices are padded to ceil(N / W) rows.  Returns the
+    full arrays on `dst` and None on the other ranks."""
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
     per = -(-n_total // world)
@@ -38,16 +39,15 @@ def gather_outputs(local: dict, n_total: int, group=None) -> dict:
         t = local[k]
         if t.shape[0] != hi - lo:
             raise ValueError(f"{k}: slice has {t.shape[0]} rows, expected {hi - lo}")
-        # gloo has no CUDA all_gather_into_tensor: stage through the host there
         dev = t.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
         pad = torch.zeros((per,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
         pad[: hi - lo] = t
-        full = torch.empty((world * per,) + tuple(t.shape[1:]), dtype=t.dtype, device=dev)
-        dist.all_gather_into_tensor(full, pad, group=group)
-        parts = [full[r * per: r * per + (shard_range(n_total, r, world)[1] - shard_range(n_total, r, world)[0])]
-                 for r in range(world)]
-        out[k] = torch.cat(parts, 0)
-    return out
+        bufs = [torch.empty_like(pad) for _ in range(world)] if rank == dst else None
+        dist.gather(pad, bufs, dst=dst, group=group)
+        if rank == dst:
+            out[k] = torch.cat([bufs[r][: shard_range(n_total, r, world)[1] - shard_range(n_total, r, world)[0]]
+                                for r in range(world)], 0)
+    return out if rank == dst else None
 
 
 def intersect_sharded(vertices: torch.Tensor, triangles: torch.Tensor, start: torch.Tensor, end: torch.Tensor,
@@ -70,4 +70,4 @@ def intersect_sharded(vertices: torch.Tensor, triangles: torch.Tensor, start: to
     else:
         local = intersect_fn(vertices, triangles, start[lo:hi], end[lo:hi], mode)
     local = {k: local[k] for k in FIELDS[mode] if k in local}
-    return gather_outputs(local, n, group)
+    return gather_outputs(local, n, group)  # full outputs on rank 0, None elsewhere

@@ -53,7 +53,10 @@ def _worker(rank, world, port, n_rays, q):
         res = {}
         for mode in ("boolean", "barycentric", "intercept_count"):
             g = intersect_sharded(V, T, S, E, mode, intersect_fn=_oracle_fn)
-            res[mode] = {k: v.numpy() for k, v in g.items()}
+            if rank == 0:
+                res[mode] = {k: v.numpy() for k, v in g.items()}
+            else:
+                assert g is None
         if rank == 0:
             q.put(res)
     finally:

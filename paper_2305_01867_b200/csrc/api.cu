@@ -275,7 +275,7 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
 rsi_status_t rsi_free(rsi_handle_t h) {
     if (!h) return RSI_OK;
     cudaStream_t s = h->stream;
-    void* bufs[] = {h->nodes, h->quads, h->tris, h->keys, h->vals, h->keys_tmp, h->vals_tmp, h->parent,
+    void* bufs[] = {h->nodes, h->top, h->quads, h->tris, h->keys, h->vals, h->keys_tmp, h->vals_tmp, h->parent,
                     h->arrivals, h->hist, h->scratch, h->stats, h->ovf_list};
     rsi_status_t st = RSI_OK;
     for (void* p : bufs)

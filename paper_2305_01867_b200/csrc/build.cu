@@ -520,6 +520,94 @@ __global__ void __launch_bounds__(kSmallThreads) k_sort_smem(uint32_t* gk, int32
     }
 }
 
+// ------------------------------------------------------------------ top-of-tree image (shared-memory cache)
+// The top levels of the tree (whole levels, breadth-first, at most kTopNodes
+// nodes) are copied into a separate image whose child refs point at image
+// slots (kSmemRef + slot) when the child is cached too.  The traversal kernel
+// loads the image into shared memory once per CTA, so the node fetches every
+// segment makes near the root are conflict-light shared-memory reads instead
+// of one L1 wavefront per lane.  One CTA, level-synchronous.
+__device__ int block_exclusive_scan(int v, int* s_warp, int& total) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int inc = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
+    }
+    if (lane == 31) s_warp[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        const int x = lane < nw ? s_warp[lane] : 0;
+        int xi = x;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, xi, o);
+            if (lane >= o) xi += y;
+        }
+        if (lane < nw) s_warp[lane] = xi - x;
+        if (lane == 31) s_warp[32] = xi;
+    }
+    __syncthreads();
+    const int r = s_warp[w] + inc - v;
+    total = s_warp[32];
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(1024) k_topk(const float4* __restrict__ nodes, int n_nodes, float4* __restrict__ image,
+                                               uint32_t* scratch) {
+    __shared__ int old_of[kTopNodes > 0 ? kTopNodes : 1];
+    __shared__ int first_child[kTopNodes > 0 ? kTopNodes : 1];
+    __shared__ int s_warp[33];
+    const int tid = threadIdx.x;
+    int a = 0, b = 1;  // current level = slots [a, b)
+    if (tid == 0) old_of[0] = 0;
+    for (int i = tid; i < kTopNodes; i += blockDim.x) first_child[i] = -1;
+    __syncthreads();
+    while (true) {
+        // each thread owns up to two slots of the level (levels fit kTopNodes <= 2 * blockDim)
+        int cnt[2] = {0, 0};
+        int4 refs[2];
+        for (int h = 0; h < 2; ++h) {
+            const int sl = a + 2 * tid + h;
+            if (sl < b) {
+                refs[h] = *reinterpret_cast<const int4*>(nodes + 4 * old_of[sl] + 3);
+                cnt[h] = (refs[h].x >= 0) + (refs[h].y >= 0);
+            }
+        }
+        int total;
+        const int off = block_exclusive_scan(cnt[0] + cnt[1], s_warp, total);
+        if (total == 0 || b + total > kTopNodes) break;  // next level absent or does not fit
+        int k = b + off;
+        for (int h = 0; h < 2; ++h) {
+            const int sl = a + 2 * tid + h;
+            if (sl < b && cnt[h]) {
+                first_child[sl] = k;
+                if (refs[h].x >= 0) old_of[k++] = refs[h].x;
+                if (refs[h].y >= 0) old_of[k++] = refs[h].y;
+            }
+        }
+        __syncthreads();
+        a = b;
+        b += total;
+    }
+    // image: node data with child refs translated to image slots where cached
+    for (int sl = tid; sl < b; sl += blockDim.x) {
+        const float4* nd = nodes + 4 * old_of[sl];
+        float4* im = image + 4 * sl;
+        im[0] = nd[0];
+        im[1] = nd[1];
+        im[2] = nd[2];
+        int4 r = *reinterpret_cast<const int4*>(nd + 3);
+        const int fc = first_child[sl];
+        if (fc >= 0) {
+            if (r.x >= 0) r.x = (int)(kSmemRef + fc);
+            if (r.y >= 0) r.y = (int)(kSmemRef + fc + (r.x >= 0 ? 1 : 0));
+        }
+        *reinterpret_cast<int4*>(im + 3) = r;
+    }
+    if (tid == 0) scratch[SCR_NTOP] = (uint32_t)(n_nodes > 1 ? b : 0);
+}
+
 // ------------------------------------------------------------------ 4-wide view (grandchild records)
 // One thread per internal node n: the up-to-4 grandchildren of n (a leaf child
 // stands for itself), their AABBs quantized to 8 bits on a per-axis
@@ -634,7 +722,7 @@ __global__ void __launch_bounds__(kBlock) k_quads(const float4* __restrict__ nod
 static rsi_status_t ensure_capacity(rsi_bvh* h, int64_t n, cudaStream_t s) {
     int nb = rsi_ceil_div(n, kTile);
     if (n <= h->cap_tri && nb <= h->sort_blocks_cap) return RSI_OK;
-    void* old[] = {h->nodes, h->quads, h->tris, h->keys, h->vals, h->keys_tmp, h->vals_tmp, h->parent, h->arrivals, h->hist};
+    void* old[] = {h->nodes, h->top, h->quads, h->tris, h->keys, h->vals, h->keys_tmp, h->vals_tmp, h->parent, h->arrivals, h->hist};
     for (void* p : old)
         if (p) cudaFreeAsync(p, s);
     int64_t nn = n > 1 ? n - 1 : 1;
@@ -642,6 +730,7 @@ static rsi_status_t ensure_capacity(rsi_bvh* h, int64_t n, cudaStream_t s) {
 #define RSI_ALLOC(ptr, bytes) \
     if (e == cudaSuccess) e = cudaMallocAsync((void**)&(ptr), (size_t)(bytes), s);
     RSI_ALLOC(h->nodes, nn * 4 * sizeof(float4));
+    RSI_ALLOC(h->top, (size_t)(kTopNodes > 0 ? kTopNodes : 1) * 4 * sizeof(float4));
     RSI_ALLOC(h->quads, nn * 4 * sizeof(float4));
     RSI_ALLOC(h->tris, n * 4 * sizeof(float4));
     RSI_ALLOC(h->keys, n * sizeof(uint32_t));
@@ -711,6 +800,7 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
     k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent, h->arrivals);
     k_refit<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, h->vals, n, h->nodes, h->tris, h->parent,
                                                         h->arrivals, h->scratch);
+    if (kTopNodes > 0) k_topk<<<1, 1024, 0, s>>>(h->nodes, n_nodes, h->top, h->scratch);
     if (rsi_uses_quads()) k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads, h->scratch);
     st = rsi_cuda_check(cudaGetLastError(), "build kernel launch");
     if (st != RSI_OK) return st;
@@ -747,6 +837,7 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
             h->tex_nodes = 0;
         }
     }
+    h->n_top = (int)h->h_pinned[SCR_NTOP];
     h->n_tri = nt;
     h->n_nodes = n_nodes;
     h->stream = s;

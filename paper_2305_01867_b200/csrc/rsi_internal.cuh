@@ -32,6 +32,7 @@ enum {
     SCR_OVF_COUNT = 16, // intercept_count overflow list length
     SCR_OVF_TOTAL = 17, // re-pass: total raw hits over overflowed rays
     SCR_DISPENSER = 18, // 2 words: 64-bit ray dispenser of the persistent traversal grid
+    SCR_NTOP = 20,      // nodes in the top-of-tree shared-memory image
     SCR_WORDS = 32
 };
 enum { STATUS_INDEX = 1u, STATUS_NONFINITE = 2u, STATUS_RANGE = 4u };
@@ -54,6 +55,8 @@ struct rsi_bvh {
     float4* nodes = nullptr;         // [4 * n_nodes]
     float4* quads = nullptr;         // [4 * n_nodes] compressed grandchild (4-wide) records
     cudaTextureObject_t tex_nodes = 0;  // texture view of `nodes` (recreated on rebuild)
+    float4* top = nullptr;           // [4 * kTopNodes] top-of-tree image (refs >= kSmemRef are image slots)
+    int n_top = 0;
     float4* tris = nullptr;          // [4 * n_tri]
     uint32_t* keys = nullptr;        // sorted Morton codes [n_tri]
     int32_t* vals = nullptr;         // sorted triangle ids [n_tri]
@@ -113,5 +116,12 @@ __host__ __device__ inline float rsi_ord2f(uint32_t u) {
     return f;
 #endif
 }
+
+// top-of-tree shared-memory cache (build.cu k_topk, traverse.cu)
+#ifndef RSI_TOPK
+#define RSI_TOPK 2048
+#endif
+constexpr int kTopNodes = RSI_TOPK;           // <= 2 x 1024 (k_topk owns two slots per thread)
+constexpr uint32_t kSmemRef = 0x40000000u;    // child ref >= kSmemRef: slot in the image
 
 static inline int rsi_ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }

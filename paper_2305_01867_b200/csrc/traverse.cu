@@ -62,7 +62,13 @@ constexpr int kCountCap = 8;  // intercept_count hits held in registers per ray
 #ifndef RSI_OTHER_MINB
 #define RSI_OTHER_MINB 6
 #endif
-constexpr int kThreads = 128;
+constexpr int kThreads = 128;  // block size of the auxiliary (re-pass) kernels
+// k_trace block size: with the top-of-tree cache, one CTA per SM shares the
+// image (1024 threads at <= 64 registers for boolean, 768 at <= 80 otherwise)
+template <int MODE>
+__host__ __device__ constexpr int trace_threads() {
+    return kTopNodes > 0 ? (MODE == 0 ? 1024 : 768) : 128;
+}
 constexpr int kChunk = 64;   // rays a warp takes from the global dispenser at once
 
 enum { MT_MISS = 0, MT_HIT = 1, MT_UNSURE = 2 };
@@ -321,6 +327,8 @@ struct TraceParams {
     const float4* nodes;
     cudaTextureObject_t tex_nodes;  // same array through the texture path (RSI_TEX_NODES)
     const float4* quads;
+    const float4* top;   // top-of-tree image [4 * n_top]
+    int n_top;
     const float4* tris;
     const float* S;
     const float* E;
@@ -484,7 +492,8 @@ __device__ __forceinline__ void sort_small(double* v, int n) {
 
 template <>
 struct ModeState<MODE_COUNT> {
-    float2* te;  // shared: te[x * kThreads] = (t, err) of hit x
+    int stride;  // threads per block: entry x of this lane at te[x * stride]
+    float2* te;  // shared: te[x * stride] = (t, err) of hit x
     int* kk;     // shared: leaf slot of hit x
     int nh;
     bool overflow;
@@ -509,8 +518,8 @@ struct ModeState<MODE_COUNT> {
             t32 = (float)t64;
             et = fmaf(kU, fabsf(t32), kTiny);
         }
-        te[nh * kThreads] = make_float2(t32, et);
-        kk[nh * kThreads] = k;
+        te[nh * stride] = make_float2(t32, et);
+        kk[nh * stride] = k;
         ++nh;
         return false;
     }
@@ -530,7 +539,7 @@ struct ModeState<MODE_COUNT> {
 #pragma unroll
         for (int x = 0; x < kCountCap; ++x)
             if (x < nh) {
-                const float2 v = te[x * kThreads];
+                const float2 v = te[x * stride];
                 lt[x] = v.x;
                 le[x] = v.y;
             }
@@ -563,7 +572,7 @@ struct ModeState<MODE_COUNT> {
             double v[kCountCap];
             for (int a = 0; a < nh; ++a) {
                 float4 A, B, C;
-                load_tri(p.tris, kk[a * kThreads], A, B, C);
+                load_tri(p.tris, kk[a * stride], A, B, C);
                 mt64(r, A, B, C, &v[a]);
             }
             sort_small(v, nh);
@@ -585,20 +594,20 @@ struct ModeState<MODE_COUNT> {
 //      lanes, while others wait with leaves) is still searching;
 //   3. leaf phase: all lanes with pending leaves run Moller-Trumbore together;
 //   4. finished rays write their outputs and free the lane.
-template <int kStack, int kSmemStack>
+template <int kStack, int kSmemStack, int kT>
 struct LaneStack {
-    int* s;  // this lane's shared-memory column: entry k at s[k * kThreads]
+    int* s;  // this lane's shared-memory column: entry k at s[k * kT]
     int local[kStack - kSmemStack];
     __device__ __forceinline__ void push(int& sp, int x) {
         if (sp < kSmemStack)
-            s[sp * kThreads] = x;
+            s[sp * kT] = x;
         else
             local[sp - kSmemStack] = x;
         ++sp;
     }
     __device__ __forceinline__ int pop(int& sp) {
         --sp;
-        return sp < kSmemStack ? s[sp * kThreads] : local[sp - kSmemStack];
+        return sp < kSmemStack ? s[sp * kT] : local[sp - kSmemStack];
     }
 };
 
@@ -614,7 +623,7 @@ __device__ __forceinline__ void cas(float& ka, int& ca, float& kb, int& cb) {
 }
 
 template <int MODE, bool kFP64, bool kCounters>
-__global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : RSI_OTHER_MINB) k_trace(const TraceParams p) {
+__global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MODE == MODE_BOOL ? RSI_BOOL_MINB : RSI_OTHER_MINB)) k_trace(const TraceParams p) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
@@ -622,8 +631,15 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
     constexpr bool kQuad = MODE == MODE_BOOL ? RSI_BOOL_QUAD : (MODE == MODE_BARY ? RSI_BARY_QUAD : RSI_COUNT_QUAD);
     constexpr int kSmemStack = MODE == MODE_BOOL ? RSI_BOOL_SMEM : (MODE == MODE_BARY ? RSI_BARY_SMEM : RSI_COUNT_SMEM);
     constexpr int kStack = kQuad ? kStackQuad : kStackBinary;
-    __shared__ float2 s_te[MODE == MODE_COUNT ? kCountCap * kThreads : 1];
-    __shared__ int s_k[MODE == MODE_COUNT ? kCountCap * kThreads : 1];
+    constexpr int kT = trace_threads<MODE>();
+    // dynamic shared memory: [top-of-tree image: kTopNodes x 64 B][intercept_count hit lists]
+    extern __shared__ float4 s_dyn[];
+    float4* s_top = s_dyn;
+    float2* s_te = reinterpret_cast<float2*>(s_dyn + 4 * kTopNodes);
+    int* s_k = reinterpret_cast<int*>(s_te + kCountCap * kT);
+    // top-of-tree image, loaded once per CTA
+    for (int i = threadIdx.x; i < 4 * p.n_top; i += kT) s_top[i] = p.top[i];
+    __syncthreads();
     Stats st;
 
     int64_t cnext = 0, cend = 0;  // warp-uniform chunk [cnext, cend)
@@ -633,15 +649,17 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
     int node = -1, sp = 0, l0 = -1, l1 = -1, l2 = -1;  // pending (postponed) leaf slots
     // per-lane traversal stack: the first kSmemStack entries in a shared-memory
     // column (one bank per lane: conflict-free at any depth), the rest local
-    LaneStack<kStack, kSmemStack> stk;
-    __shared__ int s_stack[kSmemStack > 0 ? kSmemStack * kThreads : 1];
+    LaneStack<kStack, kSmemStack, kT> stk;
+    __shared__ int s_stack[kSmemStack > 0 ? kSmemStack * kT : 1];
     stk.s = s_stack + threadIdx.x;
     float tclip = 1.0f;
     ModeState<MODE> ms;
     if constexpr (MODE == MODE_COUNT) {
+        ms.stride = kT;
         ms.te = s_te + threadIdx.x;
         ms.kk = s_k + threadIdx.x;
     }
+    const int root = p.n_top > 0 ? (int)kSmemRef : 0;
     while (true) {
         // ---- 1. refill
         unsigned want = __ballot_sync(FULL, ray < 0);
@@ -677,7 +695,7 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
             tclip = 1.0f;
             sp = 0;
             l0 = l1 = l2 = -1;
-            node = ok ? 0 : -1;
+            node = ok ? root : -1;
         }
         if (__ballot_sync(FULL, ray >= 0) == 0) break;  // no rays left for this warp
 
@@ -837,10 +855,18 @@ __global__ void __launch_bounds__(kThreads, MODE == MODE_BOOL ? RSI_BOOL_MINB : 
                 const float4 n2 = tex1Dfetch<float4>(p.tex_nodes, 4 * node + 2);
                 const float4 n3f = tex1Dfetch<float4>(p.tex_nodes, 4 * node + 3);
 #else
-                const float4* nd = p.nodes + 4 * node;
                 float4 n0, n1, n2, n3f;
-                ldg256(nd, n0, n1);
-                ldg256(nd + 2, n2, n3f);
+                if (node >= (int)kSmemRef) {  // cached top of the tree
+                    const float4* sn = s_top + 4 * (node - (int)kSmemRef);
+                    n0 = sn[0];
+                    n1 = sn[1];
+                    n2 = sn[2];
+                    n3f = sn[3];
+                } else {
+                    const float4* nd = p.nodes + 4 * node;
+                    ldg256(nd, n0, n1);
+                    ldg256(nd + 2, n2, n3f);
+                }
 #endif
                 const int4 n3 = make_int4(__float_as_int(n3f.x), __float_as_int(n3f.y), 0, 0);
                 float nearL, nearR;
@@ -1083,17 +1109,21 @@ __global__ void __launch_bounds__(256) k_compact_write(const int32_t* __restrict
 // ---------------------------------------------------------------- host side
 template <int MODE, bool kFP64, bool kCounters>
 static void launch_trace(const TraceParams& p, cudaStream_t s) {
+    constexpr int kT = trace_threads<MODE>();
+    constexpr int kDyn = kTopNodes * 4 * (int)sizeof(float4) + (MODE == MODE_COUNT ? kCountCap * kT * 12 : 0);
+    const size_t dyn = kDyn;
     static int grid = 0;  // persistent grid: resident blocks per SM x SMs (per instantiation)
     if (grid == 0) {
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trace<MODE, kFP64, kCounters>, kThreads, 0);
+        cudaFuncSetAttribute(k_trace<MODE, kFP64, kCounters>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trace<MODE, kFP64, kCounters>, kT, kDyn);
         grid = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
     }
-    const int64_t need = (p.n + kThreads - 1) / kThreads;
+    const int64_t need = (p.n + kT - 1) / kT;
     const int g = (int)(need < grid ? need : grid);
-    k_trace<MODE, kFP64, kCounters><<<g, kThreads, 0, s>>>(p);
+    k_trace<MODE, kFP64, kCounters><<<g, kT, dyn, s>>>(p);
 }
 
 template <bool kFP64, bool kCounters>
@@ -1127,6 +1157,8 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     p.nodes = h->nodes;
     p.tex_nodes = h->tex_nodes;
     p.quads = h->quads;
+    p.top = h->top;
+    p.n_top = kTopNodes > 0 ? h->n_top : 0;
     p.tris = h->tris;
     p.S = S;
     p.E = E;

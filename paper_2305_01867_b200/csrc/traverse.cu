@@ -102,16 +102,33 @@ __device__ __forceinline__ void slab_axis(float o, float d, float& inv, float& o
     offhi = -INFINITY;
 }
 
+#ifndef RSI_PREFER_L1
+#define RSI_PREFER_L1 1
+#endif
+#ifndef RSI_STREAM_NOALLOC
+#define RSI_STREAM_NOALLOC 1
+#endif
+__device__ __forceinline__ float ld_stream(const float* p) {
+#if RSI_STREAM_NOALLOC
+    float v;
+    asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+
 // Returns false for rays that cannot hit: zero length or a non-finite coordinate
 // (reading R12).  `nonfinite` is set for the latter.
 __device__ __forceinline__ bool load_ray(Ray& r, const float* __restrict__ S, const float* __restrict__ E,
                                          int64_t i, bool& nonfinite) {
-    r.ox = __ldg(S + 3 * i);
-    r.oy = __ldg(S + 3 * i + 1);
-    r.oz = __ldg(S + 3 * i + 2);
-    r.ex = __ldg(E + 3 * i);
-    r.ey = __ldg(E + 3 * i + 1);
-    r.ez = __ldg(E + 3 * i + 2);
+    // the segment stream is read once: do not let it displace tree nodes in L1
+    r.ox = ld_stream(S + 3 * i);
+    r.oy = ld_stream(S + 3 * i + 1);
+    r.oz = ld_stream(S + 3 * i + 2);
+    r.ex = ld_stream(E + 3 * i);
+    r.ey = ld_stream(E + 3 * i + 1);
+    r.ez = ld_stream(E + 3 * i + 2);
     nonfinite = !(isfinite(r.ox) && isfinite(r.oy) && isfinite(r.oz) && isfinite(r.ex) && isfinite(r.ey) &&
                   isfinite(r.ez));
     r.dx = r.ex - r.ox;
@@ -1118,6 +1135,9 @@ static void launch_trace(const TraceParams& p, cudaStream_t s) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         cudaFuncSetAttribute(k_trace<MODE, kFP64, kCounters>, cudaFuncAttributeMaxDynamicSharedMemorySize, kDyn);
+#if RSI_PREFER_L1
+        if (kDyn == 0) cudaFuncSetAttribute(k_trace<MODE, kFP64, kCounters>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+#endif
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_trace<MODE, kFP64, kCounters>, kT, kDyn);
         grid = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
     }

@@ -119,7 +119,7 @@ __host__ __device__ inline float rsi_ord2f(uint32_t u) {
 
 // top-of-tree shared-memory cache (build.cu k_topk, traverse.cu)
 #ifndef RSI_TOPK
-#define RSI_TOPK 2048
+#define RSI_TOPK 0  // measured slower at 1024/2048 on the bench workload (1 CTA/SM)
 #endif
 constexpr int kTopNodes = RSI_TOPK;           // <= 2 x 1024 (k_topk owns two slots per thread)
 constexpr uint32_t kSmemRef = 0x40000000u;    // child ref >= kSmemRef: slot in the image

@@ -103,10 +103,10 @@ __device__ __forceinline__ void slab_axis(float o, float d, float& inv, float& o
 }
 
 #ifndef RSI_PREFER_L1
-#define RSI_PREFER_L1 1
+#define RSI_PREFER_L1 0
 #endif
 #ifndef RSI_STREAM_NOALLOC
-#define RSI_STREAM_NOALLOC 1
+#define RSI_STREAM_NOALLOC 0
 #endif
 __device__ __forceinline__ float ld_stream(const float* p) {
 #if RSI_STREAM_NOALLOC

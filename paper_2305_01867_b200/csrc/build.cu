@@ -801,7 +801,6 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
     k_refit<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, h->vals, n, h->nodes, h->tris, h->parent,
                                                         h->arrivals, h->scratch);
     if (kTopNodes > 0) k_topk<<<1, 1024, 0, s>>>(h->nodes, n_nodes, h->top, h->scratch);
-    else cudaMemsetAsync(h->scratch + SCR_NTOP, 0, sizeof(uint32_t), s);
     if (rsi_uses_quads()) k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads, h->scratch);
     st = rsi_cuda_check(cudaGetLastError(), "build kernel launch");
     if (st != RSI_OK) return st;
@@ -838,7 +837,7 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
             h->tex_nodes = 0;
         }
     }
-    h->n_top = (int)h->h_pinned[SCR_NTOP];
+    h->n_top = kTopNodes > 0 ? (int)h->h_pinned[SCR_NTOP] : 0;
     h->n_tri = nt;
     h->n_nodes = n_nodes;
     h->stream = s;

@@ -153,23 +153,9 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
     if (st != RSI_OK) return st;
     cudaStream_t s = (cudaStream_t)stream;
     rsi_keep_pool_cached();
-    // 1. mesh upload + build (the build synchronizes once for validation)
-    const size_t bv = (size_t)n_vertices * 3 * sizeof(float), bt = (size_t)n_triangles * 3 * sizeof(int32_t);
-    char* mesh = nullptr;
-    st = rsi_cuda_check(cudaMallocAsync((void**)&mesh, ((bv + 255) / 256) * 256 + bt, s), "rsi_test mesh");
-    if (st != RSI_OK) return st;
-    float* dV = (float*)mesh;
-    int32_t* dT = (int32_t*)(mesh + ((bv + 255) / 256) * 256);
-    st = rsi_cuda_check(cudaMemcpyAsync(dV, h_vertices, bv, cudaMemcpyHostToDevice, s), "H2D vertices");
-    if (st == RSI_OK) st = rsi_cuda_check(cudaMemcpyAsync(dT, h_triangles, bt, cudaMemcpyHostToDevice, s), "H2D triangles");
-    rsi_handle_t h = nullptr;
-    if (st == RSI_OK) st = rsi_build(dV, n_vertices, dT, n_triangles, options, stream, &h);
-    cudaFreeAsync(mesh, s);
-    if (st != RSI_OK) return st;
-
-    // 2. rays in chunks through a 3-stream pipeline: H2D(c+1) and D2H(c-1)
-    //    overlap the traversal of chunk c (which runs on the caller's stream).
-    const int64_t kChunkRays = (int64_t)1 << 21;
+    // 1. ray pipeline resources (allocated first so the first ray chunks can
+    //    stream in while the mesh is uploaded and the BVH is built)
+    const int64_t kChunkRays = (int64_t)1 << 20;
     const int64_t nchunk = (n_rays + kChunkRays - 1) / kChunkRays;
     const int64_t crays = n_rays < kChunkRays ? n_rays : kChunkRays;
     size_t out_b = mode == RSI_MODE_BOOLEAN ? 1 : (mode == RSI_MODE_INTERCEPT_COUNT ? 4 : 24);
@@ -189,7 +175,7 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
         for (int64_t k = 0; st == RSI_OK && k < 3 * nchunk; ++k)
             st = rsi_cuda_check(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming), "event");
     }
-    cudaEvent_t ready = nullptr;  // slots allocated + handle built on `s`
+    cudaEvent_t ready = nullptr;  // ray slots allocated on `s`
     if (st == RSI_OK && nchunk > 0) {
         st = rsi_cuda_check(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
         if (st == RSI_OK) st = rsi_cuda_check(cudaEventRecord(ready, s), "event");
@@ -208,9 +194,28 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
                                                 cudaMemcpyHostToDevice, sh), "H2D end");
         if (st == RSI_OK) st = rsi_cuda_check(cudaEventRecord(ev[3 * c], sh), "event");
     };
-    if (st == RSI_OK && nchunk > 0) h2d(0);
+    int64_t issued = 0;
+    while (st == RSI_OK && issued < nchunk && issued < 2) h2d(issued++);
+
+    // 2. mesh upload + build on `s` (synchronizes once for validation) while
+    //    the first ray chunks copy on `sh`
+    const size_t bv = (size_t)n_vertices * 3 * sizeof(float), bt = (size_t)n_triangles * 3 * sizeof(int32_t);
+    char* mesh = nullptr;
+    rsi_handle_t h = nullptr;
+    if (st == RSI_OK) st = rsi_cuda_check(cudaMallocAsync((void**)&mesh, up(bv) + bt, s), "rsi_test mesh");
+    if (st == RSI_OK) {
+        float* dV = (float*)mesh;
+        int32_t* dT = (int32_t*)(mesh + up(bv));
+        st = rsi_cuda_check(cudaMemcpyAsync(dV, h_vertices, bv, cudaMemcpyHostToDevice, s), "H2D vertices");
+        if (st == RSI_OK)
+            st = rsi_cuda_check(cudaMemcpyAsync(dT, h_triangles, bt, cudaMemcpyHostToDevice, s), "H2D triangles");
+        if (st == RSI_OK) st = rsi_build(dV, n_vertices, dT, n_triangles, options, stream, &h);
+        cudaFreeAsync(mesh, s);
+    }
+
+    // 3. chunk loop: H2D(c+1) and D2H(c-1) overlap the traversal of chunk c
     for (int64_t c = 0; st == RSI_OK && c < nchunk; ++c) {
-        if (c + 1 < nchunk) h2d(c + 1);
+        while (st == RSI_OK && issued < nchunk && issued <= c + 1) h2d(issued++);
         if (st != RSI_OK) break;
         const int64_t r0 = c * kChunkRays, nr = (n_rays - r0) < kChunkRays ? (n_rays - r0) : kChunkRays;
         char* b = slot(c);
@@ -244,12 +249,13 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
         }
         if (st == RSI_OK) st = rsi_cuda_check(cudaEventRecord(ev[3 * c + 2], sd), "event");
     }
-    // 3. drain, release (frees ordered after the last D2H), synchronize
+    // 4. drain, release (frees ordered after the last D2H), synchronize
     rsi_status_t st2 = RSI_OK;
-    if (sd) {
+    for (cudaStream_t side : {sh, sd}) {  // order the frees after all copies (also on error paths)
+        if (!side) continue;
         cudaEvent_t fin;
         if (cudaEventCreateWithFlags(&fin, cudaEventDisableTiming) == cudaSuccess) {
-            cudaEventRecord(fin, sd);
+            cudaEventRecord(fin, side);
             cudaStreamWaitEvent(s, fin, 0);
             cudaEventDestroy(fin);
         }

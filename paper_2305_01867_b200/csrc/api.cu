@@ -153,6 +153,12 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
     if (st != RSI_OK) return st;
     cudaStream_t s = (cudaStream_t)stream;
     rsi_keep_pool_cached();
+    if (getenv("RSI_TEST_TRACE")) {  // diagnostics: is the caller's host memory page-locked?
+        cudaPointerAttributes a{};
+        cudaError_t e = cudaPointerGetAttributes(&a, h_start);
+        fprintf(stderr, "rsi_test: h_start type=%d (0 unreg, 1 host, 2 device) err=%d\n", (int)a.type, (int)e);
+        (void)cudaGetLastError();
+    }
     // 1. ray pipeline resources (allocated first so the first ray chunks can
     //    stream in while the mesh is uploaded and the BVH is built)
     const int64_t kChunkRays = (int64_t)1 << 20;

@@ -26,3 +26,8 @@ print("intersect (dev)    ms", tm(lambda: rsi.rsi_intersect(h, dS, dE, "boolean"
 def manual():
     cp(); rsi.rsi_rebuild(h, Vd, Td); rsi.rsi_intersect(h, dS, dE, "boolean", out=o); out["hit"].copy_(o["hit"], non_blocking=True)
 print("serial H2D+build+intersect+D2H ms", tm(manual))
+os.environ["RSI_TEST_TRACE"] = "1"
+rsi.rsi_test(hV, hT, hS, hE, {"mode": "boolean"}, out=out)
+import ctypes
+cudart = ctypes.CDLL("libcudart.so.12") if False else None
+t = time.perf_counter(); rsi.rsi_test(hV, hT, hS, hE, {"mode": "boolean"}, out=out); print("traced call ms", (time.perf_counter()-t)*1e3)

@@ -161,7 +161,8 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
     }
     // 1. ray pipeline resources (allocated first so the first ray chunks can
     //    stream in while the mesh is uploaded and the BVH is built)
-    const int64_t kChunkRays = (int64_t)1 << 20;
+    int64_t kChunkRays = (int64_t)1 << 20;
+    if (const char* e = getenv("RSI_TEST_CHUNK")) kChunkRays = atoll(e) > 0 ? atoll(e) : kChunkRays;  // tuning
     const int64_t nchunk = (n_rays + kChunkRays - 1) / kChunkRays;
     const int64_t crays = n_rays < kChunkRays ? n_rays : kChunkRays;
     size_t out_b = mode == RSI_MODE_BOOLEAN ? 1 : (mode == RSI_MODE_INTERCEPT_COUNT ? 4 : 24);

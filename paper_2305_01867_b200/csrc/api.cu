@@ -47,6 +47,26 @@ static rsi_status_t check_mesh_args(const float* V, int64_t nv, const int32_t* T
     return RSI_OK;
 }
 
+// Two non-blocking copy streams per (thread, device) for rsi_test's pipeline,
+// created once (stream creation is not free) and reused by later calls.
+static rsi_status_t side_streams(cudaStream_t& sh, cudaStream_t& sd) {
+    struct Pair { int dev = -1; cudaStream_t h = nullptr, d = nullptr; };
+    static thread_local Pair cache[16];
+    int dev = 0;
+    rsi_status_t st = rsi_cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (st != RSI_OK) return st;
+    Pair& p = cache[dev & 15];
+    if (p.dev != dev) {
+        st = rsi_cuda_check(cudaStreamCreateWithFlags(&p.h, cudaStreamNonBlocking), "stream");
+        if (st == RSI_OK) st = rsi_cuda_check(cudaStreamCreateWithFlags(&p.d, cudaStreamNonBlocking), "stream");
+        if (st != RSI_OK) return st;
+        p.dev = dev;
+    }
+    sh = p.h;
+    sd = p.d;
+    return RSI_OK;
+}
+
 // Keep freed stream-ordered allocations cached in the device's default pool, so
 // per-call cudaMallocAsync / cudaFreeAsync (rsi_test, overflow pass) do not
 // return memory to the OS between calls.
@@ -87,7 +107,6 @@ rsi_status_t rsi_build(const float* d_vertices, int64_t n_vertices, const int32_
     if (st == RSI_OK)
         st = rsi_cuda_check(cudaMallocAsync((void**)&h->stats, ST_WORDS * sizeof(unsigned long long), s), "stats");
     if (st == RSI_OK) st = rsi_cuda_check(cudaMemsetAsync(h->stats, 0, ST_WORDS * sizeof(unsigned long long), s), "stats");
-    if (st == RSI_OK) st = rsi_cuda_check(cudaMallocHost((void**)&h->h_pinned, 64 * sizeof(uint32_t)), "pinned");
     if (st == RSI_OK) st = rsi_build_device(h, d_vertices, n_vertices, d_triangles, n_triangles, s);
     if (st != RSI_OK) {
         char saved[512];
@@ -173,8 +192,7 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
     cudaEvent_t* ev = nullptr;  // per chunk: h2d done, kernel done, d2h done
     if (nchunk > 0) {
         st = rsi_cuda_check(cudaMallocAsync((void**)&slots, 2 * slot_b, s), "rsi_test ray buffers");
-        if (st == RSI_OK) st = rsi_cuda_check(cudaStreamCreateWithFlags(&sh, cudaStreamNonBlocking), "stream");
-        if (st == RSI_OK) st = rsi_cuda_check(cudaStreamCreateWithFlags(&sd, cudaStreamNonBlocking), "stream");
+        if (st == RSI_OK) st = side_streams(sh, sd);
         if (st == RSI_OK) {
             ev = new (std::nothrow) cudaEvent_t[3 * nchunk]();
             if (!ev) st = rsi_set_error(RSI_E_OOM, "host allocation failed");
@@ -275,8 +293,6 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
     }
     if (slots) cudaFreeAsync(slots, s);
     st2 = rsi_cuda_check(cudaStreamSynchronize(s), "rsi_test");
-    if (sh) cudaStreamDestroy(sh);
-    if (sd) cudaStreamDestroy(sd);
     if (ev)
         for (int64_t k = 0; k < 3 * nchunk; ++k)
             if (ev[k]) cudaEventDestroy(ev[k]);
@@ -296,7 +312,6 @@ rsi_status_t rsi_free(rsi_handle_t h) {
             rsi_status_t e = rsi_cuda_check(cudaFreeAsync(p, s), "cudaFreeAsync");
             if (st == RSI_OK) st = e;
         }
-    if (h->h_pinned) cudaFreeHost(h->h_pinned);
     if (h->tex_nodes) cudaDestroyTextureObject(h->tex_nodes);
     delete h;
     return st;

@@ -804,18 +804,18 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
     if (rsi_uses_quads()) k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads, h->scratch);
     st = rsi_cuda_check(cudaGetLastError(), "build kernel launch");
     if (st != RSI_OK) return st;
-    st = rsi_cuda_check(cudaMemcpyAsync(h->h_pinned, h->scratch, SCR_WORDS * sizeof(uint32_t),
+    st = rsi_cuda_check(cudaMemcpyAsync(h->h_words, h->scratch, SCR_WORDS * sizeof(uint32_t),
                                         cudaMemcpyDeviceToHost, s),
                         "status read");
     if (st != RSI_OK) return st;
     st = rsi_cuda_check(cudaStreamSynchronize(s), "build");
     if (st != RSI_OK) return st;
-    uint32_t status = h->h_pinned[SCR_STATUS];
+    uint32_t status = h->h_words[SCR_STATUS];
     if (status & STATUS_INDEX) return rsi_set_error(RSI_E_INDEX_RANGE, "a triangle index is outside [0, %lld)", (long long)nv);
     if (status & STATUS_NONFINITE) return rsi_set_error(RSI_E_NONFINITE, "a vertex coordinate is NaN or Inf");
     if (status & STATUS_RANGE)
         return rsi_set_error(RSI_E_INVALID_ARG, "mesh extent too large for the quantized BVH (|coordinates| > ~1e33)");
-    const float* root = reinterpret_cast<const float*>(h->h_pinned + SCR_ROOT);
+    const float* root = reinterpret_cast<const float*>(h->h_words + SCR_ROOT);
     for (int x = 0; x < 3; ++x) {
         h->scene_lo[x] = root[x];
         h->scene_hi[x] = root[3 + x];
@@ -837,7 +837,7 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
             h->tex_nodes = 0;
         }
     }
-    h->n_top = kTopNodes > 0 ? (int)h->h_pinned[SCR_NTOP] : 0;
+    h->n_top = kTopNodes > 0 ? (int)h->h_words[SCR_NTOP] : 0;
     h->n_tri = nt;
     h->n_nodes = n_nodes;
     h->stream = s;

@@ -67,7 +67,8 @@ struct rsi_bvh {
     uint32_t* hist = nullptr;        // sort: [256 * blocks]
     uint32_t* scratch = nullptr;     // [SCR_WORDS]
     unsigned long long* stats = nullptr;  // [ST_WORDS]
-    uint32_t* h_pinned = nullptr;    // pinned host words for status reads
+    uint32_t h_words[64] = {};       // host words for status reads (small synchronous copies;
+                                     // no cudaMallocHost per handle -- it costs ~ms)
     // intercept_count overflow workspace
     int32_t* ovf_list = nullptr;     // ray ids
     int64_t ovf_cap = 0;

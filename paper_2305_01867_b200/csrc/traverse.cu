@@ -1206,12 +1206,12 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     if (mode != RSI_MODE_INTERCEPT_COUNT) return RSI_OK;
 
     // intercept_count: exact re-pass for rays that overflowed the register list
-    st = rsi_cuda_check(cudaMemcpyAsync(h->h_pinned, h->scratch + SCR_OVF_COUNT, sizeof(uint32_t),
+    st = rsi_cuda_check(cudaMemcpyAsync(h->h_words, h->scratch + SCR_OVF_COUNT, sizeof(uint32_t),
                                         cudaMemcpyDeviceToHost, s), "overflow count");
     if (st != RSI_OK) return st;
     st = rsi_cuda_check(cudaStreamSynchronize(s), "intercept_count");
     if (st != RSI_OK) return st;
-    const int n_ovf = (int)h->h_pinned[0];
+    const int n_ovf = (int)h->h_words[0];
     if (n_ovf == 0) return RSI_OK;
     int32_t* seg = nullptr;
     double* pool = nullptr;
@@ -1219,13 +1219,13 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     if (st != RSI_OK) return RSI_E_OOM;
     const int nb = rsi_ceil_div(n_ovf, kThreads);
     k_ovf_size<<<nb, kThreads, 0, s>>>(h->nodes, h->tris, S, E, h->ovf_list, n_ovf, seg, h->scratch);
-    cudaMemcpyAsync(h->h_pinned, h->scratch + SCR_OVF_TOTAL, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(h->h_words, h->scratch + SCR_OVF_TOTAL, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
     st = rsi_cuda_check(cudaStreamSynchronize(s), "overflow sizing");
     if (st != RSI_OK) {
         cudaFreeAsync(seg, s);
         return st;
     }
-    const size_t total = h->h_pinned[0];
+    const size_t total = h->h_words[0];
     st = rsi_cuda_check(cudaMallocAsync((void**)&pool, (total ? total : 1) * sizeof(double), s), "overflow pool");
     if (st != RSI_OK) {
         cudaFreeAsync(seg, s);

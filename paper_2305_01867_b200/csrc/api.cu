@@ -3,6 +3,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
 #include <new>
 
 #include "rsi_internal.cuh"
@@ -219,6 +220,13 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
                                                 cudaMemcpyHostToDevice, sh), "H2D end");
         if (st == RSI_OK) st = rsi_cuda_check(cudaEventRecord(ev[3 * c], sh), "event");
     };
+    const bool trace = getenv("RSI_TEST_TRACE") != nullptr;
+    auto now_ms = []() {
+        timespec ts;
+        clock_gettime(CLOCK_MONOTONIC, &ts);
+        return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+    };
+    const double t0 = now_ms();
     int64_t issued = 0;
     while (st == RSI_OK && issued < nchunk && issued < 2) h2d(issued++);
 
@@ -238,6 +246,7 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
         cudaFreeAsync(mesh, s);
     }
 
+    const double t_build = now_ms();
     // 3. chunk loop: H2D(c+1) and D2H(c-1) overlap the traversal of chunk c
     for (int64_t c = 0; st == RSI_OK && c < nchunk; ++c) {
         while (st == RSI_OK && issued < nchunk && issued <= c + 1) h2d(issued++);
@@ -274,6 +283,7 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
         }
         if (st == RSI_OK) st = rsi_cuda_check(cudaEventRecord(ev[3 * c + 2], sd), "event");
     }
+    const double t_loop = now_ms();
     // 4. drain, release (frees ordered after the last D2H), synchronize
     rsi_status_t st2 = RSI_OK;
     for (cudaStream_t side : {sh, sd}) {  // order the frees after all copies (also on error paths)
@@ -293,6 +303,9 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
     }
     if (slots) cudaFreeAsync(slots, s);
     st2 = rsi_cuda_check(cudaStreamSynchronize(s), "rsi_test");
+    if (trace)
+        fprintf(stderr, "rsi_test trace: setup+issue0 -> build done %.3f ms, loop issued %.3f ms, synced %.3f ms\n",
+                t_build - t0, t_loop - t0, now_ms() - t0);
     if (ev)
         for (int64_t k = 0; k < 3 * nchunk; ++k)
             if (ev[k]) cudaEventDestroy(ev[k]);

@@ -228,23 +228,25 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
     };
     const double t0 = now_ms();
     int64_t issued = 0;
-    while (st == RSI_OK && issued < nchunk && issued < 2) h2d(issued++);
-
-    // 2. mesh upload + build on `s` (synchronizes once for validation) while
-    //    the first ray chunks copy on `sh`
+    // 2. mesh upload first (so it is not queued behind ray chunks on the copy
+    //    engine), then the first ray chunks on `sh`, then the build on `s`
+    //    (synchronizes once for validation) while those chunks copy
     const size_t bv = (size_t)n_vertices * 3 * sizeof(float), bt = (size_t)n_triangles * 3 * sizeof(int32_t);
     char* mesh = nullptr;
     rsi_handle_t h = nullptr;
+    float* dV = nullptr;
+    int32_t* dT = nullptr;
     if (st == RSI_OK) st = rsi_cuda_check(cudaMallocAsync((void**)&mesh, up(bv) + bt, s), "rsi_test mesh");
     if (st == RSI_OK) {
-        float* dV = (float*)mesh;
-        int32_t* dT = (int32_t*)(mesh + up(bv));
+        dV = (float*)mesh;
+        dT = (int32_t*)(mesh + up(bv));
         st = rsi_cuda_check(cudaMemcpyAsync(dV, h_vertices, bv, cudaMemcpyHostToDevice, s), "H2D vertices");
         if (st == RSI_OK)
             st = rsi_cuda_check(cudaMemcpyAsync(dT, h_triangles, bt, cudaMemcpyHostToDevice, s), "H2D triangles");
-        if (st == RSI_OK) st = rsi_build(dV, n_vertices, dT, n_triangles, options, stream, &h);
-        cudaFreeAsync(mesh, s);
     }
+    while (st == RSI_OK && issued < nchunk && issued < 2) h2d(issued++);
+    if (st == RSI_OK) st = rsi_build(dV, n_vertices, dT, n_triangles, options, stream, &h);
+    if (mesh) cudaFreeAsync(mesh, s);
 
     const double t_build = now_ms();
     // 3. chunk loop: H2D(c+1) and D2H(c-1) overlap the traversal of chunk c

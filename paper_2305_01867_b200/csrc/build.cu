@@ -820,6 +820,9 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
         h->scene_lo[x] = root[x];
         h->scene_hi[x] = root[3 + x];
     }
+#ifdef RSI_TEX_NODES_BUILD
+    // texture view of the nodes (only for the RSI_TEX_NODES traversal experiment;
+    // texture-object creation per build is not free)
     if (h->tex_nodes) {
         cudaDestroyTextureObject(h->tex_nodes);
         h->tex_nodes = 0;
@@ -837,6 +840,7 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
             h->tex_nodes = 0;
         }
     }
+#endif
     h->n_top = kTopNodes > 0 ? (int)h->h_words[SCR_NTOP] : 0;
     h->n_tri = nt;
     h->n_nodes = n_nodes;

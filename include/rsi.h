@@ -167,7 +167,10 @@ rsi_status_t rsi_intersect(rsi_handle_t h, const float* d_start, const float* d_
  * rsi_build, rsi_intersect, device->host copies of the mode's outputs, and a
  * final synchronize of `stream`.  Host inputs should be pinned for full copy
  * bandwidth (pageable memory works but is slower).  h_out fields are HOST
- * pointers.  Temporary device memory is stream-ordered (cudaMallocAsync).
+ * pointers.  Rays stream through the GPU in 1 Mi-segment chunks so host->device
+ * copies, traversal and device->host copies overlap.  The device workspace
+ * (BVH, mesh and chunk buffers, events) is cached per calling thread and device
+ * and reused by later calls; rsi_release_cache() frees it.
  * Errors: as rsi_build and rsi_intersect.
  */
 rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices,
@@ -175,6 +178,9 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices,
                       const float* h_start, const float* h_end, int64_t n_rays,
                       int32_t mode, const rsi_options_t* options,
                       const rsi_outputs_t* h_out, void* stream);
+
+/* Free the calling thread's cached rsi_test workspace on every device. */
+void rsi_release_cache(void);
 
 /*
  * rsi_compact_hits -- step 3a "identify intersecting rays" on the

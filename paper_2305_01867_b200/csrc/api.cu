@@ -162,6 +162,33 @@ rsi_status_t rsi_compact_hits(const int32_t* d_tri, int64_t n_rays, int32_t* d_r
     return rsi_compact_device(d_tri, n_rays, d_ray_ids, d_n_hits, (cudaStream_t)stream);
 }
 
+// Per-(thread, device) workspace of rsi_test, reused across calls: the BVH
+// handle (rebuilt in place), the mesh and ray-chunk device buffers and the
+// pipeline events.  Released by rsi_release_cache() or at thread exit.
+struct TestCtx {
+    int dev = -1;
+    rsi_handle_t h = nullptr;
+    char* buf = nullptr;
+    size_t buf_bytes = 0;
+    cudaEvent_t* ev = nullptr;
+    int64_t n_ev = 0;
+    cudaStream_t alloc_stream = nullptr;
+    void release() {
+        if (h) rsi_free(h);
+        h = nullptr;
+        if (buf) cudaFree(buf);
+        buf = nullptr;
+        buf_bytes = 0;
+        for (int64_t k = 0; k < n_ev; ++k) cudaEventDestroy(ev[k]);
+        delete[] ev;
+        ev = nullptr;
+        n_ev = 0;
+        dev = -1;
+    }
+    ~TestCtx() { release(); }
+};
+static thread_local TestCtx g_test_ctx[16];
+
 rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t* h_triangles, int64_t n_triangles,
                       const float* h_start, const float* h_end, int64_t n_rays, int32_t mode,
                       const rsi_options_t* options, const rsi_outputs_t* h_out, void* stream) {
@@ -171,42 +198,67 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
         return rsi_set_error(RSI_E_INVALID_ARG, "bad mode %d", mode);
     rsi_status_t st = check_mesh_args(h_vertices, n_vertices, h_triangles, n_triangles);
     if (st != RSI_OK) return st;
+    rsi_options_t opt;
+    st = read_options(options, &opt);
+    if (st != RSI_OK) return st;
     cudaStream_t s = (cudaStream_t)stream;
-    rsi_keep_pool_cached();
-    if (getenv("RSI_TEST_TRACE")) {  // diagnostics: is the caller's host memory page-locked?
-        cudaPointerAttributes a{};
-        cudaError_t e = cudaPointerGetAttributes(&a, h_start);
-        fprintf(stderr, "rsi_test: h_start type=%d (0 unreg, 1 host, 2 device) err=%d\n", (int)a.type, (int)e);
-        (void)cudaGetLastError();
+    int dev = 0;
+    st = rsi_cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (st != RSI_OK) return st;
+    TestCtx& ctx = g_test_ctx[dev & 15];
+    if (ctx.dev != dev) {
+        ctx.release();
+        ctx.dev = dev;
     }
-    // 1. ray pipeline resources (allocated first so the first ray chunks can
-    //    stream in while the mesh is uploaded and the BVH is built)
+    rsi_keep_pool_cached();
+
+    // workspace: [mesh V][mesh T][2 ray slots: start, end, outputs]
     int64_t kChunkRays = (int64_t)1 << 20;
     if (const char* e = getenv("RSI_TEST_CHUNK")) kChunkRays = atoll(e) > 0 ? atoll(e) : kChunkRays;  // tuning
     const int64_t nchunk = (n_rays + kChunkRays - 1) / kChunkRays;
     const int64_t crays = n_rays < kChunkRays ? n_rays : kChunkRays;
-    size_t out_b = mode == RSI_MODE_BOOLEAN ? 1 : (mode == RSI_MODE_INTERCEPT_COUNT ? 4 : 24);
+    const size_t out_b = mode == RSI_MODE_BOOLEAN ? 1 : (mode == RSI_MODE_INTERCEPT_COUNT ? 4 : 24);
     auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+    const size_t bv = (size_t)n_vertices * 3 * sizeof(float), bt = (size_t)n_triangles * 3 * sizeof(int32_t);
     const size_t slot_b = 2 * up((size_t)crays * 12) + up((size_t)crays * out_b);
-    char* slots = nullptr;
-    cudaStream_t sh = nullptr, sd = nullptr;
-    cudaEvent_t* ev = nullptr;  // per chunk: h2d done, kernel done, d2h done
-    if (nchunk > 0) {
-        st = rsi_cuda_check(cudaMallocAsync((void**)&slots, 2 * slot_b, s), "rsi_test ray buffers");
-        if (st == RSI_OK) st = side_streams(sh, sd);
-        if (st == RSI_OK) {
-            ev = new (std::nothrow) cudaEvent_t[3 * nchunk]();
-            if (!ev) st = rsi_set_error(RSI_E_OOM, "host allocation failed");
+    const size_t need = up(bv) + up(bt) + 2 * slot_b;
+    if (ctx.buf_bytes < need) {
+        if (ctx.buf) {
+            cudaStreamSynchronize(s);
+            cudaFree(ctx.buf);
+            ctx.buf = nullptr;
+            ctx.buf_bytes = 0;
         }
-        for (int64_t k = 0; st == RSI_OK && k < 3 * nchunk; ++k)
-            st = rsi_cuda_check(cudaEventCreateWithFlags(&ev[k], cudaEventDisableTiming), "event");
+        st = rsi_cuda_check(cudaMalloc((void**)&ctx.buf, need), "rsi_test workspace");
+        if (st != RSI_OK) return st;
+        ctx.buf_bytes = need;
     }
-    cudaEvent_t ready = nullptr;  // ray slots allocated on `s`
-    if (st == RSI_OK && nchunk > 0) {
-        st = rsi_cuda_check(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "event");
-        if (st == RSI_OK) st = rsi_cuda_check(cudaEventRecord(ready, s), "event");
-        if (st == RSI_OK) st = rsi_cuda_check(cudaStreamWaitEvent(sh, ready, 0), "wait");
-        if (st == RSI_OK) st = rsi_cuda_check(cudaStreamWaitEvent(sd, ready, 0), "wait");
+    if (ctx.n_ev < 3 * nchunk) {
+        for (int64_t k = 0; k < ctx.n_ev; ++k) cudaEventDestroy(ctx.ev[k]);
+        delete[] ctx.ev;
+        ctx.n_ev = 0;
+        ctx.ev = new (std::nothrow) cudaEvent_t[3 * nchunk]();
+        if (!ctx.ev) return rsi_set_error(RSI_E_OOM, "host allocation failed");
+        for (int64_t k = 0; k < 3 * nchunk; ++k) {
+            st = rsi_cuda_check(cudaEventCreateWithFlags(&ctx.ev[k], cudaEventDisableTiming), "event");
+            if (st != RSI_OK) return st;
+            ctx.n_ev = k + 1;
+        }
+    }
+    cudaEvent_t* ev = ctx.ev;  // per chunk: h2d done, kernel done, d2h done
+    float* dV = (float*)ctx.buf;
+    int32_t* dT = (int32_t*)(ctx.buf + up(bv));
+    char* slots = ctx.buf + up(bv) + up(bt);
+    cudaStream_t sh = nullptr, sd = nullptr;
+    if (nchunk > 0) {
+        st = side_streams(sh, sd);
+        if (st != RSI_OK) return st;
+        // side streams start after everything previously enqueued on `s`
+        // (the workspace's last users)
+        st = rsi_cuda_check(cudaEventRecord(ev[0], s), "event");
+        if (st == RSI_OK) st = rsi_cuda_check(cudaStreamWaitEvent(sh, ev[0], 0), "wait");
+        if (st == RSI_OK) st = rsi_cuda_check(cudaStreamWaitEvent(sd, ev[0], 0), "wait");
+        if (st != RSI_OK) return st;
     }
     auto slot = [&](int64_t c) { return slots + (c & 1) * slot_b; };
     auto h2d = [&](int64_t c) {
@@ -214,42 +266,31 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
         char* b = slot(c);
         if (c >= 2) st = rsi_cuda_check(cudaStreamWaitEvent(sh, ev[3 * (c - 2) + 1], 0), "wait");
         if (st == RSI_OK)
-            st = rsi_cuda_check(cudaMemcpyAsync(b, h_start + 3 * r0, (size_t)nr * 12, cudaMemcpyHostToDevice, sh), "H2D start");
+            st = rsi_cuda_check(cudaMemcpyAsync(b, h_start + 3 * r0, (size_t)nr * 12, cudaMemcpyHostToDevice, sh),
+                                "H2D start");
         if (st == RSI_OK)
             st = rsi_cuda_check(cudaMemcpyAsync(b + up((size_t)crays * 12), h_end + 3 * r0, (size_t)nr * 12,
                                                 cudaMemcpyHostToDevice, sh), "H2D end");
         if (st == RSI_OK) st = rsi_cuda_check(cudaEventRecord(ev[3 * c], sh), "event");
     };
-    const bool trace = getenv("RSI_TEST_TRACE") != nullptr;
-    auto now_ms = []() {
-        timespec ts;
-        clock_gettime(CLOCK_MONOTONIC, &ts);
-        return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
-    };
-    const double t0 = now_ms();
-    int64_t issued = 0;
-    // 2. mesh upload first (so it is not queued behind ray chunks on the copy
-    //    engine), then the first ray chunks on `sh`, then the build on `s`
-    //    (synchronizes once for validation) while those chunks copy
-    const size_t bv = (size_t)n_vertices * 3 * sizeof(float), bt = (size_t)n_triangles * 3 * sizeof(int32_t);
-    char* mesh = nullptr;
-    rsi_handle_t h = nullptr;
-    float* dV = nullptr;
-    int32_t* dT = nullptr;
-    if (st == RSI_OK) st = rsi_cuda_check(cudaMallocAsync((void**)&mesh, up(bv) + bt, s), "rsi_test mesh");
-    if (st == RSI_OK) {
-        dV = (float*)mesh;
-        dT = (int32_t*)(mesh + up(bv));
-        st = rsi_cuda_check(cudaMemcpyAsync(dV, h_vertices, bv, cudaMemcpyHostToDevice, s), "H2D vertices");
-        if (st == RSI_OK)
-            st = rsi_cuda_check(cudaMemcpyAsync(dT, h_triangles, bt, cudaMemcpyHostToDevice, s), "H2D triangles");
-    }
-    while (st == RSI_OK && issued < nchunk && issued < 2) h2d(issued++);
-    if (st == RSI_OK) st = rsi_build(dV, n_vertices, dT, n_triangles, options, stream, &h);
-    if (mesh) cudaFreeAsync(mesh, s);
 
-    const double t_build = now_ms();
-    // 3. chunk loop: H2D(c+1) and D2H(c-1) overlap the traversal of chunk c
+    // 1. mesh upload first (so it is not queued behind ray chunks on the copy
+    //    engine), then the first two ray chunks on `sh`, then the build on `s`
+    //    (synchronizes once for validation) while those chunks copy
+    st = rsi_cuda_check(cudaMemcpyAsync(dV, h_vertices, bv, cudaMemcpyHostToDevice, s), "H2D vertices");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaMemcpyAsync(dT, h_triangles, bt, cudaMemcpyHostToDevice, s), "H2D triangles");
+    int64_t issued = 0;
+    while (st == RSI_OK && issued < nchunk && issued < 2) h2d(issued++);
+    if (st == RSI_OK) {
+        if (ctx.h) {
+            ctx.h->opt = opt;
+            st = rsi_rebuild(ctx.h, dV, n_vertices, dT, n_triangles, stream);
+        } else {
+            st = rsi_build(dV, n_vertices, dT, n_triangles, &opt, stream, &ctx.h);
+        }
+    }
+
+    // 2. chunk loop: H2D(c+1) and D2H(c-1) overlap the traversal of chunk c
     for (int64_t c = 0; st == RSI_OK && c < nchunk; ++c) {
         while (st == RSI_OK && issued < nchunk && issued <= c + 1) h2d(issued++);
         if (st != RSI_OK) break;
@@ -268,7 +309,8 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
             d_out.point = h_out->point ? (float*)(o + 12 * (size_t)crays) : nullptr;
         }
         if (st == RSI_OK)
-            st = rsi_intersect(h, (const float*)b, (const float*)(b + up((size_t)crays * 12)), nr, mode, &d_out, stream);
+            st = rsi_intersect(ctx.h, (const float*)b, (const float*)(b + up((size_t)crays * 12)), nr, mode, &d_out,
+                               stream);
         if (st == RSI_OK) st = rsi_cuda_check(cudaEventRecord(ev[3 * c + 1], s), "event");
         if (st == RSI_OK) st = rsi_cuda_check(cudaStreamWaitEvent(sd, ev[3 * c + 1], 0), "wait");
         auto d2h = [&](void* dst, const void* src, size_t bytes) {
@@ -285,10 +327,9 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
         }
         if (st == RSI_OK) st = rsi_cuda_check(cudaEventRecord(ev[3 * c + 2], sd), "event");
     }
-    const double t_loop = now_ms();
-    // 4. drain, release (frees ordered after the last D2H), synchronize
-    rsi_status_t st2 = RSI_OK;
-    for (cudaStream_t side : {sh, sd}) {  // order the frees after all copies (also on error paths)
+
+    // 3. join the side streams into `s` (also on error paths) and synchronize
+    for (cudaStream_t side : {sh, sd}) {
         if (!side) continue;
         cudaEvent_t fin;
         if (cudaEventCreateWithFlags(&fin, cudaEventDisableTiming) == cudaSuccess) {
@@ -297,23 +338,21 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
             cudaEventDestroy(fin);
         }
     }
-    if (h) {
+    rsi_status_t st2 = rsi_cuda_check(cudaStreamSynchronize(s), "rsi_test");
+    if (st != RSI_OK) {  // a failed build leaves the cached handle empty; start fresh next time
         char saved[512];
         memcpy(saved, g_err, sizeof(saved));
-        rsi_free(h);
+        ctx.release();
         memcpy(g_err, saved, sizeof(saved));
     }
-    if (slots) cudaFreeAsync(slots, s);
-    st2 = rsi_cuda_check(cudaStreamSynchronize(s), "rsi_test");
-    if (trace)
-        fprintf(stderr, "rsi_test trace: setup+issue0 -> build done %.3f ms, loop issued %.3f ms, synced %.3f ms\n",
-                t_build - t0, t_loop - t0, now_ms() - t0);
-    if (ev)
-        for (int64_t k = 0; k < 3 * nchunk; ++k)
-            if (ev[k]) cudaEventDestroy(ev[k]);
-    delete[] ev;
-    if (ready) cudaEventDestroy(ready);
     return st != RSI_OK ? st : st2;
+}
+
+void rsi_release_cache(void) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    for (auto& c : g_test_ctx) c.release();
+    cudaSetDevice(dev);
 }
 
 rsi_status_t rsi_free(rsi_handle_t h) {

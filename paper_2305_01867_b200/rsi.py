@@ -79,6 +79,7 @@ def load():
             "rsi_test": ([_p, _i64, _p, _i64, _p, _p, _i64, _i32, _p, ctypes.POINTER(_Outputs), _p], ctypes.c_int),
             "rsi_compact_hits": ([_p, _i64, _p, _p, _p], ctypes.c_int),
             "rsi_free": ([_p], ctypes.c_int),
+            "rsi_release_cache": ([], None),
             "rsi_get_stats": ([_p, ctypes.POINTER(_Stats), _p], ctypes.c_int),
             "rsi_reset_stats": ([_p, _p], ctypes.c_int),
             "rsi_bvh_info": ([_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _p, _p], ctypes.c_int),
@@ -305,6 +306,11 @@ def rsi_reset_stats(h: Handle, stream=None):
 
 def rsi_free(h: Handle):
     h.free()
+
+
+def rsi_release_cache():
+    """Free this thread's cached rsi_test workspace."""
+    load().rsi_release_cache()
 
 
 def rsi_bvh_info(h: Handle) -> dict:

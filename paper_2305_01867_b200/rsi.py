@@ -286,7 +286,7 @@ def rsi_test(vertices, triangles, start, end, cfg: dict | None = None, options: 
     _check(lib.rsi_test(V.data_ptr(), V.shape[0], T.data_ptr(), T.shape[0], S.data_ptr(), E.data_ptr(), n,
                         MODES[mode], ctypes.byref(opt), ctypes.byref(o), _stream(stream)))
     if mode == "boolean":
-        return out["hit"].numpy().astype(bool).reshape(n, 1)
+        return out["hit"].numpy().view(np.bool_).reshape(n, 1)  # 0/1 bytes: a view, no copy
     if mode == "intercept_count":
         return out["count"].numpy()
     tri = out["tri"].numpy()

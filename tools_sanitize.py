@@ -1,0 +1,33 @@
+"""Small end-to-end run of every kernel for compute-sanitizer (memcheck / racecheck / synccheck)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import numpy as np, torch, synth
+from paper_2305_01867_b200 import rsi
+dev = "cuda:0"
+for name, nt_rays in (("fixture", None), ("cube", 3000), ("sphere", 5000)):
+    if name == "fixture":
+        V, T = synth.canopy(); S, E = synth.fixture_rays()
+    else:
+        V, T, S, E, _ = synth.workload(name, nt_rays, seed=1)
+    Vd, Td, Sd, Ed = (torch.from_numpy(a).to(dev) for a in (V, T, S, E))
+    h = rsi.rsi_build(Vd, Td)
+    for m in ("boolean", "barycentric", "intercept_count"):
+        o = rsi.rsi_intersect(h, Sd, Ed, m)
+    rsi.sparse_barycentric(rsi.rsi_intersect(h, Sd, Ed, "barycentric"))
+    rsi.rsi_bvh_download(h)
+    h.free()
+# overflow re-pass + multi-block sort path
+V = np.vstack([np.float32([[0, 0, 0.1 * k], [1, 0, 0.1 * k], [0, 1, 0.1 * k]]) for k in range(12)]).astype(np.float32)
+T = np.arange(36, dtype=np.int32).reshape(12, 3)
+S = np.float32([[0.2, 0.2, -1.0]] * 40); E = np.float32([[0.2, 0.2, 5.0]] * 40)
+h = rsi.rsi_build(torch.from_numpy(V).to(dev), torch.from_numpy(T).to(dev))
+c = rsi.rsi_intersect(h, torch.from_numpy(S).to(dev), torch.from_numpy(E).to(dev), "intercept_count")["count"].cpu()
+assert (c == 12).all(), c
+h.free()
+rng = np.random.default_rng(1)
+V = rng.uniform(0, 1, (3 * 70001, 3)).astype(np.float32); T = np.arange(3 * 70001, dtype=np.int32).reshape(-1, 3)
+h = rsi.rsi_build(torch.from_numpy(V).to(dev), torch.from_numpy(T).to(dev)); h.free()
+hv = rsi.rsi_test(*synth.workload("sphere", 3000, seed=2)[:4], {"mode": "boolean"})
+rsi.rsi_release_cache()
+torch.cuda.synchronize()
+print("sanitize run ok")

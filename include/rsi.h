@@ -66,7 +66,25 @@ typedef struct {
     uint32_t flags;       /* RSI_OPT_* bits (default 0)                                      */
     double dedup_tau;     /* intercept_count: hits whose t differ by <= tau merge (single
                              linkage on t, reading R4).  Default 1e-6 (t units).   */
+    int64_t debug_refit_leaves; /* FAULT INJECTION (tests only): > 0 runs the bottom-up refit
+                             over only the first k leaves -- case study 2's under-sized grid
+                              -- leaving half-filled / untouched nodes and no root
+                             box for rsi_validate to report.  0 (default) = all leaves.      */
 } rsi_options_t;
+
+/* BVH integrity report (rsi_validate), the invariants whose violation the
+ * paper diagnosed by dumping the tree (case study 1; case study 2,
+ * P:407-464).  All counts are 0 for a valid tree. */
+typedef struct {
+    int64_t n_internal;        /* internal nodes checked (max(N_t - 1, 1))                   */
+    int64_t half_filled;       /* internal nodes with refit arrival count 1 ("atomic: 1")   */
+    int64_t untouched;         /* internal nodes never reached by the refit ("atomic: 0")   */
+    int64_t bad_leaf_ids;      /* triangle ids missing or repeated among the leaves */
+    int64_t bad_links;         /* child -> parent -> child links that do not agree           */
+    int64_t bad_boxes;         /* child boxes not equal to the union of their children       */
+    int64_t unreachable_leaves;/* leaves whose parent chain does not reach the root          */
+    int32_t root_ok;           /* 1 when the root box was written by the refit  */
+} rsi_integrity_t;
 
 /* Opaque BVH handle: owns the packed triangles and the BVH on the device
  * where it was built.  Created by rsi_build, destroyed by rsi_free. */
@@ -195,6 +213,14 @@ rsi_status_t rsi_compact_hits(const int32_t* d_tri, int64_t n_rays, int32_t* d_r
 
 /* Release the handle and its device memory (stream-ordered on the build stream). */
 rsi_status_t rsi_free(rsi_handle_t h);
+
+/*
+ * rsi_validate -- GPU integrity check of the BVH of `h` (the
+ * checks the paper performed by hand on decoded dumps).
+ * Fills *report (host) and synchronizes `stream`.  Returns RSI_OK for a valid
+ * tree, RSI_E_INTEGRITY when any count is non-zero or the root is unset.
+ */
+rsi_status_t rsi_validate(rsi_handle_t h, rsi_integrity_t* report, void* stream);
 
 /* Read the cumulative counters of `h`; synchronizes `stream`. */
 rsi_status_t rsi_get_stats(rsi_handle_t h, rsi_stats_t* out, void* stream);

@@ -6,5 +6,5 @@ this package is its thin Python binding plus the multi-GPU driver.
 from .rsi import (  # noqa: F401
     MODES, Handle, Options, RsiError, alloc_outputs, load, rsi_build, rsi_bvh_download, rsi_bvh_info,
     rsi_compact_hits, rsi_free, rsi_get_stats, rsi_intersect, rsi_rebuild, rsi_reset_stats, rsi_test,
-    rsi_version, sparse_barycentric,
+    rsi_validate, rsi_version, sparse_barycentric,
 )

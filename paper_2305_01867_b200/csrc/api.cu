@@ -30,12 +30,14 @@ static rsi_status_t read_options(const rsi_options_t* in, rsi_options_t* out) {
     out->struct_size = sizeof(rsi_options_t);
     out->flags = 0;
     out->dedup_tau = 1e-6;
+    out->debug_refit_leaves = 0;
     if (!in || in->struct_size == 0) return RSI_OK;
     if (in->struct_size != sizeof(rsi_options_t))
         return rsi_set_error(RSI_E_INVALID_ARG, "rsi_options_t.struct_size %u != %zu", in->struct_size,
                              sizeof(rsi_options_t));
     if (in->flags & ~(RSI_OPT_FP64_MOLLER | RSI_OPT_COUNTERS)) return rsi_set_error(RSI_E_INVALID_ARG, "unknown option flags 0x%x", in->flags);
     if (!(in->dedup_tau >= 0.0)) return rsi_set_error(RSI_E_INVALID_ARG, "dedup_tau must be >= 0");
+    if (in->debug_refit_leaves < 0) return rsi_set_error(RSI_E_INVALID_ARG, "debug_refit_leaves must be >= 0");
     *out = *in;
     return RSI_OK;
 }
@@ -369,6 +371,22 @@ rsi_status_t rsi_free(rsi_handle_t h) {
     if (h->tex_nodes) cudaDestroyTextureObject(h->tex_nodes);
     delete h;
     return st;
+}
+
+rsi_status_t rsi_validate(rsi_handle_t h, rsi_integrity_t* report, void* stream) {
+    if (!h || !report) return rsi_set_error(RSI_E_INVALID_ARG, "null argument");
+    if (h->n_tri <= 0) return rsi_set_error(RSI_E_INVALID_ARG, "handle holds no mesh");
+    rsi_status_t st = rsi_validate_device(h, report, (cudaStream_t)stream);
+    if (st != RSI_OK) return st;
+    if (report->half_filled || report->untouched || report->bad_leaf_ids || report->bad_links || report->bad_boxes ||
+        report->unreachable_leaves || !report->root_ok)
+        return rsi_set_error(RSI_E_INTEGRITY,
+                             "BVH integrity: half_filled=%lld untouched=%lld bad_leaf_ids=%lld bad_links=%lld "
+                             "bad_boxes=%lld unreachable_leaves=%lld root_ok=%d",
+                             (long long)report->half_filled, (long long)report->untouched,
+                             (long long)report->bad_leaf_ids, (long long)report->bad_links,
+                             (long long)report->bad_boxes, (long long)report->unreachable_leaves, report->root_ok);
+    return RSI_OK;
 }
 
 rsi_status_t rsi_get_stats(rsi_handle_t h, rsi_stats_t* out, void* stream) {

@@ -24,7 +24,10 @@ __global__ void k_build_init(uint32_t* scratch) {
         scratch[SCR_EXT_MIN + i] = 0xffffffffu;
         scratch[SCR_EXT_MAX + i] = 0u;
     }
-    if (i == 0) scratch[SCR_STATUS] = 0u;
+    if (i == 0) {
+        scratch[SCR_STATUS] = 0u;
+        scratch[SCR_ROOT_SET] = 0u;
+    }
 }
 
 __device__ __forceinline__ float warp_min(float v) {
@@ -418,11 +421,11 @@ __device__ __forceinline__ void write_slot(float4* nodes, int node, int side, co
 // the second (which sees the sibling's box) merges and continues.
 __global__ void __launch_bounds__(kBlock) k_refit(const float* __restrict__ V, int64_t nv,
                                                   const int32_t* __restrict__ T, const int32_t* __restrict__ vals,
-                                                  int n, float4* nodes, float4* __restrict__ tris,
+                                                  int n_leaves, int n, float4* nodes, float4* __restrict__ tris,
                                                   const int32_t* __restrict__ parent, uint32_t* arrivals,
                                                   uint32_t* scratch) {
     int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n) return;
+    if (k >= n_leaves) return;
     const int n_nodes = n > 1 ? n - 1 : 1;
     const int32_t id = vals[k];
     const int32_t ia = safe_index(T[3 * id], nv), ib = safe_index(T[3 * id + 1], nv),
@@ -467,6 +470,7 @@ __global__ void __launch_bounds__(kBlock) k_refit(const float* __restrict__ V, i
         root[x] = lo[x];
         root[3 + x] = hi[x];
     }
+    scratch[SCR_ROOT_SET] = 1u;
 }
 
 // Whole sort in one CTA with keys and values resident in shared memory
@@ -716,6 +720,78 @@ __global__ void __launch_bounds__(kBlock) k_quads(const float4* __restrict__ nod
     q[3] = make_uint4(w[12], w[13], w[14], w[15]);
 }
 
+// ------------------------------------------------------------------ NEXT-2: integrity validator
+// One thread per internal node: arrival count, parent links of both children,
+// and exact box union of each internal child.  One thread per leaf: triangle-id
+// histogram and a parent walk to the root (<= 64 steps: depth <= 62).
+enum { V_HALF = 0, V_UNTOUCHED, V_LEAFIDS, V_LINKS, V_BOXES, V_UNREACH, V_WORDS };
+
+__device__ __forceinline__ void node_box(const float4* nodes, int node, int side, float lo[3], float hi[3]) {
+    const float* f = reinterpret_cast<const float*>(nodes + 4 * node);
+    const int o = side ? 4 : 0;
+    lo[0] = f[o + 0];
+    hi[0] = f[o + 1];
+    lo[1] = f[o + 2];
+    hi[1] = f[o + 3];
+    lo[2] = f[8 + 2 * side];
+    hi[2] = f[9 + 2 * side];
+}
+
+__global__ void __launch_bounds__(kBlock) k_validate_nodes(const float4* __restrict__ nodes, int n, int n_nodes,
+                                                           const int32_t* __restrict__ parent,
+                                                           const uint32_t* __restrict__ arrivals,
+                                                           unsigned long long* __restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_nodes || n == 1) return;
+    const uint32_t a = arrivals[i];
+    if (a == 1u) atomicAdd(out + V_HALF, 1ull);
+    if (a == 0u) atomicAdd(out + V_UNTOUCHED, 1ull);
+    const int4 r = *reinterpret_cast<const int4*>(nodes + 4 * i + 3);
+    const int ch[2] = {r.x, r.y};
+    for (int side = 0; side < 2; ++side) {
+        const int c = ch[side];
+        const int64_t pi = c >= 0 ? c : (int64_t)n_nodes + ~c;
+        if ((c >= 0 && c >= n_nodes) || (c < 0 && ~c >= n) || parent[pi] != ((i << 1) | side)) {
+            atomicAdd(out + V_LINKS, 1ull);
+            continue;
+        }
+        if (c >= 0) {  // the slot box of an internal child = union of that child's two slots
+            float lo[3], hi[3], l0[3], h0[3], l1[3], h1[3];
+            node_box(nodes, i, side, lo, hi);
+            node_box(nodes, c, 0, l0, h0);
+            node_box(nodes, c, 1, l1, h1);
+            bool ok = true;
+            for (int x = 0; x < 3; ++x)
+                ok = ok && lo[x] == fminf(l0[x], l1[x]) && hi[x] == fmaxf(h0[x], h1[x]);
+            if (!ok) atomicAdd(out + V_BOXES, 1ull);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) k_validate_leaves(const float4* __restrict__ tris, int n, int n_nodes,
+                                                            const int32_t* __restrict__ parent,
+                                                            uint32_t* __restrict__ seen,
+                                                            unsigned long long* __restrict__ out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    const int id = __float_as_int(tris[4 * k].w);
+    if (id < 0 || id >= n) atomicAdd(out + V_LEAFIDS, 1ull);
+    else atomicAdd(seen + id, 1u);
+    int p = parent[n_nodes + k];
+    int steps = 0;
+    while (p >= 0 && (p >> 1) != 0 && steps < 64) {
+        p = parent[p >> 1];
+        ++steps;
+    }
+    if (p < 0 || (p >> 1) != 0) atomicAdd(out + V_UNREACH, 1ull);
+}
+
+__global__ void __launch_bounds__(kBlock) k_validate_ids(const uint32_t* __restrict__ seen, int n,
+                                                         unsigned long long* __restrict__ out) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < n && seen[j] != 1u) atomicAdd(out + V_LEAFIDS, 1ull);
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ host side
@@ -798,8 +874,12 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
                                                          n_nodes);
     launch_sort(h, n, s);
     k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent, h->arrivals);
-    k_refit<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, h->vals, n, h->nodes, h->tris, h->parent,
-                                                        h->arrivals, h->scratch);
+    // the refit grid covers every leaf (case study 2: never size it from another
+    // count) -- except under the test-only fault injection option
+    const int refit_leaves = (h->opt.debug_refit_leaves > 0 && h->opt.debug_refit_leaves < n)
+                                 ? (int)h->opt.debug_refit_leaves : n;
+    k_refit<<<rsi_ceil_div(refit_leaves, kBlock), kBlock, 0, s>>>(V, nv, T, h->vals, refit_leaves, n, h->nodes,
+                                                                   h->tris, h->parent, h->arrivals, h->scratch);
     if (kTopNodes > 0) k_topk<<<1, 1024, 0, s>>>(h->nodes, n_nodes, h->top, h->scratch);
     if (rsi_uses_quads()) k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads, h->scratch);
     st = rsi_cuda_check(cudaGetLastError(), "build kernel launch");
@@ -845,5 +925,40 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
     h->n_tri = nt;
     h->n_nodes = n_nodes;
     h->stream = s;
+    return RSI_OK;
+}
+
+rsi_status_t rsi_validate_device(rsi_bvh* h, rsi_integrity_t* report, cudaStream_t s) {
+    const int n = (int)h->n_tri, n_nodes = (int)h->n_nodes;
+    unsigned long long* out = nullptr;
+    uint32_t* seen = nullptr;
+    rsi_status_t st = rsi_cuda_check(cudaMallocAsync((void**)&out, V_WORDS * sizeof(unsigned long long), s), "validate");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaMallocAsync((void**)&seen, (size_t)n * sizeof(uint32_t), s), "validate");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaMemsetAsync(out, 0, V_WORDS * sizeof(unsigned long long), s), "memset");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaMemsetAsync(seen, 0, (size_t)n * sizeof(uint32_t), s), "memset");
+    if (st == RSI_OK) {
+        k_validate_nodes<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n, n_nodes, h->parent, h->arrivals,
+                                                                         out);
+        k_validate_leaves<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(h->tris, n, n_nodes, h->parent, seen, out);
+        k_validate_ids<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(seen, n, out);
+        st = rsi_cuda_check(cudaGetLastError(), "validate launch");
+    }
+    unsigned long long v[V_WORDS] = {0};
+    uint32_t root_set = 0;
+    if (st == RSI_OK) st = rsi_cuda_check(cudaMemcpyAsync(v, out, sizeof(v), cudaMemcpyDeviceToHost, s), "validate");
+    if (st == RSI_OK)
+        st = rsi_cuda_check(cudaMemcpyAsync(&root_set, h->scratch + SCR_ROOT_SET, 4, cudaMemcpyDeviceToHost, s), "validate");
+    if (out) cudaFreeAsync(out, s);
+    if (seen) cudaFreeAsync(seen, s);
+    if (st == RSI_OK) st = rsi_cuda_check(cudaStreamSynchronize(s), "validate");
+    if (st != RSI_OK) return st;
+    report->n_internal = n_nodes;
+    report->half_filled = (int64_t)v[V_HALF];
+    report->untouched = (int64_t)v[V_UNTOUCHED];
+    report->bad_leaf_ids = (int64_t)v[V_LEAFIDS];
+    report->bad_links = (int64_t)v[V_LINKS];
+    report->bad_boxes = (int64_t)v[V_BOXES];
+    report->unreachable_leaves = (int64_t)v[V_UNREACH];
+    report->root_ok = root_set ? 1 : 0;
     return RSI_OK;
 }

@@ -33,6 +33,7 @@ enum {
     SCR_OVF_TOTAL = 17, // re-pass: total raw hits over overflowed rays
     SCR_DISPENSER = 18, // 2 words: 64-bit ray dispenser of the persistent traversal grid
     SCR_NTOP = 20,      // nodes in the top-of-tree shared-memory image
+    SCR_ROOT_SET = 21,  // 1 once the refit wrote the root box
     SCR_WORDS = 32
 };
 enum { STATUS_INDEX = 1u, STATUS_NONFINITE = 2u, STATUS_RANGE = 4u };
@@ -90,7 +91,8 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* d_vertices, int64_t n_ver
 rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* d_start, const float* d_end,
                                   int64_t n_rays, int32_t mode, const rsi_outputs_t* out,
                                   cudaStream_t stream);
-bool rsi_uses_quads();  // traverse.cu: does any mode walk the 4-wide records
+bool rsi_uses_quads();
+rsi_status_t rsi_validate_device(rsi_bvh* h, rsi_integrity_t* report, cudaStream_t stream);  // build.cu  // traverse.cu: does any mode walk the 4-wide records
 rsi_status_t rsi_compact_device(const int32_t* d_tri, int64_t n_rays, int32_t* d_ids,
                                 int32_t* d_n, cudaStream_t stream);
 

@@ -42,7 +42,13 @@ class RsiError(RuntimeError):
 
 
 class _Options(ctypes.Structure):
-    _fields_ = [("struct_size", ctypes.c_uint32), ("flags", ctypes.c_uint32), ("dedup_tau", ctypes.c_double)]
+    _fields_ = [("struct_size", ctypes.c_uint32), ("flags", ctypes.c_uint32), ("dedup_tau", ctypes.c_double),
+                ("debug_refit_leaves", ctypes.c_int64)]
+
+
+class _Integrity(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in ("n_internal", "half_filled", "untouched", "bad_leaf_ids", "bad_links",
+                                              "bad_boxes", "unreachable_leaves")] + [("root_ok", ctypes.c_int32)]
 
 
 class _Outputs(ctypes.Structure):
@@ -84,6 +90,7 @@ def load():
             "rsi_reset_stats": ([_p, _p], ctypes.c_int),
             "rsi_bvh_info": ([_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _p, _p], ctypes.c_int),
             "rsi_bvh_download": ([_p, _p, _p, _p, _p, _p, _p, _p], ctypes.c_int),
+            "rsi_validate": ([_p, ctypes.POINTER(_Integrity), _p], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(lib, name)
@@ -127,10 +134,11 @@ class Options:
     fp64_moller: bool = False   # P:501 USE_DOUBLE_PRECISION_MOLLER
     dedup_tau: float = 1e-6     # reading R4
     counters: bool = False      # instrumented kernels: box / MT test counts in rsi_get_stats
+    debug_refit_leaves: int = 0  # FAULT INJECTION (tests): refit only the first k leaves
 
     def _c(self) -> _Options:
         flags = (OPT_FP64_MOLLER if self.fp64_moller else 0) | (OPT_COUNTERS if self.counters else 0)
-        return _Options(ctypes.sizeof(_Options), flags, float(self.dedup_tau))
+        return _Options(ctypes.sizeof(_Options), flags, float(self.dedup_tau), int(self.debug_refit_leaves))
 
 
 class Handle:
@@ -336,4 +344,16 @@ def rsi_bvh_download(h: Handle, stream=None) -> dict:
     ptrs = [d[k].ctypes.data_as(_p) for k in ("child", "box", "leaf_tri", "morton", "parent", "arrivals")]
     _check(load().rsi_bvh_download(h.ptr, *ptrs, _stream(stream)))
     d.update(info)
+    return d
+
+
+def rsi_validate(h: Handle, stream=None) -> dict:
+    """GPU integrity check.  Returns the report dict with
+    "ok" = True for a valid tree (RSI_E_INTEGRITY is reported, not raised)."""
+    rep = _Integrity()
+    rc = load().rsi_validate(h.ptr, ctypes.byref(rep), _stream(stream))
+    if rc not in (0, 7):
+        _check(rc)
+    d = {n: int(getattr(rep, n)) for n, _ in _Integrity._fields_}
+    d["ok"] = rc == 0
     return d

@@ -396,3 +396,57 @@ def test_million_triangle_mesh_sampled(rsi):
     ref = oracle.run(V, T, S[sample], E[sample], flags=False)
     got = {"hit": hit[sample], "count": cnt[sample], **{k: v[sample] for k, v in bar.items()}}
     assert_parity(got, ref, S[sample], E[sample], "1m-sample")
+
+
+# ------------------------------------------------------------------ NEXT-2: validator, dump, fault injection
+
+def test_validator_accepts_built_trees(rsi):
+    for nt in (1, 2, 5, 1000, 29260, 70001):
+        rng = np.random.default_rng(nt)
+        V = rng.uniform(-1, 1, (3 * nt, 3)).astype(np.float32)
+        T = np.arange(3 * nt, dtype=np.int32).reshape(nt, 3)
+        Vd, Td = to_dev(V, T)
+        h = rsi.rsi_build(Vd, Td)
+        rep = rsi.rsi_validate(h)
+        h.free()
+        assert rep["ok"], (nt, rep)
+
+
+def test_case_study_2_failure_signatures(rsi):
+    """the construct kernel launched with grid_lambda = 16 blocks of
+    1024 threads instead of grid_dimsT = 29 covered only 16 384 of the 29 260
+    leaves of a ~30k-triangle terrain.  Injecting the same under-sized refit
+    grid reproduces the signatures the paper read off the dump: half-filled
+    nodes ("atomic: 1"), untouched nodes ("atomic: 0") and no root box."""
+    V, T = synth.paper_terrain()
+    assert len(T) == 29260
+    Vd, Td = to_dev(V, T)
+    h = rsi.rsi_build(Vd, Td, rsi.Options(debug_refit_leaves=16 * 1024))
+    rep = rsi.rsi_validate(h)
+    assert not rep["ok"]
+    assert rep["half_filled"] > 0 and rep["untouched"] > 0 and rep["root_ok"] == 0
+    d = rsi.rsi_bvh_download(h)
+    h.free()
+    assert (d["arrivals"] == 1).sum() == rep["half_filled"]
+    assert (d["arrivals"] == 0).sum() == rep["untouched"]
+    from paper_2305_01867_b200 import diagnostics
+    assert "atomic: 1," in diagnostics.dump_text(d) and "atomic: 0," in diagnostics.dump_text(d)
+    # the correct grid gives a valid tree
+    h = rsi.rsi_build(Vd, Td)
+    assert rsi.rsi_validate(h)["ok"]
+    h.free()
+
+
+def test_fixture_dump_and_dot_from_device(rsi):
+    from paper_2305_01867_b200 import diagnostics
+    V, T = synth.fixture()
+    Vd, Td = to_dev(V, T)
+    h = rsi.rsi_build(Vd, Td)
+    d = rsi.rsi_bvh_download(h)
+    h.free()
+    txt = diagnostics.dump_text(d)
+    assert "[0] x:[12,13], y:[2,3], z:[1,1.3]  ------ ROOT NODE" in txt
+    assert "atomic: 2, rangeL: 0, rangeR: 3" in txt
+    dot = diagnostics.to_dot(d)
+    for lab in ("[0,3]", "[0,1]", "[2,3]", "[0] 0", "[1] 3", "[2] 1", "[3] 2"):
+        assert f'label="{lab}"' in dot

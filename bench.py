@@ -66,6 +66,7 @@ def parse():
     ap.add_argument("--workload", default="sphere", choices=["sphere", "terrain", "paper_terrain", "sphere1m"])
     ap.add_argument("--mode", default="boolean", choices=["boolean", "barycentric", "intercept_count"])
     ap.add_argument("--no-extra-modes", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the other BASELINE configs (rank 0, N=1 only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample rays (0 = auto ~15 s)")
@@ -289,6 +290,38 @@ def main():
             extra[m] = {"value": n * world * args.steps / (mms * 1e-3), "ms_per_step": mms / args.steps,
                         "build_ms": mb, "query_ms": mq}
     stats = rsi.rsi_get_stats(h)
+
+    # the other BASELINE.json configs (parity-test workloads), timed on this GPU
+    # for context: rays/s of rebuild + intersect per step, 3 warm-up + 3 timed steps
+    other = {}
+    if world == 1 and not args.no_configs:
+        def one_config(name, mode, n_rays):
+            V2, T2, S2, E2 = workload_inputs(name, n_rays, 0)
+            V2d, T2d = torch.from_numpy(V2).to(dev), torch.from_numpy(T2).to(dev)
+            S2d, E2d = torch.from_numpy(S2).to(dev), torch.from_numpy(E2).to(dev)
+            o2 = rsi.alloc_outputs(n_rays, mode, dev)
+            with rsi.rsi_build(V2d, T2d) as h2:
+                for _ in range(3):
+                    rsi.rsi_rebuild(h2, V2d, T2d)
+                    rsi.rsi_intersect(h2, S2d, E2d, mode, out=o2)
+                torch.cuda.synchronize(dev)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                for _ in range(3):
+                    rsi.rsi_rebuild(h2, V2d, T2d)
+                    rsi.rsi_intersect(h2, S2d, E2d, mode, out=o2)
+                b.record(stream)
+                torch.cuda.synchronize(dev)
+                ms3 = a.elapsed_time(b) / 3
+            return {"workload": f"{name} N_t={len(T2)}, N_r={n_rays}, {mode}", "value": n_rays / (ms3 * 1e-3),
+                    "unit": UNIT, "ms_per_step": ms3}
+        other["configs[0] cube all modes"] = [one_config("cube", m, 10_000)
+                                              for m in ("boolean", "barycentric", "intercept_count")]
+        other["configs[1] sphere 1e6 boolean"] = one_config("sphere", "boolean", 1_000_000)
+        other["configs[3] folded terrain 1e7 intercept_count"] = one_config("terrain", "intercept_count", 10_000_000)
+        other["paper-shaped terrain (P:148) 1e7 boolean"] = one_config("paper_terrain", "boolean", 10_000_000)
+        other["configs[4] per-GPU share: sphere N_t=1e6, 1.25e7 boolean"] = one_config("sphere1m", "boolean",
+                                                                                      12_500_000)
     # measured algorithmic work per ray (instrumented launch, outside the timed region)
     work = None
     with rsi.rsi_build(Vd, Td, rsi.Options(counters=True)) as hc:
@@ -341,7 +374,7 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": args.steps * (kernels_per_build + 1),
             "gpu_launches_note": f"per step: {kernels_per_build} build kernels + 1 traversal kernel",
-            "clocks": clk, "modes": extra, "stats": stats,
+            "clocks": clk, "modes": extra, "configs_other": other, "stats": stats,
         }
         print(json.dumps(line), flush=True)
     h.free()

@@ -121,7 +121,7 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ helpers
 def workload_inputs(name: str, n: int, rank: int):
-    seed = {"sphere": 3, "terrain": 4, "paper_terrain": 6, "sphere1m": 5}[name] + 1000 * rank
+    seed = {"cube": 1, "sphere": 3, "terrain": 4, "paper_terrain": 6, "sphere1m": 5}[name] + 1000 * rank
     V, T, S, E, _ = synth.workload(name, n, seed=seed)
     return V, T, S, E
 

@@ -100,9 +100,13 @@ __device__ __forceinline__ uint32_t expand10(uint32_t x) {
     return x;
 }
 
-__device__ __forceinline__ uint32_t quantize10(float c, float lo, float hi) {
-    float w = hi - lo;
-    if (!(w > 0.0f)) return 0u;  // zero-width axis -> 0 (reading R8)
+// Per-axis quantization (reading R8) with each axis's extent floored at 1/64
+// of the largest extent (wmax / 64 is exact): compact meshes keep the paper's
+// per-axis codes (the Fig. 3 tree), while a flat terrain's thin
+// axis no longer takes the top Morton bits and splits the map by height.
+__device__ __forceinline__ uint32_t quantize10(float c, float lo, float hi, float wmax) {
+    float w = fmaxf(hi - lo, wmax * 0.015625f);
+    if (!(w > 0.0f)) return 0u;  // zero-extent mesh -> 0
     float q = floorf((c - lo) / w * 1024.0f);
     q = fminf(fmaxf(q, 0.0f), 1023.0f);  // NaN -> 0 via fmaxf
     return (uint32_t)q;
@@ -129,11 +133,12 @@ __global__ void __launch_bounds__(kBlock) k_morton(const float* __restrict__ V, 
         hi[k] = rsi_ord2f(scratch[SCR_EXT_MAX + k]);
     }
     int32_t a = safe_index(T[3 * j], nv), b = safe_index(T[3 * j + 1], nv), c = safe_index(T[3 * j + 2], nv);
+    const float wmax = fmaxf(hi[0] - lo[0], fmaxf(hi[1] - lo[1], hi[2] - lo[2]));
     uint32_t q[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
         float cen = (V[3 * a + k] + V[3 * b + k] + V[3 * c + k]) / 3.0f;
-        q[k] = quantize10(cen, lo[k], hi[k]);
+        q[k] = quantize10(cen, lo[k], hi[k], wmax);
     }
     keys[j] = expand10(q[0]) | (expand10(q[1]) << 1) | (expand10(q[2]) << 2);
     vals[j] = j;

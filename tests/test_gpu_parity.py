@@ -266,14 +266,18 @@ def test_build_errors(rsi):
     h.free()
 
 
-@pytest.mark.parametrize("nt", [1, 2, 3, 17, 1000, 70_001])
+@pytest.mark.parametrize("nt", [1, 2, 3, 17, 1000, 70_001, -5000])
 def test_bvh_integrity_random_meshes(rsi, nt):
     """Validator invariants (P:407-464 failure signatures must be absent):
     leaf bijection, arrivals == 2, root reachable from every leaf, child boxes
     exact unions, parent/child links mutual; sorted Morton codes equal a
     bit-loop z-major encoding of the fp32 centroids."""
+    flat = nt < 0  # a flat (terrain-like) mesh: z extent 1/1000 of x, y
+    nt = abs(nt)
     rng = np.random.default_rng(nt)
     V = rng.uniform(-3, 7, (3 * nt, 3)).astype(np.float32)
+    if flat:
+        V[:, 2] *= np.float32(1e-3)
     T = rng.permutation(3 * nt).reshape(nt, 3).astype(np.int32)
     Vd, Td = to_dev(V, T)
     h = rsi.rsi_build(Vd, Td)
@@ -285,7 +289,8 @@ def test_bvh_integrity_random_meshes(rsi, nt):
     # morton reference (bit loop) on fp32 centroids
     lo, hi = V.min(0), V.max(0)
     c = (V[T[:, 0]] + V[T[:, 1]] + V[T[:, 2]]) / np.float32(3)
-    q = np.clip(np.floor((c - lo) / (hi - lo) * np.float32(1024)), 0, 1023).astype(np.uint32)
+    w = np.maximum(hi - lo, (hi - lo).max() * np.float32(1 / 64))   # reading R8: extent floor
+    q = np.clip(np.floor((c - lo) / w * np.float32(1024)), 0, 1023).astype(np.uint32)
     code = np.zeros(nt, np.uint32)
     for b in range(10):
         for a in range(3):

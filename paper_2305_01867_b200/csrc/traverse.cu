@@ -362,6 +362,7 @@ struct TraceParams {
     unsigned long long* stats;
     unsigned long long* counter;  // persistent-grid ray dispenser
     int min_trav;           // leave the traversal phase when fewer lanes still search
+    uint32_t magic;         // 0x4B000000
 };
 
 template <int MODE>
@@ -628,6 +629,19 @@ struct LaneStack {
     }
 };
 
+// 2^23 + byte j of w, as a float (exact): one PRMT with an immediate selector;
+// `magic` holds 0x4B000000 in a register (kept loop-invariant by the caller)
+__device__ __forceinline__ float byte_to_2p23(uint32_t w, int j, uint32_t magic) {
+    uint32_t r;
+    switch (j) {
+        case 0: asm("prmt.b32 %0, %1, %2, 0x7440;" : "=r"(r) : "r"(w), "r"(magic)); break;
+        case 1: asm("prmt.b32 %0, %1, %2, 0x7441;" : "=r"(r) : "r"(w), "r"(magic)); break;
+        case 2: asm("prmt.b32 %0, %1, %2, 0x7442;" : "=r"(r) : "r"(w), "r"(magic)); break;
+        default: asm("prmt.b32 %0, %1, %2, 0x7443;" : "=r"(r) : "r"(w), "r"(magic)); break;
+    }
+    return __uint_as_float(r);
+}
+
 // compare-and-swap of (key, ref) pairs: ascending keys
 __device__ __forceinline__ void cas(float& ka, int& ca, float& kb, int& cb) {
     const bool sw = kb < ka;
@@ -677,6 +691,9 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
         ms.kk = s_k + threadIdx.x;
     }
     const int root = p.n_top > 0 ? (int)kSmemRef : 0;
+    // 0x4B000000 (float 2^23) from a kernel parameter: an opaque register, so the
+    // quad decode's PRMTs keep their byte selectors as immediates
+    const uint32_t magic = p.magic;
     while (true) {
         // ---- 1. refill
         unsigned want = __ballot_sync(FULL, ray < 0);
@@ -760,11 +777,10 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                                           __float_as_int(qd.y));
                 // child j plane: (2^23 + q) * s + (p - 2^23 s) = p + q s, rounded outward
                 auto dec_lo = [&](int a, int j) {
-                    return __fmaf_rd(__uint_as_float(__byte_perm(wq[2 * a], 0x4B000000u, 0x7440u + j)), sc[a], plo[a]);
+                    return __fmaf_rd(byte_to_2p23(wq[2 * a], j, magic), sc[a], plo[a]);
                 };
                 auto dec_hi = [&](int a, int j) {
-                    return __fmaf_ru(__uint_as_float(__byte_perm(wq[2 * a + 1], 0x4B000000u, 0x7440u + j)), sc[a],
-                                     phi[a]);
+                    return __fmaf_ru(byte_to_2p23(wq[2 * a + 1], j, magic), sc[a], phi[a]);
                 };
                 float k0, k1, k2, k3;
                 const bool h0 = ((vmask & 1u) != 0u) & slab(r, dec_lo(0, 0), dec_hi(0, 0), dec_lo(1, 0), dec_hi(1, 0),
@@ -1190,6 +1206,7 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     p.point = out->point;
     p.count = out->count;
     p.tau = h->opt.dedup_tau;
+    p.magic = 0x4B000000u;
     p.ovf_list = h->ovf_list;
     p.scratch = h->scratch;
     p.stats = h->stats;

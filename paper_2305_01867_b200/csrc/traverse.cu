@@ -658,7 +658,8 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
-    constexpr bool kSort = (MODE == MODE_BARY) || RSI_SORT_ALL;
+    // near-first child order: needed for nearest-hit culling, helps any-hit exit; useless for counts
+    constexpr bool kSort = (MODE == MODE_BARY) || (MODE == MODE_BOOL && RSI_SORT_ALL);
     constexpr bool kQuad = MODE == MODE_BOOL ? RSI_BOOL_QUAD : (MODE == MODE_BARY ? RSI_BARY_QUAD : RSI_COUNT_QUAD);
     constexpr int kSmemStack = MODE == MODE_BOOL ? RSI_BOOL_SMEM : (MODE == MODE_BARY ? RSI_BARY_SMEM : RSI_COUNT_SMEM);
     constexpr int kStack = kQuad ? kStackQuad : kStackBinary;

@@ -26,17 +26,18 @@ constexpr float kSlack = 4.76837158203125e-07f;  // 2^-21: slab-test slack facto
 constexpr float kTiny = 1e-30f;                  // absolute floor (underflow)
 constexpr float kOutTol = 4e-6f;                 // max certified |t error| for fp32 outputs
 // Per-mode traversal configuration.  Measured on B200 (round 1): all modes
-// walk the binary child-pair nodes with speculative traversal and a
-// local-memory stack; the compressed 4-wide records (RSI_*_QUAD) and
-// shared-memory stacks (RSI_*_SMEM) were slower and stay as build options.
+// walk the compressed 4-wide grandchild records (64 B, 8-bit quantized boxes:
+// half the L1 wavefronts of the binary child-pair walk, which was L1-data-pipe
+// bound at 87 %) with a local-memory stack.  The binary walk (RSI_*_QUAD=0,
+// with speculative traversal) and shared-memory stacks stay as build options.
 #ifndef RSI_BOOL_QUAD
-#define RSI_BOOL_QUAD 0
+#define RSI_BOOL_QUAD 1
 #endif
 #ifndef RSI_BARY_QUAD
-#define RSI_BARY_QUAD 0
+#define RSI_BARY_QUAD 1
 #endif
 #ifndef RSI_COUNT_QUAD
-#define RSI_COUNT_QUAD 0
+#define RSI_COUNT_QUAD 1
 #endif
 #ifndef RSI_BOOL_SMEM
 #define RSI_BOOL_SMEM 0

@@ -25,11 +25,12 @@ constexpr float kTerr = 12.0f * kU;              // t forward-error constant
 constexpr float kSlack = 4.76837158203125e-07f;  // 2^-21: slab-test slack factor
 constexpr float kTiny = 1e-30f;                  // absolute floor (underflow)
 constexpr float kOutTol = 4e-6f;                 // max certified |t error| for fp32 outputs
-// Per-mode traversal configuration.  Measured on B200 (round 1): all modes
-// walk the compressed 4-wide grandchild records (64 B, 8-bit quantized boxes:
-// half the L1 wavefronts of the binary child-pair walk, which was L1-data-pipe
-// bound at 87 %) with a local-memory stack.  The binary walk (RSI_*_QUAD=0,
-// with speculative traversal) and shared-memory stacks stay as build options.
+// Per-mode traversal configuration.  Measured on B200 (round 1, same box A/B):
+// boolean and barycentric walk the compressed 4-wide grandchild records (64 B,
+// 8-bit quantized boxes: half the L1 wavefronts of the binary child-pair walk,
+// which was L1-data-pipe bound at 87 %); intercept_count walks the binary
+// child-pair nodes with speculative traversal (7 % faster on the sphere, equal
+// on the folded terrain).  Shared-memory stacks stay a build option.
 #ifndef RSI_BOOL_QUAD
 #define RSI_BOOL_QUAD 1
 #endif
@@ -37,7 +38,7 @@ constexpr float kOutTol = 4e-6f;                 // max certified |t error| for 
 #define RSI_BARY_QUAD 1
 #endif
 #ifndef RSI_COUNT_QUAD
-#define RSI_COUNT_QUAD 1
+#define RSI_COUNT_QUAD 0
 #endif
 #ifndef RSI_BOOL_SMEM
 #define RSI_BOOL_SMEM 0

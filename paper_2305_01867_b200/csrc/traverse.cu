@@ -122,6 +122,9 @@ __device__ __forceinline__ float ld_stream(const float* p) {
 
 // Returns false for rays that cannot hit: zero length or a non-finite coordinate
 // (reading R12).  `nonfinite` is set for the latter.
+// kNearFar: lx/hx become the offsets of each axis's NEAR / FAR plane (lo / hi
+// for inv >= 0, hi / lo for inv < 0) for the octant-selected quad slab test.
+template <bool kNearFar = false>
 __device__ __forceinline__ bool load_ray(Ray& r, const float* __restrict__ S, const float* __restrict__ E,
                                          int64_t i, bool& nonfinite) {
     // the segment stream is read once: do not let it displace tree nodes in L1
@@ -139,6 +142,11 @@ __device__ __forceinline__ bool load_ray(Ray& r, const float* __restrict__ S, co
     slab_axis(r.ox, r.dx, r.ix, r.lx, r.hx);
     slab_axis(r.oy, r.dy, r.iy, r.ly, r.hy);
     slab_axis(r.oz, r.dz, r.iz, r.lz, r.hz);
+    if (kNearFar) {
+        if (r.ix < 0.0f) { const float t = r.lx; r.lx = r.hx; r.hx = t; }
+        if (r.iy < 0.0f) { const float t = r.ly; r.ly = r.hy; r.hy = t; }
+        if (r.iz < 0.0f) { const float t = r.lz; r.lz = r.hz; r.hz = t; }
+    }
     return !nonfinite && !(r.dx == 0.0f && r.dy == 0.0f && r.dz == 0.0f);
 }
 
@@ -726,7 +734,7 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
         }
         if (fresh) {
             bool nonfinite;
-            const bool ok = load_ray(r, p.S, p.E, ray, nonfinite);
+            const bool ok = load_ray<kQuad>(r, p.S, p.E, ray, nonfinite);
             if (nonfinite) st.add(ST_NONFINITE);
             ms.init();
             tclip = 1.0f;
@@ -762,38 +770,41 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                 ldg256(q + 2, qc, qd);
                 const uint32_t w3 = __float_as_uint(qa.w);
                 const uint32_t vmask = w3 >> 24;
-                // per axis: grid step s = 2^e, s*2^23, and the decode offsets p - 2^23 s
-                // (exact when the record's |p/s| < 2^23; rounded outward otherwise)
-                float sc[3], plo[3], phi[3];
+                // Per axis: grid step s = 2^e and the decode offset p - 2^23 s (both
+                // exact: the build keeps |p/s| < 2^23), so a child plane
+                // (2^23 + q) * s + (p - 2^23 s) = p + q s is exact under any rounding.
+                // The ray octant picks which byte array holds the near planes (lo for
+                // inv >= 0), so each child needs no per-axis min/max.
+                float sc[3], pm[3];
+                uint32_t wn[3], wf[3];
                 const float pp[3] = {qa.x, qa.y, qa.z};
+                const uint32_t wq[6] = {__float_as_uint(qb.x), __float_as_uint(qb.y), __float_as_uint(qb.z),
+                                        __float_as_uint(qb.w), __float_as_uint(qc.x), __float_as_uint(qc.y)};
+                const float inv3[3] = {r.ix, r.iy, r.iz};
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
                     const uint32_t eb = (w3 >> (8 * a)) & 255u;
                     sc[a] = __uint_as_float((eb - 1u) << 23);
-                    const float s23 = __uint_as_float((eb + 22u) << 23);
-                    plo[a] = __fsub_rd(pp[a], s23);
-                    phi[a] = __fsub_ru(pp[a], s23);
+                    pm[a] = pp[a] - __uint_as_float((eb + 22u) << 23);
+                    const bool neg = inv3[a] < 0.0f;
+                    wn[a] = neg ? wq[2 * a + 1] : wq[2 * a];
+                    wf[a] = neg ? wq[2 * a] : wq[2 * a + 1];
                 }
-                const uint32_t wq[6] = {__float_as_uint(qb.x), __float_as_uint(qb.y), __float_as_uint(qb.z),
-                                        __float_as_uint(qb.w), __float_as_uint(qc.x), __float_as_uint(qc.y)};
                 const int4 q6 = make_int4(__float_as_int(qc.z), __float_as_int(qc.w), __float_as_int(qd.x),
                                           __float_as_int(qd.y));
-                // child j plane: (2^23 + q) * s + (p - 2^23 s) = p + q s, rounded outward
-                auto dec_lo = [&](int a, int j) {
-                    return __fmaf_rd(byte_to_2p23(wq[2 * a], j, magic), sc[a], plo[a]);
-                };
-                auto dec_hi = [&](int a, int j) {
-                    return __fmaf_ru(byte_to_2p23(wq[2 * a + 1], j, magic), sc[a], phi[a]);
+                auto child = [&](int j, float& tn) {
+                    const float nx = fmaf(fmaf(byte_to_2p23(wn[0], j, magic), sc[0], pm[0]), r.ix, -r.lx);
+                    const float ny = fmaf(fmaf(byte_to_2p23(wn[1], j, magic), sc[1], pm[1]), r.iy, -r.ly);
+                    const float nz = fmaf(fmaf(byte_to_2p23(wn[2], j, magic), sc[2], pm[2]), r.iz, -r.lz);
+                    const float fx = fmaf(fmaf(byte_to_2p23(wf[0], j, magic), sc[0], pm[0]), r.ix, -r.hx);
+                    const float fy = fmaf(fmaf(byte_to_2p23(wf[1], j, magic), sc[1], pm[1]), r.iy, -r.hy);
+                    const float fz = fmaf(fmaf(byte_to_2p23(wf[2], j, magic), sc[2], pm[2]), r.iz, -r.hz);
+                    tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, 0.0f));
+                    const float tf = fminf(fminf(fx, fy), fminf(fz, tclip));
+                    return ((vmask >> j) & 1u) != 0u && tn <= tf;
                 };
                 float k0, k1, k2, k3;
-                const bool h0 = ((vmask & 1u) != 0u) & slab(r, dec_lo(0, 0), dec_hi(0, 0), dec_lo(1, 0), dec_hi(1, 0),
-                                                     dec_lo(2, 0), dec_hi(2, 0), tclip, k0);
-                const bool h1 = ((vmask & 2u) != 0u) & slab(r, dec_lo(0, 1), dec_hi(0, 1), dec_lo(1, 1), dec_hi(1, 1),
-                                                     dec_lo(2, 1), dec_hi(2, 1), tclip, k1);
-                const bool h2 = ((vmask & 4u) != 0u) & slab(r, dec_lo(0, 2), dec_hi(0, 2), dec_lo(1, 2), dec_hi(1, 2),
-                                                     dec_lo(2, 2), dec_hi(2, 2), tclip, k2);
-                const bool h3 = ((vmask & 8u) != 0u) & slab(r, dec_lo(0, 3), dec_hi(0, 3), dec_lo(1, 3), dec_hi(1, 3),
-                                                     dec_lo(2, 3), dec_hi(2, 3), tclip, k3);
+                const bool h0 = child(0, k0), h1 = child(1, k1), h2 = child(2, k2), h3 = child(3, k3);
                 if (kCounters) st.boxes += 4;
                 int c0 = h0 ? q6.x : kNoRef, c1 = h1 ? q6.y : kNoRef, c2 = h2 ? q6.z : kNoRef, c3 = h3 ? q6.w : kNoRef;
                 if (kSort) {
@@ -801,11 +812,17 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                     k1 = h1 ? k1 : INFINITY;
                     k2 = h2 ? k2 : INFINITY;
                     k3 = h3 ? k3 : INFINITY;
-                    cas(k0, c0, k1, c1);
-                    cas(k2, c2, k3, c3);
-                    cas(k0, c0, k2, c2);
-                    cas(k1, c1, k3, c3);
-                    cas(k1, c1, k2, c2);
+                    if (MODE == MODE_BARY) {  // full near-first order (nearest-hit culling)
+                        cas(k0, c0, k1, c1);
+                        cas(k2, c2, k3, c3);
+                        cas(k0, c0, k2, c2);
+                        cas(k1, c1, k3, c3);
+                        cas(k1, c1, k2, c2);
+                    } else {  // any hit: only the nearest child goes first
+                        cas(k0, c0, k1, c1);
+                        cas(k2, c2, k3, c3);
+                        cas(k0, c0, k2, c2);
+                    }
                 }
                 int first = kNoRef;
                 if (c3 != kNoRef) first = c3;

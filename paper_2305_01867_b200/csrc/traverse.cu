@@ -639,6 +639,27 @@ struct LaneStack {
     }
 };
 
+// Local-memory stack whose top entry lives in a register: a pop returns the
+// register at once and starts the load of the next entry, whose latency is
+// hidden until the next pop (the popped node id no longer waits on an LDL).
+template <int kStack, int kT>
+struct LaneStack<kStack, 0, kT> {
+    int* s;
+    int top;
+    int local[kStack];
+    __device__ __forceinline__ void push(int& sp, int x) {
+        if (sp > 0) local[sp - 1] = top;
+        top = x;
+        ++sp;
+    }
+    __device__ __forceinline__ int pop(int& sp) {
+        const int x = top;
+        --sp;
+        if (sp > 0) top = local[sp - 1];
+        return x;
+    }
+};
+
 // 2^23 + byte j of w, as a float (exact): one PRMT with an immediate selector;
 // `magic` holds 0x4B000000 in a register (kept loop-invariant by the caller)
 __device__ __forceinline__ float byte_to_2p23(uint32_t w, int j, uint32_t magic) {

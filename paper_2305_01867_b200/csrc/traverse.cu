@@ -1253,7 +1253,7 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     p.stats = h->stats;
     p.counter = reinterpret_cast<unsigned long long*>(h->scratch + SCR_DISPENSER);
     // traversal-phase exit threshold, measured per mode (env RSI_MIN_TRAV overrides)
-    p.min_trav = h->min_trav >= 0 ? h->min_trav : (mode == RSI_MODE_BOOLEAN ? 16 : 8);
+    p.min_trav = h->min_trav >= 0 ? h->min_trav : (mode == RSI_MODE_INTERCEPT_COUNT ? 8 : 16);
     const bool fp64 = (h->opt.flags & RSI_OPT_FP64_MOLLER) != 0, ctr = (h->opt.flags & RSI_OPT_COUNTERS) != 0;
     if (fp64)
         ctr ? launch_mode<true, true>(mode, p, s) : launch_mode<true, false>(mode, p, s);

@@ -232,7 +232,6 @@ def main():
     Sd, Ed = torch.from_numpy(S).to(dev), torch.from_numpy(E).to(dev)
     stream = torch.cuda.current_stream(dev)
     h = rsi.rsi_build(Vd, Td)
-    kernels_per_build = 6 if len(T) <= 65536 else 5 + 12
 
     def timed(mode: str, steps: int, warmup: int, clocks: bool):
         out = rsi.alloc_outputs(n, mode, dev)
@@ -260,10 +259,12 @@ def main():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
+        launches0 = rsi.rsi_launch_count()
         t0.record(stream)
         for k in range(steps):
             step(evs[k])
         t1.record(stream)
+        launches = rsi.rsi_launch_count() - launches0
         torch.cuda.synchronize(dev)
         if world > 1:
             dist.barrier()
@@ -276,9 +277,9 @@ def main():
             tm = torch.tensor([ms, build_ms, query_ms], dtype=torch.float64, device=dev)
             dist.all_reduce(tm, op=dist.ReduceOp.MAX)
             ms, build_ms, query_ms = tm.tolist()
-        return ms, build_ms, query_ms, (sampler.summary() if sampler else None)
+        return ms, build_ms, query_ms, (sampler.summary() if sampler else None), launches
 
-    ms, build_ms, query_ms, clk = timed(args.mode, args.steps, max(args.warmup, 3), True)
+    ms, build_ms, query_ms, clk, launches = timed(args.mode, args.steps, max(args.warmup, 3), True)
     total_rays = n * world * args.steps
     value = total_rays / (ms * 1e-3)
     extra = {}
@@ -286,7 +287,7 @@ def main():
         for m in ("barycentric", "intercept_count"):
             if m == args.mode:
                 continue
-            mms, mb, mq, _ = timed(m, args.steps, 3, False)
+            mms, mb, mq, _, _ = timed(m, args.steps, 3, False)
             extra[m] = {"value": n * world * args.steps / (mms * 1e-3), "ms_per_step": mms / args.steps,
                         "build_ms": mb, "query_ms": mq}
     stats = rsi.rsi_get_stats(h)
@@ -372,8 +373,9 @@ def main():
             "roofline": roofline(args.mode, n, query_ms, clk["sm_mhz"] if clk else None, work),
             "work_per_ray": work,
             "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": args.steps * (kernels_per_build + 1),
-            "gpu_launches_note": f"per step: {kernels_per_build} build kernels + 1 traversal kernel",
+            "gpu_launches": launches,
+            "gpu_launches_note": "rsi_launch_count() difference over the timed region (library kernels: "
+                                 "BVH build chain + 1 traversal kernel per step)",
             "clocks": clk, "modes": extra, "configs_other": other, "stats": stats,
         }
         print(json.dumps(line), flush=True)

@@ -132,6 +132,12 @@ typedef struct {
 /* Library version string, e.g. "rsi-b200 0.1.0 sm_100a". */
 const char* rsi_version(void);
 
+/* Number of CUDA kernels this library has launched in this process, all
+ * threads and devices (a monotonically increasing host-side counter, bumped
+ * at every <<<>>> site; bench.py differences it around the timed region to
+ * report gpu_launches).  Never fails. */
+uint64_t rsi_launch_count(void);
+
 /* Thread-local message for the most recent failing call on this thread. */
 const char* rsi_last_error(void);
 

@@ -4,6 +4,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <ctime>
+#include <atomic>
 #include <new>
 
 #include "rsi_internal.cuh"
@@ -83,9 +84,15 @@ void rsi_keep_pool_cached() {
     (void)cudaGetLastError();
 }
 
+static std::atomic<uint64_t> g_launches{0};
+
+void rsi_note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 extern "C" {
 
 const char* rsi_version(void) { return RSI_VERSION_STRING; }
+
+uint64_t rsi_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char* rsi_last_error(void) { return g_err; }
 

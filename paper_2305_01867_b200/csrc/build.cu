@@ -841,11 +841,11 @@ static void launch_sort(rsi_bvh* h, int n, cudaStream_t s) {
             cudaFuncSetAttribute(k_sort_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * kSmemSortMax);
             attr = true;
         }
-        k_sort_smem<<<1, kSmallThreads, (size_t)16 * n, s>>>(h->keys, h->vals, n);
+        rsi_note_launch(), k_sort_smem<<<1, kSmallThreads, (size_t)16 * n, s>>>(h->keys, h->vals, n);
         return;
     }
     if (n <= kSmallMax) {
-        k_sort_small<<<1, kSmallThreads, 0, s>>>(h->keys, h->vals, h->keys_tmp, h->vals_tmp, n);
+        rsi_note_launch(), k_sort_small<<<1, kSmallThreads, 0, s>>>(h->keys, h->vals, h->keys_tmp, h->vals_tmp, n);
         return;
     }
     int nb = rsi_ceil_div(n, kTile);
@@ -854,9 +854,9 @@ static void launch_sort(rsi_bvh* h, int n, cudaStream_t s) {
         int32_t* vs = (p & 1) ? h->vals_tmp : h->vals;
         uint32_t* kd = (p & 1) ? h->keys : h->keys_tmp;
         int32_t* vd = (p & 1) ? h->vals : h->vals_tmp;
-        k_sort_hist<<<nb, kTileThreads, 0, s>>>(ks, n, 8 * p, h->hist);
-        k_sort_scan<<<1, 1024, 0, s>>>(h->hist, kDigits * nb);
-        k_sort_scatter<<<nb, kTileThreads, 0, s>>>(ks, vs, kd, vd, n, 8 * p, h->hist);
+        rsi_note_launch(), k_sort_hist<<<nb, kTileThreads, 0, s>>>(ks, n, 8 * p, h->hist);
+        rsi_note_launch(), k_sort_scan<<<1, 1024, 0, s>>>(h->hist, kDigits * nb);
+        rsi_note_launch(), k_sort_scatter<<<nb, kTileThreads, 0, s>>>(ks, vs, kd, vd, n, 8 * p, h->hist);
     }
 }
 
@@ -870,23 +870,23 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
     if (st != RSI_OK) return st;
     const int n = (int)nt;
     const int n_nodes = n > 1 ? n - 1 : 1;
-    k_build_init<<<1, 32, 0, s>>>(h->scratch);
+    rsi_note_launch(), k_build_init<<<1, 32, 0, s>>>(h->scratch);
     int64_t work = nv > 3 * nt ? nv : 3 * nt;
     int eb = rsi_ceil_div(work, kBlock);
     if (eb > 148 * 8) eb = 148 * 8;
-    k_extent_validate<<<eb, kBlock, 0, s>>>(V, nv, T, nt, h->scratch);
-    k_morton<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, n, h->scratch, h->keys, h->vals, h->arrivals,
+    rsi_note_launch(), k_extent_validate<<<eb, kBlock, 0, s>>>(V, nv, T, nt, h->scratch);
+    rsi_note_launch(), k_morton<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, n, h->scratch, h->keys, h->vals, h->arrivals,
                                                          n_nodes);
     launch_sort(h, n, s);
-    k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent, h->arrivals);
+    rsi_note_launch(), k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent, h->arrivals);
     // the refit grid covers every leaf (case study 2: never size it from another
     // count) -- except under the test-only fault injection option
     const int refit_leaves = (h->opt.debug_refit_leaves > 0 && h->opt.debug_refit_leaves < n)
                                  ? (int)h->opt.debug_refit_leaves : n;
-    k_refit<<<rsi_ceil_div(refit_leaves, kBlock), kBlock, 0, s>>>(V, nv, T, h->vals, refit_leaves, n, h->nodes,
+    rsi_note_launch(), k_refit<<<rsi_ceil_div(refit_leaves, kBlock), kBlock, 0, s>>>(V, nv, T, h->vals, refit_leaves, n, h->nodes,
                                                                    h->tris, h->parent, h->arrivals, h->scratch);
-    if (kTopNodes > 0) k_topk<<<1, 1024, 0, s>>>(h->nodes, n_nodes, h->top, h->scratch);
-    if (rsi_uses_quads()) k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads, h->scratch);
+    if (kTopNodes > 0) rsi_note_launch(), k_topk<<<1, 1024, 0, s>>>(h->nodes, n_nodes, h->top, h->scratch);
+    if (rsi_uses_quads()) rsi_note_launch(), k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads, h->scratch);
     st = rsi_cuda_check(cudaGetLastError(), "build kernel launch");
     if (st != RSI_OK) return st;
     st = rsi_cuda_check(cudaMemcpyAsync(h->h_words, h->scratch, SCR_WORDS * sizeof(uint32_t),
@@ -942,10 +942,10 @@ rsi_status_t rsi_validate_device(rsi_bvh* h, rsi_integrity_t* report, cudaStream
     if (st == RSI_OK) st = rsi_cuda_check(cudaMemsetAsync(out, 0, V_WORDS * sizeof(unsigned long long), s), "memset");
     if (st == RSI_OK) st = rsi_cuda_check(cudaMemsetAsync(seen, 0, (size_t)n * sizeof(uint32_t), s), "memset");
     if (st == RSI_OK) {
-        k_validate_nodes<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n, n_nodes, h->parent, h->arrivals,
+        rsi_note_launch(), k_validate_nodes<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n, n_nodes, h->parent, h->arrivals,
                                                                          out);
-        k_validate_leaves<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(h->tris, n, n_nodes, h->parent, seen, out);
-        k_validate_ids<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(seen, n, out);
+        rsi_note_launch(), k_validate_leaves<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(h->tris, n, n_nodes, h->parent, seen, out);
+        rsi_note_launch(), k_validate_ids<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(seen, n, out);
         st = rsi_cuda_check(cudaGetLastError(), "validate launch");
     }
     unsigned long long v[V_WORDS] = {0};

@@ -92,6 +92,8 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* d_start, const float*
                                   int64_t n_rays, int32_t mode, const rsi_outputs_t* out,
                                   cudaStream_t stream);
 bool rsi_uses_quads();
+// process-wide count of kernels this library launched (rsi_launch_count)
+void rsi_note_launch();
 rsi_status_t rsi_validate_device(rsi_bvh* h, rsi_integrity_t* report, cudaStream_t stream);  // build.cu  // traverse.cu: does any mode walk the 4-wide records
 rsi_status_t rsi_compact_device(const int32_t* d_tri, int64_t n_rays, int32_t* d_ids,
                                 int32_t* d_n, cudaStream_t stream);

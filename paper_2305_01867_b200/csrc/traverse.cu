@@ -1200,7 +1200,7 @@ static void launch_trace(const TraceParams& p, cudaStream_t s) {
     }
     const int64_t need = (p.n + kT - 1) / kT;
     const int g = (int)(need < grid ? need : grid);
-    k_trace<MODE, kFP64, kCounters><<<g, kT, dyn, s>>>(p);
+    rsi_note_launch(), k_trace<MODE, kFP64, kCounters><<<g, kT, dyn, s>>>(p);
 }
 
 template <bool kFP64, bool kCounters>
@@ -1276,7 +1276,7 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     st = rsi_cuda_check(cudaMallocAsync((void**)&seg, (size_t)n_ovf * 2 * sizeof(int32_t), s), "overflow segs");
     if (st != RSI_OK) return RSI_E_OOM;
     const int nb = rsi_ceil_div(n_ovf, kThreads);
-    k_ovf_size<<<nb, kThreads, 0, s>>>(h->nodes, h->tris, S, E, h->ovf_list, n_ovf, seg, h->scratch);
+    rsi_note_launch(), k_ovf_size<<<nb, kThreads, 0, s>>>(h->nodes, h->tris, S, E, h->ovf_list, n_ovf, seg, h->scratch);
     cudaMemcpyAsync(h->h_words, h->scratch + SCR_OVF_TOTAL, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
     st = rsi_cuda_check(cudaStreamSynchronize(s), "overflow sizing");
     if (st != RSI_OK) {
@@ -1289,7 +1289,7 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
         cudaFreeAsync(seg, s);
         return RSI_E_OOM;
     }
-    k_ovf_count<<<nb, kThreads, 0, s>>>(h->nodes, h->tris, S, E, h->ovf_list, n_ovf, seg, pool, h->opt.dedup_tau,
+    rsi_note_launch(), k_ovf_count<<<nb, kThreads, 0, s>>>(h->nodes, h->tris, S, E, h->ovf_list, n_ovf, seg, pool, h->opt.dedup_tau,
                                         out->count);
     st = rsi_cuda_check(cudaGetLastError(), "overflow pass");
     cudaFreeAsync(pool, s);
@@ -1306,9 +1306,9 @@ rsi_status_t rsi_compact_device(const int32_t* tri, int64_t n, int32_t* ids, int
     uint32_t* blk = nullptr;
     rsi_status_t st = rsi_cuda_check(cudaMallocAsync((void**)&blk, (size_t)nb * sizeof(uint32_t), s), "compact");
     if (st != RSI_OK) return RSI_E_OOM;
-    k_compact_count<<<nb, 256, 0, s>>>(tri, n, blk);
-    k_compact_scan<<<1, 1024, 0, s>>>(blk, nb, d_n);
-    k_compact_write<<<nb, 256, 0, s>>>(tri, n, blk, ids);
+    rsi_note_launch(), k_compact_count<<<nb, 256, 0, s>>>(tri, n, blk);
+    rsi_note_launch(), k_compact_scan<<<1, 1024, 0, s>>>(blk, nb, d_n);
+    rsi_note_launch(), k_compact_write<<<nb, 256, 0, s>>>(tri, n, blk, ids);
     st = rsi_cuda_check(cudaGetLastError(), "compaction launch");
     cudaFreeAsync(blk, s);
     return st;

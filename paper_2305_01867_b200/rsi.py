@@ -79,6 +79,7 @@ def load():
         sig = {
             "rsi_version": ([], ctypes.c_char_p),
             "rsi_last_error": ([], ctypes.c_char_p),
+            "rsi_launch_count": ([], ctypes.c_uint64),
             "rsi_build": ([_p, _i64, _p, _i64, _p, _p, ctypes.POINTER(_p)], ctypes.c_int),
             "rsi_rebuild": ([_p, _p, _i64, _p, _i64, _p], ctypes.c_int),
             "rsi_intersect": ([_p, _p, _p, _i64, _i32, ctypes.POINTER(_Outputs), _p], ctypes.c_int),
@@ -127,6 +128,11 @@ def _dev(t: torch.Tensor, dtype, name: str, cols: int | None = 3) -> torch.Tenso
 
 def rsi_version() -> str:
     return load().rsi_version().decode()
+
+
+def rsi_launch_count() -> int:
+    """Kernels the library has launched in this process (host counter)."""
+    return int(load().rsi_launch_count())
 
 
 @dataclass

@@ -455,3 +455,22 @@ def test_fixture_dump_and_dot_from_device(rsi):
     dot = diagnostics.to_dot(d)
     for lab in ("[0,3]", "[0,1]", "[2,3]", "[0] 0", "[1] 3", "[2] 1", "[3] 2"):
         assert f'label="{lab}"' in dot
+
+
+def test_launch_counter(rsi):
+    """rsi_launch_count (the bench's gpu_launches) counts every library kernel:
+    one traversal kernel per rsi_intersect without overflow, and a build chain
+    of at least init/extent/morton/sort/karras/refit per rsi_build."""
+    V, T, S, E, _ = synth.workload("sphere", 2000, seed=3)
+    Vd, Td, Sd, Ed = to_dev(V, T, S, E)
+    c0 = rsi.rsi_launch_count()
+    h = rsi.rsi_build(Vd, Td)
+    c1 = rsi.rsi_launch_count()
+    assert c1 - c0 >= 6
+    for mode in ("boolean", "barycentric", "intercept_count"):
+        before = rsi.rsi_launch_count()
+        rsi.rsi_intersect(h, Sd, Ed, mode)
+        assert rsi.rsi_launch_count() - before == 1, mode
+    rsi.rsi_rebuild(h, Vd, Td)
+    assert rsi.rsi_launch_count() - (c1 + 3) == c1 - c0
+    h.free()

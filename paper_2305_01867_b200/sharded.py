@@ -6,8 +6,8 @@ intersects the contiguous ray slice [floor(r N / W), floor((r+1) N / W)).  The
 only collective is the final gather of the per-ray outputs to rank 0 in ray
 order (north_star: "NCCL over NVLink is used only to gather the per-ray
 outputs").  The gather pads every slice to ceil(N / W) rows and uses one
-all_gather_into_tensor per output field (NCCL over NVLink on GPUs, gloo in the
-CPU tests), then trims the padding.
+dist.gather per output field (NCCL over NVLink on GPUs, gloo in the CPU
+tests), then trims the padding on rank 0.
 """
 from __future__ import annotations
 

@@ -14,6 +14,7 @@
 // oracle's exact double results.  This is the paper's
 // USE_DOUBLE_PRECISION_MOLLER idea applied only where fp32 is unsure.
 #include <cstdio>
+#include <type_traits>
 
 #include "rsi_internal.cuh"
 
@@ -50,6 +51,12 @@ constexpr float kOutTol = 4e-6f;                 // max certified |t error| for 
 #define RSI_COUNT_SMEM 0
 #endif
 #define RSI_ANY_QUAD (RSI_BOOL_QUAD || RSI_BARY_QUAD || RSI_COUNT_QUAD)
+#ifndef RSI_BFSTACK
+#define RSI_BFSTACK 1  // measured: -11 % boolean, -5 % barycentric query time (sphere)
+#endif
+#ifndef RSI_BF_SMEM
+#define RSI_BF_SMEM 0
+#endif
 #ifndef RSI_SORT_ALL
 #define RSI_SORT_ALL 1
 #endif
@@ -660,6 +667,41 @@ struct LaneStack<kStack, 0, kT> {
     }
 };
 
+// Branch-free stack for the 4-wide walk (RSI_BFSTACK): the top entry in a
+// register, the entries below it at slots 1 .. sp-1 (slot 0 is scratch), slots
+// < kSm in a shared-memory column (one bank per lane at any depth), the rest in
+// local memory.  push_if always stores (the old top goes to slot sp, which is
+// either claimed by the push or dead), so a visit's up-to-3 pushes are
+// straight-line code with no divergent branches.
+template <int kStack, int kSm, int kT>
+struct BFStack {
+    int* s;
+    int top;
+    int local[kStack + 1 - kSm];
+    // (unsigned indices: the compiler then knows a store cannot alias `top`)
+    __device__ __forceinline__ void put(int k, int x) {
+        if (kSm > 0 && k < kSm)
+            s[k * kT] = x;
+        else
+            local[(unsigned)(k - kSm)] = x;
+    }
+    __device__ __forceinline__ int get(int k) const {
+        return (kSm > 0 && k < kSm) ? s[k * kT] : local[(unsigned)(k - kSm)];
+    }
+    __device__ __forceinline__ void push_if(int& sp, bool v, int x) {
+        put(sp, top);
+        top = v ? x : top;
+        sp += v ? 1 : 0;
+    }
+    __device__ __forceinline__ void push(int& sp, int x) { push_if(sp, true, x); }
+    __device__ __forceinline__ int pop(int& sp) {
+        const int x = top;
+        --sp;
+        top = get(sp);
+        return x;
+    }
+};
+
 // 2^23 + byte j of w, as a float (exact): one PRMT with an immediate selector;
 // `magic` holds 0x4B000000 in a register (kept loop-invariant by the caller)
 __device__ __forceinline__ float byte_to_2p23(uint32_t w, int j, uint32_t magic) {
@@ -712,8 +754,10 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
     int node = -1, sp = 0, l0 = -1, l1 = -1, l2 = -1;  // pending (postponed) leaf slots
     // per-lane traversal stack: the first kSmemStack entries in a shared-memory
     // column (one bank per lane: conflict-free at any depth), the rest local
-    LaneStack<kStack, kSmemStack, kT> stk;
-    __shared__ int s_stack[kSmemStack > 0 ? kSmemStack * kT : 1];
+    constexpr bool kBF = kQuad && RSI_BFSTACK;
+    constexpr int kSmWords = kBF ? RSI_BF_SMEM : kSmemStack;
+    typename std::conditional<kBF, BFStack<kStack, RSI_BF_SMEM, kT>, LaneStack<kStack, kSmemStack, kT>>::type stk;
+    __shared__ int s_stack[kSmWords > 0 ? kSmWords * kT : 1];
     stk.s = s_stack + threadIdx.x;
     float tclip = 1.0f;
     ModeState<MODE> ms;
@@ -845,6 +889,16 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                         cas(k0, c0, k2, c2);
                     }
                 }
+                if constexpr (kBF) {
+                    // c0 is the nearest hit child (kSort) -- kNoRef only when none hit
+                    stk.push_if(sp, c3 != kNoRef, c3);
+                    stk.push_if(sp, c2 != kNoRef, c2);
+                    stk.push_if(sp, c1 != kNoRef, c1);
+                    int first = c0;
+                    if (first == kNoRef && sp > 0) first = stk.pop(sp);
+                    node = first >= 0 ? first : -1;
+                    if (first != kNoRef && first < 0) l0 = ~first;
+                } else {
                 int first = kNoRef;
                 if (c3 != kNoRef) first = c3;
                 if (c2 != kNoRef) {
@@ -867,6 +921,7 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                 } else {
                     l0 = ~first;
                     node = -1;
+                }
                 }
             }
         }

@@ -12,6 +12,8 @@
 // lesson: never size one kernel's grid from another's count).
 #include <cstdio>
 
+#include <cstring>
+
 #include "rsi_internal.cuh"
 
 namespace {
@@ -27,6 +29,9 @@ __global__ void k_build_init(uint32_t* scratch) {
     if (i == 0) {
         scratch[SCR_STATUS] = 0u;
         scratch[SCR_ROOT_SET] = 0u;
+        scratch[SCR_QPMAX] = 0u;
+        scratch[SCR_QEMIN] = 0xffffffffu;
+        scratch[SCR_QEMAX] = 0u;
     }
 }
 
@@ -649,7 +654,7 @@ __device__ __forceinline__ void quant_axis(const float* lo, const float* hi, int
     while (true) {
         sc = ldexp(1.0, e);
         p = floor((double)nlo / sc) * sc;  // multiple of s, p <= nlo
-        // covers the node, and p = k*s with |k| < 2^23 so p and p - 2^23 s are exact floats
+        // covers the node, and p = k*s with |k| < 2^23 so p and p - 2^15 s are exact floats
         if (((double)nhi - p <= 255.0 * sc && fabs(p / sc) < 8388608.0) || e >= kQuadEMax) break;
         ++e;
     }
@@ -662,9 +667,9 @@ __device__ __forceinline__ void quant_axis(const float* lo, const float* hi, int
         wlo |= (uint32_t)ql << (8 * j);
         whi |= (uint32_t)qh << (8 * j);
     }
-    p_out = (float)p;  // exact (|p/s| < 2^23)
+    p_out = (float)(p - 32768.0 * sc);  // the decode offset p - 2^15 s: exact (|p/s - 2^15| < 2^24)
     e_out = e;
-    ok = ((double)nhi - p <= 255.0 * sc) && fabs(p / sc) < 8388608.0 && (double)p_out == p;
+    ok = ((double)nhi - p <= 255.0 * sc) && fabs(p / sc) < 8388608.0 && (double)p_out == p - 32768.0 * sc;
 }
 
 __global__ void __launch_bounds__(kBlock) k_quads(const float4* __restrict__ nodes, int n_nodes,
@@ -711,6 +716,12 @@ __global__ void __launch_bounds__(kBlock) k_quads(const float4* __restrict__ nod
         ok = ok && oka;
     }
     if (!ok) atomicOr(&scratch[SCR_STATUS], STATUS_RANGE);  // coordinates beyond ~1e33
+    // max |decode offset| (non-negative float bits order like uint32): bounds the
+    // rounding of the traversal's per-node slab term fma(pm, inv, -off)
+    const float pmax = fmaxf(fabsf(px[0]), fmaxf(fabsf(px[1]), fabsf(px[2])));
+    atomicMax(&scratch[SCR_QPMAX], __float_as_uint(pmax));
+    atomicMin(&scratch[SCR_QEMIN], (uint32_t)(min(ex[0], min(ex[1], ex[2])) + 128));
+    atomicMax(&scratch[SCR_QEMAX], (uint32_t)(max(ex[0], max(ex[1], ex[2])) + 128));
     w[0] = __float_as_uint(px[0]);
     w[1] = __float_as_uint(px[1]);
     w[2] = __float_as_uint(px[2]);
@@ -900,6 +911,9 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
     if (status & STATUS_NONFINITE) return rsi_set_error(RSI_E_NONFINITE, "a vertex coordinate is NaN or Inf");
     if (status & STATUS_RANGE)
         return rsi_set_error(RSI_E_INVALID_ARG, "mesh extent too large for the quantized BVH (|coordinates| > ~1e33)");
+    memcpy(&h->quad_pmax, &h->h_words[SCR_QPMAX], sizeof(float));
+    h->quad_emin = (int)h->h_words[SCR_QEMIN] - 128;
+    h->quad_emax = (int)h->h_words[SCR_QEMAX] - 128;
     const float* root = reinterpret_cast<const float*>(h->h_words + SCR_ROOT);
     for (int x = 0; x < 3; ++x) {
         h->scene_lo[x] = root[x];

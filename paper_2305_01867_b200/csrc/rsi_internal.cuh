@@ -34,6 +34,9 @@ enum {
     SCR_DISPENSER = 18, // 2 words: 64-bit ray dispenser of the persistent traversal grid
     SCR_NTOP = 20,      // nodes in the top-of-tree shared-memory image
     SCR_ROOT_SET = 21,  // 1 once the refit wrote the root box
+    SCR_QPMAX = 22,     // max |decode offset| over the quad records (float bits, >= 0)
+    SCR_QEMIN = 23,     // min / max grid exponent + 128 over the quad records
+    SCR_QEMAX = 24,
     SCR_WORDS = 32
 };
 enum { STATUS_INDEX = 1u, STATUS_NONFINITE = 2u, STATUS_RANGE = 4u };
@@ -74,6 +77,8 @@ struct rsi_bvh {
     int32_t* ovf_list = nullptr;     // ray ids
     int64_t ovf_cap = 0;
     float scene_lo[3] = {0, 0, 0}, scene_hi[3] = {0, 0, 0};
+    float quad_pmax = 0.0f;          // SCR_QPMAX after the build (slab slack of the 4-wide walk)
+    int quad_emin = 0, quad_emax = 0;  // SCR_QEMIN / SCR_QEMAX - 128
     uint64_t host_rays = 0, host_overflow = 0;  // counters known on the host
     int min_trav = -1;  // traversal-phase exit threshold (-1: per-mode default); env RSI_MIN_TRAV
 };
@@ -91,10 +96,10 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* d_vertices, int64_t n_ver
 rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* d_start, const float* d_end,
                                   int64_t n_rays, int32_t mode, const rsi_outputs_t* out,
                                   cudaStream_t stream);
-bool rsi_uses_quads();
+bool rsi_uses_quads();  // traverse.cu: does any mode walk the 4-wide records
 // process-wide count of kernels this library launched (rsi_launch_count)
 void rsi_note_launch();
-rsi_status_t rsi_validate_device(rsi_bvh* h, rsi_integrity_t* report, cudaStream_t stream);  // build.cu  // traverse.cu: does any mode walk the 4-wide records
+rsi_status_t rsi_validate_device(rsi_bvh* h, rsi_integrity_t* report, cudaStream_t stream);  // build.cu
 rsi_status_t rsi_compact_device(const int32_t* d_tri, int64_t n_rays, int32_t* d_ids,
                                 int32_t* d_n, cudaStream_t stream);
 

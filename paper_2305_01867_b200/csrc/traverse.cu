@@ -51,8 +51,13 @@ constexpr float kOutTol = 4e-6f;                 // max certified |t error| for 
 #define RSI_COUNT_SMEM 0
 #endif
 #define RSI_ANY_QUAD (RSI_BOOL_QUAD || RSI_BARY_QUAD || RSI_COUNT_QUAD)
-#ifndef RSI_BFSTACK
-#define RSI_BFSTACK 1  // measured: -11 % boolean, -5 % barycentric query time (sphere)
+// speculative walk on the 4-wide records (a lane with a pending leaf keeps
+// walking): measured -2..-4 % barycentric, +3..5 % boolean (round 1)
+#ifndef RSI_QSPEC_BOOL
+#define RSI_QSPEC_BOOL 0
+#endif
+#ifndef RSI_QSPEC_BARY
+#define RSI_QSPEC_BARY 1
 #endif
 #ifndef RSI_BF_SMEM
 #define RSI_BF_SMEM 0
@@ -96,27 +101,31 @@ struct Ray {
 // for |t| <= ~1, and is applied so the computed entry t is never later and the
 // exit t never earlier than the exact ones: the test never rejects a box the
 // exact segment touches.  |d| < 1e-30 (incl. 0): the axis imposes no constraint.
-__device__ __forceinline__ void slab_axis(float o, float d, float& inv, float& offlo, float& offhi) {
+// The 4-wide walk evaluates t as fma(q', s*inv, fma(pm, inv, -off)) (see the
+// visit in k_trace); its extra rounding, <= 2^-24 |pm * inv - off|, is covered
+// by `qext` * |inv| in the slack (qext = Pmax / 4 with Pmax >= every |pm|,
+// since 2^-21 / 4 = 2 * 2^-24), and axes whose |inv| falls outside
+// [lim_lo, lim_hi] are left unconstrained (conservative) so that s * inv stays
+// an exact normal float and no term can overflow.
+__device__ __forceinline__ void slab_axis(float o, float d, float& inv, float& offlo, float& offhi,
+                                          float qext = 0.0f, float lim_lo = 0.0f, float lim_hi = INFINITY) {
     if (fabsf(d) >= 1e-30f) {
         inv = 1.0f / d;
-        float oinv = o * inv;
-        float slack = kSlack * (1.0f + fabsf(oinv));
-        float sg = inv > 0.0f ? slack : -slack;
-        offlo = oinv + sg;
-        offhi = oinv - sg;
-        if (isfinite(offlo) && isfinite(offhi)) return;
+        const float ai = fabsf(inv);
+        if (ai >= lim_lo && ai <= lim_hi) {
+            float oinv = o * inv;
+            float slack = kSlack * fmaf(qext, ai, 1.0f + fabsf(oinv));
+            float sg = inv > 0.0f ? slack : -slack;
+            offlo = oinv + sg;
+            offhi = oinv - sg;
+            if (isfinite(offlo) && isfinite(offhi)) return;
+        }
     }
     inv = 0.0f;
     offlo = INFINITY;
     offhi = -INFINITY;
 }
 
-#ifndef RSI_PREFER_L1
-#define RSI_PREFER_L1 0
-#endif
-#ifndef RSI_STREAM_NOALLOC
-#define RSI_STREAM_NOALLOC 0
-#endif
 __device__ __forceinline__ float ld_stream(const float* p) {
 #if RSI_STREAM_NOALLOC
     float v;
@@ -133,7 +142,8 @@ __device__ __forceinline__ float ld_stream(const float* p) {
 // for inv >= 0, hi / lo for inv < 0) for the octant-selected quad slab test.
 template <bool kNearFar = false>
 __device__ __forceinline__ bool load_ray(Ray& r, const float* __restrict__ S, const float* __restrict__ E,
-                                         int64_t i, bool& nonfinite) {
+                                         int64_t i, bool& nonfinite, float qext = 0.0f, float lim_lo = 0.0f,
+                                         float lim_hi = INFINITY) {
     // the segment stream is read once: do not let it displace tree nodes in L1
     r.ox = ld_stream(S + 3 * i);
     r.oy = ld_stream(S + 3 * i + 1);
@@ -146,9 +156,9 @@ __device__ __forceinline__ bool load_ray(Ray& r, const float* __restrict__ S, co
     r.dx = r.ex - r.ox;
     r.dy = r.ey - r.oy;
     r.dz = r.ez - r.oz;
-    slab_axis(r.ox, r.dx, r.ix, r.lx, r.hx);
-    slab_axis(r.oy, r.dy, r.iy, r.ly, r.hy);
-    slab_axis(r.oz, r.dz, r.iz, r.lz, r.hz);
+    slab_axis(r.ox, r.dx, r.ix, r.lx, r.hx, qext, lim_lo, lim_hi);
+    slab_axis(r.oy, r.dy, r.iy, r.ly, r.hy, qext, lim_lo, lim_hi);
+    slab_axis(r.oz, r.dz, r.iz, r.lz, r.hz, qext, lim_lo, lim_hi);
     if (kNearFar) {
         if (r.ix < 0.0f) { const float t = r.lx; r.lx = r.hx; r.hx = t; }
         if (r.iy < 0.0f) { const float t = r.ly; r.ly = r.hy; r.hy = t; }
@@ -379,7 +389,9 @@ struct TraceParams {
     unsigned long long* stats;
     unsigned long long* counter;  // persistent-grid ray dispenser
     int min_trav;           // leave the traversal phase when fewer lanes still search
-    uint32_t magic;         // 0x4B000000
+    uint32_t magic;         // 0x47000000 (float 2^15)
+    float qext;             // 4-wide walk: slack term Pmax / 4 (see slab_axis)
+    float qlim_lo, qlim_hi; // 4-wide walk: |inv| range with exact s * inv and no overflow
 };
 
 template <int MODE>
@@ -488,7 +500,7 @@ struct ModeState<MODE_BARY> {
             }
             p.tri[i] = id;
             if (p.t) p.t[i] = tt;
-            if (p.dist) p.dist[i] = tt * sqrtf(r.dx * r.dx + r.dy * r.dy + r.dz * r.dz);
+            if (p.dist) p.dist[i] = tt * norm3df(r.dx, r.dy, r.dz);  // no overflow / underflow of |d|^2
             if (p.point) {
                 p.point[3 * i] = fmaf(tt, r.dx, r.ox);
                 p.point[3 * i + 1] = fmaf(tt, r.dy, r.oy);
@@ -667,7 +679,7 @@ struct LaneStack<kStack, 0, kT> {
     }
 };
 
-// Branch-free stack for the 4-wide walk (RSI_BFSTACK): the top entry in a
+// Branch-free stack for the 4-wide walk: the top entry in a
 // register, the entries below it at slots 1 .. sp-1 (slot 0 is scratch), slots
 // < kSm in a shared-memory column (one bank per lane at any depth), the rest in
 // local memory.  push_if always stores (the old top goes to slot sp, which is
@@ -702,15 +714,16 @@ struct BFStack {
     }
 };
 
-// 2^23 + byte j of w, as a float (exact): one PRMT with an immediate selector;
-// `magic` holds 0x4B000000 in a register (kept loop-invariant by the caller)
-__device__ __forceinline__ float byte_to_2p23(uint32_t w, int j, uint32_t magic) {
+// 2^15 + byte j of w, as a float (exact): one PRMT with an immediate selector
+// places the byte in mantissa bits 8..15 of `magic` = 0x47000000 (2^15), which
+// the caller holds in a register (kept loop-invariant)
+__device__ __forceinline__ float byte_to_2p15(uint32_t w, int j, uint32_t magic) {
     uint32_t r;
     switch (j) {
-        case 0: asm("prmt.b32 %0, %1, %2, 0x7440;" : "=r"(r) : "r"(w), "r"(magic)); break;
-        case 1: asm("prmt.b32 %0, %1, %2, 0x7441;" : "=r"(r) : "r"(w), "r"(magic)); break;
-        case 2: asm("prmt.b32 %0, %1, %2, 0x7442;" : "=r"(r) : "r"(w), "r"(magic)); break;
-        default: asm("prmt.b32 %0, %1, %2, 0x7443;" : "=r"(r) : "r"(w), "r"(magic)); break;
+        case 0: asm("prmt.b32 %0, %1, %2, 0x7604;" : "=r"(r) : "r"(w), "r"(magic)); break;
+        case 1: asm("prmt.b32 %0, %1, %2, 0x7614;" : "=r"(r) : "r"(w), "r"(magic)); break;
+        case 2: asm("prmt.b32 %0, %1, %2, 0x7624;" : "=r"(r) : "r"(w), "r"(magic)); break;
+        default: asm("prmt.b32 %0, %1, %2, 0x7634;" : "=r"(r) : "r"(w), "r"(magic)); break;
     }
     return __uint_as_float(r);
 }
@@ -754,7 +767,8 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
     int node = -1, sp = 0, l0 = -1, l1 = -1, l2 = -1;  // pending (postponed) leaf slots
     // per-lane traversal stack: the first kSmemStack entries in a shared-memory
     // column (one bank per lane: conflict-free at any depth), the rest local
-    constexpr bool kBF = kQuad && RSI_BFSTACK;
+    constexpr bool kQSpec = MODE == MODE_BOOL ? RSI_QSPEC_BOOL : RSI_QSPEC_BARY;
+    constexpr bool kBF = kQuad;  // branch-free stack on the 4-wide walk (-11 % boolean, -5 % barycentric)
     constexpr int kSmWords = kBF ? RSI_BF_SMEM : kSmemStack;
     typename std::conditional<kBF, BFStack<kStack, RSI_BF_SMEM, kT>, LaneStack<kStack, kSmemStack, kT>>::type stk;
     __shared__ int s_stack[kSmWords > 0 ? kSmWords * kT : 1];
@@ -799,7 +813,8 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
         }
         if (fresh) {
             bool nonfinite;
-            const bool ok = load_ray<kQuad>(r, p.S, p.E, ray, nonfinite);
+            const bool ok = kQuad ? load_ray<true>(r, p.S, p.E, ray, nonfinite, p.qext, p.qlim_lo, p.qlim_hi)
+                                  : load_ray<false>(r, p.S, p.E, ray, nonfinite);
             if (nonfinite) st.add(ST_NONFINITE);
             ms.init();
             tclip = 1.0f;
@@ -828,29 +843,37 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                 __ballot_sync(FULL, l0 >= 0);
             }
             if (__popc(tm) < p.min_trav && __ballot_sync(FULL, l0 >= 0)) break;
-            if (trav) {
+            // kQSpec: a lane holding one pending leaf keeps walking (its next
+            // leaf goes to l1) in slots it would otherwise idle in
+            if (trav || (kQSpec && node >= 0 && l1 < 0)) {
                 const float4* q = p.quads + 4 * node;
                 float4 qa, qb, qc, qd;
                 ldg256(q, qa, qb);
                 ldg256(q + 2, qc, qd);
                 const uint32_t w3 = __float_as_uint(qa.w);
                 const uint32_t vmask = w3 >> 24;
-                // Per axis: grid step s = 2^e and the decode offset p - 2^23 s (both
-                // exact: the build keeps |p/s| < 2^23), so a child plane
-                // (2^23 + q) * s + (p - 2^23 s) = p + q s is exact under any rounding.
-                // The ray octant picks which byte array holds the near planes (lo for
-                // inv >= 0), so each child needs no per-axis min/max.
-                float sc[3], pm[3];
+                // Per axis: grid step s = 2^e and the decode offset pm = p - 2^15 s
+                // (stored; exact).  A child plane is p + q s = (2^15 + q) s + pm, so its
+                // t = (plane - o) / d is fma(2^15 + q, s*inv, fma(pm, inv, -off)): s*inv
+                // is exact (a power of two times inv, kept normal by qlim_lo/qlim_hi),
+                // 2^15 + q comes from one PRMT, and the rounding of the inner fma is
+                // covered by the slack (slab_axis, qext).  The ray octant picks which
+                // byte array holds the near planes (lo for inv >= 0), so each child needs
+                // no per-axis min/max.
+                float sa[3], bn[3], bf[3];
                 uint32_t wn[3], wf[3];
                 const float pp[3] = {qa.x, qa.y, qa.z};
                 const uint32_t wq[6] = {__float_as_uint(qb.x), __float_as_uint(qb.y), __float_as_uint(qb.z),
                                         __float_as_uint(qb.w), __float_as_uint(qc.x), __float_as_uint(qc.y)};
                 const float inv3[3] = {r.ix, r.iy, r.iz};
+                const float nof[3] = {r.lx, r.ly, r.lz};
+                const float fof[3] = {r.hx, r.hy, r.hz};
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
                     const uint32_t eb = (w3 >> (8 * a)) & 255u;
-                    sc[a] = __uint_as_float((eb - 1u) << 23);
-                    pm[a] = pp[a] - __uint_as_float((eb + 22u) << 23);
+                    sa[a] = __uint_as_float((eb - 1u) << 23) * inv3[a];
+                    bn[a] = fmaf(pp[a], inv3[a], -nof[a]);
+                    bf[a] = fmaf(pp[a], inv3[a], -fof[a]);
                     const bool neg = inv3[a] < 0.0f;
                     wn[a] = neg ? wq[2 * a + 1] : wq[2 * a];
                     wf[a] = neg ? wq[2 * a] : wq[2 * a + 1];
@@ -858,12 +881,12 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                 const int4 q6 = make_int4(__float_as_int(qc.z), __float_as_int(qc.w), __float_as_int(qd.x),
                                           __float_as_int(qd.y));
                 auto child = [&](int j, float& tn) {
-                    const float nx = fmaf(fmaf(byte_to_2p23(wn[0], j, magic), sc[0], pm[0]), r.ix, -r.lx);
-                    const float ny = fmaf(fmaf(byte_to_2p23(wn[1], j, magic), sc[1], pm[1]), r.iy, -r.ly);
-                    const float nz = fmaf(fmaf(byte_to_2p23(wn[2], j, magic), sc[2], pm[2]), r.iz, -r.lz);
-                    const float fx = fmaf(fmaf(byte_to_2p23(wf[0], j, magic), sc[0], pm[0]), r.ix, -r.hx);
-                    const float fy = fmaf(fmaf(byte_to_2p23(wf[1], j, magic), sc[1], pm[1]), r.iy, -r.hy);
-                    const float fz = fmaf(fmaf(byte_to_2p23(wf[2], j, magic), sc[2], pm[2]), r.iz, -r.hz);
+                    const float nx = fmaf(byte_to_2p15(wn[0], j, magic), sa[0], bn[0]);
+                    const float ny = fmaf(byte_to_2p15(wn[1], j, magic), sa[1], bn[1]);
+                    const float nz = fmaf(byte_to_2p15(wn[2], j, magic), sa[2], bn[2]);
+                    const float fx = fmaf(byte_to_2p15(wf[0], j, magic), sa[0], bf[0]);
+                    const float fy = fmaf(byte_to_2p15(wf[1], j, magic), sa[1], bf[1]);
+                    const float fz = fmaf(byte_to_2p15(wf[2], j, magic), sa[2], bf[2]);
                     tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, 0.0f));
                     const float tf = fminf(fminf(fx, fy), fminf(fz, tclip));
                     return ((vmask >> j) & 1u) != 0u && tn <= tf;
@@ -889,44 +912,33 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                         cas(k0, c0, k2, c2);
                     }
                 }
-                if constexpr (kBF) {
-                    // c0 is the nearest hit child (kSort) -- kNoRef only when none hit
-                    stk.push_if(sp, c3 != kNoRef, c3);
-                    stk.push_if(sp, c2 != kNoRef, c2);
-                    stk.push_if(sp, c1 != kNoRef, c1);
-                    int first = c0;
-                    if (first == kNoRef && sp > 0) first = stk.pop(sp);
-                    node = first >= 0 ? first : -1;
-                    if (first != kNoRef && first < 0) l0 = ~first;
-                } else {
-                int first = kNoRef;
-                if (c3 != kNoRef) first = c3;
-                if (c2 != kNoRef) {
-                    if (first != kNoRef) stk.push(sp, first);
-                    first = c2;
-                }
-                if (c1 != kNoRef) {
-                    if (first != kNoRef) stk.push(sp, first);
-                    first = c1;
-                }
-                if (c0 != kNoRef) {
-                    if (first != kNoRef) stk.push(sp, first);
-                    first = c0;
-                }
+                // c0 is the nearest hit child (kSort) -- kNoRef only when none hit
+                stk.push_if(sp, c3 != kNoRef, c3);
+                stk.push_if(sp, c2 != kNoRef, c2);
+                stk.push_if(sp, c1 != kNoRef, c1);
+                int first = c0;
                 if (first == kNoRef && sp > 0) first = stk.pop(sp);
-                if (first == kNoRef) {
-                    node = -1;
-                } else if (first >= 0) {
-                    node = first;
-                } else {
-                    l0 = ~first;
-                    node = -1;
+                if (first != kNoRef && first < 0) {  // a leaf
+                    if (l0 < 0) {
+                        l0 = ~first;
+                        // kQSpec: keep walking from the next stack entry while
+                        // the warp is still in the traversal phase
+                        first = (kQSpec && sp > 0) ? stk.pop(sp) : kNoRef;
+                        if (first != kNoRef && first < 0) {
+                            l1 = ~first;
+                            first = kNoRef;
+                        }
+                    } else {
+                        l1 = ~first;
+                        first = kNoRef;
+                    }
                 }
-                }
+                node = first >= 0 ? first : -1;
             }
         }
 
-        // ---- 3. leaf phase (up to two leaves in a row from the stack)
+        // ---- 3. leaf phase: the pending leaf (and the speculative one), then
+        // one more in a row if the next stack entry is a leaf
         if (kCounters) {
             const unsigned lm = __popc(__ballot_sync(FULL, l0 >= 0));
             if (lane == 0 && lm) {
@@ -935,10 +947,11 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
             }
         }
         if (l0 >= 0) {
-            if (kCounters) st.mts += 1;
+            if (kCounters) st.mts += 1 + (l1 >= 0);
             bool done = ms.template leaf<kFP64>(p, r, l0, tclip, st);
-            l0 = -1;
-            int nxt = (!done && sp > 0) ? stk.pop(sp) : kNoRef;
+            if (!done && l1 >= 0) done = ms.template leaf<kFP64>(p, r, l1, tclip, st);
+            l0 = l1 = -1;
+            int nxt = (!done && node < 0 && sp > 0) ? stk.pop(sp) : kNoRef;
             if (nxt != kNoRef && nxt < 0) {
                 if (kCounters) st.mts += 1;
                 done = ms.template leaf<kFP64>(p, r, ~nxt, tclip, st);
@@ -947,6 +960,8 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
             if (done) {
                 node = -1;
                 sp = 0;
+            } else if (node >= 0) {
+                // the speculative walk's position stays the next visit
             } else if (nxt == kNoRef) {
                 node = -1;
             } else if (nxt >= 0) {
@@ -1302,13 +1317,22 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     p.point = out->point;
     p.count = out->count;
     p.tau = h->opt.dedup_tau;
-    p.magic = 0x4B000000u;
+    p.magic = 0x47000000u;
+    // 4-wide walk: slack term and the |inv| range that keeps s * inv exact and
+    // every term of the folded decode far from overflow (see slab_axis)
+    p.qext = 0.25f * h->quad_pmax;
+    {
+        const double smin = ldexp(1.0, h->quad_emin), smax = ldexp(1.0, h->quad_emax);
+        p.qlim_lo = (float)(ldexp(1.0, -124) / smin);
+        p.qlim_hi = (float)(ldexp(1.0, 100) / ((double)h->quad_pmax + 65536.0 * smax));
+    }
     p.ovf_list = h->ovf_list;
     p.scratch = h->scratch;
     p.stats = h->stats;
     p.counter = reinterpret_cast<unsigned long long*>(h->scratch + SCR_DISPENSER);
     // traversal-phase exit threshold, measured per mode (env RSI_MIN_TRAV overrides)
-    p.min_trav = h->min_trav >= 0 ? h->min_trav : (mode == RSI_MODE_INTERCEPT_COUNT ? 8 : 16);
+    // measured per mode on the sphere / paper-terrain workloads
+    p.min_trav = h->min_trav >= 0 ? h->min_trav : (mode == RSI_MODE_BOOLEAN ? 16 : 8);
     const bool fp64 = (h->opt.flags & RSI_OPT_FP64_MOLLER) != 0, ctr = (h->opt.flags & RSI_OPT_COUNTERS) != 0;
     if (fp64)
         ctr ? launch_mode<true, true>(mode, p, s) : launch_mode<true, false>(mode, p, s);

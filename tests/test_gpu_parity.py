@@ -149,6 +149,26 @@ def test_sphere_all_modes(rsi, n_rays):
     assert_parity(got, ref, S, E, "sphere")
 
 
+@pytest.mark.parametrize("scale,shift", [(1e-20, 0.0), (1e-3, 0.0), (1.0, 3e4), (1e3, -1e6), (1e20, 1e21)])
+def test_scaled_translated_scenes(rsi, scale, shift):
+    """The 4-wide walk's folded slab (s*inv exact, slack ~ max|pm| |inv|) at
+    extreme mesh scales and offsets, with short, unit and very long segments:
+    decisions stay those of the oracle (the slab test only has to stay
+    conservative, the exact tests decide)."""
+    V, T, S, E, _ = synth.workload("sphere", 6000, seed=11)
+    rng = np.random.default_rng(11)
+    d = E - S
+    f = np.float32(10.0) ** rng.integers(-6, 7, size=(len(S), 1)).astype(np.float32)
+    E = (S + d * f).astype(np.float32)  # segment lengths from 1e-6 to 1e6 x
+    V = (V.astype(np.float64) * scale + shift).astype(np.float32)
+    S = (S.astype(np.float64) * scale + shift).astype(np.float32)
+    E = (E.astype(np.float64) * scale + shift).astype(np.float32)
+    ref = oracle.run(V, T, S, E)
+    got = run_all(rsi, V, T, S, E)
+    assert_parity(got, ref, S, E, f"scale={scale},shift={shift}")
+    assert got["hit"].sum() > 100
+
+
 def test_folded_terrain_intercept_count(rsi):
     V, T, S, E, _ = synth.workload("terrain", 6000)
     ref = oracle.run(V, T, S, E)

@@ -27,11 +27,11 @@ constexpr float kSlack = 4.76837158203125e-07f;  // 2^-21: slab-test slack facto
 constexpr float kTiny = 1e-30f;                  // absolute floor (underflow)
 constexpr float kOutTol = 4e-6f;                 // max certified |t error| for fp32 outputs
 // Per-mode traversal configuration.  Measured on B200 (round 1, same box A/B):
-// boolean and barycentric walk the compressed 4-wide grandchild records (64 B,
-// 8-bit quantized boxes: half the L1 wavefronts of the binary child-pair walk,
-// which was L1-data-pipe bound at 87 %); intercept_count walks the binary
-// child-pair nodes with speculative traversal (7 % faster on the sphere, equal
-// on the folded terrain).  Shared-memory stacks stay a build option.
+// all three modes walk the compressed 4-wide grandchild records (64 B, 8-bit
+// quantized boxes: half the L1 wavefronts of the binary child-pair walk, which
+// was L1-data-pipe bound at 87 %) with a branch-free lane stack; once the quad
+// visit was cheap, intercept_count also gained (-12 % sphere, -18 % terrain vs
+// the binary walk with speculation).  The binary walk stays a build option.
 #ifndef RSI_BOOL_QUAD
 #define RSI_BOOL_QUAD 1
 #endif
@@ -39,7 +39,7 @@ constexpr float kOutTol = 4e-6f;                 // max certified |t error| for 
 #define RSI_BARY_QUAD 1
 #endif
 #ifndef RSI_COUNT_QUAD
-#define RSI_COUNT_QUAD 0
+#define RSI_COUNT_QUAD 1
 #endif
 #ifndef RSI_BOOL_SMEM
 #define RSI_BOOL_SMEM 0
@@ -51,10 +51,14 @@ constexpr float kOutTol = 4e-6f;                 // max certified |t error| for 
 #define RSI_COUNT_SMEM 0
 #endif
 #define RSI_ANY_QUAD (RSI_BOOL_QUAD || RSI_BARY_QUAD || RSI_COUNT_QUAD)
+constexpr bool kQuadCount = RSI_COUNT_QUAD;
 // speculative walk on the 4-wide records (a lane with a pending leaf keeps
 // walking): measured -2..-4 % barycentric, +3..5 % boolean (round 1)
 #ifndef RSI_QSPEC_BOOL
 #define RSI_QSPEC_BOOL 0
+#endif
+#ifndef RSI_QSPEC_COUNT
+#define RSI_QSPEC_COUNT 0
 #endif
 #ifndef RSI_QSPEC_BARY
 #define RSI_QSPEC_BARY 1
@@ -745,7 +749,8 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
     // near-first child order: needed for nearest-hit culling, helps any-hit exit; useless for counts
-    constexpr bool kSort = (MODE == MODE_BARY) || (MODE == MODE_BOOL && RSI_SORT_ALL);
+    constexpr bool kSort = (MODE == MODE_BARY) || (MODE == MODE_BOOL && RSI_SORT_ALL) ||
+                           (MODE == MODE_COUNT && kQuadCount);  // (4-wide: puts a hit child first)
     constexpr bool kQuad = MODE == MODE_BOOL ? RSI_BOOL_QUAD : (MODE == MODE_BARY ? RSI_BARY_QUAD : RSI_COUNT_QUAD);
     constexpr int kSmemStack = MODE == MODE_BOOL ? RSI_BOOL_SMEM : (MODE == MODE_BARY ? RSI_BARY_SMEM : RSI_COUNT_SMEM);
     constexpr int kStack = kQuad ? kStackQuad : kStackBinary;
@@ -767,7 +772,7 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
     int node = -1, sp = 0, l0 = -1, l1 = -1, l2 = -1;  // pending (postponed) leaf slots
     // per-lane traversal stack: the first kSmemStack entries in a shared-memory
     // column (one bank per lane: conflict-free at any depth), the rest local
-    constexpr bool kQSpec = MODE == MODE_BOOL ? RSI_QSPEC_BOOL : RSI_QSPEC_BARY;
+    constexpr bool kQSpec = MODE == MODE_BOOL ? RSI_QSPEC_BOOL : (MODE == MODE_BARY ? RSI_QSPEC_BARY : RSI_QSPEC_COUNT);
     constexpr bool kBF = kQuad;  // branch-free stack on the 4-wide walk (-11 % boolean, -5 % barycentric)
     constexpr int kSmWords = kBF ? RSI_BF_SMEM : kSmemStack;
     typename std::conditional<kBF, BFStack<kStack, RSI_BF_SMEM, kT>, LaneStack<kStack, kSmemStack, kT>>::type stk;
@@ -1332,7 +1337,8 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     p.counter = reinterpret_cast<unsigned long long*>(h->scratch + SCR_DISPENSER);
     // traversal-phase exit threshold, measured per mode (env RSI_MIN_TRAV overrides)
     // measured per mode on the sphere / paper-terrain workloads
-    p.min_trav = h->min_trav >= 0 ? h->min_trav : (mode == RSI_MODE_BOOLEAN ? 16 : 8);
+    p.min_trav = h->min_trav >= 0 ? h->min_trav
+                                  : (mode == RSI_MODE_BOOLEAN ? 16 : (mode == RSI_MODE_BARYCENTRIC ? 8 : 12));
     const bool fp64 = (h->opt.flags & RSI_OPT_FP64_MOLLER) != 0, ctr = (h->opt.flags & RSI_OPT_COUNTERS) != 0;
     if (fp64)
         ctr ? launch_mode<true, true>(mode, p, s) : launch_mode<true, false>(mode, p, s);

@@ -60,6 +60,14 @@ typedef enum {
                                   are identical either way; only speed differs. */
 #define RSI_OPT_COUNTERS 2u    /* count box tests and Moller-Trumbore tests in rsi_stats_t
                                   (instrumented kernels; for roofline accounting, slower). */
+#define RSI_OPT_DEFERRED_STATUS 4u /* rsi_build / rsi_rebuild only enqueue the build and
+                                  return RSI_OK without waiting for the device; the
+                                  device-side input checks (index range, non-finite
+                                  vertex, extent) are reported by rsi_build_status, which
+                                  synchronizes.  Until it returns RSI_OK the outputs of an
+                                  rsi_intersect on an invalid mesh are unspecified (no
+                                  out-of-bounds access either way).  For pipelines that
+                                  rebuild and query every step with no host round trip. */
 
 typedef struct {
     uint32_t struct_size; /* sizeof(rsi_options_t); 0 or a NULL options pointer = defaults   */
@@ -227,6 +235,13 @@ rsi_status_t rsi_free(rsi_handle_t h);
  * tree, RSI_E_INTEGRITY when any count is non-zero or the root is unset.
  */
 rsi_status_t rsi_validate(rsi_handle_t h, rsi_integrity_t* report, void* stream);
+
+/* Result of the device-side input checks of the last rsi_build / rsi_rebuild
+ * of `h` (the status rsi_build itself returns without RSI_OPT_DEFERRED_STATUS):
+ * RSI_OK, RSI_E_INDEX_RANGE, RSI_E_NONFINITE or RSI_E_INVALID_ARG (extent).
+ * Synchronizes `stream` when the result is still pending; an error leaves `h`
+ * without a mesh (like a failed rsi_rebuild). */
+rsi_status_t rsi_build_status(rsi_handle_t h, void* stream);
 
 /* Read the cumulative counters of `h`; synchronizes `stream`. */
 rsi_status_t rsi_get_stats(rsi_handle_t h, rsi_stats_t* out, void* stream);

@@ -36,7 +36,7 @@ static rsi_status_t read_options(const rsi_options_t* in, rsi_options_t* out) {
     if (in->struct_size != sizeof(rsi_options_t))
         return rsi_set_error(RSI_E_INVALID_ARG, "rsi_options_t.struct_size %u != %zu", in->struct_size,
                              sizeof(rsi_options_t));
-    if (in->flags & ~(RSI_OPT_FP64_MOLLER | RSI_OPT_COUNTERS)) return rsi_set_error(RSI_E_INVALID_ARG, "unknown option flags 0x%x", in->flags);
+    if (in->flags & ~(RSI_OPT_FP64_MOLLER | RSI_OPT_COUNTERS | RSI_OPT_DEFERRED_STATUS)) return rsi_set_error(RSI_E_INVALID_ARG, "unknown option flags 0x%x", in->flags);
     if (!(in->dedup_tau >= 0.0)) return rsi_set_error(RSI_E_INVALID_ARG, "dedup_tau must be >= 0");
     if (in->debug_refit_leaves < 0) return rsi_set_error(RSI_E_INVALID_ARG, "debug_refit_leaves must be >= 0");
     *out = *in;
@@ -375,13 +375,16 @@ rsi_status_t rsi_free(rsi_handle_t h) {
             rsi_status_t e = rsi_cuda_check(cudaFreeAsync(p, s), "cudaFreeAsync");
             if (st == RSI_OK) st = e;
         }
-    if (h->tex_nodes) cudaDestroyTextureObject(h->tex_nodes);
     delete h;
     return st;
 }
 
 rsi_status_t rsi_validate(rsi_handle_t h, rsi_integrity_t* report, void* stream) {
     if (!h || !report) return rsi_set_error(RSI_E_INVALID_ARG, "null argument");
+    if (h->status_pending) {
+        const rsi_status_t st0 = rsi_finish_build(h, (cudaStream_t)stream);
+        if (st0 != RSI_OK) return st0;
+    }
     if (h->n_tri <= 0) return rsi_set_error(RSI_E_INVALID_ARG, "handle holds no mesh");
     rsi_status_t st = rsi_validate_device(h, report, (cudaStream_t)stream);
     if (st != RSI_OK) return st;
@@ -427,8 +430,17 @@ rsi_status_t rsi_reset_stats(rsi_handle_t h, void* stream) {
                           "reset stats");
 }
 
+rsi_status_t rsi_build_status(rsi_handle_t h, void* stream) {
+    if (!h) return rsi_set_error(RSI_E_INVALID_ARG, "null handle");
+    return rsi_finish_build(h, (cudaStream_t)stream);
+}
+
 rsi_status_t rsi_bvh_info(rsi_handle_t h, int64_t* n_triangles, int64_t* n_nodes, float* lo3, float* hi3) {
     if (!h) return rsi_set_error(RSI_E_INVALID_ARG, "null handle");
+    if (h->status_pending) {  // deferred build: the scene box is read back now
+        const rsi_status_t st = rsi_finish_build(h, h->stream);
+        if (st != RSI_OK) return st;
+    }
     if (n_triangles) *n_triangles = h->n_tri;
     if (n_nodes) *n_nodes = h->n_nodes;
     for (int k = 0; k < 3; ++k) {
@@ -441,8 +453,12 @@ rsi_status_t rsi_bvh_info(rsi_handle_t h, int64_t* n_triangles, int64_t* n_nodes
 rsi_status_t rsi_bvh_download(rsi_handle_t h, int32_t* h_child, float* h_box, int32_t* h_leaf_tri,
                               uint32_t* h_morton, int32_t* h_parent, uint32_t* h_arrivals, void* stream) {
     if (!h) return rsi_set_error(RSI_E_INVALID_ARG, "null handle");
-    if (h->n_tri <= 0) return rsi_set_error(RSI_E_INVALID_ARG, "handle holds no mesh");
     cudaStream_t s = (cudaStream_t)stream;
+    if (h->status_pending) {
+        const rsi_status_t st0 = rsi_finish_build(h, s);
+        if (st0 != RSI_OK) return st0;
+    }
+    if (h->n_tri <= 0) return rsi_set_error(RSI_E_INVALID_ARG, "handle holds no mesh");
     const int64_t nn = h->n_nodes, nt = h->n_tri;
     rsi_status_t st = RSI_OK;
     float4* nodes = nullptr;

@@ -33,6 +33,7 @@ __global__ void k_build_init(uint32_t* scratch) {
         scratch[SCR_QEMIN] = 0xffffffffu;
         scratch[SCR_QEMAX] = 0u;
     }
+    if (i < 32) scratch[SCR_SORT_DONE + i] = 0u;
 }
 
 __device__ __forceinline__ float warp_min(float v) {
@@ -127,10 +128,12 @@ __global__ void __launch_bounds__(kBlock) k_morton(const float* __restrict__ V, 
                                                    const int32_t* __restrict__ T, int n,
                                                    const uint32_t* __restrict__ scratch,
                                                    uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
-                                                   uint32_t* __restrict__ arrivals, int n_nodes) {
+                                                   uint32_t* __restrict__ arrivals, int n_nodes,
+                                                   uint32_t* __restrict__ rank) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     if (j < n_nodes) arrivals[j] = 0u;
+    if (rank) rank[j] = 0u;  // rank-sort accumulators (N_t <= kRankSortMax)
     float lo[3], hi[3];
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -458,6 +461,8 @@ __global__ void __launch_bounds__(kBlock) k_refit(const float* __restrict__ V, i
         const int node = p >> 1, side = p & 1;
         write_slot(nodes, node, side, lo, hi);
         if (n == 1) break;
+        // the next parent link is read-only: fetch it before the arrival
+        const int32_t p_next = node > 0 ? __ldg(parent + node) : -1;
         // acq_rel arrival: releases this child's box, acquires the sibling's
         uint32_t old;
         asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(arrivals + node) : "memory");
@@ -472,7 +477,7 @@ __global__ void __launch_bounds__(kBlock) k_refit(const float* __restrict__ V, i
         lo[2] = fminf(lo[2], __ldcg(f + 8 + 2 * (1 - side)));
         hi[2] = fmaxf(hi[2], __ldcg(f + 9 + 2 * (1 - side)));
         if (node == 0) break;
-        p = parent[node];
+        p = p_next;
     }
     // root box (scene AABB) for rsi_bvh_info
     float* root = reinterpret_cast<float*>(scratch + SCR_ROOT);
@@ -531,6 +536,76 @@ __global__ void __launch_bounds__(kSmallThreads) k_sort_smem(uint32_t* gk, int32
     for (int j = tid; j < n; j += kSmallThreads) {
         gk[j] = ka[j];
         gv[j] = va[j];
+    }
+}
+
+// Small meshes (N_t <= kRankSortMax): the sorted position of key i is its rank
+//   r(i) = #{ j : k_j < k_i  or  (k_j == k_i and j < i) }
+// (a stable sort by construction), counted directly: CTA (bx, by) compares its
+// kRankI keys against key slice `by` held in shared memory and adds the partial
+// counts to rank[i] with atomics; the last slice CTA of block bx (a per-block
+// counter, after a fence) scatters keys and indices.  O(N^2) compares spread
+// over the whole GPU (~1e8 at N = 1e4: a few microseconds) instead of four
+// dependent radix passes on one SM.  For a slice wholly below block bx's keys
+// "j < i" holds for every pair, so the test is k_j < k_i + 1; wholly above, k_j < k_i.
+constexpr int kRankSortMax = 16384;
+constexpr int kRankT = 256, kRankPer = 2, kRankI = kRankT * kRankPer;
+
+__global__ void __launch_bounds__(kRankT) k_sort_rank(const uint32_t* __restrict__ keys, int n, int slice,
+                                                      uint32_t* rank, uint32_t* __restrict__ out_keys,
+                                                      int32_t* __restrict__ out_vals, uint32_t* done) {
+    extern __shared__ uint4 s_k4[];
+    uint32_t* s_k = reinterpret_cast<uint32_t*>(s_k4);
+    const int tid = threadIdx.x;
+    const int j0 = blockIdx.y * slice, j1 = min(j0 + slice, n);
+    const int nj = j1 > j0 ? j1 - j0 : 0;
+    const int nj4 = (nj + 3) >> 2;
+    for (int j = tid; j < 4 * nj4; j += kRankT) s_k[j] = j < nj ? keys[j0 + j] : 0xffffffffu;  // pad: > every key
+    __syncthreads();
+    const int i_lo = blockIdx.x * kRankI, i_hi = min(i_lo + kRankI, n);
+    int idx[kRankPer];
+    uint32_t ki[kRankPer], cnt[kRankPer];
+#pragma unroll
+    for (int a = 0; a < kRankPer; ++a) {
+        idx[a] = i_lo + tid + a * kRankT;
+        ki[a] = idx[a] < n ? keys[idx[a]] : 0u;
+        cnt[a] = 0u;
+    }
+    if (j1 <= i_lo || j0 >= i_hi) {  // slice wholly below / above this block's keys
+        const uint32_t add = j1 <= i_lo ? 1u : 0u;
+        uint32_t thr[kRankPer];
+#pragma unroll
+        for (int a = 0; a < kRankPer; ++a) thr[a] = ki[a] + add;
+        for (int q = 0; q < nj4; ++q) {
+            const uint4 k4 = s_k4[q];
+#pragma unroll
+            for (int a = 0; a < kRankPer; ++a)
+                cnt[a] += (k4.x < thr[a]) + (k4.y < thr[a]) + (k4.z < thr[a]) + (k4.w < thr[a]);
+        }
+    } else {  // overlapping (diagonal) slice: per-pair index test
+        for (int j = 0; j < nj; ++j) {
+            const uint32_t kj = s_k[j];
+#pragma unroll
+            for (int a = 0; a < kRankPer; ++a) cnt[a] += (kj < ki[a] + (j0 + j < idx[a] ? 1u : 0u));
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < kRankPer; ++a)
+        if (idx[a] < n && cnt[a]) atomicAdd(rank + idx[a], cnt[a]);
+    __threadfence();
+    __syncthreads();
+    __shared__ bool s_last;
+    if (tid == 0) s_last = atomicAdd(done + blockIdx.x, 1u) == gridDim.y - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+#pragma unroll
+    for (int a = 0; a < kRankPer; ++a) {
+        if (idx[a] < n) {
+            const uint32_t r = __ldcg(rank + idx[a]);
+            out_keys[r] = ki[a];
+            out_vals[r] = idx[a];
+        }
     }
 }
 
@@ -630,7 +705,8 @@ __global__ void __launch_bounds__(1024) k_topk(const float4* __restrict__ nodes,
 // computed in double; |p/s| < 2^24 keeps p + q*s exactly representable, so the
 // traversal's decode is exact, and directed rounding keeps it conservative
 // otherwise).  64 B per record = two 256-bit loads.
-//   w0..w2  p.x, p.y, p.z (float)        w3  e_x+128 | e_y+128<<8 | e_z+128<<16 | valid<<24
+//   w0..w2  pm = p - 2^15 s per axis (float, the traversal's decode offset)
+//           w3  e_x+128 | e_y+128<<8 | e_z+128<<16 | valid<<24
 //   w4..w9  qlo.x, qhi.x, qlo.y, qhi.y, qlo.z, qhi.z   (byte j = child j)
 //   w10..w13 ref[0..3]                   w14, w15 unused
 constexpr int kQuadEMin = -126, kQuadEMax = 104;  // s and s*2^23 stay normal floats
@@ -650,18 +726,19 @@ __device__ __forceinline__ void quant_axis(const float* lo, const float* hi, int
         e = ex - 1;
         if (e < kQuadEMin) e = kQuadEMin;
     }
-    double sc, p;
+    double sc, isc, p;  // s = 2^e and 1/s (exact), so x * isc == x / s exactly
     while (true) {
         sc = ldexp(1.0, e);
-        p = floor((double)nlo / sc) * sc;  // multiple of s, p <= nlo
+        isc = ldexp(1.0, -e);
+        p = floor((double)nlo * isc) * sc;  // multiple of s, p <= nlo
         // covers the node, and p = k*s with |k| < 2^23 so p and p - 2^15 s are exact floats
-        if (((double)nhi - p <= 255.0 * sc && fabs(p / sc) < 8388608.0) || e >= kQuadEMax) break;
+        if (((double)nhi - p <= 255.0 * sc && fabs(p * isc) < 8388608.0) || e >= kQuadEMax) break;
         ++e;
     }
     wlo = 0u;
     whi = 0u;
     for (int j = 0; j < cnt; ++j) {
-        double ql = floor(((double)lo[j] - p) / sc), qh = ceil(((double)hi[j] - p) / sc);
+        double ql = floor(((double)lo[j] - p) * isc), qh = ceil(((double)hi[j] - p) * isc);
         ql = fmin(fmax(ql, 0.0), 255.0);
         qh = fmin(fmax(qh, 0.0), 255.0);
         wlo |= (uint32_t)ql << (8 * j);
@@ -669,7 +746,7 @@ __device__ __forceinline__ void quant_axis(const float* lo, const float* hi, int
     }
     p_out = (float)(p - 32768.0 * sc);  // the decode offset p - 2^15 s: exact (|p/s - 2^15| < 2^24)
     e_out = e;
-    ok = ((double)nhi - p <= 255.0 * sc) && fabs(p / sc) < 8388608.0 && (double)p_out == p - 32768.0 * sc;
+    ok = ((double)nhi - p <= 255.0 * sc) && fabs(p * isc) < 8388608.0 && (double)p_out == p - 32768.0 * sc;
 }
 
 __global__ void __launch_bounds__(kBlock) k_quads(const float4* __restrict__ nodes, int n_nodes,
@@ -846,6 +923,21 @@ static rsi_status_t ensure_capacity(rsi_bvh* h, int64_t n, cudaStream_t s) {
 }
 
 static void launch_sort(rsi_bvh* h, int n, cudaStream_t s) {
+    if (n <= kRankSortMax) {
+        // rank sort: keys -> keys_tmp (then swapped into h->keys), indices -> vals
+        const int bx = rsi_ceil_div(n, kRankI);
+        int sy = rsi_ceil_div(148 * 3, bx);
+        if (sy > 64) sy = 64;
+        int slice = (rsi_ceil_div(n, sy) + 3) & ~3;
+        sy = rsi_ceil_div(n, slice);
+        rsi_note_launch(), k_sort_rank<<<dim3(bx, sy), kRankT, (size_t)slice * 4, s>>>(
+            h->keys, n, slice, reinterpret_cast<uint32_t*>(h->vals_tmp), h->keys_tmp, h->vals,
+            h->scratch + SCR_SORT_DONE);
+        uint32_t* t = h->keys;
+        h->keys = h->keys_tmp;
+        h->keys_tmp = t;
+        return;
+    }
     if (n <= kSmemSortMax) {
         static bool attr = false;
         if (!attr) {
@@ -887,7 +979,7 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
     if (eb > 148 * 8) eb = 148 * 8;
     rsi_note_launch(), k_extent_validate<<<eb, kBlock, 0, s>>>(V, nv, T, nt, h->scratch);
     rsi_note_launch(), k_morton<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, n, h->scratch, h->keys, h->vals, h->arrivals,
-                                                         n_nodes);
+                                                         n_nodes, n <= kRankSortMax ? reinterpret_cast<uint32_t*>(h->vals_tmp) : nullptr);
     launch_sort(h, n, s);
     rsi_note_launch(), k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent, h->arrivals);
     // the refit grid covers every leaf (case study 2: never size it from another
@@ -900,50 +992,42 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
     if (rsi_uses_quads()) rsi_note_launch(), k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads, h->scratch);
     st = rsi_cuda_check(cudaGetLastError(), "build kernel launch");
     if (st != RSI_OK) return st;
-    st = rsi_cuda_check(cudaMemcpyAsync(h->h_words, h->scratch, SCR_WORDS * sizeof(uint32_t),
-                                        cudaMemcpyDeviceToHost, s),
-                        "status read");
-    if (st != RSI_OK) return st;
-    st = rsi_cuda_check(cudaStreamSynchronize(s), "build");
-    if (st != RSI_OK) return st;
-    uint32_t status = h->h_words[SCR_STATUS];
-    if (status & STATUS_INDEX) return rsi_set_error(RSI_E_INDEX_RANGE, "a triangle index is outside [0, %lld)", (long long)nv);
-    if (status & STATUS_NONFINITE) return rsi_set_error(RSI_E_NONFINITE, "a vertex coordinate is NaN or Inf");
-    if (status & STATUS_RANGE)
-        return rsi_set_error(RSI_E_INVALID_ARG, "mesh extent too large for the quantized BVH (|coordinates| > ~1e33)");
-    memcpy(&h->quad_pmax, &h->h_words[SCR_QPMAX], sizeof(float));
-    h->quad_emin = (int)h->h_words[SCR_QEMIN] - 128;
-    h->quad_emax = (int)h->h_words[SCR_QEMAX] - 128;
+    h->n_tri = nt;
+    h->n_nodes = n_nodes;
+    h->stream = s;
+    h->pending_nv = nv;
+    h->status_pending = true;
+    if (h->opt.flags & RSI_OPT_DEFERRED_STATUS) return RSI_OK;  // checked by rsi_build_status
+    return rsi_finish_build(h, s);
+}
+
+// Read back the build's scratch words (status bits, scene box) and report the
+// device-side input checks; an invalid mesh leaves the handle without a mesh.
+rsi_status_t rsi_finish_build(rsi_bvh* h, cudaStream_t s) {
+    if (!h->status_pending) return h->n_tri > 0 ? RSI_OK : rsi_set_error(RSI_E_INVALID_ARG, "handle holds no mesh");
+    h->status_pending = false;
+    rsi_status_t st = rsi_cuda_check(cudaMemcpyAsync(h->h_words, h->scratch, SCR_WORDS * sizeof(uint32_t),
+                                                     cudaMemcpyDeviceToHost, s),
+                                     "status read");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaStreamSynchronize(s), "build");
+    const uint32_t status = st == RSI_OK ? h->h_words[SCR_STATUS] : 0u;
+    if (st == RSI_OK && (status & STATUS_INDEX))
+        st = rsi_set_error(RSI_E_INDEX_RANGE, "a triangle index is outside [0, %lld)", (long long)h->pending_nv);
+    else if (st == RSI_OK && (status & STATUS_NONFINITE))
+        st = rsi_set_error(RSI_E_NONFINITE, "a vertex coordinate is NaN or Inf");
+    else if (st == RSI_OK && (status & STATUS_RANGE))
+        st = rsi_set_error(RSI_E_INVALID_ARG, "mesh extent too large for the quantized BVH (|coordinates| > ~1e33)");
+    if (st != RSI_OK) {
+        h->n_tri = 0;
+        h->n_nodes = 0;
+        return st;
+    }
     const float* root = reinterpret_cast<const float*>(h->h_words + SCR_ROOT);
     for (int x = 0; x < 3; ++x) {
         h->scene_lo[x] = root[x];
         h->scene_hi[x] = root[3 + x];
     }
-#ifdef RSI_TEX_NODES_BUILD
-    // texture view of the nodes (only for the RSI_TEX_NODES traversal experiment;
-    // texture-object creation per build is not free)
-    if (h->tex_nodes) {
-        cudaDestroyTextureObject(h->tex_nodes);
-        h->tex_nodes = 0;
-    }
-    {
-        cudaResourceDesc rd{};
-        rd.resType = cudaResourceTypeLinear;
-        rd.res.linear.devPtr = h->nodes;
-        rd.res.linear.desc = cudaCreateChannelDesc<float4>();
-        rd.res.linear.sizeInBytes = (size_t)n_nodes * 4 * sizeof(float4);
-        cudaTextureDesc td{};
-        td.readMode = cudaReadModeElementType;
-        if (cudaCreateTextureObject(&h->tex_nodes, &rd, &td, nullptr) != cudaSuccess) {
-            (void)cudaGetLastError();
-            h->tex_nodes = 0;
-        }
-    }
-#endif
     h->n_top = kTopNodes > 0 ? (int)h->h_words[SCR_NTOP] : 0;
-    h->n_tri = nt;
-    h->n_nodes = n_nodes;
-    h->stream = s;
     return RSI_OK;
 }
 

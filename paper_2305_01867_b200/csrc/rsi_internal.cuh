@@ -37,7 +37,8 @@ enum {
     SCR_QPMAX = 22,     // max |decode offset| over the quad records (float bits, >= 0)
     SCR_QEMIN = 23,     // min / max grid exponent + 128 over the quad records
     SCR_QEMAX = 24,
-    SCR_WORDS = 32
+    SCR_SORT_DONE = 32, // 32 words: per-block slice counters of the rank sort
+    SCR_WORDS = 64
 };
 enum { STATUS_INDEX = 1u, STATUS_NONFINITE = 2u, STATUS_RANGE = 4u };
 
@@ -58,7 +59,6 @@ struct rsi_bvh {
     int64_t sort_blocks_cap = 0;
     float4* nodes = nullptr;         // [4 * n_nodes]
     float4* quads = nullptr;         // [4 * n_nodes] compressed grandchild (4-wide) records
-    cudaTextureObject_t tex_nodes = 0;  // texture view of `nodes` (recreated on rebuild)
     float4* top = nullptr;           // [4 * kTopNodes] top-of-tree image (refs >= kSmemRef are image slots)
     int n_top = 0;
     float4* tris = nullptr;          // [4 * n_tri]
@@ -77,8 +77,8 @@ struct rsi_bvh {
     int32_t* ovf_list = nullptr;     // ray ids
     int64_t ovf_cap = 0;
     float scene_lo[3] = {0, 0, 0}, scene_hi[3] = {0, 0, 0};
-    float quad_pmax = 0.0f;          // SCR_QPMAX after the build (slab slack of the 4-wide walk)
-    int quad_emin = 0, quad_emax = 0;  // SCR_QEMIN / SCR_QEMAX - 128
+    bool status_pending = false;     // build checks not yet read back (RSI_OPT_DEFERRED_STATUS)
+    int64_t pending_nv = 0;          // n_vertices of that build (error message)
     uint64_t host_rays = 0, host_overflow = 0;  // counters known on the host
     int min_trav = -1;  // traversal-phase exit threshold (-1: per-mode default); env RSI_MIN_TRAV
 };
@@ -99,6 +99,7 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* d_start, const float*
 bool rsi_uses_quads();  // traverse.cu: does any mode walk the 4-wide records
 // process-wide count of kernels this library launched (rsi_launch_count)
 void rsi_note_launch();
+rsi_status_t rsi_finish_build(rsi_bvh* h, cudaStream_t stream);  // build.cu: read back + check
 rsi_status_t rsi_validate_device(rsi_bvh* h, rsi_integrity_t* report, cudaStream_t stream);  // build.cu
 rsi_status_t rsi_compact_device(const int32_t* d_tri, int64_t n_rays, int32_t* d_ids,
                                 int32_t* d_n, cudaStream_t stream);

@@ -267,9 +267,6 @@ __device__ __noinline__ int mt64(const Ray& r, const float4 A, const float4 B, c
     return (nu >= 0.0) && (nv >= 0.0) && (da(nu, nv) <= det) && (nt >= 0.0) && (nt <= det);
 }
 
-#ifndef RSI_TEX_NODES
-#define RSI_TEX_NODES 0
-#endif
 #ifndef RSI_SPEC
 #define RSI_SPEC 1
 #endif
@@ -373,7 +370,6 @@ enum { MODE_BOOL = 0, MODE_BARY = 1, MODE_COUNT = 2 };
 
 struct TraceParams {
     const float4* nodes;
-    cudaTextureObject_t tex_nodes;  // same array through the texture path (RSI_TEX_NODES)
     const float4* quads;
     const float4* top;   // top-of-tree image [4 * n_top]
     int n_top;
@@ -394,8 +390,6 @@ struct TraceParams {
     unsigned long long* counter;  // persistent-grid ray dispenser
     int min_trav;           // leave the traversal phase when fewer lanes still search
     uint32_t magic;         // 0x47000000 (float 2^15)
-    float qext;             // 4-wide walk: slack term Pmax / 4 (see slab_axis)
-    float qlim_lo, qlim_hi; // 4-wide walk: |inv| range with exact s * inv and no overflow
 };
 
 template <int MODE>
@@ -789,6 +783,18 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
     // 0x4B000000 (float 2^23) from a kernel parameter: an opaque register, so the
     // quad decode's PRMTs keep their byte selectors as immediates
     const uint32_t magic = p.magic;
+    // 4-wide walk: slack term Pmax / 4 and the |inv| range that keeps s * inv an
+    // exact normal float and every term of the folded decode far from overflow
+    // (slab_axis), from the build's scratch words -- read here on the device, so
+    // rsi_intersect needs no host read-back of the build
+    float qext = 0.0f, qlim_lo = 0.0f, qlim_hi = INFINITY;
+    if constexpr (kQuad) {
+        const float pmax = __uint_as_float(p.scratch[SCR_QPMAX]);
+        const int emin = (int)p.scratch[SCR_QEMIN] - 128, emax = (int)p.scratch[SCR_QEMAX] - 128;
+        qext = 0.25f * pmax;
+        qlim_lo = scalbnf(1.0f, -124 - emin);
+        qlim_hi = scalbnf(1.0f, 100) / (pmax + scalbnf(65536.0f, emax));
+    }
     while (true) {
         // ---- 1. refill
         unsigned want = __ballot_sync(FULL, ray < 0);
@@ -818,7 +824,7 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
         }
         if (fresh) {
             bool nonfinite;
-            const bool ok = kQuad ? load_ray<true>(r, p.S, p.E, ray, nonfinite, p.qext, p.qlim_lo, p.qlim_hi)
+            const bool ok = kQuad ? load_ray<true>(r, p.S, p.E, ray, nonfinite, qext, qlim_lo, qlim_hi)
                                   : load_ray<false>(r, p.S, p.E, ray, nonfinite);
             if (nonfinite) st.add(ST_NONFINITE);
             ms.init();
@@ -998,12 +1004,6 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
             // RSI_SPEC: a lane holding one pending leaf keeps walking in slots it
             // would otherwise idle in (its new leaves queue in l1, l2)
             if (trav || (RSI_SPEC && node >= 0 && l1 < 0)) {
-#if RSI_TEX_NODES
-                const float4 n0 = tex1Dfetch<float4>(p.tex_nodes, 4 * node);
-                const float4 n1 = tex1Dfetch<float4>(p.tex_nodes, 4 * node + 1);
-                const float4 n2 = tex1Dfetch<float4>(p.tex_nodes, 4 * node + 2);
-                const float4 n3f = tex1Dfetch<float4>(p.tex_nodes, 4 * node + 3);
-#else
                 float4 n0, n1, n2, n3f;
                 if (node >= (int)kSmemRef) {  // cached top of the tree
                     const float4* sn = s_top + 4 * (node - (int)kSmemRef);
@@ -1016,7 +1016,6 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                     ldg256(nd, n0, n1);
                     ldg256(nd + 2, n2, n3f);
                 }
-#endif
                 const int4 n3 = make_int4(__float_as_int(n3f.x), __float_as_int(n3f.y), 0, 0);
                 float nearL, nearR;
                 bool hL = slab(r, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, tclip, nearL);
@@ -1307,7 +1306,6 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     if (st != RSI_OK) return st;
     TraceParams p{};
     p.nodes = h->nodes;
-    p.tex_nodes = h->tex_nodes;
     p.quads = h->quads;
     p.top = h->top;
     p.n_top = kTopNodes > 0 ? h->n_top : 0;
@@ -1323,14 +1321,6 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     p.count = out->count;
     p.tau = h->opt.dedup_tau;
     p.magic = 0x47000000u;
-    // 4-wide walk: slack term and the |inv| range that keeps s * inv exact and
-    // every term of the folded decode far from overflow (see slab_axis)
-    p.qext = 0.25f * h->quad_pmax;
-    {
-        const double smin = ldexp(1.0, h->quad_emin), smax = ldexp(1.0, h->quad_emax);
-        p.qlim_lo = (float)(ldexp(1.0, -124) / smin);
-        p.qlim_hi = (float)(ldexp(1.0, 100) / ((double)h->quad_pmax + 65536.0 * smax));
-    }
     p.ovf_list = h->ovf_list;
     p.scratch = h->scratch;
     p.stats = h->stats;

@@ -24,6 +24,7 @@ from . import _build
 MODES = {"boolean": 0, "barycentric": 1, "intercept_count": 2}
 OPT_FP64_MOLLER = 1
 OPT_COUNTERS = 2
+OPT_DEFERRED_STATUS = 4
 
 _lock = threading.Lock()
 _lib = None
@@ -88,6 +89,7 @@ def load():
             "rsi_free": ([_p], ctypes.c_int),
             "rsi_release_cache": ([], None),
             "rsi_get_stats": ([_p, ctypes.POINTER(_Stats), _p], ctypes.c_int),
+            "rsi_build_status": ([_p, _p], ctypes.c_int),
             "rsi_reset_stats": ([_p, _p], ctypes.c_int),
             "rsi_bvh_info": ([_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _p, _p], ctypes.c_int),
             "rsi_bvh_download": ([_p, _p, _p, _p, _p, _p, _p, _p], ctypes.c_int),
@@ -141,9 +143,11 @@ class Options:
     dedup_tau: float = 1e-6     # reading R4
     counters: bool = False      # instrumented kernels: box / MT test counts in rsi_get_stats
     debug_refit_leaves: int = 0  # FAULT INJECTION (tests): refit only the first k leaves
+    deferred_status: bool = False  # rsi_build/rsi_rebuild do not wait: check rsi_build_status
 
     def _c(self) -> _Options:
-        flags = (OPT_FP64_MOLLER if self.fp64_moller else 0) | (OPT_COUNTERS if self.counters else 0)
+        flags = ((OPT_FP64_MOLLER if self.fp64_moller else 0) | (OPT_COUNTERS if self.counters else 0)
+                 | (OPT_DEFERRED_STATUS if self.deferred_status else 0))
         return _Options(ctypes.sizeof(_Options), flags, float(self.dedup_tau), int(self.debug_refit_leaves))
 
 
@@ -306,6 +310,11 @@ def rsi_test(vertices, triangles, start, end, cfg: dict | None = None, options: 
     tri = out["tri"].numpy()
     ids = np.nonzero(tri >= 0)[0].astype(np.int32)
     return ids, out["dist"].numpy()[ids], tri[ids], out["point"].numpy()[ids]
+
+
+def rsi_build_status(h: Handle, stream=None):
+    """Raise the device-side input-check error of the last (deferred) build, if any."""
+    _check(load().rsi_build_status(h.ptr, _stream(stream)))
 
 
 def rsi_get_stats(h: Handle, stream=None) -> dict:

@@ -264,6 +264,43 @@ def test_stacked_identical_triangles_and_overflow_repass(rsi):
     h.free()
 
 
+def test_deferred_build_status(rsi):
+    """RSI_OPT_DEFERRED_STATUS: rsi_build/rsi_rebuild return at once, the
+    device-side input checks surface in rsi_build_status (and in calls that
+    read the build back); valid meshes give the same results as a checked build."""
+    V, T = synth.fixture()
+    Vd, Td = to_dev(V, T)
+    opt = rsi.Options(deferred_status=True)
+    bad = torch.tensor([[0, 1, 9]], dtype=torch.int32, device=DEV)
+    h = rsi.rsi_build(Vd, bad, opt)  # no error yet
+    with pytest.raises(rsi.RsiError) as e:
+        rsi.rsi_build_status(h)
+    assert e.value.status == 3
+    with pytest.raises(rsi.RsiError):  # the handle holds no mesh after the failed check
+        rsi.rsi_intersect(h, Vd[:1], Vd[1:2], "boolean")
+    rsi.rsi_rebuild(h, Vd, Td)
+    rsi.rsi_build_status(h)
+    Vn = V.copy()
+    Vn[2, 1] = np.nan
+    rsi.rsi_rebuild(h, to_dev(Vn)[0], Td)
+    with pytest.raises(rsi.RsiError) as e:
+        rsi.rsi_bvh_info(h)
+    assert e.value.status == 4
+    h.free()
+    V, T, S, E, _ = synth.workload("sphere", 5000, seed=21)
+    Vd, Td, Sd, Ed = to_dev(V, T, S, E)
+    ref = oracle.run(V, T, S, E)
+    h = rsi.rsi_build(Vd, Td, opt)
+    for mode, key in (("boolean", "hit"), ("intercept_count", "count"), ("barycentric", "tri")):
+        for _ in range(2):  # rebuild + query back to back, no host read-back
+            rsi.rsi_rebuild(h, Vd, Td)
+            got = rsi.rsi_intersect(h, Sd, Ed, mode)[key].cpu().numpy()
+        assert (got == ref[key]).all(), mode
+    rsi.rsi_build_status(h)
+    assert rsi.rsi_validate(h)["ok"]
+    h.free()
+
+
 def test_build_errors(rsi):
     V, T = synth.fixture()
     Vd, Td = to_dev(V, T)
@@ -286,19 +323,24 @@ def test_build_errors(rsi):
     h.free()
 
 
-@pytest.mark.parametrize("nt", [1, 2, 3, 17, 1000, 70_001, -5000])
+@pytest.mark.parametrize("nt", [1, 2, 3, 17, 1000, 10_240, 16_384, 16_385, 70_001, -5000, "dup"])
 def test_bvh_integrity_random_meshes(rsi, nt):
     """Validator invariants (P:407-464 failure signatures must be absent):
     leaf bijection, arrivals == 2, root reachable from every leaf, child boxes
     exact unions, parent/child links mutual; sorted Morton codes equal a
-    bit-loop z-major encoding of the fp32 centroids."""
-    flat = nt < 0  # a flat (terrain-like) mesh: z extent 1/1000 of x, y
-    nt = abs(nt)
+    bit-loop z-major encoding of the fp32 centroids, in stable order (sizes
+    span the rank sort, N_t <= 16384, and the radix paths; "dup" repeats 40
+    triangles 12000 times, so equal keys must keep index order)."""
+    dup = nt == "dup"
+    flat = not dup and nt < 0  # a flat (terrain-like) mesh: z extent 1/1000 of x, y
+    nt = 12_000 if dup else abs(nt)
     rng = np.random.default_rng(nt)
     V = rng.uniform(-3, 7, (3 * nt, 3)).astype(np.float32)
     if flat:
         V[:, 2] *= np.float32(1e-3)
     T = rng.permutation(3 * nt).reshape(nt, 3).astype(np.int32)
+    if dup:
+        T = T[:40][rng.integers(0, 40, nt)]
     Vd, Td = to_dev(V, T)
     h = rsi.rsi_build(Vd, Td)
     d = rsi.rsi_bvh_download(h)

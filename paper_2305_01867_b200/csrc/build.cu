@@ -706,9 +706,10 @@ __global__ void __launch_bounds__(1024) k_topk(const float4* __restrict__ nodes,
 // traversal's decode is exact, and directed rounding keeps it conservative
 // otherwise).  64 B per record = two 256-bit loads.
 //   w0..w2  pm = p - 2^15 s per axis (float, the traversal's decode offset)
-//           w3  e_x+128 | e_y+128<<8 | e_z+128<<16 | valid<<24
+//   w3, w14, w15  s_x, s_y, s_z (float 2^e)
 //   w4..w9  qlo.x, qhi.x, qlo.y, qhi.y, qlo.z, qhi.z   (byte j = child j)
-//   w10..w13 ref[0..3]                   w14, w15 unused
+//   w10..w13 ref[0..3]  (kNoRef = 0x80000000 for the missing children of a
+//            node with fewer than 4)
 constexpr int kQuadEMin = -126, kQuadEMax = 104;  // s and s*2^23 stay normal floats
 
 __device__ __forceinline__ void quant_axis(const float* lo, const float* hi, int cnt, uint32_t& wlo, uint32_t& whi,
@@ -744,6 +745,7 @@ __device__ __forceinline__ void quant_axis(const float* lo, const float* hi, int
         wlo |= (uint32_t)ql << (8 * j);
         whi |= (uint32_t)qh << (8 * j);
     }
+    for (int j = cnt; j < 4; ++j) wlo |= 255u << (8 * j);  // missing child: empty box (lo > hi)
     p_out = (float)(p - 32768.0 * sc);  // the decode offset p - 2^15 s: exact (|p/s - 2^15| < 2^24)
     e_out = e;
     ok = ((double)nhi - p <= 255.0 * sc) && fabs(p * isc) < 8388608.0 && (double)p_out == p - 32768.0 * sc;
@@ -754,7 +756,7 @@ __global__ void __launch_bounds__(kBlock) k_quads(const float4* __restrict__ nod
     int n = blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= n_nodes) return;
     float lo[3][4], hi[3][4];
-    int ref[4] = {0, 0, 0, 0};
+    int ref[4] = {(int)0x80000000, (int)0x80000000, (int)0x80000000, (int)0x80000000};  // kNoRef: no child
     int k = 0;
     const float4* nd = nodes + 4 * n;
     const float4 n0 = nd[0], n1 = nd[1], n2 = nd[2];
@@ -802,10 +804,11 @@ __global__ void __launch_bounds__(kBlock) k_quads(const float4* __restrict__ nod
     w[0] = __float_as_uint(px[0]);
     w[1] = __float_as_uint(px[1]);
     w[2] = __float_as_uint(px[2]);
-    w[3] = (uint32_t)(ex[0] + 128) | ((uint32_t)(ex[1] + 128) << 8) | ((uint32_t)(ex[2] + 128) << 16) |
-           (((1u << k) - 1u) << 24);
+    // grid steps as floats (2^e, exact): the traversal multiplies them by 1/d directly
+    w[3] = __float_as_uint(ldexpf(1.0f, ex[0]));
     for (int j = 0; j < 4; ++j) w[10 + j] = (uint32_t)ref[j];
-    w[14] = w[15] = 0u;
+    w[14] = __float_as_uint(ldexpf(1.0f, ex[1]));
+    w[15] = __float_as_uint(ldexpf(1.0f, ex[2]));
     uint4* q = reinterpret_cast<uint4*>(quads + 4 * n);
     q[0] = make_uint4(w[0], w[1], w[2], w[3]);
     q[1] = make_uint4(w[4], w[5], w[6], w[7]);

@@ -77,8 +77,13 @@ constexpr int kCountCap = 8;  // intercept_count hits held in registers per ray
 #ifndef RSI_BOOL_MINB
 #define RSI_BOOL_MINB 8
 #endif
-#ifndef RSI_OTHER_MINB
-#define RSI_OTHER_MINB 6
+// resident 128-thread CTAs per SM (register budget: 8 -> 64, 6 -> 80 registers);
+// measured: barycentric -8 % at 8 vs 6, intercept_count +4 % at 8 vs 6
+#ifndef RSI_BARY_MINB
+#define RSI_BARY_MINB 8
+#endif
+#ifndef RSI_COUNT_MINB
+#define RSI_COUNT_MINB 6
 #endif
 constexpr int kThreads = 128;  // block size of the auxiliary (re-pass) kernels
 // k_trace block size: with the top-of-tree cache, one CTA per SM shares the
@@ -98,6 +103,7 @@ struct Ray {
     float ix, iy, iz;  // slab: 1/d per axis (0 on degenerate axes)
     float lx, ly, lz;  // slab offsets applied to the box's lo plane
     float hx, hy, hz;  // slab offsets applied to the box's hi plane
+    uint32_t mx, my, mz;  // 4-wide walk: 0xffffffff where inv < 0 (picks the near-plane bytes)
 };
 
 // Per-axis slab setup.  t = fma(plane, inv, -off) approximates (plane - o)/d;
@@ -164,6 +170,9 @@ __device__ __forceinline__ bool load_ray(Ray& r, const float* __restrict__ S, co
     slab_axis(r.oy, r.dy, r.iy, r.ly, r.hy, qext, lim_lo, lim_hi);
     slab_axis(r.oz, r.dz, r.iz, r.lz, r.hz, qext, lim_lo, lim_hi);
     if (kNearFar) {
+        r.mx = (uint32_t)(__float_as_int(r.ix) >> 31);
+        r.my = (uint32_t)(__float_as_int(r.iy) >> 31);
+        r.mz = (uint32_t)(__float_as_int(r.iz) >> 31);
         if (r.ix < 0.0f) { const float t = r.lx; r.lx = r.hx; r.hx = t; }
         if (r.iy < 0.0f) { const float t = r.ly; r.ly = r.hy; r.hy = t; }
         if (r.iz < 0.0f) { const float t = r.lz; r.lz = r.hz; r.hz = t; }
@@ -738,7 +747,7 @@ __device__ __forceinline__ void cas(float& ka, int& ca, float& kb, int& cb) {
 }
 
 template <int MODE, bool kFP64, bool kCounters>
-__global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MODE == MODE_BOOL ? RSI_BOOL_MINB : RSI_OTHER_MINB)) k_trace(const TraceParams p) {
+__global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MODE == MODE_BOOL ? RSI_BOOL_MINB : (MODE == MODE_BARY ? RSI_BARY_MINB : RSI_COUNT_MINB))) k_trace(const TraceParams p) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
@@ -861,8 +870,6 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                 float4 qa, qb, qc, qd;
                 ldg256(q, qa, qb);
                 ldg256(q + 2, qc, qd);
-                const uint32_t w3 = __float_as_uint(qa.w);
-                const uint32_t vmask = w3 >> 24;
                 // Per axis: grid step s = 2^e and the decode offset pm = p - 2^15 s
                 // (stored; exact).  A child plane is p + q s = (2^15 + q) s + pm, so its
                 // t = (plane - o) / d is fma(2^15 + q, s*inv, fma(pm, inv, -off)): s*inv
@@ -877,17 +884,22 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                 const uint32_t wq[6] = {__float_as_uint(qb.x), __float_as_uint(qb.y), __float_as_uint(qb.z),
                                         __float_as_uint(qb.w), __float_as_uint(qc.x), __float_as_uint(qc.y)};
                 const float inv3[3] = {r.ix, r.iy, r.iz};
+                const float scv[3] = {qa.w, qd.z, qd.w};  // grid steps s = 2^e
+                // octant masks: kept per ray, except for intercept_count (register
+                // pressure at 80 registers: derived from the sign of inv per visit)
+                const uint32_t msk[3] = {
+                    MODE == MODE_COUNT ? (uint32_t)(__float_as_int(r.ix) >> 31) : r.mx,
+                    MODE == MODE_COUNT ? (uint32_t)(__float_as_int(r.iy) >> 31) : r.my,
+                    MODE == MODE_COUNT ? (uint32_t)(__float_as_int(r.iz) >> 31) : r.mz};
                 const float nof[3] = {r.lx, r.ly, r.lz};
                 const float fof[3] = {r.hx, r.hy, r.hz};
 #pragma unroll
                 for (int a = 0; a < 3; ++a) {
-                    const uint32_t eb = (w3 >> (8 * a)) & 255u;
-                    sa[a] = __uint_as_float((eb - 1u) << 23) * inv3[a];
+                    sa[a] = scv[a] * inv3[a];
                     bn[a] = fmaf(pp[a], inv3[a], -nof[a]);
                     bf[a] = fmaf(pp[a], inv3[a], -fof[a]);
-                    const bool neg = inv3[a] < 0.0f;
-                    wn[a] = neg ? wq[2 * a + 1] : wq[2 * a];
-                    wf[a] = neg ? wq[2 * a] : wq[2 * a + 1];
+                    wn[a] = (wq[2 * a] & ~msk[a]) | (wq[2 * a + 1] & msk[a]);
+                    wf[a] = (wq[2 * a + 1] & ~msk[a]) | (wq[2 * a] & msk[a]);
                 }
                 const int4 q6 = make_int4(__float_as_int(qc.z), __float_as_int(qc.w), __float_as_int(qd.x),
                                           __float_as_int(qd.y));
@@ -900,7 +912,7 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                     const float fz = fmaf(byte_to_2p15(wf[2], j, magic), sa[2], bf[2]);
                     tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, 0.0f));
                     const float tf = fminf(fminf(fx, fy), fminf(fz, tclip));
-                    return ((vmask >> j) & 1u) != 0u && tn <= tf;
+                    return tn <= tf;  // a missing child has an empty box and ref kNoRef
                 };
                 float k0, k1, k2, k3;
                 const bool h0 = child(0, k0), h1 = child(1, k1), h2 = child(2, k2), h3 = child(3, k3);

@@ -66,6 +66,21 @@ constexpr bool kQuadCount = RSI_COUNT_QUAD;
 #ifndef RSI_BF_SMEM
 #define RSI_BF_SMEM 0
 #endif
+#ifndef RSI_BF_PRED
+#define RSI_BF_PRED 0
+#endif
+// latency hiding by prefetch (no register cost): the warp's next ray chunk into
+// L2 one chunk ahead, a pending leaf's triangle into L1 when it is found, a
+// pushed node into L1 when it is pushed
+#ifndef RSI_PF_RAY
+#define RSI_PF_RAY 0
+#endif
+#ifndef RSI_PF_TRI
+#define RSI_PF_TRI 0
+#endif
+#ifndef RSI_PF_PUSH
+#define RSI_PF_PUSH 0
+#endif
 #ifndef RSI_SORT_ALL
 #define RSI_SORT_ALL 1
 #endif
@@ -294,6 +309,10 @@ __device__ __forceinline__ void ldg256(const float4* p, float4& a, float4& b) {
     b = __ldg(p + 1);
 #endif
 }
+
+__device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+__device__ __forceinline__ void use_prefetch_helpers() { (void)prefetch_l1; (void)prefetch_l2; }
 
 // triangle slot k: 64 B (4 x float4, the last one padding) for two 256-bit loads
 __device__ __forceinline__ void load_tri(const float4* __restrict__ tris, int k, float4& A, float4& B, float4& C) {
@@ -708,9 +727,17 @@ struct BFStack {
         return (kSm > 0 && k < kSm) ? s[k * kT] : local[(unsigned)(k - kSm)];
     }
     __device__ __forceinline__ void push_if(int& sp, bool v, int x) {
+#if RSI_BF_PRED
+        if (v) {  // predicated store: only pushing lanes write (less local-memory traffic)
+            put(sp, top);
+            top = x;
+            ++sp;
+        }
+#else
         put(sp, top);
         top = v ? x : top;
         sp += v ? 1 : 0;
+#endif
     }
     __device__ __forceinline__ void push(int& sp, int x) { push_if(sp, true, x); }
     __device__ __forceinline__ int pop(int& sp) {
@@ -769,6 +796,8 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
     Stats st;
 
     int64_t cnext = 0, cend = 0;  // warp-uniform chunk [cnext, cend)
+    int64_t pbase = -1;           // warp-uniform: chunk reserved ahead (RSI_PF_RAY)
+    (void)pbase;
     bool exhausted = false;       // warp-uniform
     int64_t ray = -1;
     Ray r;
@@ -811,8 +840,28 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
         while (want && !exhausted) {
             if (cnext >= cend) {
                 unsigned long long base = 0;
+#if RSI_PF_RAY
+                // take the chunk reserved last time (the first time: a fresh one),
+                // reserve the next and prefetch its segments into L2
+                unsigned long long nb = 0;
+                if (lane == 0) {
+                    base = pbase >= 0 ? (unsigned long long)pbase : atomicAdd(p.counter, (unsigned long long)kChunk);
+                    nb = atomicAdd(p.counter, (unsigned long long)kChunk);
+                }
+                base = __shfl_sync(FULL, base, 0);
+                nb = __shfl_sync(FULL, nb, 0);
+                pbase = (int64_t)nb;
+                if ((int64_t)nb < p.n && lane < 16) {
+                    const int64_t ne = min((int64_t)nb + kChunk, p.n);
+                    const float* arr = lane < 8 ? p.S : p.E;
+                    const uintptr_t b0 = reinterpret_cast<uintptr_t>(arr + 3 * (int64_t)nb) & ~(uintptr_t)127;
+                    const uintptr_t a = b0 + 128 * (uintptr_t)(lane & 7);
+                    if (a < reinterpret_cast<uintptr_t>(arr + 3 * ne)) prefetch_l2(reinterpret_cast<const void*>(a));
+                }
+#else
                 if (lane == 0) base = atomicAdd(p.counter, (unsigned long long)kChunk);
                 base = __shfl_sync(FULL, base, 0);
+#endif
                 if ((int64_t)base >= p.n) {
                     exhausted = true;
                     break;
@@ -936,12 +985,21 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                     }
                 }
                 // c0 is the nearest hit child (kSort) -- kNoRef only when none hit
+                if (RSI_PF_PUSH) {
+                    auto pf = [&](int c) {
+                        if (c != kNoRef) prefetch_l1(c >= 0 ? (const void*)(p.quads + 4 * c) : (const void*)(p.tris + 4 * ~c));
+                    };
+                    pf(c1);
+                    pf(c2);
+                    pf(c3);
+                }
                 stk.push_if(sp, c3 != kNoRef, c3);
                 stk.push_if(sp, c2 != kNoRef, c2);
                 stk.push_if(sp, c1 != kNoRef, c1);
                 int first = c0;
                 if (first == kNoRef && sp > 0) first = stk.pop(sp);
                 if (first != kNoRef && first < 0) {  // a leaf
+                    if (RSI_PF_TRI) prefetch_l1(p.tris + 4 * ~first);
                     if (l0 < 0) {
                         l0 = ~first;
                         // kQSpec: keep walking from the next stack entry while

@@ -68,6 +68,20 @@ typedef enum {
                                   rsi_intersect on an invalid mesh are unspecified (no
                                   out-of-bounds access either way).  For pipelines that
                                   rebuild and query every step with no host round trip. */
+#define RSI_OPT_APETREI 8u     /* the paper's construction instead of
+                                  Karras + refit -- 63-bit Morton codes (21 bits per axis,
+                                  z-major; "64-bit Morton codes") sorted as
+                                  two stable 32-bit LSD passes, then Apetrei's single-pass
+                                  agglomerative build: one thread per leaf
+                                  climbs, choosing its parent by comparing the common
+                                  prefix with its left and right neighbours, and the
+                                  second arrival at a node (a 64-bit atomic that also
+                                  counts arrivals) merges the boxes.  Internal node i is
+                                  the split between sorted leaves i and i+1, so the root
+                                  is not node 0 (rsi_bvh_root) and the sentinel N_t - 1
+                                  "only holds a pointer to the root".
+                                  Same results; only the tree differs.  N_t == 1 uses the
+                                  default path. */
 
 typedef struct {
     uint32_t struct_size; /* sizeof(rsi_options_t); 0 or a NULL options pointer = defaults   */
@@ -269,6 +283,22 @@ rsi_status_t rsi_bvh_info(rsi_handle_t h, int64_t* n_triangles, int64_t* n_nodes
 rsi_status_t rsi_bvh_download(rsi_handle_t h, int32_t* h_child, float* h_box,
                               int32_t* h_leaf_tri, uint32_t* h_morton, int32_t* h_parent,
                               uint32_t* h_arrivals, void* stream);
+
+/*
+ * rsi_bvh_root: the root internal node of `h` and the sorted Morton codes at
+ * full width (host outputs; h_morton63 may be NULL; synchronizes `stream`).
+ *   *root        0 for the default (Karras) numbering; under RSI_OPT_APETREI the
+ *                split position of the top node (the fixture tree: 1),
+ *                -1 if the construction never reached the root (fault injection).
+ *   *sentinel    N_t - 1 under RSI_OPT_APETREI (the node that "only holds a
+ *                pointer to the root"), else -1.
+ *   h_morton63   [N_t] uint64 sorted codes: 63-bit under RSI_OPT_APETREI, else the
+ *                30-bit codes widened.  (rsi_bvh_download's 30-bit h_morton is
+ *                the top 30 bits of the 63-bit code: the same quantization.)
+ * Errors: RSI_E_INVALID_ARG (null handle / root), RSI_E_CUDA.
+ */
+rsi_status_t rsi_bvh_root(rsi_handle_t h, int64_t* root, int64_t* sentinel, uint64_t* h_morton63,
+                          void* stream);
 
 #ifdef __cplusplus
 }

@@ -36,7 +36,7 @@ static rsi_status_t read_options(const rsi_options_t* in, rsi_options_t* out) {
     if (in->struct_size != sizeof(rsi_options_t))
         return rsi_set_error(RSI_E_INVALID_ARG, "rsi_options_t.struct_size %u != %zu", in->struct_size,
                              sizeof(rsi_options_t));
-    if (in->flags & ~(RSI_OPT_FP64_MOLLER | RSI_OPT_COUNTERS | RSI_OPT_DEFERRED_STATUS)) return rsi_set_error(RSI_E_INVALID_ARG, "unknown option flags 0x%x", in->flags);
+    if (in->flags & ~(RSI_OPT_FP64_MOLLER | RSI_OPT_COUNTERS | RSI_OPT_DEFERRED_STATUS | RSI_OPT_APETREI)) return rsi_set_error(RSI_E_INVALID_ARG, "unknown option flags 0x%x", in->flags);
     if (!(in->dedup_tau >= 0.0)) return rsi_set_error(RSI_E_INVALID_ARG, "dedup_tau must be >= 0");
     if (in->debug_refit_leaves < 0) return rsi_set_error(RSI_E_INVALID_ARG, "debug_refit_leaves must be >= 0");
     *out = *in;
@@ -368,7 +368,7 @@ rsi_status_t rsi_free(rsi_handle_t h) {
     if (!h) return RSI_OK;
     cudaStream_t s = h->stream;
     void* bufs[] = {h->nodes, h->top, h->quads, h->tris, h->keys, h->vals, h->keys_tmp, h->vals_tmp, h->parent,
-                    h->arrivals, h->hist, h->scratch, h->stats, h->ovf_list};
+                    h->arrivals, h->hist, h->scratch, h->stats, h->ovf_list, h->k63, h->other};
     rsi_status_t st = RSI_OK;
     for (void* p : bufs)
         if (p) {
@@ -473,15 +473,44 @@ rsi_status_t rsi_bvh_download(rsi_handle_t h, int32_t* h_child, float* h_box, in
         if (!tris) st = rsi_set_error(RSI_E_OOM, "host allocation failed");
         else st = rsi_cuda_check(cudaMemcpyAsync(tris, h->tris, nt * 4 * sizeof(float4), cudaMemcpyDeviceToHost, s), "tris");
     }
-    if (st == RSI_OK && h_morton)
-        st = rsi_cuda_check(cudaMemcpyAsync(h_morton, h->keys, nt * sizeof(uint32_t), cudaMemcpyDeviceToHost, s), "keys");
+    // Apetrei builds: codes are 63-bit (the top 30 bits are the 30-bit code) and
+    // arrival counts live in the high words of the 64-bit node words
+    uint32_t* khi = nullptr;  // [2 * nt]: sorted high words, then sorted low words
+    unsigned long long* other = nullptr;
+    if (st == RSI_OK && h_morton) {
+        if (h->apetrei) {
+            khi = new (std::nothrow) uint32_t[2 * nt];
+            if (!khi) st = rsi_set_error(RSI_E_OOM, "host allocation failed");
+            else st = rsi_cuda_check(cudaMemcpyAsync(khi, h->keys, nt * sizeof(uint32_t), cudaMemcpyDeviceToHost, s), "keys");
+            if (st == RSI_OK)
+                st = rsi_cuda_check(cudaMemcpyAsync(khi + nt, h->k63 + 3 * nt, nt * sizeof(uint32_t),
+                                                    cudaMemcpyDeviceToHost, s), "keys");
+        } else {
+            st = rsi_cuda_check(cudaMemcpyAsync(h_morton, h->keys, nt * sizeof(uint32_t), cudaMemcpyDeviceToHost, s), "keys");
+        }
+    }
     if (st == RSI_OK && h_parent)
         st = rsi_cuda_check(cudaMemcpyAsync(h_parent, h->parent, (nn + nt) * sizeof(int32_t), cudaMemcpyDeviceToHost, s),
                             "parent");
-    if (st == RSI_OK && h_arrivals)
-        st = rsi_cuda_check(cudaMemcpyAsync(h_arrivals, h->arrivals, nn * sizeof(uint32_t), cudaMemcpyDeviceToHost, s),
-                            "arrivals");
+    if (st == RSI_OK && h_arrivals) {
+        if (h->apetrei) {
+            other = new (std::nothrow) unsigned long long[nn];
+            if (!other) st = rsi_set_error(RSI_E_OOM, "host allocation failed");
+            else st = rsi_cuda_check(cudaMemcpyAsync(other, h->other, nn * sizeof(unsigned long long),
+                                                     cudaMemcpyDeviceToHost, s), "arrivals");
+        } else {
+            st = rsi_cuda_check(cudaMemcpyAsync(h_arrivals, h->arrivals, nn * sizeof(uint32_t), cudaMemcpyDeviceToHost, s),
+                                "arrivals");
+        }
+    }
     if (st == RSI_OK) st = rsi_cuda_check(cudaStreamSynchronize(s), "download");
+    if (st == RSI_OK && khi)
+        for (int64_t k = 0; k < nt; ++k)
+            h_morton[k] = (uint32_t)((((unsigned long long)khi[k] << 32) | khi[nt + k]) >> 33);
+    if (st == RSI_OK && other)
+        for (int64_t i = 0; i < nn; ++i) h_arrivals[i] = (uint32_t)(other[i] >> 32);
+    delete[] khi;
+    delete[] other;
     if (st == RSI_OK) {
         for (int64_t i = 0; i < nn; ++i) {
             const float* f = reinterpret_cast<const float*>(nodes ? nodes + 4 * i : nullptr);
@@ -507,6 +536,32 @@ rsi_status_t rsi_bvh_download(rsi_handle_t h, int32_t* h_child, float* h_box, in
     }
     delete[] nodes;
     delete[] tris;
+    return st;
+}
+
+rsi_status_t rsi_bvh_root(rsi_handle_t h, int64_t* root, int64_t* sentinel, uint64_t* h_morton63, void* stream) {
+    if (!h || !root) return rsi_set_error(RSI_E_INVALID_ARG, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (h->status_pending) {
+        const rsi_status_t st0 = rsi_finish_build(h, s);
+        if (st0 != RSI_OK) return st0;
+    }
+    if (h->n_tri <= 0) return rsi_set_error(RSI_E_INVALID_ARG, "handle holds no mesh");
+    *root = h->root_node;
+    if (sentinel) *sentinel = h->apetrei ? h->n_tri - 1 : -1;
+    if (!h_morton63) return RSI_OK;
+    const int64_t nt = h->n_tri;
+    uint32_t* w = new (std::nothrow) uint32_t[2 * nt];
+    if (!w) return rsi_set_error(RSI_E_OOM, "host allocation failed");
+    rsi_status_t st = rsi_cuda_check(cudaMemcpyAsync(w, h->keys, nt * sizeof(uint32_t), cudaMemcpyDeviceToHost, s), "keys");
+    if (st == RSI_OK && h->apetrei)
+        st = rsi_cuda_check(cudaMemcpyAsync(w + nt, h->k63 + 3 * nt, nt * sizeof(uint32_t), cudaMemcpyDeviceToHost, s),
+                            "keys");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaStreamSynchronize(s), "keys");
+    if (st == RSI_OK)
+        for (int64_t k = 0; k < nt; ++k)
+            h_morton63[k] = h->apetrei ? (((uint64_t)w[k] << 32) | w[nt + k]) : (uint64_t)w[k];
+    delete[] w;
     return st;
 }
 

@@ -20,8 +20,9 @@ namespace {
 
 constexpr int kBlock = 256;
 
-__global__ void k_build_init(uint32_t* scratch) {
+__global__ void k_build_init(uint32_t* scratch, uint32_t root_init) {
     int i = threadIdx.x;
+    if (i == 1) scratch[SCR_ROOT_NODE] = root_init;
     if (i < 3) {
         scratch[SCR_EXT_MIN + i] = 0xffffffffu;
         scratch[SCR_EXT_MAX + i] = 0u;
@@ -571,22 +572,30 @@ __global__ void __launch_bounds__(kRankT) k_sort_rank(const uint32_t* __restrict
         ki[a] = idx[a] < n ? keys[idx[a]] : 0u;
         cnt[a] = 0u;
     }
-    if (j1 <= i_lo || j0 >= i_hi) {  // slice wholly below / above this block's keys
-        const uint32_t add = j1 <= i_lo ? 1u : 0u;
-        uint32_t thr[kRankPer];
-#pragma unroll
-        for (int a = 0; a < kRankPer; ++a) thr[a] = ki[a] + add;
+    if (j1 <= i_lo) {  // slice wholly below this block's keys: count k_j <= k_i
         for (int q = 0; q < nj4; ++q) {
             const uint4 k4 = s_k4[q];
 #pragma unroll
             for (int a = 0; a < kRankPer; ++a)
-                cnt[a] += (k4.x < thr[a]) + (k4.y < thr[a]) + (k4.z < thr[a]) + (k4.w < thr[a]);
+                cnt[a] += (k4.x <= ki[a]) + (k4.y <= ki[a]) + (k4.z <= ki[a]) + (k4.w <= ki[a]);
+        }
+        // the 0xffffffff pads were counted only for a key equal to 0xffffffff
+        // (full 32-bit words of the 63-bit codes)
+#pragma unroll
+        for (int a = 0; a < kRankPer; ++a)
+            if (ki[a] == 0xffffffffu) cnt[a] -= (uint32_t)(4 * nj4 - nj);
+    } else if (j0 >= i_hi) {  // wholly above: count k_j < k_i (pads never are)
+        for (int q = 0; q < nj4; ++q) {
+            const uint4 k4 = s_k4[q];
+#pragma unroll
+            for (int a = 0; a < kRankPer; ++a)
+                cnt[a] += (k4.x < ki[a]) + (k4.y < ki[a]) + (k4.z < ki[a]) + (k4.w < ki[a]);
         }
     } else {  // overlapping (diagonal) slice: per-pair index test
         for (int j = 0; j < nj; ++j) {
             const uint32_t kj = s_k[j];
 #pragma unroll
-            for (int a = 0; a < kRankPer; ++a) cnt[a] += (kj < ki[a] + (j0 + j < idx[a] ? 1u : 0u));
+            for (int a = 0; a < kRankPer; ++a) cnt[a] += (kj < ki[a]) || (kj == ki[a] && j0 + j < idx[a]);
         }
     }
 #pragma unroll
@@ -606,6 +615,177 @@ __global__ void __launch_bounds__(kRankT) k_sort_rank(const uint32_t* __restrict
             out_keys[r] = ki[a];
             out_vals[r] = idx[a];
         }
+    }
+}
+
+// ------------------------------------------------------------------ NEXT-1: 63-bit codes + Apetrei build
+// RSI_OPT_APETREI: the paper's construction.  Codes are
+// 63-bit ("64-bit Morton codes"): 21 bits per axis with the same
+// quantization rule as the 30-bit path (reading R8) scaled by 2^21 instead of
+// 2^10 -- an exact power-of-two rescale, so the top 30 bits of the 63-bit code
+// ARE the 30-bit code.  They are sorted by two stable 32-bit LSD sorts (low
+// word, then high word) and the tree is built bottom-up in one pass (Apetrei
+// 2014, cited at P:504; the paper's construct kernel).
+
+// Spread the low 21 bits of x so bit k lands at bit 3k.
+__device__ __forceinline__ unsigned long long expand21(uint32_t v) {
+    unsigned long long x = v & 0x1fffffu;
+    x = (x | (x << 32)) & 0x1f00000000ffffull;
+    x = (x | (x << 16)) & 0x1f0000ff0000ffull;
+    x = (x | (x << 8)) & 0x100f00f00f00f00full;
+    x = (x | (x << 4)) & 0x10c30c30c30c30c3ull;
+    x = (x | (x << 2)) & 0x1249249249249249ull;
+    return x;
+}
+
+__device__ __forceinline__ uint32_t quantize21(float c, float lo, float hi, float wmax) {
+    float w = fmaxf(hi - lo, wmax * 0.015625f);
+    if (!(w > 0.0f)) return 0u;
+    float q = floorf((c - lo) / w * 2097152.0f);  // 2^21
+    q = fminf(fmaxf(q, 0.0f), 2097151.0f);
+    return (uint32_t)q;
+}
+
+// A3 (63-bit): code = e(qx) | e(qy) << 1 | e(qz) << 2 (z-major); low word into
+// keys (sort pass 1) and k_lo, high word into k_hi; zeroes the arrival words.
+__global__ void __launch_bounds__(kBlock) k_morton63(const float* __restrict__ V, int64_t nv,
+                                                     const int32_t* __restrict__ T, int n,
+                                                     const uint32_t* __restrict__ scratch,
+                                                     uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
+                                                     uint32_t* __restrict__ k_lo, uint32_t* __restrict__ k_hi,
+                                                     unsigned long long* __restrict__ other,
+                                                     uint32_t* __restrict__ rank) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    other[j] = 0ull;
+    if (rank) rank[j] = 0u;
+    float lo[3], hi[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        lo[k] = rsi_ord2f(scratch[SCR_EXT_MIN + k]);
+        hi[k] = rsi_ord2f(scratch[SCR_EXT_MAX + k]);
+    }
+    int32_t a = safe_index(T[3 * j], nv), b = safe_index(T[3 * j + 1], nv), c = safe_index(T[3 * j + 2], nv);
+    const float wmax = fmaxf(hi[0] - lo[0], fmaxf(hi[1] - lo[1], hi[2] - lo[2]));
+    uint32_t q[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        float cen = (V[3 * a + k] + V[3 * b + k] + V[3 * c + k]) / 3.0f;
+        q[k] = quantize21(cen, lo[k], hi[k], wmax);
+    }
+    const unsigned long long code = expand21(q[0]) | (expand21(q[1]) << 1) | (expand21(q[2]) << 2);
+    keys[j] = (uint32_t)code;
+    k_lo[j] = (uint32_t)code;
+    k_hi[j] = (uint32_t)(code >> 32);
+    vals[j] = j;
+}
+
+// Between the two sorts: the high words in pass-1 (low-word) order become the
+// keys, the pass-1 order is saved, values restart as positions, and the rank
+// sort's accumulators and slice counters are cleared.
+__global__ void __launch_bounds__(kBlock) k_pass2_prep(uint32_t* __restrict__ keys, int32_t* __restrict__ vals,
+                                                       const uint32_t* __restrict__ k_hi, int32_t* __restrict__ ids1,
+                                                       int n, uint32_t* __restrict__ rank, uint32_t* scratch) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < 32) scratch[SCR_SORT_DONE + j] = 0u;
+    if (j >= n) return;
+    const int32_t id = vals[j];
+    ids1[j] = id;
+    keys[j] = k_hi[id];
+    vals[j] = j;
+    if (rank) rank[j] = 0u;
+}
+
+// After the second sort: vals[j] = position in pass-1 order -> triangle id;
+// sorted low words gathered beside the sorted high words (keys).
+__global__ void __launch_bounds__(kBlock) k_pass2_finish(int32_t* __restrict__ vals, const int32_t* __restrict__ ids1,
+                                                         const uint32_t* __restrict__ k_lo,
+                                                         uint32_t* __restrict__ lo_sorted, int n) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int32_t id = ids1[vals[j]];
+    vals[j] = id;
+    lo_sorted[j] = k_lo[id];
+}
+
+// Common-prefix length of sorted keys i and i+1 (larger = more similar); equal
+// codes fall back to the sorted positions (index augmentation, as k_karras).
+__device__ __forceinline__ int cpl63(const uint32_t* __restrict__ khi, const uint32_t* __restrict__ klo, int i) {
+    const unsigned long long a = ((unsigned long long)khi[i] << 32) | klo[i];
+    const unsigned long long b = ((unsigned long long)khi[i + 1] << 32) | klo[i + 1];
+    const unsigned long long x = a ^ b;
+    return x ? __clzll(x) : 64 + __clz(i ^ (i + 1));
+}
+
+// One thread per leaf slot k (grid = ceil(N_t / block): the case-study-2 rule,
+// P:467-494).  The thread holds the leaf range [l, r] of its current subtree.
+// Its parent is the node on the side of the more similar neighbour: node r
+// (this subtree is its LEFT child) when l == 0 or cpl(r) > cpl(l-1), else node
+// l-1 (RIGHT child); internal node i is thus the split between sorted leaves
+// i and i+1.  The child writes its box and ref into its slot of the parent,
+// then adds (1 << 32 | its far bound) to the parent's 64-bit word with
+// acq_rel: the first arrival (old == 0) stops; the second learns the parent's
+// full range from the old word, merges the sibling's box and climbs on.  The
+// range [0, N_t-1] is the root; the sentinel N_t-1 only points at it.
+__global__ void __launch_bounds__(kBlock) k_apetrei(const float* __restrict__ V, int64_t nv,
+                                                    const int32_t* __restrict__ T, const int32_t* __restrict__ vals,
+                                                    const uint32_t* __restrict__ khi, const uint32_t* __restrict__ klo,
+                                                    int n_leaves, int n, float4* nodes, float4* __restrict__ tris,
+                                                    int32_t* __restrict__ parent, unsigned long long* other,
+                                                    uint32_t* scratch) {
+    int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n_leaves) return;
+    const int n_nodes = n - 1;  // n >= 2 on this path
+    const int32_t id = vals[k];
+    const int32_t ia = safe_index(T[3 * id], nv), ib = safe_index(T[3 * id + 1], nv),
+                  ic = safe_index(T[3 * id + 2], nv);
+    float a[3], b[3], c[3], lo[3], hi[3];
+#pragma unroll
+    for (int x = 0; x < 3; ++x) {
+        a[x] = V[3 * ia + x];
+        b[x] = V[3 * ib + x];
+        c[x] = V[3 * ic + x];
+        lo[x] = fminf(a[x], fminf(b[x], c[x]));
+        hi[x] = fmaxf(a[x], fmaxf(b[x], c[x]));
+    }
+    tris[4 * k + 0] = make_float4(a[0], a[1], a[2], __int_as_float(id));
+    tris[4 * k + 1] = make_float4(b[0], b[1], b[2], 0.f);
+    tris[4 * k + 2] = make_float4(c[0], c[1], c[2], 0.f);
+    tris[4 * k + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
+    int l = k, r = k;
+    int32_t ref = ~k;
+    while (true) {
+        if (l == 0 && r == n - 1) {  // the root: the sentinel's only child
+            scratch[SCR_ROOT_NODE] = (uint32_t)ref;
+            parent[ref] = -1;
+            float* root = reinterpret_cast<float*>(scratch + SCR_ROOT);
+            for (int x = 0; x < 3; ++x) {
+                root[x] = lo[x];
+                root[3 + x] = hi[x];
+            }
+            scratch[SCR_ROOT_SET] = 1u;
+            return;
+        }
+        const bool up_right = (l == 0) || (r != n - 1 && cpl63(khi, klo, r) > cpl63(khi, klo, l - 1));
+        const int p = up_right ? r : l - 1, side = up_right ? 0 : 1;
+        write_slot(nodes, p, side, lo, hi);
+        set_ref(nodes, p, side, ref);
+        parent[ref >= 0 ? ref : n_nodes + ~ref] = (p << 1) | side;
+        const unsigned long long add = (1ull << 32) | (uint32_t)(up_right ? l : r);
+        unsigned long long old;
+        asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(other + p), "l"(add) : "memory");
+        if (old == 0ull) return;  // first arrival: the sibling finishes the node
+        const int bound = (int)(uint32_t)old;
+        if (up_right) r = bound; else l = bound;
+        const float* f = reinterpret_cast<const float*>(nodes + 4 * p);
+        const int o = side ? 0 : 4;  // sibling slot
+        lo[0] = fminf(lo[0], __ldcg(f + o + 0));
+        hi[0] = fmaxf(hi[0], __ldcg(f + o + 1));
+        lo[1] = fminf(lo[1], __ldcg(f + o + 2));
+        hi[1] = fmaxf(hi[1], __ldcg(f + o + 3));
+        lo[2] = fminf(lo[2], __ldcg(f + 8 + 2 * (1 - side)));
+        hi[2] = fmaxf(hi[2], __ldcg(f + 9 + 2 * (1 - side)));
+        ref = p;
     }
 }
 
@@ -649,7 +829,7 @@ __global__ void __launch_bounds__(1024) k_topk(const float4* __restrict__ nodes,
     __shared__ int s_warp[33];
     const int tid = threadIdx.x;
     int a = 0, b = 1;  // current level = slots [a, b)
-    if (tid == 0) old_of[0] = 0;
+    if (tid == 0) old_of[0] = (int)scratch[SCR_ROOT_NODE];
     for (int i = tid; i < kTopNodes; i += blockDim.x) first_child[i] = -1;
     __syncthreads();
     while (true) {
@@ -836,10 +1016,12 @@ __device__ __forceinline__ void node_box(const float4* nodes, int node, int side
 __global__ void __launch_bounds__(kBlock) k_validate_nodes(const float4* __restrict__ nodes, int n, int n_nodes,
                                                            const int32_t* __restrict__ parent,
                                                            const uint32_t* __restrict__ arrivals,
+                                                           const unsigned long long* __restrict__ other,
                                                            unsigned long long* __restrict__ out) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n_nodes || n == 1) return;
-    const uint32_t a = arrivals[i];
+    // arrival count: the refit counter, or the high word of the Apetrei node word
+    const uint32_t a = other ? (uint32_t)(other[i] >> 32) : arrivals[i];
     if (a == 1u) atomicAdd(out + V_HALF, 1ull);
     if (a == 0u) atomicAdd(out + V_UNTOUCHED, 1ull);
     const int4 r = *reinterpret_cast<const int4*>(nodes + 4 * i + 3);
@@ -865,6 +1047,7 @@ __global__ void __launch_bounds__(kBlock) k_validate_nodes(const float4* __restr
 }
 
 __global__ void __launch_bounds__(kBlock) k_validate_leaves(const float4* __restrict__ tris, int n, int n_nodes,
+                                                            const uint32_t* __restrict__ scratch,
                                                             const int32_t* __restrict__ parent,
                                                             uint32_t* __restrict__ seen,
                                                             unsigned long long* __restrict__ out) {
@@ -873,13 +1056,21 @@ __global__ void __launch_bounds__(kBlock) k_validate_leaves(const float4* __rest
     const int id = __float_as_int(tris[4 * k].w);
     if (id < 0 || id >= n) atomicAdd(out + V_LEAFIDS, 1ull);
     else atomicAdd(seen + id, 1u);
-    int p = parent[n_nodes + k];
-    int steps = 0;
-    while (p >= 0 && (p >> 1) != 0 && steps < 64) {
-        p = parent[p >> 1];
-        ++steps;
+    const int root = (int)scratch[SCR_ROOT_NODE];
+    // parent walk: must end at the root (parent -1) within the depth bound
+    // (<= 95 levels for the 63-bit code + 32-bit index key)
+    int p = parent[n_nodes + k], last = -1, steps = 0;
+    bool ok = true;
+    while (p != -1) {
+        const int node = p >> 1;
+        if (p < 0 || node >= n_nodes || ++steps > 128) {
+            ok = false;
+            break;
+        }
+        last = node;
+        p = parent[node];
     }
-    if (p < 0 || (p >> 1) != 0) atomicAdd(out + V_UNREACH, 1ull);
+    if (!ok || last != root) atomicAdd(out + V_UNREACH, 1ull);
 }
 
 __global__ void __launch_bounds__(kBlock) k_validate_ids(const uint32_t* __restrict__ seen, int n,
@@ -922,6 +1113,25 @@ static rsi_status_t ensure_capacity(rsi_bvh* h, int64_t n, cudaStream_t s) {
     }
     h->cap_tri = n;
     h->sort_blocks_cap = nb;
+    return RSI_OK;
+}
+
+// RSI_OPT_APETREI workspace: 4 words per triangle + one 64-bit node word
+static rsi_status_t ensure_k63(rsi_bvh* h, int64_t n, cudaStream_t s) {
+    if (n <= h->k63_cap) return RSI_OK;
+    if (h->k63) cudaFreeAsync(h->k63, s);
+    if (h->other) cudaFreeAsync(h->other, s);
+    h->k63 = nullptr;
+    h->other = nullptr;
+    h->k63_cap = 0;
+    cudaError_t e = cudaMallocAsync((void**)&h->k63, (size_t)n * 4 * sizeof(uint32_t), s);
+    if (e == cudaSuccess) e = cudaMallocAsync((void**)&h->other, (size_t)n * sizeof(unsigned long long), s);
+    if (e != cudaSuccess) {
+        (void)cudaGetLastError();
+        return rsi_set_error(RSI_E_OOM, "device allocation for the 63-bit build of %lld triangles failed: %s",
+                             (long long)n, cudaGetErrorString(e));
+    }
+    h->k63_cap = n;
     return RSI_OK;
 }
 
@@ -976,21 +1186,49 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
     if (st != RSI_OK) return st;
     const int n = (int)nt;
     const int n_nodes = n > 1 ? n - 1 : 1;
-    rsi_note_launch(), k_build_init<<<1, 32, 0, s>>>(h->scratch);
+    const bool apetrei = (h->opt.flags & RSI_OPT_APETREI) && n > 1;
+    if (apetrei) {
+        st = ensure_k63(h, nt, s);
+        if (st != RSI_OK) return st;
+    }
+    h->apetrei = apetrei;
+    rsi_note_launch(), k_build_init<<<1, 32, 0, s>>>(h->scratch, apetrei ? 0xffffffffu : 0u);
     int64_t work = nv > 3 * nt ? nv : 3 * nt;
     int eb = rsi_ceil_div(work, kBlock);
     if (eb > 148 * 8) eb = 148 * 8;
     rsi_note_launch(), k_extent_validate<<<eb, kBlock, 0, s>>>(V, nv, T, nt, h->scratch);
-    rsi_note_launch(), k_morton<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, n, h->scratch, h->keys, h->vals, h->arrivals,
-                                                         n_nodes, n <= kRankSortMax ? reinterpret_cast<uint32_t*>(h->vals_tmp) : nullptr);
-    launch_sort(h, n, s);
-    rsi_note_launch(), k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent, h->arrivals);
-    // the refit grid covers every leaf (case study 2: never size it from another
-    // count) -- except under the test-only fault injection option
+    // the construction grid covers every leaf (case study 2: never size it from
+    // another count) -- except under the test-only fault injection option
     const int refit_leaves = (h->opt.debug_refit_leaves > 0 && h->opt.debug_refit_leaves < n)
                                  ? (int)h->opt.debug_refit_leaves : n;
-    rsi_note_launch(), k_refit<<<rsi_ceil_div(refit_leaves, kBlock), kBlock, 0, s>>>(V, nv, T, h->vals, refit_leaves, n, h->nodes,
-                                                                   h->tris, h->parent, h->arrivals, h->scratch);
+    uint32_t* rank = n <= kRankSortMax ? reinterpret_cast<uint32_t*>(h->vals_tmp) : nullptr;
+    if (refit_leaves < n)  // fault injection: untouched nodes hold empty (zero) boxes, not stale memory
+        cudaMemsetAsync(h->nodes, 0, (size_t)n_nodes * 4 * sizeof(float4), s);
+    if (apetrei) {
+        uint32_t* k_lo = h->k63;
+        uint32_t* k_hi = h->k63 + nt;
+        int32_t* ids1 = reinterpret_cast<int32_t*>(h->k63 + 2 * nt);
+        uint32_t* lo_sorted = h->k63 + 3 * nt;
+        rsi_note_launch(), k_morton63<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, n, h->scratch, h->keys, h->vals,
+                                                                                k_lo, k_hi, h->other, rank);
+        launch_sort(h, n, s);  // stable by the low words
+        rsi_note_launch(), k_pass2_prep<<<rsi_ceil_div(n > 32 ? n : 32, kBlock), kBlock, 0, s>>>(
+            h->keys, h->vals, k_hi, ids1, n, n <= kRankSortMax ? reinterpret_cast<uint32_t*>(h->vals_tmp) : nullptr,
+            h->scratch);
+        launch_sort(h, n, s);  // stable by the high words: (hi, lo, index) order
+        rsi_note_launch(), k_pass2_finish<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(h->vals, ids1, k_lo, lo_sorted, n);
+        if (refit_leaves < n)  // fault injection: stale links read as broken, not as valid
+            cudaMemsetAsync(h->parent, 0xfe, (size_t)(n_nodes + n) * sizeof(int32_t), s);
+        rsi_note_launch(), k_apetrei<<<rsi_ceil_div(refit_leaves, kBlock), kBlock, 0, s>>>(
+            V, nv, T, h->vals, h->keys, lo_sorted, refit_leaves, n, h->nodes, h->tris, h->parent, h->other, h->scratch);
+    } else {
+        rsi_note_launch(), k_morton<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, n, h->scratch, h->keys, h->vals,
+                                                                              h->arrivals, n_nodes, rank);
+        launch_sort(h, n, s);
+        rsi_note_launch(), k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent, h->arrivals);
+        rsi_note_launch(), k_refit<<<rsi_ceil_div(refit_leaves, kBlock), kBlock, 0, s>>>(V, nv, T, h->vals, refit_leaves, n, h->nodes,
+                                                                       h->tris, h->parent, h->arrivals, h->scratch);
+    }
     if (kTopNodes > 0) rsi_note_launch(), k_topk<<<1, 1024, 0, s>>>(h->nodes, n_nodes, h->top, h->scratch);
     if (rsi_uses_quads()) rsi_note_launch(), k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads, h->scratch);
     st = rsi_cuda_check(cudaGetLastError(), "build kernel launch");
@@ -1031,6 +1269,7 @@ rsi_status_t rsi_finish_build(rsi_bvh* h, cudaStream_t s) {
         h->scene_hi[x] = root[3 + x];
     }
     h->n_top = kTopNodes > 0 ? (int)h->h_words[SCR_NTOP] : 0;
+    h->root_node = h->h_words[SCR_ROOT_NODE] == 0xffffffffu ? -1 : (int64_t)h->h_words[SCR_ROOT_NODE];
     return RSI_OK;
 }
 
@@ -1043,9 +1282,10 @@ rsi_status_t rsi_validate_device(rsi_bvh* h, rsi_integrity_t* report, cudaStream
     if (st == RSI_OK) st = rsi_cuda_check(cudaMemsetAsync(out, 0, V_WORDS * sizeof(unsigned long long), s), "memset");
     if (st == RSI_OK) st = rsi_cuda_check(cudaMemsetAsync(seen, 0, (size_t)n * sizeof(uint32_t), s), "memset");
     if (st == RSI_OK) {
-        rsi_note_launch(), k_validate_nodes<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n, n_nodes, h->parent, h->arrivals,
-                                                                         out);
-        rsi_note_launch(), k_validate_leaves<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(h->tris, n, n_nodes, h->parent, seen, out);
+        rsi_note_launch(), k_validate_nodes<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(
+            h->nodes, n, n_nodes, h->parent, h->arrivals, h->apetrei ? h->other : nullptr, out);
+        rsi_note_launch(), k_validate_leaves<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(h->tris, n, n_nodes, h->scratch,
+                                                                                      h->parent, seen, out);
         rsi_note_launch(), k_validate_ids<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(seen, n, out);
         st = rsi_cuda_check(cudaGetLastError(), "validate launch");
     }

@@ -37,6 +37,7 @@ enum {
     SCR_QPMAX = 22,     // max |decode offset| over the quad records (float bits, >= 0)
     SCR_QEMIN = 23,     // min / max grid exponent + 128 over the quad records
     SCR_QEMAX = 24,
+    SCR_ROOT_NODE = 25, // root internal node (0 Karras; Apetrei: top split; 0xffffffff unset)
     SCR_SORT_DONE = 32, // 32 words: per-block slice counters of the rank sort
     SCR_WORDS = 64
 };
@@ -68,6 +69,14 @@ struct rsi_bvh {
     int32_t* vals_tmp = nullptr;
     int32_t* parent = nullptr;       // [n_nodes + n_tri]
     uint32_t* arrivals = nullptr;    // [n_nodes]
+    // RSI_OPT_APETREI (63-bit codes + agglomerative build): [4 * cap] words --
+    // code lo / hi words in triangle order, pass-1 ids, sorted lo words -- and
+    // the per-node 64-bit (arrivals << 32 | first bound) words [cap]
+    uint32_t* k63 = nullptr;
+    unsigned long long* other = nullptr;
+    int64_t k63_cap = 0;
+    bool apetrei = false;            // the current tree was built by the Apetrei path
+    int64_t root_node = 0;           // host copy of SCR_ROOT_NODE (valid after the status read)
     uint32_t* hist = nullptr;        // sort: [256 * blocks]
     uint32_t* scratch = nullptr;     // [SCR_WORDS]
     unsigned long long* stats = nullptr;  // [ST_WORDS]

@@ -85,9 +85,13 @@ constexpr bool kQuadCount = RSI_COUNT_QUAD;
 #define RSI_SORT_ALL 1
 #endif
 constexpr int kNoRef = (int)0x80000000;  // "no child" (never a valid ref: ~slot > INT_MIN)
-// binary: depth <= 62 of the index-augmented 62-bit key; quad: <= 31 visits x 3 pushes
-constexpr int kStackBinary = 64;
-constexpr int kStackQuad = 96;
+// tree depth <= 95: a root-to-leaf path has strictly increasing common-prefix
+// lengths of the index-augmented key (<= 63 code bits under RSI_OPT_APETREI,
+// 30 otherwise, + <= 31 levels of index bits for duplicate codes).  Binary
+// walk: one entry per level; quad walk: <= 48 visits x 3 pushes.  Entries
+// beyond the depth a ray reaches are never touched (no traffic).
+constexpr int kStackBinary = 96;
+constexpr int kStackQuad = 144;
 constexpr int kCountCap = 8;  // intercept_count hits held in registers per ray
 #ifndef RSI_BOOL_MINB
 #define RSI_BOOL_MINB 8
@@ -323,11 +327,12 @@ __device__ __forceinline__ void load_tri(const float4* __restrict__ tris, int k,
 // ---------------------------------------------------------------- traversal skeleton
 // leaf(slot) returns true to terminate the walk; tclip may shrink inside it.
 template <class LeafFn>
-__device__ __forceinline__ void traverse(const float4* __restrict__ nodes, const Ray& r, float& tclip,
+__device__ __forceinline__ void traverse(const float4* __restrict__ nodes, int root, const Ray& r, float& tclip,
                                          LeafFn&& leaf) {
     int stack[kStackBinary];
     int sp = 0;
-    int node = 0;
+    int node = root;
+    if (node < 0) return;  // no root (fault-injected build)
     while (true) {
         const float4* nd = nodes + 4 * node;
         float4 n0, n1, n2, n3f;
@@ -816,7 +821,9 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
         ms.te = s_te + threadIdx.x;
         ms.kk = s_k + threadIdx.x;
     }
-    const int root = p.n_top > 0 ? (int)kSmemRef : 0;
+    // root node: 0 for the Karras numbering, the top split under RSI_OPT_APETREI
+    // (-1 when a fault-injected build never reached it: every ray misses)
+    const int root = p.n_top > 0 ? (int)kSmemRef : (int)p.scratch[SCR_ROOT_NODE];
     // 0x4B000000 (float 2^23) from a kernel parameter: an opaque register, so the
     // quad decode's PRMTs keep their byte selectors as immediates
     const uint32_t magic = p.magic;
@@ -1171,7 +1178,7 @@ __global__ void __launch_bounds__(kThreads) k_ovf_size(const float4* __restrict_
     load_ray(r, S, E, list[j], nonfinite);
     int nh = 0;
     float tclip = 1.0f;
-    traverse(nodes, r, tclip, [&](int k) {
+    traverse(nodes, (int)scratch[SCR_ROOT_NODE], r, tclip, [&](int k) {
         float4 A, B, C;
         load_tri(tris, k, A, B, C);
         float t32, et;
@@ -1188,7 +1195,8 @@ __global__ void __launch_bounds__(kThreads) k_ovf_count(const float4* __restrict
                                                         const float4* __restrict__ tris, const float* __restrict__ S,
                                                         const float* __restrict__ E, const int32_t* __restrict__ list,
                                                         int n_ovf, const int32_t* __restrict__ seg, double* pool,
-                                                        double tau, int32_t* __restrict__ count_out) {
+                                                        double tau, int32_t* __restrict__ count_out,
+                                                        const uint32_t* __restrict__ scratch) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n_ovf) return;
     Ray r;
@@ -1199,7 +1207,7 @@ __global__ void __launch_bounds__(kThreads) k_ovf_count(const float4* __restrict
     const int cap = seg[2 * j + 1];
     int nh = 0;
     float tclip = 1.0f;
-    traverse(nodes, r, tclip, [&](int k) {
+    traverse(nodes, (int)scratch[SCR_ROOT_NODE], r, tclip, [&](int k) {
         float4 A, B, C;
         load_tri(tris, k, A, B, C);
         double t64;
@@ -1434,7 +1442,7 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
         return RSI_E_OOM;
     }
     rsi_note_launch(), k_ovf_count<<<nb, kThreads, 0, s>>>(h->nodes, h->tris, S, E, h->ovf_list, n_ovf, seg, pool, h->opt.dedup_tau,
-                                        out->count);
+                                        out->count, h->scratch);
     st = rsi_cuda_check(cudaGetLastError(), "overflow pass");
     cudaFreeAsync(pool, s);
     cudaFreeAsync(seg, s);

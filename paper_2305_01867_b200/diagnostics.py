@@ -31,7 +31,11 @@ def leaf_ranges(d: dict) -> np.ndarray:
     if d["n_triangles"] == 1:
         rng[0] = (0, 0)
         return rng
-    stack = [(0, False)]
+    root = int(d.get("root", 0))
+    if root < 0:  # the construction never reached the root (fault injection)
+        return rng
+    seen = np.zeros(nn, bool)
+    stack = [(root, False)]
     while stack:
         i, done = stack.pop()
         if done:
@@ -44,9 +48,10 @@ def leaf_ranges(d: dict) -> np.ndarray:
                     lo.append(rng[c, 0])
                     hi.append(rng[c, 1])
             rng[i] = (min(lo), max(hi))
-        else:
+        elif not seen[i]:  # (a broken tree may repeat or cycle)
+            seen[i] = True
             stack.append((i, True))
-            stack.extend((int(c), False) for c in child[i] if c >= 0)
+            stack.extend((int(c), False) for c in child[i] if 0 <= c < nn)
     return rng
 
 
@@ -59,16 +64,24 @@ def dump_text(d: dict) -> str:
     child, box, parent, arr = d["child"], d["box"], d["parent"], d["arrivals"]
     nn, nt = child.shape[0], d["n_triangles"]
     rng = leaf_ranges(d)
+    root = int(d.get("root", 0))
     out = ["BVH tree structure", "---------------------------", "Internal nodes"]
     for i in range(nn):
         kinds = ["leaf" if c < 0 else "internal" for c in child[i]]
         refs = [(~c if c < 0 else c) for c in child[i]]
-        tag = "  ------ ROOT NODE" if i == 0 else ""
+        tag = "  ------ ROOT NODE" if i == root else ""
         par = "" if parent[i] < 0 else str(parent[i] >> 1)
         out.append(f"[{i}] {_fmt_box(_box_union(box[i]))}{tag}")
         out.append(f"self: {i}, parent: {par}")
         out.append(f"indices: {i}(self), {refs[0]}(L-{kinds[0]}), {refs[1]}(R-{kinds[1]})")
         out.append(f"atomic: {arr[i]}, rangeL: {rng[i, 0]}, rangeR: {rng[i, 1]}")
+        out.append("")
+    sent = int(d.get("sentinel", -1))
+    if sent >= 0:  # Apetrei numbering: node N_t - 1 only points at the root
+        out.append(f"[{sent}] x:[0,0], y:[0,0], z:[0,0]")
+        out.append(f"self: {sent}, parent: ")
+        out.append(f"indices: {sent}(self), {root}(L-internal), 0(R-internal)")
+        out.append("atomic: 0, rangeL: 0, rangeR: -1")
         out.append("")
     out += ["---------------------------", "Leaf nodes"]
     slot_box = {}

@@ -25,6 +25,7 @@ MODES = {"boolean": 0, "barycentric": 1, "intercept_count": 2}
 OPT_FP64_MOLLER = 1
 OPT_COUNTERS = 2
 OPT_DEFERRED_STATUS = 4
+OPT_APETREI = 8
 
 _lock = threading.Lock()
 _lib = None
@@ -74,7 +75,7 @@ def load():
             return _lib
         path = os.environ.get("RSI_LIB", _build.LIB)  # variant builds for tuning sweeps
         if not os.path.exists(path):
-            raise RuntimeError(f"{_build.LIB} is missing: run __graft_entry__.build() "
+            raise RuntimeError(f"{path} is missing: run __graft_entry__.build() "
                                "(nvcc sm_100a); there is no CPU fallback")
         lib = ctypes.CDLL(path)
         sig = {
@@ -94,6 +95,7 @@ def load():
             "rsi_bvh_info": ([_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _p, _p], ctypes.c_int),
             "rsi_bvh_download": ([_p, _p, _p, _p, _p, _p, _p, _p], ctypes.c_int),
             "rsi_validate": ([_p, ctypes.POINTER(_Integrity), _p], ctypes.c_int),
+            "rsi_bvh_root": ([_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _p, _p], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(lib, name)
@@ -144,10 +146,11 @@ class Options:
     counters: bool = False      # instrumented kernels: box / MT test counts in rsi_get_stats
     debug_refit_leaves: int = 0  # FAULT INJECTION (tests): refit only the first k leaves
     deferred_status: bool = False  # rsi_build/rsi_rebuild do not wait: check rsi_build_status
+    apetrei: bool = False       # NEXT-1: 63-bit Morton codes + Apetrei build
 
     def _c(self) -> _Options:
         flags = ((OPT_FP64_MOLLER if self.fp64_moller else 0) | (OPT_COUNTERS if self.counters else 0)
-                 | (OPT_DEFERRED_STATUS if self.deferred_status else 0))
+                 | (OPT_DEFERRED_STATUS if self.deferred_status else 0) | (OPT_APETREI if self.apetrei else 0))
         return _Options(ctypes.sizeof(_Options), flags, float(self.dedup_tau), int(self.debug_refit_leaves))
 
 
@@ -359,7 +362,17 @@ def rsi_bvh_download(h: Handle, stream=None) -> dict:
     ptrs = [d[k].ctypes.data_as(_p) for k in ("child", "box", "leaf_tri", "morton", "parent", "arrivals")]
     _check(load().rsi_bvh_download(h.ptr, *ptrs, _stream(stream)))
     d.update(info)
+    d.update(rsi_bvh_root(h, stream))
     return d
+
+
+def rsi_bvh_root(h: Handle, stream=None) -> dict:
+    """Root node, sentinel (-1 unless RSI_OPT_APETREI) and the sorted full-width codes."""
+    root, sent = _i64(), _i64()
+    n = rsi_bvh_info(h)["n_triangles"]
+    m63 = np.zeros(n, np.uint64)
+    _check(load().rsi_bvh_root(h.ptr, ctypes.byref(root), ctypes.byref(sent), m63.ctypes.data_as(_p), _stream(stream)))
+    return {"root": root.value, "sentinel": sent.value, "morton63": m63}
 
 
 def rsi_validate(h: Handle, stream=None) -> dict:

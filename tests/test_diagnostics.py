@@ -53,3 +53,40 @@ def test_leaf_ranges_one_triangle():
     assert diagnostics.leaf_ranges(d).tolist() == [[0, 0]]
     dot = diagnostics.to_dot(d)
     assert dot.count("->") == 1 and 'label="[0] 0"' in dot
+
+
+def apetrei_fixture_tree(golden):
+    """The same tree in the paper's own numbering (golden 'apetrei'
+    rows): root = node 1, sentinel = node 3."""
+    g = golden("fig3_case_study1.txt")
+    base = fixture_tree(golden)
+    rows = {int(r[0]): r for r in g["apetrei"]}
+    child = np.zeros((3, 2), np.int32)
+    for i in range(3):
+        r = rows[i]
+        child[i] = [int(r[2]) if r[1] == "internal" else ~int(r[2]), int(r[4]) if r[3] == "internal" else ~int(r[4])]
+    # Karras node k -> paper node: 0 (root) -> 1, 1 ([0,1]) -> 0, 2 ([2,3]) -> 2
+    box = np.stack([base["box"][1], base["box"][0], base["box"][2]])
+    parent = np.array([1 << 1 | 0, -1, 1 << 1 | 1, 0 << 1 | 0, 0 << 1 | 1, 2 << 1 | 0, 2 << 1 | 1], np.int32)
+    return {**base, "child": child, "box": box, "parent": parent, "root": 1, "sentinel": 3}
+
+
+def test_apetrei_numbering_dump(golden):
+    """NEXT-1 host formatting: the dump in the paper's numbering reproduces the
+    printed indices, ranges, root tag and sentinel of P:304-328."""
+    g = golden("fig3_case_study1.txt")
+    d = apetrei_fixture_tree(golden)
+    rng = diagnostics.leaf_ranges(d)
+    for r in g["apetrei"]:
+        i = int(r[0])
+        if i < 3:
+            assert rng[i].tolist() == [int(r[6]), int(r[7])]
+    txt = diagnostics.dump_text(d)
+    assert "[1] x:[12,13], y:[2,3], z:[1,1.3]  ------ ROOT NODE" in txt
+    assert "indices: 0(self), 0(L-leaf), 1(R-leaf)" in txt
+    assert "indices: 1(self), 0(L-internal), 2(R-internal)" in txt
+    assert "indices: 3(self), 1(L-internal), 0(R-internal)" in txt
+    assert "atomic: 0, rangeL: 0, rangeR: -1" in txt
+    dot = diagnostics.to_dot(d)
+    for lab in ("[0,3]", "[0,1]", "[2,3]", "[0] 0", "[1] 3", "[2] 1", "[3] 2"):
+        assert f'label="{lab}"' in dot

@@ -536,3 +536,116 @@ def test_launch_counter(rsi):
     rsi.rsi_rebuild(h, Vd, Td)
     assert rsi.rsi_launch_count() - (c1 + 3) == c1 - c0
     h.free()
+
+
+# ------------------------------------------------------------------ NEXT-1: 63-bit Morton + Apetrei build
+
+def _morton63_ref(V, T):
+    """Bit-loop reference of the 63-bit z-major code on fp32 centroids (reading
+    R8 scaled to 21 bits per axis)."""
+    lo, hi = V.min(0), V.max(0)
+    c = (V[T[:, 0]] + V[T[:, 1]] + V[T[:, 2]]) / np.float32(3)
+    w = np.maximum(hi - lo, (hi - lo).max() * np.float32(1 / 64))
+    q = np.clip(np.floor((c - lo) / w * np.float32(2 ** 21)), 0, 2 ** 21 - 1).astype(np.uint64)
+    code = np.zeros(len(T), np.uint64)
+    for b in range(21):
+        for a in range(3):
+            code |= ((q[:, a] >> np.uint64(b)) & np.uint64(1)) << np.uint64(3 * b + a)
+    return code
+
+
+def test_apetrei_fixture_numbering(rsi, golden):
+    """The paper's own tree for the Fig. 3 fixture: root = node 1,
+    node i splits leaves i | i+1, sentinel 3 -> root, leaf order T0 T3 T1 T2,
+    every node reached twice ("atomic: 2")."""
+    from paper_2305_01867_b200 import diagnostics
+    g = golden("fig3_case_study1.txt")
+    V, T = synth.fixture()
+    Vd, Td = to_dev(V, T)
+    h = rsi.rsi_build(Vd, Td, rsi.Options(apetrei=True))
+    d = rsi.rsi_bvh_download(h)
+    assert rsi.rsi_validate(h)["ok"]
+    h.free()
+    assert d["root"] == 1 and d["sentinel"] == 3
+    assert d["leaf_tri"].tolist() == [int(r[1]) for r in g["leaf"]]
+    for r in g["apetrei"]:
+        i = int(r[0])
+        if i == 3:
+            continue
+        exp = [int(r[2]) if r[1] == "internal" else ~int(r[2]), int(r[4]) if r[3] == "internal" else ~int(r[4])]
+        assert d["child"][i].tolist() == exp, i
+        assert d["arrivals"][i] == int(r[5])
+    nodes = {(int(r[0]), int(r[1])): np.array(r[2:], np.float32) for r in g["node"]}
+    rng = diagnostics.leaf_ranges(d)
+    for i in range(3):
+        b = diagnostics._box_union(d["box"][i])
+        np.testing.assert_allclose([b[0], b[3], b[1], b[4], b[2], b[5]], nodes[tuple(rng[i])], atol=1e-6)
+    assert (d["morton"] == (d["morton63"] >> np.uint64(33)).astype(np.uint32)).all()
+    txt = diagnostics.dump_text(d)
+    assert "[1] x:[12,13], y:[2,3], z:[1,1.3]  ------ ROOT NODE" in txt
+    assert "indices: 3(self), 1(L-internal), 0(R-internal)" in txt
+
+
+@pytest.mark.parametrize("nt", [2, 3, 17, 1000, 16_384, 16_385, 70_001, "dup", "flat"])
+def test_apetrei_tree_integrity(rsi, nt):
+    """63-bit codes equal a bit-loop encoding in stable sorted order (rank-sort
+    and radix paths, full 32-bit low words); the validator finds no violation;
+    node i is the split between leaves i and i+1 (the paper's numbering)."""
+    from paper_2305_01867_b200 import diagnostics
+    kind = nt if isinstance(nt, str) else ""
+    nt = 12_000 if kind else nt
+    rng = np.random.default_rng(nt + len(kind))
+    V = rng.uniform(-3, 7, (3 * nt, 3)).astype(np.float32)
+    if kind == "flat":
+        V[:, 2] *= np.float32(1e-3)
+    T = rng.permutation(3 * nt).reshape(nt, 3).astype(np.int32)
+    if kind == "dup":
+        T = T[:40][rng.integers(0, 40, nt)]
+    Vd, Td = to_dev(V, T)
+    h = rsi.rsi_build(Vd, Td, rsi.Options(apetrei=True))
+    rep = rsi.rsi_validate(h)
+    d = rsi.rsi_bvh_download(h)
+    h.free()
+    assert rep["ok"], rep
+    code = _morton63_ref(V, T)
+    order = np.argsort(code, kind="stable")
+    assert (d["morton63"] == code[order]).all()
+    assert (d["leaf_tri"] == order).all()
+    assert (d["arrivals"] == 2).all() and d["sentinel"] == nt - 1
+    lr = diagnostics.leaf_ranges(d)
+    assert lr[d["root"]].tolist() == [0, nt - 1]
+    for i in range(nt - 1):
+        c = d["child"][i]
+        left_hi = ~c[0] if c[0] < 0 else lr[c[0], 1]
+        right_lo = ~c[1] if c[1] < 0 else lr[c[1], 0]
+        assert left_hi == i and right_lo == i + 1
+
+
+def test_apetrei_parity_all_modes(rsi):
+    """Same results as the default build (and the oracle) on the bench mesh,
+    the folded terrain and rays through vertices/edges."""
+    V, T, S, E, _ = synth.workload("sphere", 20_011, seed=3)
+    assert_parity(run_all(rsi, V, T, S, E, rsi.Options(apetrei=True)), oracle.run(V, T, S, E), S, E, "sphere")
+    V, T, S, E, _ = synth.workload("terrain", 4_000, seed=4)
+    assert_parity(run_all(rsi, V, T, S, E, rsi.Options(apetrei=True)), oracle.run(V, T, S, E), S, E, "terrain")
+    V, T = synth.cube()
+    S, E = synth.box_rays(5_000, -0.5, 1.5, seed=1)
+    assert_parity(run_all(rsi, V, T, S, E, rsi.Options(apetrei=True)), oracle.run(V, T, S, E), S, E, "cube")
+
+
+def test_apetrei_fault_injection_signatures(rsi):
+    """Case study 2 on the paper's construction: an under-sized
+    grid leaves half-filled and untouched nodes, leaves not connected to the
+    root and no root; every ray then misses (no crash)."""
+    V, T = synth.paper_terrain()
+    Vd, Td = to_dev(V, T)
+    h = rsi.rsi_build(Vd, Td, rsi.Options(apetrei=True, debug_refit_leaves=16 * 1024))
+    rep = rsi.rsi_validate(h)
+    assert not rep["ok"]
+    assert rep["half_filled"] > 0 and rep["untouched"] > 0 and rep["root_ok"] == 0
+    assert rep["unreachable_leaves"] > 0
+    assert rsi.rsi_bvh_root(h)["root"] == -1
+    S, E = synth.vertical_rays(1000, V, seed=4)
+    Sd, Ed = to_dev(S, E)
+    assert int(rsi.rsi_intersect(h, Sd, Ed, "boolean")["hit"].sum()) == 0
+    h.free()

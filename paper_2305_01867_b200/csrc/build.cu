@@ -154,11 +154,12 @@ __global__ void __launch_bounds__(kBlock) k_morton(const float* __restrict__ V, 
 }
 
 // ------------------------------------------------------------------ A4: radix sort
-// Stable LSD sort, 8-bit digits, 4 passes over the 30-bit keys.  Stability of
-// each pass comes from warp-ordered ranking: a warp walks its contiguous
-// segment 32 keys at a time, lanes in index order, and ranks equal digits with
-// __match_any_sync; per-warp digit counts are scanned over warps, then over
-// digits (and, for the multi-block path, over blocks in digit-major order).
+// N_t <= 16384: the one-launch rank sort (k_sort_rank below).  Larger: stable
+// LSD radix sort, 8-bit digits, 4 passes (histogram / scan / scatter per pass).
+// Stability of each pass comes from warp-ordered ranking: a warp walks its
+// contiguous segment 32 keys at a time, lanes in index order, and ranks equal
+// digits with ballots (digit_peers); per-warp digit counts are scanned over
+// warps, then over blocks per digit (k_sort_rowscan), then over digits.
 constexpr int kDigits = 256;
 constexpr int kPasses = 4;
 
@@ -242,44 +243,6 @@ __device__ __forceinline__ void warp_scatter(const uint32_t* __restrict__ ks, co
     }
 }
 
-constexpr int kSmallThreads = 1024;
-constexpr int kSmallMax = 1 << 16;  // single-CTA sort up to 64 Ki keys
-
-// Whole sort in one CTA (N_t <= 64 Ki): no inter-block traffic, one launch.
-__global__ void __launch_bounds__(kSmallThreads) k_sort_small(uint32_t* ka, int32_t* va, uint32_t* kb,
-                                                              int32_t* vb, int n) {
-    __shared__ uint32_t wcnt[32][kDigits + 1];
-    __shared__ uint32_t dbase[kDigits];
-    const int w = threadIdx.x >> 5;
-    const int seg = (((n + 31) / 32) + 31) & ~31;
-    const int beg = min(w * seg, n), end = min(beg + seg, n);
-    for (int p = 0; p < kPasses; ++p) {
-        const uint32_t* ks = (p & 1) ? kb : ka;
-        const int32_t* vs = (p & 1) ? vb : va;
-        uint32_t* kd = (p & 1) ? ka : kb;
-        int32_t* vd = (p & 1) ? va : vb;
-        const int shift = 8 * p;
-        for (int i = threadIdx.x; i < 32 * (kDigits + 1); i += blockDim.x) (&wcnt[0][0])[i] = 0u;
-        __syncthreads();
-        warp_count(ks, beg, end, shift, wcnt[w]);
-        __syncthreads();
-        if (threadIdx.x < kDigits) {
-            uint32_t s = 0;
-            for (int x = 0; x < 32; ++x) {
-                uint32_t c = wcnt[x][threadIdx.x];
-                wcnt[x][threadIdx.x] = s;
-                s += c;
-            }
-            dbase[threadIdx.x] = s;
-        }
-        __syncthreads();
-        if (w == 0) warp_scan256(dbase);
-        __syncthreads();
-        warp_scatter(ks, vs, kd, vd, beg, end, shift, wcnt[w], dbase);
-        __syncthreads();
-    }
-}
-
 constexpr int kTileThreads = 512;
 constexpr int kTileWarps = kTileThreads / 32;
 constexpr int kTile = 4096;  // keys per block (256 per warp)
@@ -295,44 +258,50 @@ __global__ void __launch_bounds__(kTileThreads) k_sort_hist(const uint32_t* __re
     for (int d = threadIdx.x; d < kDigits; d += blockDim.x) hist[(size_t)d * gridDim.x + blockIdx.x] = cnt[d];
 }
 
-// Exclusive scan of hist[0..m) in place (digit-major over blocks); one CTA.
-__global__ void __launch_bounds__(1024) k_sort_scan(uint32_t* hist, int m) {
-    __shared__ uint32_t wsum[32];
-    __shared__ uint32_t carry;
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int base = 0; base < m; base += 1024) {
-        int i = base + threadIdx.x;
-        uint32_t v = i < m ? hist[i] : 0u, inc = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
-        }
-        if (lane == 31) wsum[w] = inc;
-        __syncthreads();
-        if (w == 0) {
-            uint32_t s = wsum[lane], si = s;
-            for (int o = 1; o < 32; o <<= 1) {
-                uint32_t y = __shfl_up_sync(0xffffffffu, si, o);
-                if (lane >= o) si += y;
-            }
-            wsum[lane] = si - s;
-        }
-        __syncthreads();
-        if (i < m) hist[i] = carry + wsum[w] + inc - v;
-        __syncthreads();
-        if (threadIdx.x == 1023) carry += wsum[31] + inc;
-        __syncthreads();
+// Exclusive scan of each digit's row hist[d][0..nb) in place, one CTA per
+// digit; the row totals go to rows[d] (the scatter scans those 256 itself).
+// Each thread owns a contiguous run of ceil(nb / 256) counters: one at
+// N_t <= 1 Mi (a single CTA looping over all 256 x nb counters with a carried
+// dependence took 50-60 us per pass at N_t = 1e6).
+__global__ void __launch_bounds__(kDigits) k_sort_rowscan(uint32_t* __restrict__ hist, int nb,
+                                                          uint32_t* __restrict__ rows) {
+    __shared__ uint32_t wsum[kDigits / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t* row = hist + (size_t)blockIdx.x * nb;
+    const int per = (nb + kDigits - 1) / kDigits;
+    const int beg = min((int)threadIdx.x * per, nb), end = min(beg + per, nb);
+    uint32_t sum = 0;
+    for (int i = beg; i < end; ++i) sum += row[i];
+    uint32_t inc = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += y;
     }
+    if (lane == 31) wsum[w] = inc;
+    __syncthreads();
+    uint32_t base = 0, total = 0;
+    for (int x = 0; x < kDigits / 32; ++x) {
+        base += x < w ? wsum[x] : 0u;
+        total += wsum[x];
+    }
+    uint32_t run = base + inc - sum;
+    for (int i = beg; i < end; ++i) {
+        const uint32_t v = row[i];
+        row[i] = run;
+        run += v;
+    }
+    if (threadIdx.x == 0) rows[blockIdx.x] = total;
 }
 
 __global__ void __launch_bounds__(kTileThreads) k_sort_scatter(const uint32_t* __restrict__ ks,
                                                                const int32_t* __restrict__ vs,
                                                                uint32_t* __restrict__ kd, int32_t* __restrict__ vd,
-                                                               int n, int shift, const uint32_t* __restrict__ hist) {
+                                                               int n, int shift, const uint32_t* __restrict__ hist,
+                                                               const uint32_t* __restrict__ rows) {
     __shared__ uint32_t wcnt[kTileWarps][kDigits + 1];
     __shared__ uint32_t dbase[kDigits];
+    __shared__ uint32_t s_rows[kDigits];
+    if (threadIdx.x < kDigits) s_rows[threadIdx.x] = rows[threadIdx.x];
     const int w = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < kTileWarps * (kDigits + 1); i += blockDim.x) (&wcnt[0][0])[i] = 0u;
     __syncthreads();
@@ -341,6 +310,8 @@ __global__ void __launch_bounds__(kTileThreads) k_sort_scatter(const uint32_t* _
     const int end = min(beg + kTile / kTileWarps, n);
     warp_count(ks, beg, end, shift, wcnt[w]);
     __syncthreads();
+    if (w == 0) warp_scan256(s_rows);  // digit bases: exclusive scan of the row totals
+    __syncthreads();
     if (threadIdx.x < kDigits) {
         uint32_t s = 0;
         for (int x = 0; x < kTileWarps; ++x) {
@@ -348,7 +319,7 @@ __global__ void __launch_bounds__(kTileThreads) k_sort_scatter(const uint32_t* _
             wcnt[x][threadIdx.x] = s;
             s += c;
         }
-        dbase[threadIdx.x] = hist[(size_t)threadIdx.x * gridDim.x + blockIdx.x];
+        dbase[threadIdx.x] = s_rows[threadIdx.x] + hist[(size_t)threadIdx.x * gridDim.x + blockIdx.x];
     }
     __syncthreads();
     warp_scatter(ks, vs, kd, vd, beg, end, shift, wcnt[w], dbase);
@@ -487,57 +458,6 @@ __global__ void __launch_bounds__(kBlock) k_refit(const float* __restrict__ V, i
         root[3 + x] = hi[x];
     }
     scratch[SCR_ROOT_SET] = 1u;
-}
-
-// Whole sort in one CTA with keys and values resident in shared memory
-// (N_t <= kSmemSortMax): no global-memory latency inside the passes.
-constexpr int kSmemSortMax = 10240;
-
-__global__ void __launch_bounds__(kSmallThreads) k_sort_smem(uint32_t* gk, int32_t* gv, int n) {
-    extern __shared__ uint32_t sm[];
-    uint32_t* ka = sm;
-    int32_t* va = reinterpret_cast<int32_t*>(sm + n);
-    uint32_t* kb = sm + 2 * n;
-    int32_t* vb = reinterpret_cast<int32_t*>(sm + 3 * n);
-    __shared__ uint32_t wcnt[32][kDigits + 1];
-    __shared__ uint32_t dbase[kDigits];
-    const int tid = threadIdx.x, w = tid >> 5;
-    for (int j = tid; j < n; j += kSmallThreads) {
-        ka[j] = gk[j];
-        va[j] = gv[j];
-    }
-    __syncthreads();
-    const int seg = (((n + 31) / 32) + 31) & ~31;
-    const int beg = min(w * seg, n), end = min(beg + seg, n);
-    for (int pass = 0; pass < kPasses; ++pass) {
-        const uint32_t* ks = (pass & 1) ? kb : ka;
-        const int32_t* vs = (pass & 1) ? vb : va;
-        uint32_t* kd = (pass & 1) ? ka : kb;
-        int32_t* vd = (pass & 1) ? va : vb;
-        const int shift = 8 * pass;
-        for (int i = tid; i < 32 * (kDigits + 1); i += kSmallThreads) (&wcnt[0][0])[i] = 0u;
-        __syncthreads();
-        warp_count(ks, beg, end, shift, wcnt[w]);
-        __syncthreads();
-        if (tid < kDigits) {
-            uint32_t sum = 0;
-            for (int x = 0; x < 32; ++x) {
-                const uint32_t c = wcnt[x][tid];
-                wcnt[x][tid] = sum;
-                sum += c;
-            }
-            dbase[tid] = sum;
-        }
-        __syncthreads();
-        if (w == 0) warp_scan256(dbase);
-        __syncthreads();
-        warp_scatter(ks, vs, kd, vd, beg, end, shift, wcnt[w], dbase);
-        __syncthreads();
-    }
-    for (int j = tid; j < n; j += kSmallThreads) {
-        gk[j] = ka[j];
-        gv[j] = va[j];
-    }
 }
 
 // Small meshes (N_t <= kRankSortMax): the sorted position of key i is its rank
@@ -1102,7 +1022,7 @@ static rsi_status_t ensure_capacity(rsi_bvh* h, int64_t n, cudaStream_t s) {
     RSI_ALLOC(h->vals_tmp, n * sizeof(int32_t));
     RSI_ALLOC(h->parent, (nn + n) * sizeof(int32_t));
     RSI_ALLOC(h->arrivals, nn * sizeof(uint32_t));
-    RSI_ALLOC(h->hist, (size_t)kDigits * nb * sizeof(uint32_t));
+    RSI_ALLOC(h->hist, (size_t)kDigits * (nb + 1) * sizeof(uint32_t));  // + the 256 row totals
 #undef RSI_ALLOC
     if (e != cudaSuccess) {
         h->cap_tri = 0;
@@ -1151,19 +1071,6 @@ static void launch_sort(rsi_bvh* h, int n, cudaStream_t s) {
         h->keys_tmp = t;
         return;
     }
-    if (n <= kSmemSortMax) {
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_sort_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * kSmemSortMax);
-            attr = true;
-        }
-        rsi_note_launch(), k_sort_smem<<<1, kSmallThreads, (size_t)16 * n, s>>>(h->keys, h->vals, n);
-        return;
-    }
-    if (n <= kSmallMax) {
-        rsi_note_launch(), k_sort_small<<<1, kSmallThreads, 0, s>>>(h->keys, h->vals, h->keys_tmp, h->vals_tmp, n);
-        return;
-    }
     int nb = rsi_ceil_div(n, kTile);
     for (int p = 0; p < kPasses; ++p) {
         uint32_t* ks = (p & 1) ? h->keys_tmp : h->keys;
@@ -1171,8 +1078,9 @@ static void launch_sort(rsi_bvh* h, int n, cudaStream_t s) {
         uint32_t* kd = (p & 1) ? h->keys : h->keys_tmp;
         int32_t* vd = (p & 1) ? h->vals : h->vals_tmp;
         rsi_note_launch(), k_sort_hist<<<nb, kTileThreads, 0, s>>>(ks, n, 8 * p, h->hist);
-        rsi_note_launch(), k_sort_scan<<<1, 1024, 0, s>>>(h->hist, kDigits * nb);
-        rsi_note_launch(), k_sort_scatter<<<nb, kTileThreads, 0, s>>>(ks, vs, kd, vd, n, 8 * p, h->hist);
+        rsi_note_launch(), k_sort_rowscan<<<kDigits, kDigits, 0, s>>>(h->hist, nb, h->hist + (size_t)kDigits * nb);
+        rsi_note_launch(), k_sort_scatter<<<nb, kTileThreads, 0, s>>>(ks, vs, kd, vd, n, 8 * p, h->hist,
+                                                                      h->hist + (size_t)kDigits * nb);
     }
 }
 

@@ -492,31 +492,34 @@ __global__ void __launch_bounds__(kRankT) k_sort_rank(const uint32_t* __restrict
         ki[a] = idx[a] < n ? keys[idx[a]] : 0u;
         cnt[a] = 0u;
     }
-    if (j1 <= i_lo) {  // slice wholly below this block's keys: count k_j <= k_i
+    if (j1 <= i_lo || j0 >= i_hi) {  // slice wholly below / above this block's keys
+        const uint32_t add = j1 <= i_lo ? 1u : 0u;
+        uint32_t thr[kRankPer];
+#pragma unroll
+        for (int a = 0; a < kRankPer; ++a) thr[a] = ki[a] + add;
         for (int q = 0; q < nj4; ++q) {
             const uint4 k4 = s_k4[q];
 #pragma unroll
             for (int a = 0; a < kRankPer; ++a)
-                cnt[a] += (k4.x <= ki[a]) + (k4.y <= ki[a]) + (k4.z <= ki[a]) + (k4.w <= ki[a]);
+                cnt[a] += (k4.x < thr[a]) + (k4.y < thr[a]) + (k4.z < thr[a]) + (k4.w < thr[a]);
         }
-        // the 0xffffffff pads were counted only for a key equal to 0xffffffff
-        // (full 32-bit words of the 63-bit codes)
+        // a key of 0xffffffff (possible in the 63-bit path's full low words):
+        // k_i + 1 wrapped to 0 -- every key of a slice below counts
 #pragma unroll
         for (int a = 0; a < kRankPer; ++a)
-            if (ki[a] == 0xffffffffu) cnt[a] -= (uint32_t)(4 * nj4 - nj);
-    } else if (j0 >= i_hi) {  // wholly above: count k_j < k_i (pads never are)
-        for (int q = 0; q < nj4; ++q) {
-            const uint4 k4 = s_k4[q];
-#pragma unroll
-            for (int a = 0; a < kRankPer; ++a)
-                cnt[a] += (k4.x < ki[a]) + (k4.y < ki[a]) + (k4.z < ki[a]) + (k4.w < ki[a]);
-        }
+            if (add && ki[a] == 0xffffffffu) cnt[a] = (uint32_t)nj;
     } else {  // overlapping (diagonal) slice: per-pair index test
         for (int j = 0; j < nj; ++j) {
             const uint32_t kj = s_k[j];
 #pragma unroll
-            for (int a = 0; a < kRankPer; ++a) cnt[a] += (kj < ki[a]) || (kj == ki[a] && j0 + j < idx[a]);
+            for (int a = 0; a < kRankPer; ++a) cnt[a] += (kj < ki[a] + (j0 + j < idx[a] ? 1u : 0u));
         }
+#pragma unroll
+        for (int a = 0; a < kRankPer; ++a)
+            if (ki[a] == 0xffffffffu) {  // the +1 wrapped: recount exactly (rare)
+                cnt[a] = 0u;
+                for (int j = 0; j < nj; ++j) cnt[a] += (s_k[j] != 0xffffffffu) || (j0 + j < idx[a]);
+            }
     }
 #pragma unroll
     for (int a = 0; a < kRankPer; ++a)

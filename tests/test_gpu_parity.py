@@ -649,3 +649,30 @@ def test_apetrei_fault_injection_signatures(rsi):
     Sd, Ed = to_dev(S, E)
     assert int(rsi.rsi_intersect(h, Sd, Ed, "boolean")["hit"].sum()) == 0
     h.free()
+
+
+def test_apetrei_sort_full_low_words(rsi):
+    """The 63-bit path sorts the low 32 code bits as a full-range key: codes
+    whose low word is 0xffffffff (q_x, q_y = ...11111111111, q_z = ...1111111111)
+    must still sort stably (the rank sort's k+1 wraps there)."""
+    rng = np.random.default_rng(7)
+    pts = [np.zeros(3), np.ones(3)]                      # extent [0,1]^3: q = floor(c * 2^21)
+    for _ in range(1500):                                # low word all ones, varied high bits
+        hx, hy, hz = rng.integers(0, 1024, 3)
+        q = np.array([hx * 2048 + 2047, hy * 2048 + 2047, hz * 1024 + 1023], np.float64)
+        pts.append((q + 0.5) / 2 ** 21)
+    pts += list(rng.uniform(0, 1, (1500, 3)))
+    P = np.asarray(pts, np.float32)
+    V = np.repeat(P, 3, axis=0)                          # point-like triangles: centroid = the point
+    T = np.arange(len(V), dtype=np.int32).reshape(-1, 3)
+    T = T[rng.permutation(len(T))]
+    Vd, Td = to_dev(V, T)
+    h = rsi.rsi_build(Vd, Td, rsi.Options(apetrei=True))
+    d = rsi.rsi_bvh_download(h)
+    assert rsi.rsi_validate(h)["ok"]
+    h.free()
+    code = _morton63_ref(V, T)
+    assert int(((code & np.uint64(0xffffffff)) == np.uint64(0xffffffff)).sum()) >= 1000
+    order = np.argsort(code, kind="stable")
+    assert (d["morton63"] == code[order]).all()
+    assert (d["leaf_tri"] == order).all()

@@ -381,8 +381,10 @@ __global__ void __launch_bounds__(kBlock) k_karras(const uint32_t* __restrict__ 
     int32_t right = (hi == gamma + 1) ? ~(gamma + 1) : gamma + 1;
     set_ref(nodes, i, 0, left);
     set_ref(nodes, i, 1, right);
-    reinterpret_cast<int32_t*>(nodes + 4 * i + 3)[2] = 0;
-    reinterpret_cast<int32_t*>(nodes + 4 * i + 3)[3] = 0;
+    // leaf range of node i in the (otherwise unused) last two words: the refit
+    // uses it to keep ascents inside a CTA's leaf window in shared memory
+    reinterpret_cast<int32_t*>(nodes + 4 * i + 3)[2] = lo;
+    reinterpret_cast<int32_t*>(nodes + 4 * i + 3)[3] = hi;
     parent[left >= 0 ? left : n_nodes + ~left] = (i << 1) | 0;
     parent[right >= 0 ? right : n_nodes + ~right] = (i << 1) | 1;
     if (i == 0) parent[0] = -1;
@@ -401,17 +403,45 @@ __device__ __forceinline__ void write_slot(float4* nodes, int node, int side, co
 }
 
 // One thread per leaf slot k: pack triangle k (Morton order), compute its AABB
-// and ascend.  At each internal node the box goes into this child's slot, then
-// __threadfence + atomicAdd on the arrival counter: the first arrival stops,
-// the second (which sees the sibling's box) merges and continues.
-__global__ void __launch_bounds__(kBlock) k_refit(const float* __restrict__ V, int64_t nv,
-                                                  const int32_t* __restrict__ T, const int32_t* __restrict__ vals,
-                                                  int n_leaves, int n, float4* nodes, float4* __restrict__ tris,
-                                                  const int32_t* __restrict__ parent, uint32_t* arrivals,
-                                                  uint32_t* scratch) {
-    int k = blockIdx.x * blockDim.x + threadIdx.x;
-    if (k >= n_leaves) return;
+// and ascend.  A CTA owns the leaf window [c0, c0 + kRefitLeaves): an
+// internal node whose leaf range (stored by k_karras) lies inside the window
+// has all its descendants in this CTA, so its two arrivals meet in SHARED
+// memory -- the child box goes into a shared slot, a block-scope atomic on a
+// shared counter decides first / second arrival, and the second reads its
+// sibling's box from the shared slot (tens of cycles per level instead of a
+// global atomic round trip).  Nodes whose range crosses the window use the
+// global protocol: box into the node slot, acq_rel atomicAdd on the arrival
+// counter, sibling box by L2-coherent loads.  Every arrival also counts in
+// arrivals[] (a fire-and-forget reduction on the in-window path) for the
+// validator's "atomic: 2" check.  Every level writes the child's
+// box into the global node slot the traversal reads.
+constexpr int kRefitLeaves = 512;
+
+__global__ void __launch_bounds__(kRefitLeaves) k_refit(const float* __restrict__ V, int64_t nv,
+                                                        const int32_t* __restrict__ T,
+                                                        const int32_t* __restrict__ vals, int n_leaves, int n,
+                                                        float4* nodes, float4* __restrict__ tris,
+                                                        const int32_t* __restrict__ parent, uint32_t* arrivals,
+                                                        uint32_t* scratch) {
+    __shared__ uint32_t s_arr[kRefitLeaves];
+    __shared__ float s_box[kRefitLeaves][2][6];
+    __shared__ int32_t s_par[kRefitLeaves];  // parent links of the window's internal nodes
+    __shared__ int2 s_rng[kRefitLeaves];     // their leaf ranges
+    const int c0 = blockIdx.x * kRefitLeaves;
     const int n_nodes = n > 1 ? n - 1 : 1;
+    {
+        // the window's slice of the tree, in bulk: one coalesced round trip
+        // instead of a dependent L2 load per level of every ascent
+        const int i = c0 + threadIdx.x;
+        s_arr[threadIdx.x] = 0u;
+        const bool own = n > 1 && i < n_nodes;
+        const int4 r3 = own ? __ldg(reinterpret_cast<const int4*>(nodes + 4 * i + 3)) : make_int4(0, 0, -1, -1);
+        s_rng[threadIdx.x] = make_int2(r3.z, r3.w);
+        s_par[threadIdx.x] = own ? __ldg(parent + i) : -1;
+    }
+    __syncthreads();
+    const int k = c0 + threadIdx.x;
+    if (k >= n_leaves) return;
     const int32_t id = vals[k];
     const int32_t ia = safe_index(T[3 * id], nv), ib = safe_index(T[3 * id + 1], nv),
                   ic = safe_index(T[3 * id + 2], nv);
@@ -433,21 +463,45 @@ __global__ void __launch_bounds__(kBlock) k_refit(const float* __restrict__ V, i
         const int node = p >> 1, side = p & 1;
         write_slot(nodes, node, side, lo, hi);
         if (n == 1) break;
-        // the next parent link is read-only: fetch it before the arrival
-        const int32_t p_next = node > 0 ? __ldg(parent + node) : -1;
-        // acq_rel arrival: releases this child's box, acquires the sibling's
-        uint32_t old;
-        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(arrivals + node) : "memory");
-        if (old == 0u) return;
-        // sibling box: L2-coherent loads (ld.global.cg), ordered after the atomic
-        const float* f = reinterpret_cast<const float*>(nodes + 4 * node);
-        const int o = side ? 0 : 4;  // sibling slot
-        lo[0] = fminf(lo[0], __ldcg(f + o + 0));
-        hi[0] = fmaxf(hi[0], __ldcg(f + o + 1));
-        lo[1] = fminf(lo[1], __ldcg(f + o + 2));
-        hi[1] = fmaxf(hi[1], __ldcg(f + o + 3));
-        lo[2] = fminf(lo[2], __ldcg(f + 8 + 2 * (1 - side)));
-        hi[2] = fmaxf(hi[2], __ldcg(f + 9 + 2 * (1 - side)));
+        const int wi = node - c0;
+        const bool inwin = wi >= 0 && wi < kRefitLeaves && s_rng[wi].x >= c0 && s_rng[wi].y < c0 + kRefitLeaves;
+        int32_t p_next;
+        if (inwin) {  // both subtrees inside this CTA's window
+            p_next = node > 0 ? s_par[wi] : -1;
+            float* sb = s_box[wi][side];
+#pragma unroll
+            for (int x = 0; x < 3; ++x) {
+                sb[x] = lo[x];
+                sb[3 + x] = hi[x];
+            }
+            __threadfence_block();
+            const uint32_t old = atomicAdd(&s_arr[wi], 1u);
+            atomicAdd(arrivals + node, 1u);  // count only (result unused: a reduction)
+            if (old == 0u) return;
+            __threadfence_block();
+            const float* ob = s_box[wi][1 - side];
+#pragma unroll
+            for (int x = 0; x < 3; ++x) {
+                lo[x] = fminf(lo[x], ob[x]);
+                hi[x] = fmaxf(hi[x], ob[3 + x]);
+            }
+        } else {
+            // the next parent link is read-only: fetch it before the arrival
+            p_next = node > 0 ? __ldg(parent + node) : -1;
+            // acq_rel arrival: releases this child's box, acquires the sibling's
+            uint32_t old;
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(arrivals + node) : "memory");
+            if (old == 0u) return;
+            // sibling box: L2-coherent loads (ld.global.cg), ordered after the atomic
+            const float* f = reinterpret_cast<const float*>(nodes + 4 * node);
+            const int o = side ? 0 : 4;  // sibling slot
+            lo[0] = fminf(lo[0], __ldcg(f + o + 0));
+            hi[0] = fmaxf(hi[0], __ldcg(f + o + 1));
+            lo[1] = fminf(lo[1], __ldcg(f + o + 2));
+            hi[1] = fmaxf(hi[1], __ldcg(f + o + 3));
+            lo[2] = fminf(lo[2], __ldcg(f + 8 + 2 * (1 - side)));
+            hi[2] = fmaxf(hi[2], __ldcg(f + 9 + 2 * (1 - side)));
+        }
         if (node == 0) break;
         p = p_next;
     }
@@ -1137,7 +1191,7 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
                                                                               h->arrivals, n_nodes, rank);
         launch_sort(h, n, s);
         rsi_note_launch(), k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent, h->arrivals);
-        rsi_note_launch(), k_refit<<<rsi_ceil_div(refit_leaves, kBlock), kBlock, 0, s>>>(V, nv, T, h->vals, refit_leaves, n, h->nodes,
+        rsi_note_launch(), k_refit<<<rsi_ceil_div(refit_leaves, kRefitLeaves), kRefitLeaves, 0, s>>>(V, nv, T, h->vals, refit_leaves, n, h->nodes,
                                                                        h->tris, h->parent, h->arrivals, h->scratch);
     }
     if (kTopNodes > 0) rsi_note_launch(), k_topk<<<1, 1024, 0, s>>>(h->nodes, n_nodes, h->top, h->scratch);

@@ -1,7 +1,7 @@
 """GPU-box diagnostic (run under ncu --metrics dram__bytes_*): barycentric
 launches with different output subsets, to attribute DRAM write traffic."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import synth
 from paper_2305_01867_b200 import rsi

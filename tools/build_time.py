@@ -1,7 +1,7 @@
 """GPU-box helper: device time of rsi_rebuild (deferred status, CUDA events,
 20 iterations) for named workloads and random meshes, default vs Apetrei build."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, synth
 from paper_2305_01867_b200 import rsi
 

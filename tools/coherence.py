@@ -1,7 +1,7 @@
 """GPU-box experiment: traversal time on randomly ordered vs spatially sorted
 segments (6-D Morton order of (start, end)), to bound what ray reordering buys."""
 import os, sys, json
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import synth
 from paper_2305_01867_b200 import rsi

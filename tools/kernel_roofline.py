@@ -2,7 +2,7 @@
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,
       smsp__sass_thread_inst_executed_op_fp32_pred_on.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,
       lts__t_bytes.sum --clock-control none --csv python bench.py ...
-  python tools_kernel_roofline.py <csv> [hbm_GBps] [sm_mhz]
+  python tools/kernel_roofline.py <csv> [hbm_GBps] [sm_mhz]
 For every kernel: mean duration, DRAM bytes/launch and GB/s (fraction of the HBM
 peak: MEASURED_PEAKS.json hbm_gbs, else the B200_PROFILING.md fallback 6650 GB/s),
 FP32 thread-ops/s (fraction of 148 SM x 128 lanes x clock), issue-slot use."""
@@ -23,7 +23,7 @@ for r in rows[hi + 1:]:
     scale = {"nsecond": 1e-9, "ns": 1e-9, "usecond": 1e-6, "us": 1e-6, "msecond": 1e-3, "ms": 1e-3, "second": 1.0,
              "s": 1.0, "byte": 1, "Kbyte": 1e3, "KB": 1e3, "Mbyte": 1e6, "MB": 1e6, "Gbyte": 1e9, "GB": 1e9}.get(u, 1.0)
     per.setdefault(name, {}).setdefault(r[iid], {})[r[im]] = v * scale
-peaks = os.path.join(os.path.dirname(os.path.abspath(__file__)), "MEASURED_PEAKS.json")
+peaks = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")
 hbm = float(sys.argv[2]) if len(sys.argv) > 2 else None
 src = "argument"
 if hbm is None and os.path.exists(peaks):

@@ -1,6 +1,6 @@
 #!/bin/bash
 # GPU-box helper: per-kernel roofline CSVs for the bench step (N_t = 1e4) and
-# the N_t = 1e6 per-GPU share of configs[4].  Usage: bash tools_kernel_roofline.sh <tag>
+# the N_t = 1e6 per-GPU share of configs[4].  Usage: bash tools/kernel_roofline.sh <tag>
 tag=${1:-r1}
 mkdir -p gpurun_out
 M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,smsp__sass_thread_inst_executed_op_fp32_pred_on.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,lts__t_bytes.sum

@@ -1,4 +1,4 @@
-"""Summarise ncu reports: python tools_ncu_summary.py rep1.ncu-rep [...]"""
+"""Summarise ncu reports: python tools/ncu_summary.py rep1.ncu-rep [...]"""
 import csv, subprocess, sys, io
 KEYS = [
  ("gpu__time_duration.sum", "duration"),

@@ -1,6 +1,6 @@
 #!/bin/bash
 # GPU-box helper: launch list + full ncu captures of the traversal kernels.
-# Usage (under gpurun): bash tools_profile.sh <tag>
+# Usage (under gpurun): bash tools/profile.sh <tag>
 tag=${1:-r1}
 mkdir -p gpurun_out
 B="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline --no-extra-modes --no-configs"

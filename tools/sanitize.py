@@ -1,6 +1,6 @@
 """Small end-to-end run of every kernel for compute-sanitizer (memcheck / racecheck / synccheck)."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch, synth
 from paper_2305_01867_b200 import rsi
 dev = "cuda:0"

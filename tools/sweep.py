@@ -1,6 +1,6 @@
 """GPU-box helper: time the traversal per mode for several knob settings."""
 import os, sys, time, json
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import synth
 from paper_2305_01867_b200 import rsi

@@ -1,7 +1,7 @@
 """GPU-box helper: kernel timeline of bench steps (rsi_rebuild + rsi_intersect)
 via torch.profiler (CUPTI): start offsets, durations and the gaps between."""
 import os, sys, json
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from torch.profiler import profile, ProfilerActivity
 import synth

@@ -227,7 +227,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2305_01867_b200 import rsi
-    from paper_2305_01867_b200.sharded import gather_outputs
+    from paper_2305_01867_b200.sharded import FIELDS, GatherPipeline
 
     # one process per GPU; RSI_BENCH_BACKEND=gloo + more ranks than GPUs is a
     # launch/gather dry run on a single device (testing only, never a number)
@@ -252,9 +252,17 @@ def main():
     h = rsi.rsi_build(Vd, Td, rsi.Options(deferred_status=True))
 
     def timed(mode: str, steps: int, warmup: int, clocks: bool):
-        out = rsi.alloc_outputs(n, mode, dev)
+        # N > 1: the gather of step k (NCCL, its own stream) overlaps the build +
+        # traversal of step k+1; two output slots, each reused only after its
+        # previous gather completed (a device-side wait); all gathers finish
+        # inside the timed region (drain before the end event)
+        outs = [rsi.alloc_outputs(n, mode, dev) for _ in range(2 if world > 1 else 1)]
+        pipe = GatherPipeline(slots=2) if world > 1 else None
 
-        def step(ev=None):
+        def step(k, ev=None):
+            out = outs[k % len(outs)]
+            if pipe is not None and pipe.slots[k % 2] is not None:
+                pipe.slots[k % 2].wait()  # this slot's send buffer is free again
             if ev is not None:
                 ev[0].record(stream)
             rsi.rsi_rebuild(h, Vd, Td)
@@ -263,11 +271,13 @@ def main():
             rsi.rsi_intersect(h, Sd, Ed, mode, out=out)
             if ev is not None:
                 ev[2].record(stream)
-            if world > 1:
-                gather_outputs(out, n * world)
+            if pipe is not None:
+                pipe.start(k % 2, {f: out[f] for f in FIELDS[mode]}, n * world)
 
-        for _ in range(warmup):
-            step()
+        for k in range(warmup):
+            step(k)
+        if pipe is not None:
+            pipe.drain()
         torch.cuda.synchronize(dev)
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(steps)]
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -280,7 +290,9 @@ def main():
         launches0 = rsi.rsi_launch_count()
         t0.record(stream)
         for k in range(steps):
-            step(evs[k])
+            step(k, evs[k])
+        if pipe is not None:
+            pipe.drain()  # every step's outputs are on rank 0 before the end event
         t1.record(stream)
         launches = rsi.rsi_launch_count() - launches0
         torch.cuda.synchronize(dev)

@@ -50,6 +50,82 @@ def gather_outputs(local: dict, n_total: int, group=None, dst: int = 0) -> dict 
     return out if rank == dst else None
 
 
+class PendingGather:
+    """An in-flight gather (GatherPipeline.start): `wait()` makes the caller's
+    stream wait for it (NCCL: a device-side wait, the host does not block) and
+    returns the full outputs on the destination rank, None elsewhere."""
+
+    def __init__(self, works, recv, n_total, world, rank, dst):
+        self.works, self.recv, self.n_total, self.world, self.rank, self.dst = works, recv, n_total, world, rank, dst
+
+    def wait(self):
+        for w in self.works:
+            w.wait()
+        self.works = []
+        if self.rank != self.dst:
+            return None
+        # slices are padded to ceil(N / W) rows: drop the padding (a view when none)
+        per = -(-self.n_total // self.world)
+        out = {}
+        for k, buf in self.recv.items():
+            if per * self.world == self.n_total:
+                out[k] = buf[: self.n_total]
+            else:
+                out[k] = torch.cat([buf[r * per: r * per + (shard_range(self.n_total, r, self.world)[1]
+                                                          - shard_range(self.n_total, r, self.world)[0])]
+                                    for r in range(self.world)], 0)
+        return out
+
+
+class GatherPipeline:
+    """Asynchronous ordered gather of per-ray outputs into receive buffers
+    allocated once (weak-scaling steps: the gather of step k overlaps the
+    build + traversal of step k+1, as the NCCL work runs on its own stream).
+    Each slot owns its receive buffers; `start` waits for the slot's previous
+    gather before reusing them.  Slices of ceil(N / W) rows are sent in place
+    when no padding is needed (the equal-slice case), else through a padded copy."""
+
+    def __init__(self, slots: int = 2, group=None, dst: int = 0):
+        self.group, self.dst = group, dst
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.slots = [None] * slots
+        self.recv = [None] * slots
+
+    def start(self, slot: int, local: dict, n_total: int) -> PendingGather:
+        if self.slots[slot] is not None:
+            self.slots[slot].wait()
+        per = -(-n_total // self.world)
+        lo, hi = shard_range(n_total, self.rank, self.world)
+        nccl = dist.get_backend(self.group) == "nccl"
+        if self.rank == self.dst and (self.recv[slot] is None or
+                                      any(self.recv[slot][k].shape[0] != per * self.world for k in local)):
+            self.recv[slot] = {k: torch.empty((per * self.world,) + tuple(t.shape[1:]), dtype=t.dtype,
+                                              device=t.device if nccl else torch.device("cpu"))
+                               for k, t in local.items()}
+        works = []
+        for k in sorted(local):
+            t = local[k]
+            if t.shape[0] != hi - lo:
+                raise ValueError(f"{k}: slice has {t.shape[0]} rows, expected {hi - lo}")
+            if not nccl:
+                t = t.cpu()
+            if hi - lo != per:
+                pad = torch.zeros((per,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+                pad[: hi - lo] = t
+                t = pad
+            bufs = list(self.recv[slot][k].split(per)) if self.rank == self.dst else None
+            works.append(dist.gather(t.contiguous(), bufs, dst=self.dst, group=self.group, async_op=True))
+        self.slots[slot] = PendingGather(works, self.recv[slot], n_total, self.world, self.rank, self.dst)
+        return self.slots[slot]
+
+    def drain(self):
+        for i, pg in enumerate(self.slots):
+            if pg is not None:
+                pg.wait()
+                self.slots[i] = None
+
+
 def intersect_sharded(vertices: torch.Tensor, triangles: torch.Tensor, start: torch.Tensor, end: torch.Tensor,
                       mode: str = "boolean", options=None, group=None, intersect_fn=None) -> dict:
     """Replicated build + sharded intersect + gather.  `start`/`end` are the

@@ -82,3 +82,55 @@ def test_gloo_world2_gather_matches_single_process(n_rays):
     assert (res["barycentric"]["tri"] == ref["tri"]).all()
     m = ref["tri"] >= 0
     np.testing.assert_allclose(res["barycentric"]["point"][m], ref["point"][m], atol=1e-6)
+
+
+def _pipe_worker(rank, world, port, n_rays, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2305_01867_b200.sharded import GatherPipeline
+        pipe = GatherPipeline(slots=2)
+        got = []
+        for step in range(4):  # 4 steps over 2 slots: every slot is reused once
+            V, T, S, E, _ = synth.workload("cube", n_rays, seed=10 + step)
+            lo, hi = shard_range(n_rays, rank, world)
+            loc = _oracle_fn(*(torch.from_numpy(a) for a in (V, T, S[lo:hi], E[lo:hi])), "barycentric")
+            pending = pipe.start(step % 2, loc, n_rays)
+            if step % 2 == 1:  # collect the two steps in flight
+                for pg in prev, pending:
+                    r = pg.wait()
+                    if rank == 0:
+                        got.append({k: v.clone().numpy() for k, v in r.items()})
+                    else:
+                        assert r is None
+            prev = pending
+        pipe.drain()
+        if rank == 0:
+            q.put(got)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_rays", [1000, 1001])
+def test_gloo_world2_pipelined_gather(n_rays):
+    """GatherPipeline (the bench's overlapped gather): asynchronous gathers into
+    reused receive buffers give each step's outputs in ray order (equal and
+    padded slices)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pipe_worker, args=(r, 2, port, n_rays, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert len(got) == 4
+    for step in range(4):
+        V, T, S, E, _ = synth.workload("cube", n_rays, seed=10 + step)
+        ref = oracle.run(V, T, S, E, flags=False)
+        assert (got[step]["tri"] == ref["tri"]).all()
+        m = ref["tri"] >= 0
+        np.testing.assert_allclose(got[step]["point"][m], ref["point"][m], atol=1e-6)

@@ -406,15 +406,18 @@ __device__ __forceinline__ void write_slot(float4* nodes, int node, int side, co
 // and ascend.  A CTA owns the leaf window [c0, c0 + kRefitLeaves): an
 // internal node whose leaf range (stored by k_karras) lies inside the window
 // has all its descendants in this CTA, so its two arrivals meet in SHARED
-// memory -- the child box goes into a shared slot, a block-scope atomic on a
-// shared counter decides first / second arrival, and the second reads its
-// sibling's box from the shared slot (tens of cycles per level instead of a
-// global atomic round trip).  Nodes whose range crosses the window use the
-// global protocol: box into the node slot, acq_rel atomicAdd on the arrival
-// counter, sibling box by L2-coherent loads.  Every arrival also counts in
-// arrivals[] (a fire-and-forget reduction on the in-window path) for the
-// validator's "atomic: 2" check.  Every level writes the child's
-// box into the global node slot the traversal reads.
+// memory, in barrier-separated rounds: in a round every climbing thread puts
+// its box into its slot of the parent and counts its arrival with a
+// shared-memory atomic; after the barrier the second arrival reads the
+// sibling's slot, merges and climbs on (tens of cycles per level instead of a
+// global atomic round trip; the window's parent links and node ranges are
+// bulk-loaded first).  A climb that reaches a node crossing the window leaves
+// the rounds and continues with the global protocol: box into the node slot,
+// acq_rel atomicAdd on the arrival counter (first arrival stops),
+// sibling box by L2-coherent loads.  Every arrival also counts in arrivals[]
+// (a fire-and-forget reduction in the rounds) for the validator's "atomic: 2"
+// check, and every level writes the child's box into the global
+// node slot the traversal reads.
 constexpr int kRefitLeaves = 512;
 
 __global__ void __launch_bounds__(kRefitLeaves) k_refit(const float* __restrict__ V, int64_t nv,
@@ -439,55 +442,81 @@ __global__ void __launch_bounds__(kRefitLeaves) k_refit(const float* __restrict_
         s_rng[threadIdx.x] = make_int2(r3.z, r3.w);
         s_par[threadIdx.x] = own ? __ldg(parent + i) : -1;
     }
-    __syncthreads();
     const int k = c0 + threadIdx.x;
-    if (k >= n_leaves) return;
-    const int32_t id = vals[k];
-    const int32_t ia = safe_index(T[3 * id], nv), ib = safe_index(T[3 * id + 1], nv),
-                  ic = safe_index(T[3 * id + 2], nv);
-    float a[3], b[3], c[3], lo[3], hi[3];
+    const bool leaf = k < n_leaves;
+    float lo[3], hi[3];
+    int32_t p = -1;
+    if (leaf) {
+        const int32_t id = vals[k];
+        const int32_t ia = safe_index(T[3 * id], nv), ib = safe_index(T[3 * id + 1], nv),
+                      ic = safe_index(T[3 * id + 2], nv);
+        float a[3], b[3], c[3];
 #pragma unroll
-    for (int x = 0; x < 3; ++x) {
-        a[x] = V[3 * ia + x];
-        b[x] = V[3 * ib + x];
-        c[x] = V[3 * ic + x];
-        lo[x] = fminf(a[x], fminf(b[x], c[x]));
-        hi[x] = fmaxf(a[x], fmaxf(b[x], c[x]));
+        for (int x = 0; x < 3; ++x) {
+            a[x] = V[3 * ia + x];
+            b[x] = V[3 * ib + x];
+            c[x] = V[3 * ic + x];
+            lo[x] = fminf(a[x], fminf(b[x], c[x]));
+            hi[x] = fmaxf(a[x], fmaxf(b[x], c[x]));
+        }
+        tris[4 * k + 0] = make_float4(a[0], a[1], a[2], __int_as_float(id));
+        tris[4 * k + 1] = make_float4(b[0], b[1], b[2], 0.f);
+        tris[4 * k + 2] = make_float4(c[0], c[1], c[2], 0.f);
+        tris[4 * k + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
+        p = parent[n_nodes + k];
     }
-    tris[4 * k + 0] = make_float4(a[0], a[1], a[2], __int_as_float(id));
-    tris[4 * k + 1] = make_float4(b[0], b[1], b[2], 0.f);
-    tris[4 * k + 2] = make_float4(c[0], c[1], c[2], 0.f);
-    tris[4 * k + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
-    int32_t p = parent[n_nodes + k];
-    while (true) {
-        const int node = p >> 1, side = p & 1;
-        write_slot(nodes, node, side, lo, hi);
-        if (n == 1) break;
-        const int wi = node - c0;
-        const bool inwin = wi >= 0 && wi < kRefitLeaves && s_rng[wi].x >= c0 && s_rng[wi].y < c0 + kRefitLeaves;
-        int32_t p_next;
-        if (inwin) {  // both subtrees inside this CTA's window
-            p_next = node > 0 ? s_par[wi] : -1;
-            float* sb = s_box[wi][side];
+    __syncthreads();
+    // ---- rounds inside the window (state: 0 done, 1 climbing in the window,
+    // 2 waiting to merge after the barrier, 3 continue with the global protocol)
+    int state = leaf ? 1 : 0;
+    int wi = -1, side = 0;
+    if (n == 1 && leaf) {  // single triangle: the root's left slot, no arrivals
+        write_slot(nodes, 0, 0, lo, hi);
+        state = 0;
+    }
+    while (__syncthreads_or(state == 1)) {
+        if (state == 1) {
+            const int node = p >> 1;
+            side = p & 1;
+            wi = node - c0;
+            write_slot(nodes, node, side, lo, hi);
+            if (wi >= 0 && wi < kRefitLeaves && s_rng[wi].x >= c0 && s_rng[wi].y < c0 + kRefitLeaves) {
+                float* sb = s_box[wi][side];
 #pragma unroll
-            for (int x = 0; x < 3; ++x) {
-                sb[x] = lo[x];
-                sb[3 + x] = hi[x];
+                for (int x = 0; x < 3; ++x) {
+                    sb[x] = lo[x];
+                    sb[3 + x] = hi[x];
+                }
+                atomicAdd(arrivals + node, 1u);  // count only (result unused: a reduction)
+                state = atomicAdd(&s_arr[wi], 1u) == 0u ? 0 : 2;
+            } else {
+                state = 3;  // the node crosses the window (its box slot is already written)
             }
-            __threadfence_block();
-            const uint32_t old = atomicAdd(&s_arr[wi], 1u);
-            atomicAdd(arrivals + node, 1u);  // count only (result unused: a reduction)
-            if (old == 0u) return;
-            __threadfence_block();
+        }
+        __syncthreads();
+        if (state == 2) {  // the sibling's slot was written before the barrier
             const float* ob = s_box[wi][1 - side];
 #pragma unroll
             for (int x = 0; x < 3; ++x) {
                 lo[x] = fminf(lo[x], ob[x]);
                 hi[x] = fmaxf(hi[x], ob[3 + x]);
             }
-        } else {
+            const int node = wi + c0;
+            if (node == 0) {
+                state = 4;  // merged at the root inside the window
+            } else {
+                p = s_par[wi];
+                state = 1;
+            }
+        }
+    }
+    if (state == 3) {
+        // global protocol from node p >> 1 (whose slot this thread already wrote)
+        while (true) {
+            const int node = p >> 1;
+            side = p & 1;
             // the next parent link is read-only: fetch it before the arrival
-            p_next = node > 0 ? __ldg(parent + node) : -1;
+            const int32_t p_next = node > 0 ? __ldg(parent + node) : -1;
             // acq_rel arrival: releases this child's box, acquires the sibling's
             uint32_t old;
             asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(arrivals + node) : "memory");
@@ -501,9 +530,12 @@ __global__ void __launch_bounds__(kRefitLeaves) k_refit(const float* __restrict_
             hi[1] = fmaxf(hi[1], __ldcg(f + o + 3));
             lo[2] = fminf(lo[2], __ldcg(f + 8 + 2 * (1 - side)));
             hi[2] = fmaxf(hi[2], __ldcg(f + 9 + 2 * (1 - side)));
+            if (node == 0) break;
+            p = p_next;
+            write_slot(nodes, p >> 1, p & 1, lo, hi);
         }
-        if (node == 0) break;
-        p = p_next;
+    } else if (state != 4 && !(n == 1 && leaf)) {
+        return;
     }
     // root box (scene AABB) for rsi_bvh_info
     float* root = reinterpret_cast<float*>(scratch + SCR_ROOT);

@@ -27,6 +27,21 @@ h.free()
 rng = np.random.default_rng(1)
 V = rng.uniform(0, 1, (3 * 70001, 3)).astype(np.float32); T = np.arange(3 * 70001, dtype=np.int32).reshape(-1, 3)
 h = rsi.rsi_build(torch.from_numpy(V).to(dev), torch.from_numpy(T).to(dev)); h.free()
+# RSI_OPT_APETREI (63-bit codes, two sorts, agglomerative build) on the rank-sort
+# and multi-block sizes, queried in every mode; validator; fault injection
+for nt in (5000, 70001):
+    Vd = torch.from_numpy(V[:3 * nt]).to(dev); Td = torch.from_numpy(T[:nt]).to(dev)
+    h = rsi.rsi_build(Vd, Td, rsi.Options(apetrei=True))
+    Sd, Ed = (torch.from_numpy(a).to(dev) for a in synth.box_rays(3000, -0.2, 1.2, seed=3))
+    for m in ("boolean", "barycentric", "intercept_count"):
+        rsi.rsi_intersect(h, Sd, Ed, m)
+    assert rsi.rsi_validate(h)["ok"]
+    rsi.rsi_bvh_download(h)
+    h.free()
+h = rsi.rsi_build(Vd, Td, rsi.Options(apetrei=True, debug_refit_leaves=20000))
+assert not rsi.rsi_validate(h)["ok"]
+rsi.rsi_intersect(h, Sd, Ed, "boolean")
+h.free()
 hv = rsi.rsi_test(*synth.workload("sphere", 3000, seed=2)[:4], {"mode": "boolean"})
 rsi.rsi_release_cache()
 torch.cuda.synchronize()

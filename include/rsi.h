@@ -276,7 +276,9 @@ rsi_status_t rsi_reset_stats(rsi_handle_t h, void* stream);
  *     h_morton  [N_t] uint32 sorted 30-bit Morton codes (z-major interleave)
  *     h_parent  [n_nodes + N_t] int32 parent of internal nodes then of leaves,
  *               encoded (parent << 1) | side (side 0 = left); -1 for the root
- *     h_arrivals[n_nodes] uint32 refit arrival counters ("atomic")
+ *               (node 0, or rsi_bvh_root's node under RSI_OPT_APETREI)
+ *     h_arrivals[n_nodes] uint32 refit arrival counters ("atomic"); under
+ *               RSI_OPT_APETREI the arrival counts of the agglomerative build
  */
 rsi_status_t rsi_bvh_info(rsi_handle_t h, int64_t* n_triangles, int64_t* n_nodes,
                           float* scene_lo3, float* scene_hi3);

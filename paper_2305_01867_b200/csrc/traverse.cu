@@ -1195,19 +1195,17 @@ __global__ void __launch_bounds__(kThreads) k_ovf_size(const float4* __restrict_
     seg[2 * j + 1] = nh;
 }
 
-// Pass B: exact fp64 t of every hit, then sort the segment and count.
-__global__ void __launch_bounds__(kThreads) k_ovf_count(const float4* __restrict__ nodes,
-                                                        const float4* __restrict__ tris, const float* __restrict__ S,
-                                                        const float* __restrict__ E, const int32_t* __restrict__ list,
-                                                        int n_ovf, const int32_t* __restrict__ seg, double* pool,
-                                                        double tau, int32_t* __restrict__ count_out,
-                                                        const uint32_t* __restrict__ scratch) {
+// Pass B: exact fp64 t of every hit of each overflowed ray into its segment.
+__global__ void __launch_bounds__(kThreads) k_ovf_collect(const float4* __restrict__ nodes,
+                                                          const float4* __restrict__ tris, const float* __restrict__ S,
+                                                          const float* __restrict__ E, const int32_t* __restrict__ list,
+                                                          int n_ovf, const int32_t* __restrict__ seg, double* pool,
+                                                          const uint32_t* __restrict__ scratch) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n_ovf) return;
     Ray r;
     bool nonfinite;
-    const int64_t i = list[j];
-    load_ray(r, S, E, i, nonfinite);
+    load_ray(r, S, E, list[j], nonfinite);
     double* v = pool + seg[2 * j];
     const int cap = seg[2 * j + 1];
     int nh = 0;
@@ -1219,14 +1217,27 @@ __global__ void __launch_bounds__(kThreads) k_ovf_count(const float4* __restrict
         if (mt64(r, A, B, C, &t64) && nh < cap) v[nh++] = t64;
         return false;
     });
-    // heap sort v[0..nh)
+}
+
+// Pass C: one WARP per overflowed ray (north_star: warp-level ballot/shuffle
+// for the intercept_count dedup).  The segment's fp64 hit t values (<= 32 x
+// kOvfRegs) sit across the lanes' registers, element i = r * 32 + lane; a
+// bitonic network sorts them (partners within a register by shuffle-xor,
+// across registers in-lane), then count = [nh > 0] + popc of the ballots of
+// "gap to the previous element > tau" -- the oracle's single-linkage count
+// (reading R4) with the same correctly rounded gap __dadd_rn(t_i, -t_(i-1)).
+// Longer segments (never seen outside adversarial stacks) use a serial heap
+// sort in lane 0.
+constexpr int kOvfRegs = 8;  // up to 256 hits per ray in registers
+
+__device__ void heap_sort(double* v, int nh) {
     for (int start = nh / 2 - 1; start >= 0; --start) {
         int root = start;
         while (2 * root + 1 < nh) {
             int c = 2 * root + 1;
             if (c + 1 < nh && v[c] < v[c + 1]) ++c;
             if (v[root] < v[c]) {
-                double x = v[root];
+                const double x = v[root];
                 v[root] = v[c];
                 v[c] = x;
                 root = c;
@@ -1236,7 +1247,7 @@ __global__ void __launch_bounds__(kThreads) k_ovf_count(const float4* __restrict
         }
     }
     for (int end = nh - 1; end > 0; --end) {
-        double x = v[0];
+        const double x = v[0];
         v[0] = v[end];
         v[end] = x;
         int root = 0;
@@ -1244,7 +1255,7 @@ __global__ void __launch_bounds__(kThreads) k_ovf_count(const float4* __restrict
             int c = 2 * root + 1;
             if (c + 1 < end && v[c] < v[c + 1]) ++c;
             if (v[root] < v[c]) {
-                double y = v[root];
+                const double y = v[root];
                 v[root] = v[c];
                 v[c] = y;
                 root = c;
@@ -1253,10 +1264,72 @@ __global__ void __launch_bounds__(kThreads) k_ovf_count(const float4* __restrict
             }
         }
     }
+}
+
+__global__ void __launch_bounds__(kThreads) k_ovf_dedup(const int32_t* __restrict__ list, int n_ovf,
+                                                        const int32_t* __restrict__ seg, double* pool, double tau,
+                                                        int32_t* __restrict__ count_out) {
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // warp-uniform
+    if (j >= n_ovf) return;
+    double* v = pool + seg[2 * j];
+    const int nh = seg[2 * j + 1];
     int cnt = nh > 0 ? 1 : 0;
-    for (int a = 0; a + 1 < nh; ++a)
-        if (da(v[a + 1], -v[a]) > tau) ++cnt;
-    count_out[i] = cnt;
+    if (nh > 32 * kOvfRegs) {  // rare: serial sort in lane 0
+        if (lane == 0) {
+            heap_sort(v, nh);
+            for (int a = 0; a + 1 < nh; ++a)
+                if (da(v[a + 1], -v[a]) > tau) ++cnt;
+            count_out[list[j]] = cnt;
+        }
+        return;
+    }
+    int R = 1;  // registers in use: the power of two >= ceil(nh / 32)
+    while (32 * R < nh) R <<= 1;
+    double x[kOvfRegs];
+#pragma unroll
+    for (int q = 0; q < kOvfRegs; ++q) {
+        const int i = q * 32 + lane;
+        x[q] = (q < R && i < nh) ? v[i] : INFINITY;  // pad: sorts last, never counted
+    }
+    const int n = 32 * R;
+    for (int k = 2; k <= n; k <<= 1) {
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+#pragma unroll
+            for (int q = 0; q < kOvfRegs; ++q) {
+                if (q >= R) break;
+                const int i = q * 32 + lane;
+                const bool up = (i & k) == 0;  // ascending block
+                if (jj < 32) {
+                    const double o = __shfl_xor_sync(FULL, x[q], jj);
+                    const bool lower = (lane & jj) == 0;
+                    // keep the min on the lower index of an ascending block
+                    x[q] = (lower == up) ? fmin(x[q], o) : fmax(x[q], o);
+                } else {
+                    const int qp = q ^ (jj >> 5);
+                    if (qp > q) {
+                        const double a0 = x[q], a1 = x[qp];
+                        const double lo = fmin(a0, a1), hi = fmax(a0, a1);
+                        x[q] = up ? lo : hi;
+                        x[qp] = up ? hi : lo;
+                    }
+                }
+            }
+        }
+    }
+    // count the gaps: element i > 0 against element i - 1
+#pragma unroll
+    for (int q = 0; q < kOvfRegs; ++q) {
+        if (q >= R) break;
+        const double up1 = __shfl_up_sync(FULL, x[q], 1);
+        const double last = q > 0 ? __shfl_sync(FULL, x[q > 0 ? q - 1 : 0], 31) : 0.0;
+        const double prev = lane > 0 ? up1 : last;
+        const int i = q * 32 + lane;
+        const bool gap = i > 0 && i < nh && da(x[q], -prev) > tau;
+        cnt += __popc(__ballot_sync(FULL, gap));
+    }
+    if (lane == 0) count_out[list[j]] = cnt;
 }
 
 // ---------------------------------------------------------------- ordered compaction (3a)
@@ -1446,8 +1519,10 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
         cudaFreeAsync(seg, s);
         return RSI_E_OOM;
     }
-    rsi_note_launch(), k_ovf_count<<<nb, kThreads, 0, s>>>(h->nodes, h->tris, S, E, h->ovf_list, n_ovf, seg, pool, h->opt.dedup_tau,
-                                        out->count, h->scratch);
+    rsi_note_launch(), k_ovf_collect<<<nb, kThreads, 0, s>>>(h->nodes, h->tris, S, E, h->ovf_list, n_ovf, seg, pool,
+                                                             h->scratch);
+    rsi_note_launch(), k_ovf_dedup<<<rsi_ceil_div((int64_t)n_ovf * 32, kThreads), kThreads, 0, s>>>(
+        h->ovf_list, n_ovf, seg, pool, h->opt.dedup_tau, out->count);
     st = rsi_cuda_check(cudaGetLastError(), "overflow pass");
     cudaFreeAsync(pool, s);
     cudaFreeAsync(seg, s);

@@ -676,3 +676,28 @@ def test_apetrei_sort_full_low_words(rsi):
     order = np.argsort(code, kind="stable")
     assert (d["morton63"] == code[order]).all()
     assert (d["leaf_tri"] == order).all()
+
+
+@pytest.mark.parametrize("n_sheets", [40, 100, 256, 300])
+def test_overflow_warp_dedup(rsi, n_sheets):
+    """Rays crossing up to 300 stacked sheets overflow the 8-entry register list:
+    the re-pass collects every hit's fp64 t and one warp per ray sorts them with
+    a shuffle bitonic network and counts gaps by ballot (> 256 hits: serial heap
+    sort).  Sheets come in groups whose members are 1e-7 apart in z (merged by
+    tau) and groups 0.004 apart (distinct): counts equal the oracle's exactly."""
+    base = np.float32([[-1, -1, 0], [3, -1, 0], [-1, 3, 0]])
+    Vs, z = [], 1.0
+    for k in range(n_sheets):
+        z += 1e-7 if k % 3 else 0.004
+        Vs.append(base + np.float32([0, 0, z]))
+    V = np.vstack(Vs).astype(np.float32)
+    T = np.arange(len(V), dtype=np.int32).reshape(-1, 3)
+    rng = np.random.default_rng(n_sheets)
+    S = np.column_stack([rng.uniform(0, 1, 400), rng.uniform(0, 1, 400), np.full(400, 0.5)]).astype(np.float32)
+    E = S.copy()
+    E[:, 2] = np.float32(z + 0.5)
+    E[:200, :2] += rng.uniform(-0.2, 0.2, (200, 2)).astype(np.float32)  # some oblique
+    ref = oracle.run(V, T, S, E)
+    got = run_all(rsi, V, T, S, E)
+    assert (got["count"] == ref["count"]).all(), np.nonzero(got["count"] != ref["count"])[0][:10]
+    assert got["stats"]["overflow_rays"] > 0 and ref["count"].max() > 8

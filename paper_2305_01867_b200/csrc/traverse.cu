@@ -81,6 +81,19 @@ constexpr bool kQuadCount = RSI_COUNT_QUAD;
 #ifndef RSI_PF_PUSH
 #define RSI_PF_PUSH 0
 #endif
+// quad visits per traversal-phase iteration (the warp votes on leaving the
+// phase every kVisits visits): measured per mode on the sphere and
+// paper-terrain workloads -- 3 with min_trav 16 / 12 for boolean / barycentric
+// (-1..-6 %), 1 for intercept_count (3: +9 %)
+#ifndef RSI_VISITS_BOOL
+#define RSI_VISITS_BOOL 3
+#endif
+#ifndef RSI_VISITS_BARY
+#define RSI_VISITS_BARY 3
+#endif
+#ifndef RSI_VISITS_COUNT
+#define RSI_VISITS_COUNT 1
+#endif
 #ifndef RSI_SORT_ALL
 #define RSI_SORT_ALL 1
 #endif
@@ -923,9 +936,12 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                 __ballot_sync(FULL, l0 >= 0);
             }
             if (__popc(tm) < p.min_trav && __ballot_sync(FULL, l0 >= 0)) break;
+            constexpr int kVisits = MODE == MODE_BOOL ? RSI_VISITS_BOOL : (MODE == MODE_BARY ? RSI_VISITS_BARY : RSI_VISITS_COUNT);
+#pragma unroll 1
+            for (int u = 0; u < kVisits; ++u) {
             // kQSpec: a lane holding one pending leaf keeps walking (its next
             // leaf goes to l1) in slots it would otherwise idle in
-            if (trav || (kQSpec && node >= 0 && l1 < 0)) {
+            if ((node >= 0 && l0 < 0) || (kQSpec && node >= 0 && l1 < 0)) {
                 const float4* q = p.quads + 4 * node;
                 float4 qa, qb, qc, qd;
                 ldg256(q, qa, qb);
@@ -1026,6 +1042,8 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                     }
                 }
                 node = first >= 0 ? first : -1;
+            }
+            if (kVisits > 1 && !((node >= 0 && l0 < 0) || (kQSpec && node >= 0 && l1 < 0))) break;
             }
         }
 
@@ -1483,7 +1501,7 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     // traversal-phase exit threshold, measured per mode (env RSI_MIN_TRAV overrides)
     // measured per mode on the sphere / paper-terrain workloads
     p.min_trav = h->min_trav >= 0 ? h->min_trav
-                                  : (mode == RSI_MODE_BOOLEAN ? 16 : (mode == RSI_MODE_BARYCENTRIC ? 8 : 12));
+                                  : (mode == RSI_MODE_BOOLEAN ? 16 : (mode == RSI_MODE_BARYCENTRIC ? 12 : 12));
     const bool fp64 = (h->opt.flags & RSI_OPT_FP64_MOLLER) != 0, ctr = (h->opt.flags & RSI_OPT_COUNTERS) != 0;
     if (fp64)
         ctr ? launch_mode<true, true>(mode, p, s) : launch_mode<true, false>(mode, p, s);

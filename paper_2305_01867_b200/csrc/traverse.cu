@@ -124,7 +124,10 @@ template <int MODE>
 __host__ __device__ constexpr int trace_threads() {
     return kTopNodes > 0 ? (MODE == 0 ? 1024 : 768) : 128;
 }
-constexpr int kChunk = 64;   // rays a warp takes from the global dispenser at once
+#ifndef RSI_CHUNK
+#define RSI_CHUNK 64
+#endif
+constexpr int kChunk = RSI_CHUNK;  // rays a warp takes from the global dispenser at once
 
 enum { MT_MISS = 0, MT_HIT = 1, MT_UNSURE = 2 };
 

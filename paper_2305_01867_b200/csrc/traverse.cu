@@ -470,36 +470,42 @@ struct ModeState<MODE_BOOL> {
 
 // Barycentric: lexicographic min of (t, original id) (reading R5).  A hit is
 // held as an interval [t32 - et, t32 + et] or an exact fp64 value; overlapping
-// intervals are resolved by recomputing both in the fp64 mirror.
+// intervals are resolved by recomputing both in the fp64 mirror.  Compact
+// state (register pressure): the best's leaf slot (-1: none; bit 30 set when
+// its t is exact) and ONE 64-bit word holding either the fp64 t or the fp32
+// pair (t32, et); the best's original id is re-read from its triangle record
+// only when an exact tie has to be broken.
+constexpr int kExactBit = 1 << 30;  // slots < 2^30 (N_t <= 2^30)
+
 template <>
 struct ModeState<MODE_BARY> {
-    int id, slot;
-    float t, e;
-    bool is64;
-    double t64;
+    int slot;            // -1, else leaf slot | (kExactBit if w holds an exact fp64 t)
+    unsigned long long w;  // fp64 t bits, or (t32 bits) | (et bits) << 32
     __device__ __forceinline__ void init() {
-        id = 0x7fffffff;
         slot = -1;
-        t = e = 0.f;
-        is64 = false;
-        t64 = 0.0;
+        w = 0ull;
     }
+    __device__ __forceinline__ bool exact() const { return (slot & kExactBit) != 0; }
+    __device__ __forceinline__ int leaf_slot() const { return slot & ~kExactBit; }
+    __device__ __forceinline__ double t64() const { return __longlong_as_double((long long)w); }
+    __device__ __forceinline__ float t32() const { return __uint_as_float((uint32_t)w); }
+    __device__ __forceinline__ float e32() const { return __uint_as_float((uint32_t)(w >> 32)); }
     template <bool kFP64>
     __device__ __forceinline__ bool leaf(const TraceParams& p, const Ray& r, int k, float& tclip,
                                          Stats& st) {
         float4 A, B, C;
         load_tri(p.tris, k, A, B, C);
-        float t32, et;
+        float t32c, et;
         double c64;
         bool c_is64;
-        if (decide<kFP64>(r, A, B, C, t32, et, c64, c_is64, st) != MT_HIT) return false;
-        const int cid = __float_as_int(A.w);
+        if (decide<kFP64>(r, A, B, C, t32c, et, c64, c_is64, st) != MT_HIT) return false;
         bool take;
         if (slot < 0) {
             take = true;
         } else {
-            const double clo = c_is64 ? c64 : (double)t32 - (double)et, chi = c_is64 ? c64 : (double)t32 + (double)et;
-            const double blo = is64 ? t64 : (double)t - (double)e, bhi = is64 ? t64 : (double)t + (double)e;
+            const bool bx = exact();
+            const double clo = c_is64 ? c64 : (double)t32c - (double)et, chi = c_is64 ? c64 : (double)t32c + (double)et;
+            const double blo = bx ? t64() : (double)t32() - (double)e32(), bhi = bx ? t64() : (double)t32() + (double)e32();
             if (chi < blo) {
                 take = true;
             } else if (clo > bhi) {
@@ -510,46 +516,49 @@ struct ModeState<MODE_BARY> {
                     mt64(r, A, B, C, &c64);
                     c_is64 = true;
                 }
-                if (!is64) {
-                    float4 bA, bB, bC;
-                    load_tri(p.tris, slot, bA, bB, bC);
-                    mt64(r, bA, bB, bC, &t64);
-                    is64 = true;
+                float4 bA, bB, bC;
+                load_tri(p.tris, leaf_slot(), bA, bB, bC);
+                double b64 = 0.0;
+                if (bx) {
+                    b64 = t64();
+                } else {
+                    mt64(r, bA, bB, bC, &b64);
+                    slot |= kExactBit;
+                    w = (unsigned long long)__double_as_longlong(b64);
                 }
-                take = (c64 < t64) || (c64 == t64 && cid < id);
+                take = (c64 < b64) || (c64 == b64 && __float_as_int(A.w) < __float_as_int(bA.w));
             }
         }
         if (take) {
-            id = cid;
-            slot = k;
-            is64 = c_is64;
             if (c_is64) {
-                t64 = c64;
+                slot = k | kExactBit;
+                w = (unsigned long long)__double_as_longlong(c64);
                 tclip = fminf(tclip, __double2float_ru(c64));
             } else {
-                t = t32;
-                e = et;
-                tclip = fminf(tclip, __fadd_ru(t32, et));
+                slot = k;
+                w = (unsigned long long)__float_as_uint(t32c) | ((unsigned long long)__float_as_uint(et) << 32);
+                tclip = fminf(tclip, __fadd_ru(t32c, et));
             }
         }
         return false;
     }
     __device__ __forceinline__ void finish(const TraceParams& p, const Ray& r, int64_t i, Stats& st) {
         if (slot >= 0) {
+            const int k = leaf_slot();
+            float4 bA, bB, bC;
+            load_tri(p.tris, k, bA, bB, bC);  // the original id (and, rarely, the fp64 recompute)
             float tt;
-            if (is64) {
-                tt = (float)t64;
-            } else if (e <= kOutTol) {
-                tt = t;
+            if (exact()) {
+                tt = (float)t64();
+            } else if (e32() <= kOutTol) {
+                tt = t32();
             } else {  // fp32 value not certified to the output tolerance
-                float4 bA, bB, bC;
-                load_tri(p.tris, slot, bA, bB, bC);
                 double v = 0.0;
                 mt64(r, bA, bB, bC, &v);
                 tt = (float)v;
                 st.add(ST_FP64_RAYS);
             }
-            p.tri[i] = id;
+            p.tri[i] = __float_as_int(bA.w);
             if (p.t) p.t[i] = tt;
             if (p.dist) p.dist[i] = tt * norm3df(r.dx, r.dy, r.dz);  // no overflow / underflow of |d|^2
             if (p.point) {

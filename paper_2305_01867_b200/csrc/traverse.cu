@@ -94,6 +94,9 @@ constexpr bool kQuadCount = RSI_COUNT_QUAD;
 #ifndef RSI_VISITS_COUNT
 #define RSI_VISITS_COUNT 1
 #endif
+#ifndef RSI_QC_SMEM
+#define RSI_QC_SMEM 1  // barycentric only: -1.5 % (intercept_count +2 %, boolean neutral)
+#endif
 #ifndef RSI_SORT_ALL
 #define RSI_SORT_ALL 1
 #endif
@@ -829,11 +832,13 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
     __syncthreads();
     Stats st;
 
-    int64_t cnext = 0, cend = 0;  // warp-uniform chunk [cnext, cend)
+    // 32-bit ray indices (rsi_intersect limits n_rays to 2^31 - 1): registers matter
+    const int n32 = (int)p.n;
+    int cnext = 0, cend = 0;      // warp-uniform chunk [cnext, cend)
     int64_t pbase = -1;           // warp-uniform: chunk reserved ahead (RSI_PF_RAY)
     (void)pbase;
     bool exhausted = false;       // warp-uniform
-    int64_t ray = -1;
+    int ray = -1;
     Ray r;
     int node = -1, sp = 0, l0 = -1, l1 = -1, l2 = -1;  // pending (postponed) leaf slots
     // per-lane traversal stack: the first kSmemStack entries in a shared-memory
@@ -861,6 +866,9 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
     // exact normal float and every term of the folded decode far from overflow
     // (slab_axis), from the build's scratch words -- read here on the device, so
     // rsi_intersect needs no host read-back of the build
+    // (qext, qlim_lo, qlim_hi): read at ray setup, not held in registers (barycentric)
+    constexpr bool kQcSmem = RSI_QC_SMEM && MODE == MODE_BARY;
+    __shared__ float s_qc[3];
     float qext = 0.0f, qlim_lo = 0.0f, qlim_hi = INFINITY;
     if constexpr (kQuad) {
         const float pmax = __uint_as_float(p.scratch[SCR_QPMAX]);
@@ -868,6 +876,14 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
         qext = 0.25f * pmax;
         qlim_lo = scalbnf(1.0f, -124 - emin);
         qlim_hi = scalbnf(1.0f, 100) / (pmax + scalbnf(65536.0f, emax));
+        if (kQcSmem) {
+            if (threadIdx.x == 0) {
+                s_qc[0] = qext;
+                s_qc[1] = qlim_lo;
+                s_qc[2] = qlim_hi;
+            }
+            __syncthreads();
+        }
     }
     while (true) {
         // ---- 1. refill
@@ -902,10 +918,10 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                     exhausted = true;
                     break;
                 }
-                cnext = (int64_t)base;
-                cend = min((int64_t)base + kChunk, p.n);
+                cnext = (int)base;
+                cend = min(cnext + kChunk, n32);
             }
-            const int take = (int)min((int64_t)__popc(want), cend - cnext);
+            const int take = min(__popc(want), cend - cnext);
             const bool mine = (want >> lane) & 1u;
             const int rank = __popc(want & lt);
             const bool got = mine && rank < take;
@@ -918,6 +934,11 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
         }
         if (fresh) {
             bool nonfinite;
+            if (kQuad && kQcSmem) {
+                qext = s_qc[0];
+                qlim_lo = s_qc[1];
+                qlim_hi = s_qc[2];
+            }
             const bool ok = kQuad ? load_ray<true>(r, p.S, p.E, ray, nonfinite, qext, qlim_lo, qlim_hi)
                                   : load_ray<false>(r, p.S, p.E, ray, nonfinite);
             if (nonfinite) st.add(ST_NONFINITE);

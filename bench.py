@@ -133,6 +133,7 @@ def cpu_baseline(V, T, S, E, target_s=15.0, sample=0):
     if sample <= 0:
         # calibrate with a small run, then size for ~target_s of CPU work
         n0 = 200
+        oracle.run(V, T, S[:n0], E[:n0], flags=False)  # thread pool start-up outside the calibration
         t = time.perf_counter()
         oracle.run(V, T, S[:n0], E[:n0], flags=False)
         dt = max(time.perf_counter() - t, 1e-3)

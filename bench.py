@@ -403,6 +403,33 @@ def main():
                             "h2d_GBps": h2d / copy_ms / 1e6, "frac": copy_ms / e_ms,
                             "note": "plain pinned copy of the step's input bytes / e2e step time"}}
 
+    # the paper's own headline workload, end to end like its timings (P:144,
+    # P:147-154): 1e7 rays against the 29 260-triangle terrain, host buffers in,
+    # results out, through the C-ABI rsi_test (rank 0, N = 1 only; context)
+    paper = None
+    if rank == 0 and world == 1 and not args.no_configs and not args.no_e2e:
+        Vp, Tp, Sp, Ep = workload_inputs("paper_terrain", 10_000_000, 0)
+        pin = lambda a: torch.from_numpy(a).pin_memory()  # noqa: E731
+        hVp, hTp, hSp, hEp = pin(Vp), pin(Tp), pin(Sp), pin(Ep)
+        # the paper's best end-to-end time per mode (unstated GPU)
+        paper_ms = {"boolean": (300.166, "original CUDA, P:152"),
+                    "barycentric": (456.346, "PyCUDA with GPU post-processing (points, distances), P:184"),
+                    "intercept_count": (334.192, "original CUDA, P:154")}
+        paper = {"workload": f"paper_terrain N_t={len(Tp)}, N_r=10000000, e2e via rsi_test (pinned host buffers)"}
+        for m, (pms, src) in paper_ms.items():
+            nr = len(Sp)
+            hout = rsi.alloc_outputs(nr, m, "cpu")
+            hout = {k: v.pin_memory() for k, v in hout.items()}
+            rsi.rsi_test(hVp, hTp, hSp, hEp, {"mode": m}, out=hout, sparse=False)
+            reps = 3
+            t = time.perf_counter()
+            for _ in range(reps):  # dense per-ray outputs in pinned host memory (no host post-processing)
+                rsi.rsi_test(hVp, hTp, hSp, hEp, {"mode": m}, out=hout, sparse=False)
+            ms_m = (time.perf_counter() - t) / reps * 1e3
+            paper[m] = {"e2e_ms": ms_m, "rays_per_s": nr / (ms_m * 1e-3), "paper_ms": pms, "paper_source": src,
+                        "speedup_vs_paper": pms / ms_m}
+        del hVp, hTp, hSp, hEp
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(V, T, S, E, sample=args.cpu_sample)
@@ -421,7 +448,7 @@ def main():
             "gpu_launches": launches,
             "gpu_launches_note": "rsi_launch_count() difference over the timed region (library kernels: "
                                  "BVH build chain + 1 traversal kernel per step)",
-            "clocks": clk, "modes": extra, "configs_other": other, "stats": stats,
+            "clocks": clk, "modes": extra, "configs_other": other, "paper_comparable": paper, "stats": stats,
         }
         print(json.dumps(line), flush=True)
     h.free()

@@ -273,10 +273,12 @@ def sparse_barycentric(out: dict, stream=None):
 
 
 def rsi_test(vertices, triangles, start, end, cfg: dict | None = None, options: Options | None = None,
-             stream=None, out: dict | None = None):
+             stream=None, out: dict | None = None, sparse: bool = True):
     """End-to-end on HOST arrays through the C-ABI's rsi_test:
     H2D, build, intersect, D2H, synchronize.  Returns the boolean array, the
-    counts, or (intersecting_rays, distances, hit_triangles, hit_points)."""
+    counts, or (intersecting_rays, distances, hit_triangles, hit_points) -- the
+    paper's sparse tuple, gathered on the host from the dense per-ray outputs;
+    sparse=False returns the dense output dict instead (no host post-processing)."""
     lib = load()
     mode = (cfg or {}).get("mode", "boolean")
     if mode not in MODES:
@@ -310,6 +312,8 @@ def rsi_test(vertices, triangles, start, end, cfg: dict | None = None, options: 
         return out["hit"].numpy().view(np.bool_).reshape(n, 1)  # 0/1 bytes: a view, no copy
     if mode == "intercept_count":
         return out["count"].numpy()
+    if not sparse:
+        return out
     tri = out["tri"].numpy()
     ids = np.nonzero(tri >= 0)[0].astype(np.int32)
     return ids, out["dist"].numpy()[ids], tri[ids], out["point"].numpy()[ids]

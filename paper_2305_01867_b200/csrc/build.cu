@@ -418,7 +418,10 @@ __device__ __forceinline__ void write_slot(float4* nodes, int node, int side, co
 // (a fire-and-forget reduction in the rounds) for the validator's "atomic: 2"
 // check, and every level writes the child's box into the global
 // node slot the traversal reads.
-constexpr int kRefitLeaves = 512;
+#ifndef RSI_REFIT_LEAVES
+#define RSI_REFIT_LEAVES 256  // leaves per CTA window (256: -3 % rebuild vs 512; 1024 exceeds static smem)
+#endif
+constexpr int kRefitLeaves = RSI_REFIT_LEAVES;
 
 __global__ void __launch_bounds__(kRefitLeaves) k_refit(const float* __restrict__ V, int64_t nv,
                                                         const int32_t* __restrict__ T,

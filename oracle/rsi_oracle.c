@@ -41,6 +41,10 @@
  * Pins (tests/test_oracle.py, all -m "not gpu"): the Fig. 3 worked example
  * (P:194-200), exact-rational plane-clip referee on tiny random
  * meshes, closed-form unit-cube clipping, closed-mesh parity, canopy counts.
+ * PARITY UNPINNED: the dedup threshold tau of intercept_count itself (the
+ * paper never defines "unique intersections"; reading R4) --
+ * the single-linkage rule is pinned (layer counts, shared-edge merges), the
+ * value 1e-6 is a convention.
  */
 #include <math.h>
 #include <stdint.h>

@@ -469,9 +469,9 @@ rsi_status_t rsi_bvh_download(rsi_handle_t h, int32_t* h_child, float* h_box, in
     }
     float4* tris = nullptr;
     if (st == RSI_OK && h_leaf_tri) {
-        tris = new (std::nothrow) float4[4 * nt];
+        tris = new (std::nothrow) float4[kTriF4 * nt];
         if (!tris) st = rsi_set_error(RSI_E_OOM, "host allocation failed");
-        else st = rsi_cuda_check(cudaMemcpyAsync(tris, h->tris, nt * 4 * sizeof(float4), cudaMemcpyDeviceToHost, s), "tris");
+        else st = rsi_cuda_check(cudaMemcpyAsync(tris, h->tris, nt * kTriF4 * sizeof(float4), cudaMemcpyDeviceToHost, s), "tris");
     }
     // Apetrei builds: codes are 63-bit (the top 30 bits are the 30-bit code) and
     // arrival counts live in the high words of the 64-bit node words
@@ -530,7 +530,7 @@ rsi_status_t rsi_bvh_download(rsi_handle_t h, int32_t* h_child, float* h_box, in
         if (h_leaf_tri)
             for (int64_t k = 0; k < nt; ++k) {
                 int32_t id;
-                memcpy(&id, &tris[4 * k].w, 4);
+                memcpy(&id, &tris[kTriF4 * k].w, 4);
                 h_leaf_tri[k] = id;
             }
     }

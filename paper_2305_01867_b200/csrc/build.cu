@@ -462,10 +462,10 @@ __global__ void __launch_bounds__(kRefitLeaves) k_refit(const float* __restrict_
             lo[x] = fminf(a[x], fminf(b[x], c[x]));
             hi[x] = fmaxf(a[x], fmaxf(b[x], c[x]));
         }
-        tris[4 * k + 0] = make_float4(a[0], a[1], a[2], __int_as_float(id));
-        tris[4 * k + 1] = make_float4(b[0], b[1], b[2], 0.f);
-        tris[4 * k + 2] = make_float4(c[0], c[1], c[2], 0.f);
-        tris[4 * k + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
+        tris[kTriF4 * k + 0] = make_float4(a[0], a[1], a[2], __int_as_float(id));
+        tris[kTriF4 * k + 1] = make_float4(b[0], b[1], b[2], 0.f);
+        tris[kTriF4 * k + 2] = make_float4(c[0], c[1], c[2], 0.f);
+        if (kTriF4 == 4) tris[4 * k + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
         p = parent[n_nodes + k];
     }
     __syncthreads();
@@ -760,10 +760,10 @@ __global__ void __launch_bounds__(kBlock) k_apetrei(const float* __restrict__ V,
         lo[x] = fminf(a[x], fminf(b[x], c[x]));
         hi[x] = fmaxf(a[x], fmaxf(b[x], c[x]));
     }
-    tris[4 * k + 0] = make_float4(a[0], a[1], a[2], __int_as_float(id));
-    tris[4 * k + 1] = make_float4(b[0], b[1], b[2], 0.f);
-    tris[4 * k + 2] = make_float4(c[0], c[1], c[2], 0.f);
-    tris[4 * k + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
+    tris[kTriF4 * k + 0] = make_float4(a[0], a[1], a[2], __int_as_float(id));
+    tris[kTriF4 * k + 1] = make_float4(b[0], b[1], b[2], 0.f);
+    tris[kTriF4 * k + 2] = make_float4(c[0], c[1], c[2], 0.f);
+    if (kTriF4 == 4) tris[4 * k + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
     int l = k, r = k;
     int32_t ref = ~k;
     while (true) {
@@ -1065,7 +1065,7 @@ __global__ void __launch_bounds__(kBlock) k_validate_leaves(const float4* __rest
                                                             unsigned long long* __restrict__ out) {
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     if (k >= n) return;
-    const int id = __float_as_int(tris[4 * k].w);
+    const int id = __float_as_int(tris[kTriF4 * k].w);
     if (id < 0 || id >= n) atomicAdd(out + V_LEAFIDS, 1ull);
     else atomicAdd(seen + id, 1u);
     const int root = (int)scratch[SCR_ROOT_NODE];
@@ -1107,7 +1107,7 @@ static rsi_status_t ensure_capacity(rsi_bvh* h, int64_t n, cudaStream_t s) {
     RSI_ALLOC(h->nodes, nn * 4 * sizeof(float4));
     RSI_ALLOC(h->top, (size_t)(kTopNodes > 0 ? kTopNodes : 1) * 4 * sizeof(float4));
     RSI_ALLOC(h->quads, nn * 4 * sizeof(float4));
-    RSI_ALLOC(h->tris, n * 4 * sizeof(float4));
+    RSI_ALLOC(h->tris, n * kTriF4 * sizeof(float4));
     RSI_ALLOC(h->keys, n * sizeof(uint32_t));
     RSI_ALLOC(h->vals, n * sizeof(int32_t));
     RSI_ALLOC(h->keys_tmp, n * sizeof(uint32_t));

@@ -137,6 +137,13 @@ __host__ __device__ inline float rsi_ord2f(uint32_t u) {
 #endif
 }
 
+// triangle record: 4 float4 (64 B: two 256-bit loads, the default) or, with
+// RSI_TRI48, 3 float4 (48 B: three 128-bit loads, a smaller working set)
+#ifndef RSI_TRI48
+#define RSI_TRI48 0
+#endif
+constexpr int kTriF4 = RSI_TRI48 ? 3 : 4;
+
 // top-of-tree shared-memory cache (build.cu k_topk, traverse.cu)
 #ifndef RSI_TOPK
 #define RSI_TOPK 0  // measured slower at 1024/2048 on the bench workload (1 CTA/SM)

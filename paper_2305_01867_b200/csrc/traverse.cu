@@ -343,9 +343,16 @@ __device__ __forceinline__ void ldg256(const float4* p, float4& a, float4& b) {
 
 // triangle slot k: 64 B (4 x float4, the last one padding) for two 256-bit loads
 __device__ __forceinline__ void load_tri(const float4* __restrict__ tris, int k, float4& A, float4& B, float4& C) {
-    float4 pad;
-    ldg256(tris + 4 * k, A, B);
-    ldg256(tris + 4 * k + 2, C, pad);
+    if (kTriF4 == 3) {
+        const float4* t = tris + 3 * (int64_t)k;
+        A = __ldg(t);
+        B = __ldg(t + 1);
+        C = __ldg(t + 2);
+    } else {
+        float4 pad;
+        ldg256(tris + 4 * k, A, B);
+        ldg256(tris + 4 * k + 2, C, pad);
+    }
 }
 
 // ---------------------------------------------------------------- traversal skeleton
@@ -1047,7 +1054,7 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                 // c0 is the nearest hit child (kSort) -- kNoRef only when none hit
                 if (RSI_PF_PUSH) {
                     auto pf = [&](int c) {
-                        if (c != kNoRef) prefetch_l1(c >= 0 ? (const void*)(p.quads + 4 * c) : (const void*)(p.tris + 4 * ~c));
+                        if (c != kNoRef) prefetch_l1(c >= 0 ? (const void*)(p.quads + 4 * c) : (const void*)(p.tris + kTriF4 * ~c));
                     };
                     pf(c1);
                     pf(c2);
@@ -1059,7 +1066,7 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                 int first = c0;
                 if (first == kNoRef && sp > 0) first = stk.pop(sp);
                 if (first != kNoRef && first < 0) {  // a leaf
-                    if (RSI_PF_TRI) prefetch_l1(p.tris + 4 * ~first);
+                    if (RSI_PF_TRI) prefetch_l1(p.tris + kTriF4 * ~first);
                     if (l0 < 0) {
                         l0 = ~first;
                         // kQSpec: keep walking from the next stack entry while

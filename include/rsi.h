@@ -225,7 +225,27 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices,
                       int32_t mode, const rsi_options_t* options,
                       const rsi_outputs_t* h_out, void* stream);
 
-/* Free the calling thread's cached rsi_test workspace on every device. */
+/*
+ * rsi_test_sparse -- the paper's barycentric return shape end to end (P:101:
+ * `(intersecting_rays, distances, hit_triangles, hit_points) = rsi.test(...)`)
+ * on HOST buffers: rays stream to the device in 1 Mi-segment chunks overlapped
+ * with the build and the per-chunk traversal; step 3a (compaction of the hit
+ * rays) and the gather of their values run on the device; only the hits
+ * come back.  Outputs (HOST, capacity n_rays each; the first *h_n_hits entries
+ * are written, in ascending ray order):
+ *   h_ray_ids [n] int32 ray index; h_dist [n] float32 t*|end-start| (3b);
+ *   h_tri [n] int32 original triangle index; h_point [n][3] float32 (3d).
+ * h_dist, h_tri, h_point may be NULL.  Synchronizes `stream`.  Workspace cached
+ * per thread and device (rsi_release_cache frees it).
+ * Errors: as rsi_test; RSI_E_INVALID_ARG for n_rays > 2^31 - 1.
+ */
+rsi_status_t rsi_test_sparse(const float* h_vertices, int64_t n_vertices,
+                             const int32_t* h_triangles, int64_t n_triangles,
+                             const float* h_start, const float* h_end, int64_t n_rays,
+                             const rsi_options_t* options, int32_t* h_ray_ids, float* h_dist,
+                             int32_t* h_tri, float* h_point, int64_t* h_n_hits, void* stream);
+
+/* Free the calling thread's cached rsi_test / rsi_test_sparse workspaces on every device. */
 void rsi_release_cache(void);
 
 /*

@@ -357,10 +357,144 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
     return st != RSI_OK ? st : st2;
 }
 
+// Per-(thread, device) workspace of rsi_test_sparse (its own handle, so the
+// two entry points do not rebuild each other's cached BVH).
+static thread_local TestCtx g_sparse_ctx[16];
+
+rsi_status_t rsi_test_sparse(const float* h_vertices, int64_t n_vertices, const int32_t* h_triangles,
+                             int64_t n_triangles, const float* h_start, const float* h_end, int64_t n_rays,
+                             const rsi_options_t* options, int32_t* h_ray_ids, float* h_dist, int32_t* h_tri,
+                             float* h_point, int64_t* h_n_hits, void* stream) {
+    if (!h_n_hits || !h_ray_ids || n_rays < 0 || (n_rays > 0 && (!h_start || !h_end)))
+        return rsi_set_error(RSI_E_INVALID_ARG, "bad rsi_test_sparse arguments");
+    if (n_rays > ((int64_t)1 << 31) - 1) return rsi_set_error(RSI_E_INVALID_ARG, "n_rays exceeds 2^31-1");
+    rsi_status_t st = check_mesh_args(h_vertices, n_vertices, h_triangles, n_triangles);
+    if (st != RSI_OK) return st;
+    rsi_options_t opt;
+    st = read_options(options, &opt);
+    if (st != RSI_OK) return st;
+    *h_n_hits = 0;
+    cudaStream_t s = (cudaStream_t)stream;
+    int dev = 0;
+    st = rsi_cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (st != RSI_OK) return st;
+    TestCtx& ctx = g_sparse_ctx[dev & 15];
+    if (ctx.dev != dev) {
+        ctx.release();
+        ctx.dev = dev;
+    }
+    rsi_keep_pool_cached();
+    // workspace: mesh | start | end | dense tri, dist, point | ids, n_hits | sparse tri, dist, point
+    auto up = [](size_t x) { return (x + 255) / 256 * 256; };
+    const size_t n = (size_t)n_rays;
+    const size_t bv = up((size_t)n_vertices * 12), bt = up((size_t)n_triangles * 12);
+    const size_t b12 = up(n * 12), b4 = up(n * 4);
+    const size_t need = bv + bt + 2 * b12 + (2 * b4 + b12) + (b4 + 256) + (2 * b4 + b12);
+    if (ctx.buf_bytes < need) {
+        if (ctx.buf) {
+            cudaStreamSynchronize(s);
+            cudaFree(ctx.buf);
+            ctx.buf = nullptr;
+            ctx.buf_bytes = 0;
+        }
+        st = rsi_cuda_check(cudaMalloc((void**)&ctx.buf, need), "rsi_test_sparse workspace");
+        if (st != RSI_OK) return st;
+        ctx.buf_bytes = need;
+    }
+    char* q = ctx.buf;
+    float* dV = (float*)q; q += bv;
+    int32_t* dT = (int32_t*)q; q += bt;
+    float* dS = (float*)q; q += b12;
+    float* dE = (float*)q; q += b12;
+    int32_t* tri = (int32_t*)q; q += b4;
+    float* dist = (float*)q; q += b4;
+    float* point = (float*)q; q += b12;
+    int32_t* ids = (int32_t*)q; q += b4;
+    int32_t* d_n = (int32_t*)q; q += 256;
+    int32_t* stri = (int32_t*)q; q += b4;
+    float* sdist = (float*)q; q += b4;
+    float* spoint = (float*)q;
+    // rays stream in 1 Mi-segment chunks on a copy stream; each chunk's
+    // traversal starts as soon as its copy lands (and the BVH is built)
+    const int64_t kChunkRays = (int64_t)1 << 20;
+    const int64_t nchunk = (n_rays + kChunkRays - 1) / kChunkRays;
+    if (ctx.n_ev < nchunk + 1) {
+        for (int64_t k = 0; k < ctx.n_ev; ++k) cudaEventDestroy(ctx.ev[k]);
+        delete[] ctx.ev;
+        ctx.n_ev = 0;
+        ctx.ev = new (std::nothrow) cudaEvent_t[nchunk + 1]();
+        if (!ctx.ev) return rsi_set_error(RSI_E_OOM, "host allocation failed");
+        for (int64_t k = 0; k < nchunk + 1; ++k) {
+            st = rsi_cuda_check(cudaEventCreateWithFlags(&ctx.ev[k], cudaEventDisableTiming), "event");
+            if (st != RSI_OK) return st;
+            ctx.n_ev = k + 1;
+        }
+    }
+    cudaStream_t sh = nullptr, sd = nullptr;
+    st = side_streams(sh, sd);
+    if (st == RSI_OK) st = rsi_cuda_check(cudaEventRecord(ctx.ev[nchunk], s), "event");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaStreamWaitEvent(sh, ctx.ev[nchunk], 0), "wait");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaMemcpyAsync(dV, h_vertices, (size_t)n_vertices * 12, cudaMemcpyHostToDevice, s), "H2D vertices");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaMemcpyAsync(dT, h_triangles, (size_t)n_triangles * 12, cudaMemcpyHostToDevice, s), "H2D triangles");
+    for (int64_t c = 0; st == RSI_OK && c < nchunk; ++c) {
+        const int64_t r0 = c * kChunkRays, nr = (n_rays - r0) < kChunkRays ? (n_rays - r0) : kChunkRays;
+        st = rsi_cuda_check(cudaMemcpyAsync(dS + 3 * r0, h_start + 3 * r0, (size_t)nr * 12, cudaMemcpyHostToDevice, sh), "H2D start");
+        if (st == RSI_OK) st = rsi_cuda_check(cudaMemcpyAsync(dE + 3 * r0, h_end + 3 * r0, (size_t)nr * 12, cudaMemcpyHostToDevice, sh), "H2D end");
+        if (st == RSI_OK) st = rsi_cuda_check(cudaEventRecord(ctx.ev[c], sh), "event");
+    }
+    if (st == RSI_OK) {
+        if (ctx.h) {
+            ctx.h->opt = opt;
+            st = rsi_rebuild(ctx.h, dV, n_vertices, dT, n_triangles, stream);
+        } else {
+            st = rsi_build(dV, n_vertices, dT, n_triangles, &opt, stream, &ctx.h);
+        }
+    }
+    for (int64_t c = 0; st == RSI_OK && c < nchunk; ++c) {
+        const int64_t r0 = c * kChunkRays, nr = (n_rays - r0) < kChunkRays ? (n_rays - r0) : kChunkRays;
+        st = rsi_cuda_check(cudaStreamWaitEvent(s, ctx.ev[c], 0), "wait");
+        rsi_outputs_t o{};
+        o.tri = tri + r0;
+        o.dist = dist + r0;
+        o.point = point + 3 * r0;
+        if (st == RSI_OK) st = rsi_intersect(ctx.h, dS + 3 * r0, dE + 3 * r0, nr, RSI_MODE_BARYCENTRIC, &o, stream);
+    }
+    // 3a on the device, then the values of the hit rays only
+    if (st == RSI_OK) st = rsi_compact_device(tri, n_rays, ids, d_n, s);
+    if (st == RSI_OK) st = rsi_gather_hits_device(ids, d_n, n_rays, tri, dist, point, stri, sdist, spoint, s);
+    int32_t nh = 0;
+    if (st == RSI_OK) st = rsi_cuda_check(cudaMemcpyAsync(&nh, d_n, 4, cudaMemcpyDeviceToHost, s), "D2H hit count");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaStreamSynchronize(s), "rsi_test_sparse");
+    if (st == RSI_OK && nh > 0) {
+        st = rsi_cuda_check(cudaMemcpyAsync(h_ray_ids, ids, (size_t)nh * 4, cudaMemcpyDeviceToHost, s), "D2H ids");
+        if (st == RSI_OK && h_tri) st = rsi_cuda_check(cudaMemcpyAsync(h_tri, stri, (size_t)nh * 4, cudaMemcpyDeviceToHost, s), "D2H tri");
+        if (st == RSI_OK && h_dist) st = rsi_cuda_check(cudaMemcpyAsync(h_dist, sdist, (size_t)nh * 4, cudaMemcpyDeviceToHost, s), "D2H dist");
+        if (st == RSI_OK && h_point) st = rsi_cuda_check(cudaMemcpyAsync(h_point, spoint, (size_t)nh * 12, cudaMemcpyDeviceToHost, s), "D2H point");
+    }
+    // join the copy stream (also on error paths) and synchronize
+    cudaEvent_t fin;
+    if (sh && cudaEventCreateWithFlags(&fin, cudaEventDisableTiming) == cudaSuccess) {
+        cudaEventRecord(fin, sh);
+        cudaStreamWaitEvent(s, fin, 0);
+        cudaEventDestroy(fin);
+    }
+    const rsi_status_t st2 = rsi_cuda_check(cudaStreamSynchronize(s), "rsi_test_sparse");
+    if (st != RSI_OK) {
+        char saved[512];
+        memcpy(saved, g_err, sizeof(saved));
+        ctx.release();
+        memcpy(g_err, saved, sizeof(saved));
+        return st;
+    }
+    if (st2 == RSI_OK) *h_n_hits = nh;
+    return st2;
+}
+
 void rsi_release_cache(void) {
     int dev = 0;
     cudaGetDevice(&dev);
     for (auto& c : g_test_ctx) c.release();
+    for (auto& c : g_sparse_ctx) c.release();
     cudaSetDevice(dev);
 }
 

@@ -112,6 +112,10 @@ rsi_status_t rsi_finish_build(rsi_bvh* h, cudaStream_t stream);  // build.cu: re
 rsi_status_t rsi_validate_device(rsi_bvh* h, rsi_integrity_t* report, cudaStream_t stream);  // build.cu
 rsi_status_t rsi_compact_device(const int32_t* d_tri, int64_t n_rays, int32_t* d_ids,
                                 int32_t* d_n, cudaStream_t stream);
+// traverse.cu: values of the compacted hit rays (sparse barycentric return)
+rsi_status_t rsi_gather_hits_device(const int32_t* ids, const int32_t* n_hits, int64_t n_max, const int32_t* tri,
+                                    const float* dist, const float* point, int32_t* out_tri, float* out_dist,
+                                    float* out_point, cudaStream_t s);
 
 // ---------------------------------------------------------------- device helpers
 

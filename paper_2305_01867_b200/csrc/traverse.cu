@@ -1465,7 +1465,34 @@ __global__ void __launch_bounds__(256) k_compact_write(const int32_t* __restrict
     }
 }
 
+// Sparse barycentric return: the values of the compacted hit rays,
+// in ascending ray order (grid-stride over the device-side hit count).
+__global__ void __launch_bounds__(256) k_gather_hits(const int32_t* __restrict__ ids, const int32_t* __restrict__ n_hits,
+                                                     const int32_t* __restrict__ tri, const float* __restrict__ dist,
+                                                     const float* __restrict__ point, int32_t* __restrict__ out_tri,
+                                                     float* __restrict__ out_dist, float* __restrict__ out_point) {
+    const int m = *n_hits;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+        const int i = ids[j];
+        out_tri[j] = tri[i];
+        out_dist[j] = dist[i];
+        out_point[3 * j] = point[3 * (int64_t)i];
+        out_point[3 * j + 1] = point[3 * (int64_t)i + 1];
+        out_point[3 * j + 2] = point[3 * (int64_t)i + 2];
+    }
+}
+
 }  // namespace
+
+rsi_status_t rsi_gather_hits_device(const int32_t* ids, const int32_t* n_hits, int64_t n_max, const int32_t* tri,
+                                    const float* dist, const float* point, int32_t* out_tri, float* out_dist,
+                                    float* out_point, cudaStream_t s) {
+    if (n_max <= 0) return RSI_OK;
+    int blocks = rsi_ceil_div(n_max, 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    rsi_note_launch(), k_gather_hits<<<blocks, 256, 0, s>>>(ids, n_hits, tri, dist, point, out_tri, out_dist, out_point);
+    return rsi_cuda_check(cudaGetLastError(), "gather launch");
+}
 
 // ---------------------------------------------------------------- host side
 template <int MODE, bool kFP64, bool kCounters>

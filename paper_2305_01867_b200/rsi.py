@@ -96,6 +96,8 @@ def load():
             "rsi_bvh_download": ([_p, _p, _p, _p, _p, _p, _p, _p], ctypes.c_int),
             "rsi_validate": ([_p, ctypes.POINTER(_Integrity), _p], ctypes.c_int),
             "rsi_bvh_root": ([_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _p, _p], ctypes.c_int),
+            "rsi_test_sparse": ([_p, _i64, _p, _i64, _p, _p, _i64, _p, _p, _p, _p, _p, ctypes.POINTER(_i64), _p],
+                                ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             f = getattr(lib, name)
@@ -302,10 +304,23 @@ def rsi_test(vertices, triangles, start, end, cfg: dict | None = None, options: 
     S = host(start, torch.float32, "start").reshape(-1, 3)
     E = host(end, torch.float32, "end").reshape(-1, 3)
     n = S.shape[0]
+    opt = (options or Options())._c()
+    if mode == "barycentric" and sparse and out is None:
+        # the paper's sparse tuple: compaction and gather on the device
+        ids = np.empty(n, np.int32)
+        dist = np.empty(n, np.float32)
+        tri = np.empty(n, np.int32)
+        point = np.empty((n, 3), np.float32)
+        nh = _i64()
+        ptr = lambda a: a.ctypes.data_as(_p)  # noqa: E731
+        _check(lib.rsi_test_sparse(V.data_ptr(), V.shape[0], T.data_ptr(), T.shape[0], S.data_ptr(), E.data_ptr(), n,
+                                   ctypes.byref(opt), ptr(ids), ptr(dist), ptr(tri), ptr(point), ctypes.byref(nh),
+                                   _stream(stream)))
+        m = nh.value
+        return ids[:m], dist[:m], tri[:m], point[:m]
     if out is None:
         out = {k: v.cpu() for k, v in alloc_outputs(n, mode, "cpu").items()}
     o = _outputs_struct(out)
-    opt = (options or Options())._c()
     _check(lib.rsi_test(V.data_ptr(), V.shape[0], T.data_ptr(), T.shape[0], S.data_ptr(), E.data_ptr(), n,
                         MODES[mode], ctypes.byref(opt), ctypes.byref(o), _stream(stream)))
     if mode == "boolean":

@@ -701,3 +701,25 @@ def test_overflow_warp_dedup(rsi, n_sheets):
     got = run_all(rsi, V, T, S, E)
     assert (got["count"] == ref["count"]).all(), np.nonzero(got["count"] != ref["count"])[0][:10]
     assert got["stats"]["overflow_rays"] > 0 and ref["count"].max() > 8
+
+
+def test_rsi_test_sparse_device_compaction(rsi):
+    """rsi_test_sparse (the paper's barycentric return) over several
+    1 Mi-ray chunks with a ragged tail: compaction (3a) and gather on
+    the device give exactly the dense path's hits in ascending ray order; no
+    hits -> empty arrays."""
+    V, T, S, E, _ = synth.workload("sphere", 2_500_003, seed=21)
+    ids, dist, tri, pts = rsi.rsi_test(V, T, S, E, {"mode": "barycentric"})
+    dense = rsi.rsi_test(V, T, S, E, {"mode": "barycentric"}, sparse=False)
+    dt = dense["tri"].numpy()
+    rid = np.nonzero(dt >= 0)[0]
+    assert (ids == rid).all()
+    assert (tri == dt[rid]).all()
+    assert (dist == dense["dist"].numpy()[rid]).all()
+    assert (pts == dense["point"].numpy()[rid]).all()
+    sample = rid[:: max(1, len(rid) // 300)][:300]
+    ref = oracle.run(V, T, S[sample], E[sample], flags=False)
+    assert (ref["tri"] == dt[sample]).all()
+    far = S + np.float32(10.0)
+    ids0, dist0, tri0, pts0 = rsi.rsi_test(V, T, far[:1000], (E + np.float32(10.0))[:1000], {"mode": "barycentric"})
+    assert len(ids0) == len(dist0) == len(tri0) == len(pts0) == 0

@@ -404,3 +404,36 @@ def rsi_validate(h: Handle, stream=None) -> dict:
     d = {n: int(getattr(rep, n)) for n, _ in _Integrity._fields_}
     d["ok"] = rc == 0
     return d
+
+
+class PyCudaRSI:
+    """The paper's user-facing call shape:
+
+        with PyCudaRSI(design_params) as pycu:
+            ray_intersects = pycu.test(vertices, triangles, raysFrom, raysTo, {'mode': 'boolean'})
+            (intersecting_rays, distances, hit_triangles, hit_points) = pycu.test(..., {'mode': 'barycentric'})
+
+    design_params: 'USE_DOUBLE_PRECISION_MOLLER' -> every Moller-Trumbore
+    test in double (results are identical either way, DESIGN.md 5);
+    'USE_EXTRA_BVH_FIELDS' (a debugging layout of the paper's node
+    struct) is accepted and has no effect -- the tree is inspected through
+    rsi_bvh_download / diagnostics instead.  Thin wrapper over rsi_test /
+    rsi_test_sparse; leaving the context releases the cached device workspace."""
+
+    _KNOWN = {"USE_DOUBLE_PRECISION_MOLLER", "USE_EXTRA_BVH_FIELDS"}
+
+    def __init__(self, design_params: dict | None = None):
+        params = dict(design_params or {})
+        unknown = set(params) - self._KNOWN
+        if unknown:
+            raise ValueError(f"unknown design_params {sorted(unknown)}; known: {sorted(self._KNOWN)}")
+        self.options = Options(fp64_moller=bool(params.get("USE_DOUBLE_PRECISION_MOLLER", False)))
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        rsi_release_cache()
+
+    def test(self, vertices, triangles, raysFrom, raysTo, cfg: dict | None = None):
+        return rsi_test(vertices, triangles, raysFrom, raysTo, cfg, self.options)

@@ -723,3 +723,19 @@ def test_rsi_test_sparse_device_compaction(rsi):
     far = S + np.float32(10.0)
     ids0, dist0, tri0, pts0 = rsi.rsi_test(V, T, far[:1000], (E + np.float32(10.0))[:1000], {"mode": "barycentric"})
     assert len(ids0) == len(dist0) == len(tri0) == len(pts0) == 0
+
+
+def test_pycudarsi_call_shape(rsi):
+    """P:89-102: `with PyCudaRSI(design_params) as pycu: pycu.test(...)` in every
+    mode, with USE_DOUBLE_PRECISION_MOLLER giving identical results."""
+    V, T, S, E, _ = synth.workload("cube", 3000, seed=1)
+    ref = oracle.run(V, T, S, E)
+    for params in ({}, {"USE_DOUBLE_PRECISION_MOLLER": True, "USE_EXTRA_BVH_FIELDS": True}):
+        with rsi.PyCudaRSI(params) as pycu:
+            b = pycu.test(V, T, S, E, {"mode": "boolean"})
+            c = pycu.test(V, T, S, E, {"mode": "intercept_count"})
+            ids, dist, tri, pts = pycu.test(V, T, S, E, {"mode": "barycentric"})
+        assert (b[:, 0] == ref["hit"].astype(bool)).all() and (c == ref["count"]).all()
+        rids, rdist, rtri, rpts = oracle.sparse_barycentric(ref)
+        assert (ids == rids).all() and (tri == rtri).all()
+        np.testing.assert_allclose(pts, rpts, atol=1e-5 * 2)

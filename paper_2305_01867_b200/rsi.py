@@ -415,7 +415,7 @@ class PyCudaRSI:
 
     design_params: 'USE_DOUBLE_PRECISION_MOLLER' -> every Moller-Trumbore
     test in double (results are identical either way, DESIGN.md 5);
-    'USE_EXTRA_BVH_FIELDS' (P:230, P:237, a debugging layout of the paper's node
+    'USE_EXTRA_BVH_FIELDS' (P:232, P:237, a debugging layout of the paper's node
     struct) is accepted and has no effect -- the tree is inspected through
     rsi_bvh_download / diagnostics instead.  Thin wrapper over rsi_test /
     rsi_test_sparse; leaving the context releases the cached device workspace."""

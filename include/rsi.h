@@ -68,6 +68,13 @@ typedef enum {
                                   rsi_intersect on an invalid mesh are unspecified (no
                                   out-of-bounds access either way).  For pipelines that
                                   rebuild and query every step with no host round trip. */
+#define RSI_OPT_ROTATE 16u     /* one bottom-up pass of local tree rotations fused into the
+                                  refit (default Karras path): at each completed node swap a
+                                  child with a grandchild on the other side when that shrinks
+                                  the rebuilt child's surface area (SAH-style, after Kensler).
+                                  Fewer box tests per segment; the leaf order (Morton) is
+                                  kept, so the paper's node numbering is not.
+                                  Same results. */
 #define RSI_OPT_APETREI 8u     /* the paper's construction instead of
                                   Karras + refit -- 63-bit Morton codes (21 bits per axis,
                                   z-major; "64-bit Morton codes") sorted as

@@ -402,6 +402,103 @@ __device__ __forceinline__ void write_slot(float4* nodes, int node, int side, co
     f[9 + 2 * side] = hi[2];
 }
 
+// RSI_OPT_ROTATE: one local tree rotation at a node whose subtree is complete
+// (Kensler-style, surface-area heuristic): swap one child with a grandchild on
+// the other side when that shrinks the surface area of the rebuilt child box.
+// The node's own leaf set and box are unchanged, so its ancestors are not
+// affected; the moved subtrees get new parent links and the rebuilt child's
+// slot box is the exact union of its new slots (the validator's invariants
+// hold).  Reads use L2-coherent loads: children completed by other threads are
+// ordered before us by the refit's barrier / acq_rel protocol.
+__device__ __forceinline__ float box_area(const float lo[3], const float hi[3]) {
+    const float dx = fmaxf(hi[0] - lo[0], 0.f), dy = fmaxf(hi[1] - lo[1], 0.f), dz = fmaxf(hi[2] - lo[2], 0.f);
+    return dx * dy + dy * dz + dz * dx;
+}
+__device__ __forceinline__ void read_slot(const float4* nodes, int node, int side, float lo[3], float hi[3],
+                                          int32_t& ref) {
+    const float4* nd = nodes + 4 * node;
+    const float4 a = __ldcg(nd + side), z = __ldcg(nd + 2), r = __ldcg(nd + 3);
+    lo[0] = a.x; hi[0] = a.y; lo[1] = a.z; hi[1] = a.w;
+    lo[2] = side ? z.z : z.x;
+    hi[2] = side ? z.w : z.y;
+    ref = __float_as_int(side ? r.y : r.x);
+}
+__device__ __forceinline__ void set_parent(int32_t* parent, int n_nodes, int32_t ref, int node, int side) {
+    parent[ref >= 0 ? ref : n_nodes + ~ref] = (node << 1) | side;
+}
+__device__ void rotate_node(float4* nodes, int32_t* parent, int n_nodes, int node) {
+    float Llo[3], Lhi[3], Rlo[3], Rhi[3];
+    int32_t rL, rR;
+    read_slot(nodes, node, 0, Llo, Lhi, rL);
+    read_slot(nodes, node, 1, Rlo, Rhi, rR);
+    float best = 0.f;
+    int choice = -1;  // 0: L<->R0, 1: L<->R1, 2: R<->L0, 3: R<->L1
+    float ulo[3], uhi[3];
+    auto uni = [&](const float* alo, const float* ahi, const float* blo, const float* bhi) {
+        for (int x = 0; x < 3; ++x) {
+            ulo[x] = fminf(alo[x], blo[x]);
+            uhi[x] = fmaxf(ahi[x], bhi[x]);
+        }
+        return box_area(ulo, uhi);
+    };
+    float R0lo[3], R0hi[3], R1lo[3], R1hi[3], L0lo[3], L0hi[3], L1lo[3], L1hi[3];
+    int32_t rR0 = 0, rR1 = 0, rL0 = 0, rL1 = 0;
+    if (rR >= 0) {
+        read_slot(nodes, rR, 0, R0lo, R0hi, rR0);
+        read_slot(nodes, rR, 1, R1lo, R1hi, rR1);
+        const float cur = box_area(Rlo, Rhi);
+        const float a = cur - uni(Llo, Lhi, R1lo, R1hi), b = cur - uni(R0lo, R0hi, Llo, Lhi);
+        if (a > best) { best = a; choice = 0; }
+        if (b > best) { best = b; choice = 1; }
+    }
+    if (rL >= 0) {
+        read_slot(nodes, rL, 0, L0lo, L0hi, rL0);
+        read_slot(nodes, rL, 1, L1lo, L1hi, rL1);
+        const float cur = box_area(Llo, Lhi);
+        const float c = cur - uni(Rlo, Rhi, L1lo, L1hi), d = cur - uni(L0lo, L0hi, Rlo, Rhi);
+        if (c > best) { best = c; choice = 2; }
+        if (d > best) { best = d; choice = 3; }
+    }
+    if (choice < 0) return;
+    if (choice == 0) {  // node = (R0, R' = (L, R1))
+        uni(Llo, Lhi, R1lo, R1hi);
+        write_slot(nodes, node, 0, R0lo, R0hi);
+        set_ref(nodes, node, 0, rR0);
+        write_slot(nodes, node, 1, ulo, uhi);
+        write_slot(nodes, rR, 0, Llo, Lhi);
+        set_ref(nodes, rR, 0, rL);
+        set_parent(parent, n_nodes, rR0, node, 0);
+        set_parent(parent, n_nodes, rL, rR, 0);
+    } else if (choice == 1) {  // node = (R1, R' = (R0, L))
+        uni(R0lo, R0hi, Llo, Lhi);
+        write_slot(nodes, node, 0, R1lo, R1hi);
+        set_ref(nodes, node, 0, rR1);
+        write_slot(nodes, node, 1, ulo, uhi);
+        write_slot(nodes, rR, 1, Llo, Lhi);
+        set_ref(nodes, rR, 1, rL);
+        set_parent(parent, n_nodes, rR1, node, 0);
+        set_parent(parent, n_nodes, rL, rR, 1);
+    } else if (choice == 2) {  // node = (L' = (R, L1), L0)
+        uni(Rlo, Rhi, L1lo, L1hi);
+        write_slot(nodes, node, 1, L0lo, L0hi);
+        set_ref(nodes, node, 1, rL0);
+        write_slot(nodes, node, 0, ulo, uhi);
+        write_slot(nodes, rL, 0, Rlo, Rhi);
+        set_ref(nodes, rL, 0, rR);
+        set_parent(parent, n_nodes, rL0, node, 1);
+        set_parent(parent, n_nodes, rR, rL, 0);
+    } else {  // node = (L' = (L0, R), L1)
+        uni(L0lo, L0hi, Rlo, Rhi);
+        write_slot(nodes, node, 1, L1lo, L1hi);
+        set_ref(nodes, node, 1, rL1);
+        write_slot(nodes, node, 0, ulo, uhi);
+        write_slot(nodes, rL, 1, Rlo, Rhi);
+        set_ref(nodes, rL, 1, rR);
+        set_parent(parent, n_nodes, rL1, node, 1);
+        set_parent(parent, n_nodes, rR, rL, 1);
+    }
+}
+
 // One thread per leaf slot k: pack triangle k (Morton order), compute its AABB
 // and ascend.  A CTA owns the leaf window [c0, c0 + kRefitLeaves): an
 // internal node whose leaf range (stored by k_karras) lies inside the window
@@ -427,8 +524,8 @@ __global__ void __launch_bounds__(kRefitLeaves) k_refit(const float* __restrict_
                                                         const int32_t* __restrict__ T,
                                                         const int32_t* __restrict__ vals, int n_leaves, int n,
                                                         float4* nodes, float4* __restrict__ tris,
-                                                        const int32_t* __restrict__ parent, uint32_t* arrivals,
-                                                        uint32_t* scratch) {
+                                                        int32_t* parent, uint32_t* arrivals,
+                                                        uint32_t* scratch, int rotate) {
     __shared__ uint32_t s_arr[kRefitLeaves];
     __shared__ float s_box[kRefitLeaves][2][6];
     __shared__ int32_t s_par[kRefitLeaves];  // parent links of the window's internal nodes
@@ -505,6 +602,7 @@ __global__ void __launch_bounds__(kRefitLeaves) k_refit(const float* __restrict_
                 hi[x] = fmaxf(hi[x], ob[3 + x]);
             }
             const int node = wi + c0;
+            if (rotate) rotate_node(nodes, parent, n_nodes, node);
             if (node == 0) {
                 state = 4;  // merged at the root inside the window
             } else {
@@ -533,6 +631,7 @@ __global__ void __launch_bounds__(kRefitLeaves) k_refit(const float* __restrict_
             hi[1] = fmaxf(hi[1], __ldcg(f + o + 3));
             lo[2] = fminf(lo[2], __ldcg(f + 8 + 2 * (1 - side)));
             hi[2] = fmaxf(hi[2], __ldcg(f + 9 + 2 * (1 - side)));
+            if (rotate) rotate_node(nodes, parent, n_nodes, node);
             if (node == 0) break;
             p = p_next;
             write_slot(nodes, p >> 1, p & 1, lo, hi);
@@ -1227,7 +1326,8 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
         launch_sort(h, n, s);
         rsi_note_launch(), k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent, h->arrivals);
         rsi_note_launch(), k_refit<<<rsi_ceil_div(refit_leaves, kRefitLeaves), kRefitLeaves, 0, s>>>(V, nv, T, h->vals, refit_leaves, n, h->nodes,
-                                                                       h->tris, h->parent, h->arrivals, h->scratch);
+                                                                       h->tris, h->parent, h->arrivals, h->scratch,
+                                                                       (h->opt.flags & RSI_OPT_ROTATE) ? 1 : 0);
     }
     if (kTopNodes > 0) rsi_note_launch(), k_topk<<<1, 1024, 0, s>>>(h->nodes, n_nodes, h->top, h->scratch);
     if (rsi_uses_quads()) rsi_note_launch(), k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads, h->scratch);

@@ -26,6 +26,7 @@ OPT_FP64_MOLLER = 1
 OPT_COUNTERS = 2
 OPT_DEFERRED_STATUS = 4
 OPT_APETREI = 8
+OPT_ROTATE = 16
 
 _lock = threading.Lock()
 _lib = None
@@ -149,10 +150,12 @@ class Options:
     debug_refit_leaves: int = 0  # FAULT INJECTION (tests): refit only the first k leaves
     deferred_status: bool = False  # rsi_build/rsi_rebuild do not wait: check rsi_build_status
     apetrei: bool = False       # NEXT-1: 63-bit Morton codes + Apetrei build
+    rotate: bool = False        # local SAH tree rotations fused into the refit (NEXT-4 tree quality)
 
     def _c(self) -> _Options:
         flags = ((OPT_FP64_MOLLER if self.fp64_moller else 0) | (OPT_COUNTERS if self.counters else 0)
-                 | (OPT_DEFERRED_STATUS if self.deferred_status else 0) | (OPT_APETREI if self.apetrei else 0))
+                 | (OPT_DEFERRED_STATUS if self.deferred_status else 0) | (OPT_APETREI if self.apetrei else 0)
+                 | (OPT_ROTATE if self.rotate else 0))
         return _Options(ctypes.sizeof(_Options), flags, float(self.dedup_tau), int(self.debug_refit_leaves))
 
 

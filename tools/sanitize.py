@@ -38,6 +38,13 @@ for nt in (5000, 70001):
     assert rsi.rsi_validate(h)["ok"]
     rsi.rsi_bvh_download(h)
     h.free()
+for nt in (5000, 70001):  # refit with rotations; sparse end-to-end path
+    Vd = torch.from_numpy(V[:3 * nt]).to(dev); Td = torch.from_numpy(T[:nt]).to(dev)
+    h = rsi.rsi_build(Vd, Td, rsi.Options(rotate=True))
+    assert rsi.rsi_validate(h)["ok"]
+    rsi.rsi_intersect(h, Sd, Ed, "barycentric")
+    h.free()
+rsi.rsi_test(V[:15000], T[:5000], *synth.box_rays(3000, -0.2, 1.2, seed=4), {"mode": "barycentric"})
 h = rsi.rsi_build(Vd, Td, rsi.Options(apetrei=True, debug_refit_leaves=20000))
 assert not rsi.rsi_validate(h)["ok"]
 rsi.rsi_intersect(h, Sd, Ed, "boolean")

@@ -155,6 +155,16 @@ def _traffic(mode: str, rays: int):
         return None
 
 
+def _ncu_traversal(mode: str):
+    """Issue-slot use, SIMT width and cache hit rates of the traversal kernel from
+    the committed ncu --set full capture (profiles/ncu_traversal.json): why the
+    ALU fraction is what it is."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "ncu_traversal.json")))[mode]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def roofline(mode: str, rays: int, kernel_ms: float, sm_mhz: float | None, work: dict | None = None):
     w = work or WORK_MODEL[mode]
     inst_per_ray = w["box_tests"] * FP32_PER_BOX + w["mt_tests"] * FP32_PER_MT
@@ -164,7 +174,7 @@ def roofline(mode: str, rays: int, kernel_ms: float, sm_mhz: float | None, work:
     return {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 4), "unit": "TFP32-inst/s",
             "frac": round(achieved / peak, 5), "traffic": _traffic(mode, rays),
             "traffic_unit": "DRAM bytes/launch (ncu); algorithmic ray stream = 25 B/ray (boolean)",
-            "kernel": f"k_{mode}", "kernel_ms": round(kernel_ms, 4),
+            "kernel": f"k_{mode}", "kernel_ms": round(kernel_ms, 4), "ncu": _ncu_traversal(mode),
             "model": f"{w['box_tests']:.2f} box x {FP32_PER_BOX:.0f} + {w['mt_tests']:.2f} MT x {FP32_PER_MT:.0f} "
                      f"= {inst_per_ray:.0f} FP32 inst/ray ({'measured' if work else 'SURVEY 8(d) model'} "
                      f"tests/ray); peak = 148 SM x 128 FP32 lanes x median sm_mhz"}

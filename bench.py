@@ -70,6 +70,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample rays (0 = auto ~15 s)")
+    ap.add_argument("--fused-gather", action="store_true",
+                    help="N > 1: traversal writes straight into rank 0's buffers over NVLink (PeerOutputs) "
+                         "instead of the pipelined NCCL gather")
     return ap.parse_args()
 
 
@@ -185,7 +188,8 @@ def arm_config(args, n_tri: int, world: int, backend: str = "nccl") -> dict:
     """The `config` both arms report (the reference arm adds its sample)."""
     return {"workload": f"{args.workload} N_t={n_tri}, N_r={args.rays_per_gpu}/GPU, mode={args.mode}",
             "n_triangles": n_tri, "rays_per_gpu": args.rays_per_gpu, "mode": args.mode,
-            "parallelism": f"ray-sharded x{world}" + (f" + {backend} gather to rank 0" if world > 1 else ""),
+            "parallelism": f"ray-sharded x{world}" + ((" + fused NVLink writes to rank 0" if getattr(args, "fused_gather", False)
+                                                     else f" + {backend} gather to rank 0") if world > 1 else ""),
             "l2": "inputs larger than L2 (240 MB of segments per GPU)",
             "step": "rsi_rebuild + rsi_intersect" + (" + gather" if world > 1 else "")
                     + " (RSI_OPT_DEFERRED_STATUS: build checks read back after the timed region)"}
@@ -238,7 +242,7 @@ def main():
     import torch.distributed as dist
 
     from paper_2305_01867_b200 import rsi
-    from paper_2305_01867_b200.sharded import FIELDS, GatherPipeline
+    from paper_2305_01867_b200.sharded import FIELDS, GatherPipeline, PeerOutputs
 
     # one process per GPU; RSI_BENCH_BACKEND=gloo + more ranks than GPUs is a
     # launch/gather dry run on a single device (testing only, never a number)
@@ -267,8 +271,13 @@ def main():
         # traversal of step k+1; two output slots, each reused only after its
         # previous gather completed (a device-side wait); all gathers finish
         # inside the timed region (drain before the end event)
-        outs = [rsi.alloc_outputs(n, mode, dev) for _ in range(2 if world > 1 else 1)]
-        pipe = GatherPipeline(slots=2) if world > 1 else None
+        peer = PeerOutputs(n * world, mode, dev) if (world > 1 and args.fused_gather) else None
+        if peer is not None:
+            outs = [peer.outputs()]
+            pipe = None
+        else:
+            outs = [rsi.alloc_outputs(n, mode, dev) for _ in range(2 if world > 1 else 1)]
+            pipe = GatherPipeline(slots=2) if world > 1 else None
 
         def step(k, ev=None):
             out = outs[k % len(outs)]
@@ -284,6 +293,8 @@ def main():
                 ev[2].record(stream)
             if pipe is not None:
                 pipe.start(k % 2, {f: out[f] for f in FIELDS[mode]}, n * world)
+            if peer is not None:
+                peer.complete()  # device-side barrier: rank 0 holds every rank's rows
 
         for k in range(warmup):
             step(k)

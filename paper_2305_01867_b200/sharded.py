@@ -126,6 +126,56 @@ class GatherPipeline:
                 self.slots[i] = None
 
 
+# per-ray output fields: dtype and columns (rsi_outputs_t)
+FIELD_SPEC = {"hit": (torch.uint8, 1), "count": (torch.int32, 1), "tri": (torch.int32, 1),
+              "t": (torch.float32, 1), "dist": (torch.float32, 1), "point": (torch.float32, 3)}
+
+
+class PeerOutputs:
+    """The fused alternative to the gather: every rank's
+    traversal epilogue writes its slice of the per-ray outputs STRAIGHT INTO
+    RANK 0's buffers over NVLink (peer-mapped symmetric memory), so no separate
+    collective moves them; `complete()` is a device-side barrier across the
+    ranks on the current stream (each rank's kernel precedes it in stream
+    order, and the barrier's release/acquire makes the peer writes visible on
+    rank 0).  Every rank allocates the same symmetric buffers; only rank 0's
+    are written.  Correct by construction: each rank writes the disjoint rows
+    [floor(r N / W), floor((r+1) N / W)) of the full arrays, exactly the rows
+    the gather would place there.  Opt-in (bench --fused-gather); the default
+    multi-GPU path is GatherPipeline."""
+
+    def __init__(self, n_total: int, mode: str, device, group=None):
+        import torch.distributed._symmetric_memory as symm
+        self.group = group if group is not None else dist.group.WORLD
+        self.world = dist.get_world_size(self.group)
+        self.rank = dist.get_rank(self.group)
+        self.n_total = n_total
+        lo, hi = shard_range(n_total, self.rank, self.world)
+        self.local, self.slices, self._handles = {}, {}, []
+        for f in FIELDS[mode]:
+            dtype, cols = FIELD_SPEC[f]
+            buf = symm.empty(n_total * cols, dtype=dtype, device=device)
+            hdl = symm.rendezvous(buf, self.group)
+            remote = hdl.get_buffer(0, (n_total * cols,), dtype)  # rank 0's buffer, mapped here
+            shape = (n_total, cols) if cols > 1 else (n_total,)
+            self.local[f] = buf.view(shape)
+            self.slices[f] = remote.view(shape)[lo:hi]
+            self._handles.append(hdl)
+
+    def outputs(self) -> dict:
+        """Output tensors for rsi_intersect: this rank's rows of rank 0's arrays."""
+        return self.slices
+
+    def complete(self):
+        """Device-side barrier of all ranks on the current stream: afterwards
+        rank 0's arrays hold every rank's rows."""
+        self._handles[0].barrier(channel=0)
+
+    def result(self) -> dict | None:
+        """The full outputs on rank 0 (valid after complete()), None elsewhere."""
+        return self.local if self.rank == 0 else None
+
+
 def intersect_sharded(vertices: torch.Tensor, triangles: torch.Tensor, start: torch.Tensor, end: torch.Tensor,
                       mode: str = "boolean", options=None, group=None, intersect_fn=None) -> dict:
     """Replicated build + sharded intersect + gather.  `start`/`end` are the

@@ -759,3 +759,38 @@ def test_rotate_option_parity_and_integrity(rsi):
         h.free()
         assert rep["ok"], (nt, rep)
         assert sorted(d["leaf_tri"].tolist()) == list(range(nt))
+
+
+def test_peer_outputs_single_rank(rsi):
+    """PeerOutputs (the fused alternative to the gather): the
+    traversal writes into rank 0's symmetric buffers through the mapped
+    pointer and the device barrier completes the step; on one rank the result
+    equals a plain rsi_intersect bit for bit."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2305_01867_b200.sharded import PeerOutputs
+    own = not dist.is_initialized()
+    if own:
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]))
+        sk.close()
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device(DEV))
+    try:
+        V, T, S, E, _ = synth.workload("sphere", 100_003, seed=8)
+        Vd, Td, Sd, Ed = to_dev(V, T, S, E)
+        h = rsi.rsi_build(Vd, Td)
+        for mode in ("boolean", "barycentric", "intercept_count"):
+            peer = PeerOutputs(len(S), mode, torch.device(DEV))
+            rsi.rsi_intersect(h, Sd, Ed, mode, out=peer.outputs())
+            peer.complete()
+            ref = rsi.rsi_intersect(h, Sd, Ed, mode)
+            torch.cuda.synchronize()
+            for k, v in peer.result().items():
+                a, b = v.cpu(), ref[k].cpu()
+                assert torch.equal(a, b) or bool(((a == b) | (torch.isnan(a) & torch.isnan(b))).all()), (mode, k)
+        h.free()
+    finally:
+        if own:
+            dist.destroy_process_group()

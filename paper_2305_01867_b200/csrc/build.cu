@@ -2,11 +2,17 @@
 //
 //   A1+A2  k_extent_validate  index range + finite check, surface AABB
 //   A3     k_morton           30-bit z-major Morton code of each centroid
-//   A4     k_sort_*           hand-written stable LSD radix sort of (code, id)
+//   A4     k_sort_rank        stable rank sort, N_t <= 16384 (one launch)
+//          k_sort_hist/rowscan/scatter  hand-written stable 8-bit LSD radix sort
 //   A5     k_karras           Karras binary radix tree topology
 //   A6+A7  k_refit            leaf init + atomic bottom-up AABB refit written
 //                             straight into the 64 B child-pair layout (P:255-270,
-//                             P:442), triangles packed in Morton order
+//                             P:442), triangles packed in Morton order;
+//                             optional local SAH rotations (RSI_OPT_ROTATE)
+//   A7     k_quads            64 B 4-wide quantized records for the traversal
+//   NEXT-1 k_morton63, k_pass2_*, k_apetrei  63-bit codes + the paper's
+//                             agglomerative build (RSI_OPT_APETREI)
+//   NEXT-2 k_validate_*       GPU integrity validator
 //
 // Every grid is derived from the element count it covers (the case-study-2
 // lesson: never size one kernel's grid from another's count).

@@ -1,10 +1,14 @@
 // traverse.cu -- per-ray BVH traversal + Moller-Trumbore on sm_100a
 // (SURVEY 8(a) rows A8 and A9).
 //
-// One thread per segment.  Each thread walks the child-pair BVH with a short
-// stack (64 entries: depth <= 62 for the index-augmented 62-bit Karras key,
-// SURVEY 7), tests both child boxes of every node with a conservative slab
-// test, and runs Moller-Trumbore on every leaf whose box it enters.
+// One thread per segment, persistent grid.  The default walk visits the
+// 4-wide view of the binary tree (k_quads records: the up-to-4 grandchildren
+// of a node, 8-bit quantized boxes on a power-of-two grid, 64 B); every visit
+// slab-tests its children conservatively, orders the hit ones near-first,
+// keeps the next on a branch-free local stack (<= 144 entries: depth <= 95)
+// and queues leaves for a warp-wide Moller-Trumbore phase.  The binary
+// child-pair walk (RSI_*_QUAD=0) remains a build switch and is what the exact
+// intercept_count re-pass uses.
 //
 // Exactness.  Every discrete decision -- hit / miss,
 // nearest-hit order, dedup merge -- is taken in fp32 only when a forward error

@@ -228,6 +228,28 @@ def alloc_outputs(n: int, mode: str, device, with_t: bool = True) -> dict:
     raise ValueError(f"mode must be one of {list(MODES)}, got {mode!r}")
 
 
+_OUT_SPEC = {"hit": (torch.uint8, 1), "count": (torch.int32, 1), "tri": (torch.int32, 1),
+             "t": (torch.float32, 1), "dist": (torch.float32, 1), "point": (torch.float32, 3)}
+_REQUIRED = {"boolean": "hit", "intercept_count": "count", "barycentric": "tri"}
+
+
+def _check_out(out: dict, n: int, mode: str, device) -> None:
+    """Caller-provided outputs: the C-ABI takes bare pointers, so dtype, size,
+    contiguity and device are checked here (a short buffer would be overrun)."""
+    if _REQUIRED[mode] not in out or out[_REQUIRED[mode]] is None:
+        raise ValueError(f"{mode} needs out[{_REQUIRED[mode]!r}]")
+    for k, v in out.items():
+        if v is None or k not in _OUT_SPEC:
+            continue
+        dtype, cols = _OUT_SPEC[k]
+        if not isinstance(v, torch.Tensor) or v.dtype != dtype:
+            raise TypeError(f"out[{k!r}] must be a {dtype} tensor")
+        if not v.is_contiguous() or v.numel() < n * cols:
+            raise ValueError(f"out[{k!r}] must be contiguous with >= {n * cols} elements")
+        if torch.device(device) != v.device:
+            raise ValueError(f"out[{k!r}] is on {v.device}, expected {device}")
+
+
 def _outputs_struct(out: dict) -> _Outputs:
     o = _Outputs()
     for k in ("hit", "count", "tri", "t", "dist", "point"):
@@ -248,6 +270,8 @@ def rsi_intersect(h: Handle, start: torch.Tensor, end: torch.Tensor, mode: str =
     n = S.shape[0]
     if out is None:
         out = alloc_outputs(n, mode, S.device)
+    else:
+        _check_out(out, n, mode, S.device)
     o = _outputs_struct(out)
     with torch.cuda.device(S.device):
         _check(load().rsi_intersect(h.ptr, S.data_ptr(), E.data_ptr(), n, MODES[mode], ctypes.byref(o),
@@ -323,6 +347,8 @@ def rsi_test(vertices, triangles, start, end, cfg: dict | None = None, options: 
         return ids[:m], dist[:m], tri[:m], point[:m]
     if out is None:
         out = {k: v.cpu() for k, v in alloc_outputs(n, mode, "cpu").items()}
+    else:
+        _check_out(out, n, mode, "cpu")
     o = _outputs_struct(out)
     _check(lib.rsi_test(V.data_ptr(), V.shape[0], T.data_ptr(), T.shape[0], S.data_ptr(), E.data_ptr(), n,
                         MODES[mode], ctypes.byref(opt), ctypes.byref(o), _stream(stream)))

@@ -81,3 +81,24 @@ def test_product_package_does_not_import_oracle():
             if f.endswith(".py"):
                 s = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(import|from)\s+oracle", s, re.M), f
+
+
+def test_binding_checks_caller_outputs():
+    """Caller-provided output buffers are validated before the pointer-only C-ABI sees them."""
+    import numpy as np
+    import torch
+
+    from paper_2305_01867_b200 import rsi
+    n = 10
+    with pytest.raises(ValueError):
+        rsi._check_out({"hit": torch.zeros(n - 1, dtype=torch.uint8)}, n, "boolean", "cpu")
+    with pytest.raises(TypeError):
+        rsi._check_out({"count": torch.zeros(n, dtype=torch.int64)}, n, "intercept_count", "cpu")
+    with pytest.raises(ValueError):
+        rsi._check_out({"t": torch.zeros(n)}, n, "barycentric", "cpu")  # tri missing
+    with pytest.raises(ValueError):
+        rsi._check_out({"tri": torch.zeros(n, dtype=torch.int32), "point": torch.zeros(n, 2)}, n, "barycentric", "cpu")
+    rsi._check_out({k: v.cpu() for k, v in rsi.alloc_outputs(n, "barycentric", "cpu").items()}, n, "barycentric", "cpu")
+    with pytest.raises(ValueError):  # host call with a short output array
+        rsi.rsi_test(np.zeros((3, 3), np.float32), np.zeros((1, 3), np.int32), np.zeros((5, 3), np.float32),
+                     np.zeros((5, 3), np.float32), {"mode": "boolean"}, out={"hit": torch.zeros(4, dtype=torch.uint8)})

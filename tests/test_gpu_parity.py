@@ -531,10 +531,14 @@ def test_launch_counter(rsi):
     assert c1 - c0 >= 6
     for mode in ("boolean", "barycentric", "intercept_count"):
         before = rsi.rsi_launch_count()
+        ovf0 = rsi.rsi_get_stats(h)["overflow_rays"]
         rsi.rsi_intersect(h, Sd, Ed, mode)
-        assert rsi.rsi_launch_count() - before == 1, mode
+        # + the 3 re-pass kernels when some segment overflowed the count list
+        extra = 3 if rsi.rsi_get_stats(h)["overflow_rays"] > ovf0 else 0
+        assert rsi.rsi_launch_count() - before == 1 + extra, mode
+    c2 = rsi.rsi_launch_count()
     rsi.rsi_rebuild(h, Vd, Td)
-    assert rsi.rsi_launch_count() - (c1 + 3) == c1 - c0
+    assert rsi.rsi_launch_count() - c2 == c1 - c0
     h.free()
 
 
@@ -680,7 +684,7 @@ def test_apetrei_sort_full_low_words(rsi):
 
 @pytest.mark.parametrize("n_sheets", [40, 100, 256, 300])
 def test_overflow_warp_dedup(rsi, n_sheets):
-    """Rays crossing up to 300 stacked sheets overflow the 8-entry register list:
+    """Rays crossing up to 300 stacked sheets overflow the 4-entry hit list:
     the re-pass collects every hit's fp64 t and one warp per ray sorts them with
     a shuffle bitonic network and counts gaps by ballot (> 256 hits: serial heap
     sort).  Sheets come in groups whose members are 1e-7 apart in z (merged by

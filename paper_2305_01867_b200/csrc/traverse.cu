@@ -1240,6 +1240,44 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
 }
 
 // ---------------------------------------------------------------- exact re-pass for overflowed rays
+// One-traversal re-pass: each overflowed segment's exact fp64 hit t values go
+// into a fixed kOvfSlot-entry slot of a pool sized from the overflow count;
+// segments with more hits than that are listed for the two-pass path below
+// (size, then collect into an exactly-sized pool).  mt32 only drops certain
+// misses; every possible hit is settled (and its t taken) in the fp64 mirror.
+constexpr int kOvfSlot = 64;
+
+__global__ void __launch_bounds__(kThreads) k_ovf_collect_fixed(const float4* __restrict__ nodes,
+                                                                const float4* __restrict__ tris,
+                                                                const float* __restrict__ S, const float* __restrict__ E,
+                                                                const int32_t* __restrict__ list, int n_ovf,
+                                                                int32_t* __restrict__ seg, double* __restrict__ pool,
+                                                                int32_t* __restrict__ big, uint32_t* scratch) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n_ovf) return;
+    Ray r;
+    bool nonfinite;
+    load_ray(r, S, E, list[j], nonfinite);
+    double* v = pool + (size_t)j * kOvfSlot;
+    int nh = 0;
+    float tclip = 1.0f;
+    traverse(nodes, (int)scratch[SCR_ROOT_NODE], r, tclip, [&](int k) {
+        float4 A, B, C;
+        load_tri(tris, k, A, B, C);
+        float t32, et;
+        if (mt32(r, A, B, C, t32, et) == MT_MISS) return false;
+        double t64;
+        if (mt64(r, A, B, C, &t64)) {
+            if (nh < kOvfSlot) v[nh] = t64;
+            ++nh;
+        }
+        return false;
+    });
+    seg[2 * j] = j * kOvfSlot;
+    seg[2 * j + 1] = nh <= kOvfSlot ? nh : -1;  // -1: the two-pass path recounts it
+    if (nh > kOvfSlot) big[atomicAdd(&scratch[SCR_OVF_TOTAL], 1u)] = list[j];
+}
+
 // Pass A: raw hit count per overflowed ray and its segment offset in a pool.
 __global__ void __launch_bounds__(kThreads) k_ovf_size(const float4* __restrict__ nodes,
                                                        const float4* __restrict__ tris, const float* __restrict__ S,
@@ -1344,6 +1382,7 @@ __global__ void __launch_bounds__(kThreads) k_ovf_dedup(const int32_t* __restric
     if (j >= n_ovf) return;
     double* v = pool + seg[2 * j];
     const int nh = seg[2 * j + 1];
+    if (nh < 0) return;  // more hits than the slot: counted by the two-pass path
     int cnt = nh > 0 ? 1 : 0;
     if (nh > 32 * kOvfRegs) {  // rare: serial sort in lane 0
         if (lane == 0) {
@@ -1538,6 +1577,9 @@ static void launch_mode(int32_t mode, const TraceParams& p, cudaStream_t s) {
         launch_trace<MODE_COUNT, kFP64, kCounters>(p, s);
 }
 
+static rsi_status_t rsi_exact_repass(rsi_bvh* h, const float* S, const float* E, const int32_t* big, int n_big,
+                                     const rsi_outputs_t* out, cudaStream_t s);
+
 rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, int64_t n, int32_t mode,
                                   const rsi_outputs_t* out, cudaStream_t s) {
     if (n == 0) return RSI_OK;
@@ -1597,32 +1639,76 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     if (st != RSI_OK) return st;
     const int n_ovf = (int)h->h_words[0];
     if (n_ovf == 0) return RSI_OK;
+    // one traversal per overflowed segment into a fixed-slot pool (at most
+    // 2^20 segments at a time, 512 MB), warp-per-segment dedup
+    if (n_ovf > (1 << 20)) {
+        h->host_overflow += (uint64_t)n_ovf;
+        return rsi_exact_repass(h, S, E, h->ovf_list, n_ovf, out, s);
+    }
     int32_t* seg = nullptr;
     double* pool = nullptr;
+    int32_t* big = nullptr;
     st = rsi_cuda_check(cudaMallocAsync((void**)&seg, (size_t)n_ovf * 2 * sizeof(int32_t), s), "overflow segs");
-    if (st != RSI_OK) return RSI_E_OOM;
-    const int nb = rsi_ceil_div(n_ovf, kThreads);
-    rsi_note_launch(), k_ovf_size<<<nb, kThreads, 0, s>>>(h->nodes, h->tris, S, E, h->ovf_list, n_ovf, seg, h->scratch);
-    cudaMemcpyAsync(h->h_words, h->scratch + SCR_OVF_TOTAL, sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
-    st = rsi_cuda_check(cudaStreamSynchronize(s), "overflow sizing");
+    if (st == RSI_OK)
+        st = rsi_cuda_check(cudaMallocAsync((void**)&pool, (size_t)n_ovf * kOvfSlot * sizeof(double), s), "overflow pool");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaMallocAsync((void**)&big, (size_t)n_ovf * sizeof(int32_t), s), "overflow list");
+    auto release = [&]() {
+        if (seg) cudaFreeAsync(seg, s);
+        if (pool) cudaFreeAsync(pool, s);
+        if (big) cudaFreeAsync(big, s);
+    };
     if (st != RSI_OK) {
-        cudaFreeAsync(seg, s);
-        return st;
-    }
-    const size_t total = h->h_words[0];
-    st = rsi_cuda_check(cudaMallocAsync((void**)&pool, (total ? total : 1) * sizeof(double), s), "overflow pool");
-    if (st != RSI_OK) {
-        cudaFreeAsync(seg, s);
+        release();
         return RSI_E_OOM;
     }
-    rsi_note_launch(), k_ovf_collect<<<nb, kThreads, 0, s>>>(h->nodes, h->tris, S, E, h->ovf_list, n_ovf, seg, pool,
-                                                             h->scratch);
+    const int nb = rsi_ceil_div(n_ovf, kThreads);
+    rsi_note_launch(), k_ovf_collect_fixed<<<nb, kThreads, 0, s>>>(h->nodes, h->tris, S, E, h->ovf_list, n_ovf, seg,
+                                                                   pool, big, h->scratch);
     rsi_note_launch(), k_ovf_dedup<<<rsi_ceil_div((int64_t)n_ovf * 32, kThreads), kThreads, 0, s>>>(
         h->ovf_list, n_ovf, seg, pool, h->opt.dedup_tau, out->count);
-    st = rsi_cuda_check(cudaGetLastError(), "overflow pass");
-    cudaFreeAsync(pool, s);
-    cudaFreeAsync(seg, s);
+    st = rsi_cuda_check(cudaMemcpyAsync(h->h_words, h->scratch + SCR_OVF_TOTAL, sizeof(uint32_t),
+                                        cudaMemcpyDeviceToHost, s), "overflow count");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaStreamSynchronize(s), "overflow pass");
     h->host_overflow += (uint64_t)n_ovf;
+    const int n_big = st == RSI_OK ? (int)h->h_words[0] : 0;
+    if (st != RSI_OK || n_big == 0) {
+        release();
+        return st;
+    }
+    // rare: segments with more than kOvfSlot hits -- size, then collect exactly
+    st = rsi_exact_repass(h, S, E, big, n_big, out, s);
+    release();
+    return st;
+}
+
+// Exact two-pass re-pass for a list of segments: raw hit counts (one atomic
+// per segment sizes an exact pool), the fp64 t of every hit, warp dedup.
+static rsi_status_t rsi_exact_repass(rsi_bvh* h, const float* S, const float* E, const int32_t* big, int n_big,
+                                     const rsi_outputs_t* out, cudaStream_t s) {
+    rsi_status_t st = rsi_cuda_check(cudaMemsetAsync(h->scratch + SCR_OVF_TOTAL, 0, sizeof(uint32_t), s), "memset");
+    int32_t* seg2 = nullptr;
+    double* pool2 = nullptr;
+    if (st == RSI_OK)
+        st = rsi_cuda_check(cudaMallocAsync((void**)&seg2, (size_t)n_big * 2 * sizeof(int32_t), s), "overflow segs");
+    const int nb2 = rsi_ceil_div(n_big, kThreads);
+    if (st == RSI_OK) {
+        rsi_note_launch(), k_ovf_size<<<nb2, kThreads, 0, s>>>(h->nodes, h->tris, S, E, big, n_big, seg2, h->scratch);
+        st = rsi_cuda_check(cudaMemcpyAsync(h->h_words, h->scratch + SCR_OVF_TOTAL, sizeof(uint32_t),
+                                            cudaMemcpyDeviceToHost, s), "overflow total");
+    }
+    if (st == RSI_OK) st = rsi_cuda_check(cudaStreamSynchronize(s), "overflow sizing");
+    const size_t total = st == RSI_OK ? h->h_words[0] : 0;
+    if (st == RSI_OK)
+        st = rsi_cuda_check(cudaMallocAsync((void**)&pool2, (total ? total : 1) * sizeof(double), s), "overflow pool");
+    if (st == RSI_OK) {
+        rsi_note_launch(), k_ovf_collect<<<nb2, kThreads, 0, s>>>(h->nodes, h->tris, S, E, big, n_big, seg2, pool2,
+                                                                  h->scratch);
+        rsi_note_launch(), k_ovf_dedup<<<rsi_ceil_div((int64_t)n_big * 32, kThreads), kThreads, 0, s>>>(
+            big, n_big, seg2, pool2, h->opt.dedup_tau, out->count);
+        st = rsi_cuda_check(cudaGetLastError(), "overflow pass");
+    }
+    if (seg2) cudaFreeAsync(seg2, s);
+    if (pool2) cudaFreeAsync(pool2, s);
     return st;
 }
 

@@ -533,9 +533,13 @@ def test_launch_counter(rsi):
         before = rsi.rsi_launch_count()
         ovf0 = rsi.rsi_get_stats(h)["overflow_rays"]
         rsi.rsi_intersect(h, Sd, Ed, mode)
-        # + the 3 re-pass kernels when some segment overflowed the count list
-        extra = 3 if rsi.rsi_get_stats(h)["overflow_rays"] > ovf0 else 0
-        assert rsi.rsi_launch_count() - before == 1 + extra, mode
+        # + the re-pass kernels when some segment overflowed the count list
+        # (one-traversal pass + dedup; + size / collect / dedup beyond 64 hits)
+        launched = rsi.rsi_launch_count() - before
+        if rsi.rsi_get_stats(h)["overflow_rays"] > ovf0:
+            assert launched in (3, 6), (mode, launched)
+        else:
+            assert launched == 1, (mode, launched)
     c2 = rsi.rsi_launch_count()
     rsi.rsi_rebuild(h, Vd, Td)
     assert rsi.rsi_launch_count() - c2 == c1 - c0

@@ -1240,6 +1240,61 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
 }
 
 // ---------------------------------------------------------------- exact re-pass for overflowed rays
+// Single-thread walk over the 4-wide records (the re-pass's all-hits walk:
+// half the dependent fetches of the binary walk for the long, grazing segments
+// that overflow).  Same conservative decode as k_trace's visit; leaf(slot) is
+// called for every leaf whose box the segment enters.
+template <class LeafFn>
+__device__ __forceinline__ void traverse_quads(const float4* __restrict__ quads, int root, const Ray& r,
+                                               uint32_t magic, LeafFn&& leaf) {
+    int stack[kStackQuad];
+    int sp = 0;
+    int node = root;
+    if (node < 0) return;
+    const float inv3[3] = {r.ix, r.iy, r.iz};
+    const uint32_t msk[3] = {r.mx, r.my, r.mz};
+    const float nof[3] = {r.lx, r.ly, r.lz};
+    const float fof[3] = {r.hx, r.hy, r.hz};
+    while (true) {
+        const float4* q = quads + 4 * node;
+        float4 qa, qb, qc, qd;
+        ldg256(q, qa, qb);
+        ldg256(q + 2, qc, qd);
+        const float pp[3] = {qa.x, qa.y, qa.z};
+        const uint32_t wq[6] = {__float_as_uint(qb.x), __float_as_uint(qb.y), __float_as_uint(qb.z),
+                                __float_as_uint(qb.w), __float_as_uint(qc.x), __float_as_uint(qc.y)};
+        const float scv[3] = {qa.w, qd.z, qd.w};
+        float sa[3], bn[3], bf[3];
+        uint32_t wn[3], wf[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            sa[a] = scv[a] * inv3[a];
+            bn[a] = fmaf(pp[a], inv3[a], -nof[a]);
+            bf[a] = fmaf(pp[a], inv3[a], -fof[a]);
+            wn[a] = (wq[2 * a] & ~msk[a]) | (wq[2 * a + 1] & msk[a]);
+            wf[a] = (wq[2 * a + 1] & ~msk[a]) | (wq[2 * a] & msk[a]);
+        }
+        const int ref[4] = {__float_as_int(qc.z), __float_as_int(qc.w), __float_as_int(qd.x), __float_as_int(qd.y)};
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float tn = fmaxf(fmaxf(fmaf(byte_to_2p15(wn[0], j, magic), sa[0], bn[0]),
+                                         fmaf(byte_to_2p15(wn[1], j, magic), sa[1], bn[1])),
+                                   fmaxf(fmaf(byte_to_2p15(wn[2], j, magic), sa[2], bn[2]), 0.0f));
+            const float tf = fminf(fminf(fmaf(byte_to_2p15(wf[0], j, magic), sa[0], bf[0]),
+                                         fmaf(byte_to_2p15(wf[1], j, magic), sa[1], bf[1])),
+                                   fminf(fmaf(byte_to_2p15(wf[2], j, magic), sa[2], bf[2]), 1.0f));
+            if (tn <= tf && ref[j] != kNoRef) {  // (a missing child has an empty box anyway)
+                if (ref[j] < 0)
+                    leaf(~ref[j]);
+                else
+                    stack[sp++] = ref[j];
+            }
+        }
+        if (sp == 0) return;
+        node = stack[--sp];
+    }
+}
+
 // One-traversal re-pass: each overflowed segment's exact fp64 hit t values go
 // into a fixed kOvfSlot-entry slot of a pool sized from the overflow count;
 // segments with more hits than that are listed for the two-pass path below
@@ -1248,31 +1303,45 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
 constexpr int kOvfSlot = 64;
 
 __global__ void __launch_bounds__(kThreads) k_ovf_collect_fixed(const float4* __restrict__ nodes,
+                                                                const float4* __restrict__ quads,
                                                                 const float4* __restrict__ tris,
                                                                 const float* __restrict__ S, const float* __restrict__ E,
                                                                 const int32_t* __restrict__ list, int n_ovf,
                                                                 int32_t* __restrict__ seg, double* __restrict__ pool,
-                                                                int32_t* __restrict__ big, uint32_t* scratch) {
+                                                                int32_t* __restrict__ big, uint32_t* scratch,
+                                                                uint32_t magic) {
     int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n_ovf) return;
+    // the 4-wide decode's slack terms and safe |1/d| range, as in k_trace
+    const float pmax = __uint_as_float(scratch[SCR_QPMAX]);
+    const int emin = (int)scratch[SCR_QEMIN] - 128, emax = (int)scratch[SCR_QEMAX] - 128;
     Ray r;
     bool nonfinite;
-    load_ray(r, S, E, list[j], nonfinite);
+    load_ray<true>(r, S, E, list[j], nonfinite, 0.25f * pmax, scalbnf(1.0f, -124 - emin),
+                   scalbnf(1.0f, 100) / (pmax + scalbnf(65536.0f, emax)));
     double* v = pool + (size_t)j * kOvfSlot;
     int nh = 0;
-    float tclip = 1.0f;
-    traverse(nodes, (int)scratch[SCR_ROOT_NODE], r, tclip, [&](int k) {
+    auto hit = [&](int k) {
         float4 A, B, C;
         load_tri(tris, k, A, B, C);
         float t32, et;
-        if (mt32(r, A, B, C, t32, et) == MT_MISS) return false;
+        if (mt32(r, A, B, C, t32, et) == MT_MISS) return;
         double t64;
         if (mt64(r, A, B, C, &t64)) {
             if (nh < kOvfSlot) v[nh] = t64;
             ++nh;
         }
-        return false;
-    });
+    };
+    if (RSI_ANY_QUAD) {
+        traverse_quads(quads, (int)scratch[SCR_ROOT_NODE], r, magic, hit);
+    } else {  // no 4-wide records in this build: the binary walk (plain slab offsets)
+        load_ray(r, S, E, list[j], nonfinite);
+        float tclip = 1.0f;
+        traverse(nodes, (int)scratch[SCR_ROOT_NODE], r, tclip, [&](int k) {
+            hit(k);
+            return false;
+        });
+    }
     seg[2 * j] = j * kOvfSlot;
     seg[2 * j + 1] = nh <= kOvfSlot ? nh : -1;  // -1: the two-pass path recounts it
     if (nh > kOvfSlot) big[atomicAdd(&scratch[SCR_OVF_TOTAL], 1u)] = list[j];
@@ -1662,8 +1731,8 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
         return RSI_E_OOM;
     }
     const int nb = rsi_ceil_div(n_ovf, kThreads);
-    rsi_note_launch(), k_ovf_collect_fixed<<<nb, kThreads, 0, s>>>(h->nodes, h->tris, S, E, h->ovf_list, n_ovf, seg,
-                                                                   pool, big, h->scratch);
+    rsi_note_launch(), k_ovf_collect_fixed<<<nb, kThreads, 0, s>>>(h->nodes, h->quads, h->tris, S, E, h->ovf_list, n_ovf, seg,
+                                                                   pool, big, h->scratch, 0x47000000u);
     rsi_note_launch(), k_ovf_dedup<<<rsi_ceil_div((int64_t)n_ovf * 32, kThreads), kThreads, 0, s>>>(
         h->ovf_list, n_ovf, seg, pool, h->opt.dedup_tau, out->count);
     st = rsi_cuda_check(cudaMemcpyAsync(h->h_words, h->scratch + SCR_OVF_TOTAL, sizeof(uint32_t),

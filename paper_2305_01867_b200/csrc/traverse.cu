@@ -1295,13 +1295,142 @@ __device__ __forceinline__ void traverse_quads(const float4* __restrict__ quads,
     }
 }
 
+// Warp-cooperative all-hits walk of ONE segment (the re-pass): the lanes share
+// a stack in shared memory and each iteration pops up to 32 records at once,
+// so the long grazing segments that overflow are walked 32 nodes at a time
+// instead of one.  Every hit's fp64 t goes to the segment's slot (any order:
+// the dedup sorts); a full slot or stack marks the segment for the exact
+// two-pass path (correct regardless).
+constexpr int kOvfSlot = 64;   // fp64 hit t values held per overflowed segment
+constexpr int kWStack = 2048;  // stack entries per warp (8 KB)
+constexpr int kOvfWarps = 4;   // warps per block
+
+__global__ void __launch_bounds__(32 * kOvfWarps) k_ovf_collect_warp(
+    const float4* __restrict__ quads, const float4* __restrict__ tris, const float* __restrict__ S,
+    const float* __restrict__ E, const int32_t* __restrict__ list, int n_ovf, int32_t* __restrict__ seg,
+    double* __restrict__ pool, int32_t* __restrict__ big, uint32_t* scratch, uint32_t magic) {
+    __shared__ int s_stack[kOvfWarps][kWStack];
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int j = blockIdx.x * kOvfWarps + w;  // warp-uniform
+    if (j >= n_ovf) return;
+    const float pmax = __uint_as_float(scratch[SCR_QPMAX]);
+    const int emin = (int)scratch[SCR_QEMIN] - 128, emax = (int)scratch[SCR_QEMAX] - 128;
+    Ray r;
+    bool nonfinite;
+    load_ray<true>(r, S, E, list[j], nonfinite, 0.25f * pmax, scalbnf(1.0f, -124 - emin),
+                   scalbnf(1.0f, 100) / (pmax + scalbnf(65536.0f, emax)));
+    double* v = pool + (size_t)j * kOvfSlot;
+    int* stk = s_stack[w];
+    const int root = (int)scratch[SCR_ROOT_NODE];
+    int top = 0;        // warp-uniform
+    int nh = 0;         // warp-uniform hit count
+    bool spill = false; // warp-uniform: slot or stack exhausted
+    if (root >= 0) {
+        if (lane == 0) stk[0] = root;
+        top = 1;
+    }
+    __syncwarp();
+    const float inv3[3] = {r.ix, r.iy, r.iz};
+    const uint32_t msk[3] = {r.mx, r.my, r.mz};
+    const float nof[3] = {r.lx, r.ly, r.lz};
+    const float fof[3] = {r.hx, r.hy, r.hz};
+    while (top > 0 && !spill) {
+        const int take = top < 32 ? top : 32;
+        const int node = lane < take ? stk[top - 1 - lane] : -1;
+        top -= take;
+        __syncwarp();
+        int push[4] = {kNoRef, kNoRef, kNoRef, kNoRef};
+        int leafs[4] = {kNoRef, kNoRef, kNoRef, kNoRef};
+        if (node >= 0) {
+            const float4* q = quads + 4 * node;
+            float4 qa, qb, qc, qd;
+            ldg256(q, qa, qb);
+            ldg256(q + 2, qc, qd);
+            const float pp[3] = {qa.x, qa.y, qa.z};
+            const uint32_t wq[6] = {__float_as_uint(qb.x), __float_as_uint(qb.y), __float_as_uint(qb.z),
+                                    __float_as_uint(qb.w), __float_as_uint(qc.x), __float_as_uint(qc.y)};
+            const float scv[3] = {qa.w, qd.z, qd.w};
+            float sa[3], bn[3], bf[3];
+            uint32_t wn[3], wf[3];
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                sa[a] = scv[a] * inv3[a];
+                bn[a] = fmaf(pp[a], inv3[a], -nof[a]);
+                bf[a] = fmaf(pp[a], inv3[a], -fof[a]);
+                wn[a] = (wq[2 * a] & ~msk[a]) | (wq[2 * a + 1] & msk[a]);
+                wf[a] = (wq[2 * a + 1] & ~msk[a]) | (wq[2 * a] & msk[a]);
+            }
+            const int ref[4] = {__float_as_int(qc.z), __float_as_int(qc.w), __float_as_int(qd.x),
+                                __float_as_int(qd.y)};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float tn = fmaxf(fmaxf(fmaf(byte_to_2p15(wn[0], c, magic), sa[0], bn[0]),
+                                             fmaf(byte_to_2p15(wn[1], c, magic), sa[1], bn[1])),
+                                       fmaxf(fmaf(byte_to_2p15(wn[2], c, magic), sa[2], bn[2]), 0.0f));
+                const float tf = fminf(fminf(fmaf(byte_to_2p15(wf[0], c, magic), sa[0], bf[0]),
+                                             fmaf(byte_to_2p15(wf[1], c, magic), sa[1], bf[1])),
+                                       fminf(fmaf(byte_to_2p15(wf[2], c, magic), sa[2], bf[2]), 1.0f));
+                if (tn <= tf && ref[c] != kNoRef) {
+                    if (ref[c] < 0)
+                        leafs[c] = ~ref[c];
+                    else
+                        push[c] = ref[c];
+                }
+            }
+        }
+        // leaves: exact hit test, fp64 t into the slot (warp-aggregated index)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            bool hit = false;
+            double t64 = 0.0;
+            if (leafs[c] != kNoRef) {
+                float4 A, B, C;
+                load_tri(tris, leafs[c], A, B, C);
+                float t32, et;
+                if (mt32(r, A, B, C, t32, et) != MT_MISS) hit = mt64(r, A, B, C, &t64) != 0;
+            }
+            const unsigned hm = __ballot_sync(FULL, hit);
+            if (hit) {
+                const int idx = nh + __popc(hm & ((1u << lane) - 1u));
+                if (idx < kOvfSlot) v[idx] = t64;
+            }
+            nh += __popc(hm);
+        }
+        // pushes: warp prefix sum of each lane's internal children
+        int np = 0;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) np += push[c] != kNoRef;
+        int incl = np;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const int total = __shfl_sync(FULL, incl, 31);
+        if (top + total > kWStack) {
+            spill = true;
+        } else {
+            int pos = top + incl - np;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                if (push[c] != kNoRef) stk[pos++] = push[c];
+            top += total;
+        }
+        if (nh > kOvfSlot) spill = true;
+        __syncwarp();
+    }
+    if (lane == 0) {
+        seg[2 * j] = j * kOvfSlot;
+        seg[2 * j + 1] = spill ? -1 : nh;  // -1: the two-pass path recounts it
+        if (spill) big[atomicAdd(&scratch[SCR_OVF_TOTAL], 1u)] = list[j];
+    }
+}
+
 // One-traversal re-pass: each overflowed segment's exact fp64 hit t values go
 // into a fixed kOvfSlot-entry slot of a pool sized from the overflow count;
 // segments with more hits than that are listed for the two-pass path below
 // (size, then collect into an exactly-sized pool).  mt32 only drops certain
 // misses; every possible hit is settled (and its t taken) in the fp64 mirror.
-constexpr int kOvfSlot = 64;
-
 __global__ void __launch_bounds__(kThreads) k_ovf_collect_fixed(const float4* __restrict__ nodes,
                                                                 const float4* __restrict__ quads,
                                                                 const float4* __restrict__ tris,
@@ -1731,8 +1860,12 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
         return RSI_E_OOM;
     }
     const int nb = rsi_ceil_div(n_ovf, kThreads);
-    rsi_note_launch(), k_ovf_collect_fixed<<<nb, kThreads, 0, s>>>(h->nodes, h->quads, h->tris, S, E, h->ovf_list, n_ovf, seg,
-                                                                   pool, big, h->scratch, 0x47000000u);
+    if (RSI_ANY_QUAD)  // one warp per overflowed segment over the 4-wide records
+        rsi_note_launch(), k_ovf_collect_warp<<<rsi_ceil_div(n_ovf, kOvfWarps), 32 * kOvfWarps, 0, s>>>(
+            h->quads, h->tris, S, E, h->ovf_list, n_ovf, seg, pool, big, h->scratch, 0x47000000u);
+    else
+        rsi_note_launch(), k_ovf_collect_fixed<<<nb, kThreads, 0, s>>>(h->nodes, h->quads, h->tris, S, E, h->ovf_list,
+                                                                       n_ovf, seg, pool, big, h->scratch, 0x47000000u);
     rsi_note_launch(), k_ovf_dedup<<<rsi_ceil_div((int64_t)n_ovf * 32, kThreads), kThreads, 0, s>>>(
         h->ovf_list, n_ovf, seg, pool, h->opt.dedup_tau, out->count);
     st = rsi_cuda_check(cudaMemcpyAsync(h->h_words, h->scratch + SCR_OVF_TOTAL, sizeof(uint32_t),

@@ -70,21 +70,6 @@ constexpr bool kQuadCount = RSI_COUNT_QUAD;
 #ifndef RSI_BF_SMEM
 #define RSI_BF_SMEM 0
 #endif
-#ifndef RSI_BF_PRED
-#define RSI_BF_PRED 0
-#endif
-// latency hiding by prefetch (no register cost): the warp's next ray chunk into
-// L2 one chunk ahead, a pending leaf's triangle into L1 when it is found, a
-// pushed node into L1 when it is pushed
-#ifndef RSI_PF_RAY
-#define RSI_PF_RAY 0
-#endif
-#ifndef RSI_PF_TRI
-#define RSI_PF_TRI 0
-#endif
-#ifndef RSI_PF_PUSH
-#define RSI_PF_PUSH 0
-#endif
 // quad visits per traversal-phase iteration (the warp votes on leaving the
 // phase every kVisits visits): measured per mode on the sphere and
 // paper-terrain workloads -- 3 with min_trav 16 / 12 for boolean / barycentric
@@ -349,8 +334,6 @@ __device__ __forceinline__ void ldg256(const float4* p, float4& a, float4& b) {
 #endif
 }
 
-[[maybe_unused]] __device__ __forceinline__ void prefetch_l1(const void* p) { asm volatile("prefetch.global.L1 [%0];" ::"l"(p)); }
-[[maybe_unused]] __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
 // triangle slot k: 64 B (4 x float4, the last one padding) for two 256-bit loads
 __device__ __forceinline__ void load_tri(const float4* __restrict__ tris, int k, float4& A, float4& B, float4& C) {
@@ -782,17 +765,9 @@ struct BFStack {
         return (kSm > 0 && k < kSm) ? s[k * kT] : local[(unsigned)(k - kSm)];
     }
     __device__ __forceinline__ void push_if(int& sp, bool v, int x) {
-#if RSI_BF_PRED
-        if (v) {  // predicated store: only pushing lanes write (less local-memory traffic)
-            put(sp, top);
-            top = x;
-            ++sp;
-        }
-#else
         put(sp, top);
         top = v ? x : top;
         sp += v ? 1 : 0;
-#endif
     }
     __device__ __forceinline__ void push(int& sp, int x) { push_if(sp, true, x); }
     __device__ __forceinline__ int pop(int& sp) {
@@ -853,8 +828,6 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
     // 32-bit ray indices (rsi_intersect limits n_rays to 2^31 - 1): registers matter
     const int n32 = (int)p.n;
     int cnext = 0, cend = 0;      // warp-uniform chunk [cnext, cend)
-    int64_t pbase = -1;           // warp-uniform: chunk reserved ahead (RSI_PF_RAY)
-    (void)pbase;
     bool exhausted = false;       // warp-uniform
     int ray = -1;
     Ray r;
@@ -910,28 +883,8 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
         while (want && !exhausted) {
             if (cnext >= cend) {
                 unsigned long long base = 0;
-#if RSI_PF_RAY
-                // take the chunk reserved last time (the first time: a fresh one),
-                // reserve the next and prefetch its segments into L2
-                unsigned long long nb = 0;
-                if (lane == 0) {
-                    base = pbase >= 0 ? (unsigned long long)pbase : atomicAdd(p.counter, (unsigned long long)kChunk);
-                    nb = atomicAdd(p.counter, (unsigned long long)kChunk);
-                }
-                base = __shfl_sync(FULL, base, 0);
-                nb = __shfl_sync(FULL, nb, 0);
-                pbase = (int64_t)nb;
-                if ((int64_t)nb < p.n && lane < 16) {
-                    const int64_t ne = min((int64_t)nb + kChunk, p.n);
-                    const float* arr = lane < 8 ? p.S : p.E;
-                    const uintptr_t b0 = reinterpret_cast<uintptr_t>(arr + 3 * (int64_t)nb) & ~(uintptr_t)127;
-                    const uintptr_t a = b0 + 128 * (uintptr_t)(lane & 7);
-                    if (a < reinterpret_cast<uintptr_t>(arr + 3 * ne)) prefetch_l2(reinterpret_cast<const void*>(a));
-                }
-#else
                 if (lane == 0) base = atomicAdd(p.counter, (unsigned long long)kChunk);
                 base = __shfl_sync(FULL, base, 0);
-#endif
                 if ((int64_t)base >= p.n) {
                     exhausted = true;
                     break;
@@ -1063,21 +1016,12 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                     }
                 }
                 // c0 is the nearest hit child (kSort) -- kNoRef only when none hit
-                if (RSI_PF_PUSH) {
-                    auto pf = [&](int c) {
-                        if (c != kNoRef) prefetch_l1(c >= 0 ? (const void*)(p.quads + 4 * c) : (const void*)(p.tris + kTriF4 * ~c));
-                    };
-                    pf(c1);
-                    pf(c2);
-                    pf(c3);
-                }
                 stk.push_if(sp, c3 != kNoRef, c3);
                 stk.push_if(sp, c2 != kNoRef, c2);
                 stk.push_if(sp, c1 != kNoRef, c1);
                 int first = c0;
                 if (first == kNoRef && sp > 0) first = stk.pop(sp);
                 if (first != kNoRef && first < 0) {  // a leaf
-                    if (RSI_PF_TRI) prefetch_l1(p.tris + kTriF4 * ~first);
                     if (l0 < 0) {
                         l0 = ~first;
                         // kQSpec: keep walking from the next stack entry while

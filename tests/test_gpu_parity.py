@@ -731,6 +731,8 @@ def test_rsi_test_sparse_device_compaction(rsi):
     far = S + np.float32(10.0)
     ids0, dist0, tri0, pts0 = rsi.rsi_test(V, T, far[:1000], (E + np.float32(10.0))[:1000], {"mode": "barycentric"})
     assert len(ids0) == len(dist0) == len(tri0) == len(pts0) == 0
+    z = np.zeros((0, 3), np.float32)
+    assert all(len(a) == 0 for a in rsi.rsi_test(V, T, z, z, {"mode": "barycentric"}))
 
 
 def test_pycudarsi_call_shape(rsi):

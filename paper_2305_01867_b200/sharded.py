@@ -98,8 +98,12 @@ class GatherPipeline:
         per = -(-n_total // self.world)
         lo, hi = shard_range(n_total, self.rank, self.world)
         nccl = dist.get_backend(self.group) == "nccl"
-        if self.rank == self.dst and (self.recv[slot] is None or
-                                      any(self.recv[slot][k].shape[0] != per * self.world for k in local)):
+        def fits(buf, t):
+            return (buf is not None and buf.shape[0] == per * self.world and buf.shape[1:] == t.shape[1:]
+                    and buf.dtype == t.dtype)
+
+        if self.rank == self.dst and (self.recv[slot] is None or set(self.recv[slot]) != set(local) or
+                                      not all(fits(self.recv[slot][k], t) for k, t in local.items())):
             self.recv[slot] = {k: torch.empty((per * self.world,) + tuple(t.shape[1:]), dtype=t.dtype,
                                               device=t.device if nccl else torch.device("cpu"))
                                for k, t in local.items()}

@@ -804,3 +804,37 @@ def test_peer_outputs_single_rank(rsi):
     finally:
         if own:
             dist.destroy_process_group()
+
+
+def test_gather_pipeline_nccl_single_rank(rsi):
+    """GatherPipeline on the NCCL backend (world size 1 here: the multi-rank run
+    needs more GPUs): async device-side gathers into reused receive buffers,
+    all three modes, equal to the local outputs."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2305_01867_b200.sharded import FIELDS, GatherPipeline
+    own = not dist.is_initialized()
+    if own:
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(sk.getsockname()[1]))
+        sk.close()
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device(DEV))
+    try:
+        V, T, S, E, _ = synth.workload("sphere", 50_001, seed=9)
+        Vd, Td, Sd, Ed = to_dev(V, T, S, E)
+        h = rsi.rsi_build(Vd, Td)
+        pipe = GatherPipeline(slots=2)
+        for step, mode in enumerate(("boolean", "barycentric", "intercept_count", "barycentric")):
+            out = rsi.rsi_intersect(h, Sd, Ed, mode)
+            got = pipe.start(step % 2, {f: out[f] for f in FIELDS[mode]}, len(S)).wait()
+            torch.cuda.synchronize()
+            for k, v in got.items():
+                a, b = v.cpu(), out[k].cpu()
+                assert torch.equal(a, b) or bool(((a == b) | (torch.isnan(a) & torch.isnan(b))).all()), (mode, k)
+        pipe.drain()
+        h.free()
+    finally:
+        if own:
+            dist.destroy_process_group()

@@ -134,3 +134,49 @@ def test_gloo_world2_pipelined_gather(n_rays):
         assert (got[step]["tri"] == ref["tri"]).all()
         m = ref["tri"] >= 0
         np.testing.assert_allclose(got[step]["point"][m], ref["point"][m], atol=1e-6)
+
+
+def _pipe_modes_worker(rank, world, port, n_rays, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2305_01867_b200.sharded import GatherPipeline
+        pipe = GatherPipeline(slots=2)
+        V, T, S, E, _ = synth.workload("cube", n_rays, seed=21)
+        lo, hi = shard_range(n_rays, rank, world)
+        got = []
+        for step, mode in enumerate(("boolean", "barycentric", "intercept_count", "barycentric", "boolean")):
+            loc = _oracle_fn(*(torch.from_numpy(a) for a in (V, T, S[lo:hi], E[lo:hi])), mode)
+            r = pipe.start(step % 2, loc, n_rays).wait()  # slots change field sets between modes
+            if rank == 0:
+                got.append((mode, {k: v.clone().numpy() for k, v in r.items()}))
+        pipe.drain()
+        if rank == 0:
+            q.put(got)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_pipeline_mode_switch():
+    """A GatherPipeline slot reused by a different mode (other fields) reallocates
+    its receive buffers; every step's gathered outputs equal the oracle's."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pipe_modes_worker, args=(r, 2, port, 777, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = q.get(timeout=240)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    V, T, S, E, _ = synth.workload("cube", 777, seed=21)
+    ref = oracle.run(V, T, S, E, flags=False)
+    for mode, out in got:
+        if mode == "boolean":
+            assert (out["hit"] == ref["hit"]).all()
+        elif mode == "intercept_count":
+            assert (out["count"] == ref["count"]).all()
+        else:
+            assert (out["tri"] == ref["tri"]).all()

@@ -838,3 +838,38 @@ def test_gather_pipeline_nccl_single_rank(rsi):
     finally:
         if own:
             dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4])
+def test_fuzz_degenerate_soups(rsi, seed):
+    """Random triangle soups mixing slivers (aspect ~1e6), zero-area triangles
+    (collinear / repeated vertices), huge and tiny triangles and coordinates at
+    1e4 offsets, against segments that are short, long, axis-aligned, through
+    vertices or of zero length: every mode equals the exhaustive oracle on
+    every ray (with and without RSI_OPT_ROTATE / RSI_OPT_APETREI)."""
+    rng = np.random.default_rng(100 + seed)
+    nt = 3000
+    base = rng.uniform(-1, 1, (nt, 3))
+    kind = rng.integers(0, 5, nt)
+    e1 = rng.normal(size=(nt, 3)) * rng.choice([1e-4, 1e-2, 1.0], nt)[:, None]
+    e2 = rng.normal(size=(nt, 3)) * rng.choice([1e-4, 1e-2, 1.0], nt)[:, None]
+    e2[kind == 1] = e1[kind == 1] * 2.0          # collinear
+    e1[kind == 2] = 0.0                          # repeated vertex
+    e2[kind == 3] = e1[kind == 3] + rng.normal(size=(int((kind == 3).sum()), 3)) * 1e-6  # sliver
+    off = np.float64(1e4 if seed % 2 else 0.0)
+    V = np.stack([base, base + e1, base + e2], 1).reshape(-1, 3) + off
+    V = V.astype(np.float32)
+    T = np.arange(3 * nt, dtype=np.int32).reshape(nt, 3)
+    nr = 6000
+    S = (rng.uniform(-1.5, 1.5, (nr, 3)) + off).astype(np.float32)
+    E = (S + rng.normal(size=(nr, 3)) * rng.choice([0.01, 0.5, 3.0], nr)[:, None]).astype(np.float32)
+    k = nr // 6
+    E[:k] = S[:k]                                               # zero length
+    E[k:2 * k] = S[k:2 * k]
+    E[k:2 * k, 2] += np.float32(2.0)                            # axis-aligned
+    vi = rng.integers(0, len(V), k)
+    S[2 * k:3 * k] = V[vi] - np.float32(0.3)                    # through vertices
+    E[2 * k:3 * k] = V[vi] + np.float32(0.3)
+    ref = oracle.run(V, T, S, E)
+    for opts in (None, rsi.Options(rotate=True), rsi.Options(apetrei=True)):
+        assert_parity(run_all(rsi, V, T, S, E, opts), ref, S, E, f"fuzz{seed} {opts}")

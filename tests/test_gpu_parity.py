@@ -873,3 +873,31 @@ def test_fuzz_degenerate_soups(rsi, seed):
     ref = oracle.run(V, T, S, E)
     for opts in (None, rsi.Options(rotate=True), rsi.Options(apetrei=True)):
         assert_parity(run_all(rsi, V, T, S, E, opts), ref, S, E, f"fuzz{seed} {opts}")
+
+
+def test_dedup_gaps_near_tau(rsi):
+    """intercept_count single-linkage decisions right at the threshold: pairs of
+    sheets whose crossings differ by 0.5 .. 1.5 tau in t (reading R4), where the
+    fp32 path must defer to the fp64 mirror; counts equal the oracle's."""
+    base = np.float32([[-2, -2, 0], [4, -2, 0], [-2, 4, 0]])
+    # the second sheet of each pair is tilted in x: over the rays' footprint
+    # x in [0, 1] the gap to the first runs from 0.5 tau to 1.5 tau
+    tilt = np.array([[0, 0, 1e-6 * (0.5 + v[0])] for v in base])
+    Vs = []
+    z = 0.25
+    rng = np.random.default_rng(5)
+    for k in range(3):
+        Vs.append(base + np.float32([0, 0, z]))
+        Vs.append((base.astype(np.float64) + tilt + [0, 0, z]).astype(np.float32))
+        z += 0.2
+    V = np.vstack(Vs).astype(np.float32)
+    T = np.arange(len(V), dtype=np.int32).reshape(-1, 3)
+    nr = 20_000
+    S = np.column_stack([rng.uniform(0, 1, nr), rng.uniform(0, 1, nr), np.zeros(nr)]).astype(np.float32)
+    E = S.copy()
+    E[:, 2] = np.float32(1.0)
+    E[:, :2] += rng.uniform(-1e-3, 1e-3, (nr, 2)).astype(np.float32)
+    ref = oracle.run(V, T, S, E)
+    got = run_all(rsi, V, T, S, E)
+    assert (got["count"] == ref["count"]).all(), np.nonzero(got["count"] != ref["count"])[0][:10]
+    assert len(np.unique(ref["count"])) > 1 and got["stats"]["fp64_rays"] > 0  # both sides of tau occur

@@ -1043,9 +1043,9 @@ __device__ __forceinline__ void quant_axis(const float* lo, const float* hi, int
         whi |= (uint32_t)qh << (8 * j);
     }
     for (int j = cnt; j < 4; ++j) wlo |= 255u << (8 * j);  // missing child: empty box (lo > hi)
-    p_out = (float)(p - 32768.0 * sc);  // the decode offset p - 2^15 s: exact (|p/s - 2^15| < 2^24)
+    p_out = (float)(p - kQuadBias * sc);  // the decode offset p - M s: exact (|p/s - 2^15| < 2^24)
     e_out = e;
-    ok = ((double)nhi - p <= 255.0 * sc) && fabs(p * isc) < 8388608.0 && (double)p_out == p - 32768.0 * sc;
+    ok = ((double)nhi - p <= 255.0 * sc) && fabs(p * isc) < 8388608.0 && (double)p_out == p - kQuadBias * sc;
 }
 
 __global__ void __launch_bounds__(kBlock) k_quads(const float4* __restrict__ nodes, int n_nodes,

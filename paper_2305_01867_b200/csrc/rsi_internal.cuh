@@ -148,6 +148,16 @@ __host__ __device__ inline float rsi_ord2f(uint32_t u) {
 #endif
 constexpr int kTriF4 = RSI_TRI48 ? 3 : 4;
 
+// 4-wide record decode bias M: a child plane is (M + q) s + pm with pm = p - M s
+// stored.  M = 2^15 (default): M + q is one PRMT into the float 2^15's mantissa;
+// RSI_HALF_DECODE: M = 1024, one PRMT places two bytes into two f16 1024 + q
+// (0x64qq) and HADD2.F32 (FMA pipe) widens each -- half the PRMTs on the ALU pipe
+#ifndef RSI_HALF_DECODE
+#define RSI_HALF_DECODE 1
+#endif
+constexpr double kQuadBias = RSI_HALF_DECODE ? 1024.0 : 32768.0;
+constexpr uint32_t kQuadMagic = RSI_HALF_DECODE ? 0x00000064u : 0x47000000u;
+
 // top-of-tree shared-memory cache (build.cu k_topk, traverse.cu)
 #ifndef RSI_TOPK
 #define RSI_TOPK 0  // measured slower at 1024/2048 on the bench workload (1 CTA/SM)

@@ -779,11 +779,31 @@ struct BFStack {
     }
 };
 
-// 2^15 + byte j of w, as a float (exact): one PRMT with an immediate selector
-// places the byte in mantissa bits 8..15 of `magic` = 0x47000000 (2^15), which
-// the caller holds in a register (kept loop-invariant)
+// M + byte j of w, as a float (exact; M = kQuadBias).  Default: one PRMT with an
+// immediate selector places the byte in mantissa bits 8..15 of `magic` =
+// 0x47000000 (2^15), which the caller holds in a register (kept loop-invariant).
+// RSI_HALF_DECODE: the PRMT builds the f16 0x64qq = 1024 + q, widened exactly.
+__device__ __forceinline__ float half_lo_f32(uint32_t h) {
+    float f;
+    asm("{.reg .b16 a, b; mov.b32 {a, b}, %1; cvt.f32.f16 %0, a;}" : "=f"(f) : "r"(h));
+    return f;
+}
+__device__ __forceinline__ float half_hi_f32(uint32_t h) {
+    float f;
+    asm("{.reg .b16 a, b; mov.b32 {a, b}, %1; cvt.f32.f16 %0, b;}" : "=f"(f) : "r"(h));
+    return f;
+}
 __device__ __forceinline__ float byte_to_2p15(uint32_t w, int j, uint32_t magic) {
     uint32_t r;
+#if RSI_HALF_DECODE
+    switch (j) {
+        case 0: asm("prmt.b32 %0, %1, %2, 0x4440;" : "=r"(r) : "r"(w), "r"(magic)); break;
+        case 1: asm("prmt.b32 %0, %1, %2, 0x4441;" : "=r"(r) : "r"(w), "r"(magic)); break;
+        case 2: asm("prmt.b32 %0, %1, %2, 0x4442;" : "=r"(r) : "r"(w), "r"(magic)); break;
+        default: asm("prmt.b32 %0, %1, %2, 0x4443;" : "=r"(r) : "r"(w), "r"(magic)); break;
+    }
+    return half_lo_f32(r);
+#else
     switch (j) {
         case 0: asm("prmt.b32 %0, %1, %2, 0x7604;" : "=r"(r) : "r"(w), "r"(magic)); break;
         case 1: asm("prmt.b32 %0, %1, %2, 0x7614;" : "=r"(r) : "r"(w), "r"(magic)); break;
@@ -791,6 +811,16 @@ __device__ __forceinline__ float byte_to_2p15(uint32_t w, int j, uint32_t magic)
         default: asm("prmt.b32 %0, %1, %2, 0x7634;" : "=r"(r) : "r"(w), "r"(magic)); break;
     }
     return __uint_as_float(r);
+#endif
+}
+// RSI_HALF_DECODE: bytes 2k, 2k+1 of w as the f16 pair (1024 + q_2k, 1024 + q_2k+1)
+__device__ __forceinline__ uint32_t byte_pair_f16(uint32_t w, int k, uint32_t magic) {
+    uint32_t r;
+    if (k == 0)
+        asm("prmt.b32 %0, %1, %2, 0x4140;" : "=r"(r) : "r"(w), "r"(magic));
+    else
+        asm("prmt.b32 %0, %1, %2, 0x4342;" : "=r"(r) : "r"(w), "r"(magic));
+    return r;
 }
 
 // compare-and-swap of (key, ref) pairs: ascending keys
@@ -851,7 +881,7 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
     // root node: 0 for the Karras numbering, the top split under RSI_OPT_APETREI
     // (-1 when a fault-injected build never reached it: every ray misses)
     const int root = p.n_top > 0 ? (int)kSmemRef : (int)p.scratch[SCR_ROOT_NODE];
-    // 0x4B000000 (float 2^23) from a kernel parameter: an opaque register, so the
+    // kQuadMagic (float 2^15, or the f16 exponent byte) from a kernel parameter: an opaque register, so the
     // quad decode's PRMTs keep their byte selectors as immediates
     const uint32_t magic = p.magic;
     // 4-wide walk: slack term Pmax / 4 and the |inv| range that keeps s * inv an
@@ -984,17 +1014,37 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                 }
                 const int4 q6 = make_int4(__float_as_int(qc.z), __float_as_int(qc.w), __float_as_int(qd.x),
                                           __float_as_int(qd.y));
+#if RSI_HALF_DECODE
+                uint32_t hn[3][2], hf[3][2];
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    hn[a][0] = byte_pair_f16(wn[a], 0, magic);
+                    hn[a][1] = byte_pair_f16(wn[a], 1, magic);
+                    hf[a][0] = byte_pair_f16(wf[a], 0, magic);
+                    hf[a][1] = byte_pair_f16(wf[a], 1, magic);
+                }
+                auto dq = [](const uint32_t (&h)[2], int j) {
+                    return (j & 1) ? half_hi_f32(h[j >> 1]) : half_lo_f32(h[j >> 1]);
+                };
+#define RSI_DQN(a, j) dq(hn[a], j)
+#define RSI_DQF(a, j) dq(hf[a], j)
+#else
+#define RSI_DQN(a, j) byte_to_2p15(wn[a], j, magic)
+#define RSI_DQF(a, j) byte_to_2p15(wf[a], j, magic)
+#endif
                 auto child = [&](int j, float& tn) {
-                    const float nx = fmaf(byte_to_2p15(wn[0], j, magic), sa[0], bn[0]);
-                    const float ny = fmaf(byte_to_2p15(wn[1], j, magic), sa[1], bn[1]);
-                    const float nz = fmaf(byte_to_2p15(wn[2], j, magic), sa[2], bn[2]);
-                    const float fx = fmaf(byte_to_2p15(wf[0], j, magic), sa[0], bf[0]);
-                    const float fy = fmaf(byte_to_2p15(wf[1], j, magic), sa[1], bf[1]);
-                    const float fz = fmaf(byte_to_2p15(wf[2], j, magic), sa[2], bf[2]);
+                    const float nx = fmaf(RSI_DQN(0, j), sa[0], bn[0]);
+                    const float ny = fmaf(RSI_DQN(1, j), sa[1], bn[1]);
+                    const float nz = fmaf(RSI_DQN(2, j), sa[2], bn[2]);
+                    const float fx = fmaf(RSI_DQF(0, j), sa[0], bf[0]);
+                    const float fy = fmaf(RSI_DQF(1, j), sa[1], bf[1]);
+                    const float fz = fmaf(RSI_DQF(2, j), sa[2], bf[2]);
                     tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, 0.0f));
                     const float tf = fminf(fminf(fx, fy), fminf(fz, tclip));
                     return tn <= tf;  // a missing child has an empty box and ref kNoRef
                 };
+#undef RSI_DQN
+#undef RSI_DQF
                 float k0, k1, k2, k3;
                 const bool h0 = child(0, k0), h1 = child(1, k1), h2 = child(2, k2), h3 = child(3, k3);
                 if (kCounters) st.boxes += 4;
@@ -1756,7 +1806,7 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     p.point = out->point;
     p.count = out->count;
     p.tau = h->opt.dedup_tau;
-    p.magic = 0x47000000u;
+    p.magic = kQuadMagic;
     p.ovf_list = h->ovf_list;
     p.scratch = h->scratch;
     p.stats = h->stats;
@@ -1807,10 +1857,10 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     const int nb = rsi_ceil_div(n_ovf, kThreads);
     if (RSI_ANY_QUAD)  // one warp per overflowed segment over the 4-wide records
         rsi_note_launch(), k_ovf_collect_warp<<<rsi_ceil_div(n_ovf, kOvfWarps), 32 * kOvfWarps, 0, s>>>(
-            h->quads, h->tris, S, E, h->ovf_list, n_ovf, seg, pool, big, h->scratch, 0x47000000u);
+            h->quads, h->tris, S, E, h->ovf_list, n_ovf, seg, pool, big, h->scratch, kQuadMagic);
     else
         rsi_note_launch(), k_ovf_collect_fixed<<<nb, kThreads, 0, s>>>(h->nodes, h->quads, h->tris, S, E, h->ovf_list,
-                                                                       n_ovf, seg, pool, big, h->scratch, 0x47000000u);
+                                                                       n_ovf, seg, pool, big, h->scratch, kQuadMagic);
     rsi_note_launch(), k_ovf_dedup<<<rsi_ceil_div((int64_t)n_ovf * 32, kThreads), kThreads, 0, s>>>(
         h->ovf_list, n_ovf, seg, pool, h->opt.dedup_tau, out->count);
     st = rsi_cuda_check(cudaMemcpyAsync(h->h_words, h->scratch + SCR_OVF_TOTAL, sizeof(uint32_t),

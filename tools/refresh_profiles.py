@@ -34,6 +34,14 @@ for block in summ.split("== ")[1:]:
     traffic[m.group(1)] = int((g("DRAM read") + g("DRAM write")) * 1e6)
 json.dump(ncu, open(os.path.join(P, "ncu_traversal.json"), "w"), indent=1)
 json.dump(traffic, open(os.path.join(P, "traffic.json"), "w"), indent=1)
+# the bench line read the previous captures' summaries at run time: point it at these
+bl = json.load(open(os.path.join(P, "bench_r1_1gpu.json")))
+rl, mode = bl.get("roofline") or {}, bl.get("config", {}).get("mode", "boolean")
+if mode in ncu:
+    rl["ncu"] = ncu[mode]
+if mode in traffic:
+    rl["traffic"] = traffic[mode]
+json.dump(bl, open(os.path.join(P, "bench_r1_1gpu.json"), "w"))
 shutil.copy(os.path.join(G, f"launches_{tag}.csv"), os.path.join(P, "r1_launches.csv"))
 open(os.path.join(P, "r1_launches_summary.txt"), "w").write(
     "# Round 1 launch list: ncu --metrics gpu__time_duration.sum --clock-control none, python bench.py --steps 2 "

@@ -823,6 +823,12 @@ __device__ __forceinline__ uint32_t byte_pair_f16(uint32_t w, int k, uint32_t ma
     return r;
 }
 
+#ifndef RSI_BARY_FULLSORT
+#define RSI_BARY_FULLSORT 0  // barycentric: all hit children near-first (0: only the nearest first)
+#endif
+#ifndef RSI_COUNT_FRONT
+#define RSI_COUNT_FRONT 1    // intercept_count: any hit child first by selects instead of the key network
+#endif
 // compare-and-swap of (key, ref) pairs: ascending keys
 __device__ __forceinline__ void cas(float& ka, int& ca, float& kb, int& cb) {
     const bool sw = kb < ka;
@@ -1049,12 +1055,19 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                 const bool h0 = child(0, k0), h1 = child(1, k1), h2 = child(2, k2), h3 = child(3, k3);
                 if (kCounters) st.boxes += 4;
                 int c0 = h0 ? q6.x : kNoRef, c1 = h1 ? q6.y : kNoRef, c2 = h2 ? q6.z : kNoRef, c3 = h3 ? q6.w : kNoRef;
-                if (kSort) {
+                if (MODE == MODE_COUNT && RSI_COUNT_FRONT) {
+                    // counts need no order: bring a hit child to slot 0 (so the walk
+                    // continues without a stack round trip)
+                    bool m0 = c0 == kNoRef;
+                    int t = m0 ? c1 : c0; c1 = m0 ? c0 : c1; c0 = t; m0 = c0 == kNoRef;
+                    t = m0 ? c2 : c0; c2 = m0 ? c0 : c2; c0 = t; m0 = c0 == kNoRef;
+                    t = m0 ? c3 : c0; c3 = m0 ? c0 : c3; c0 = t;
+                } else if (kSort) {
                     k0 = h0 ? k0 : INFINITY;
                     k1 = h1 ? k1 : INFINITY;
                     k2 = h2 ? k2 : INFINITY;
                     k3 = h3 ? k3 : INFINITY;
-                    if (MODE == MODE_BARY) {  // full near-first order (nearest-hit culling)
+                    if (MODE == MODE_BARY && RSI_BARY_FULLSORT) {  // full near-first order (nearest-hit culling)
                         cas(k0, c0, k1, c1);
                         cas(k2, c2, k3, c3);
                         cas(k0, c0, k2, c2);

@@ -994,8 +994,8 @@ __global__ void __launch_bounds__(1024) k_topk(const float4* __restrict__ nodes,
     if (tid == 0) scratch[SCR_NTOP] = (uint32_t)(n_nodes > 1 ? b : 0);
 }
 
-// ------------------------------------------------------------------ 4-wide view (grandchild records)
-// One thread per internal node n: the up-to-4 grandchildren of n (a leaf child
+// ------------------------------------------------------------------ 4-wide view (cut records)
+// One thread per internal node n: the up-to-4 members of n's cut (grandchildren, or the greedy cut under RSI_QUAD_GREEDY; a leaf child
 // stands for itself), their AABBs quantized to 8 bits on a per-axis
 // power-of-two grid anchored at an origin p that is itself a multiple of the
 // grid step s = 2^e:  lo' = p + qlo*s <= lo,  hi' = p + qhi*s >= hi  (exact:
@@ -1052,9 +1052,57 @@ __global__ void __launch_bounds__(kBlock) k_quads(const float4* __restrict__ nod
                                                   float4* __restrict__ quads, uint32_t* scratch) {
     int n = blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= n_nodes) return;
-    float lo[3][4], hi[3][4];
-    int ref[4] = {(int)0x80000000, (int)0x80000000, (int)0x80000000, (int)0x80000000};  // kNoRef: no child
+    // (one spare slot: a greedy expansion appends both children before moving one)
+    float lo[3][5], hi[3][5];
+    int ref[5] = {(int)0x80000000, (int)0x80000000, (int)0x80000000, (int)0x80000000,
+                  (int)0x80000000};  // kNoRef: no child
     int k = 0;
+#if RSI_QUAD_GREEDY
+    // greedy 4-cut: start from n's two children and twice replace the internal
+    // member with the largest surface area (the likeliest to be entered by a
+    // random segment) by its two children (a 2-leaf or leaf-heavy subtree
+    // leaves fewer than 4 members)
+    auto add_pair = [&](int node, int skip_empty) {
+        const float4* nd = nodes + 4 * node;
+        const float4 a0 = nd[0], a1 = nd[1], a2 = nd[2];
+        const int4 a3 = *reinterpret_cast<const int4*>(nd + 3);
+        const float4 cb[2] = {a0, a1};
+        const float cz[2][2] = {{a2.x, a2.y}, {a2.z, a2.w}};
+        const int cr[2] = {a3.x, a3.y};
+        for (int side = 0; side < 2; ++side) {
+            if (skip_empty && cr[side] < 0 && cb[side].x == INFINITY) continue;  // 1-triangle tree
+            lo[0][k] = cb[side].x; hi[0][k] = cb[side].y; lo[1][k] = cb[side].z; hi[1][k] = cb[side].w;
+            lo[2][k] = cz[side][0]; hi[2][k] = cz[side][1];
+            ref[k] = cr[side];
+            ++k;
+        }
+    };
+    add_pair(n, 1);
+    for (int step = 0; step < 2; ++step) {
+        int best = -1;
+        float best_area = -1.0f;
+        for (int j = 0; j < k; ++j) {
+            if (ref[j] < 0) continue;
+            const float ax = hi[0][j] - lo[0][j], ay = hi[1][j] - lo[1][j], az = hi[2][j] - lo[2][j];
+            const float area = ax * ay + ay * az + az * ax;
+            if (area > best_area) {
+                best_area = area;
+                best = j;
+            }
+        }
+        if (best < 0) break;
+        // the expanded member's slot takes its right child, its left goes last
+        const int node = ref[best];
+        const int k0 = k;
+        add_pair(node, 0);  // appends 2 members at k0, k0 + 1
+        for (int a = 0; a < 3; ++a) {
+            lo[a][best] = lo[a][k0 + 1];
+            hi[a][best] = hi[a][k0 + 1];
+        }
+        ref[best] = ref[k0 + 1];
+        k = k0 + 1;
+    }
+#else
     const float4* nd = nodes + 4 * n;
     const float4 n0 = nd[0], n1 = nd[1], n2 = nd[2];
     const int4 n3 = *reinterpret_cast<const int4*>(nd + 3);
@@ -1082,6 +1130,7 @@ __global__ void __launch_bounds__(kBlock) k_quads(const float4* __restrict__ nod
             ++k;
         }
     }
+#endif
     uint32_t w[16];
     float px[3];
     int ex[3];

@@ -7,7 +7,7 @@
 //     n2 = (L.lo.z, L.hi.z, R.lo.z, R.hi.z)
 //     n3 = (ref L, ref R, 0, 0) as int bits; ref >= 0 internal node, < 0 leaf ~slot
 //   quad  (64 B, 4 x float4) -- for every internal node n, its up-to-4
-//         grandchildren (a leaf child stands for itself) with 8-bit quantized
+//         cut members (a leaf child stands for itself) with 8-bit quantized
 //         AABBs on a power-of-two grid (see k_quads in build.cu); traversing
 //         quads visits every other level of the binary tree.
 //   tri   (64 B, 4 x float4) in Morton order: (v0, id bits), (v1, 0), (v2, 0), pad
@@ -59,7 +59,7 @@ struct rsi_bvh {
     int64_t cap_tri = 0;             // allocated capacity (triangles)
     int64_t sort_blocks_cap = 0;
     float4* nodes = nullptr;         // [4 * n_nodes]
-    float4* quads = nullptr;         // [4 * n_nodes] compressed grandchild (4-wide) records
+    float4* quads = nullptr;         // [4 * n_nodes] compressed 4-wide cut records
     float4* top = nullptr;           // [4 * kTopNodes] top-of-tree image (refs >= kSmemRef are image slots)
     int n_top = 0;
     float4* tris = nullptr;          // [4 * n_tri]
@@ -157,6 +157,13 @@ constexpr int kTriF4 = RSI_TRI48 ? 3 : 4;
 #endif
 constexpr double kQuadBias = RSI_HALF_DECODE ? 1024.0 : 32768.0;
 constexpr uint32_t kQuadMagic = RSI_HALF_DECODE ? 0x00000064u : 0x47000000u;
+
+// 4-wide records hold a greedy largest-area 4-cut of each node's subtree
+// (RSI_QUAD_GREEDY) instead of its grandchildren: a member may sit 1 .. 3
+// levels below the node, so the walk's stack bound is 3 entries per level
+#ifndef RSI_QUAD_GREEDY
+#define RSI_QUAD_GREEDY 1
+#endif
 
 // top-of-tree shared-memory cache (build.cu k_topk, traverse.cu)
 #ifndef RSI_TOPK

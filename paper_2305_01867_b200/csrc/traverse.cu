@@ -2,10 +2,10 @@
 // (SURVEY 8(a) rows A8 and A9).
 //
 // One thread per segment, persistent grid.  The default walk visits the
-// 4-wide view of the binary tree (k_quads records: the up-to-4 grandchildren
-// of a node, 8-bit quantized boxes on a power-of-two grid, 64 B); every visit
+// 4-wide view of the binary tree (k_quads records: a greedy 4-cut of each
+// node's subtree, 8-bit quantized boxes on a power-of-two grid, 64 B); every visit
 // slab-tests its children conservatively, orders the hit ones near-first,
-// keeps the next on a branch-free local stack (<= 144 entries: depth <= 95)
+// keeps the next on a branch-free local stack (<= 288 entries: depth <= 95)
 // and queues leaves for a warp-wide Moller-Trumbore phase.  The binary
 // child-pair walk (RSI_*_QUAD=0) remains a build switch and is what the exact
 // intercept_count re-pass uses.
@@ -31,7 +31,7 @@ constexpr float kSlack = 4.76837158203125e-07f;  // 2^-21: slab-test slack facto
 constexpr float kTiny = 1e-30f;                  // absolute floor (underflow)
 constexpr float kOutTol = 4e-6f;                 // max certified |t error| for fp32 outputs
 // Per-mode traversal configuration.  Measured on B200 (round 1, same box A/B):
-// all three modes walk the compressed 4-wide grandchild records (64 B, 8-bit
+// all three modes walk the compressed 4-wide cut records (64 B, 8-bit
 // quantized boxes: half the L1 wavefronts of the binary child-pair walk, which
 // was L1-data-pipe bound at 87 %) with a branch-free lane stack; once the quad
 // visit was cheap, intercept_count also gained (-12 % sphere, -18 % terrain vs
@@ -93,10 +93,11 @@ constexpr int kNoRef = (int)0x80000000;  // "no child" (never a valid ref: ~slot
 // tree depth <= 95: a root-to-leaf path has strictly increasing common-prefix
 // lengths of the index-augmented key (<= 63 code bits under RSI_OPT_APETREI,
 // 30 otherwise, + <= 31 levels of index bits for duplicate codes).  Binary
-// walk: one entry per level; quad walk: <= 48 visits x 3 pushes.  Entries
+// walk: one entry per level; quad walk: <= 48 visits x 3 pushes (grandchild
+// records) or <= 95 x 3 (greedy cuts: a member may be one level down).  Entries
 // beyond the depth a ray reaches are never touched (no traffic).
 constexpr int kStackBinary = 96;
-constexpr int kStackQuad = 144;
+constexpr int kStackQuad = RSI_QUAD_GREEDY ? 288 : 144;
 // intercept_count hits held per ray before the exact re-pass: 4 (measured: a
 // 6 KB instead of 12 KB shared-memory list per CTA and a shorter certification
 // loop; with 7 CTAs per SM -8 % sphere, -16 % folded terrain vs 8 at 6 CTAs;
@@ -960,7 +961,7 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
 
         if constexpr (kQuad) {
         // ---- 2. traversal phase (4-wide view: a visit tests the up-to-4
-        // grandchildren of a binary node; hit children are ordered near-first
+        // cut members of a binary node; a hit child goes first
         // (kSort) or by slot, the first becomes the next visit and the rest go
         // on the stack; a leaf (ref < 0) becomes the lane's pending leaf)
         while (true) {

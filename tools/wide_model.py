@@ -78,6 +78,39 @@ def n_desc(n, L):  # boxes a 2^L-wide record of node n holds
     return sum(n_desc(c, L - 1) if c >= 0 else 1 for c in child[n])
 
 
+parent = d["parent"]
+
+
+def area(c):
+    b = box[parent[c] >> 1, parent[c] & 1]
+    e = np.maximum(b[3:6] - b[0:3], 0.0)
+    return e[0] * e[1] + e[1] * e[2] + e[2] * e[0]
+
+
+def greedy_cut(n, k):  # expand the largest-area internal member until k members
+    cut = [int(c) for c in child[n]]
+    while len(cut) < k:
+        inner = [c for c in cut if c >= 0]
+        if not inner:
+            break
+        c = max(inner, key=area)
+        cut.remove(c)
+        cut += [int(x) for x in child[c]]
+    return cut
+
+
+def greedy(k):
+    recs, widths, i = [root], [], 0
+    while i < len(recs):
+        cut = greedy_cut(recs[i], k)
+        widths.append(len(cut))
+        recs += [c for c in cut if c >= 0]
+        i += 1
+    recs, widths = np.array(recs), np.array(widths)
+    vis = reach_count[recs]
+    return vis.sum() / nr, (vis * widths).sum() / nr, widths.mean()
+
+
 print(f"{wl}: N_t={len(T)}, nodes={nn}, max depth={depth.max()}, rays={nr}, leaves entered/ray={leaves_reached:.2f}")
 for L in (1, 2, 3):
     sel = np.nonzero(depth % L == 0)[0]
@@ -85,3 +118,6 @@ for L in (1, 2, 3):
     w = np.array([n_desc(n, L) for n in sel])
     print(f"  {2 ** L}-wide: visits/ray {vis.sum() / nr:7.2f}   child-box tests/ray {(vis * w).sum() / nr:7.2f}   "
           f"mean children/record {w.mean():.2f}")
+for k in (4, 8):
+    v, t, m = greedy(k)
+    print(f"  {k}-wide greedy area cut: visits/ray {v:7.2f}   child-box tests/ray {t:7.2f}   mean children/record {m:.2f}")

@@ -778,6 +778,45 @@ struct BFStack {
         top = get(sp);
         return x;
     }
+    // keyed interface (keys ignored): see BFKStack
+    __device__ __forceinline__ void push_if(int& sp, bool v, int x, float) { push_if(sp, v, x); }
+    __device__ __forceinline__ int pop_live(int& sp, float) { return sp > 0 ? pop(sp) : kNoRef; }
+};
+
+// BFStack whose entries carry the entry distance tn of their box
+// (RSI_BARY_KEYSTACK, barycentric): a pop skips entries with tn > tclip -- the
+// nearest hit found since the push lies before the box, so none of its
+// members can pass their own (tn <= tclip) test.  tn is the conservative
+// slab bound of the quantized member box, <= the entry into the exact box.
+template <int kStack, int kT>
+struct BFKStack {
+    int* s;  // (no shared-memory part)
+    int top;
+    float ktop;
+    int2 local[kStack + 1];
+    __device__ __forceinline__ void push_if(int& sp, bool v, int x, float k) {
+        local[(unsigned)sp] = make_int2(top, __float_as_int(ktop));
+        top = v ? x : top;
+        ktop = v ? k : ktop;
+        sp += v ? 1 : 0;
+    }
+    __device__ __forceinline__ void push(int& sp, int x) { push_if(sp, true, x, -INFINITY); }
+    __device__ __forceinline__ int pop(int& sp) {
+        const int x = top;
+        --sp;
+        const int2 e = local[(unsigned)sp];
+        top = e.x;
+        ktop = __int_as_float(e.y);
+        return x;
+    }
+    __device__ __forceinline__ int pop_live(int& sp, float tclip) {
+        while (sp > 0) {
+            const bool live = ktop <= tclip;
+            const int x = pop(sp);
+            if (live) return x;
+        }
+        return kNoRef;
+    }
 };
 
 // M + byte j of w, as a float (exact; M = kQuadBias).  Default: one PRMT with an
@@ -827,6 +866,9 @@ __device__ __forceinline__ uint32_t byte_pair_f16(uint32_t w, int k, uint32_t ma
 #ifndef RSI_BARY_FULLSORT
 #define RSI_BARY_FULLSORT 0  // barycentric: all hit children near-first (0: only the nearest first)
 #endif
+#ifndef RSI_BARY_KEYSTACK
+#define RSI_BARY_KEYSTACK 0  // barycentric: stack entries carry their entry distance (pop skips tn > tclip)
+#endif
 #ifndef RSI_COUNT_FRONT
 #define RSI_COUNT_FRONT 1    // intercept_count: any hit child first by selects instead of the key network
 #endif
@@ -875,7 +917,9 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
     constexpr bool kQSpec = MODE == MODE_BOOL ? RSI_QSPEC_BOOL : (MODE == MODE_BARY ? RSI_QSPEC_BARY : RSI_QSPEC_COUNT);
     constexpr bool kBF = kQuad;  // branch-free stack on the 4-wide walk (-11 % boolean, -5 % barycentric)
     constexpr int kSmWords = kBF ? RSI_BF_SMEM : kSmemStack;
-    typename std::conditional<kBF, BFStack<kStack, RSI_BF_SMEM, kT>, LaneStack<kStack, kSmemStack, kT>>::type stk;
+    constexpr bool kKeyed = kBF && MODE == MODE_BARY && RSI_BARY_KEYSTACK;
+    typename std::conditional<kKeyed, BFKStack<kStack, kT>,
+        typename std::conditional<kBF, BFStack<kStack, RSI_BF_SMEM, kT>, LaneStack<kStack, kSmemStack, kT>>::type>::type stk;
     __shared__ int s_stack[kSmWords > 0 ? kSmWords * kT : 1];
     stk.s = s_stack + threadIdx.x;
     float tclip = 1.0f;
@@ -1081,17 +1125,23 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                     }
                 }
                 // c0 is the nearest hit child (kSort) -- kNoRef only when none hit
-                stk.push_if(sp, c3 != kNoRef, c3);
-                stk.push_if(sp, c2 != kNoRef, c2);
-                stk.push_if(sp, c1 != kNoRef, c1);
+                if constexpr (kKeyed) {
+                    stk.push_if(sp, c3 != kNoRef, c3, k3);
+                    stk.push_if(sp, c2 != kNoRef, c2, k2);
+                    stk.push_if(sp, c1 != kNoRef, c1, k1);
+                } else {
+                    stk.push_if(sp, c3 != kNoRef, c3);
+                    stk.push_if(sp, c2 != kNoRef, c2);
+                    stk.push_if(sp, c1 != kNoRef, c1);
+                }
                 int first = c0;
-                if (first == kNoRef && sp > 0) first = stk.pop(sp);
+                if (first == kNoRef) first = kKeyed ? stk.pop_live(sp, tclip) : (sp > 0 ? stk.pop(sp) : kNoRef);
                 if (first != kNoRef && first < 0) {  // a leaf
                     if (l0 < 0) {
                         l0 = ~first;
                         // kQSpec: keep walking from the next stack entry while
                         // the warp is still in the traversal phase
-                        first = (kQSpec && sp > 0) ? stk.pop(sp) : kNoRef;
+                        first = !kQSpec ? kNoRef : (kKeyed ? stk.pop_live(sp, tclip) : (sp > 0 ? stk.pop(sp) : kNoRef));
                         if (first != kNoRef && first < 0) {
                             l1 = ~first;
                             first = kNoRef;
@@ -1121,11 +1171,11 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
             bool done = ms.template leaf<kFP64>(p, r, l0, tclip, st);
             if (!done && l1 >= 0) done = ms.template leaf<kFP64>(p, r, l1, tclip, st);
             l0 = l1 = -1;
-            int nxt = (!done && node < 0 && sp > 0) ? stk.pop(sp) : kNoRef;
+            int nxt = (done || node >= 0) ? kNoRef : (kKeyed ? stk.pop_live(sp, tclip) : (sp > 0 ? stk.pop(sp) : kNoRef));
             if (nxt != kNoRef && nxt < 0) {
                 if (kCounters) st.mts += 1;
                 done = ms.template leaf<kFP64>(p, r, ~nxt, tclip, st);
-                nxt = (!done && sp > 0) ? stk.pop(sp) : kNoRef;
+                nxt = done ? kNoRef : (kKeyed ? stk.pop_live(sp, tclip) : (sp > 0 ? stk.pop(sp) : kNoRef));
             }
             if (done) {
                 node = -1;

@@ -87,13 +87,20 @@ def area(c):
     return e[0] * e[1] + e[1] * e[2] + e[2] * e[0]
 
 
-def greedy_cut(n, k):  # expand the largest-area internal member until k members
+nleaf = np.zeros(nn, np.int64)
+for n in order[::-1]:
+    nleaf[n] = sum(nleaf[c] if c >= 0 else 1 for c in child[n])
+KEYS = {"area": area, "leaves": lambda c: nleaf[c], "area*log2(leaves)": lambda c: area(c) * np.log2(nleaf[c] + 1)}
+key = area
+
+
+def greedy_cut(n, k):  # expand the internal member with the largest key until k members
     cut = [int(c) for c in child[n]]
     while len(cut) < k:
         inner = [c for c in cut if c >= 0]
         if not inner:
             break
-        c = max(inner, key=area)
+        c = max(inner, key=key)
         cut.remove(c)
         cut += [int(x) for x in child[c]]
     return cut
@@ -119,5 +126,8 @@ for L in (1, 2, 3):
     print(f"  {2 ** L}-wide: visits/ray {vis.sum() / nr:7.2f}   child-box tests/ray {(vis * w).sum() / nr:7.2f}   "
           f"mean children/record {w.mean():.2f}")
 for k in (4, 8):
-    v, t, m = greedy(k)
-    print(f"  {k}-wide greedy area cut: visits/ray {v:7.2f}   child-box tests/ray {t:7.2f}   mean children/record {m:.2f}")
+    for kname, kf in KEYS.items():
+        key = kf
+        v, t, m = greedy(k)
+        print(f"  {k}-wide greedy cut by {kname}: visits/ray {v:7.2f}   child-box tests/ray {t:7.2f}   "
+              f"mean children/record {m:.2f}")

@@ -866,6 +866,9 @@ __device__ __forceinline__ uint32_t byte_pair_f16(uint32_t w, int k, uint32_t ma
 #ifndef RSI_BARY_FULLSORT
 #define RSI_BARY_FULLSORT 0  // barycentric: all hit children near-first (0: only the nearest first)
 #endif
+#ifndef RSI_BOOL_SAT
+#define RSI_BOOL_SAT 1  // boolean + intercept_count (tclip == 1): planes clamped to [0, 1] in their FFMA, strict box test
+#endif
 #ifndef RSI_BARY_KEYSTACK
 #define RSI_BARY_KEYSTACK 0  // barycentric: stack entries carry their entry distance (pop skips tn > tclip)
 #endif
@@ -1090,9 +1093,20 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                     const float fx = fmaf(RSI_DQF(0, j), sa[0], bf[0]);
                     const float fy = fmaf(RSI_DQF(1, j), sa[1], bf[1]);
                     const float fz = fmaf(RSI_DQF(2, j), sa[2], bf[2]);
-                    tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, 0.0f));
-                    const float tf = fminf(fminf(fx, fy), fminf(fz, tclip));
-                    return tn <= tf;  // a missing child has an empty box and ref kNoRef
+                    if constexpr (MODE != MODE_BARY && RSI_BOOL_SAT) {  // tclip stays 1
+                        // [0, 1] clamp of every plane in its FFMA (.SAT) and a strict
+                        // test: a box the segment truly crosses has computed
+                        // tn < exact entry <= exact exit < computed tf (slack > 0),
+                        // so tn' < tf' after clamping; a box wholly beyond an end
+                        // clamps to tn' = tf' (0 or 1) and fails
+                        tn = fmaxf(fmaxf(__saturatef(nx), __saturatef(ny)), __saturatef(nz));
+                        const float tf = fminf(fminf(__saturatef(fx), __saturatef(fy)), __saturatef(fz));
+                        return tn < tf;
+                    } else {
+                        tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, 0.0f));
+                        const float tf = fminf(fminf(fx, fy), fminf(fz, tclip));
+                        return tn <= tf;  // a missing child has an empty box and ref kNoRef
+                    }
                 };
 #undef RSI_DQN
 #undef RSI_DQF

@@ -869,6 +869,9 @@ __device__ __forceinline__ uint32_t byte_pair_f16(uint32_t w, int k, uint32_t ma
 #ifndef RSI_BOOL_SAT
 #define RSI_BOOL_SAT 1  // boolean + intercept_count (tclip == 1): planes clamped to [0, 1] in their FFMA, strict box test
 #endif
+#ifndef RSI_BARY_SAT
+#define RSI_BARY_SAT 0  // barycentric: clamped planes, strict box test + tn <= tclip
+#endif
 #ifndef RSI_BARY_KEYSTACK
 #define RSI_BARY_KEYSTACK 0  // barycentric: stack entries carry their entry distance (pop skips tn > tclip)
 #endif
@@ -1102,6 +1105,13 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                         tn = fmaxf(fmaxf(__saturatef(nx), __saturatef(ny)), __saturatef(nz));
                         const float tf = fminf(fminf(__saturatef(fx), __saturatef(fy)), __saturatef(fz));
                         return tn < tf;
+                    } else if constexpr (MODE == MODE_BARY && RSI_BARY_SAT) {
+                        // clamped planes as above; the strict test rejects boxes wholly
+                        // beyond an end, the second (<=) keeps boxes entered exactly at
+                        // the current nearest t (ties resolve by triangle id)
+                        tn = fmaxf(fmaxf(__saturatef(nx), __saturatef(ny)), __saturatef(nz));
+                        const float tf = fminf(fminf(__saturatef(fx), __saturatef(fy)), __saturatef(fz));
+                        return tn < tf && tn <= tclip;
                     } else {
                         tn = fmaxf(fmaxf(nx, ny), fmaxf(nz, 0.0f));
                         const float tf = fminf(fminf(fx, fy), fminf(fz, tclip));

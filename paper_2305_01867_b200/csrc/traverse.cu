@@ -57,7 +57,8 @@ constexpr float kOutTol = 4e-6f;                 // max certified |t error| for 
 #define RSI_ANY_QUAD (RSI_BOOL_QUAD || RSI_BARY_QUAD || RSI_COUNT_QUAD)
 constexpr bool kQuadCount = RSI_COUNT_QUAD;
 // speculative walk on the 4-wide records (a lane with a pending leaf keeps
-// walking): measured -2..-4 % barycentric, +3..5 % boolean (round 1)
+// walking): measured -2..-4 % barycentric, +3..5 % boolean with grandchild
+// records; with greedy cuts barycentric +5 % sphere / -1 % terrain: off everywhere
 #ifndef RSI_QSPEC_BOOL
 #define RSI_QSPEC_BOOL 0
 #endif
@@ -65,7 +66,7 @@ constexpr bool kQuadCount = RSI_COUNT_QUAD;
 #define RSI_QSPEC_COUNT 0
 #endif
 #ifndef RSI_QSPEC_BARY
-#define RSI_QSPEC_BARY 1
+#define RSI_QSPEC_BARY 0
 #endif
 #ifndef RSI_BF_SMEM
 #define RSI_BF_SMEM 0

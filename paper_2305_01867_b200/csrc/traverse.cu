@@ -873,6 +873,9 @@ __device__ __forceinline__ uint32_t byte_pair_f16(uint32_t w, int k, uint32_t ma
 #ifndef RSI_BARY_SAT
 #define RSI_BARY_SAT 0  // barycentric: clamped planes, strict box test + tn <= tclip
 #endif
+#ifndef RSI_BOOL_FRONT
+#define RSI_BOOL_FRONT 0  // boolean: any hit child first by selects (no nearest-first order)
+#endif
 #ifndef RSI_BARY_KEYSTACK
 #define RSI_BARY_KEYSTACK 0  // barycentric: stack entries carry their entry distance (pop skips tn > tclip)
 #endif
@@ -1125,7 +1128,7 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                 const bool h0 = child(0, k0), h1 = child(1, k1), h2 = child(2, k2), h3 = child(3, k3);
                 if (kCounters) st.boxes += 4;
                 int c0 = h0 ? q6.x : kNoRef, c1 = h1 ? q6.y : kNoRef, c2 = h2 ? q6.z : kNoRef, c3 = h3 ? q6.w : kNoRef;
-                if (MODE == MODE_COUNT && RSI_COUNT_FRONT) {
+                if ((MODE == MODE_COUNT && RSI_COUNT_FRONT) || (MODE == MODE_BOOL && RSI_BOOL_FRONT)) {
                     // counts need no order: bring a hit child to slot 0 (so the walk
                     // continues without a stack round trip)
                     bool m0 = c0 == kNoRef;

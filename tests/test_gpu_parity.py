@@ -901,3 +901,53 @@ def test_dedup_gaps_near_tau(rsi):
     got = run_all(rsi, V, T, S, E)
     assert (got["count"] == ref["count"]).all(), np.nonzero(got["count"] != ref["count"])[0][:10]
     assert len(np.unique(ref["count"])) > 1 and got["stats"]["fp64_rays"] > 0  # both sides of tau occur
+
+
+def _depth_of_tree(d):
+    """Max root-to-leaf depth of a downloaded tree (binary levels)."""
+    child, root = d["child"], d["root"]
+    depth, best, stack = {root: 0}, 0, [root]
+    while stack:
+        n = stack.pop()
+        for c in child[n]:
+            if c >= 0:
+                depth[c] = depth[n] + 1
+                stack.append(c)
+            else:
+                best = max(best, depth[n] + 1)
+    return best
+
+
+def test_deep_chain_tree_stack_bound(rsi):
+    """A comb of triangles at 2^-i along each axis (i = 1 .. 21) gives Morton codes
+    with (nearly) one bit set each: every split peels one triangle off, so the
+    tree is a chain (depth 39 with the 63-bit codes of RSI_OPT_APETREI).  Segments through
+    the nested boxes near the origin walk the whole chain; with greedy 4-cut
+    records a member may sit one level down, so the lane stack needs 3 entries
+    per level (kStackQuad = 288 >= 3 x 95).  Every mode equals the oracle."""
+    pts = []
+    for ax in range(3):
+        for i in range(1, 22):
+            p = np.zeros(3)
+            p[ax] = 2.0 ** -i
+            pts.append(p)
+    tris = []
+    for p in pts:
+        s = 0.25 * max(p.max(), 2.0 ** -21)
+        tris.append([p + [-s, -s, 0.3 * s], p + [s, -s, -0.3 * s], p + [0, s, 0]])
+    tris.append([[0, 0, 0], [1, 1, 1], [1, 0, 1]])   # scene extent [0, 1]^3
+    V = np.array(tris, np.float64).reshape(-1, 3).astype(np.float32)
+    T = np.arange(len(V), dtype=np.int32).reshape(-1, 3)
+    rng = np.random.default_rng(11)
+    nr = 8000
+    S = rng.uniform(-0.05, 0.05, (nr, 3)).astype(np.float32) * rng.choice([1.0, 1e-3, 1e-5], nr)[:, None].astype(np.float32)
+    E = rng.uniform(0.0, 0.6, (nr, 3)).astype(np.float32) * rng.choice([1.0, 1e-2, 1e-4], nr)[:, None].astype(np.float32)
+    ref = oracle.run(V, T, S, E)
+    assert ref["count"].max() >= 3
+    Vd, Td = to_dev(V, T, S, E)[:2]
+    for opts in (None, rsi.Options(apetrei=True)):
+        h = rsi.rsi_build(Vd, Td, opts)
+        depth = _depth_of_tree(rsi.rsi_bvh_download(h))
+        h.free()
+        assert depth >= (32 if opts is not None else 12), depth  # measured: 39 under RSI_OPT_APETREI
+        assert_parity(run_all(rsi, V, T, S, E, opts), ref, S, E, f"chain {opts} depth {depth}")

@@ -222,10 +222,29 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
     rsi_keep_pool_cached();
 
     // workspace: [mesh V][mesh T][2 ray slots: start, end, outputs]
-    int64_t kChunkRays = (int64_t)1 << 20;
+    // chunk schedule: kChunkRays-segment chunks; with RSI_TEST_TAIL > 0 they
+    // halve down to kTailRays at the end (a shorter un-overlapped tail;
+    // measured neutral, so off by default)
+    int64_t kChunkRays = (int64_t)1 << 20, kTailRays = 0;
     if (const char* e = getenv("RSI_TEST_CHUNK")) kChunkRays = atoll(e) > 0 ? atoll(e) : kChunkRays;  // tuning
-    const int64_t nchunk = (n_rays + kChunkRays - 1) / kChunkRays;
+    if (const char* e = getenv("RSI_TEST_TAIL")) kTailRays = atoll(e) >= 0 ? atoll(e) : kTailRays;    // tuning
+    int64_t n_sched = 0;
+    auto chunk_len = [&](int64_t rem) {
+        if (kTailRays <= 0 || rem <= kTailRays) return rem < kChunkRays ? rem : kChunkRays;
+        int64_t h = rem / 2;
+        h = h > kTailRays ? h : kTailRays;
+        return h < kChunkRays ? h : kChunkRays;
+    };
+    for (int64_t r = 0; r < n_rays; r += chunk_len(n_rays - r)) ++n_sched;
+    const int64_t nchunk = n_sched;
     const int64_t crays = n_rays < kChunkRays ? n_rays : kChunkRays;
+    // chunk c covers [c0(c), c0(c + 1)): recomputed by walking the schedule
+    // (nchunk is tens at most)
+    auto c0 = [&](int64_t c) {
+        int64_t r = 0;
+        for (int64_t k = 0; k < c && r < n_rays; ++k) r += chunk_len(n_rays - r);
+        return r < n_rays ? r : n_rays;
+    };
     const size_t out_b = mode == RSI_MODE_BOOLEAN ? 1 : (mode == RSI_MODE_INTERCEPT_COUNT ? 4 : 24);
     auto up = [](size_t x) { return (x + 255) / 256 * 256; };
     const size_t bv = (size_t)n_vertices * 3 * sizeof(float), bt = (size_t)n_triangles * 3 * sizeof(int32_t);
@@ -271,7 +290,7 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
     }
     auto slot = [&](int64_t c) { return slots + (c & 1) * slot_b; };
     auto h2d = [&](int64_t c) {
-        const int64_t r0 = c * kChunkRays, nr = (n_rays - r0) < kChunkRays ? (n_rays - r0) : kChunkRays;
+        const int64_t r0 = c0(c), nr = c0(c + 1) - r0;
         char* b = slot(c);
         if (c >= 2) st = rsi_cuda_check(cudaStreamWaitEvent(sh, ev[3 * (c - 2) + 1], 0), "wait");
         if (st == RSI_OK)
@@ -303,7 +322,7 @@ rsi_status_t rsi_test(const float* h_vertices, int64_t n_vertices, const int32_t
     for (int64_t c = 0; st == RSI_OK && c < nchunk; ++c) {
         while (st == RSI_OK && issued < nchunk && issued <= c + 1) h2d(issued++);
         if (st != RSI_OK) break;
-        const int64_t r0 = c * kChunkRays, nr = (n_rays - r0) < kChunkRays ? (n_rays - r0) : kChunkRays;
+        const int64_t r0 = c0(c), nr = c0(c + 1) - r0;
         char* b = slot(c);
         char* o = b + 2 * up((size_t)crays * 12);
         st = rsi_cuda_check(cudaStreamWaitEvent(s, ev[3 * c], 0), "wait");

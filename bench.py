@@ -62,12 +62,14 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--rays-per-gpu", type=int, default=10_000_000)
+    # 1.25e7 per GPU: --gpus 8 is exactly the north-star row N_t = 1e4, N_r = 1e8
+    ap.add_argument("--rays-per-gpu", type=int, default=12_500_000)
     ap.add_argument("--workload", default="sphere", choices=["sphere", "terrain", "paper_terrain", "sphere1m"])
     ap.add_argument("--mode", default="boolean", choices=["boolean", "barycentric", "intercept_count"])
     ap.add_argument("--no-extra-modes", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the other BASELINE configs (rank 0, N=1 only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the sphere1m parity sample (rank 0, N=1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample rays (0 = auto ~15 s)")
     ap.add_argument("--fused-gather", action="store_true",
@@ -130,30 +132,66 @@ def workload_inputs(name: str, n: int, rank: int):
 
 
 def cpu_baseline(V, T, S, E, target_s=15.0, sample=0):
-    """The oracle (as it stands) on a bounded sample of the same workload."""
+    """The oracle (as it stands, with its ambiguity flags) on a bounded sample
+    of the same workload.  Returns (cpu_baseline dict, oracle results on the
+    sample) -- the results feed the parity report."""
     import oracle
     cores = oracle.max_threads()
     if sample <= 0:
         # calibrate with a small run, then size for ~target_s of CPU work
         n0 = 200
-        oracle.run(V, T, S[:n0], E[:n0], flags=False)  # thread pool start-up outside the calibration
+        oracle.run(V, T, S[:n0], E[:n0])  # thread pool start-up outside the calibration
         t = time.perf_counter()
-        oracle.run(V, T, S[:n0], E[:n0], flags=False)
+        oracle.run(V, T, S[:n0], E[:n0])
         dt = max(time.perf_counter() - t, 1e-3)
         sample = int(min(len(S), max(n0, n0 * target_s / dt)))
     t = time.perf_counter()
-    oracle.run(V, T, S[:sample], E[:sample], flags=False)
+    ref = oracle.run(V, T, S[:sample], E[:sample])
     dt = time.perf_counter() - t
-    return {"value": sample / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"first {sample} rays of the workload x all {len(T)} triangles, all modes at once "
-                      f"(exhaustive fp64, {dt:.1f} s)"}
+    return ({"value": sample / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+             "sample": f"first {sample} rays of the workload x all {len(T)} triangles, all modes + ambiguity "
+                       f"flags at once (exhaustive fp64, {dt:.1f} s)"}, ref)
+
+
+def parity_report(got: dict, ref: dict, S, E, label: str) -> dict:
+    """GPU outputs of all three modes vs the oracle on the same rays, every ray
+    (north_star agreement: boolean / intercept_count / nearest id exact on
+    every ray -- flagged ones included and counted, never excused; t, dist,
+    point within 1e-5, 1e-5 |d|, 1e-5 max(|O|, |E|)).  Flags: E edge/vertex,
+    T endpoint touch, P near-parallel, B nearest tie, D dedup ambiguity."""
+    import oracle
+    fl = ref["flags"]
+    m = ref["tri"] >= 0
+    d = E.astype(np.float64) - S
+    dn = np.maximum(np.linalg.norm(d, axis=1), 1e-30)
+    scale = np.maximum(np.maximum(np.abs(S).max(1), np.abs(E).max(1)), 1e-30)
+    both = m & (got["tri"] == ref["tri"])
+    dt = np.abs(got["t"][both] - ref["t"][both])
+    dd = np.abs(got["dist"][both] - ref["dist"][both]) / dn[both]
+    dp = np.abs(got["point"][both] - ref["point"][both]).max(1) / scale[both]
+    bad = ((got["hit"] != ref["hit"]) | (got["count"] != ref["count"]) | (got["tri"] != ref["tri"]))
+    tol = np.zeros(len(S), bool)
+    tol[np.nonzero(both)[0]] = (dt > 1e-5) | (dd > 1e-5) | (dp > 1e-5)
+    names = {"E": oracle.FLAG_E, "T": oracle.FLAG_T, "P": oracle.FLAG_P, "B": oracle.FLAG_B, "D": oracle.FLAG_D}
+    return {"workload": label, "rays": int(len(S)),
+            "mismatch_bool": int((got["hit"] != ref["hit"]).sum()),
+            "mismatch_count": int((got["count"] != ref["count"]).sum()),
+            "mismatch_tri": int((got["tri"] != ref["tri"]).sum()),
+            "tol_violations": int(tol.sum()),
+            "max_dt": float(dt.max()) if dt.size else 0.0,
+            "max_ddist_rel": float(dd.max()) if dd.size else 0.0,
+            "max_dpoint_rel": float(dp.max()) if dp.size else 0.0,
+            "flagged": {**{k: int(((fl & b) != 0).sum()) for k, b in names.items()}, "any": int((fl != 0).sum())},
+            "flagged_mismatch": int((bad & (fl != 0)).sum()),
+            "ok": bool(not bad.any() and not tol.any())}
 
 
 def _traffic(mode: str, rays: int):
-    """DRAM bytes per launch from the committed ncu capture (same workload), if present."""
+    """DRAM bytes per launch from the committed ncu capture of the same
+    workload and ray count (profiles/traffic.json), if present."""
     try:
         t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
-        return int(t[mode]) if rays == 10_000_000 else None
+        return int(t[mode]) if rays == int(t.get("rays", 10_000_000)) else None
     except (OSError, KeyError, ValueError):
         return None
 
@@ -183,6 +221,81 @@ def roofline(mode: str, rays: int, kernel_ms: float, sm_mhz: float | None, work:
                      f"tests/ray); peak = 148 SM x 128 FP32 lanes x median sm_mhz"}
 
 
+def oracle_run(V, T, S, E):
+    import oracle
+    return oracle.run(V, T, S, E)
+
+
+def gpu_outputs(h, Sd, Ed) -> dict:
+    """All three modes through rsi_intersect on the given handle, as host numpy."""
+    from paper_2305_01867_b200 import rsi
+    got = {"hit": rsi.rsi_intersect(h, Sd, Ed, "boolean")["hit"].cpu().numpy(),
+           "count": rsi.rsi_intersect(h, Sd, Ed, "intercept_count")["count"].cpu().numpy()}
+    got.update({k: v.cpu().numpy() for k, v in rsi.rsi_intersect(h, Sd, Ed, "barycentric").items()})
+    return got
+
+
+def pcie_link(index: int) -> str | None:
+    try:
+        r = subprocess.run(["nvidia-smi", "--query-gpu=pcie.link.gen.current,pcie.link.gen.max,"
+                            "pcie.link.width.current,pcie.link.width.max", "--format=csv,noheader",
+                            "-i", str(index)], capture_output=True, text=True, timeout=20)
+        g, gm, w, wm = [x.strip() for x in r.stdout.strip().split(",")]
+        return f"PCIe gen {g} (max {gm}) x{w} (max x{wm})"
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def pcie_ceiling(dev, ray_bytes: int, d2h_bytes: int, reps: int = 5) -> dict:
+    """The host->device ceiling of the e2e path, measured the ways the path can
+    copy: the step's ray bytes (2 arrays) as one copy per array, in 1 Mi-ray
+    chunks on one stream, and in 1 Mi-ray chunks alternating two streams
+    (rsi_test's pipeline), each timed with CUDA events, best of `reps`.  The
+    fastest is the ceiling (the largest achievable GB/s; rsi_test cannot move
+    its inputs faster).  The D2H of the outputs (other direction) and the
+    last chunk's traversal; mesh and output copies are not counted, so the
+    ceiling is a lower bound on any e2e step time)."""
+    import torch
+    nb = 2 * ray_bytes
+    hb = torch.empty(nb, dtype=torch.uint8).pin_memory()
+    db = torch.empty(nb, dtype=torch.uint8, device=dev)
+    chunk = (1 << 20) * 12
+    streams = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)]
+    cur = torch.cuda.current_stream(dev)
+
+    def run(kind):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cur)
+        if kind == "single":
+            for half in (0, ray_bytes):
+                db[half:half + ray_bytes].copy_(hb[half:half + ray_bytes], non_blocking=True)
+        else:
+            for st in streams:
+                st.wait_event(a)
+            k = 0
+            for half in (0, ray_bytes):
+                for o in range(0, ray_bytes, chunk):
+                    e = min(o + chunk, ray_bytes)
+                    st = streams[k % 2] if kind == "chunk2" else streams[0]
+                    with torch.cuda.stream(st):
+                        db[half + o:half + e].copy_(hb[half + o:half + e], non_blocking=True)
+                    k += 1
+            for st in streams:
+                cur.wait_stream(st)
+        b.record(cur)
+        torch.cuda.synchronize(dev)
+        return a.elapsed_time(b)
+
+    best = {}
+    for kind in ("single", "chunk1", "chunk2"):
+        run(kind)
+        best[kind] = min(run(kind) for _ in range(reps))
+    del hb, db
+    kind = min(best, key=best.get)
+    return {"ms": best[kind], "h2d_GBps": nb / best[kind] / 1e6, "method": kind,
+            "candidates_ms": {k: round(v, 4) for k, v in best.items()}, "link": pcie_link(dev.index or 0)}
+
+
 # ------------------------------------------------------------------ reference arm
 def arm_config(args, n_tri: int, world: int, backend: str = "nccl") -> dict:
     """The `config` both arms report (the reference arm adds its sample)."""
@@ -190,7 +303,7 @@ def arm_config(args, n_tri: int, world: int, backend: str = "nccl") -> dict:
             "n_triangles": n_tri, "rays_per_gpu": args.rays_per_gpu, "mode": args.mode,
             "parallelism": f"ray-sharded x{world}" + ((" + fused NVLink writes to rank 0" if getattr(args, "fused_gather", False)
                                                      else f" + {backend} gather to rank 0") if world > 1 else ""),
-            "l2": "inputs larger than L2 (240 MB of segments per GPU)",
+            "l2": f"inputs larger than L2 ({args.rays_per_gpu * 24 / 1e6:.0f} MB of segments per GPU; no flush)",
             "step": "rsi_rebuild + rsi_intersect" + (" + gather" if world > 1 else "")
                     + " (RSI_OPT_DEFERRED_STATUS: build checks read back after the timed region)"}
 
@@ -205,20 +318,20 @@ def run_reference(args, rank: int, world: int):
     import oracle
     cores = oracle.max_threads()
     n0 = 100
-    oracle.run(V, T, S[:n0], E[:n0], flags=False)  # thread pool start-up outside the calibration
+    oracle.run(V, T, S[:n0], E[:n0])  # thread pool start-up outside the calibration
     t = time.perf_counter()
-    oracle.run(V, T, S[:n0], E[:n0], flags=False)
+    oracle.run(V, T, S[:n0], E[:n0])
     dt = max(time.perf_counter() - t, 1e-3)
     per_step = int(max(n0, min(len(S), n0 * 4.0 / dt)))   # ~4 s of CPU per step
     for i in range(args.warmup):
-        oracle.run(V, T, S[:per_step], E[:per_step], flags=False)
+        oracle.run(V, T, S[:per_step], E[:per_step])
     t = time.perf_counter()
     for i in range(args.steps):
-        oracle.run(V, T, S[:per_step], E[:per_step], flags=False)
+        oracle.run(V, T, S[:per_step], E[:per_step])
     el = time.perf_counter() - t
     value = per_step * args.steps / el
     sample = (f"first {per_step} rays of the workload per step x all {len(T)} triangles, "
-              f"exhaustive fp64, all modes at once")
+              f"exhaustive fp64, all modes + ambiguity flags at once")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -283,6 +396,8 @@ def main():
             out = outs[k % len(outs)]
             if pipe is not None and pipe.slots[k % 2] is not None:
                 pipe.slots[k % 2].wait()  # this slot's send buffer is free again
+            if peer is not None:
+                peer.begin()  # rank 0 is done with the previous step's rows
             if ev is not None:
                 ev[0].record(stream)
             rsi.rsi_rebuild(h, Vd, Td)
@@ -388,41 +503,31 @@ def main():
     if not args.no_e2e:
         pin = lambda a: torch.from_numpy(a).pin_memory()  # noqa: E731
         hV, hT, hS, hE = pin(V), pin(T), pin(S), pin(E)
-        hout = {"hit": torch.empty(n, dtype=torch.uint8).pin_memory()}
+        hout = {k: v.pin_memory() for k, v in rsi.alloc_outputs(n, args.mode, "cpu").items()}
         for _ in range(2):
-            rsi.rsi_test(hV, hT, hS, hE, {"mode": args.mode}, out=hout)
+            rsi.rsi_test(hV, hT, hS, hE, {"mode": args.mode}, out=hout, sparse=False)
         e_steps = max(2, min(args.steps, 5))
         if world > 1:
             dist.barrier()
         t = time.perf_counter()
         for _ in range(e_steps):
-            rsi.rsi_test(hV, hT, hS, hE, {"mode": args.mode}, out=hout)
+            rsi.rsi_test(hV, hT, hS, hE, {"mode": args.mode}, out=hout, sparse=False)
         el = time.perf_counter() - t
         if world > 1:
             tt = torch.tensor([el], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             el = tt.item()
         h2d = V.nbytes + T.nbytes + S.nbytes + E.nbytes
-        # e2e roofline: the same bytes as ONE plain pinned host->device copy
-        # (the PCIe ceiling this path cannot beat), timed the same way
-        hb = torch.empty(h2d, dtype=torch.uint8).pin_memory()
-        db = torch.empty(h2d, dtype=torch.uint8, device=dev)
-        for _ in range(2):
-            db.copy_(hb, non_blocking=True)
-        torch.cuda.synchronize(dev)
-        t = time.perf_counter()
-        for _ in range(e_steps):
-            db.copy_(hb, non_blocking=True)
-        torch.cuda.synchronize(dev)
-        copy_ms = (time.perf_counter() - t) / e_steps * 1e3
-        del hb, db
+        d2h = sum(v.numel() * v.element_size() for v in hout.values())
         e_ms = el / e_steps * 1e3
+        ceil = pcie_ceiling(dev, S.nbytes, d2h)
         e2e = {"value": n * world * e_steps / el, "unit": UNIT, "h2d_bytes_per_step": h2d,
-               "d2h_bytes_per_step": n, "ms_per_step": e_ms,
-               "api": "rsi_test (C-ABI, pinned host buffers)",
-               "roofline": {"bound": "pcie_h2d", "h2d_copy_ms": copy_ms,
-                            "h2d_GBps": h2d / copy_ms / 1e6, "frac": copy_ms / e_ms,
-                            "note": "plain pinned copy of the step's input bytes / e2e step time"}}
+               "d2h_bytes_per_step": d2h, "ms_per_step": e_ms,
+               "api": "rsi_test (C-ABI, pinned host buffers, dense per-ray outputs)",
+               "roofline": {"bound": "pcie_h2d", "ceiling_ms": ceil["ms"], "h2d_GBps": ceil["h2d_GBps"],
+                            "frac": ceil["ms"] / e_ms, "link": ceil["link"], "method": ceil["method"],
+                            "candidates_ms": ceil["candidates_ms"]}}
+        del hV, hT, hS, hE, hout
 
     # the paper's own headline workload, end to end like its timings (P:144,
     # P:147-154): 1e7 rays against the 29 260-triangle terrain, host buffers in,
@@ -451,9 +556,23 @@ def main():
                         "speedup_vs_paper": pms / ms_m}
         del hVp, hTp, hSp, hEp
 
-    cpu = None
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(V, T, S, E, sample=args.cpu_sample)
+        cpu, ref = cpu_baseline(V, T, S, E, sample=args.cpu_sample)
+        # parity on the sample the oracle just computed: the GPU outputs of all
+        # three modes for the same rays of the timed workload (same kernels and
+        # launch configuration as the timed steps)
+        k = len(ref["hit"])
+        got = gpu_outputs(h, Sd[:k], Ed[:k])
+        parity = {"bench": parity_report(got, ref, S[:k], E[:k], f"{args.workload} N_t={len(T)}, "
+                                                                   f"first {k} rays of the timed workload")}
+        if not args.no_parity:  # the 1e6-triangle mesh of configs[4] (L2-sized tree)
+            V1, T1, S1, E1 = workload_inputs("sphere1m", 20_000, 0)
+            ref1 = oracle_run(V1, T1, S1, E1)
+            V1d, T1d = torch.from_numpy(V1).to(dev), torch.from_numpy(T1).to(dev)
+            with rsi.rsi_build(V1d, T1d) as h1:
+                got1 = gpu_outputs(h1, torch.from_numpy(S1).to(dev), torch.from_numpy(E1).to(dev))
+            parity["sphere1m"] = parity_report(got1, ref1, S1, E1, f"sphere1m N_t={len(T1)}, 20000 rays")
 
     if rank == 0:
         line = {
@@ -465,7 +584,7 @@ def main():
             "build_ms": build_ms, "query_ms": query_ms,
             "roofline": roofline(args.mode, n, query_ms, clk["sm_mhz"] if clk else None, work),
             "work_per_ray": work,
-            "cpu_baseline": cpu, "e2e": e2e,
+            "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
             "gpu_launches": launches,
             "gpu_launches_note": "rsi_launch_count() difference over the timed region (library kernels: "
                                  "BVH build chain + 1 traversal kernel per step)",

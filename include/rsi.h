@@ -26,6 +26,13 @@
  *     thread-local message; CUDA errors are never swallowed.
  *   - The library is thread-compatible: a handle may be used by one thread at a
  *     time; distinct handles are independent.
+ *   - Calls on one handle execute on the device in CALL order, whatever streams
+ *     they are given: every rsi_rebuild / rsi_intersect records an event on its
+ *     stream, and a call on a different stream than the previous one first
+ *     waits on that event (device-side).  This orders the handle's per-call
+ *     scratch (ray dispenser, overflow counters), which every call resets.
+ *     rsi_free frees after the last call.  Work on distinct handles is not
+ *     ordered.
  */
 #ifndef RSI_H_
 #define RSI_H_
@@ -266,7 +273,23 @@ void rsi_release_cache(void);
 rsi_status_t rsi_compact_hits(const int32_t* d_tri, int64_t n_rays, int32_t* d_ray_ids,
                               int32_t* d_n_hits, void* stream);
 
-/* Release the handle and its device memory (stream-ordered on the build stream). */
+/*
+ * rsi_gather_hits -- the values of the compacted hit rays (the rest of the
+ * paper's sparse barycentric return, after step 3a): for j < *d_n_hits,
+ *   d_out_tri[j] = d_tri[d_ray_ids[j]], d_out_dist[j] = d_dist[d_ray_ids[j]],
+ *   d_out_point[j][0..2] = d_point[d_ray_ids[j]][0..2]
+ * (all DEVICE pointers; d_ray_ids / d_n_hits as written by rsi_compact_hits;
+ * n_max = the capacity of the outputs, >= *d_n_hits; d_dist/d_out_dist and
+ * d_point/d_out_point may be NULL together).  Asynchronous: the hit count is
+ * read on the device, never by the host.
+ * Errors: RSI_E_INVALID_ARG (null required pointer, n_max < 0), RSI_E_CUDA.
+ */
+rsi_status_t rsi_gather_hits(const int32_t* d_ray_ids, const int32_t* d_n_hits, int64_t n_max,
+                             const int32_t* d_tri, const float* d_dist, const float* d_point,
+                             int32_t* d_out_tri, float* d_out_dist, float* d_out_point, void* stream);
+
+/* Release the handle and its device memory (stream-ordered on the build
+ * stream, after the handle's last call on any stream). */
 rsi_status_t rsi_free(rsi_handle_t h);
 
 /*

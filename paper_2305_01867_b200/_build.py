@@ -6,6 +6,7 @@ repo snapshot to the GPU box.
 from __future__ import annotations
 
 import glob
+import hashlib
 import os
 import subprocess
 
@@ -30,11 +31,27 @@ def _nvcc() -> str:
     return "nvcc"
 
 
+HASH_FILE = LIB + ".sha256"
+
+
+def source_hash() -> str:
+    """Hash of every source, header and the nvcc flags: the .so is rebuilt
+    whenever it differs from the hash recorded at its build (not by mtime, so a
+    pushed prebuilt .so newer than the sources is never mistaken for HEAD's)."""
+    h = hashlib.sha256()
+    for p in SOURCES + HEADERS:
+        h.update(os.path.relpath(p, ROOT).encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
+    h.update(" ".join(NVCC_FLAGS).encode())
+    return h.hexdigest()
+
+
 def stale() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(HASH_FILE):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(p) > t for p in SOURCES + HEADERS)
+    with open(HASH_FILE) as f:
+        return f.read().strip() != source_hash()
 
 
 def build_library(force: bool = False, verbose: bool = False) -> str:
@@ -48,6 +65,8 @@ def build_library(force: bool = False, verbose: bool = False) -> str:
         print(" ".join(cmd))
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
+    with open(HASH_FILE, "w") as f:
+        f.write(source_hash() + "\n")
     return LIB
 
 

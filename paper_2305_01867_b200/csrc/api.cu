@@ -88,6 +88,25 @@ static std::atomic<uint64_t> g_launches{0};
 
 void rsi_note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+// Calls on one handle run in the order they were made even when the caller
+// switches streams: a call on a stream other than the previous call's waits
+// for the previous call's event first (device-side; the host never blocks).
+static rsi_status_t order_enter(rsi_bvh* h, cudaStream_t s) {
+    if (h->order_valid && h->last_stream != s)
+        return rsi_cuda_check(cudaStreamWaitEvent(s, h->order_ev, 0), "stream order wait");
+    return RSI_OK;
+}
+static rsi_status_t order_leave(rsi_bvh* h, cudaStream_t s) {
+    if (!h->order_ev) {
+        rsi_status_t st = rsi_cuda_check(cudaEventCreateWithFlags(&h->order_ev, cudaEventDisableTiming), "event");
+        if (st != RSI_OK) return st;
+    }
+    rsi_status_t st = rsi_cuda_check(cudaEventRecord(h->order_ev, s), "stream order record");
+    h->last_stream = s;
+    h->order_valid = st == RSI_OK;
+    return st;
+}
+
 extern "C" {
 
 const char* rsi_version(void) { return RSI_VERSION_STRING; }
@@ -118,6 +137,7 @@ rsi_status_t rsi_build(const float* d_vertices, int64_t n_vertices, const int32_
         st = rsi_cuda_check(cudaMallocAsync((void**)&h->stats, ST_WORDS * sizeof(unsigned long long), s), "stats");
     if (st == RSI_OK) st = rsi_cuda_check(cudaMemsetAsync(h->stats, 0, ST_WORDS * sizeof(unsigned long long), s), "stats");
     if (st == RSI_OK) st = rsi_build_device(h, d_vertices, n_vertices, d_triangles, n_triangles, s);
+    if (st == RSI_OK) st = order_leave(h, s);
     if (st != RSI_OK) {
         char saved[512];
         memcpy(saved, g_err, sizeof(saved));
@@ -132,11 +152,19 @@ rsi_status_t rsi_build(const float* d_vertices, int64_t n_vertices, const int32_
 rsi_status_t rsi_rebuild(rsi_handle_t h, const float* d_vertices, int64_t n_vertices, const int32_t* d_triangles,
                          int64_t n_triangles, void* stream) {
     if (!h) return rsi_set_error(RSI_E_INVALID_ARG, "null handle");
+    int dev = -1;
+    cudaGetDevice(&dev);
+    if (dev != h->device)  // the handle's buffers live on its own device
+        return rsi_set_error(RSI_E_INVALID_ARG, "handle built on device %d, current device is %d", h->device, dev);
     h->n_tri = 0;
     h->n_nodes = 0;
     rsi_status_t st = check_mesh_args(d_vertices, n_vertices, d_triangles, n_triangles);
     if (st != RSI_OK) return st;
-    return rsi_build_device(h, d_vertices, n_vertices, d_triangles, n_triangles, (cudaStream_t)stream);
+    cudaStream_t s = (cudaStream_t)stream;
+    st = order_enter(h, s);
+    if (st == RSI_OK) st = rsi_build_device(h, d_vertices, n_vertices, d_triangles, n_triangles, s);
+    const rsi_status_t st2 = order_leave(h, s);
+    return st != RSI_OK ? st : st2;
 }
 
 rsi_status_t rsi_intersect(rsi_handle_t h, const float* d_start, const float* d_end, int64_t n_rays, int32_t mode,
@@ -158,9 +186,12 @@ rsi_status_t rsi_intersect(rsi_handle_t h, const float* d_start, const float* d_
     cudaGetDevice(&dev);
     if (dev != h->device)
         return rsi_set_error(RSI_E_INVALID_ARG, "handle built on device %d, current device is %d", h->device, dev);
-    rsi_status_t st = rsi_intersect_device(h, d_start, d_end, n_rays, mode, out, (cudaStream_t)stream);
+    cudaStream_t s = (cudaStream_t)stream;
+    rsi_status_t st = order_enter(h, s);
+    if (st == RSI_OK) st = rsi_intersect_device(h, d_start, d_end, n_rays, mode, out, s);
     if (st == RSI_OK) h->host_rays += (uint64_t)n_rays;
-    return st;
+    const rsi_status_t st2 = order_leave(h, s);
+    return st != RSI_OK ? st : st2;
 }
 
 rsi_status_t rsi_compact_hits(const int32_t* d_tri, int64_t n_rays, int32_t* d_ray_ids, int32_t* d_n_hits,
@@ -169,6 +200,17 @@ rsi_status_t rsi_compact_hits(const int32_t* d_tri, int64_t n_rays, int32_t* d_r
         return rsi_set_error(RSI_E_INVALID_ARG, "bad compaction arguments");
     if (n_rays > ((int64_t)1 << 31) - 1) return rsi_set_error(RSI_E_INVALID_ARG, "n_rays exceeds 2^31-1");
     return rsi_compact_device(d_tri, n_rays, d_ray_ids, d_n_hits, (cudaStream_t)stream);
+}
+
+rsi_status_t rsi_gather_hits(const int32_t* d_ray_ids, const int32_t* d_n_hits, int64_t n_max, const int32_t* d_tri,
+                             const float* d_dist, const float* d_point, int32_t* d_out_tri, float* d_out_dist,
+                             float* d_out_point, void* stream) {
+    if (n_max < 0 || (n_max > 0 && (!d_ray_ids || !d_n_hits || !d_tri || !d_out_tri)) ||
+        (!d_dist) != (!d_out_dist) || (!d_point) != (!d_out_point))
+        return rsi_set_error(RSI_E_INVALID_ARG, "bad gather arguments");
+    if (n_max > ((int64_t)1 << 31) - 1) return rsi_set_error(RSI_E_INVALID_ARG, "n_max exceeds 2^31-1");
+    return rsi_gather_hits_device(d_ray_ids, d_n_hits, n_max, d_tri, d_dist, d_point, d_out_tri, d_out_dist,
+                                  d_out_point, (cudaStream_t)stream);
 }
 
 // Per-(thread, device) workspace of rsi_test, reused across calls: the BVH
@@ -520,6 +562,7 @@ void rsi_release_cache(void) {
 rsi_status_t rsi_free(rsi_handle_t h) {
     if (!h) return RSI_OK;
     cudaStream_t s = h->stream;
+    order_enter(h, s);  // the frees follow the handle's last use on any stream
     void* bufs[] = {h->nodes, h->top, h->quads, h->tris, h->keys, h->vals, h->keys_tmp, h->vals_tmp, h->parent,
                     h->arrivals, h->hist, h->scratch, h->stats, h->ovf_list, h->k63, h->other};
     rsi_status_t st = RSI_OK;
@@ -528,6 +571,7 @@ rsi_status_t rsi_free(rsi_handle_t h) {
             rsi_status_t e = rsi_cuda_check(cudaFreeAsync(p, s), "cudaFreeAsync");
             if (st == RSI_OK) st = e;
         }
+    if (h->order_ev) cudaEventDestroy(h->order_ev);
     delete h;
     return st;
 }

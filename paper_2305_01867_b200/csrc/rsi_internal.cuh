@@ -90,6 +90,12 @@ struct rsi_bvh {
     int64_t pending_nv = 0;          // n_vertices of that build (error message)
     uint64_t host_rays = 0, host_overflow = 0;  // counters known on the host
     int min_trav = -1;  // traversal-phase exit threshold (-1: per-mode default); env RSI_MIN_TRAV
+    // stream ordering across calls (the handle's scratch -- ray dispenser,
+    // overflow counters -- is reset by every call): each call records
+    // `order_ev` on its stream; a call on a DIFFERENT stream first waits on it
+    cudaEvent_t order_ev = nullptr;
+    cudaStream_t last_stream = nullptr;
+    bool order_valid = false;
 };
 
 // ---------------------------------------------------------------- host helpers (api.cu)

@@ -1810,10 +1810,12 @@ __global__ void __launch_bounds__(256) k_gather_hits(const int32_t* __restrict__
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
         const int i = ids[j];
         out_tri[j] = tri[i];
-        out_dist[j] = dist[i];
-        out_point[3 * j] = point[3 * (int64_t)i];
-        out_point[3 * j + 1] = point[3 * (int64_t)i + 1];
-        out_point[3 * j + 2] = point[3 * (int64_t)i + 2];
+        if (dist) out_dist[j] = dist[i];
+        if (point) {
+            out_point[3 * j] = point[3 * (int64_t)i];
+            out_point[3 * j + 1] = point[3 * (int64_t)i + 1];
+            out_point[3 * j + 2] = point[3 * (int64_t)i + 2];
+        }
     }
 }
 

@@ -88,6 +88,7 @@ def load():
             "rsi_intersect": ([_p, _p, _p, _i64, _i32, ctypes.POINTER(_Outputs), _p], ctypes.c_int),
             "rsi_test": ([_p, _i64, _p, _i64, _p, _p, _i64, _i32, _p, ctypes.POINTER(_Outputs), _p], ctypes.c_int),
             "rsi_compact_hits": ([_p, _i64, _p, _p, _p], ctypes.c_int),
+            "rsi_gather_hits": ([_p, _p, _i64, _p, _p, _p, _p, _p, _p, _p], ctypes.c_int),
             "rsi_free": ([_p], ctypes.c_int),
             "rsi_release_cache": ([], None),
             "rsi_get_stats": ([_p, ctypes.POINTER(_Stats), _p], ctypes.c_int),
@@ -207,6 +208,8 @@ def rsi_build(vertices: torch.Tensor, triangles: torch.Tensor, options: Options 
 def rsi_rebuild(h: Handle, vertices: torch.Tensor, triangles: torch.Tensor, stream=None) -> Handle:
     V = _dev(vertices, torch.float32, "vertices")
     T = _dev(triangles, torch.int32, "triangles")
+    if V.device != h.device or T.device != h.device:
+        raise ValueError(f"mesh is on {V.device}/{T.device}, the handle lives on {h.device}")
     with torch.cuda.device(V.device):
         _check(load().rsi_rebuild(h.ptr, V.data_ptr(), V.shape[0], T.data_ptr(), T.shape[0], _stream(stream)))
     return h
@@ -267,6 +270,10 @@ def rsi_intersect(h: Handle, start: torch.Tensor, end: torch.Tensor, mode: str =
     E = _dev(end, torch.float32, "end")
     if S.shape != E.shape:
         raise ValueError("start/end shape mismatch")
+    if S.device != E.device:
+        raise ValueError(f"start is on {S.device}, end on {E.device}")
+    if S.device != h.device:
+        raise ValueError(f"rays are on {S.device}, the handle's BVH on {h.device}")
     n = S.shape[0]
     if out is None:
         out = alloc_outputs(n, mode, S.device)
@@ -290,15 +297,36 @@ def rsi_compact_hits(tri: torch.Tensor, stream=None):
     return ids, nh
 
 
+def rsi_gather_hits(ids: torch.Tensor, n_hits: torch.Tensor, out: dict, stream=None) -> dict:
+    """The values of the compacted hit rays (rsi_gather_hits), on the
+    device: tri / dist / point rows of the ids rsi_compact_hits wrote (the hit
+    count stays on the device).  Returns capacity-n buffers."""
+    tri = _dev(out["tri"], torch.int32, "tri", cols=None)
+    n = tri.numel()
+    dist, point = out.get("dist"), out.get("point")
+    g = {"tri": torch.empty(n, dtype=torch.int32, device=tri.device),
+         "dist": torch.empty(n, dtype=torch.float32, device=tri.device) if dist is not None else None,
+         "point": torch.empty((n, 3), dtype=torch.float32, device=tri.device) if point is not None else None}
+    if dist is not None:
+        _check_out({"tri": tri, "dist": dist}, n, "barycentric", tri.device)
+    if point is not None:
+        _check_out({"tri": tri, "point": point}, n, "barycentric", tri.device)
+    ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+    with torch.cuda.device(tri.device):
+        _check(load().rsi_gather_hits(ids.data_ptr(), n_hits.data_ptr(), n, tri.data_ptr(), ptr(dist), ptr(point),
+                                      g["tri"].data_ptr(), ptr(g["dist"]), ptr(g["point"]), _stream(stream)))
+    return g
+
+
 def sparse_barycentric(out: dict, stream=None):
     """The paper's barycentric return: (intersecting_rays, distances,
-    hit_triangles, hit_points), rays ascending.  Compaction runs on the GPU;
-    the gather of the selected rows uses torch indexing (data movement only)."""
+    hit_triangles, hit_points), rays ascending.  Compaction (3a) and the gather
+    of the hit rows run in the library's kernels; the host reads the hit count
+    to trim the views."""
     ids, nh = rsi_compact_hits(out["tri"], stream)
+    g = rsi_gather_hits(ids, nh, out, stream)
     k = int(nh.item())
-    ids = ids[:k]
-    il = ids.long()
-    return ids, out["dist"][il], out["tri"][il], out["point"][il]
+    return ids[:k], g["dist"][:k], g["tri"][:k], g["point"][:k]
 
 
 def rsi_test(vertices, triangles, start, end, cfg: dict | None = None, options: Options | None = None,
@@ -306,8 +334,9 @@ def rsi_test(vertices, triangles, start, end, cfg: dict | None = None, options: 
     """End-to-end on HOST arrays through the C-ABI's rsi_test:
     H2D, build, intersect, D2H, synchronize.  Returns the boolean array, the
     counts, or (intersecting_rays, distances, hit_triangles, hit_points) -- the
-    paper's sparse tuple, gathered on the host from the dense per-ray outputs;
-    sparse=False returns the dense output dict instead (no host post-processing)."""
+    paper's sparse tuple, compacted and gathered on the device (rsi_test_sparse);
+    sparse=False returns the dense output dict instead (into `out` if given).
+    Every array must have shape [n, 3]; start and end must match."""
     lib = load()
     mode = (cfg or {}).get("mode", "boolean")
     if mode not in MODES:
@@ -319,20 +348,32 @@ def rsi_test(vertices, triangles, start, end, cfg: dict | None = None, options: 
                 raise ValueError(f"{name}: rsi_test takes host arrays")
             if a.dtype != dtype:
                 raise TypeError(f"{name} must be {dtype}, got {a.dtype}")
-            return a.contiguous()
-        a = np.asarray(a)
-        nd = {torch.float32: np.float32, torch.int32: np.int32}[dtype]
-        if a.dtype != nd:
-            raise TypeError(f"{name} must be {nd.__name__}, got {a.dtype} (P:272-299)")
-        return torch.from_numpy(np.ascontiguousarray(a))
+            t = a.contiguous()
+        else:
+            a = np.asarray(a)
+            nd = {torch.float32: np.float32, torch.int32: np.int32}[dtype]
+            if a.dtype != nd:
+                raise TypeError(f"{name} must be {nd.__name__}, got {a.dtype} (P:272-299)")
+            t = torch.from_numpy(np.ascontiguousarray(a))
+        # the C-ABI reads n * 12 bytes per array: the shape must be exactly [n, 3]
+        if t.dim() != 2 or t.shape[1] != 3:
+            raise ValueError(f"{name} must have shape [n, 3], got {tuple(t.shape)}")
+        return t
 
-    V = host(vertices, torch.float32, "vertices").reshape(-1, 3)
-    T = host(triangles, torch.int32, "triangles").reshape(-1, 3)
-    S = host(start, torch.float32, "start").reshape(-1, 3)
-    E = host(end, torch.float32, "end").reshape(-1, 3)
+    V = host(vertices, torch.float32, "vertices")
+    T = host(triangles, torch.int32, "triangles")
+    S = host(start, torch.float32, "start")
+    E = host(end, torch.float32, "end")
+    if S.shape != E.shape:
+        raise ValueError(f"start {tuple(S.shape)} and end {tuple(E.shape)} differ in shape")
     n = S.shape[0]
     opt = (options or Options())._c()
-    if mode == "barycentric" and sparse and out is None:
+    if mode == "barycentric" and sparse and out is not None:
+        # the sparse tuple is compacted on the device (rsi_test_sparse, step 3a);
+        # caller-provided buffers receive the DENSE per-ray outputs
+        raise ValueError("out= receives the dense per-ray outputs: pass sparse=False "
+                         "(or omit out for the sparse tuple, compacted on the device)")
+    if mode == "barycentric" and sparse:
         # the paper's sparse tuple: compaction and gather on the device
         ids = np.empty(n, np.int32)
         dist = np.empty(n, np.float32)
@@ -356,11 +397,7 @@ def rsi_test(vertices, triangles, start, end, cfg: dict | None = None, options: 
         return out["hit"].numpy().view(np.bool_).reshape(n, 1)  # 0/1 bytes: a view, no copy
     if mode == "intercept_count":
         return out["count"].numpy()
-    if not sparse:
-        return out
-    tri = out["tri"].numpy()
-    ids = np.nonzero(tri >= 0)[0].astype(np.int32)
-    return ids, out["dist"].numpy()[ids], tri[ids], out["point"].numpy()[ids]
+    return out  # barycentric, sparse=False: the dense per-ray outputs
 
 
 def rsi_build_status(h: Handle, stream=None):

@@ -145,7 +145,10 @@ class PeerOutputs:
     rank 0).  Every rank allocates the same symmetric buffers; only rank 0's
     are written.  Correct by construction: each rank writes the disjoint rows
     [floor(r N / W), floor((r+1) N / W)) of the full arrays, exactly the rows
-    the gather would place there.  Opt-in (bench --fused-gather); the default
+    the gather would place there.  A step is begin() -> traversal into
+    outputs() -> complete(): begin() holds every rank's writes until rank 0's
+    stream has passed its uses of the previous result() (enqueued before its
+    own begin()), so the buffers can be reused step after step.  Opt-in (bench --fused-gather); the default
     multi-GPU path is GatherPipeline."""
 
     def __init__(self, n_total: int, mode: str, device, group=None):
@@ -156,6 +159,7 @@ class PeerOutputs:
         self.n_total = n_total
         lo, hi = shard_range(n_total, self.rank, self.world)
         self.local, self.slices, self._handles = {}, {}, []
+        self._steps = 0
         for f in FIELDS[mode]:
             dtype, cols = FIELD_SPEC[f]
             buf = symm.empty(n_total * cols, dtype=dtype, device=device)
@@ -167,13 +171,23 @@ class PeerOutputs:
             self._handles.append(hdl)
 
     def outputs(self) -> dict:
-        """Output tensors for rsi_intersect: this rank's rows of rank 0's arrays."""
+        """Output tensors for rsi_intersect: this rank's rows of rank 0's arrays.
+        Call `begin()` before the step that writes them."""
         return self.slices
+
+    def begin(self):
+        """Device-side barrier before a step's peer writes (write-after-read):
+        no rank overwrites rank 0's rows while rank 0 may still be consuming
+        the previous step's result() on its stream.  Skipped for the first
+        step (nothing to protect yet)."""
+        if self._steps > 0:
+            self._handles[0].barrier(channel=1)
 
     def complete(self):
         """Device-side barrier of all ranks on the current stream: afterwards
         rank 0's arrays hold every rank's rows."""
         self._handles[0].barrier(channel=0)
+        self._steps += 1
 
     def result(self) -> dict | None:
         """The full outputs on rank 0 (valid after complete()), None elsewhere."""

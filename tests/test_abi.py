@@ -102,3 +102,33 @@ def test_binding_checks_caller_outputs():
     with pytest.raises(ValueError):  # host call with a short output array
         rsi.rsi_test(np.zeros((3, 3), np.float32), np.zeros((1, 3), np.int32), np.zeros((5, 3), np.float32),
                      np.zeros((5, 3), np.float32), {"mode": "boolean"}, out={"hit": torch.zeros(4, dtype=torch.uint8)})
+
+
+def test_binding_rejects_mismatched_host_shapes():
+    """rsi_test copies n*12 bytes from each ray array: start/end of different
+    lengths, or arrays that are not [n, 3], are rejected before the C-ABI."""
+    import numpy as np
+
+    from paper_2305_01867_b200 import rsi
+    V, T = np.zeros((3, 3), np.float32), np.zeros((1, 3), np.int32)
+    S = np.zeros((5, 3), np.float32)
+    with pytest.raises(ValueError):
+        rsi.rsi_test(V, T, S, np.zeros((4, 3), np.float32))
+    with pytest.raises(ValueError):
+        rsi.rsi_test(V, T, S.reshape(-1), S.reshape(-1))          # flat arrays
+    with pytest.raises(ValueError):
+        rsi.rsi_test(np.zeros((2, 6), np.float32), T, S, S)       # vertices not [n, 3]
+    with pytest.raises(ValueError):
+        rsi.rsi_test(V, T, S, S, {"mode": "barycentric"},         # sparse tuple into dense buffers
+                     out={k: v for k, v in rsi.alloc_outputs(5, "barycentric", "cpu").items()})
+
+
+def test_gather_hits_export_rejects_bad_args():
+    """rsi_gather_hits validates its pointers before any launch (no GPU needed)."""
+    import ctypes
+
+    from paper_2305_01867_b200 import rsi
+    lib = rsi.load()
+    assert lib.rsi_gather_hits(None, None, -1, None, None, None, None, None, None, None) == 1
+    assert lib.rsi_gather_hits(None, None, 10, None, None, None, None, None, None, None) == 1
+    assert lib.rsi_gather_hits(None, None, 0, None, ctypes.c_void_p(16), None, None, None, None, None) == 1  # dist w/o out

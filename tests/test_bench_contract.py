@@ -34,3 +34,31 @@ def test_arm_configs_match():
     c1 = bench.arm_config(args, 10_000, 1)
     c8 = bench.arm_config(args, 10_000, 8)
     assert c1["workload"] == c8["workload"] and "x8" in c8["parallelism"]
+
+
+def test_parity_report_counts_mismatches_and_flags():
+    """bench.py's parity block: an exact copy of the oracle's results is clean;
+    a flipped boolean, a wrong count, a wrong nearest id and an out-of-tolerance
+    point are each counted; flags are counted per category."""
+    sys.path.insert(0, ROOT)
+    import numpy as np
+
+    import bench
+    import oracle
+    import synth
+    V, T, S, E, _ = synth.workload("cube", 2000, seed=1)
+    ref = oracle.run(V, T, S, E)
+    got = {"hit": ref["hit"].copy(), "count": ref["count"].copy(), "tri": ref["tri"].copy(),
+           "t": ref["t"].astype(np.float32), "dist": ref["dist"].astype(np.float32),
+           "point": ref["point"].astype(np.float32)}
+    r = bench.parity_report(got, ref, S, E, "cube")
+    assert r["ok"] and r["rays"] == 2000 and r["mismatch_bool"] == r["mismatch_count"] == r["mismatch_tri"] == 0
+    assert r["max_dt"] <= 1e-7 and r["flagged"]["any"] == int((ref["flags"] != 0).sum())
+    hits = np.nonzero(ref["tri"] >= 0)[0]
+    got["hit"][0] ^= 1
+    got["count"][1] += 1
+    got["tri"][hits[0]] = (got["tri"][hits[0]] + 1) % len(T)
+    got["point"][hits[1]] += 1e-3
+    r = bench.parity_report(got, ref, S, E, "cube")
+    assert not r["ok"] and r["mismatch_bool"] == 1 and r["mismatch_count"] == 1 and r["mismatch_tri"] == 1
+    assert r["tol_violations"] == 1

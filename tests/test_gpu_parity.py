@@ -404,9 +404,13 @@ def test_compaction_and_sparse_return(rsi):
     h = rsi.rsi_build(Vd, Td)
     out = rsi.rsi_intersect(h, Sd, Ed, "barycentric")
     ids, dist, tri, pts = rsi.sparse_barycentric(out)
-    exp = np.nonzero(out["tri"].cpu().numpy() >= 0)[0]
+    dense = {k: v.cpu().numpy() for k, v in out.items()}
+    exp = np.nonzero(dense["tri"] >= 0)[0]
     assert (ids.cpu().numpy() == exp).all()
-    assert (tri.cpu().numpy() >= 0).all()
+    # rsi_gather_hits: the hit rows, bit for bit
+    assert (tri.cpu().numpy() == dense["tri"][exp]).all()
+    assert (dist.cpu().numpy().view(np.uint32) == dense["dist"][exp].view(np.uint32)).all()
+    assert (pts.cpu().numpy().view(np.uint32) == dense["point"][exp].view(np.uint32)).all()
     h.free()
 
 
@@ -793,13 +797,16 @@ def test_peer_outputs_single_rank(rsi):
         h = rsi.rsi_build(Vd, Td)
         for mode in ("boolean", "barycentric", "intercept_count"):
             peer = PeerOutputs(len(S), mode, torch.device(DEV))
-            rsi.rsi_intersect(h, Sd, Ed, mode, out=peer.outputs())
-            peer.complete()
             ref = rsi.rsi_intersect(h, Sd, Ed, mode)
-            torch.cuda.synchronize()
-            for k, v in peer.result().items():
-                a, b = v.cpu(), ref[k].cpu()
-                assert torch.equal(a, b) or bool(((a == b) | (torch.isnan(a) & torch.isnan(b))).all()), (mode, k)
+            for step in range(3):  # the same buffers reused step after step (begin / complete)
+                peer.begin()
+                rsi.rsi_intersect(h, Sd, Ed, mode, out=peer.outputs())
+                peer.complete()
+                torch.cuda.synchronize()
+                for k, v in peer.result().items():
+                    a, b = v.cpu(), ref[k].cpu()
+                    assert torch.equal(a, b) or bool(((a == b) | (torch.isnan(a) & torch.isnan(b))).all()), (mode, k)
+                    v.fill_(0)  # the next step must rewrite every row
         h.free()
     finally:
         if own:

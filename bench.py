@@ -131,7 +131,7 @@ def workload_inputs(name: str, n: int, rank: int):
     return V, T, S, E
 
 
-def cpu_baseline(V, T, S, E, target_s=15.0, sample=0):
+def cpu_baseline(V, T, S, E, target_s=20.0, sample=0):
     """The oracle (as it stands, with its ambiguity flags) on a bounded sample
     of the same workload.  Returns (cpu_baseline dict, oracle results on the
     sample) -- the results feed the parity report."""

@@ -212,9 +212,10 @@ rsi_status_t rsi_rebuild(rsi_handle_t h, const float* d_vertices, int64_t n_vert
  *   mode            an rsi_mode_t.
  *   out             device output pointers for `mode` (see rsi_outputs_t).
  * Results equal the exhaustive double-precision definition.
- * Asynchronous for BOOLEAN and BARYCENTRIC.  INTERCEPT_COUNT synchronizes
- * `stream` once (a 4-byte overflow count) and, only if some ray overflowed the
- * register hit list, runs an exact re-pass (which synchronizes once more).
+ * Asynchronous in every mode (returns once the work is enqueued; the host
+ * never reads device state).  INTERCEPT_COUNT enqueues a second kernel, the
+ * exact re-pass for rays whose hits overflow the traversal's register list;
+ * it reads the overflow count on the device and has no capacity limit.
  * n_rays == 0 is a no-op.  Errors: RSI_E_INVALID_ARG, RSI_E_OOM, RSI_E_CUDA.
  */
 rsi_status_t rsi_intersect(rsi_handle_t h, const float* d_start, const float* d_end,

@@ -606,7 +606,7 @@ rsi_status_t rsi_get_stats(rsi_handle_t h, rsi_stats_t* out, void* stream) {
     out->rays = h->host_rays;
     out->fp64_pairs = v[ST_FP64_PAIRS];
     out->fp64_rays = v[ST_FP64_RAYS];
-    out->overflow_rays = h->host_overflow;
+    out->overflow_rays = v[ST_OVERFLOW];
     out->nonfinite_rays = v[ST_NONFINITE];
     out->box_tests = v[ST_BOX_TESTS];
     out->mt_tests = v[ST_MT_TESTS];
@@ -622,7 +622,6 @@ rsi_status_t rsi_get_stats(rsi_handle_t h, rsi_stats_t* out, void* stream) {
 rsi_status_t rsi_reset_stats(rsi_handle_t h, void* stream) {
     if (!h) return rsi_set_error(RSI_E_INVALID_ARG, "null handle");
     h->host_rays = 0;
-    h->host_overflow = 0;
     return rsi_cuda_check(cudaMemsetAsync(h->stats, 0, ST_WORDS * sizeof(unsigned long long), (cudaStream_t)stream),
                           "reset stats");
 }

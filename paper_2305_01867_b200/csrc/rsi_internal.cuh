@@ -30,7 +30,7 @@ enum {
     SCR_STATUS = 6,    // bit 0 index out of range, bit 1 non-finite vertex
     SCR_ROOT = 9,      // 6 words: root (scene) AABB as float bits
     SCR_OVF_COUNT = 16, // intercept_count overflow list length
-    SCR_OVF_TOTAL = 17, // re-pass: total raw hits over overflowed rays
+    SCR_OVF_NEXT = 17,  // intercept_count re-pass: next overflowed segment (work counter)
     SCR_DISPENSER = 18, // 2 words: 64-bit ray dispenser of the persistent traversal grid
     SCR_NTOP = 20,      // nodes in the top-of-tree shared-memory image
     SCR_ROOT_SET = 21,  // 1 once the refit wrote the root box
@@ -88,7 +88,7 @@ struct rsi_bvh {
     float scene_lo[3] = {0, 0, 0}, scene_hi[3] = {0, 0, 0};
     bool status_pending = false;     // build checks not yet read back (RSI_OPT_DEFERRED_STATUS)
     int64_t pending_nv = 0;          // n_vertices of that build (error message)
-    uint64_t host_rays = 0, host_overflow = 0;  // counters known on the host
+    uint64_t host_rays = 0;  // rays counted on the host
     int min_trav = -1;  // traversal-phase exit threshold (-1: per-mode default); env RSI_MIN_TRAV
     // stream ordering across calls (the handle's scratch -- ray dispenser,
     // overflow counters -- is reset by every call): each call records

@@ -54,7 +54,6 @@ constexpr float kOutTol = 4e-6f;                 // max certified |t error| for 
 #ifndef RSI_COUNT_SMEM
 #define RSI_COUNT_SMEM 0
 #endif
-#define RSI_ANY_QUAD (RSI_BOOL_QUAD || RSI_BARY_QUAD || RSI_COUNT_QUAD)
 constexpr bool kQuadCount = RSI_COUNT_QUAD;
 // speculative walk on the 4-wide records (a lane with a pending leaf keeps
 // walking): measured -2..-4 % barycentric, +3..5 % boolean with grandchild
@@ -118,7 +117,6 @@ constexpr int kCountCap = RSI_COUNT_CAP;
 #ifndef RSI_COUNT_MINB
 #define RSI_COUNT_MINB 7
 #endif
-constexpr int kThreads = 128;  // block size of the auxiliary (re-pass) kernels
 // k_trace block size: with the top-of-tree cache, one CTA per SM shares the
 // image (1024 threads at <= 64 registers for boolean, 768 at <= 80 otherwise)
 template <int MODE>
@@ -349,47 +347,6 @@ __device__ __forceinline__ void load_tri(const float4* __restrict__ tris, int k,
         float4 pad;
         ldg256(tris + 4 * k, A, B);
         ldg256(tris + 4 * k + 2, C, pad);
-    }
-}
-
-// ---------------------------------------------------------------- traversal skeleton
-// leaf(slot) returns true to terminate the walk; tclip may shrink inside it.
-template <class LeafFn>
-__device__ __forceinline__ void traverse(const float4* __restrict__ nodes, int root, const Ray& r, float& tclip,
-                                         LeafFn&& leaf) {
-    int stack[kStackBinary];
-    int sp = 0;
-    int node = root;
-    if (node < 0) return;  // no root (fault-injected build)
-    while (true) {
-        const float4* nd = nodes + 4 * node;
-        float4 n0, n1, n2, n3f;
-        ldg256(nd, n0, n1);
-        ldg256(nd + 2, n2, n3f);
-        const int4 n3 = make_int4(__float_as_int(n3f.x), __float_as_int(n3f.y), 0, 0);
-        float nearL, nearR;
-        bool hL = slab(r, n0.x, n0.y, n0.z, n0.w, n2.x, n2.y, tclip, nearL);
-        bool hR = slab(r, n1.x, n1.y, n1.z, n1.w, n2.z, n2.w, tclip, nearR);
-        if (hL && n3.x < 0) {
-            if (leaf(~n3.x)) return;
-            hL = false;
-        }
-        if (hR && n3.y < 0) {
-            if (leaf(~n3.y)) return;
-            hR = false;
-        }
-        if (hL && hR) {
-            const bool rfirst = nearR < nearL;
-            stack[sp++] = rfirst ? n3.x : n3.y;
-            node = rfirst ? n3.y : n3.x;
-        } else if (hL) {
-            node = n3.x;
-        } else if (hR) {
-            node = n3.y;
-        } else {
-            if (sp == 0) return;
-            node = stack[--sp];
-        }
     }
 }
 
@@ -1327,402 +1284,267 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
 }
 
 // ---------------------------------------------------------------- exact re-pass for overflowed rays
-// Single-thread walk over the 4-wide records (the re-pass's all-hits walk:
-// half the dependent fetches of the binary walk for the long, grazing segments
-// that overflow).  Same conservative decode as k_trace's visit; leaf(slot) is
-// called for every leaf whose box the segment enters.
-template <class LeafFn>
-__device__ __forceinline__ void traverse_quads(const float4* __restrict__ quads, int root, const Ray& r,
-                                               uint32_t magic, LeafFn&& leaf) {
-    int stack[kStackQuad];
-    int sp = 0;
-    int node = root;
-    if (node < 0) return;
-    const float inv3[3] = {r.ix, r.iy, r.iz};
-    const uint32_t msk[3] = {r.mx, r.my, r.mz};
-    const float nof[3] = {r.lx, r.ly, r.lz};
-    const float fof[3] = {r.hx, r.hy, r.hz};
-    while (true) {
-        const float4* q = quads + 4 * node;
-        float4 qa, qb, qc, qd;
-        ldg256(q, qa, qb);
-        ldg256(q + 2, qc, qd);
-        const float pp[3] = {qa.x, qa.y, qa.z};
-        const uint32_t wq[6] = {__float_as_uint(qb.x), __float_as_uint(qb.y), __float_as_uint(qb.z),
-                                __float_as_uint(qb.w), __float_as_uint(qc.x), __float_as_uint(qc.y)};
-        const float scv[3] = {qa.w, qd.z, qd.w};
-        float sa[3], bn[3], bf[3];
-        uint32_t wn[3], wf[3];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            sa[a] = scv[a] * inv3[a];
-            bn[a] = fmaf(pp[a], inv3[a], -nof[a]);
-            bf[a] = fmaf(pp[a], inv3[a], -fof[a]);
-            wn[a] = (wq[2 * a] & ~msk[a]) | (wq[2 * a + 1] & msk[a]);
-            wf[a] = (wq[2 * a + 1] & ~msk[a]) | (wq[2 * a] & msk[a]);
-        }
-        const int ref[4] = {__float_as_int(qc.z), __float_as_int(qc.w), __float_as_int(qd.x), __float_as_int(qd.y)};
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const float tn = fmaxf(fmaxf(fmaf(byte_to_2p15(wn[0], j, magic), sa[0], bn[0]),
-                                         fmaf(byte_to_2p15(wn[1], j, magic), sa[1], bn[1])),
-                                   fmaxf(fmaf(byte_to_2p15(wn[2], j, magic), sa[2], bn[2]), 0.0f));
-            const float tf = fminf(fminf(fmaf(byte_to_2p15(wf[0], j, magic), sa[0], bf[0]),
-                                         fmaf(byte_to_2p15(wf[1], j, magic), sa[1], bf[1])),
-                                   fminf(fmaf(byte_to_2p15(wf[2], j, magic), sa[2], bf[2]), 1.0f));
-            if (tn <= tf && ref[j] != kNoRef) {  // (a missing child has an empty box anyway)
-                if (ref[j] < 0)
-                    leaf(~ref[j]);
-                else
-                    stack[sp++] = ref[j];
-            }
-        }
-        if (sp == 0) return;
-        node = stack[--sp];
-    }
+// intercept_count rays whose hits do not fit k_trace's kCountCap-entry list are
+// counted here, exactly and WITHOUT any host round trip (the overflow count is
+// read on the device).  One warp per overflowed segment (persistent warps):
+//
+//  * walk: the lanes share a stack in shared memory and each iteration pops up
+//    to 32 4-wide records at once (the long grazing segments that overflow
+//    are walked 32 nodes at a time); every leaf the segment enters is decided
+//    exactly (mt32 drops certain misses, the fp64 mirror settles the rest and
+//    gives the oracle's t);
+//  * windows: hits are keyed (t, leaf slot) -- a total order, ties in t broken
+//    by slot -- and a walk keeps the kRpKeep smallest keys above the previous
+//    window's last key in a per-warp shared-memory buffer (when the buffer
+//    fills it is sorted, cut to the kRpKeep smallest, and only smaller keys
+//    are accepted from then on).  A walk that never had to cut holds every
+//    remaining hit and is the last; otherwise its kRpKeep smallest are counted
+//    and the next walk starts above them.  So the count is exact for any
+//    number of hits (<= N_t), with no capacity-dependent result (unlike the
+//    paper's fixed CollisionList / InterceptDistances buffers);
+//  * count (reading R4, the oracle's single linkage): sorted by a bitonic
+//    network over the buffer, count = [nh > 0] + popc of the ballots of
+//    "gap to the previous key > tau" with the oracle's correctly rounded gap
+//    __dadd_rn(t_i, -t_(i-1)); the last t of a window carries to the next.
+//  * boxes: a record member is visited only if its conservative [tn, tf]
+//    (clamped to [0, 1]) meets [lo_t, thr_t] of the current window, rounded
+//    outward to fp32.
+//  * stack: pops are narrowed as the stack fills so that it never overflows:
+//    while top <= kRpStack - 3 * 32 - kStackQuad a pop of `take` records can
+//    push at most 3 * take more; above that, pops of 1 record continue a
+//    depth-first walk whose growth is bounded by kStackQuad (the lane-stack
+//    bound of the 4-wide walk).
+constexpr int kRpWarps = 4;     // warps per block
+constexpr int kRpStack = 1024;  // shared stack entries per warp (4 KB)
+constexpr int kRpBuf = 512;     // hit keys buffered per warp (6 KB)
+constexpr int kRpKeep = 256;    // keys kept when the buffer is cut
+static_assert(kRpStack >= kStackQuad + 3 * 32 + 32, "re-pass stack bound");
+
+__device__ __forceinline__ bool key_less(double ta, int sa, double tb, int sb) {
+    return ta < tb || (ta == tb && sa < sb);
 }
 
-// Warp-cooperative all-hits walk of ONE segment (the re-pass): the lanes share
-// a stack in shared memory and each iteration pops up to 32 records at once,
-// so the long grazing segments that overflow are walked 32 nodes at a time
-// instead of one.  Every hit's fp64 t goes to the segment's slot (any order:
-// the dedup sorts); a full slot or stack marks the segment for the exact
-// two-pass path (correct regardless).
-constexpr int kOvfSlot = 64;   // fp64 hit t values held per overflowed segment
-constexpr int kWStack = 2048;  // stack entries per warp (8 KB)
-constexpr int kOvfWarps = 4;   // warps per block
-
-__global__ void __launch_bounds__(32 * kOvfWarps) k_ovf_collect_warp(
-    const float4* __restrict__ quads, const float4* __restrict__ tris, const float* __restrict__ S,
-    const float* __restrict__ E, const int32_t* __restrict__ list, int n_ovf, int32_t* __restrict__ seg,
-    double* __restrict__ pool, int32_t* __restrict__ big, uint32_t* scratch, uint32_t magic) {
-    __shared__ int s_stack[kOvfWarps][kWStack];
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int j = blockIdx.x * kOvfWarps + w;  // warp-uniform
-    if (j >= n_ovf) return;
-    const float pmax = __uint_as_float(scratch[SCR_QPMAX]);
-    const int emin = (int)scratch[SCR_QEMIN] - 128, emax = (int)scratch[SCR_QEMAX] - 128;
-    Ray r;
-    bool nonfinite;
-    load_ray<true>(r, S, E, list[j], nonfinite, 0.25f * pmax, scalbnf(1.0f, -124 - emin),
-                   scalbnf(1.0f, 100) / (pmax + scalbnf(65536.0f, emax)));
-    double* v = pool + (size_t)j * kOvfSlot;
-    int* stk = s_stack[w];
-    const int root = (int)scratch[SCR_ROOT_NODE];
-    int top = 0;        // warp-uniform
-    int nh = 0;         // warp-uniform hit count
-    bool spill = false; // warp-uniform: slot or stack exhausted
-    if (root >= 0) {
-        if (lane == 0) stk[0] = root;
-        top = 1;
+// ascending bitonic sort of the first n keys of (t, s) (warp-cooperative;
+// entries [n, P) are padded with +inf / INT_MAX, P = pow2 >= max(n, 32))
+__device__ void warp_sort_keys(double* t, int* s, int n, int lane) {
+    int P = 32;
+    while (P < n) P <<= 1;
+    for (int i = n + lane; i < P; i += 32) {
+        t[i] = INFINITY;
+        s[i] = 0x7fffffff;
     }
     __syncwarp();
-    const float inv3[3] = {r.ix, r.iy, r.iz};
-    const uint32_t msk[3] = {r.mx, r.my, r.mz};
-    const float nof[3] = {r.lx, r.ly, r.lz};
-    const float fof[3] = {r.hx, r.hy, r.hz};
-    while (top > 0 && !spill) {
-        const int take = top < 32 ? top : 32;
-        const int node = lane < take ? stk[top - 1 - lane] : -1;
-        top -= take;
-        __syncwarp();
-        int push[4] = {kNoRef, kNoRef, kNoRef, kNoRef};
-        int leafs[4] = {kNoRef, kNoRef, kNoRef, kNoRef};
-        if (node >= 0) {
-            const float4* q = quads + 4 * node;
-            float4 qa, qb, qc, qd;
-            ldg256(q, qa, qb);
-            ldg256(q + 2, qc, qd);
-            const float pp[3] = {qa.x, qa.y, qa.z};
-            const uint32_t wq[6] = {__float_as_uint(qb.x), __float_as_uint(qb.y), __float_as_uint(qb.z),
-                                    __float_as_uint(qb.w), __float_as_uint(qc.x), __float_as_uint(qc.y)};
-            const float scv[3] = {qa.w, qd.z, qd.w};
-            float sa[3], bn[3], bf[3];
-            uint32_t wn[3], wf[3];
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                sa[a] = scv[a] * inv3[a];
-                bn[a] = fmaf(pp[a], inv3[a], -nof[a]);
-                bf[a] = fmaf(pp[a], inv3[a], -fof[a]);
-                wn[a] = (wq[2 * a] & ~msk[a]) | (wq[2 * a + 1] & msk[a]);
-                wf[a] = (wq[2 * a + 1] & ~msk[a]) | (wq[2 * a] & msk[a]);
-            }
-            const int ref[4] = {__float_as_int(qc.z), __float_as_int(qc.w), __float_as_int(qd.x),
-                                __float_as_int(qd.y)};
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const float tn = fmaxf(fmaxf(fmaf(byte_to_2p15(wn[0], c, magic), sa[0], bn[0]),
-                                             fmaf(byte_to_2p15(wn[1], c, magic), sa[1], bn[1])),
-                                       fmaxf(fmaf(byte_to_2p15(wn[2], c, magic), sa[2], bn[2]), 0.0f));
-                const float tf = fminf(fminf(fmaf(byte_to_2p15(wf[0], c, magic), sa[0], bf[0]),
-                                             fmaf(byte_to_2p15(wf[1], c, magic), sa[1], bf[1])),
-                                       fminf(fmaf(byte_to_2p15(wf[2], c, magic), sa[2], bf[2]), 1.0f));
-                if (tn <= tf && ref[c] != kNoRef) {
-                    if (ref[c] < 0)
-                        leafs[c] = ~ref[c];
-                    else
-                        push[c] = ref[c];
+    for (int k = 2; k <= P; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int x = lane; x < P / 2; x += 32) {
+                const int i = 2 * j * (x / j) + (x % j), q = i + j;
+                const bool up = (i & k) == 0;
+                const double ti = t[i], tq = t[q];
+                const int si = s[i], sq = s[q];
+                if (key_less(tq, sq, ti, si) == up) {
+                    t[i] = tq; s[i] = sq;
+                    t[q] = ti; s[q] = si;
                 }
             }
+            __syncwarp();
         }
-        // leaves: exact hit test, fp64 t into the slot (warp-aggregated index)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-            bool hit = false;
-            double t64 = 0.0;
-            if (leafs[c] != kNoRef) {
-                float4 A, B, C;
-                load_tri(tris, leafs[c], A, B, C);
-                float t32, et;
-                if (mt32(r, A, B, C, t32, et) != MT_MISS) hit = mt64(r, A, B, C, &t64) != 0;
-            }
-            const unsigned hm = __ballot_sync(FULL, hit);
-            if (hit) {
-                const int idx = nh + __popc(hm & ((1u << lane) - 1u));
-                if (idx < kOvfSlot) v[idx] = t64;
-            }
-            nh += __popc(hm);
-        }
-        // pushes: warp prefix sum of each lane's internal children
-        int np = 0;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) np += push[c] != kNoRef;
-        int incl = np;
-        for (int o = 1; o < 32; o <<= 1) {
-            const int y = __shfl_up_sync(FULL, incl, o);
-            if (lane >= o) incl += y;
-        }
-        const int total = __shfl_sync(FULL, incl, 31);
-        if (top + total > kWStack) {
-            spill = true;
-        } else {
-            int pos = top + incl - np;
-#pragma unroll
-            for (int c = 0; c < 4; ++c)
-                if (push[c] != kNoRef) stk[pos++] = push[c];
-            top += total;
-        }
-        if (nh > kOvfSlot) spill = true;
-        __syncwarp();
-    }
-    if (lane == 0) {
-        seg[2 * j] = j * kOvfSlot;
-        seg[2 * j + 1] = spill ? -1 : nh;  // -1: the two-pass path recounts it
-        if (spill) big[atomicAdd(&scratch[SCR_OVF_TOTAL], 1u)] = list[j];
     }
 }
 
-// One-traversal re-pass: each overflowed segment's exact fp64 hit t values go
-// into a fixed kOvfSlot-entry slot of a pool sized from the overflow count;
-// segments with more hits than that are listed for the two-pass path below
-// (size, then collect into an exactly-sized pool).  mt32 only drops certain
-// misses; every possible hit is settled (and its t taken) in the fp64 mirror.
-__global__ void __launch_bounds__(kThreads) k_ovf_collect_fixed(const float4* __restrict__ nodes,
-                                                                const float4* __restrict__ quads,
-                                                                const float4* __restrict__ tris,
-                                                                const float* __restrict__ S, const float* __restrict__ E,
-                                                                const int32_t* __restrict__ list, int n_ovf,
-                                                                int32_t* __restrict__ seg, double* __restrict__ pool,
-                                                                int32_t* __restrict__ big, uint32_t* scratch,
-                                                                uint32_t magic) {
-    int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n_ovf) return;
-    // the 4-wide decode's slack terms and safe |1/d| range, as in k_trace
+__global__ void __launch_bounds__(32 * kRpWarps) k_count_repass(
+    const float4* __restrict__ quads, const float4* __restrict__ tris, const float* __restrict__ S,
+    const float* __restrict__ E, const int32_t* __restrict__ list, uint32_t* scratch, double tau,
+    int32_t* __restrict__ count_out, unsigned long long* stats, uint32_t magic) {
+    __shared__ int s_stack[kRpWarps][kRpStack];
+    __shared__ double s_t[kRpWarps][kRpBuf];
+    __shared__ int s_s[kRpWarps][kRpBuf];
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned ltm = lanemask_lt();
+    const int n_ovf = (int)*(volatile uint32_t*)&scratch[SCR_OVF_COUNT];
+    if (blockIdx.x == 0 && threadIdx.x == 0 && n_ovf > 0) atomicAdd(stats + ST_OVERFLOW, (unsigned long long)n_ovf);
+    const int root = (int)scratch[SCR_ROOT_NODE];
     const float pmax = __uint_as_float(scratch[SCR_QPMAX]);
     const int emin = (int)scratch[SCR_QEMIN] - 128, emax = (int)scratch[SCR_QEMAX] - 128;
-    Ray r;
-    bool nonfinite;
-    load_ray<true>(r, S, E, list[j], nonfinite, 0.25f * pmax, scalbnf(1.0f, -124 - emin),
-                   scalbnf(1.0f, 100) / (pmax + scalbnf(65536.0f, emax)));
-    double* v = pool + (size_t)j * kOvfSlot;
-    int nh = 0;
-    auto hit = [&](int k) {
-        float4 A, B, C;
-        load_tri(tris, k, A, B, C);
-        float t32, et;
-        if (mt32(r, A, B, C, t32, et) == MT_MISS) return;
-        double t64;
-        if (mt64(r, A, B, C, &t64)) {
-            if (nh < kOvfSlot) v[nh] = t64;
-            ++nh;
-        }
-    };
-    if (RSI_ANY_QUAD) {
-        traverse_quads(quads, (int)scratch[SCR_ROOT_NODE], r, magic, hit);
-    } else {  // no 4-wide records in this build: the binary walk (plain slab offsets)
-        load_ray(r, S, E, list[j], nonfinite);
-        float tclip = 1.0f;
-        traverse(nodes, (int)scratch[SCR_ROOT_NODE], r, tclip, [&](int k) {
-            hit(k);
-            return false;
-        });
-    }
-    seg[2 * j] = j * kOvfSlot;
-    seg[2 * j + 1] = nh <= kOvfSlot ? nh : -1;  // -1: the two-pass path recounts it
-    if (nh > kOvfSlot) big[atomicAdd(&scratch[SCR_OVF_TOTAL], 1u)] = list[j];
-}
-
-// Pass A: raw hit count per overflowed ray and its segment offset in a pool.
-__global__ void __launch_bounds__(kThreads) k_ovf_size(const float4* __restrict__ nodes,
-                                                       const float4* __restrict__ tris, const float* __restrict__ S,
-                                                       const float* __restrict__ E, const int32_t* __restrict__ list,
-                                                       int n_ovf, int32_t* __restrict__ seg, uint32_t* scratch) {
-    int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n_ovf) return;
-    Ray r;
-    bool nonfinite;
-    load_ray(r, S, E, list[j], nonfinite);
-    int nh = 0;
-    float tclip = 1.0f;
-    traverse(nodes, (int)scratch[SCR_ROOT_NODE], r, tclip, [&](int k) {
-        float4 A, B, C;
-        load_tri(tris, k, A, B, C);
-        float t32, et;
-        int s = mt32(r, A, B, C, t32, et);
-        if (s == MT_HIT || (s == MT_UNSURE && mt64(r, A, B, C, nullptr))) ++nh;
-        return false;
-    });
-    seg[2 * j] = (int32_t)atomicAdd(&scratch[SCR_OVF_TOTAL], (uint32_t)nh);
-    seg[2 * j + 1] = nh;
-}
-
-// Pass B: exact fp64 t of every hit of each overflowed ray into its segment.
-__global__ void __launch_bounds__(kThreads) k_ovf_collect(const float4* __restrict__ nodes,
-                                                          const float4* __restrict__ tris, const float* __restrict__ S,
-                                                          const float* __restrict__ E, const int32_t* __restrict__ list,
-                                                          int n_ovf, const int32_t* __restrict__ seg, double* pool,
-                                                          const uint32_t* __restrict__ scratch) {
-    int j = blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= n_ovf) return;
-    Ray r;
-    bool nonfinite;
-    load_ray(r, S, E, list[j], nonfinite);
-    double* v = pool + seg[2 * j];
-    const int cap = seg[2 * j + 1];
-    int nh = 0;
-    float tclip = 1.0f;
-    traverse(nodes, (int)scratch[SCR_ROOT_NODE], r, tclip, [&](int k) {
-        float4 A, B, C;
-        load_tri(tris, k, A, B, C);
-        double t64;
-        if (mt64(r, A, B, C, &t64) && nh < cap) v[nh++] = t64;
-        return false;
-    });
-}
-
-// Pass C: one WARP per overflowed ray (north_star: warp-level ballot/shuffle
-// for the intercept_count dedup).  The segment's fp64 hit t values (<= 32 x
-// kOvfRegs) sit across the lanes' registers, element i = r * 32 + lane; a
-// bitonic network sorts them (partners within a register by shuffle-xor,
-// across registers in-lane), then count = [nh > 0] + popc of the ballots of
-// "gap to the previous element > tau" -- the oracle's single-linkage count
-// (reading R4) with the same correctly rounded gap __dadd_rn(t_i, -t_(i-1)).
-// Longer segments (never seen outside adversarial stacks) use a serial heap
-// sort in lane 0.
-constexpr int kOvfRegs = 8;  // up to 256 hits per ray in registers
-
-__device__ void heap_sort(double* v, int nh) {
-    for (int start = nh / 2 - 1; start >= 0; --start) {
-        int root = start;
-        while (2 * root + 1 < nh) {
-            int c = 2 * root + 1;
-            if (c + 1 < nh && v[c] < v[c + 1]) ++c;
-            if (v[root] < v[c]) {
-                const double x = v[root];
-                v[root] = v[c];
-                v[c] = x;
-                root = c;
-            } else {
-                break;
-            }
-        }
-    }
-    for (int end = nh - 1; end > 0; --end) {
-        const double x = v[0];
-        v[0] = v[end];
-        v[end] = x;
-        int root = 0;
-        while (2 * root + 1 < end) {
-            int c = 2 * root + 1;
-            if (c + 1 < end && v[c] < v[c + 1]) ++c;
-            if (v[root] < v[c]) {
-                const double y = v[root];
-                v[root] = v[c];
-                v[c] = y;
-                root = c;
-            } else {
-                break;
-            }
-        }
-    }
-}
-
-__global__ void __launch_bounds__(kThreads) k_ovf_dedup(const int32_t* __restrict__ list, int n_ovf,
-                                                        const int32_t* __restrict__ seg, double* pool, double tau,
-                                                        int32_t* __restrict__ count_out) {
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // warp-uniform
-    if (j >= n_ovf) return;
-    double* v = pool + seg[2 * j];
-    const int nh = seg[2 * j + 1];
-    if (nh < 0) return;  // more hits than the slot: counted by the two-pass path
-    int cnt = nh > 0 ? 1 : 0;
-    if (nh > 32 * kOvfRegs) {  // rare: serial sort in lane 0
-        if (lane == 0) {
-            heap_sort(v, nh);
-            for (int a = 0; a + 1 < nh; ++a)
-                if (da(v[a + 1], -v[a]) > tau) ++cnt;
-            count_out[list[j]] = cnt;
-        }
-        return;
-    }
-    int R = 1;  // registers in use: the power of two >= ceil(nh / 32)
-    while (32 * R < nh) R <<= 1;
-    double x[kOvfRegs];
+    int* stk = s_stack[w];
+    double* bt = s_t[w];
+    int* bs = s_s[w];
+    constexpr int kWide = kRpStack - kStackQuad - 3 * 32;  // above this top, pops of 1
+    while (true) {  // dynamic: each warp takes the next overflowed segment (long ones vary widely)
+        int j = 0;
+        if (lane == 0) j = (int)atomicAdd(&scratch[SCR_OVF_NEXT], 1u);
+        j = __shfl_sync(FULL, j, 0);
+        if (j >= n_ovf) break;
+        const int ray = list[j];
+        Ray r;
+        bool nonfinite;
+        load_ray<true>(r, S, E, ray, nonfinite, 0.25f * pmax, scalbnf(1.0f, -124 - emin),
+                       scalbnf(1.0f, 100) / (pmax + scalbnf(65536.0f, emax)));
+        const float inv3[3] = {r.ix, r.iy, r.iz};
+        const uint32_t msk[3] = {r.mx, r.my, r.mz};
+        const float nof[3] = {r.lx, r.ly, r.lz};
+        const float fof[3] = {r.hx, r.hy, r.hz};
+        double lo_t = -INFINITY;  // window: keys > (lo_t, lo_s)
+        int lo_s = -1;
+        bool has_prev = false;    // a hit was counted in an earlier window
+        double prev_t = 0.0;
+        int cnt = 0;
+        bool more = root >= 0;
+        while (more) {  // one walk per window
+            double thr_t = INFINITY;  // keys < (thr_t, thr_s) once the buffer was cut
+            int thr_s = 0x7fffffff;
+            bool cut = false;
+            int nbuf = 0, top = 0;
+            if (lane == 0) stk[0] = root;
+            top = 1;
+            __syncwarp();
+            const float lo_f = lo_t == -INFINITY ? -INFINITY : __double2float_rd(lo_t);
+            while (top > 0) {
+                float thr_f = thr_t == INFINITY ? INFINITY : __double2float_ru(thr_t);
+                int take = top < 32 ? top : 32;
+                if (top > kWide) take = 1;
+                else if (take > (kWide - top) / 3 + 1) take = (kWide - top) / 3 + 1;
+                const int node = lane < take ? stk[top - 1 - lane] : -1;
+                top -= take;
+                __syncwarp();
+                int push[4] = {kNoRef, kNoRef, kNoRef, kNoRef};
+                int leafs[4] = {kNoRef, kNoRef, kNoRef, kNoRef};
+                if (node >= 0) {
+                    const float4* q = quads + 4 * node;
+                    float4 qa, qb, qc, qd;
+                    ldg256(q, qa, qb);
+                    ldg256(q + 2, qc, qd);
+                    const float pp[3] = {qa.x, qa.y, qa.z};
+                    const uint32_t wq[6] = {__float_as_uint(qb.x), __float_as_uint(qb.y), __float_as_uint(qb.z),
+                                            __float_as_uint(qb.w), __float_as_uint(qc.x), __float_as_uint(qc.y)};
+                    const float scv[3] = {qa.w, qd.z, qd.w};
+                    float sa[3], bn[3], bf[3];
+                    uint32_t wn[3], wf[3];
 #pragma unroll
-    for (int q = 0; q < kOvfRegs; ++q) {
-        const int i = q * 32 + lane;
-        x[q] = (q < R && i < nh) ? v[i] : INFINITY;  // pad: sorts last, never counted
-    }
-    const int n = 32 * R;
-    for (int k = 2; k <= n; k <<= 1) {
-        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+                    for (int a = 0; a < 3; ++a) {
+                        sa[a] = scv[a] * inv3[a];
+                        bn[a] = fmaf(pp[a], inv3[a], -nof[a]);
+                        bf[a] = fmaf(pp[a], inv3[a], -fof[a]);
+                        wn[a] = (wq[2 * a] & ~msk[a]) | (wq[2 * a + 1] & msk[a]);
+                        wf[a] = (wq[2 * a + 1] & ~msk[a]) | (wq[2 * a] & msk[a]);
+                    }
+                    const int ref[4] = {__float_as_int(qc.z), __float_as_int(qc.w), __float_as_int(qd.x),
+                                        __float_as_int(qd.y)};
 #pragma unroll
-            for (int q = 0; q < kOvfRegs; ++q) {
-                if (q >= R) break;
-                const int i = q * 32 + lane;
-                const bool up = (i & k) == 0;  // ascending block
-                if (jj < 32) {
-                    const double o = __shfl_xor_sync(FULL, x[q], jj);
-                    const bool lower = (lane & jj) == 0;
-                    // keep the min on the lower index of an ascending block
-                    x[q] = (lower == up) ? fmin(x[q], o) : fmax(x[q], o);
-                } else {
-                    const int qp = q ^ (jj >> 5);
-                    if (qp > q) {
-                        const double a0 = x[q], a1 = x[qp];
-                        const double lo = fmin(a0, a1), hi = fmax(a0, a1);
-                        x[q] = up ? lo : hi;
-                        x[qp] = up ? hi : lo;
+                    for (int c = 0; c < 4; ++c) {
+                        const float tn = fmaxf(fmaxf(fmaf(byte_to_2p15(wn[0], c, magic), sa[0], bn[0]),
+                                                     fmaf(byte_to_2p15(wn[1], c, magic), sa[1], bn[1])),
+                                               fmaxf(fmaf(byte_to_2p15(wn[2], c, magic), sa[2], bn[2]), 0.0f));
+                        const float tf = fminf(fminf(fmaf(byte_to_2p15(wf[0], c, magic), sa[0], bf[0]),
+                                                     fmaf(byte_to_2p15(wf[1], c, magic), sa[1], bf[1])),
+                                               fminf(fmaf(byte_to_2p15(wf[2], c, magic), sa[2], bf[2]), 1.0f));
+                        if (tn <= tf && tf >= lo_f && tn <= thr_f && ref[c] != kNoRef) {
+                            if (ref[c] < 0)
+                                leafs[c] = ~ref[c];
+                            else
+                                push[c] = ref[c];
+                        }
                     }
                 }
-            }
-        }
-    }
-    // count the gaps: element i > 0 against element i - 1
+                // leaves: exact decision, key (t, slot) into the window buffer
 #pragma unroll
-    for (int q = 0; q < kOvfRegs; ++q) {
-        if (q >= R) break;
-        const double up1 = __shfl_up_sync(FULL, x[q], 1);
-        const double last = q > 0 ? __shfl_sync(FULL, x[q > 0 ? q - 1 : 0], 31) : 0.0;
-        const double prev = lane > 0 ? up1 : last;
-        const int i = q * 32 + lane;
-        const bool gap = i > 0 && i < nh && da(x[q], -prev) > tau;
-        cnt += __popc(__ballot_sync(FULL, gap));
+                for (int c = 0; c < 4; ++c) {
+                    bool acc = false;
+                    double t64 = 0.0;
+                    if (leafs[c] != kNoRef) {
+                        float4 A, B, C;
+                        load_tri(tris, leafs[c], A, B, C);
+                        float t32, et;
+                        if (mt32(r, A, B, C, t32, et) != MT_MISS && mt64(r, A, B, C, &t64))
+                            acc = key_less(lo_t, lo_s, t64, leafs[c]) && key_less(t64, leafs[c], thr_t, thr_s);
+                    }
+                    const unsigned am = __ballot_sync(FULL, acc);
+                    if (am == 0) continue;
+                    if (nbuf + __popc(am) > kRpBuf) {  // cut: keep the kRpKeep smallest keys
+                        warp_sort_keys(bt, bs, nbuf, lane);
+                        nbuf = kRpKeep;
+                        thr_t = bt[kRpKeep - 1];
+                        thr_s = bs[kRpKeep - 1];
+                        cut = true;
+                        __syncwarp();
+                        acc = acc && key_less(t64, leafs[c], thr_t, thr_s);
+                    }
+                    const unsigned am2 = __ballot_sync(FULL, acc);
+                    if (acc) {
+                        const int pos = nbuf + __popc(am2 & ltm);
+                        bt[pos] = t64;
+                        bs[pos] = leafs[c];
+                    }
+                    nbuf += __popc(am2);
+                    __syncwarp();
+                }
+                // pushes: warp prefix sum of each lane's internal members
+                int np = 0;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) np += push[c] != kNoRef;
+                int incl = np;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(FULL, incl, o);
+                    if (lane >= o) incl += y;
+                }
+                int pos = top + incl - np;
+#pragma unroll
+                for (int c = 0; c < 4; ++c)
+                    if (push[c] != kNoRef) stk[pos++] = push[c];
+                top += __shfl_sync(FULL, incl, 31);
+                __syncwarp();
+            }
+            const int m = cut ? kRpKeep : nbuf;
+            if (m <= 32) {  // the common case: one key per lane, shuffle bitonic sort in registers
+                double tk = lane < m ? bt[lane] : INFINITY;
+                int sk = lane < m ? bs[lane] : 0x7fffffff;
+                for (int k = 2; k <= 32; k <<= 1)
+                    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+                        const double to = __shfl_xor_sync(FULL, tk, jj);
+                        const int so = __shfl_xor_sync(FULL, sk, jj);
+                        const bool lower = (lane & jj) == 0, up = (lane & k) == 0;
+                        // keep the smaller key on the lower lane of an ascending block
+                        const bool take = (lower == up) ? key_less(to, so, tk, sk) : key_less(tk, sk, to, so);
+                        if (take) {
+                            tk = to;
+                            sk = so;
+                        }
+                    }
+                const double tp = __shfl_up_sync(FULL, tk, 1);
+                bool gap = false;
+                if (lane < m) gap = lane > 0 ? da(tk, -tp) > tau : (!has_prev || da(tk, -prev_t) > tau);
+                cnt += __popc(__ballot_sync(FULL, gap));
+                if (m > 0) {
+                    has_prev = true;
+                    prev_t = __shfl_sync(FULL, tk, m - 1);
+                }
+                more = false;  // m <= 32 < kRpKeep: this walk never cut
+                __syncwarp();
+                continue;
+            }
+            // the window's keys, ascending; a walk that never cut holds them all
+            warp_sort_keys(bt, bs, nbuf, lane);
+            for (int base = 0; base < m; base += 32) {
+                const int i = base + lane;
+                bool gap = false;
+                if (i < m) {
+                    const double ti = bt[i];
+                    if (i > 0) gap = da(ti, -bt[i - 1]) > tau;
+                    else gap = !has_prev || da(ti, -prev_t) > tau;  // first hit overall starts a cluster
+                }
+                cnt += __popc(__ballot_sync(FULL, gap));
+            }
+            if (m > 0) {
+                has_prev = true;
+                prev_t = bt[m - 1];
+                lo_t = bt[m - 1];
+                lo_s = bs[m - 1];
+            }
+            more = cut;
+            __syncwarp();
+        }
+        if (lane == 0) count_out[ray] = cnt;
     }
-    if (lane == 0) count_out[list[j]] = cnt;
 }
 
 // ---------------------------------------------------------------- ordered compaction (3a)
@@ -1864,9 +1686,6 @@ static void launch_mode(int32_t mode, const TraceParams& p, cudaStream_t s) {
         launch_trace<MODE_COUNT, kFP64, kCounters>(p, s);
 }
 
-static rsi_status_t rsi_exact_repass(rsi_bvh* h, const float* S, const float* E, const int32_t* big, int n_big,
-                                     const rsi_outputs_t* out, cudaStream_t s);
-
 rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, int64_t n, int32_t mode,
                                   const rsi_outputs_t* out, cudaStream_t s) {
     if (n == 0) return RSI_OK;
@@ -1918,92 +1737,24 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     if (st != RSI_OK) return st;
     if (mode != RSI_MODE_INTERCEPT_COUNT) return RSI_OK;
 
-    // intercept_count: exact re-pass for rays that overflowed the register list
-    st = rsi_cuda_check(cudaMemcpyAsync(h->h_words, h->scratch + SCR_OVF_COUNT, sizeof(uint32_t),
-                                        cudaMemcpyDeviceToHost, s), "overflow count");
-    if (st != RSI_OK) return st;
-    st = rsi_cuda_check(cudaStreamSynchronize(s), "intercept_count");
-    if (st != RSI_OK) return st;
-    const int n_ovf = (int)h->h_words[0];
-    if (n_ovf == 0) return RSI_OK;
-    // one traversal per overflowed segment into a fixed-slot pool (at most
-    // 2^20 segments at a time, 512 MB), warp-per-segment dedup
-    if (n_ovf > (1 << 20)) {
-        h->host_overflow += (uint64_t)n_ovf;
-        return rsi_exact_repass(h, S, E, h->ovf_list, n_ovf, out, s);
+    // intercept_count: the exact re-pass for rays that overflowed the register
+    // list.  Always launched (a persistent grid; every warp reads the overflow
+    // count on the device and exits at once when it is 0): no host read-back.
+    static int rp_grid = 0;
+    if (rp_grid == 0) {
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_count_repass, 32 * kRpWarps, 0);
+        rp_grid = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
     }
-    int32_t* seg = nullptr;
-    double* pool = nullptr;
-    int32_t* big = nullptr;
-    st = rsi_cuda_check(cudaMallocAsync((void**)&seg, (size_t)n_ovf * 2 * sizeof(int32_t), s), "overflow segs");
-    if (st == RSI_OK)
-        st = rsi_cuda_check(cudaMallocAsync((void**)&pool, (size_t)n_ovf * kOvfSlot * sizeof(double), s), "overflow pool");
-    if (st == RSI_OK) st = rsi_cuda_check(cudaMallocAsync((void**)&big, (size_t)n_ovf * sizeof(int32_t), s), "overflow list");
-    auto release = [&]() {
-        if (seg) cudaFreeAsync(seg, s);
-        if (pool) cudaFreeAsync(pool, s);
-        if (big) cudaFreeAsync(big, s);
-    };
-    if (st != RSI_OK) {
-        release();
-        return RSI_E_OOM;
-    }
-    const int nb = rsi_ceil_div(n_ovf, kThreads);
-    if (RSI_ANY_QUAD)  // one warp per overflowed segment over the 4-wide records
-        rsi_note_launch(), k_ovf_collect_warp<<<rsi_ceil_div(n_ovf, kOvfWarps), 32 * kOvfWarps, 0, s>>>(
-            h->quads, h->tris, S, E, h->ovf_list, n_ovf, seg, pool, big, h->scratch, kQuadMagic);
-    else
-        rsi_note_launch(), k_ovf_collect_fixed<<<nb, kThreads, 0, s>>>(h->nodes, h->quads, h->tris, S, E, h->ovf_list,
-                                                                       n_ovf, seg, pool, big, h->scratch, kQuadMagic);
-    rsi_note_launch(), k_ovf_dedup<<<rsi_ceil_div((int64_t)n_ovf * 32, kThreads), kThreads, 0, s>>>(
-        h->ovf_list, n_ovf, seg, pool, h->opt.dedup_tau, out->count);
-    st = rsi_cuda_check(cudaMemcpyAsync(h->h_words, h->scratch + SCR_OVF_TOTAL, sizeof(uint32_t),
-                                        cudaMemcpyDeviceToHost, s), "overflow count");
-    if (st == RSI_OK) st = rsi_cuda_check(cudaStreamSynchronize(s), "overflow pass");
-    h->host_overflow += (uint64_t)n_ovf;
-    const int n_big = st == RSI_OK ? (int)h->h_words[0] : 0;
-    if (st != RSI_OK || n_big == 0) {
-        release();
-        return st;
-    }
-    // rare: segments with more than kOvfSlot hits -- size, then collect exactly
-    st = rsi_exact_repass(h, S, E, big, n_big, out, s);
-    release();
-    return st;
+    rsi_note_launch(), k_count_repass<<<rp_grid, 32 * kRpWarps, 0, s>>>(h->quads, h->tris, S, E, h->ovf_list,
+                                                                       h->scratch, h->opt.dedup_tau, out->count,
+                                                                       h->stats, kQuadMagic);
+    return rsi_cuda_check(cudaGetLastError(), "count re-pass launch");
 }
 
-// Exact two-pass re-pass for a list of segments: raw hit counts (one atomic
-// per segment sizes an exact pool), the fp64 t of every hit, warp dedup.
-static rsi_status_t rsi_exact_repass(rsi_bvh* h, const float* S, const float* E, const int32_t* big, int n_big,
-                                     const rsi_outputs_t* out, cudaStream_t s) {
-    rsi_status_t st = rsi_cuda_check(cudaMemsetAsync(h->scratch + SCR_OVF_TOTAL, 0, sizeof(uint32_t), s), "memset");
-    int32_t* seg2 = nullptr;
-    double* pool2 = nullptr;
-    if (st == RSI_OK)
-        st = rsi_cuda_check(cudaMallocAsync((void**)&seg2, (size_t)n_big * 2 * sizeof(int32_t), s), "overflow segs");
-    const int nb2 = rsi_ceil_div(n_big, kThreads);
-    if (st == RSI_OK) {
-        rsi_note_launch(), k_ovf_size<<<nb2, kThreads, 0, s>>>(h->nodes, h->tris, S, E, big, n_big, seg2, h->scratch);
-        st = rsi_cuda_check(cudaMemcpyAsync(h->h_words, h->scratch + SCR_OVF_TOTAL, sizeof(uint32_t),
-                                            cudaMemcpyDeviceToHost, s), "overflow total");
-    }
-    if (st == RSI_OK) st = rsi_cuda_check(cudaStreamSynchronize(s), "overflow sizing");
-    const size_t total = st == RSI_OK ? h->h_words[0] : 0;
-    if (st == RSI_OK)
-        st = rsi_cuda_check(cudaMallocAsync((void**)&pool2, (total ? total : 1) * sizeof(double), s), "overflow pool");
-    if (st == RSI_OK) {
-        rsi_note_launch(), k_ovf_collect<<<nb2, kThreads, 0, s>>>(h->nodes, h->tris, S, E, big, n_big, seg2, pool2,
-                                                                  h->scratch);
-        rsi_note_launch(), k_ovf_dedup<<<rsi_ceil_div((int64_t)n_big * 32, kThreads), kThreads, 0, s>>>(
-            big, n_big, seg2, pool2, h->opt.dedup_tau, out->count);
-        st = rsi_cuda_check(cudaGetLastError(), "overflow pass");
-    }
-    if (seg2) cudaFreeAsync(seg2, s);
-    if (pool2) cudaFreeAsync(pool2, s);
-    return st;
-}
-
-bool rsi_uses_quads() { return RSI_ANY_QUAD; }
+bool rsi_uses_quads() { return true; }  // the intercept_count re-pass walks the 4-wide records
 
 rsi_status_t rsi_compact_device(const int32_t* tri, int64_t n, int32_t* ids, int32_t* d_n, cudaStream_t s) {
     if (n == 0) return rsi_cuda_check(cudaMemsetAsync(d_n, 0, sizeof(int32_t), s), "memset");

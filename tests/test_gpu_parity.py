@@ -540,10 +540,8 @@ def test_launch_counter(rsi):
         # + the re-pass kernels when some segment overflowed the count list
         # (one-traversal pass + dedup; + size / collect / dedup beyond 64 hits)
         launched = rsi.rsi_launch_count() - before
-        if rsi.rsi_get_stats(h)["overflow_rays"] > ovf0:
-            assert launched in (3, 6), (mode, launched)
-        else:
-            assert launched == 1, (mode, launched)
+        # intercept_count always enqueues its exact re-pass (no host read-back of the overflow count)
+        assert launched == (2 if mode == "intercept_count" else 1), (mode, launched)
     c2 = rsi.rsi_launch_count()
     rsi.rsi_rebuild(h, Vd, Td)
     assert rsi.rsi_launch_count() - c2 == c1 - c0
@@ -690,21 +688,32 @@ def test_apetrei_sort_full_low_words(rsi):
     assert (d["leaf_tri"] == order).all()
 
 
-@pytest.mark.parametrize("n_sheets", [40, 100, 256, 300])
+@pytest.mark.parametrize("n_sheets", [40, 100, 256, 300, 700, 1500, "coincident"])
 def test_overflow_warp_dedup(rsi, n_sheets):
-    """Rays crossing up to 300 stacked sheets overflow the 4-entry hit list:
-    the re-pass collects every hit's fp64 t and one warp per ray sorts them with
-    a shuffle bitonic network and counts gaps by ballot (> 256 hits: serial heap
-    sort).  Sheets come in groups whose members are 1e-7 apart in z (merged by
-    tau) and groups 0.004 apart (distinct): counts equal the oracle's exactly."""
+    """Rays crossing up to 1500 stacked sheets overflow the 4-entry hit list:
+    the re-pass (k_count_repass) takes every hit's fp64 t, one warp per ray
+    sorts the keys (t, slot) and counts gaps by ballot; more than 512 hits
+    take several windows of 256 keys (700, 1500 sheets), with the last t
+    carried across windows.  Sheets come in groups whose members are 1e-7
+    apart in z (merged by tau) and groups 0.004 apart (distinct);
+    "coincident": 600 copies of one sheet (t ties across a window boundary)
+    between distinct sheets.  Counts equal the oracle's exactly."""
     base = np.float32([[-1, -1, 0], [3, -1, 0], [-1, 3, 0]])
     Vs, z = [], 1.0
-    for k in range(n_sheets):
+    if n_sheets == "coincident":
+        for k in range(5):
+            Vs.append(base + np.float32([0, 0, 1.0 + 0.01 * k]))
+        for k in range(600):
+            Vs.append(base + np.float32([0, 0, 1.1]))
+        for k in range(5):
+            Vs.append(base + np.float32([0, 0, 1.2 + 0.01 * k]))
+        z = 1.3
+    for k in range(n_sheets if isinstance(n_sheets, int) else 0):
         z += 1e-7 if k % 3 else 0.004
         Vs.append(base + np.float32([0, 0, z]))
     V = np.vstack(Vs).astype(np.float32)
     T = np.arange(len(V), dtype=np.int32).reshape(-1, 3)
-    rng = np.random.default_rng(n_sheets)
+    rng = np.random.default_rng(n_sheets if isinstance(n_sheets, int) else 7)
     S = np.column_stack([rng.uniform(0, 1, 400), rng.uniform(0, 1, 400), np.full(400, 0.5)]).astype(np.float32)
     E = S.copy()
     E[:, 2] = np.float32(z + 0.5)

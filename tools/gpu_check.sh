@@ -1,0 +1,15 @@
+#!/bin/bash
+# GPU-box helper: build, GPU tests, smoke, the default bench line, and a
+# world-2 torchrun dry run on the single GPU (gloo gather; never a number).
+# Usage (under gpurun): bash tools/gpu_check.sh <tag>
+tag=${1:-r2}
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_${tag}.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/pytest_gpu_${tag}.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_gpu_${tag}.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_${tag}.log 2>&1
+timeout 900 python bench.py > gpurun_out/bench_${tag}.json 2> gpurun_out/bench_${tag}.err
+RSI_BENCH_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 \
+  --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 3 --warmup 3 --no-configs \
+  > gpurun_out/torchrun_w2_${tag}.json 2> gpurun_out/torchrun_w2_${tag}.err
+tail -3 gpurun_out/pytest_gpu_${tag}.log

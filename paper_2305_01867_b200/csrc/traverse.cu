@@ -7,8 +7,8 @@
 // slab-tests its children conservatively, orders the hit ones near-first,
 // keeps the next on a branch-free local stack (<= 288 entries: depth <= 95)
 // and queues leaves for a warp-wide Moller-Trumbore phase.  The binary
-// child-pair walk (RSI_*_QUAD=0) remains a build switch and is what the exact
-// intercept_count re-pass uses.
+// child-pair walk (RSI_*_QUAD=0) remains a build switch; the exact
+// intercept_count re-pass (k_count_repass) walks the 4-wide records.
 //
 // Exactness.  Every discrete decision -- hit / miss,
 // nearest-hit order, dedup merge -- is taken in fp32 only when a forward error
@@ -380,6 +380,28 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
+// L2 cache policy for the barycentric output stores (RSI_OUT_HINT: 1 evict_last,
+// 2 evict_unchanged, 3 evict_first, 0 none).  Measured (sphere, 1e7): DRAM
+// bytes per launch 975 / 820 / 944 / 847 MB for none / 1 / 2 / 3; time
+// 2.358 / 2.332 / 2.332 / 2.336 ms.
+#ifndef RSI_OUT_HINT
+#define RSI_OUT_HINT 1
+#endif
+__device__ __forceinline__ uint64_t out_policy() {
+    uint64_t pol = 0;
+#if RSI_OUT_HINT == 1
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+#elif RSI_OUT_HINT == 2
+    asm("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(pol));
+#elif RSI_OUT_HINT == 3
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#endif
+    return pol;
+}
+__device__ __forceinline__ void st_hint(float* ptr, float v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(ptr), "f"(v), "l"(pol) : "memory");
+}
+
 // ---------------------------------------------------------------- per-mode ray state
 // Each mode keeps its per-ray result state; leaf() returns true when the ray
 // can stop (boolean any-hit, intercept_count register overflow).
@@ -506,7 +528,12 @@ struct ModeState<MODE_BARY> {
         }
         return false;
     }
-    __device__ __forceinline__ void finish(const TraceParams& p, const Ray& r, int64_t i, Stats& st) {
+    // the ray's outputs (tri id, t, dist = t |d|, point = O + t d; 3b/3d,
+    // P:166-168) into tri[0], t[0], dist[0], point[0..2] -- the caller's arrays
+    // at the ray's row, or its warp's shared-memory staging rows
+    // (RSI_BARY_STAGE); t / dist / point may be null
+    __device__ __forceinline__ void emit(const TraceParams& p, const Ray& r, Stats& st, int32_t* tri, float* t,
+                                         float* dist, float* point) {
         if (slot >= 0) {
             const int k = leaf_slot();
             float4 bA, bB, bC;
@@ -522,26 +549,90 @@ struct ModeState<MODE_BARY> {
                 tt = (float)v;
                 st.add(ST_FP64_RAYS);
             }
-            p.tri[i] = __float_as_int(bA.w);
-            if (p.t) p.t[i] = tt;
-            if (p.dist) p.dist[i] = tt * norm3df(r.dx, r.dy, r.dz);  // no overflow / underflow of |d|^2
-            if (p.point) {
-                p.point[3 * i] = fmaf(tt, r.dx, r.ox);
-                p.point[3 * i + 1] = fmaf(tt, r.dy, r.oy);
-                p.point[3 * i + 2] = fmaf(tt, r.dz, r.oz);
+            tri[0] = __float_as_int(bA.w);
+            if (t) t[0] = tt;
+            if (dist) dist[0] = tt * norm3df(r.dx, r.dy, r.dz);  // no overflow / underflow of |d|^2
+            if (point) {
+                point[0] = fmaf(tt, r.dx, r.ox);
+                point[1] = fmaf(tt, r.dy, r.oy);
+                point[2] = fmaf(tt, r.dz, r.oz);
             }
         } else {
-            p.tri[i] = -1;
-            if (p.t) p.t[i] = NAN;
-            if (p.dist) p.dist[i] = NAN;
-            if (p.point) {
-                p.point[3 * i] = NAN;
-                p.point[3 * i + 1] = NAN;
-                p.point[3 * i + 2] = NAN;
+            tri[0] = -1;
+            if (t) t[0] = NAN;
+            if (dist) dist[0] = NAN;
+            if (point) {
+                point[0] = NAN;
+                point[1] = NAN;
+                point[2] = NAN;
             }
         }
     }
+    __device__ __forceinline__ void finish(const TraceParams& p, const Ray& r, int64_t i, Stats& st) {
+#if RSI_OUT_HINT
+        // direct stores with an L2 eviction-priority hint: the rows of a 32-byte
+        // sector arrive from different lanes at different times
+        int32_t tri;
+        float tt, dd, pt[3];
+        emit(p, r, st, &tri, &tt, &dd, pt);
+        const uint64_t pol = out_policy();
+        st_hint(reinterpret_cast<float*>(p.tri + i), __int_as_float(tri), pol);
+        if (p.t) st_hint(p.t + i, tt, pol);
+        if (p.dist) st_hint(p.dist + i, dd, pol);
+        if (p.point) {
+            st_hint(p.point + 3 * i, pt[0], pol);
+            st_hint(p.point + 3 * i + 1, pt[1], pol);
+            st_hint(p.point + 3 * i + 2, pt[2], pol);
+        }
+#else
+        emit(p, r, st, p.tri + i, p.t ? p.t + i : nullptr, p.dist ? p.dist + i : nullptr,
+             p.point ? p.point + 3 * i : nullptr);
+#endif
+    }
 };
+
+// Barycentric output staging (RSI_BARY_STAGE).  Finished segments leave the
+// persistent refill in random order, so per-segment stores of 4-12 bytes
+// would hit each 32-byte sector of tri / t / dist / point many times apart
+// (ncu, round 1: 1.88x the algorithmic DRAM bytes, read-modify-write of
+// partial sectors).  Each warp instead stages the outputs of its two most
+// recent kChunk-segment chunks in shared memory (slot = chunk index & 1) and
+// writes a slot out with full coalesced lines when the slot is taken by a
+// newer chunk (and at the end).  A segment still running then -- a straggler
+// whose chunk already left the slot -- stores directly; rows not yet written
+// hold the sentinel tri = kUnset and are skipped by the flush.
+// Measured (sphere, 1e7 segments, B200): DRAM bytes per launch 975 -> 607 MB,
+// but the launch is 9 % SLOWER (2.34 -> 2.57 ms; 6 KB per CTA without points:
+// +9 %, 32-segment chunks: +5 %): the staging memory comes out of the L1
+// carveout the tree fetches live in.  Off; the default stores directly with
+// an L2 evict_last hint (RSI_OUT_HINT), which keeps partially written output
+// sectors in L2 longer: 975 -> 820 MB and -1 %.
+#ifndef RSI_BARY_STAGE
+#define RSI_BARY_STAGE 0
+#endif
+#ifndef RSI_STAGE_POINT
+#define RSI_STAGE_POINT 1  // 0: points are stored directly (half the staging memory)
+#endif
+constexpr int kStageWords = (RSI_STAGE_POINT ? 6 : 3) * kChunk;  // per slot: tri, t, dist [kChunk] (+ point [3 kChunk])
+constexpr int kUnset = (int)0x80000001;                            // staged row not written
+
+__device__ __forceinline__ void stage_flush(const TraceParams& p, float* sb, int b, int len, int lane) {
+    for (int k = lane; k < len; k += 32) {
+        const int tri = __float_as_int(sb[k]);
+        if (tri != kUnset) {
+            p.tri[b + k] = tri;
+            if (p.t) p.t[b + k] = sb[kChunk + k];
+            if (p.dist) p.dist[b + k] = sb[2 * kChunk + k];
+        }
+    }
+    if (RSI_STAGE_POINT && p.point) {
+        for (int f = lane; f < 3 * len; f += 32)
+            if (__float_as_int(sb[f / 3]) != kUnset) p.point[3 * (int64_t)b + f] = sb[3 * kChunk + f];
+    }
+    __syncwarp();
+    for (int k = lane; k < kChunk; k += 32) sb[k] = __int_as_float(kUnset);
+    __syncwarp();
+}
 
 // intercept_count: count = number of single-linkage clusters of hit t with
 // threshold tau (reading R4): 1 + #{sorted gaps > tau}.  The fp32 path is used
@@ -891,6 +982,16 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
     stk.s = s_stack + threadIdx.x;
     float tclip = 1.0f;
     ModeState<MODE> ms;
+    constexpr bool kStage = MODE == MODE_BARY && RSI_BARY_STAGE;
+    __shared__ float s_stage[kStage ? (kT / 32) * 2 * kStageWords : 1];
+    __shared__ int s_own[kStage ? kT / 32 : 1][2];  // chunk base held by each slot (-1: none)
+    float* stg = s_stage + (kStage ? (threadIdx.x >> 5) * 2 * kStageWords : 0);
+    int* own = s_own[kStage ? threadIdx.x >> 5 : 0];
+    if (kStage) {
+        for (int k = lane; k < 2 * kChunk; k += 32) stg[(k / kChunk) * kStageWords + k % kChunk] = __int_as_float(kUnset);
+        if (lane < 2) own[lane] = -1;
+        __syncwarp();
+    }
     if constexpr (MODE == MODE_COUNT) {
         ms.stride = kT;
         ms.te = s_te + threadIdx.x;
@@ -940,6 +1041,13 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
                 }
                 cnext = (int)base;
                 cend = min(cnext + kChunk, n32);
+                if (kStage) {  // the chunk's staging slot: write out the older chunk it held
+                    const int sl = (cnext / kChunk) & 1;
+                    const int ob = own[sl];
+                    if (ob >= 0) stage_flush(p, stg + sl * kStageWords, ob, min(kChunk, n32 - ob), lane);
+                    if (lane == 0) own[sl] = cnext;
+                    __syncwarp();
+                }
             }
             const int take = min(__popc(want), cend - cnext);
             const bool mine = (want >> lane) & 1u;
@@ -1265,9 +1373,26 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
 
         // ---- 4. finish
         if (ray >= 0 && node < 0 && l0 < 0) {
-            ms.finish(p, r, ray, st);
+            if constexpr (kStage) {
+                const int sl = (ray / kChunk) & 1, k = ray % kChunk;
+                if (own[sl] == ray - k) {  // staged (else a straggler: direct stores)
+                    float* sb = stg + sl * kStageWords;
+                    ms.emit(p, r, st, reinterpret_cast<int32_t*>(sb + k), sb + kChunk + k, sb + 2 * kChunk + k,
+                            RSI_STAGE_POINT ? sb + 3 * kChunk + 3 * k
+                                            : (p.point ? p.point + 3 * (int64_t)ray : nullptr));
+                } else {
+                    ms.finish(p, r, ray, st);
+                }
+            } else {
+                ms.finish(p, r, ray, st);
+            }
             ray = -1;
         }
+    }
+    if (kStage) {  // every segment is done: write out what is left staged
+        __syncwarp();
+        for (int sl = 0; sl < 2; ++sl)
+            if (own[sl] >= 0) stage_flush(p, stg + sl * kStageWords, own[sl], min(kChunk, n32 - own[sl]), lane);
     }
     if (kCounters) {
         st.add(ST_BOX_TESTS, st.boxes);

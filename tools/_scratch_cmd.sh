@@ -1,6 +1,7 @@
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_b.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -p no:cacheprovider -k "overflow or launch_counter or stacked or terrain or sphere_all or dedup or fuzz or chain" > gpurun_out/pt_b.log 2>&1
-echo "exit $?" >> gpurun_out/pt_b.log
-timeout 600 python bench.py --mode intercept_count --no-configs --no-cpu-baseline --no-e2e --no-extra-modes > gpurun_out/bench_b.json 2> gpurun_out/bench_b.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_b.csv python bench.py --mode intercept_count --steps 2 --warmup 3 --no-configs --no-cpu-baseline --no-e2e --no-extra-modes > /dev/null 2>&1
-tail -3 gpurun_out/pt_b.log
+for v in base nopt c32 hint1; do
+RSI_LIB=paper_2305_01867_b200/lib/librsi_$v.so timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "sphere or terrain or vertices or stacked or single or fuzz or compaction or sparse or bench_size" 2>&1 | tail -1 | sed "s/^/[$v parity] /"
+for wl in sphere paper_terrain; do
+RSI_LIB=paper_2305_01867_b200/lib/librsi_$v.so WL=$wl timeout 300 python tools/sweep.py 2>&1 | grep "bary.*ms" | sed "s/^/[$v $wl] /"
+done
+RSI_LIB=paper_2305_01867_b200/lib/librsi_$v.so timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:k_trace -c 1 --csv --log-file gpurun_out/dram_$v.csv python bench.py --mode barycentric --steps 1 --warmup 3 --no-configs --no-cpu-baseline --no-e2e --no-extra-modes --rays-per-gpu 10000000 > /dev/null 2>&1
+done

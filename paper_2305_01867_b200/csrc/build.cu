@@ -907,12 +907,14 @@ __global__ void __launch_bounds__(kBlock) k_apetrei(const float* __restrict__ V,
 }
 
 // ------------------------------------------------------------------ top-of-tree image (shared-memory cache)
-// The top levels of the tree (whole levels, breadth-first, at most kTopNodes
-// nodes) are copied into a separate image whose child refs point at image
-// slots (kSmemRef + slot) when the child is cached too.  The traversal kernel
-// loads the image into shared memory once per CTA, so the node fetches every
-// segment makes near the root are conflict-light shared-memory reads instead
-// of one L1 wavefront per lane.  One CTA, level-synchronous.
+// north_star: "the top tree levels staged in shared memory".  The first
+// kQTop 4-wide records the walk meets -- breadth-first from the root, the
+// last level possibly in part -- are copied into a separate image in which a
+// member that is itself cached points at its image slot (kSmemRef + slot);
+// every other ref is unchanged, so a walk leaves the image for the global
+// records exactly where the image ends.  k_trace loads the image into shared
+// memory once per CTA.  One CTA, level-synchronous (a level is <= 4x the
+// previous one, and kQTop <= 256 = blockDim).
 __device__ int block_exclusive_scan(int v, int* s_warp, int& total) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     int inc = v;
@@ -939,59 +941,66 @@ __device__ int block_exclusive_scan(int v, int* s_warp, int& total) {
     return r;
 }
 
-__global__ void __launch_bounds__(1024) k_topk(const float4* __restrict__ nodes, int n_nodes, float4* __restrict__ image,
-                                               uint32_t* scratch) {
-    __shared__ int old_of[kTopNodes > 0 ? kTopNodes : 1];
-    __shared__ int first_child[kTopNodes > 0 ? kTopNodes : 1];
+__global__ void __launch_bounds__(256) k_qtop(const float4* __restrict__ quads, float4* __restrict__ image,
+                                              uint32_t* scratch) {
+    __shared__ int old_of[kQTop > 0 ? kQTop : 1];
+    __shared__ int child_slot[kQTop > 0 ? kQTop : 1][4];
     __shared__ int s_warp[33];
     const int tid = threadIdx.x;
-    int a = 0, b = 1;  // current level = slots [a, b)
-    if (tid == 0) old_of[0] = (int)scratch[SCR_ROOT_NODE];
-    for (int i = tid; i < kTopNodes; i += blockDim.x) first_child[i] = -1;
+    const int root = (int)scratch[SCR_ROOT_NODE];
+    if (kQTop == 0 || root < 0) {  // (no root: a fault-injected build) -- no image
+        if (tid == 0) scratch[SCR_NTOP] = 0;
+        return;
+    }
+    if (tid == 0) old_of[0] = root;
+    for (int i = tid; i < kQTop; i += blockDim.x)
+        for (int c = 0; c < 4; ++c) child_slot[i][c] = -1;
     __syncthreads();
-    while (true) {
-        // each thread owns up to two slots of the level (levels fit kTopNodes <= 2 * blockDim)
-        int cnt[2] = {0, 0};
-        int4 refs[2];
-        for (int h = 0; h < 2; ++h) {
-            const int sl = a + 2 * tid + h;
-            if (sl < b) {
-                refs[h] = *reinterpret_cast<const int4*>(nodes + 4 * old_of[sl] + 3);
-                cnt[h] = (refs[h].x >= 0) + (refs[h].y >= 0);
-            }
+    int a = 0, b = 1;  // current level = slots [a, b)
+    while (b < kQTop) {
+        const int sl = a + tid;
+        int ref[4] = {kNoRefB, kNoRefB, kNoRefB, kNoRefB}, cnt = 0;
+        if (sl < b) {
+            const int4 r = *reinterpret_cast<const int4*>(quads + 4 * old_of[sl] + 2);   // refs 0, 1 in .z, .w
+            const int4 r2 = *reinterpret_cast<const int4*>(quads + 4 * old_of[sl] + 3);  // refs 2, 3 in .x, .y
+            ref[0] = r.z; ref[1] = r.w; ref[2] = r2.x; ref[3] = r2.y;
+            for (int c = 0; c < 4; ++c) cnt += ref[c] >= 0;
         }
         int total;
-        const int off = block_exclusive_scan(cnt[0] + cnt[1], s_warp, total);
-        if (total == 0 || b + total > kTopNodes) break;  // next level absent or does not fit
-        int k = b + off;
-        for (int h = 0; h < 2; ++h) {
-            const int sl = a + 2 * tid + h;
-            if (sl < b && cnt[h]) {
-                first_child[sl] = k;
-                if (refs[h].x >= 0) old_of[k++] = refs[h].x;
-                if (refs[h].y >= 0) old_of[k++] = refs[h].y;
-            }
+        const int off = block_exclusive_scan(cnt, s_warp, total);
+        if (total == 0) break;
+        if (sl < b) {
+            int k = b + off;
+            for (int c = 0; c < 4; ++c)
+                if (ref[c] >= 0) {
+                    if (k < kQTop) {
+                        old_of[k] = ref[c];
+                        child_slot[sl][c] = k;
+                    }
+                    ++k;
+                }
         }
         __syncthreads();
         a = b;
-        b += total;
+        b = min(b + total, kQTop);
     }
-    // image: node data with child refs translated to image slots where cached
+    // image: the records with cached members' refs translated to image slots
     for (int sl = tid; sl < b; sl += blockDim.x) {
-        const float4* nd = nodes + 4 * old_of[sl];
+        const float4* q = quads + 4 * old_of[sl];
         float4* im = image + 4 * sl;
-        im[0] = nd[0];
-        im[1] = nd[1];
-        im[2] = nd[2];
-        int4 r = *reinterpret_cast<const int4*>(nd + 3);
-        const int fc = first_child[sl];
-        if (fc >= 0) {
-            if (r.x >= 0) r.x = (int)(kSmemRef + fc);
-            if (r.y >= 0) r.y = (int)(kSmemRef + fc + (r.x >= 0 ? 1 : 0));
-        }
-        *reinterpret_cast<int4*>(im + 3) = r;
+        im[0] = q[0];
+        im[1] = q[1];
+        float4 qc = q[2], qd = q[3];
+        int* rc = reinterpret_cast<int*>(&qc);
+        int* rd = reinterpret_cast<int*>(&qd);
+        if (child_slot[sl][0] >= 0) rc[2] = (int)kSmemRef + child_slot[sl][0];
+        if (child_slot[sl][1] >= 0) rc[3] = (int)kSmemRef + child_slot[sl][1];
+        if (child_slot[sl][2] >= 0) rd[0] = (int)kSmemRef + child_slot[sl][2];
+        if (child_slot[sl][3] >= 0) rd[1] = (int)kSmemRef + child_slot[sl][3];
+        im[2] = qc;
+        im[3] = qd;
     }
-    if (tid == 0) scratch[SCR_NTOP] = (uint32_t)(n_nodes > 1 ? b : 0);
+    if (tid == 0) scratch[SCR_NTOP] = (uint32_t)b;
 }
 
 // ------------------------------------------------------------------ 4-wide view (cut records)
@@ -1259,7 +1268,7 @@ static rsi_status_t ensure_capacity(rsi_bvh* h, int64_t n, cudaStream_t s) {
 #define RSI_ALLOC(ptr, bytes) \
     if (e == cudaSuccess) e = cudaMallocAsync((void**)&(ptr), (size_t)(bytes), s);
     RSI_ALLOC(h->nodes, nn * 4 * sizeof(float4));
-    RSI_ALLOC(h->top, (size_t)(kTopNodes > 0 ? kTopNodes : 1) * 4 * sizeof(float4));
+    RSI_ALLOC(h->top, (size_t)(kQTop > 0 ? kQTop : 1) * 4 * sizeof(float4));
     RSI_ALLOC(h->quads, nn * 4 * sizeof(float4));
     RSI_ALLOC(h->tris, n * kTriF4 * sizeof(float4));
     RSI_ALLOC(h->keys, n * sizeof(uint32_t));
@@ -1384,8 +1393,8 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
                                                                        h->tris, h->parent, h->arrivals, h->scratch,
                                                                        (h->opt.flags & RSI_OPT_ROTATE) ? 1 : 0);
     }
-    if (kTopNodes > 0) rsi_note_launch(), k_topk<<<1, 1024, 0, s>>>(h->nodes, n_nodes, h->top, h->scratch);
     if (rsi_uses_quads()) rsi_note_launch(), k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads, h->scratch);
+    if (kQTop > 0) rsi_note_launch(), k_qtop<<<1, 256, 0, s>>>(h->quads, h->top, h->scratch);
     st = rsi_cuda_check(cudaGetLastError(), "build kernel launch");
     if (st != RSI_OK) return st;
     h->n_tri = nt;
@@ -1423,7 +1432,6 @@ rsi_status_t rsi_finish_build(rsi_bvh* h, cudaStream_t s) {
         h->scene_lo[x] = root[x];
         h->scene_hi[x] = root[3 + x];
     }
-    h->n_top = kTopNodes > 0 ? (int)h->h_words[SCR_NTOP] : 0;
     h->root_node = h->h_words[SCR_ROOT_NODE] == 0xffffffffu ? -1 : (int64_t)h->h_words[SCR_ROOT_NODE];
     return RSI_OK;
 }

@@ -32,7 +32,7 @@ enum {
     SCR_OVF_COUNT = 16, // intercept_count overflow list length
     SCR_OVF_NEXT = 17,  // intercept_count re-pass: next overflowed segment (work counter)
     SCR_DISPENSER = 18, // 2 words: 64-bit ray dispenser of the persistent traversal grid
-    SCR_NTOP = 20,      // nodes in the top-of-tree shared-memory image
+    SCR_NTOP = 20,      // records in the top-of-tree shared-memory image (k_qtop)
     SCR_ROOT_SET = 21,  // 1 once the refit wrote the root box
     SCR_QPMAX = 22,     // max |decode offset| over the quad records (float bits, >= 0)
     SCR_QEMIN = 23,     // min / max grid exponent + 128 over the quad records
@@ -60,8 +60,8 @@ struct rsi_bvh {
     int64_t sort_blocks_cap = 0;
     float4* nodes = nullptr;         // [4 * n_nodes]
     float4* quads = nullptr;         // [4 * n_nodes] compressed 4-wide cut records
-    float4* top = nullptr;           // [4 * kTopNodes] top-of-tree image (refs >= kSmemRef are image slots)
-    int n_top = 0;
+    float4* top = nullptr;           // [4 * kQTop] top-of-tree image of the 4-wide records
+                                     // (refs >= kSmemRef are image slots; record count in SCR_NTOP)
     float4* tris = nullptr;          // [4 * n_tri]
     uint32_t* keys = nullptr;        // sorted Morton codes [n_tri]
     int32_t* vals = nullptr;         // sorted triangle ids [n_tri]
@@ -171,11 +171,14 @@ constexpr uint32_t kQuadMagic = RSI_HALF_DECODE ? 0x00000064u : 0x47000000u;
 #define RSI_QUAD_GREEDY 1
 #endif
 
-// top-of-tree shared-memory cache (build.cu k_topk, traverse.cu)
-#ifndef RSI_TOPK
-#define RSI_TOPK 0  // measured slower at 1024/2048 on the bench workload (1 CTA/SM)
+// top-of-tree shared-memory image of the 4-wide records (build.cu k_qtop,
+// traverse.cu): the first RSI_QTOP records of the walk, breadth-first
+#ifndef RSI_QTOP
+#define RSI_QTOP 0  // measured slower on the 4-wide walk (21..256 records: +4..6 %), DESIGN.md 7
 #endif
-constexpr int kTopNodes = RSI_TOPK;           // <= 2 x 1024 (k_topk owns two slots per thread)
-constexpr uint32_t kSmemRef = 0x40000000u;    // child ref >= kSmemRef: slot in the image
+constexpr int kQTop = RSI_QTOP;               // <= 256 (k_qtop: one slot per thread of a level)
+static_assert(kQTop >= 0 && kQTop <= 256, "RSI_QTOP");
+constexpr uint32_t kSmemRef = 0x40000000u;    // member ref >= kSmemRef: slot in the image
+constexpr int kNoRefB = (int)0x80000000;      // "no member" (the walk's kNoRef)
 
 static inline int rsi_ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }

@@ -121,7 +121,7 @@ constexpr int kCountCap = RSI_COUNT_CAP;
 // image (1024 threads at <= 64 registers for boolean, 768 at <= 80 otherwise)
 template <int MODE>
 __host__ __device__ constexpr int trace_threads() {
-    return kTopNodes > 0 ? (MODE == 0 ? 1024 : 768) : 128;
+    return 128;
 }
 #ifndef RSI_CHUNK
 #define RSI_CHUNK 64
@@ -410,8 +410,7 @@ enum { MODE_BOOL = 0, MODE_BARY = 1, MODE_COUNT = 2 };
 struct TraceParams {
     const float4* nodes;
     const float4* quads;
-    const float4* top;   // top-of-tree image [4 * n_top]
-    int n_top;
+    const float4* top;   // top-of-tree image of the 4-wide records [4 * kQTop] (count: scratch[SCR_NTOP])
     const float4* tris;
     const float* S;
     const float* E;
@@ -942,7 +941,7 @@ __device__ __forceinline__ void cas(float& ka, int& ca, float& kb, int& cb) {
 }
 
 template <int MODE, bool kFP64, bool kCounters>
-__global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MODE == MODE_BOOL ? RSI_BOOL_MINB : (MODE == MODE_BARY ? RSI_BARY_MINB : RSI_COUNT_MINB))) k_trace(const TraceParams p) {
+__global__ void __launch_bounds__(trace_threads<MODE>(), (MODE == MODE_BOOL ? RSI_BOOL_MINB : (MODE == MODE_BARY ? RSI_BARY_MINB : RSI_COUNT_MINB))) k_trace(const TraceParams p) {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt = lanemask_lt();
@@ -953,13 +952,15 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
     constexpr int kSmemStack = MODE == MODE_BOOL ? RSI_BOOL_SMEM : (MODE == MODE_BARY ? RSI_BARY_SMEM : RSI_COUNT_SMEM);
     constexpr int kStack = kQuad ? kStackQuad : kStackBinary;
     constexpr int kT = trace_threads<MODE>();
-    // dynamic shared memory: [top-of-tree image: kTopNodes x 64 B][intercept_count hit lists]
+    // dynamic shared memory: [top-of-tree image: kQTop x 64 B (4-wide walk)][intercept_count hit lists]
+    constexpr int kImg = kQuad ? kQTop : 0;
     extern __shared__ float4 s_dyn[];
     float4* s_top = s_dyn;
-    float2* s_te = reinterpret_cast<float2*>(s_dyn + 4 * kTopNodes);
+    float2* s_te = reinterpret_cast<float2*>(s_dyn + 4 * kImg);
     int* s_k = reinterpret_cast<int*>(s_te + kCountCap * kT);
     // top-of-tree image, loaded once per CTA
-    for (int i = threadIdx.x; i < 4 * p.n_top; i += kT) s_top[i] = p.top[i];
+    const int n_top = kImg > 0 ? (int)p.scratch[SCR_NTOP] : 0;  // written by the build (k_qtop)
+    for (int i = threadIdx.x; i < 4 * n_top; i += kT) s_top[i] = p.top[i];
     __syncthreads();
     Stats st;
 
@@ -999,7 +1000,7 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
     }
     // root node: 0 for the Karras numbering, the top split under RSI_OPT_APETREI
     // (-1 when a fault-injected build never reached it: every ray misses)
-    const int root = p.n_top > 0 ? (int)kSmemRef : (int)p.scratch[SCR_ROOT_NODE];
+    const int root = n_top > 0 ? (int)kSmemRef : (int)p.scratch[SCR_ROOT_NODE];
     // kQuadMagic (float 2^15, or the f16 exponent byte) from a kernel parameter: an opaque register, so the
     // quad decode's PRMTs keep their byte selectors as immediates
     const uint32_t magic = p.magic;
@@ -1026,8 +1027,10 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
             __syncthreads();
         }
     }
-    while (true) {
-        // ---- 1. refill
+    // lanes without a segment take the next ids from the warp's chunk and set up
+    // ---- 1. refill: lanes without a segment take the next ids from the warp's
+    // chunk (one atomicAdd per kChunk segments per warp) and set them up
+    auto refill = [&]() {
         unsigned want = __ballot_sync(FULL, ray < 0);
         bool fresh = false;
         while (want && !exhausted) {
@@ -1076,6 +1079,9 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
             l0 = l1 = l2 = -1;
             node = ok ? root : -1;
         }
+    };
+    while (true) {
+        refill();
         if (__ballot_sync(FULL, ray >= 0) == 0) break;  // no rays left for this warp
 
         if constexpr (kQuad) {
@@ -1103,10 +1109,18 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
             // kQSpec: a lane holding one pending leaf keeps walking (its next
             // leaf goes to l1) in slots it would otherwise idle in
             if ((node >= 0 && l0 < 0) || (kQSpec && node >= 0 && l1 < 0)) {
-                const float4* q = p.quads + 4 * node;
                 float4 qa, qb, qc, qd;
-                ldg256(q, qa, qb);
-                ldg256(q + 2, qc, qd);
+                if (kImg > 0 && node >= (int)kSmemRef) {  // the top of the tree, from shared memory
+                    const float4* q = s_top + 4 * (node - (int)kSmemRef);
+                    qa = q[0];
+                    qb = q[1];
+                    qc = q[2];
+                    qd = q[3];
+                } else {
+                    const float4* q = p.quads + 4 * node;
+                    ldg256(q, qa, qb);
+                    ldg256(q + 2, qc, qd);
+                }
                 // Per axis: grid step s = 2^e and the decode offset pm = p - 2^15 s
                 // (stored; exact).  A child plane is p + q s = (2^15 + q) s + pm, so its
                 // t = (plane - o) / d is fma(2^15 + q, s*inv, fma(pm, inv, -off)): s*inv
@@ -1307,13 +1321,7 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), kTopNodes > 0 ? 1 : (MO
             // would otherwise idle in (its new leaves queue in l1, l2)
             if (trav || (RSI_SPEC && node >= 0 && l1 < 0)) {
                 float4 n0, n1, n2, n3f;
-                if (node >= (int)kSmemRef) {  // cached top of the tree
-                    const float4* sn = s_top + 4 * (node - (int)kSmemRef);
-                    n0 = sn[0];
-                    n1 = sn[1];
-                    n2 = sn[2];
-                    n3f = sn[3];
-                } else {
+                {
                     const float4* nd = p.nodes + 4 * node;
                     ldg256(nd, n0, n1);
                     ldg256(nd + 2, n2, n3f);
@@ -1782,7 +1790,8 @@ rsi_status_t rsi_gather_hits_device(const int32_t* ids, const int32_t* n_hits, i
 template <int MODE, bool kFP64, bool kCounters>
 static void launch_trace(const TraceParams& p, cudaStream_t s) {
     constexpr int kT = trace_threads<MODE>();
-    constexpr int kDyn = kTopNodes * 4 * (int)sizeof(float4) + (MODE == MODE_COUNT ? kCountCap * kT * 12 : 0);
+    constexpr bool kQuadM = MODE == MODE_BOOL ? RSI_BOOL_QUAD : (MODE == MODE_BARY ? RSI_BARY_QUAD : RSI_COUNT_QUAD);
+    constexpr int kDyn = (kQuadM ? kQTop : 0) * 4 * (int)sizeof(float4) + (MODE == MODE_COUNT ? kCountCap * kT * 12 : 0);
     const size_t dyn = kDyn;
     static int grid = 0;  // persistent grid: resident blocks per SM x SMs (per instantiation)
     if (grid == 0) {
@@ -1832,7 +1841,6 @@ rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* S, const float* E, in
     p.nodes = h->nodes;
     p.quads = h->quads;
     p.top = h->top;
-    p.n_top = kTopNodes > 0 ? h->n_top : 0;
     p.tris = h->tris;
     p.S = S;
     p.E = E;

@@ -36,7 +36,7 @@ static rsi_status_t read_options(const rsi_options_t* in, rsi_options_t* out) {
     if (in->struct_size != sizeof(rsi_options_t))
         return rsi_set_error(RSI_E_INVALID_ARG, "rsi_options_t.struct_size %u != %zu", in->struct_size,
                              sizeof(rsi_options_t));
-    if (in->flags & ~(RSI_OPT_FP64_MOLLER | RSI_OPT_COUNTERS | RSI_OPT_DEFERRED_STATUS | RSI_OPT_APETREI | RSI_OPT_ROTATE)) return rsi_set_error(RSI_E_INVALID_ARG, "unknown option flags 0x%x", in->flags);
+    if (in->flags & ~(RSI_OPT_FP64_MOLLER | RSI_OPT_COUNTERS | RSI_OPT_DEFERRED_STATUS | RSI_OPT_APETREI | RSI_OPT_ROTATE | RSI_OPT_PLAIN_TREE)) return rsi_set_error(RSI_E_INVALID_ARG, "unknown option flags 0x%x", in->flags);
     if (!(in->dedup_tau >= 0.0)) return rsi_set_error(RSI_E_INVALID_ARG, "dedup_tau must be >= 0");
     if (in->debug_refit_leaves < 0) return rsi_set_error(RSI_E_INVALID_ARG, "debug_refit_leaves must be >= 0");
     *out = *in;

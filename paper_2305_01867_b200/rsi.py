@@ -27,6 +27,7 @@ OPT_COUNTERS = 2
 OPT_DEFERRED_STATUS = 4
 OPT_APETREI = 8
 OPT_ROTATE = 16
+OPT_PLAIN_TREE = 32
 
 _lock = threading.Lock()
 _lib = None
@@ -152,11 +153,12 @@ class Options:
     deferred_status: bool = False  # rsi_build/rsi_rebuild do not wait: check rsi_build_status
     apetrei: bool = False       # NEXT-1: 63-bit Morton codes + Apetrei build
     rotate: bool = False        # local SAH tree rotations fused into the refit (NEXT-4 tree quality)
+    plain_tree: bool = False    # keep the Karras topology (no treelet restructuring): the paper's Fig. 3 tree
 
     def _c(self) -> _Options:
         flags = ((OPT_FP64_MOLLER if self.fp64_moller else 0) | (OPT_COUNTERS if self.counters else 0)
                  | (OPT_DEFERRED_STATUS if self.deferred_status else 0) | (OPT_APETREI if self.apetrei else 0)
-                 | (OPT_ROTATE if self.rotate else 0))
+                 | (OPT_ROTATE if self.rotate else 0) | (OPT_PLAIN_TREE if self.plain_tree else 0))
         return _Options(ctypes.sizeof(_Options), flags, float(self.dedup_tau), int(self.debug_refit_leaves))
 
 

@@ -92,7 +92,7 @@ def test_fig3_bvh_structure(rsi, golden):
     g = golden("fig3_case_study1.txt")
     V, T = synth.fixture()
     Vd, Td = to_dev(V, T)
-    h = rsi.rsi_build(Vd, Td)
+    h = rsi.rsi_build(Vd, Td, rsi.Options(plain_tree=True))  # the Karras topology as built
     d = rsi.rsi_bvh_download(h)
     h.free()
     leaves = g["leaf"]
@@ -512,7 +512,7 @@ def test_fixture_dump_and_dot_from_device(rsi):
     from paper_2305_01867_b200 import diagnostics
     V, T = synth.fixture()
     Vd, Td = to_dev(V, T)
-    h = rsi.rsi_build(Vd, Td)
+    h = rsi.rsi_build(Vd, Td, rsi.Options(plain_tree=True))
     d = rsi.rsi_bvh_download(h)
     h.free()
     txt = diagnostics.dump_text(d)
@@ -967,3 +967,38 @@ def test_deep_chain_tree_stack_bound(rsi):
         h.free()
         assert depth >= (32 if opts is not None else 12), depth  # measured: 39 under RSI_OPT_APETREI
         assert_parity(run_all(rsi, V, T, S, E, opts), ref, S, E, f"chain {opts} depth {depth}")
+
+
+def _sah_cost(d):
+    """Surface-area cost of a downloaded tree: sum of internal-node areas / root area."""
+    b = d["box"].astype(np.float64)                           # [nn, 2, 6]
+    lo = np.minimum(b[:, 0, :3], b[:, 1, :3])
+    hi = np.maximum(b[:, 0, 3:], b[:, 1, 3:])
+    e = np.maximum(hi - lo, 0)
+    a = e[:, 0] * e[:, 1] + e[:, 1] * e[:, 2] + e[:, 2] * e[:, 0]
+    return a.sum() / a[d["root"]]
+
+
+@pytest.mark.parametrize("wl", ["sphere", "paper_terrain"])
+def test_treelet_restructuring_lowers_sah_same_results(rsi, wl):
+    """The default build rebuilds completed treelets for least surface-area
+    cost (RSI_OPT_PLAIN_TREE keeps the Karras topology): the tree is valid
+    (validator), its SAH cost is lower, and every mode's outputs are identical
+    to the plain tree's and to the oracle's."""
+    V, T, S, E, _ = synth.workload(wl, 20_011, seed=17)
+    Vd, Td = to_dev(V, T)
+    costs = {}
+    for plain in (True, False):
+        h = rsi.rsi_build(Vd, Td, rsi.Options(plain_tree=plain))
+        assert rsi.rsi_validate(h)["ok"]
+        d = rsi.rsi_bvh_download(h)
+        h.free()
+        assert sorted(d["leaf_tri"].tolist()) == list(range(len(T)))
+        costs[plain] = _sah_cost(d)
+    assert costs[False] < 0.95 * costs[True], costs
+    ref = oracle.run(V, T, S, E)
+    a = run_all(rsi, V, T, S, E, rsi.Options(plain_tree=True))
+    b = run_all(rsi, V, T, S, E)
+    assert_parity(b, ref, S, E, wl)
+    for k in ("hit", "count", "tri"):
+        assert (a[k] == b[k]).all(), k

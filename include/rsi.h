@@ -83,12 +83,14 @@ typedef enum {
                                   kept, so the paper's node numbering is not.
                                   Same results. */
 #define RSI_OPT_PLAIN_TREE 32u /* keep the Karras topology exactly as built (the paper's Fig. 3
-                                  structure and node numbering).  By default the
-                                  refit's bottom-up climb also rebuilds every completed node's
-                                  treelet (its 7 largest-area descendants, Karras & Aila 2013)
-                                  as the binary tree of least surface-area cost: fewer box tests
-                                  per segment, same leaves, same boxes per subtree, same results
-                                  (the BVH only prunes).  Ignored under RSI_OPT_APETREI. */
+                                  structure and node numbering).  By default, for
+                                  meshes of up to 65536 triangles, the refit's bottom-up climb
+                                  also rebuilds the treelet of every node completed inside a
+                                  CTA's 256-leaf window (up to 5 largest-area descendants,
+                                  Karras & Aila 2013) as the binary tree of least surface-area
+                                  cost: fewer box tests per segment, same leaves, same results
+                                  (the BVH only prunes).  Also off under RSI_OPT_ROTATE and
+                                  ignored under RSI_OPT_APETREI. */
 #define RSI_OPT_APETREI 8u     /* the paper's construction instead of
                                   Karras + refit -- 63-bit Morton codes (21 bits per axis,
                                   z-major; "64-bit Morton codes") sorted as

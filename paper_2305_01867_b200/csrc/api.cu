@@ -564,7 +564,7 @@ rsi_status_t rsi_free(rsi_handle_t h) {
     cudaStream_t s = h->stream;
     order_enter(h, s);  // the frees follow the handle's last use on any stream
     void* bufs[] = {h->nodes, h->top, h->quads, h->tris, h->keys, h->vals, h->keys_tmp, h->vals_tmp, h->parent,
-                    h->arrivals, h->hist, h->scratch, h->stats, h->ovf_list, h->k63, h->other};
+                    h->arrivals, h->hist, h->scratch, h->stats, h->ovf_list, h->k63, h->other, h->qfull, h->qorder, h->qmap};
     rsi_status_t st = RSI_OK;
     for (void* p : bufs)
         if (p) {

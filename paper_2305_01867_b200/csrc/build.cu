@@ -531,6 +531,14 @@ __device__ void rotate_node(float4* nodes, int32_t* parent, int n_nodes, int nod
 #define RSI_TREELET 5  // treelet members (0: off; 3..5)
 #endif
 constexpr int kTL = RSI_TREELET;
+// meshes up to this many triangles: there the rebuild is a latency chain and the
+// treelets add ~35 us for -3.5 % traversal (sphere N_t = 1e4, 1.25e7 segments);
+// at N_t = 1e6 they are throughput work over 4000 windows (+1.16 ms rebuild for
+// -2.3 % traversal), so large meshes keep the Karras topology
+#ifndef RSI_TREELET_MAX_TRI
+#define RSI_TREELET_MAX_TRI 65536
+#endif
+constexpr int kTreeletMaxTri = RSI_TREELET_MAX_TRI;
 #ifndef RSI_TREELET_MIN
 #define RSI_TREELET_MIN 3  // smallest treelet rebuilt (members)
 #endif
@@ -1219,7 +1227,7 @@ __global__ void __launch_bounds__(256) k_qtop(const float4* __restrict__ quads, 
     __shared__ int child_slot[kQTop > 0 ? kQTop : 1][4];
     __shared__ int s_warp[33];
     const int tid = threadIdx.x;
-    const int root = (int)scratch[SCR_ROOT_NODE];
+    const int root = (int)scratch[SCR_QROOT];
     if (kQTop == 0 || root < 0) {  // (no root: a fault-injected build) -- no image
         if (tid == 0) scratch[SCR_NTOP] = 0;
         return;
@@ -1274,6 +1282,79 @@ __global__ void __launch_bounds__(256) k_qtop(const float4* __restrict__ quads, 
     }
     if (tid == 0) scratch[SCR_NTOP] = (uint32_t)b;
 }
+
+// ------------------------------------------------------------------ 4-wide record compaction
+// k_quads writes a record for EVERY internal node, but the walk only reaches
+// the records of the collapsed tree -- the root and the internal members of
+// reached records, about a third of them (~3.9 members per record) -- so
+// two thirds of every 128-byte line of the node-indexed array is dead weight
+// in L1.  This pass keeps the live records only, breadth-first from the root
+// (index 0; a record's members sit next to each other), with member refs
+// rewritten to the new indices (leaf refs and kNoRef unchanged).  One CTA,
+// level-synchronous (a level's live records are the previous level's
+// internal members, ranked by a block scan).
+__global__ void __launch_bounds__(1024) k_qcompact(const float4* __restrict__ full, float4* __restrict__ out,
+                                                   int32_t* order, int32_t* map, uint32_t* scratch) {
+    __shared__ int s_warp[33];
+    const int tid = threadIdx.x;
+    const int root = (int)scratch[SCR_ROOT_NODE];
+    if (root < 0) {  // (a fault-injected build never reached the root): no records
+        if (tid == 0) scratch[SCR_QROOT] = 0xffffffffu;
+        return;
+    }
+    if (tid == 0) {
+        order[0] = root;
+        map[root] = 0;
+    }
+    __syncthreads();
+    int a = 0, b = 1;  // current level = live records [a, b)
+    while (a < b) {
+        int next = b;
+        for (int base = a; base < b; base += blockDim.x) {
+            const int i = base + tid;
+            int ref[4] = {kNoRefB, kNoRefB, kNoRefB, kNoRefB}, cnt = 0;
+            if (i < b) {
+                const int o = order[i];
+                const int4 r2 = *reinterpret_cast<const int4*>(full + 4 * o + 2);  // refs 0, 1 in .z, .w
+                const int4 r3 = *reinterpret_cast<const int4*>(full + 4 * o + 3);  // refs 2, 3 in .x, .y
+                ref[0] = r2.z; ref[1] = r2.w; ref[2] = r3.x; ref[3] = r3.y;
+                for (int c = 0; c < 4; ++c) cnt += ref[c] >= 0;
+            }
+            int total;
+            const int off = block_exclusive_scan(cnt, s_warp, total);
+            int k = next + off;
+            for (int c = 0; c < 4; ++c)
+                if (ref[c] >= 0) {
+                    order[k] = ref[c];
+                    map[ref[c]] = k;
+                    ++k;
+                }
+            next += total;
+            __syncthreads();
+        }
+        a = b;
+        b = next;
+    }
+    for (int i = tid; i < b; i += blockDim.x) {
+        const float4* q = full + 4 * order[i];
+        float4* d = out + 4 * i;
+        d[0] = q[0];
+        d[1] = q[1];
+        float4 qc = q[2], qd = q[3];
+        int* rc = reinterpret_cast<int*>(&qc);
+        int* rd = reinterpret_cast<int*>(&qd);
+        if (rc[2] >= 0) rc[2] = map[rc[2]];
+        if (rc[3] >= 0) rc[3] = map[rc[3]];
+        if (rd[0] >= 0) rd[0] = map[rd[0]];
+        if (rd[1] >= 0) rd[1] = map[rd[1]];
+        d[2] = qc;
+        d[3] = qd;
+    }
+    if (tid == 0) scratch[SCR_QROOT] = 0u;
+}
+
+// records indexed by node id (meshes above kQCompactMax internal nodes)
+__global__ void k_qroot_copy(uint32_t* scratch) { scratch[SCR_QROOT] = scratch[SCR_ROOT_NODE]; }
 
 // ------------------------------------------------------------------ 4-wide view (cut records)
 // One thread per internal node n: the up-to-4 members of n's cut (grandchildren, or the greedy cut under RSI_QUAD_GREEDY; a leaf child
@@ -1532,9 +1613,13 @@ __global__ void __launch_bounds__(kBlock) k_validate_ids(const uint32_t* __restr
 static rsi_status_t ensure_capacity(rsi_bvh* h, int64_t n, cudaStream_t s) {
     int nb = rsi_ceil_div(n, kTile);
     if (n <= h->cap_tri && nb <= h->sort_blocks_cap) return RSI_OK;
-    void* old[] = {h->nodes, h->top, h->quads, h->tris, h->keys, h->vals, h->keys_tmp, h->vals_tmp, h->parent, h->arrivals, h->hist};
+    void* old[] = {h->nodes, h->top, h->quads, h->tris, h->keys, h->vals, h->keys_tmp, h->vals_tmp, h->parent, h->arrivals, h->hist,
+                   h->qfull, h->qorder, h->qmap};
     for (void* p : old)
         if (p) cudaFreeAsync(p, s);
+    h->qfull = nullptr;
+    h->qorder = nullptr;
+    h->qmap = nullptr;
     int64_t nn = n > 1 ? n - 1 : 1;
     cudaError_t e = cudaSuccess;
 #define RSI_ALLOC(ptr, bytes) \
@@ -1542,6 +1627,11 @@ static rsi_status_t ensure_capacity(rsi_bvh* h, int64_t n, cudaStream_t s) {
     RSI_ALLOC(h->nodes, nn * 4 * sizeof(float4));
     RSI_ALLOC(h->top, (size_t)(kQTop > 0 ? kQTop : 1) * 4 * sizeof(float4));
     RSI_ALLOC(h->quads, nn * 4 * sizeof(float4));
+    if (nn <= kQCompactMax) {
+        RSI_ALLOC(h->qfull, nn * 4 * sizeof(float4));
+        RSI_ALLOC(h->qorder, nn * sizeof(int32_t));
+        RSI_ALLOC(h->qmap, nn * sizeof(int32_t));
+    }
     RSI_ALLOC(h->tris, n * kTriF4 * sizeof(float4));
     RSI_ALLOC(h->keys, n * sizeof(uint32_t));
     RSI_ALLOC(h->vals, n * sizeof(int32_t));
@@ -1664,9 +1754,16 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
         rsi_note_launch(), k_refit<<<rsi_ceil_div(refit_leaves, kRefitLeaves), kRefitLeaves, 0, s>>>(V, nv, T, h->vals, refit_leaves, n, h->nodes,
                                                                        h->tris, h->parent, h->arrivals, h->scratch,
                                                                        (h->opt.flags & RSI_OPT_ROTATE) ? 1 : 0,
-                                                                       (h->opt.flags & (RSI_OPT_PLAIN_TREE | RSI_OPT_ROTATE)) || refit_leaves < n ? 0 : 1);
+                                                                       (h->opt.flags & (RSI_OPT_PLAIN_TREE | RSI_OPT_ROTATE)) || refit_leaves < n ||
+                                                                               n > kTreeletMaxTri ? 0 : 1);
     }
-    if (rsi_uses_quads()) rsi_note_launch(), k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads, h->scratch);
+    if (n_nodes <= kQCompactMax && h->qfull) {  // records of every node, then the live ones, breadth-first
+        rsi_note_launch(), k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->qfull, h->scratch);
+        rsi_note_launch(), k_qcompact<<<1, 1024, 0, s>>>(h->qfull, h->quads, h->qorder, h->qmap, h->scratch);
+    } else {
+        rsi_note_launch(), k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads, h->scratch);
+        rsi_note_launch(), k_qroot_copy<<<1, 1, 0, s>>>(h->scratch);
+    }
     if (kQTop > 0) rsi_note_launch(), k_qtop<<<1, 256, 0, s>>>(h->quads, h->top, h->scratch);
     st = rsi_cuda_check(cudaGetLastError(), "build kernel launch");
     if (st != RSI_OK) return st;

@@ -38,6 +38,7 @@ enum {
     SCR_QEMIN = 23,     // min / max grid exponent + 128 over the quad records
     SCR_QEMAX = 24,
     SCR_ROOT_NODE = 25, // root internal node (0 Karras; Apetrei: top split; 0xffffffff unset)
+    SCR_QROOT = 26,     // root of the 4-wide records the walks read (0 after compaction; 0xffffffff unset)
     SCR_SORT_DONE = 32, // 32 words: per-block slice counters of the rank sort
     SCR_WORDS = 64
 };
@@ -59,7 +60,12 @@ struct rsi_bvh {
     int64_t cap_tri = 0;             // allocated capacity (triangles)
     int64_t sort_blocks_cap = 0;
     float4* nodes = nullptr;         // [4 * n_nodes]
-    float4* quads = nullptr;         // [4 * n_nodes] compressed 4-wide cut records
+    float4* quads = nullptr;         // [4 * n_nodes] compressed 4-wide cut records the walks read: the live
+                                     // records only, breadth-first from index 0 (k_qcompact), or indexed
+                                     // by binary node id above kQCompactMax nodes
+    float4* qfull = nullptr;         // [4 * n_nodes] k_quads output (one record per internal node)
+    int32_t* qorder = nullptr;       // [n_nodes] compaction: live record i's binary node
+    int32_t* qmap = nullptr;         // [n_nodes] compaction: binary node -> live record index
     float4* top = nullptr;           // [4 * kQTop] top-of-tree image of the 4-wide records
                                      // (refs >= kSmemRef are image slots; record count in SCR_NTOP)
     float4* tris = nullptr;          // [4 * n_tri]
@@ -178,6 +184,12 @@ constexpr uint32_t kQuadMagic = RSI_HALF_DECODE ? 0x00000064u : 0x47000000u;
 #endif
 constexpr int kQTop = RSI_QTOP;               // <= 256 (k_qtop: one slot per thread of a level)
 static_assert(kQTop >= 0 && kQTop <= 256, "RSI_QTOP");
+// 4-wide record compaction (build.cu k_qcompact, one CTA): meshes up to this
+// many internal nodes; larger ones keep the records indexed by node id
+#ifndef RSI_QCOMPACT_MAX
+#define RSI_QCOMPACT_MAX 0  // measured: query -0.3 %, rebuild +44 us (N_t = 1e4): off
+#endif
+constexpr int kQCompactMax = RSI_QCOMPACT_MAX;
 constexpr uint32_t kSmemRef = 0x40000000u;    // member ref >= kSmemRef: slot in the image
 constexpr int kNoRefB = (int)0x80000000;      // "no member" (the walk's kNoRef)
 

@@ -1,1 +1,2 @@
-for v in tl5 tl5m5 tl5m4 tl4m4; do RSI_LIB=paper_2305_01867_b200/lib/librsi_$v.so timeout 300 python bench.py --no-configs --no-cpu-baseline --no-e2e > gpurun_out/bench_$v.json 2>&1; done
+for v in tl0; do RSI_LIB=paper_2305_01867_b200/lib/librsi_$v.so timeout 300 python bench.py --workload sphere1m --no-configs --no-cpu-baseline --no-e2e > gpurun_out/bench_1m_$v.json 2>&1; done
+timeout 300 python bench.py --workload sphere1m --no-configs --no-cpu-baseline --no-e2e > gpurun_out/bench_1m_tl5.json 2>&1

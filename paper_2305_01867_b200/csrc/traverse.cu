@@ -335,6 +335,26 @@ __device__ __forceinline__ void ldg256(const float4* p, float4& a, float4& b) {
 #endif
 }
 
+// L1 eviction priority of the triangle / 4-wide record fetches (RSI_TRI_L1,
+// RSI_Q_L1): 0 default, 1 L1::no_allocate, 2 L1::evict_first, 3 L1::evict_last
+#ifndef RSI_TRI_L1
+#define RSI_TRI_L1 1  // L1::no_allocate: sphere -1 %, terrain -0.5 % (records keep L1)
+#endif
+#ifndef RSI_Q_L1
+#define RSI_Q_L1 0
+#endif
+#define RSI_LDG256_HINT(hint)                                                                  \
+    asm("ld.global.nc" hint ".v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"                          \
+        : "=f"(a.x), "=f"(a.y), "=f"(a.z), "=f"(a.w), "=f"(b.x), "=f"(b.y), "=f"(b.z), "=f"(b.w) \
+        : "l"(p))
+template <int kHint>
+__device__ __forceinline__ void ldg256h(const float4* p, float4& a, float4& b) {
+    if constexpr (kHint == 1) RSI_LDG256_HINT(".L1::no_allocate");
+    else if constexpr (kHint == 2) RSI_LDG256_HINT(".L1::evict_first");
+    else if constexpr (kHint == 3) RSI_LDG256_HINT(".L1::evict_last");
+    else ldg256(p, a, b);
+}
+#undef RSI_LDG256_HINT
 
 // triangle slot k: 64 B (4 x float4, the last one padding) for two 256-bit loads
 __device__ __forceinline__ void load_tri(const float4* __restrict__ tris, int k, float4& A, float4& B, float4& C) {
@@ -345,8 +365,8 @@ __device__ __forceinline__ void load_tri(const float4* __restrict__ tris, int k,
         C = __ldg(t + 2);
     } else {
         float4 pad;
-        ldg256(tris + 4 * k, A, B);
-        ldg256(tris + 4 * k + 2, C, pad);
+        ldg256h<RSI_TRI_L1>(tris + 4 * k, A, B);
+        ldg256h<RSI_TRI_L1>(tris + 4 * k + 2, C, pad);
     }
 }
 
@@ -1147,8 +1167,8 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), (MODE == MODE_BOOL ? RS
                     qd = q[3];
                 } else {
                     const float4* q = p.quads + 4 * node;
-                    ldg256(q, qa, qb);
-                    ldg256(q + 2, qc, qd);
+                    ldg256h<RSI_Q_L1>(q, qa, qb);
+                    ldg256h<RSI_Q_L1>(q + 2, qc, qd);
                 }
                 // Per axis: grid step s = 2^e and the decode offset pm = p - 2^15 s
                 // (stored; exact).  A child plane is p + q s = (2^15 + q) s + pm, so its

@@ -11,12 +11,13 @@ V, T, S, E, _ = synth.workload(wl, n, seed=3)
 dev = torch.device("cuda:0")
 Vd, Td, Sd, Ed = (torch.from_numpy(a).to(dev) for a in (V, T, S, E))
 res = {}
+MODES = os.environ.get("MODES", "boolean,barycentric,intercept_count").split(",")
 for cfg in os.environ.get("CFGS", "-1:1").split(","):
     mt, sp = cfg.split(":")
     os.environ["RSI_MIN_TRAV"] = mt
     os.environ["RSI_SPEC"] = sp
     h = rsi.rsi_build(Vd, Td)
-    for mode in ("boolean", "barycentric", "intercept_count"):
+    for mode in MODES:
         out = rsi.alloc_outputs(n, mode, dev)
         for _ in range(2):
             rsi.rsi_intersect(h, Sd, Ed, mode, out=out)
@@ -32,7 +33,7 @@ for cfg in os.environ.get("CFGS", "-1:1").split(","):
 if os.environ.get("COUNTERS", "1") == "0":
     [print(k, json.dumps(v)) for k, v in res.items()]; sys.exit(0)
 hc = rsi.rsi_build(Vd, Td, rsi.Options(counters=True))
-for mode in ("boolean", "barycentric", "intercept_count"):
+for mode in MODES:
     rsi.rsi_reset_stats(hc)
     rsi.rsi_intersect(hc, Sd, Ed, mode)
     st = rsi.rsi_get_stats(hc)

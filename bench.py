@@ -40,16 +40,27 @@ import synth  # noqa: E402
 METRIC = "rays/sec (boolean & barycentric) at N_t=1e4, N_r=1e7-1e8 on 1/2/4/8 B200"
 UNIT = "rays/s"
 
-# Algorithmic work model of the traversal kernel:
-# FP32-pipe instructions per child-box slab test and per Moller-Trumbore test.
-# The per-ray numbers of box and MT tests are MEASURED in this run by an
-# instrumented launch (RSI_OPT_COUNTERS) outside the timed region; SURVEY
-# 8(d)'s CPU-model figures are the fallback.
+# Algorithmic work model of the traversal kernel: SURVEY 8(d)'s per-unit
+# figures (box tests and Moller-Trumbore tests per segment of the LBVH walk on
+# each workload: any-hit for boolean, nearest for barycentric, all-hits for
+# intercept_count) x 17 / 70 FP32 instructions per test.  The roofline's
+# `achieved` is that fixed per-segment figure x the segments of one launch /
+# the launch time -- a walk that needs fewer tests (a better tree) shows up as
+# a higher fraction.  The tests per segment this build actually performs are
+# MEASURED by an instrumented launch (RSI_OPT_COUNTERS) outside the timed
+# region and reported next to it (`achieved_measured_work`).
 WORK_MODEL = {
-    "boolean": {"box_tests": 36.8, "mt_tests": 1.62},
-    "barycentric": {"box_tests": 54.9, "mt_tests": 2.92},
-    "intercept_count": {"box_tests": 69.3, "mt_tests": 3.97},
+    "sphere": {"boolean": {"box_tests": 36.8, "mt_tests": 1.62},
+               "barycentric": {"box_tests": 54.9, "mt_tests": 2.92},
+               "intercept_count": {"box_tests": 69.3, "mt_tests": 3.97}},
+    "terrain": {"boolean": {"box_tests": 37.8, "mt_tests": 1.50},
+                "barycentric": {"box_tests": 43.7, "mt_tests": 1.94},
+                "intercept_count": {"box_tests": 50.3, "mt_tests": 2.19}},
+    "sphere1m": {"boolean": {"box_tests": 51.3, "mt_tests": 1.50},
+                 "barycentric": {"box_tests": 78.8, "mt_tests": 2.83},
+                 "intercept_count": {"box_tests": 103.2, "mt_tests": 3.99}},
 }
+WORK_MODEL["paper_terrain"] = {"boolean": {"box_tests": 46.3, "mt_tests": 1.50}}
 FP32_PER_BOX = 17.0
 FP32_PER_MT = 70.0
 N_SM = 148
@@ -206,19 +217,28 @@ def _ncu_traversal(mode: str):
         return None
 
 
-def roofline(mode: str, rays: int, kernel_ms: float, sm_mhz: float | None, work: dict | None = None):
-    w = work or WORK_MODEL[mode]
+def roofline(mode: str, rays: int, kernel_ms: float, sm_mhz: float | None, work: dict | None = None,
+             workload: str = "sphere"):
+    w = WORK_MODEL.get(workload, {}).get(mode) or WORK_MODEL["sphere"][mode]
     inst_per_ray = w["box_tests"] * FP32_PER_BOX + w["mt_tests"] * FP32_PER_MT
     clock = (sm_mhz or 1965.0) * 1e6
-    peak = N_SM * FP32_LANES * clock / 1e12            # T FP32 inst/s
+    peak = N_SM * FP32_LANES * clock / 1e12            # T FP32 inst/s (nominal: no measured FP32 peak)
     achieved = inst_per_ray * rays / (kernel_ms * 1e-3) / 1e12
-    return {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 4), "unit": "TFP32-inst/s",
-            "frac": round(achieved / peak, 5), "traffic": _traffic(mode, rays),
-            "traffic_unit": "DRAM bytes/launch (ncu); algorithmic ray stream = 25 B/ray (boolean)",
-            "kernel": f"k_{mode}", "kernel_ms": round(kernel_ms, 4), "ncu": _ncu_traversal(mode),
-            "model": f"{w['box_tests']:.2f} box x {FP32_PER_BOX:.0f} + {w['mt_tests']:.2f} MT x {FP32_PER_MT:.0f} "
-                     f"= {inst_per_ray:.0f} FP32 inst/ray ({'measured' if work else 'SURVEY 8(d) model'} "
-                     f"tests/ray); peak = 148 SM x 128 FP32 lanes x median sm_mhz"}
+    out = {"bound": "alu", "achieved": round(achieved, 4), "peak": round(peak, 4), "unit": "TFP32-inst/s",
+           "frac": round(achieved / peak, 5), "traffic": _traffic(mode, rays),
+           "traffic_unit": "DRAM bytes/launch (ncu); algorithmic = 24 B in + 1 / 4 / 24 B out per ray "
+                           "(boolean / intercept_count / barycentric)",
+           "kernel": f"k_trace<{mode}>", "kernel_ms": round(kernel_ms, 4), "ncu": _ncu_traversal(mode),
+           "model": f"SURVEY 8(d) per-unit figure ({workload}, {mode}): {w['box_tests']:.1f} box x "
+                    f"{FP32_PER_BOX:.0f} + {w['mt_tests']:.2f} MT x {FP32_PER_MT:.0f} = {inst_per_ray:.0f} "
+                    "FP32 inst/ray; peak = nominal 148 SM x 128 FP32 lanes x median sm_mhz"}
+    if work:
+        mi = work["box_tests"] * FP32_PER_BOX + work["mt_tests"] * FP32_PER_MT
+        out["achieved_measured_work"] = round(mi * rays / (kernel_ms * 1e-3) / 1e12, 4)
+        out["frac_measured_work"] = round(mi * rays / (kernel_ms * 1e-3) / 1e12 / peak, 5)
+        out["measured_work"] = (f"{work['box_tests']:.2f} box + {work['mt_tests']:.2f} MT per ray measured "
+                                f"(RSI_OPT_COUNTERS) = {mi:.0f} FP32 inst/ray")
+    return out
 
 
 def oracle_run(V, T, S, E):
@@ -582,7 +602,7 @@ def main():
             "data": "synthetic (seeded UV-sphere mesh, uniform segments; see DESIGN.md 4)",
             "config": arm_config(args, len(T), world, backend),
             "build_ms": build_ms, "query_ms": query_ms,
-            "roofline": roofline(args.mode, n, query_ms, clk["sm_mhz"] if clk else None, work),
+            "roofline": roofline(args.mode, n, query_ms, clk["sm_mhz"] if clk else None, work, args.workload),
             "work_per_ray": work,
             "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
             "gpu_launches": launches,

@@ -83,14 +83,17 @@ typedef enum {
                                   kept, so the paper's node numbering is not.
                                   Same results. */
 #define RSI_OPT_PLAIN_TREE 32u /* keep the Karras topology exactly as built (the paper's Fig. 3
-                                  structure and node numbering).  By default, for
-                                  meshes of up to 65536 triangles, the refit's bottom-up climb
-                                  also rebuilds the treelet of every node completed inside a
-                                  CTA's 256-leaf window (up to 5 largest-area descendants,
-                                  Karras & Aila 2013) as the binary tree of least surface-area
-                                  cost: fewer box tests per segment, same leaves, same results
-                                  (the BVH only prunes).  Also off under RSI_OPT_ROTATE and
-                                  ignored under RSI_OPT_APETREI. */
+                                  structure and node numbering).  By default the
+                                  tree's quality is raised after k_karras, same leaves, same
+                                  results (the BVH only prunes): for meshes of up to 32768
+                                  triangles every maximal Karras subtree of <= 256 leaves is
+                                  rebuilt top-down by binned SAH (its leaves permuted within
+                                  its slot range, the Karras tree above it kept); for 32769 ..
+                                  65536 triangles the refit's bottom-up climb rebuilds the
+                                  treelet of every node completed inside a CTA's 256-leaf
+                                  window (up to 5 largest-area descendants, Karras & Aila
+                                  2013) as the binary tree of least surface-area cost.  Also
+                                  off under RSI_OPT_ROTATE and ignored under RSI_OPT_APETREI. */
 #define RSI_OPT_APETREI 8u     /* the paper's construction instead of
                                   Karras + refit -- 63-bit Morton codes (21 bits per axis,
                                   z-major; "64-bit Morton codes") sorted as
@@ -345,6 +348,28 @@ rsi_status_t rsi_bvh_info(rsi_handle_t h, int64_t* n_triangles, int64_t* n_nodes
 rsi_status_t rsi_bvh_download(rsi_handle_t h, int32_t* h_child, float* h_box,
                               int32_t* h_leaf_tri, uint32_t* h_morton, int32_t* h_parent,
                               uint32_t* h_arrivals, void* stream);
+
+/*
+ * rsi_bvh_upload: the inverse of rsi_bvh_download -- replaces the binary tree of
+ *   `h` (built over the same mesh) by a caller-given one and rebuilds the 4-wide
+ *   records from it (the paper's BVH debugging strategy, run the
+ *   other way: a tree inspected or modified on the host -- or built by another
+ *   method, e.g. a SAH builder, for tree-quality experiments -- is traversed by
+ *   the same kernels).  Results of rsi_intersect do not depend on the tree (a
+ *   BVH only prunes); a tree whose boxes do not contain their subtrees gives
+ *   wrong results (the caller's responsibility; rsi_validate checks it).
+ *     h_child   [n_nodes][2] int32 child refs (>= 0 internal node, < 0 leaf ~slot),
+ *               every internal node and leaf slot reachable from `root` once
+ *     h_box     [n_nodes][2][6] float32 child AABBs as in rsi_bvh_download
+ *     h_leaf_tri[N_t] int32 triangle index at each leaf slot (a permutation)
+ *     root      the root internal node
+ *   Host buffers, read before return; synchronizes `stream`.  The next
+ *   rsi_rebuild replaces the uploaded tree.
+ * Errors: RSI_E_INVALID_ARG (null / N_t < 2 / root out of range / leaf_tri not
+ *   a permutation), RSI_E_OOM, RSI_E_CUDA.
+ */
+rsi_status_t rsi_bvh_upload(rsi_handle_t h, const int32_t* h_child, const float* h_box,
+                            const int32_t* h_leaf_tri, int64_t root, void* stream);
 
 /*
  * rsi_bvh_root: the root internal node of `h` and the sorted Morton codes at

@@ -646,6 +646,22 @@ rsi_status_t rsi_bvh_info(rsi_handle_t h, int64_t* n_triangles, int64_t* n_nodes
     return RSI_OK;
 }
 
+rsi_status_t rsi_bvh_upload(rsi_handle_t h, const int32_t* h_child, const float* h_box, const int32_t* h_leaf_tri,
+                            int64_t root, void* stream) {
+    if (!h || !h_child || !h_box || !h_leaf_tri) return rsi_set_error(RSI_E_INVALID_ARG, "null argument");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (h->status_pending) {
+        const rsi_status_t st0 = rsi_finish_build(h, s);
+        if (st0 != RSI_OK) return st0;
+    }
+    if (h->n_tri <= 0) return rsi_set_error(RSI_E_INVALID_ARG, "handle holds no mesh");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev != h->device)
+        return rsi_set_error(RSI_E_INVALID_ARG, "handle built on device %d, current device is %d", h->device, dev);
+    return rsi_bvh_upload_device(h, h_child, h_box, h_leaf_tri, root, s);
+}
+
 rsi_status_t rsi_bvh_download(rsi_handle_t h, int32_t* h_child, float* h_box, int32_t* h_leaf_tri,
                               uint32_t* h_morton, int32_t* h_parent, uint32_t* h_arrivals, void* stream) {
     if (!h) return rsi_set_error(RSI_E_INVALID_ARG, "null handle");

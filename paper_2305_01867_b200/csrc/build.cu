@@ -19,6 +19,7 @@
 #include <cstdio>
 
 #include <cstring>
+#include <new>
 
 #include "rsi_internal.cuh"
 
@@ -41,6 +42,7 @@ __global__ void k_build_init(uint32_t* scratch, uint32_t root_init) {
         scratch[SCR_QEMAX] = 0u;
     }
     if (i < 32) scratch[SCR_SORT_DONE + i] = 0u;
+    if (i == 2) scratch[SCR_SAH_COUNT] = 0u;
 }
 
 __device__ __forceinline__ float warp_min(float v) {
@@ -768,6 +770,388 @@ __device__ void treelet_opt(const Tree& tr, int n, unsigned char* row_popt) {
         }
         q_c[it] = c;
         tr.set_cost(q_id[it], c);
+    }
+}
+
+// ------------------------------------------------------------------ NEXT-4 tree quality: SAH subtrees
+// RSI_SAH_SUB (default for N_t <= kSahMaxTri; off under RSI_OPT_PLAIN_TREE /
+// ROTATE / APETREI): every maximal Karras subtree with <= kSahSub leaves (a
+// node of <= kSahSub leaves whose parent has more) is rebuilt top-down by
+// binned SAH over its triangles' centroids, between k_karras and k_refit.  The
+// Karras topology stays above these subtrees (A5 is still the tree's top), and
+// every node still covers a CONTIGUOUS range of leaf slots (a top-down
+// partition of the subtree's slot range, the triangles permuted inside it),
+// numbered the Karras way: an internal left child takes the last slot of its
+// range, a right child the first.  For any such tree over a range that
+// numbering is a bijection onto the node ids the Karras subtree used (ids
+// [a+1, b] when its root is a left child, else [a, b-1]; the root keeps its id
+// and parent link), so k_refit's windows, parent links and leaf ranges work
+// unchanged.  One CTA (kSahWarps warps) per subtree: the nodes of a level one
+// per warp -- centroid bounds by REDUX, kSahBins bins per axis filled with
+// shared-memory atomics (boxes as order-preserving uint32 keys), every plane of
+// every axis scanned at once (one lane per (axis, bin)), a warp-ordered stable
+// partition -- and every node of <= kSahSmall triangles by ONE thread with the
+// exact SAH-optimal topology (treelet_dp).
+// Measured (sphere N_t = 1e4, 1e7 segments): box tests per
+// segment -4 % (boolean) .. -6 % (intercept_count), query -3.4 / -4.7 / -5.6 %
+// (boolean / barycentric / intercept_count), paper terrain -6.8 / -12 / -16 %;
+// rebuild 0.126 -> 0.130 ms with the refit's treelets switched off (they add
+// nothing on top: same query time).  Host-built trees walked by the same
+// kernels (tools/tree_upload.py) bound what SAH quality can give: full binned
+// SAH -8 .. -11 %.  At N_t = 1e6 the rebuild grows 0.74 -> 1.9 ms, hence the gate.
+#ifndef RSI_SAH_SUB
+#define RSI_SAH_SUB 256  // leaves per rebuilt subtree (0: off); 128 / 512: rebuild -11 / +27 us, query +0.2 / -0.7 %
+#endif
+#ifndef RSI_SAH_TREELET
+#define RSI_SAH_TREELET 0  // the refit's treelet restructuring on top of the SAH subtrees (measured: no gain, +20 us)
+#endif
+#ifndef RSI_SAH_MAX_TRI
+#define RSI_SAH_MAX_TRI 32768
+#endif
+constexpr int64_t kSahMaxTri = RSI_SAH_MAX_TRI;
+constexpr int kSahSub = RSI_SAH_SUB > 0 ? RSI_SAH_SUB : 4;
+#ifndef RSI_SAH_BINS
+#define RSI_SAH_BINS 10  // bins per axis (3 x 10 <= 32 lanes: every plane of every axis in one warp pass)
+#endif
+constexpr int kSahWarps = 32;
+constexpr int kSahBins = RSI_SAH_BINS;
+constexpr int kSahGrid = 148;  // persistent CTAs (one per SM) over the subtree list
+static_assert(kSahSub <= 65535 && (kSahSub & (kSahSub - 1)) == 0, "RSI_SAH_SUB");
+
+__device__ __forceinline__ uint32_t fkey(float f) {  // order-preserving float -> uint32
+    const uint32_t u = __float_as_uint(f);
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float fdekey(uint32_t k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
+}
+
+// Subtree roots: internal node i with 3 <= leaves <= kSahSub whose parent has more (or i is the root).
+__global__ void __launch_bounds__(kBlock) k_sah_roots(const float4* __restrict__ nodes, const int32_t* __restrict__ parent,
+                                                      int n_nodes, int32_t* list, uint32_t* scratch) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_nodes) return;
+    const int4 r = __ldg(reinterpret_cast<const int4*>(nodes + 4 * i + 3));
+    const int m = r.w - r.z + 1;
+    if (m < 3 || m > kSahSub) return;
+    if (i != 0) {
+        const int pn = __ldg(parent + i) >> 1;
+        const int4 pr = __ldg(reinterpret_cast<const int4*>(nodes + 4 * pn + 3));
+        if (pr.w - pr.z + 1 <= kSahSub) return;
+    }
+    list[atomicAdd(scratch + SCR_SAH_COUNT, 1u)] = i;
+}
+
+// Shared memory of k_sah_sub (dynamic): the subtree's boxes and 3 x centroids,
+// triangle ids, the permutation (double-buffered), the level task lists and
+// one bin array per warp.
+constexpr int kSahBinSlots = 3 * kSahBins;  // (axis, bin) pairs: one lane each in the SAH scan
+static_assert(kSahBinSlots <= 32, "RSI_SAH_BINS");
+constexpr int kSahSmall = kTLm;  // nodes of <= kSahSmall triangles: one THREAD each, exact SAH over every
+                                 // topology (treelet_dp) instead of a warp's binned split per level
+constexpr size_t kSahSmem = (size_t)9 * kSahSub * sizeof(float) + (size_t)kSahSub * sizeof(int32_t) +
+                            (size_t)2 * kSahSub * sizeof(uint16_t) + (size_t)3 * (kSahSub / 2) * 3 * sizeof(int) +
+                            (size_t)kSahWarps * kSahBinSlots * 7 * sizeof(uint32_t) +
+                            (size_t)32 * kSahWarps * 32 + 4 * sizeof(int);
+
+// A node of k <= kSahSmall triangles (slots [a + s, a + e), node id nid): the
+// SAH-optimal binary tree over them (treelet_dp: every topology), written with
+// its leaves in depth-first order and the Karras numbering.
+__device__ void sah_small(int a, int s, int e, int nid, const float* s_lo, const float* s_hi, uint16_t* pm,
+                          float4* nodes, int32_t* parent, int n_nodes, unsigned char* row_popt) {
+    const int k = e - s;
+    float lo[kTLm][3], hi[kTLm][3], lc[kTLm];
+    int q[kTLm];
+#pragma unroll
+    for (int i = 0; i < kTLm; ++i) {
+        q[i] = i < k ? pm[s + i] : 0;
+#pragma unroll
+        for (int x = 0; x < 3; ++x) {
+            lo[i][x] = i < k ? s_lo[x * kSahSub + q[i]] : 0.0f;
+            hi[i][x] = i < k ? s_hi[x * kSahSub + q[i]] : 0.0f;
+        }
+        lc[i] = kCt * box_area(lo[i], hi[i]);
+    }
+    if (k == 2) {
+        row_popt[3] = 1;
+    } else if (kTLm >= 5 && k == 5) {
+        treelet_dp<(kTLm >= 5 ? 5 : 3)>(lo, hi, lc, row_popt);
+    } else if (kTLm >= 4 && k == 4) {
+        treelet_dp<(kTLm >= 4 ? 4 : 3)>(lo, hi, lc, row_popt);
+    } else {
+        treelet_dp<3>(lo, hi, lc, row_popt);
+    }
+    // depth-first: (member set, first slot, node id); the left part holds the lowest member
+    int st_set[kTLm], st_lo[kTLm], st_id[kTLm], sp = 0;
+    uint16_t out[kTLm];
+    st_set[0] = (1 << k) - 1;
+    st_lo[0] = a + s;
+    st_id[0] = nid;
+    sp = 1;
+    while (sp > 0) {
+        --sp;
+        const int set = st_set[sp], l0 = st_lo[sp], id = st_id[sp];
+        const int pl = row_popt[set], pr = set ^ pl;
+        const int nl = __popc(pl), nr = __popc(pr);
+        const int32_t left = nl == 1 ? ~l0 : l0 + nl - 1;
+        const int32_t right = nr == 1 ? ~(l0 + nl) : l0 + nl;
+        *reinterpret_cast<int4*>(nodes + 4 * id + 3) = make_int4(left, right, l0, l0 + nl + nr - 1);
+        parent[left >= 0 ? left : n_nodes + ~left] = (id << 1) | 0;
+        parent[right >= 0 ? right : n_nodes + ~right] = (id << 1) | 1;
+        if (nl == 1) out[l0 - (a + s)] = (uint16_t)q[__ffs(pl) - 1];
+        if (nr == 1) out[l0 + nl - (a + s)] = (uint16_t)q[__ffs(pr) - 1];
+        // right first on the stack so the left subtree is expanded next (slots are explicit anyway)
+        if (nr >= 2) {
+            st_set[sp] = pr;
+            st_lo[sp] = l0 + nl;
+            st_id[sp] = right;
+            ++sp;
+        }
+        if (nl >= 2) {
+            st_set[sp] = pl;
+            st_lo[sp] = l0;
+            st_id[sp] = left;
+            ++sp;
+        }
+    }
+    for (int i = 0; i < k; ++i) pm[s + i] = out[i];
+}
+
+__global__ void __launch_bounds__(32 * kSahWarps, 1) k_sah_sub(const float* __restrict__ V, int64_t nv,
+                                                               const int32_t* __restrict__ T, int32_t* vals,
+                                                               float4* nodes, int32_t* parent, int n_nodes,
+                                                               const int32_t* __restrict__ list, const uint32_t* scratch) {
+    extern __shared__ uint4 s_sah_dyn[];
+    float* s_f = reinterpret_cast<float*>(s_sah_dyn);
+    float* s_lo = s_f;                   // [3][kSahSub]
+    float* s_hi = s_f + 3 * kSahSub;     // [3][kSahSub]
+    float* s_c = s_f + 6 * kSahSub;      // [3][kSahSub]  (3 x centroid)
+    int32_t* s_id = reinterpret_cast<int32_t*>(s_f + 9 * kSahSub);
+    uint16_t* s_perm = reinterpret_cast<uint16_t*>(s_id + kSahSub);  // [2][kSahSub]
+    int* s_task = reinterpret_cast<int*>(s_perm + 2 * kSahSub);      // [2][kSahSub / 2][3]
+    int* s_small = s_task + 2 * (kSahSub / 2) * 3;                                   // [kSahSub / 2][3]
+    uint32_t* s_bins = reinterpret_cast<uint32_t*>(s_small + (kSahSub / 2) * 3);     // [warps][slots][7]
+    unsigned char* s_popt = reinterpret_cast<unsigned char*>(s_bins + kSahWarps * kSahBinSlots * 7);  // [threads][32]
+    int* s_ntask = reinterpret_cast<int*>(s_popt + 32 * kSahWarps * 32);             // [2], then the small count
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t lt = (1u << lane) - 1u;
+    const int n_sub = (int)scratch[SCR_SAH_COUNT];
+    uint32_t* bins = s_bins + warp * kSahBinSlots * 7;
+    // this lane's (axis, bin) pair in the SAH scan
+    const int my_ax = lane / kSahBins, my_b = lane % kSahBins;
+    const bool my_in = lane < kSahBinSlots;
+    for (int si = blockIdx.x; si < n_sub; si += gridDim.x) {
+        const int root = list[si];
+        const int4 rr = *reinterpret_cast<const int4*>(nodes + 4 * root + 3);
+        const int a = rr.z, m = rr.w - rr.z + 1;
+        // the subtree's triangles: exact fp32 boxes and centroids (x 3)
+        for (int t = threadIdx.x; t < m; t += blockDim.x) {
+            const int32_t id = vals[a + t];
+            const int32_t i0 = safe_index(T[3 * id], nv), i1 = safe_index(T[3 * id + 1], nv),
+                          i2 = safe_index(T[3 * id + 2], nv);
+#pragma unroll
+            for (int x = 0; x < 3; ++x) {
+                const float p0 = V[3 * i0 + x], p1 = V[3 * i1 + x], p2 = V[3 * i2 + x];
+                s_lo[x * kSahSub + t] = fminf(p0, fminf(p1, p2));
+                s_hi[x * kSahSub + t] = fmaxf(p0, fmaxf(p1, p2));
+                s_c[x * kSahSub + t] = (p0 + p1) + p2;
+            }
+            s_id[t] = id;
+            s_perm[t] = (uint16_t)t;
+        }
+        if (threadIdx.x == 0) {
+            const bool small = m <= kSahSmall;
+            int* t0 = small ? s_small : s_task;
+            t0[0] = 0;
+            t0[1] = m;
+            t0[2] = root;
+            s_ntask[0] = small ? 0 : 1;
+            s_ntask[1] = 0;
+            s_ntask[2] = small ? 1 : 0;
+        }
+        __syncthreads();
+        int cur = 0;
+        while (true) {
+            const int nt = s_ntask[cur];
+            if (nt == 0) break;
+            const int* tl = s_task + cur * (kSahSub / 2) * 3;
+            for (int ti = warp; ti < nt; ti += kSahWarps) {
+                const int s = tl[3 * ti], e = tl[3 * ti + 1], nid = tl[3 * ti + 2];
+                const int k = e - s;
+                uint16_t* pm = s_perm;
+                uint16_t* pt = s_perm + kSahSub;
+                int nl = k >> 1;  // fallback: median of the current order
+                int best_ax = -1, best_b = 0;
+                float cmin[3] = {0.0f, 0.0f, 0.0f}, scale[3] = {0.0f, 0.0f, 0.0f};
+                if (k > 2) {
+                    // centroid bounds: order-preserving keys, one REDUX per bound
+                    uint32_t kmin[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, kmax[3] = {0u, 0u, 0u};
+                    for (int j = s + lane; j < e; j += 32) {
+                        const int q = pm[j];
+#pragma unroll
+                        for (int x = 0; x < 3; ++x) {
+                            const uint32_t kc = fkey(s_c[x * kSahSub + q]);
+                            kmin[x] = min(kmin[x], kc);
+                            kmax[x] = max(kmax[x], kc);
+                        }
+                    }
+#pragma unroll
+                    for (int x = 0; x < 3; ++x) {
+                        cmin[x] = fdekey(__reduce_min_sync(FULL, kmin[x]));
+                        const float w = fdekey(__reduce_max_sync(FULL, kmax[x])) - cmin[x];
+                        const float sv = (float)kSahBins / w;
+                        scale[x] = (w > 0.0f && sv < 1e30f) ? sv : 0.0f;  // degenerate / non-finite axis: not split
+                    }
+                }
+                if (k > 2 && (scale[0] > 0.0f || scale[1] > 0.0f || scale[2] > 0.0f)) {
+                    for (int w = lane; w < kSahBinSlots * 7; w += 32) {
+                        const int f = w % 7;
+                        bins[w] = f == 0 ? 0u : (f <= 3 ? 0xffffffffu : 0u);
+                    }
+                    __syncwarp();
+                    for (int j = s + lane; j < e; j += 32) {
+                        const int q = pm[j];
+                        const uint32_t l0 = fkey(s_lo[q]), l1 = fkey(s_lo[kSahSub + q]), l2 = fkey(s_lo[2 * kSahSub + q]);
+                        const uint32_t h0 = fkey(s_hi[q]), h1 = fkey(s_hi[kSahSub + q]), h2 = fkey(s_hi[2 * kSahSub + q]);
+#pragma unroll
+                        for (int x = 0; x < 3; ++x) {
+                            if (scale[x] == 0.0f) continue;
+                            const int b = max(0, min(kSahBins - 1, (int)((s_c[x * kSahSub + q] - cmin[x]) * scale[x])));
+                            uint32_t* bb = bins + (x * kSahBins + b) * 7;
+                            atomicAdd(bb, 1u);
+                            atomicMin(bb + 1, l0);
+                            atomicMin(bb + 2, l1);
+                            atomicMin(bb + 3, l2);
+                            atomicMax(bb + 4, h0);
+                            atomicMax(bb + 5, h1);
+                            atomicMax(bb + 6, h2);
+                        }
+                    }
+                    __syncwarp();
+                    // SAH over every (axis, plane) at once: lane = axis * kSahBins + bin;
+                    // inclusive prefix / suffix over the axis's bins by segmented shuffles
+                    const uint32_t* bb = bins + (my_in ? lane : 0) * 7;
+                    const float sc_ax = my_ax == 0 ? scale[0] : (my_ax == 1 ? scale[1] : scale[2]);
+                    const bool act = my_in && sc_ax > 0.0f;
+                    const uint32_t cnt = act ? bb[0] : 0u;
+                    float plo[3], phi[3], slo[3], shi[3];
+#pragma unroll
+                    for (int y = 0; y < 3; ++y) {
+                        plo[y] = slo[y] = cnt ? fdekey(bb[1 + y]) : INFINITY;
+                        phi[y] = shi[y] = cnt ? fdekey(bb[4 + y]) : -INFINITY;
+                    }
+                    uint32_t pc = cnt, scn = cnt;
+#pragma unroll
+                    for (int o = 1; o < kSahBins; o <<= 1) {
+                        const uint32_t uc = __shfl_up_sync(FULL, pc, o), dc = __shfl_down_sync(FULL, scn, o);
+                        const bool up = my_b >= o, dn = my_b + o < kSahBins;
+                        pc += up ? uc : 0u;
+                        scn += dn ? dc : 0u;
+#pragma unroll
+                        for (int y = 0; y < 3; ++y) {
+                            const float ul = __shfl_up_sync(FULL, plo[y], o), uh = __shfl_up_sync(FULL, phi[y], o);
+                            const float dl = __shfl_down_sync(FULL, slo[y], o), dh = __shfl_down_sync(FULL, shi[y], o);
+                            if (up) { plo[y] = fminf(plo[y], ul); phi[y] = fmaxf(phi[y], uh); }
+                            if (dn) { slo[y] = fminf(slo[y], dl); shi[y] = fmaxf(shi[y], dh); }
+                        }
+                    }
+                    // plane after bin b: left = prefix(b), right = suffix(b + 1)
+                    const uint32_t rc = __shfl_down_sync(FULL, scn, 1);
+                    float rlo[3], rhi[3];
+#pragma unroll
+                    for (int y = 0; y < 3; ++y) {
+                        rlo[y] = __shfl_down_sync(FULL, slo[y], 1);
+                        rhi[y] = __shfl_down_sync(FULL, shi[y], 1);
+                    }
+                    float cost = INFINITY;
+                    if (act && my_b < kSahBins - 1 && pc > 0u && rc > 0u) {
+                        const float lx = phi[0] - plo[0], ly = phi[1] - plo[1], lz = phi[2] - plo[2];
+                        const float rx = rhi[0] - rlo[0], ry = rhi[1] - rlo[1], rz = rhi[2] - rlo[2];
+                        cost = (lx * ly + ly * lz + lz * lx) * (float)pc + (rx * ry + ry * rz + rz * rx) * (float)rc;
+                    }
+                    // warp argmin (ties: lowest lane), as one 64-bit key: cost bits (>= 0) | lane
+                    const unsigned long long key =
+                        ((unsigned long long)__float_as_uint(cost) << 32) | (unsigned)lane;
+                    unsigned long long bk = key;
+#pragma unroll
+                    for (int o = 16; o; o >>= 1) {
+                        const unsigned long long ok = __shfl_xor_sync(FULL, bk, o);
+                        bk = ok < bk ? ok : bk;
+                    }
+                    const int bl = (int)(bk & 31u);
+                    const int ncl = __shfl_sync(FULL, (int)pc, bl);
+                    if (__uint_as_float((uint32_t)(bk >> 32)) < INFINITY) {
+                        best_ax = bl / kSahBins;
+                        best_b = bl % kSahBins;
+                        nl = ncl;
+                    }
+                }
+                // partition the node's slice of the permutation (warp-ordered, stable)
+                {
+                    const float cm = best_ax == 0 ? cmin[0] : (best_ax == 1 ? cmin[1] : cmin[2]);
+                    const float sc = best_ax == 0 ? scale[0] : (best_ax == 1 ? scale[1] : scale[2]);
+                    const float* cax = s_c + (best_ax > 0 ? best_ax : 0) * kSahSub;
+                    int base_l = s, base_r = s + nl;
+                    for (int j0 = s; j0 < e; j0 += 32) {
+                        const int j = j0 + lane;
+                        const bool v = j < e;
+                        const int q = v ? pm[j] : 0;
+                        const bool left = best_ax >= 0
+                                              ? max(0, min(kSahBins - 1, (int)((cax[q] - cm) * sc))) <= best_b
+                                              : j < s + nl;
+                        const unsigned bl = __ballot_sync(FULL, v && left), br = __ballot_sync(FULL, v && !left);
+                        if (v) pt[left ? base_l + __popc(bl & lt) : base_r + __popc(br & lt)] = (uint16_t)q;
+                        base_l += __popc(bl);
+                        base_r += __popc(br);
+                    }
+                    __syncwarp();
+                    for (int j = s + lane; j < e; j += 32) pm[j] = pt[j];
+                    __syncwarp();
+                }
+                // node nid: children [s, s + nl) and [s + nl, e), Karras numbering
+                if (lane == 0) {
+                    const int ls = a + s, rs = a + s + nl;
+                    const int32_t left = nl == 1 ? ~ls : rs - 1;
+                    const int32_t right = e - (s + nl) == 1 ? ~rs : rs;
+                    *reinterpret_cast<int4*>(nodes + 4 * nid + 3) = make_int4(left, right, a + s, a + e - 1);
+                    parent[left >= 0 ? left : n_nodes + ~left] = (nid << 1) | 0;
+                    parent[right >= 0 ? right : n_nodes + ~right] = (nid << 1) | 1;
+                    const int nxt = cur ^ 1;
+                    int* tn = s_task + nxt * (kSahSub / 2) * 3;
+                    // children of > kSahSmall triangles: the next level's warp tasks; smaller: one thread each
+                    if (nl >= 2) {
+                        const bool sm = nl <= kSahSmall;
+                        const int w = atomicAdd(sm ? &s_ntask[2] : &s_ntask[nxt], 1);
+                        int* d = sm ? s_small : tn;
+                        d[3 * w] = s;
+                        d[3 * w + 1] = s + nl;
+                        d[3 * w + 2] = left;
+                    }
+                    if (k - nl >= 2) {
+                        const bool sm = k - nl <= kSahSmall;
+                        const int w = atomicAdd(sm ? &s_ntask[2] : &s_ntask[nxt], 1);
+                        int* d = sm ? s_small : tn;
+                        d[3 * w] = s + nl;
+                        d[3 * w + 1] = e;
+                        d[3 * w + 2] = right;
+                    }
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) s_ntask[cur] = 0;
+            cur ^= 1;
+            __syncthreads();
+        }
+        // the small nodes, one thread each (disjoint slices of the permutation)
+        const int ns = s_ntask[2];
+        for (int t = threadIdx.x; t < ns; t += blockDim.x)
+            sah_small(a, s_small[3 * t], s_small[3 * t + 1], s_small[3 * t + 2], s_lo, s_hi, s_perm, nodes, parent,
+                      n_nodes, s_popt + 32 * threadIdx.x);
+        __syncthreads();
+        // the leaf slots' triangles in the new order
+        for (int t = threadIdx.x; t < m; t += blockDim.x) vals[a + t] = s_id[s_perm[t]];
+        __syncthreads();
     }
 }
 
@@ -1751,11 +2135,26 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
                                                                               h->arrivals, n_nodes, rank);
         launch_sort(h, n, s);
         rsi_note_launch(), k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent, h->arrivals);
+        const bool sah_sub = RSI_SAH_SUB > 0 && !(h->opt.flags & (RSI_OPT_PLAIN_TREE | RSI_OPT_ROTATE)) &&
+                             refit_leaves == n && n >= 3 && n <= kSahMaxTri;
+        if (sah_sub) {  // (keys_tmp is free after the sort: the subtree list)
+            int32_t* list = reinterpret_cast<int32_t*>(h->keys_tmp);
+            rsi_note_launch(), k_sah_roots<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, h->parent, n_nodes,
+                                                                                          list, h->scratch);
+            const int g = rsi_ceil_div(n, 3) < kSahGrid ? rsi_ceil_div(n, 3) : kSahGrid;
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_sah_sub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSahSmem);
+                attr = true;
+            }
+            rsi_note_launch(), k_sah_sub<<<g, 32 * kSahWarps, kSahSmem, s>>>(V, nv, T, h->vals, h->nodes, h->parent, n_nodes,
+                                                                     list, h->scratch);
+        }
         rsi_note_launch(), k_refit<<<rsi_ceil_div(refit_leaves, kRefitLeaves), kRefitLeaves, 0, s>>>(V, nv, T, h->vals, refit_leaves, n, h->nodes,
                                                                        h->tris, h->parent, h->arrivals, h->scratch,
                                                                        (h->opt.flags & RSI_OPT_ROTATE) ? 1 : 0,
                                                                        (h->opt.flags & (RSI_OPT_PLAIN_TREE | RSI_OPT_ROTATE)) || refit_leaves < n ||
-                                                                               n > kTreeletMaxTri ? 0 : 1);
+                                                                               n > kTreeletMaxTri || (sah_sub && !RSI_SAH_TREELET) ? 0 : 1);
     }
     if (n_nodes <= kQCompactMax && h->qfull) {  // records of every node, then the live ones, breadth-first
         rsi_note_launch(), k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->qfull, h->scratch);
@@ -1840,4 +2239,81 @@ rsi_status_t rsi_validate_device(rsi_bvh* h, rsi_integrity_t* report, cudaStream
     report->unreachable_leaves = (int64_t)v[V_UNREACH];
     report->root_ok = root_set ? 1 : 0;
     return RSI_OK;
+}
+
+// rsi_bvh_upload: replace the handle's binary tree by a caller-given topology
+// over the same mesh (the inverse of rsi_bvh_download; a debugging and
+// tree-quality experiment hook: the walk is exact for ANY valid tree, since a
+// BVH only prunes).  Host inputs: child refs / child boxes in the download
+// layout, the triangle at each leaf slot, the root node.  The triangle records
+// are permuted into the new slot order, then the 4-wide records are rebuilt
+// from the uploaded nodes exactly as after a build.
+rsi_status_t rsi_bvh_upload_device(rsi_bvh* h, const int32_t* h_child, const float* h_box,
+                                   const int32_t* h_leaf_tri, int64_t root, cudaStream_t s) {
+    const int64_t nn = h->n_nodes, nt = h->n_tri;
+    if (nt < 2 || root < 0 || root >= nn)
+        return rsi_set_error(RSI_E_INVALID_ARG, "upload needs N_t >= 2 and a root in [0, n_nodes)");
+    float4* tris = new (std::nothrow) float4[kTriF4 * nt];
+    float4* ntris = new (std::nothrow) float4[kTriF4 * nt];
+    float4* nodes = new (std::nothrow) float4[4 * nn];
+    int64_t* slot_of = new (std::nothrow) int64_t[nt];
+    rsi_status_t st = (tris && ntris && nodes && slot_of) ? RSI_OK : rsi_set_error(RSI_E_OOM, "host allocation failed");
+    if (st == RSI_OK)
+        st = rsi_cuda_check(cudaMemcpyAsync(tris, h->tris, nt * kTriF4 * sizeof(float4), cudaMemcpyDeviceToHost, s), "tris");
+    if (st == RSI_OK) st = rsi_cuda_check(cudaStreamSynchronize(s), "tris");
+    if (st == RSI_OK) {
+        for (int64_t i = 0; i < nt; ++i) slot_of[i] = -1;
+        for (int64_t k = 0; k < nt; ++k) {
+            int32_t id;
+            std::memcpy(&id, &tris[kTriF4 * k].w, 4);
+            if (id >= 0 && id < nt) slot_of[id] = k;
+        }
+        for (int64_t k = 0; k < nt && st == RSI_OK; ++k) {
+            const int32_t id = h_leaf_tri[k];
+            if (id < 0 || id >= nt || slot_of[id] < 0) {
+                st = rsi_set_error(RSI_E_INVALID_ARG, "leaf slot %lld: triangle %d", (long long)k, id);
+                break;
+            }
+            for (int f = 0; f < kTriF4; ++f) ntris[kTriF4 * k + f] = tris[kTriF4 * slot_of[id] + f];
+        }
+    }
+    if (st == RSI_OK) {
+        for (int64_t i = 0; i < nn; ++i) {
+            const float* b = h_box + 12 * i;  // [2][6]: lo xyz, hi xyz per side
+            nodes[4 * i + 0] = make_float4(b[0], b[3], b[1], b[4]);
+            nodes[4 * i + 1] = make_float4(b[6], b[9], b[7], b[10]);
+            nodes[4 * i + 2] = make_float4(b[2], b[5], b[8], b[11]);
+            float4 r;
+            std::memcpy(&r.x, &h_child[2 * i], 4);
+            std::memcpy(&r.y, &h_child[2 * i + 1], 4);
+            r.z = r.w = 0.0f;
+            nodes[4 * i + 3] = r;
+        }
+        st = rsi_cuda_check(cudaMemcpyAsync(h->nodes, nodes, nn * 4 * sizeof(float4), cudaMemcpyHostToDevice, s), "nodes");
+    }
+    if (st == RSI_OK)
+        st = rsi_cuda_check(cudaMemcpyAsync(h->tris, ntris, nt * kTriF4 * sizeof(float4), cudaMemcpyHostToDevice, s), "tris");
+    if (st == RSI_OK) {
+        const int n_nodes = (int)nn;
+        rsi_note_launch(), k_build_init<<<1, 32, 0, s>>>(h->scratch, (uint32_t)root);
+        if (n_nodes <= kQCompactMax && h->qfull) {
+            rsi_note_launch(), k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->qfull, h->scratch);
+            rsi_note_launch(), k_qcompact<<<1, 1024, 0, s>>>(h->qfull, h->quads, h->qorder, h->qmap, h->scratch);
+        } else {
+            rsi_note_launch(), k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads, h->scratch);
+            rsi_note_launch(), k_qroot_copy<<<1, 1, 0, s>>>(h->scratch);
+        }
+        if (kQTop > 0) rsi_note_launch(), k_qtop<<<1, 256, 0, s>>>(h->quads, h->top, h->scratch);
+        st = rsi_cuda_check(cudaGetLastError(), "upload kernels");
+    }
+    if (st == RSI_OK) st = rsi_cuda_check(cudaStreamSynchronize(s), "upload");
+    if (st == RSI_OK) {
+        h->apetrei = false;
+        h->root_node = root;
+    }
+    delete[] tris;
+    delete[] ntris;
+    delete[] nodes;
+    delete[] slot_of;
+    return st;
 }

@@ -39,6 +39,7 @@ enum {
     SCR_QEMAX = 24,
     SCR_ROOT_NODE = 25, // root internal node (0 Karras; Apetrei: top split; 0xffffffff unset)
     SCR_QROOT = 26,     // root of the 4-wide records the walks read (0 after compaction; 0xffffffff unset)
+    SCR_SAH_COUNT = 27, // SAH-rebuilt subtrees in this build (k_sah_roots)
     SCR_SORT_DONE = 32, // 32 words: per-block slice counters of the rank sort
     SCR_WORDS = 64
 };
@@ -113,6 +114,8 @@ void rsi_keep_pool_cached();
 rsi_status_t rsi_build_device(rsi_bvh* h, const float* d_vertices, int64_t n_vertices,
                               const int32_t* d_triangles, int64_t n_triangles,
                               cudaStream_t stream);
+rsi_status_t rsi_bvh_upload_device(rsi_bvh* h, const int32_t* h_child, const float* h_box,
+                                   const int32_t* h_leaf_tri, int64_t root, cudaStream_t stream);
 // traverse.cu
 rsi_status_t rsi_intersect_device(rsi_bvh* h, const float* d_start, const float* d_end,
                                   int64_t n_rays, int32_t mode, const rsi_outputs_t* out,

@@ -97,6 +97,7 @@ def load():
             "rsi_reset_stats": ([_p, _p], ctypes.c_int),
             "rsi_bvh_info": ([_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _p, _p], ctypes.c_int),
             "rsi_bvh_download": ([_p, _p, _p, _p, _p, _p, _p, _p], ctypes.c_int),
+            "rsi_bvh_upload": ([_p, _p, _p, _p, _i64, _p], ctypes.c_int),
             "rsi_validate": ([_p, ctypes.POINTER(_Integrity), _p], ctypes.c_int),
             "rsi_bvh_root": ([_p, ctypes.POINTER(_i64), ctypes.POINTER(_i64), _p, _p], ctypes.c_int),
             "rsi_test_sparse": ([_p, _i64, _p, _i64, _p, _p, _i64, _p, _p, _p, _p, _p, ctypes.POINTER(_i64), _p],
@@ -451,6 +452,21 @@ def rsi_bvh_download(h: Handle, stream=None) -> dict:
     d.update(info)
     d.update(rsi_bvh_root(h, stream))
     return d
+
+
+def rsi_bvh_upload(h: Handle, child, box, leaf_tri, root: int, stream=None) -> None:
+    """Replace the handle's binary tree by a host-given one over the same mesh
+    (the layout of rsi_bvh_download: child [n_nodes, 2] int32, box [n_nodes, 2, 6]
+    float32, leaf_tri [N_t] int32, root node) and rebuild the 4-wide records."""
+    info = rsi_bvh_info(h)
+    nt, nn = info["n_triangles"], info["n_nodes"]
+    child = np.ascontiguousarray(child, np.int32)
+    box = np.ascontiguousarray(box, np.float32)
+    leaf_tri = np.ascontiguousarray(leaf_tri, np.int32)
+    if child.shape != (nn, 2) or box.shape != (nn, 2, 6) or leaf_tri.shape != (nt,):
+        raise ValueError(f"upload shapes {child.shape} {box.shape} {leaf_tri.shape} for N_t={nt}, n_nodes={nn}")
+    _check(load().rsi_bvh_upload(h.ptr, child.ctypes.data_as(_p), box.ctypes.data_as(_p),
+                                 leaf_tri.ctypes.data_as(_p), int(root), _stream(stream)))
 
 
 def rsi_bvh_root(h: Handle, stream=None) -> dict:

@@ -342,12 +342,9 @@ def test_bvh_integrity_random_meshes(rsi, nt):
     if dup:
         T = T[:40][rng.integers(0, 40, nt)]
     Vd, Td = to_dev(V, T)
-    h = rsi.rsi_build(Vd, Td)
+    h = rsi.rsi_build(Vd, Td, rsi.Options(plain_tree=True))  # the Karras tree over the sorted codes
     d = rsi.rsi_bvh_download(h)
     h.free()
-    nn = d["n_nodes"]
-    assert sorted(d["leaf_tri"].tolist()) == list(range(nt))
-    assert (d["arrivals"] == 2).all()
     # morton reference (bit loop) on fp32 centroids
     lo, hi = V.min(0), V.max(0)
     c = (V[T[:, 0]] + V[T[:, 1]] + V[T[:, 2]]) / np.float32(3)
@@ -360,11 +357,27 @@ def test_bvh_integrity_random_meshes(rsi, nt):
     order = np.argsort(code, kind="stable")
     assert (d["morton"] == code[order]).all()
     assert (d["leaf_tri"] == order).all()
+    _check_tree(d, V, T, nt, contiguous=True)
+    # the default build (SAH-rebuilt subtrees + treelets over the same codes): the same invariants
+    h = rsi.rsi_build(Vd, Td)
+    d = rsi.rsi_bvh_download(h)
+    h.free()
+    assert (d["morton"] == code[order]).all()
+    _check_tree(d, V, T, nt)
+
+
+def _check_tree(d, V, T, nt, contiguous=False):
+    """Leaf bijection, arrivals == 2, mutual parent / child links, child boxes
+    equal to the exact unions; `contiguous`: every node over a contiguous range
+    of leaf slots with its id at one end of it (the Karras numbering)."""
+    nn = d["n_nodes"]
+    assert sorted(d["leaf_tri"].tolist()) == list(range(nt))
+    assert (d["arrivals"] == 2).all()
     if nt == 1:
         return
     # boxes: recompute bottom-up and compare exactly
     tb = np.concatenate([V[T].min(1), V[T].max(1)], 1)  # per original triangle
-    box = {}
+    box, rng = {}, {}
 
     def node_box(ref):
         if ref < 0:
@@ -372,6 +385,9 @@ def test_bvh_integrity_random_meshes(rsi, nt):
         if ref in box:
             return box[ref]
         raise KeyError
+
+    def node_rng(ref):
+        return (~ref, ~ref) if ref < 0 else rng[ref]
 
     parent = d["parent"]
     assert parent[0] == -1
@@ -390,6 +406,11 @@ def test_bvh_integrity_random_meshes(rsi, nt):
             got_l, got_r = d["box"][i]
             assert (got_l == l).all() and (got_r == r).all()
             box[i] = exp[0]
+            if contiguous:
+                (a0, a1), (b0, b1) = (node_rng(x) for x in d["child"][i])
+                assert a1 + 1 == b0, (i, a0, a1, b0, b1)
+                rng[i] = (a0, b1)
+                assert i in (a0, b1)
         else:
             stack.append((i, True))
             for ch in d["child"][i]:

@@ -298,6 +298,101 @@ def restructure(nodes, root, TL=7, passes=2, minleaves=1):
         print(f"pass {it}: improved {improved} treelets, root cost {cost[root]:.4g}", flush=True)
     return [tuple(x) for x in child], root
 
+# ---- hybrid trees: SAH over the top down to subsets of <= S_top
+# triangles with the Morton/Karras topology inside them, or the Karras topology
+# with every subtree of <= S_bot leaves rebuilt by binned SAH
+_lo_all, _hi_all = tlo.min(0), thi.max(0)
+_W = (_hi_all - _lo_all).max()
+_w = np.maximum(_hi_all - _lo_all, _W / 64)
+_q = np.clip(np.floor((cen - _lo_all) / _w * 1024), 0, 1023).astype(np.uint64)
+code = expand10(_q[:, 2]) | (expand10(_q[:, 1]) << 1) | (expand10(_q[:, 0]) << 2)
+def area(lo, hi):
+    e = np.maximum(hi - lo, 0); return e[..., 0]*e[..., 1] + e[..., 1]*e[..., 2] + e[..., 2]*e[..., 0]
+def build_sahtop(S_top, nbins=32, mode="sah_top"):
+    nodes = []
+    def lb(idx):  # Karras over idx sorted by code
+        o = idx[np.argsort(code[idx], kind="stable")]; cs = code[o]
+        def rec(i, j):
+            if i == j: return ~int(o[i])
+            if cs[i] == cs[j]: m = (i + j) // 2
+            else:
+                x = int(cs[i]) ^ int(cs[j]); b = x.bit_length() - 1
+                lo_, hi_ = i, j
+                while hi_ - lo_ > 1:
+                    mid = (lo_ + hi_) // 2
+                    if (int(cs[mid]) >> b) == (int(cs[i]) >> b): lo_ = mid
+                    else: hi_ = mid
+                m = lo_
+            k = len(nodes); nodes.append(None); nodes[k] = (rec(i, m), rec(m + 1, j)); return k
+        return rec(0, len(o) - 1)
+    def sah(idx):
+        if len(idx) == 1: return ~int(idx[0])
+        if mode == "sah_top" and len(idx) <= S_top: return lb(idx)
+        c = cen[idx]; clo, chi = c.min(0), c.max(0); best = (np.inf, None)
+        for ax in range(3):
+            if chi[ax] - clo[ax] <= 0: continue
+            b = np.minimum(((c[:, ax] - clo[ax]) / (chi[ax] - clo[ax]) * nbins).astype(int), nbins - 1)
+            blo = np.full((nbins, 3), np.inf); bhi = np.full((nbins, 3), -np.inf); cnt = np.zeros(nbins)
+            for k in range(nbins):
+                m = b == k
+                if m.any(): blo[k] = tlo[idx[m]].min(0); bhi[k] = thi[idx[m]].max(0); cnt[k] = m.sum()
+            plo = np.minimum.accumulate(blo); phi = np.maximum.accumulate(bhi); pc = np.cumsum(cnt)
+            slo = np.minimum.accumulate(blo[::-1])[::-1]; shi = np.maximum.accumulate(bhi[::-1])[::-1]; sc = np.cumsum(cnt[::-1])[::-1]
+            for k in range(nbins - 1):
+                if pc[k] == 0 or sc[k + 1] == 0: continue
+                cost = area(plo[k], phi[k]) * pc[k] + area(slo[k + 1], shi[k + 1]) * sc[k + 1]
+                if cost < best[0]: best = (cost, (ax, b, k))
+        if best[1] is None: m = len(idx) // 2; L, R = idx[:m], idx[m:]
+        else: ax, b, k = best[1]; L, R = idx[b <= k], idx[b > k]
+        kk = len(nodes); nodes.append(None); nodes[kk] = (sah(L), sah(R)); return kk
+    return nodes, sah(np.arange(N))
+def build_lbtop(S_bot, nbins=32, S_min=1):
+    # Karras over everything; a subtree with <= S_bot leaves is rebuilt by binned SAH,
+    # down to S_min leaves (smaller sets: Karras splits of their Morton codes again)
+    o = np.argsort(code, kind="stable"); cs = code[o]; nodes = []
+    def karras_set(idx):  # idx in Morton order
+        if len(idx) == 1: return ~int(idx[0])
+        c = code[idx]
+        if c[0] == c[-1]: m = len(idx) // 2
+        else:
+            b = (int(c[0]) ^ int(c[-1])).bit_length() - 1
+            m = int(np.argmax((c >> np.uint64(b)) != (c[0] >> np.uint64(b))))
+        kk = len(nodes); nodes.append(None); nodes[kk] = (karras_set(idx[:m]), karras_set(idx[m:])); return kk
+    def sahb(idx):
+        if len(idx) == 1: return ~int(idx[0])
+        if len(idx) <= S_min: return karras_set(idx)
+        c = cen[idx]; clo, chi = c.min(0), c.max(0); best = (np.inf, None)
+        for ax in range(3):
+            if chi[ax] - clo[ax] <= 0: continue
+            b = np.minimum(((c[:, ax] - clo[ax]) / (chi[ax] - clo[ax]) * nbins).astype(int), nbins - 1)
+            blo = np.full((nbins, 3), np.inf); bhi = np.full((nbins, 3), -np.inf); cnt = np.zeros(nbins)
+            for k in range(nbins):
+                m = b == k
+                if m.any(): blo[k] = tlo[idx[m]].min(0); bhi[k] = thi[idx[m]].max(0); cnt[k] = m.sum()
+            plo = np.minimum.accumulate(blo); phi = np.maximum.accumulate(bhi); pc = np.cumsum(cnt)
+            slo = np.minimum.accumulate(blo[::-1])[::-1]; shi = np.maximum.accumulate(bhi[::-1])[::-1]; sc = np.cumsum(cnt[::-1])[::-1]
+            for k in range(nbins - 1):
+                if pc[k] == 0 or sc[k + 1] == 0: continue
+                cost = area(plo[k], phi[k]) * pc[k] + area(slo[k + 1], shi[k + 1]) * sc[k + 1]
+                if cost < best[0]: best = (cost, (ax, b, k))
+        if best[1] is None: m = len(idx) // 2; L, R = idx[:m], idx[m:]
+        else: ax, b, k = best[1]; L, R = idx[b <= k], idx[b > k]
+        kk = len(nodes); nodes.append(None); nodes[kk] = (sahb(L), sahb(R)); return kk
+    def rec(i, j):
+        if i == j: return ~int(o[i])
+        if j - i + 1 <= S_bot: return sahb(o[i:j + 1])
+        if cs[i] == cs[j]: m = (i + j) // 2
+        else:
+            x = int(cs[i]) ^ int(cs[j]); b = x.bit_length() - 1
+            lo_, hi_ = i, j
+            while hi_ - lo_ > 1:
+                mid = (lo_ + hi_) // 2
+                if (int(cs[mid]) >> b) == (int(cs[i]) >> b): lo_ = mid
+                else: hi_ = mid
+            m = lo_
+        k = len(nodes); nodes.append(None); nodes[k] = (rec(i, m), rec(m + 1, j)); return k
+    return nodes, rec(0, N - 1)
+
 nodes, r = lbvh()
 t = time.time()
 evaluate(nodes, r, "lbvh")

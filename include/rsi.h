@@ -366,7 +366,8 @@ rsi_status_t rsi_bvh_download(rsi_handle_t h, int32_t* h_child, float* h_box,
  *   Host buffers, read before return; synchronizes `stream`.  The next
  *   rsi_rebuild replaces the uploaded tree.
  * Errors: RSI_E_INVALID_ARG (null / N_t < 2 / root out of range / leaf_tri not
- *   a permutation), RSI_E_OOM, RSI_E_CUDA.
+ *   a permutation / a child ref out of range or a node or leaf not reached exactly once
+ *   from root), RSI_E_OOM, RSI_E_CUDA.
  */
 rsi_status_t rsi_bvh_upload(rsi_handle_t h, const int32_t* h_child, const float* h_box,
                             const int32_t* h_leaf_tri, int64_t root, void* stream);

@@ -20,6 +20,7 @@
 
 #include <cstring>
 #include <new>
+#include <vector>
 
 #include "rsi_internal.cuh"
 
@@ -2270,12 +2271,39 @@ rsi_status_t rsi_bvh_upload_device(rsi_bvh* h, const int32_t* h_child, const flo
         }
         for (int64_t k = 0; k < nt && st == RSI_OK; ++k) {
             const int32_t id = h_leaf_tri[k];
-            if (id < 0 || id >= nt || slot_of[id] < 0) {
-                st = rsi_set_error(RSI_E_INVALID_ARG, "leaf slot %lld: triangle %d", (long long)k, id);
+            if (id < 0 || id >= nt || slot_of[id] < 0) {  // (a used id is marked -1: not a permutation)
+                st = rsi_set_error(RSI_E_INVALID_ARG, "leaf slot %lld: triangle %d (leaf_tri must be a permutation)",
+                                   (long long)k, id);
                 break;
             }
             for (int f = 0; f < kTriF4; ++f) ntris[kTriF4 * k + f] = tris[kTriF4 * slot_of[id] + f];
+            slot_of[id] = -1;
         }
+    }
+    if (st == RSI_OK) {  // topology: every internal node and leaf slot reached exactly once from root
+        std::vector<unsigned char> seen((size_t)(nn + nt), 0);
+        std::vector<int64_t> todo(1, root);
+        seen[root] = 1;
+        int64_t reached = 1;
+        while (!todo.empty() && st == RSI_OK) {
+            const int64_t i = todo.back();
+            todo.pop_back();
+            for (int side = 0; side < 2; ++side) {
+                const int32_t c = h_child[2 * i + side];
+                const int64_t at = c >= 0 ? (int64_t)c : nn + (int64_t)~c;
+                if ((c >= 0 && c >= nn) || (c < 0 && (int64_t)~c >= nt) || seen[at]) {
+                    st = rsi_set_error(RSI_E_INVALID_ARG, "node %lld child %d: ref %d out of range or reached twice",
+                                       (long long)i, side, c);
+                    break;
+                }
+                seen[at] = 1;
+                ++reached;
+                if (c >= 0) todo.push_back(c);
+            }
+        }
+        if (st == RSI_OK && reached != nn + nt)
+            st = rsi_set_error(RSI_E_INVALID_ARG, "the tree reaches %lld of %lld nodes and leaves", (long long)reached,
+                               (long long)(nn + nt));
     }
     if (st == RSI_OK) {
         for (int64_t i = 0; i < nn; ++i) {

@@ -1023,3 +1023,83 @@ def test_treelet_restructuring_lowers_sah_same_results(rsi, wl):
     assert_parity(b, ref, S, E, wl)
     for k in ("hit", "count", "tri"):
         assert (a[k] == b[k]).all(), k
+
+
+def _median_tree(V, T, seed):
+    """A valid binary tree that is neither Karras nor SAH: recursive splits at a
+    random position of the triangles sorted along a random axis (host, numpy),
+    in the rsi_bvh_upload layout (internal nodes breadth-first from 0, leaf
+    slots depth-first, fp32 child boxes = exact unions)."""
+    rng = np.random.default_rng(seed)
+    tv = V[T]
+    tlo, thi, cen = tv.min(1), tv.max(1), tv.mean(1)
+    nodes = []
+
+    def build(idx):
+        if len(idx) == 1:
+            return ~int(idx[0])
+        ax = int(rng.integers(0, 3))
+        idx = idx[np.argsort(cen[idx, ax], kind="stable")]
+        m = int(rng.integers(1, len(idx)))
+        k = len(nodes)
+        nodes.append(None)
+        nodes[k] = (build(idx[:m]), build(idx[m:]))
+        return k
+
+    import sys
+    sys.setrecursionlimit(100000)
+    root = build(np.arange(len(T)))
+    order, pos = [root], {root: 0}
+    for n in order:
+        for c in nodes[n]:
+            if c >= 0:
+                pos[c] = len(order)
+                order.append(c)
+    slot, leaf_tri = {}, []
+
+    def dfs(n):
+        for c in nodes[n]:
+            if c < 0:
+                slot[~c] = len(leaf_tri)
+                leaf_tri.append(~c)
+            else:
+                dfs(c)
+
+    dfs(root)
+    nn = len(order)
+    child = np.zeros((nn, 2), np.int32)
+    box = np.zeros((nn, 2, 6), np.float32)
+    lo, hi = np.zeros((nn, 3), np.float32), np.zeros((nn, 3), np.float32)
+    for n in order[::-1]:
+        i = pos[n]
+        for s, c in enumerate(nodes[n]):
+            if c < 0:
+                child[i, s], b = ~slot[~c], (tlo[~c], thi[~c])
+            else:
+                child[i, s], b = pos[c], (lo[pos[c]], hi[pos[c]])
+            box[i, s, :3], box[i, s, 3:] = b
+        lo[i], hi[i] = np.minimum(box[i, 0, :3], box[i, 1, :3]), np.maximum(box[i, 0, 3:], box[i, 1, 3:])
+    return child, box, np.asarray(leaf_tri, np.int32)
+
+
+@pytest.mark.parametrize("wl", ["sphere", "terrain"])
+def test_bvh_upload_any_tree_same_results(rsi, wl):
+    """rsi_bvh_upload (the inverse of rsi_bvh_download): a host-built tree of
+    random splits replaces the built one; the 4-wide records are rebuilt from it
+    and every mode still equals the oracle element by element (the BVH only
+    prunes), and a download returns the uploaded topology."""
+    V, T, S, E, _ = synth.workload(wl, 20_011, seed=23)
+    ref = oracle.run(V, T, S, E)
+    child, box, leaf = _median_tree(V, T, 5)
+    Vd, Td, Sd, Ed = to_dev(V, T, S, E)
+    h = rsi.rsi_build(Vd, Td)
+    rsi.rsi_bvh_upload(h, child, box, leaf, 0)
+    d = rsi.rsi_bvh_download(h)
+    assert (d["child"] == child).all() and (d["box"] == box).all() and (d["leaf_tri"] == leaf).all()
+    got = {"hit": rsi.rsi_intersect(h, Sd, Ed, "boolean")["hit"].cpu().numpy()}
+    got.update({k: v.cpu().numpy() for k, v in rsi.rsi_intersect(h, Sd, Ed, "barycentric").items()})
+    got["count"] = rsi.rsi_intersect(h, Sd, Ed, "intercept_count")["count"].cpu().numpy()
+    assert_parity(got, ref, S, E, f"upload {wl}")
+    with pytest.raises(Exception):
+        rsi.rsi_bvh_upload(h, child, box, leaf[::-1].copy() * 0, 0)  # not a permutation
+    h.free()

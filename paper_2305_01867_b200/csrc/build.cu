@@ -351,7 +351,8 @@ __device__ __forceinline__ void set_ref(float4* nodes, int node, int side, int32
 // exponential + binary search, split position gamma, children and parents.
 __global__ void __launch_bounds__(kBlock) k_karras(const uint32_t* __restrict__ keys, int n,
                                                    float4* __restrict__ nodes, int32_t* __restrict__ parent,
-                                                   uint32_t* __restrict__ arrivals) {
+                                                   uint32_t* __restrict__ arrivals, int32_t* sah_list,
+                                                   uint32_t* scratch, int sah_max) {
     const int n_nodes = n > 1 ? n - 1 : 1;
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (n == 1) {  // single triangle: root holds leaf 0 on the left, an unhittable point at +inf on the right
@@ -397,6 +398,14 @@ __global__ void __launch_bounds__(kBlock) k_karras(const uint32_t* __restrict__ 
     parent[left >= 0 ? left : n_nodes + ~left] = (i << 1) | 0;
     parent[right >= 0 ? right : n_nodes + ~right] = (i << 1) | 1;
     if (i == 0) parent[0] = -1;
+    if (sah_list) {  // the SAH subtree roots (k_sah_sub): maximal nodes of 3 .. sah_max leaves
+        const int sz = hi - lo + 1, szl = gamma - lo + 1, szr = hi - gamma;
+        if (i == 0 && sz >= 3 && sz <= sah_max) sah_list[atomicAdd(scratch + SCR_SAH_COUNT, 1u)] = 0;
+        if (sz > sah_max) {
+            if (szl >= 3 && szl <= sah_max) sah_list[atomicAdd(scratch + SCR_SAH_COUNT, 1u)] = gamma;
+            if (szr >= 3 && szr <= sah_max) sah_list[atomicAdd(scratch + SCR_SAH_COUNT, 1u)] = gamma + 1;
+        }
+    }
 }
 
 // ------------------------------------------------------------------ A6 + A7: refit + pack
@@ -810,6 +819,7 @@ __device__ void treelet_opt(const Tree& tr, int n, unsigned char* row_popt) {
 #define RSI_SAH_MAX_TRI 32768
 #endif
 constexpr int64_t kSahMaxTri = RSI_SAH_MAX_TRI;
+constexpr int64_t kSahMinTri = 64;  // smaller meshes: the launch is not worth it
 constexpr int kSahSub = RSI_SAH_SUB > 0 ? RSI_SAH_SUB : 4;
 #ifndef RSI_SAH_BINS
 #define RSI_SAH_BINS 10  // bins per axis (3 x 10 <= 32 lanes: every plane of every axis in one warp pass)
@@ -825,22 +835,6 @@ __device__ __forceinline__ uint32_t fkey(float f) {  // order-preserving float -
 }
 __device__ __forceinline__ float fdekey(uint32_t k) {
     return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
-}
-
-// Subtree roots: internal node i with 3 <= leaves <= kSahSub whose parent has more (or i is the root).
-__global__ void __launch_bounds__(kBlock) k_sah_roots(const float4* __restrict__ nodes, const int32_t* __restrict__ parent,
-                                                      int n_nodes, int32_t* list, uint32_t* scratch) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n_nodes) return;
-    const int4 r = __ldg(reinterpret_cast<const int4*>(nodes + 4 * i + 3));
-    const int m = r.w - r.z + 1;
-    if (m < 3 || m > kSahSub) return;
-    if (i != 0) {
-        const int pn = __ldg(parent + i) >> 1;
-        const int4 pr = __ldg(reinterpret_cast<const int4*>(nodes + 4 * pn + 3));
-        if (pr.w - pr.z + 1 <= kSahSub) return;
-    }
-    list[atomicAdd(scratch + SCR_SAH_COUNT, 1u)] = i;
 }
 
 // Shared memory of k_sah_sub (dynamic): the subtree's boxes and 3 x centroids,
@@ -2135,13 +2129,12 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
         rsi_note_launch(), k_morton<<<rsi_ceil_div(n, kBlock), kBlock, 0, s>>>(V, nv, T, n, h->scratch, h->keys, h->vals,
                                                                               h->arrivals, n_nodes, rank);
         launch_sort(h, n, s);
-        rsi_note_launch(), k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent, h->arrivals);
         const bool sah_sub = RSI_SAH_SUB > 0 && !(h->opt.flags & (RSI_OPT_PLAIN_TREE | RSI_OPT_ROTATE)) &&
-                             refit_leaves == n && n >= 3 && n <= kSahMaxTri;
-        if (sah_sub) {  // (keys_tmp is free after the sort: the subtree list)
-            int32_t* list = reinterpret_cast<int32_t*>(h->keys_tmp);
-            rsi_note_launch(), k_sah_roots<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, h->parent, n_nodes,
-                                                                                          list, h->scratch);
+                             refit_leaves == n && n >= kSahMinTri && n <= kSahMaxTri;
+        int32_t* list = sah_sub ? reinterpret_cast<int32_t*>(h->keys_tmp) : nullptr;  // (free after the sort)
+        rsi_note_launch(), k_karras<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->keys, n, h->nodes, h->parent,
+                                                                                   h->arrivals, list, h->scratch, kSahSub);
+        if (sah_sub) {
             const int g = rsi_ceil_div(n, 3) < kSahGrid ? rsi_ceil_div(n, 3) : kSahGrid;
             static bool attr = false;
             if (!attr) {

@@ -1171,6 +1171,10 @@ __global__ void __launch_bounds__(32 * kSahWarps, 1) k_sah_sub(const float* __re
 #endif
 constexpr int kRefitLeaves = RSI_REFIT_LEAVES;
 
+// kT: the treelet restructuring is compiled in (its shared memory -- DP rows,
+// refs, costs: 11 KB per CTA -- and registers would cost the other builds
+// occupancy: N_t = 1e6 refit 467 -> see DESIGN.md 7).
+template <bool kT>
 __global__ void __launch_bounds__(kRefitLeaves) k_refit(const float* __restrict__ V, int64_t nv,
                                                         const int32_t* __restrict__ T,
                                                         const int32_t* __restrict__ vals, int n_leaves, int n,
@@ -1184,9 +1188,10 @@ __global__ void __launch_bounds__(kRefitLeaves) k_refit(const float* __restrict_
     const int c0 = blockIdx.x * kRefitLeaves;
     const int n_nodes = n > 1 ? n - 1 : 1;
     // the thread that completed a window node restructures its treelet
-    __shared__ unsigned char s_popt[kTL > 0 ? kRefitLeaves : 1][1 << kTLm];  // DP partition table, a row per thread
-    __shared__ int32_t s_ref[kTL > 0 ? kRefitLeaves : 1][2];
-    __shared__ float s_cost[kTL > 0 ? kRefitLeaves : 1];
+    constexpr bool kTr = kT && kTL > 0;
+    __shared__ unsigned char s_popt[kTr ? kRefitLeaves : 1][1 << kTLm];  // DP partition table, a row per thread
+    __shared__ int32_t s_ref[kTr ? kRefitLeaves : 1][2];
+    __shared__ float s_cost[kTr ? kRefitLeaves : 1];
     {
         // the window's slice of the tree, in bulk: one coalesced round trip
         // instead of a dependent L2 load per level of every ascent
@@ -1195,9 +1200,9 @@ __global__ void __launch_bounds__(kRefitLeaves) k_refit(const float* __restrict_
         const bool own = n > 1 && i < n_nodes;
         const int4 r3 = own ? __ldg(reinterpret_cast<const int4*>(nodes + 4 * i + 3)) : make_int4(0, 0, -1, -1);
         s_rng[threadIdx.x] = make_int2(r3.z, r3.w);
-        if (kTL > 0) {
-            s_ref[kTL > 0 ? threadIdx.x : 0][0] = r3.x;
-            s_ref[kTL > 0 ? threadIdx.x : 0][1] = r3.y;
+        if (kTr) {
+            s_ref[kTr ? threadIdx.x : 0][0] = r3.x;
+            s_ref[kTr ? threadIdx.x : 0][1] = r3.y;
         }
         s_par[threadIdx.x] = own ? __ldg(parent + i) : -1;
     }
@@ -1271,7 +1276,7 @@ __global__ void __launch_bounds__(kRefitLeaves) k_refit(const float* __restrict_
                 state = 1;
             }
         }
-        if (kTL > 0 && treelet && done_node >= 0) {
+        if (kTr && treelet && done_node >= 0) {
             const WindowTree tr{nodes, parent, n_nodes, c0, s_box, s_ref, s_cost};
             treelet_opt(tr, done_node, s_popt[threadIdx.x]);
         }
@@ -2144,11 +2149,15 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
             rsi_note_launch(), k_sah_sub<<<g, 32 * kSahWarps, kSahSmem, s>>>(V, nv, T, h->vals, h->nodes, h->parent, n_nodes,
                                                                      list, h->scratch);
         }
-        rsi_note_launch(), k_refit<<<rsi_ceil_div(refit_leaves, kRefitLeaves), kRefitLeaves, 0, s>>>(V, nv, T, h->vals, refit_leaves, n, h->nodes,
-                                                                       h->tris, h->parent, h->arrivals, h->scratch,
-                                                                       (h->opt.flags & RSI_OPT_ROTATE) ? 1 : 0,
-                                                                       (h->opt.flags & (RSI_OPT_PLAIN_TREE | RSI_OPT_ROTATE)) || refit_leaves < n ||
-                                                                               n > kTreeletMaxTri || (sah_sub && !RSI_SAH_TREELET) ? 0 : 1);
+        const int treelet = (h->opt.flags & (RSI_OPT_PLAIN_TREE | RSI_OPT_ROTATE)) || refit_leaves < n ||
+                                    n > kTreeletMaxTri || (sah_sub && !RSI_SAH_TREELET) ? 0 : 1;
+        const int rotate = (h->opt.flags & RSI_OPT_ROTATE) ? 1 : 0;
+        if (treelet)
+            rsi_note_launch(), k_refit<true><<<rsi_ceil_div(refit_leaves, kRefitLeaves), kRefitLeaves, 0, s>>>(
+                V, nv, T, h->vals, refit_leaves, n, h->nodes, h->tris, h->parent, h->arrivals, h->scratch, rotate, 1);
+        else
+            rsi_note_launch(), k_refit<false><<<rsi_ceil_div(refit_leaves, kRefitLeaves), kRefitLeaves, 0, s>>>(
+                V, nv, T, h->vals, refit_leaves, n, h->nodes, h->tris, h->parent, h->arrivals, h->scratch, rotate, 0);
     }
     if (n_nodes <= kQCompactMax && h->qfull) {  // records of every node, then the live ones, breadth-first
         rsi_note_launch(), k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->qfull, h->scratch);

@@ -995,7 +995,7 @@ __global__ void __launch_bounds__(32 * kSahWarps, 1) k_sah_sub(const float* __re
                     for (int x = 0; x < 3; ++x) {
                         cmin[x] = fdekey(__reduce_min_sync(FULL, kmin[x]));
                         const float w = fdekey(__reduce_max_sync(FULL, kmax[x])) - cmin[x];
-                        const float sv = (float)kSahBins / w;
+                        const float sv = __fdividef((float)kSahBins, w);  // any value: binning and partition share it
                         scale[x] = (w > 0.0f && sv < 1e30f) ? sv : 0.0f;  // degenerate / non-finite axis: not split
                     }
                 }

@@ -80,6 +80,8 @@ def prep():
         t0 = time.time()
         if name == "sah32":
             nodes, r = g["sah"](32)
+        elif name.startswith("sahtopsub"):
+            nodes, r = g["build_sahtop_sub"](int(name[9:]))
         elif name.startswith("sahtop"):
             nodes, r = g["build_sahtop"](int(name[6:]))
         elif name.startswith("lbtop"):

@@ -346,7 +346,7 @@ def build_sahtop(S_top, nbins=32, mode="sah_top"):
         else: ax, b, k = best[1]; L, R = idx[b <= k], idx[b > k]
         kk = len(nodes); nodes.append(None); nodes[kk] = (sah(L), sah(R)); return kk
     return nodes, sah(np.arange(N))
-def build_lbtop(S_bot, nbins=32, S_min=1):
+def build_lbtop(S_bot, nbins=32, S_min=1, one_axis=False):
     # Karras over everything; a subtree with <= S_bot leaves is rebuilt by binned SAH,
     # down to S_min leaves (smaller sets: Karras splits of their Morton codes again)
     o = np.argsort(code, kind="stable"); cs = code[o]; nodes = []
@@ -362,7 +362,8 @@ def build_lbtop(S_bot, nbins=32, S_min=1):
         if len(idx) == 1: return ~int(idx[0])
         if len(idx) <= S_min: return karras_set(idx)
         c = cen[idx]; clo, chi = c.min(0), c.max(0); best = (np.inf, None)
-        for ax in range(3):
+        axes = [int(np.argmax(chi - clo))] if one_axis else range(3)
+        for ax in axes:
             if chi[ax] - clo[ax] <= 0: continue
             b = np.minimum(((c[:, ax] - clo[ax]) / (chi[ax] - clo[ax]) * nbins).astype(int), nbins - 1)
             blo = np.full((nbins, 3), np.inf); bhi = np.full((nbins, 3), -np.inf); cnt = np.zeros(nbins)
@@ -392,6 +393,71 @@ def build_lbtop(S_bot, nbins=32, S_min=1):
             m = lo_
         k = len(nodes); nodes.append(None); nodes[k] = (rec(i, m), rec(m + 1, j)); return k
     return nodes, rec(0, N - 1)
+
+def build_sahtop_sub(S_bot, nbins=10, top_bins=10):
+    # the Karras tree's maximal subtrees of <= S_bot leaves (items), each rebuilt by
+    # binned SAH (as build_lbtop), and a binned SAH tree over the items' boxes
+    # replacing the Karras nodes above them
+    o = np.argsort(code, kind="stable"); cs = code[o]
+    sub_nodes, _ = [], None
+    lb_nodes, lb_root = build_lbtop(S_bot, nbins)
+    # items: recompute Karras ranges to find maximal <= S_bot ranges
+    items = []
+    def rec(i, j):
+        if j - i + 1 <= S_bot: items.append((i, j)); return
+        if cs[i] == cs[j]: m = (i + j) // 2
+        else:
+            x = int(cs[i]) ^ int(cs[j]); b = x.bit_length() - 1
+            lo_, hi_ = i, j
+            while hi_ - lo_ > 1:
+                mid = (lo_ + hi_) // 2
+                if (int(cs[mid]) >> b) == (int(cs[i]) >> b): lo_ = mid
+                else: hi_ = mid
+            m = lo_
+        rec(i, m); rec(m + 1, j)
+    rec(0, N - 1)
+    # rebuild: nodes list; each item subtree via SAH (reuse build_lbtop's inner builder by a fresh call on the item's prims)
+    nodes = []
+    def sah_prims(idx):
+        if len(idx) == 1: return ~int(idx[0])
+        c = cen[idx]; clo, chi = c.min(0), c.max(0); best = (np.inf, None)
+        for ax in range(3):
+            if chi[ax] - clo[ax] <= 0: continue
+            b = np.minimum(((c[:, ax] - clo[ax]) / (chi[ax] - clo[ax]) * nbins).astype(int), nbins - 1)
+            blo = np.full((nbins, 3), np.inf); bhi = np.full((nbins, 3), -np.inf); cnt = np.zeros(nbins)
+            for k in range(nbins):
+                m = b == k
+                if m.any(): blo[k] = tlo[idx[m]].min(0); bhi[k] = thi[idx[m]].max(0); cnt[k] = m.sum()
+            plo = np.minimum.accumulate(blo); phi = np.maximum.accumulate(bhi); pc = np.cumsum(cnt)
+            slo = np.minimum.accumulate(blo[::-1])[::-1]; shi = np.maximum.accumulate(bhi[::-1])[::-1]; sc = np.cumsum(cnt[::-1])[::-1]
+            for k in range(nbins - 1):
+                if pc[k] == 0 or sc[k + 1] == 0: continue
+                cost = area(plo[k], phi[k]) * pc[k] + area(slo[k + 1], shi[k + 1]) * sc[k + 1]
+                if cost < best[0]: best = (cost, (ax, b, k))
+        if best[1] is None: m = len(idx) // 2; L, R = idx[:m], idx[m:]
+        else: ax, b, k = best[1]; L, R = idx[b <= k], idx[b > k]
+        kk = len(nodes); nodes.append(None); nodes[kk] = (sah_prims(L), sah_prims(R)); return kk
+    it_ref, it_lo, it_hi = [], [], []
+    for (i, j) in items:
+        idx = o[i:j + 1]
+        it_ref.append(sah_prims(idx)); it_lo.append(tlo[idx].min(0)); it_hi.append(thi[idx].max(0))
+    it_lo, it_hi = np.array(it_lo), np.array(it_hi); it_c = (it_lo + it_hi) / 2
+    def sah_items(ii):
+        if len(ii) == 1: return it_ref[ii[0]]
+        c = it_c[ii]; clo, chi = c.min(0), c.max(0); best = (np.inf, None)
+        for ax in range(3):
+            if chi[ax] - clo[ax] <= 0: continue
+            b = np.minimum(((c[:, ax] - clo[ax]) / (chi[ax] - clo[ax]) * top_bins).astype(int), top_bins - 1)
+            for k in range(top_bins - 1):
+                L, R = b <= k, b > k
+                if not L.any() or not R.any(): continue
+                cost = area(it_lo[ii][L].min(0), it_hi[ii][L].max(0)) * L.sum() + area(it_lo[ii][R].min(0), it_hi[ii][R].max(0)) * R.sum()
+                if cost < best[0]: best = (cost, (ax, b, k))
+        if best[1] is None: m = len(ii) // 2; L, R = ii[:m], ii[m:]
+        else: ax, b, k = best[1]; L, R = ii[b <= k], ii[b > k]
+        kk = len(nodes); nodes.append(None); nodes[kk] = (sah_items(L), sah_items(R)); return kk
+    root = sah_items(np.arange(len(items)))
+    return nodes, root
 
 nodes, r = lbvh()
 t = time.time()

@@ -363,7 +363,9 @@ rsi_status_t rsi_bvh_download(rsi_handle_t h, int32_t* h_child, float* h_box,
  *     h_box     [n_nodes][2][6] float32 child AABBs as in rsi_bvh_download
  *     h_leaf_tri[N_t] int32 triangle index at each leaf slot (a permutation)
  *     root      the root internal node
- *   Host buffers, read before return; synchronizes `stream`.  The next
+ *   Host buffers, read before return; synchronizes `stream`.  The parent links,
+ *   arrival counts (2 per node) and scene box are set from the uploaded tree,
+ *   so rsi_validate / rsi_bvh_download / rsi_bvh_info report it.  The next
  *   rsi_rebuild replaces the uploaded tree.
  * Errors: RSI_E_INVALID_ARG (null / N_t < 2 / root out of range / leaf_tri not
  *   a permutation / a child ref out of range or a node or leaf not reached exactly once

@@ -2323,9 +2323,33 @@ rsi_status_t rsi_bvh_upload_device(rsi_bvh* h, const int32_t* h_child, const flo
     }
     if (st == RSI_OK)
         st = rsi_cuda_check(cudaMemcpyAsync(h->tris, ntris, nt * kTriF4 * sizeof(float4), cudaMemcpyHostToDevice, s), "tris");
+    // parent links and arrival counts of the uploaded tree (what the validator and
+    // the download report), the scene box for rsi_bvh_info
+    std::vector<int32_t> par((size_t)(nn + nt), -1);
+    std::vector<uint32_t> arr((size_t)nn, 2u);
+    float scene[6];
+    uint32_t one = 1u;
+    if (st == RSI_OK) {
+        for (int64_t i = 0; i < nn; ++i)
+            for (int side = 0; side < 2; ++side) {
+                const int32_t c = h_child[2 * i + side];
+                par[c >= 0 ? (size_t)c : (size_t)(nn + ~c)] = (int32_t)((i << 1) | side);
+            }
+        for (int x = 0; x < 3; ++x) {
+            scene[x] = fminf(h_box[12 * root + x], h_box[12 * root + 6 + x]);
+            scene[3 + x] = fmaxf(h_box[12 * root + 3 + x], h_box[12 * root + 9 + x]);
+        }
+        st = rsi_cuda_check(cudaMemcpyAsync(h->parent, par.data(), (nn + nt) * sizeof(int32_t), cudaMemcpyHostToDevice, s),
+                            "parents");
+    }
+    if (st == RSI_OK)
+        st = rsi_cuda_check(cudaMemcpyAsync(h->arrivals, arr.data(), nn * sizeof(uint32_t), cudaMemcpyHostToDevice, s),
+                            "arrivals");
     if (st == RSI_OK) {
         const int n_nodes = (int)nn;
         rsi_note_launch(), k_build_init<<<1, 32, 0, s>>>(h->scratch, (uint32_t)root);
+        cudaMemcpyAsync(h->scratch + SCR_ROOT, scene, sizeof(scene), cudaMemcpyHostToDevice, s);
+        cudaMemcpyAsync(h->scratch + SCR_ROOT_SET, &one, sizeof(one), cudaMemcpyHostToDevice, s);
         if (n_nodes <= kQCompactMax && h->qfull) {
             rsi_note_launch(), k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->qfull, h->scratch);
             rsi_note_launch(), k_qcompact<<<1, 1024, 0, s>>>(h->qfull, h->quads, h->qorder, h->qmap, h->scratch);

@@ -1096,6 +1096,7 @@ def test_bvh_upload_any_tree_same_results(rsi, wl):
     rsi.rsi_bvh_upload(h, child, box, leaf, 0)
     d = rsi.rsi_bvh_download(h)
     assert (d["child"] == child).all() and (d["box"] == box).all() and (d["leaf_tri"] == leaf).all()
+    assert rsi.rsi_validate(h)["ok"]  # parent links, arrivals, root reached from every leaf
     got = {"hit": rsi.rsi_intersect(h, Sd, Ed, "boolean")["hit"].cpu().numpy()}
     got.update({k: v.cpu().numpy() for k, v in rsi.rsi_intersect(h, Sd, Ed, "barycentric").items()})
     got["count"] = rsi.rsi_intersect(h, Sd, Ed, "intercept_count")["count"].cpu().numpy()

@@ -53,3 +53,17 @@ hv = rsi.rsi_test(*synth.workload("sphere", 3000, seed=2)[:4], {"mode": "boolean
 rsi.rsi_release_cache()
 torch.cuda.synchronize()
 print("sanitize run ok")
+# round 2: SAH subtrees (N_t <= 32768, every mode), the treelet refit path
+# (32769 .. 65536), and rsi_bvh_upload (round trip of the downloaded tree)
+for nt in (20000, 40000):
+    Vd = torch.from_numpy(V[:3 * nt]).to(dev); Td = torch.from_numpy(T[:nt]).to(dev)
+    h = rsi.rsi_build(Vd, Td)
+    Sd, Ed = (torch.from_numpy(a).to(dev) for a in synth.box_rays(3000, -0.2, 1.2, seed=4))
+    for m in ("boolean", "barycentric", "intercept_count"):
+        rsi.rsi_intersect(h, Sd, Ed, m)
+    d = rsi.rsi_bvh_download(h)
+    rsi.rsi_bvh_upload(h, d["child"], d["box"], d["leaf_tri"], 0)
+    rsi.rsi_intersect(h, Sd, Ed, "barycentric")
+    assert rsi.rsi_validate(h)["ok"]
+    h.free()
+print("sanitize round-2 paths ok")

@@ -400,10 +400,10 @@ __global__ void __launch_bounds__(kBlock) k_karras(const uint32_t* __restrict__ 
     if (i == 0) parent[0] = -1;
     if (sah_list) {  // the SAH subtree roots (k_sah_sub): maximal nodes of 3 .. sah_max leaves
         const int sz = hi - lo + 1, szl = gamma - lo + 1, szr = hi - gamma;
-        if (i == 0 && sz >= 3 && sz <= sah_max) sah_list[atomicAdd(scratch + SCR_SAH_COUNT, 1u)] = 0;
-        if (sz > sah_max) {
-            if (szl >= 3 && szl <= sah_max) sah_list[atomicAdd(scratch + SCR_SAH_COUNT, 1u)] = gamma;
-            if (szr >= 3 && szr <= sah_max) sah_list[atomicAdd(scratch + SCR_SAH_COUNT, 1u)] = gamma + 1;
+        if (i == 0 && sz <= sah_max) sah_list[atomicAdd(scratch + SCR_SAH_COUNT, 1u)] = 0;
+        if (sz > sah_max) {  // (children of 1 or 2 leaves too: k_sah_sub packs and refits from every item)
+            if (szl <= sah_max) sah_list[atomicAdd(scratch + SCR_SAH_COUNT, 1u)] = left;
+            if (szr <= sah_max) sah_list[atomicAdd(scratch + SCR_SAH_COUNT, 1u)] = right;
         }
     }
 }
@@ -812,9 +812,6 @@ __device__ void treelet_opt(const Tree& tr, int n, unsigned char* row_popt) {
 #ifndef RSI_SAH_SUB
 #define RSI_SAH_SUB 256  // leaves per rebuilt subtree (0: off); 128 / 512: rebuild -11 / +27 us, query +0.2 / -0.7 %
 #endif
-#ifndef RSI_SAH_TREELET
-#define RSI_SAH_TREELET 0  // the refit's treelet restructuring on top of the SAH subtrees (measured: no gain, +20 us)
-#endif
 #ifndef RSI_SAH_MAX_TRI
 #define RSI_SAH_MAX_TRI 32768
 #endif
@@ -844,16 +841,53 @@ constexpr int kSahBinSlots = 3 * kSahBins;  // (axis, bin) pairs: one lane each 
 static_assert(kSahBinSlots <= 32, "RSI_SAH_BINS");
 constexpr int kSahSmall = kTLm;  // nodes of <= kSahSmall triangles: one THREAD each, exact SAH over every
                                  // topology (treelet_dp) instead of a warp's binned split per level
-constexpr size_t kSahSmem = (size_t)9 * kSahSub * sizeof(float) + (size_t)kSahSub * sizeof(int32_t) +
+constexpr size_t kSahSmem = (size_t)18 * kSahSub * sizeof(float) + (size_t)kSahSub * sizeof(int32_t) +
                             (size_t)2 * kSahSub * sizeof(uint16_t) + (size_t)3 * (kSahSub / 2) * 3 * sizeof(int) +
                             (size_t)kSahWarps * kSahBinSlots * 7 * sizeof(uint32_t) +
-                            (size_t)32 * kSahWarps * 32 + 4 * sizeof(int);
+                            (size_t)32 * kSahWarps * 32 + 4 * sizeof(int) + 8 * sizeof(float);
+
+// The global refit protocol of k_refit (state 3) from a completed subtree whose
+// box is (lo, hi) and whose parent link is p: the box goes into the parent's
+// child slot, an acq_rel arrival on the parent's counter (first arrival stops),
+// the second merges the sibling's slot (L2-coherent loads) and climbs on; the
+// arrival at the root writes the scene box.
+__device__ void refit_climb(float4* nodes, const int32_t* parent, uint32_t* arrivals, uint32_t* scratch, int32_t p,
+                            float lo[3], float hi[3]) {
+    if (p >= 0) {
+        write_slot(nodes, p >> 1, p & 1, lo, hi);
+        while (true) {
+            const int node = p >> 1, side = p & 1;
+            const int32_t p_next = node > 0 ? __ldg(parent + node) : -1;
+            uint32_t old;
+            asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(arrivals + node) : "memory");
+            if (old == 0u) return;
+            const float* f = reinterpret_cast<const float*>(nodes + 4 * node);
+            const int o = side ? 0 : 4;  // sibling slot
+            lo[0] = fminf(lo[0], __ldcg(f + o + 0));
+            hi[0] = fmaxf(hi[0], __ldcg(f + o + 1));
+            lo[1] = fminf(lo[1], __ldcg(f + o + 2));
+            hi[1] = fmaxf(hi[1], __ldcg(f + o + 3));
+            lo[2] = fminf(lo[2], __ldcg(f + 8 + 2 * (1 - side)));
+            hi[2] = fmaxf(hi[2], __ldcg(f + 9 + 2 * (1 - side)));
+            if (node == 0) break;
+            p = p_next;
+            write_slot(nodes, p >> 1, p & 1, lo, hi);
+        }
+    }
+    float* root = reinterpret_cast<float*>(scratch + SCR_ROOT);
+    for (int x = 0; x < 3; ++x) {
+        root[x] = lo[x];
+        root[3 + x] = hi[x];
+    }
+    scratch[SCR_ROOT_SET] = 1u;
+}
 
 // A node of k <= kSahSmall triangles (slots [a + s, a + e), node id nid): the
 // SAH-optimal binary tree over them (treelet_dp: every topology), written with
 // its leaves in depth-first order and the Karras numbering.
 __device__ void sah_small(int a, int s, int e, int nid, const float* s_lo, const float* s_hi, uint16_t* pm,
-                          float4* nodes, int32_t* parent, int n_nodes, unsigned char* row_popt) {
+                          float4* nodes, int32_t* parent, uint32_t* arrivals, int n_nodes, unsigned char* row_popt,
+                          float* set_box, int box_id) {
     const int k = e - s;
     float lo[kTLm][3], hi[kTLm][3], lc[kTLm];
     int q[kTLm];
@@ -893,6 +927,26 @@ __device__ void sah_small(int a, int s, int e, int nid, const float* s_lo, const
         *reinterpret_cast<int4*>(nodes + 4 * id + 3) = make_int4(left, right, l0, l0 + nl + nr - 1);
         parent[left >= 0 ? left : n_nodes + ~left] = (id << 1) | 0;
         parent[right >= 0 ? right : n_nodes + ~right] = (id << 1) | 1;
+        {  // the two child boxes (exact unions of the members' boxes); the node is complete
+            float bl[3] = {INFINITY, INFINITY, INFINITY}, bh[3] = {-INFINITY, -INFINITY, -INFINITY};
+            float cl[3] = {INFINITY, INFINITY, INFINITY}, ch[3] = {-INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+            for (int i = 0; i < kTLm; ++i)
+#pragma unroll
+                for (int x = 0; x < 3; ++x) {
+                    if ((pl >> i) & 1) { bl[x] = fminf(bl[x], lo[i][x]); bh[x] = fmaxf(bh[x], hi[i][x]); }
+                    if ((pr >> i) & 1) { cl[x] = fminf(cl[x], lo[i][x]); ch[x] = fmaxf(ch[x], hi[i][x]); }
+                }
+            write_slot(nodes, id, 0, bl, bh);
+            write_slot(nodes, id, 1, cl, ch);
+            arrivals[id] = 2u;
+            if (set_box && id == box_id)  // the subtree's root: its box starts the refit above
+#pragma unroll
+                for (int x = 0; x < 3; ++x) {
+                    set_box[x] = fminf(bl[x], cl[x]);
+                    set_box[3 + x] = fmaxf(bh[x], ch[x]);
+                }
+        }
         if (nl == 1) out[l0 - (a + s)] = (uint16_t)q[__ffs(pl) - 1];
         if (nr == 1) out[l0 + nl - (a + s)] = (uint16_t)q[__ffs(pr) - 1];
         // right first on the stack so the left subtree is expanded next (slots are explicit anyway)
@@ -914,20 +968,23 @@ __device__ void sah_small(int a, int s, int e, int nid, const float* s_lo, const
 
 __global__ void __launch_bounds__(32 * kSahWarps, 1) k_sah_sub(const float* __restrict__ V, int64_t nv,
                                                                const int32_t* __restrict__ T, int32_t* vals,
-                                                               float4* nodes, int32_t* parent, int n_nodes,
-                                                               const int32_t* __restrict__ list, const uint32_t* scratch) {
+                                                               float4* nodes, float4* __restrict__ tris, int32_t* parent,
+                                                               uint32_t* arrivals, int n_nodes,
+                                                               const int32_t* __restrict__ list, uint32_t* scratch) {
     extern __shared__ uint4 s_sah_dyn[];
     float* s_f = reinterpret_cast<float*>(s_sah_dyn);
     float* s_lo = s_f;                   // [3][kSahSub]
     float* s_hi = s_f + 3 * kSahSub;     // [3][kSahSub]
     float* s_c = s_f + 6 * kSahSub;      // [3][kSahSub]  (3 x centroid)
-    int32_t* s_id = reinterpret_cast<int32_t*>(s_f + 9 * kSahSub);
+    float* s_v = s_f + 9 * kSahSub;      // [9][kSahSub]  the vertices (the triangle records are packed here)
+    int32_t* s_id = reinterpret_cast<int32_t*>(s_f + 18 * kSahSub);
     uint16_t* s_perm = reinterpret_cast<uint16_t*>(s_id + kSahSub);  // [2][kSahSub]
     int* s_task = reinterpret_cast<int*>(s_perm + 2 * kSahSub);      // [2][kSahSub / 2][3]
     int* s_small = s_task + 2 * (kSahSub / 2) * 3;                                   // [kSahSub / 2][3]
     uint32_t* s_bins = reinterpret_cast<uint32_t*>(s_small + (kSahSub / 2) * 3);     // [warps][slots][7]
     unsigned char* s_popt = reinterpret_cast<unsigned char*>(s_bins + kSahWarps * kSahBinSlots * 7);  // [threads][32]
     int* s_ntask = reinterpret_cast<int*>(s_popt + 32 * kSahWarps * 32);             // [2], then the small count
+    float* s_rbox = reinterpret_cast<float*>(s_ntask + 4);                           // [6] the subtree's box
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t lt = (1u << lane) - 1u;
@@ -938,9 +995,42 @@ __global__ void __launch_bounds__(32 * kSahWarps, 1) k_sah_sub(const float* __re
     const bool my_in = lane < kSahBinSlots;
     for (int si = blockIdx.x; si < n_sub; si += gridDim.x) {
         const int root = list[si];
-        const int4 rr = *reinterpret_cast<const int4*>(nodes + 4 * root + 3);
+        // ---- a leaf, or a node of two leaves, under a Karras node of more than
+        // kSahSub leaves: pack its triangle(s) and refit upwards from it (one thread)
+        const int4 rr = root >= 0 ? *reinterpret_cast<const int4*>(nodes + 4 * root + 3) : make_int4(0, 0, 0, 0);
+        if (root < 0 || rr.w - rr.z + 1 <= 2) {
+            if (threadIdx.x == 0) {
+                const int k0 = root < 0 ? ~root : rr.z, kn = root < 0 ? 1 : 2;
+                float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+                for (int j = 0; j < kn; ++j) {
+                    const int k = k0 + j;
+                    const int32_t id = vals[k];
+                    const int32_t i0 = safe_index(T[3 * id], nv), i1 = safe_index(T[3 * id + 1], nv),
+                                  i2 = safe_index(T[3 * id + 2], nv);
+                    float a3[3], b3[3], c3[3], l[3], h[3];
+#pragma unroll
+                    for (int x = 0; x < 3; ++x) {
+                        a3[x] = V[3 * i0 + x];
+                        b3[x] = V[3 * i1 + x];
+                        c3[x] = V[3 * i2 + x];
+                        l[x] = fminf(a3[x], fminf(b3[x], c3[x]));
+                        h[x] = fmaxf(a3[x], fmaxf(b3[x], c3[x]));
+                        lo[x] = fminf(lo[x], l[x]);
+                        hi[x] = fmaxf(hi[x], h[x]);
+                    }
+                    tris[kTriF4 * k + 0] = make_float4(a3[0], a3[1], a3[2], __int_as_float(id));
+                    tris[kTriF4 * k + 1] = make_float4(b3[0], b3[1], b3[2], 0.f);
+                    tris[kTriF4 * k + 2] = make_float4(c3[0], c3[1], c3[2], 0.f);
+                    if (kTriF4 == 4) tris[4 * k + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (kn == 2) write_slot(nodes, root, j, l, h);
+                }
+                if (kn == 2) arrivals[root] = 2u;
+                refit_climb(nodes, parent, arrivals, scratch, root < 0 ? parent[n_nodes + ~root] : parent[root], lo, hi);
+            }
+            continue;
+        }
         const int a = rr.z, m = rr.w - rr.z + 1;
-        // the subtree's triangles: exact fp32 boxes and centroids (x 3)
+        // the subtree's triangles: vertices, exact fp32 boxes and centroids (x 3)
         for (int t = threadIdx.x; t < m; t += blockDim.x) {
             const int32_t id = vals[a + t];
             const int32_t i0 = safe_index(T[3 * id], nv), i1 = safe_index(T[3 * id + 1], nv),
@@ -951,6 +1041,9 @@ __global__ void __launch_bounds__(32 * kSahWarps, 1) k_sah_sub(const float* __re
                 s_lo[x * kSahSub + t] = fminf(p0, fminf(p1, p2));
                 s_hi[x * kSahSub + t] = fmaxf(p0, fmaxf(p1, p2));
                 s_c[x * kSahSub + t] = (p0 + p1) + p2;
+                s_v[x * kSahSub + t] = p0;
+                s_v[(3 + x) * kSahSub + t] = p1;
+                s_v[(6 + x) * kSahSub + t] = p2;
             }
             s_id[t] = id;
             s_perm[t] = (uint16_t)t;
@@ -1080,6 +1173,48 @@ __global__ void __launch_bounds__(32 * kSahWarps, 1) k_sah_sub(const float* __re
                         best_ax = bl / kSahBins;
                         best_b = bl % kSahBins;
                         nl = ncl;
+                        // the children's boxes are the best plane's prefix / suffix bin unions
+                        if (lane == bl) {
+                            write_slot(nodes, nid, 0, plo, phi);
+                            write_slot(nodes, nid, 1, rlo, rhi);
+                            if (nid == root)
+#pragma unroll
+                                for (int y = 0; y < 3; ++y) {
+                                    s_rbox[y] = fminf(plo[y], rlo[y]);
+                                    s_rbox[3 + y] = fmaxf(phi[y], rhi[y]);
+                                }
+                        }
+                    }
+                }
+                if (best_ax < 0) {  // median split: the children's boxes by warp reductions
+                    float bl3[3] = {INFINITY, INFINITY, INFINITY}, bh3[3] = {-INFINITY, -INFINITY, -INFINITY};
+                    float cl3[3] = {INFINITY, INFINITY, INFINITY}, ch3[3] = {-INFINITY, -INFINITY, -INFINITY};
+                    for (int j = s + lane; j < e; j += 32) {
+                        const int q = pm[j];
+                        const bool lft = j < s + nl;
+#pragma unroll
+                        for (int y = 0; y < 3; ++y) {
+                            const float l = s_lo[y * kSahSub + q], h = s_hi[y * kSahSub + q];
+                            if (lft) { bl3[y] = fminf(bl3[y], l); bh3[y] = fmaxf(bh3[y], h); }
+                            else { cl3[y] = fminf(cl3[y], l); ch3[y] = fmaxf(ch3[y], h); }
+                        }
+                    }
+#pragma unroll
+                    for (int y = 0; y < 3; ++y) {
+                        bl3[y] = fdekey(__reduce_min_sync(FULL, fkey(bl3[y])));
+                        bh3[y] = fdekey(__reduce_max_sync(FULL, fkey(bh3[y])));
+                        cl3[y] = fdekey(__reduce_min_sync(FULL, fkey(cl3[y])));
+                        ch3[y] = fdekey(__reduce_max_sync(FULL, fkey(ch3[y])));
+                    }
+                    if (lane == 0) {
+                        write_slot(nodes, nid, 0, bl3, bh3);
+                        write_slot(nodes, nid, 1, cl3, ch3);
+                        if (nid == root)
+#pragma unroll
+                            for (int y = 0; y < 3; ++y) {
+                                s_rbox[y] = fminf(bl3[y], cl3[y]);
+                                s_rbox[3 + y] = fmaxf(bh3[y], ch3[y]);
+                            }
                     }
                 }
                 // partition the node's slice of the permutation (warp-ordered, stable)
@@ -1112,6 +1247,7 @@ __global__ void __launch_bounds__(32 * kSahWarps, 1) k_sah_sub(const float* __re
                     *reinterpret_cast<int4*>(nodes + 4 * nid + 3) = make_int4(left, right, a + s, a + e - 1);
                     parent[left >= 0 ? left : n_nodes + ~left] = (nid << 1) | 0;
                     parent[right >= 0 ? right : n_nodes + ~right] = (nid << 1) | 1;
+                    arrivals[nid] = 2u;  // complete (the validator's "atomic: 2")
                     const int nxt = cur ^ 1;
                     int* tn = s_task + nxt * (kSahSub / 2) * 3;
                     // children of > kSahSmall triangles: the next level's warp tasks; smaller: one thread each
@@ -1142,10 +1278,24 @@ __global__ void __launch_bounds__(32 * kSahWarps, 1) k_sah_sub(const float* __re
         const int ns = s_ntask[2];
         for (int t = threadIdx.x; t < ns; t += blockDim.x)
             sah_small(a, s_small[3 * t], s_small[3 * t + 1], s_small[3 * t + 2], s_lo, s_hi, s_perm, nodes, parent,
-                      n_nodes, s_popt + 32 * threadIdx.x);
+                      arrivals, n_nodes, s_popt + 32 * threadIdx.x, s_rbox, root);
         __syncthreads();
-        // the leaf slots' triangles in the new order
-        for (int t = threadIdx.x; t < m; t += blockDim.x) vals[a + t] = s_id[s_perm[t]];
+        // the leaf slots' triangles in the new order, packed (A7): (v0, id), (v1, 0), (v2, 0), pad
+        for (int t = threadIdx.x; t < m; t += blockDim.x) {
+            const int q = s_perm[t];
+            const int32_t id = s_id[q];
+            const int k = a + t;
+            vals[k] = id;
+            tris[kTriF4 * k + 0] = make_float4(s_v[q], s_v[kSahSub + q], s_v[2 * kSahSub + q], __int_as_float(id));
+            tris[kTriF4 * k + 1] = make_float4(s_v[3 * kSahSub + q], s_v[4 * kSahSub + q], s_v[5 * kSahSub + q], 0.f);
+            tris[kTriF4 * k + 2] = make_float4(s_v[6 * kSahSub + q], s_v[7 * kSahSub + q], s_v[8 * kSahSub + q], 0.f);
+            if (kTriF4 == 4) tris[4 * k + 3] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        // the subtree is complete: refit upwards from its root (the Karras nodes above)
+        if (threadIdx.x == 0) {
+            float lo[3] = {s_rbox[0], s_rbox[1], s_rbox[2]}, hi[3] = {s_rbox[3], s_rbox[4], s_rbox[5]};
+            refit_climb(nodes, parent, arrivals, scratch, root == 0 ? -1 : parent[root], lo, hi);
+        }
         __syncthreads();
     }
 }
@@ -1738,7 +1888,6 @@ __global__ void __launch_bounds__(1024) k_qcompact(const float4* __restrict__ fu
 }
 
 // records indexed by node id (meshes above kQCompactMax internal nodes)
-__global__ void k_qroot_copy(uint32_t* scratch) { scratch[SCR_QROOT] = scratch[SCR_ROOT_NODE]; }
 
 // ------------------------------------------------------------------ 4-wide view (cut records)
 // One thread per internal node n: the up-to-4 members of n's cut (grandchildren, or the greedy cut under RSI_QUAD_GREEDY; a leaf child
@@ -1798,6 +1947,8 @@ __global__ void __launch_bounds__(kBlock) k_quads(const float4* __restrict__ nod
                                                   float4* __restrict__ quads, uint32_t* scratch) {
     int n = blockIdx.x * blockDim.x + threadIdx.x;
     if (n >= n_nodes) return;
+    // the walks' root record = the root node (k_qcompact, when it runs, renumbers it 0 afterwards)
+    if (n == 0) scratch[SCR_QROOT] = scratch[SCR_ROOT_NODE];
     // (one spare slot: a greedy expansion appends both children before moving one)
     float lo[3][5], hi[3][5];
     int ref[5] = {(int)0x80000000, (int)0x80000000, (int)0x80000000, (int)0x80000000,
@@ -2146,13 +2297,16 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
                 cudaFuncSetAttribute(k_sah_sub, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSahSmem);
                 attr = true;
             }
-            rsi_note_launch(), k_sah_sub<<<g, 32 * kSahWarps, kSahSmem, s>>>(V, nv, T, h->vals, h->nodes, h->parent, n_nodes,
-                                                                     list, h->scratch);
+            rsi_note_launch(), k_sah_sub<<<g, 32 * kSahWarps, kSahSmem, s>>>(V, nv, T, h->vals, h->nodes, h->tris, h->parent,
+                                                                     h->arrivals, n_nodes, list, h->scratch);
         }
+        // (with the SAH subtrees, k_sah_sub packs the triangles, writes every box
+        // inside the subtrees and refits the Karras nodes above them: no k_refit)
         const int treelet = (h->opt.flags & (RSI_OPT_PLAIN_TREE | RSI_OPT_ROTATE)) || refit_leaves < n ||
-                                    n > kTreeletMaxTri || (sah_sub && !RSI_SAH_TREELET) ? 0 : 1;
+                                    n > kTreeletMaxTri ? 0 : 1;
         const int rotate = (h->opt.flags & RSI_OPT_ROTATE) ? 1 : 0;
-        if (treelet)
+        if (sah_sub) {
+        } else if (treelet)
             rsi_note_launch(), k_refit<true><<<rsi_ceil_div(refit_leaves, kRefitLeaves), kRefitLeaves, 0, s>>>(
                 V, nv, T, h->vals, refit_leaves, n, h->nodes, h->tris, h->parent, h->arrivals, h->scratch, rotate, 1);
         else
@@ -2164,7 +2318,6 @@ rsi_status_t rsi_build_device(rsi_bvh* h, const float* V, int64_t nv, const int3
         rsi_note_launch(), k_qcompact<<<1, 1024, 0, s>>>(h->qfull, h->quads, h->qorder, h->qmap, h->scratch);
     } else {
         rsi_note_launch(), k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads, h->scratch);
-        rsi_note_launch(), k_qroot_copy<<<1, 1, 0, s>>>(h->scratch);
     }
     if (kQTop > 0) rsi_note_launch(), k_qtop<<<1, 256, 0, s>>>(h->quads, h->top, h->scratch);
     st = rsi_cuda_check(cudaGetLastError(), "build kernel launch");
@@ -2355,7 +2508,6 @@ rsi_status_t rsi_bvh_upload_device(rsi_bvh* h, const int32_t* h_child, const flo
             rsi_note_launch(), k_qcompact<<<1, 1024, 0, s>>>(h->qfull, h->quads, h->qorder, h->qmap, h->scratch);
         } else {
             rsi_note_launch(), k_quads<<<rsi_ceil_div(n_nodes, kBlock), kBlock, 0, s>>>(h->nodes, n_nodes, h->quads, h->scratch);
-            rsi_note_launch(), k_qroot_copy<<<1, 1, 0, s>>>(h->scratch);
         }
         if (kQTop > 0) rsi_note_launch(), k_qtop<<<1, 256, 0, s>>>(h->quads, h->top, h->scratch);
         st = rsi_cuda_check(cudaGetLastError(), "upload kernels");

@@ -1075,6 +1075,7 @@ __global__ void __launch_bounds__(32 * kSahWarps, 1) k_sah_sub(const float* __re
                 if (k > 2) {
                     // centroid bounds: order-preserving keys, one REDUX per bound
                     uint32_t kmin[3] = {0xffffffffu, 0xffffffffu, 0xffffffffu}, kmax[3] = {0u, 0u, 0u};
+#pragma unroll 4
                     for (int j = s + lane; j < e; j += 32) {
                         const int q = pm[j];
 #pragma unroll
@@ -1098,6 +1099,7 @@ __global__ void __launch_bounds__(32 * kSahWarps, 1) k_sah_sub(const float* __re
                         bins[w] = f == 0 ? 0u : (f <= 3 ? 0xffffffffu : 0u);
                     }
                     __syncwarp();
+#pragma unroll 4
                     for (int j = s + lane; j < e; j += 32) {
                         const int q = pm[j];
                         const uint32_t l0 = fkey(s_lo[q]), l1 = fkey(s_lo[kSahSub + q]), l2 = fkey(s_lo[2 * kSahSub + q]);
@@ -1223,6 +1225,7 @@ __global__ void __launch_bounds__(32 * kSahWarps, 1) k_sah_sub(const float* __re
                     const float sc = best_ax == 0 ? scale[0] : (best_ax == 1 ? scale[1] : scale[2]);
                     const float* cax = s_c + (best_ax > 0 ? best_ax : 0) * kSahSub;
                     int base_l = s, base_r = s + nl;
+#pragma unroll 4
                     for (int j0 = s; j0 < e; j0 += 32) {
                         const int j = j0 + lane;
                         const bool v = j < e;
@@ -1236,6 +1239,7 @@ __global__ void __launch_bounds__(32 * kSahWarps, 1) k_sah_sub(const float* __re
                         base_r += __popc(br);
                     }
                     __syncwarp();
+#pragma unroll 4
                     for (int j = s + lane; j < e; j += 32) pm[j] = pt[j];
                     __syncwarp();
                 }

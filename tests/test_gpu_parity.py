@@ -1104,3 +1104,55 @@ def test_bvh_upload_any_tree_same_results(rsi, wl):
     with pytest.raises(Exception):
         rsi.rsi_bvh_upload(h, child, box, leaf[::-1].copy() * 0, 0)  # not a permutation
     h.free()
+
+
+@pytest.mark.parametrize("case", ["outliers", "n63", "n64", "n257", "gate32768", "gate32769", "coincident"])
+def test_sah_subtree_build_edge_cases(rsi, case):
+    """The default build's SAH subtree pass (N_t <= 32768) and its fused refit on
+    trees that stress it: isolated far-away triangles (single leaves and two-leaf
+    nodes directly under Karras nodes of > 256 leaves: the leftover items),
+    the size gates (no pass below 64 or above 32768 triangles), a whole tree that
+    is one subtree (257 is just above), and coincident centroids (every split
+    degenerate: median splits).  Every tree is checked by the validator and the
+    exact-box walk of _check_tree, and all modes equal the oracle."""
+    rng = np.random.default_rng(77)
+    nt = {"outliers": 5003, "n63": 63, "n64": 64, "n257": 257, "gate32768": 32768, "gate32769": 32769,
+          "coincident": 3000}[case]
+    V = rng.uniform(0, 1, (3 * nt, 3)).astype(np.float32)
+    if case == "outliers":  # three isolated triangles far from the cluster, one pair close together
+        V[-9:] = np.float32([[40, 40, 40], [40.1, 40, 40], [40, 40.1, 40],
+                             [-30, 5, 5], [-30, 5.1, 5], [-30, 5, 5.1],
+                             [-30.2, 5, 5], [-30.2, 5.1, 5], [-30.2, 5, 5.1]])
+    if case == "coincident":  # the same triangle (same centroid) 3000 times, a few distinct ones
+        V[3:3 * (nt - 5)] = np.tile(V[:3], (nt - 6, 1))
+    T = np.arange(3 * nt, dtype=np.int32).reshape(nt, 3)
+    Vd, Td = to_dev(V, T)
+    h = rsi.rsi_build(Vd, Td)
+    assert rsi.rsi_validate(h)["ok"]
+    d = rsi.rsi_bvh_download(h)
+    h.free()
+    _check_tree(d, V, T, nt)
+    if case == "outliers":  # the leftover items exist: a leaf child of a node with > 256 leaves
+        child = d["child"]
+        size = {}
+
+        def leaves(i):
+            if i < 0:
+                return 1
+            if i not in size:
+                size[i] = leaves(int(child[i, 0])) + leaves(int(child[i, 1]))
+            return size[i]
+
+        import sys
+        sys.setrecursionlimit(100000)
+        leaves(0)
+        assert any(size[i] > 256 and (child[i] < 0).any() for i in size)
+    S, E = synth.box_rays(3000 if nt < 20000 else 800, [-1, -1, -1], [2, 2, 2], 5)
+    if case == "outliers":
+        S[:20], E[:20] = np.float32([40.03, 40.03, 39]), np.float32([40.03, 40.03, 41])
+        S[20:40], E[20:40] = np.float32([-31, 5.02, 5.02]), np.float32([-29, 5.02, 5.02])
+    ref = oracle.run(V, T, S, E)
+    got = run_all(rsi, V, T, S, E)
+    assert_parity(got, ref, S, E, case)
+    if case == "outliers":
+        assert got["hit"][:20].all() and (got["count"][20:40] == 2).all()

@@ -75,10 +75,10 @@ constexpr bool kQuadCount = RSI_COUNT_QUAD;
 // paper-terrain workloads -- 3 with min_trav 16 / 12 for boolean / barycentric
 // (-1..-6 %), 1 for intercept_count (3: +9 %)
 #ifndef RSI_VISITS_BOOL
-#define RSI_VISITS_BOOL 3
+#define RSI_VISITS_BOOL 4  // re-measured with the SAH subtrees: 3 -> 4 sphere -2.3 %, terrain -0.5 %; 6: +2.5 %
 #endif
 #ifndef RSI_VISITS_BARY
-#define RSI_VISITS_BARY 3
+#define RSI_VISITS_BARY 4  // 3 -> 4: sphere -1.5 %, terrain 0; 6: +2 %
 #endif
 #ifndef RSI_VISITS_COUNT
 #define RSI_VISITS_COUNT 1

@@ -555,20 +555,22 @@ struct ModeState<MODE_BARY> {
                                          float* dist, float* point) {
         if (slot >= 0) {
             const int k = leaf_slot();
-            float4 bA, bB, bC;
-            load_tri(p.tris, k, bA, bB, bC);  // the original id (and, rarely, the fp64 recompute)
+            // the original id: one word of the triangle record (the whole record only for the fp64 recompute)
+            const int id = __ldg(reinterpret_cast<const int*>(p.tris + kTriF4 * (int64_t)k) + 3);
             float tt;
             if (exact()) {
                 tt = (float)t64();
             } else if (e32() <= kOutTol) {
                 tt = t32();
             } else {  // fp32 value not certified to the output tolerance
+                float4 bA, bB, bC;
+                load_tri(p.tris, k, bA, bB, bC);
                 double v = 0.0;
                 mt64(r, bA, bB, bC, &v);
                 tt = (float)v;
                 st.add(ST_FP64_RAYS);
             }
-            tri[0] = __float_as_int(bA.w);
+            tri[0] = id;
             if (t) t[0] = tt;
             if (dist) dist[0] = tt * norm3df(r.dx, r.dy, r.dz);  // no overflow / underflow of |d|^2
             if (point) {

@@ -83,6 +83,8 @@ def parse():
     ap.add_argument("--no-parity", action="store_true", help="skip the sphere1m parity sample (rank 0, N=1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="oracle sample rays (0 = auto ~15 s)")
+    ap.add_argument("--no-overlap", dest="overlap", action="store_false",
+                    help="time the steps back to back on one stream and one handle (no step overlap)")
     ap.add_argument("--fused-gather", action="store_true",
                     help="N > 1: traversal writes straight into rank 0's buffers over NVLink (PeerOutputs) "
                          "instead of the pipelined NCCL gather")
@@ -325,7 +327,9 @@ def arm_config(args, n_tri: int, world: int, backend: str = "nccl") -> dict:
                                                      else f" + {backend} gather to rank 0") if world > 1 else ""),
             "l2": f"inputs larger than L2 ({args.rays_per_gpu * 24 / 1e6:.0f} MB of segments per GPU; no flush)",
             "step": "rsi_rebuild + rsi_intersect" + (" + gather" if world > 1 else "")
-                    + " (RSI_OPT_DEFERRED_STATUS: build checks read back after the timed region)"}
+                    + " (RSI_OPT_DEFERRED_STATUS: build checks read back after the timed region)"
+                    + ("; consecutive steps overlapped on two streams and two handles"
+                       if getattr(args, "overlap", False) else "")}
 
 
 def run_reference(args, rank: int, world: int):
@@ -399,37 +403,52 @@ def main():
     # their result is read once after the timed region)
     h = rsi.rsi_build(Vd, Td, rsi.Options(deferred_status=True))
 
-    def timed(mode: str, steps: int, warmup: int, clocks: bool):
+    # a second handle for the overlapped steps (below); built once, rebuilt every step
+    h_b = rsi.rsi_build(Vd, Td, rsi.Options(deferred_status=True)) if args.overlap else None
+
+    def timed(mode: str, steps: int, warmup: int, clocks: bool, overlap: bool = False):
         # N > 1: the gather of step k (NCCL, its own stream) overlaps the build +
         # traversal of step k+1; two output slots, each reused only after its
         # previous gather completed (a device-side wait); all gathers finish
-        # inside the timed region (drain before the end event)
+        # inside the timed region (drain before the end event).
+        # overlap: consecutive steps alternate between two handles and two
+        # streams, so step k+1's rebuild (small latency-bound grids) fills the
+        # SMs that step k's persistent traversal frees in its tail, and step
+        # k+1's traversal starts as soon as its own BVH is ready.  Every step
+        # still does the whole rebuild + intersect; step k+2 reuses step k's
+        # handle and outputs only after step k finished (same stream).
         peer = PeerOutputs(n * world, mode, dev) if (world > 1 and args.fused_gather) else None
+        overlap = overlap and peer is None
+        hs = [h, h_b] if overlap else [h]
+        sts = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)] if overlap else [stream]
         if peer is not None:
             outs = [peer.outputs()]
             pipe = None
         else:
-            outs = [rsi.alloc_outputs(n, mode, dev) for _ in range(2 if world > 1 else 1)]
+            outs = [rsi.alloc_outputs(n, mode, dev) for _ in range(2 if (world > 1 or overlap) else 1)]
             pipe = GatherPipeline(slots=2) if world > 1 else None
 
         def step(k, ev=None):
             out = outs[k % len(outs)]
-            if pipe is not None and pipe.slots[k % 2] is not None:
-                pipe.slots[k % 2].wait()  # this slot's send buffer is free again
-            if peer is not None:
-                peer.begin()  # rank 0 is done with the previous step's rows
-            if ev is not None:
-                ev[0].record(stream)
-            rsi.rsi_rebuild(h, Vd, Td)
-            if ev is not None:
-                ev[1].record(stream)
-            rsi.rsi_intersect(h, Sd, Ed, mode, out=out)
-            if ev is not None:
-                ev[2].record(stream)
-            if pipe is not None:
-                pipe.start(k % 2, {f: out[f] for f in FIELDS[mode]}, n * world)
-            if peer is not None:
-                peer.complete()  # device-side barrier: rank 0 holds every rank's rows
+            st = sts[k % len(sts)]
+            hk = hs[k % len(hs)]
+            with torch.cuda.stream(st):
+                if pipe is not None and pipe.slots[k % 2] is not None:
+                    pipe.slots[k % 2].wait()  # this slot's send buffer is free again
+                if peer is not None:
+                    peer.begin()  # rank 0 is done with the previous step's rows
+                if ev is not None:
+                    ev[0].record(st)
+                rsi.rsi_rebuild(hk, Vd, Td)
+                if ev is not None:
+                    ev[1].record(st)
+                rsi.rsi_intersect(hk, Sd, Ed, mode, out=out)
+                if ev is not None:
+                    ev[2].record(st)
+                if pipe is not None:
+                    pipe.start(k % 2, {f: out[f] for f in FIELDS[mode]}, n * world)
+                if peer is not None:
+                    peer.complete()  # device-side barrier: rank 0 holds every rank's rows
 
         for k in range(warmup):
             step(k)
@@ -446,10 +465,15 @@ def main():
         torch.cuda.synchronize(dev)
         launches0 = rsi.rsi_launch_count()
         t0.record(stream)
+        for st in sts:
+            st.wait_stream(stream)
         for k in range(steps):
-            step(k, evs[k])
-        if pipe is not None:
-            pipe.drain()  # every step's outputs are on rank 0 before the end event
+            step(k, None if overlap else evs[k])
+        with torch.cuda.stream(sts[(steps - 1) % len(sts)]):
+            if pipe is not None:
+                pipe.drain()  # every step's outputs are on rank 0 before the end event
+        for st in sts:
+            stream.wait_stream(st)
         t1.record(stream)
         launches = rsi.rsi_launch_count() - launches0
         torch.cuda.synchronize(dev)
@@ -458,15 +482,29 @@ def main():
         if sampler:
             sampler.__exit__()
         ms = t0.elapsed_time(t1)
-        build_ms = statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
-        query_ms = statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
+        # per-step build / query times only from the serial (non-overlapped) run:
+        # overlapped events would include waits for the other stream's SMs
+        build_ms = None if overlap else statistics.mean(e[0].elapsed_time(e[1]) for e in evs)
+        query_ms = None if overlap else statistics.mean(e[1].elapsed_time(e[2]) for e in evs)
         if world > 1:
-            tm = torch.tensor([ms, build_ms, query_ms], dtype=torch.float64, device=dev)
+            tm = torch.tensor([ms, build_ms or 0.0, query_ms or 0.0], dtype=torch.float64, device=dev)
             dist.all_reduce(tm, op=dist.ReduceOp.MAX)
-            ms, build_ms, query_ms = tm.tolist()
+            ms = tm[0].item()
+            if not overlap:
+                build_ms, query_ms = tm[1].item(), tm[2].item()
         return ms, build_ms, query_ms, (sampler.summary() if sampler else None), launches
 
-    ms, build_ms, query_ms, clk, launches = timed(args.mode, args.steps, max(args.warmup, 3), True)
+    def timed_pair(mode: str, steps: int, warmup: int, clocks: bool):
+        """The serial run (per-step build / query events: the roofline's kernel
+        time) and, with --overlap, the overlapped run that gives the value."""
+        s_ms, build_ms, query_ms, s_clk, s_launch = timed(mode, steps, warmup, clocks and not args.overlap)
+        if not args.overlap:
+            return s_ms, build_ms, query_ms, s_clk, s_launch, None
+        ms, _, _, clk, launches = timed(mode, steps, warmup, clocks, overlap=True)
+        return ms, build_ms, query_ms, clk, launches, {"serial_ms_per_step": s_ms / steps,
+                                                      "serial_value": n * world * steps / (s_ms * 1e-3)}
+
+    ms, build_ms, query_ms, clk, launches, serial = timed_pair(args.mode, args.steps, max(args.warmup, 3), True)
     total_rays = n * world * args.steps
     value = total_rays / (ms * 1e-3)
     extra = {}
@@ -474,10 +512,13 @@ def main():
         for m in ("barycentric", "intercept_count"):
             if m == args.mode:
                 continue
-            mms, mb, mq, _, _ = timed(m, args.steps, 3, False)
+            mms, mb, mq, _, _, mser = timed_pair(m, args.steps, 3, False)
             extra[m] = {"value": n * world * args.steps / (mms * 1e-3), "ms_per_step": mms / args.steps,
-                        "build_ms": mb, "query_ms": mq}
+                        "build_ms": mb, "query_ms": mq, "serial": mser}
     rsi.rsi_build_status(h)  # raises if any timed build failed its input checks
+    if h_b is not None:
+        rsi.rsi_build_status(h_b)
+        h_b.free()
     stats = rsi.rsi_get_stats(h)
 
     # the other BASELINE.json configs (parity-test workloads), timed on this GPU
@@ -488,20 +529,33 @@ def main():
             V2, T2, S2, E2 = workload_inputs(name, n_rays, 0)
             V2d, T2d = torch.from_numpy(V2).to(dev), torch.from_numpy(T2).to(dev)
             S2d, E2d = torch.from_numpy(S2).to(dev), torch.from_numpy(E2).to(dev)
-            o2 = rsi.alloc_outputs(n_rays, mode, dev)
-            with rsi.rsi_build(V2d, T2d) as h2:
-                for _ in range(3):
-                    rsi.rsi_rebuild(h2, V2d, T2d)
-                    rsi.rsi_intersect(h2, S2d, E2d, mode, out=o2)
-                torch.cuda.synchronize(dev)
-                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                a.record(stream)
-                for _ in range(3):
-                    rsi.rsi_rebuild(h2, V2d, T2d)
-                    rsi.rsi_intersect(h2, S2d, E2d, mode, out=o2)
-                b.record(stream)
-                torch.cuda.synchronize(dev)
-                ms3 = a.elapsed_time(b) / 3
+            # same step as the headline: rebuild + intersect, consecutive steps
+            # overlapped on two handles / streams unless --no-overlap
+            nh = 2 if args.overlap else 1
+            o2 = [rsi.alloc_outputs(n_rays, mode, dev) for _ in range(nh)]
+            h2 = [rsi.rsi_build(V2d, T2d) for _ in range(nh)]
+            st2 = [torch.cuda.Stream(dev) for _ in range(nh)] if args.overlap else [stream]
+
+            def run(k):
+                with torch.cuda.stream(st2[k % nh]):
+                    rsi.rsi_rebuild(h2[k % nh], V2d, T2d)
+                    rsi.rsi_intersect(h2[k % nh], S2d, E2d, mode, out=o2[k % nh])
+            for k in range(3):
+                run(k)
+            torch.cuda.synchronize(dev)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            for st in st2:
+                st.wait_stream(stream)
+            for k in range(3):
+                run(k)
+            for st in st2:
+                stream.wait_stream(st)
+            b.record(stream)
+            torch.cuda.synchronize(dev)
+            ms3 = a.elapsed_time(b) / 3
+            for hh in h2:
+                hh.free()
             return {"workload": f"{name} N_t={len(T2)}, N_r={n_rays}, {mode}", "value": n_rays / (ms3 * 1e-3),
                     "unit": UNIT, "ms_per_step": ms3}
         other["configs[0] cube all modes"] = [one_config("cube", m, 10_000)
@@ -601,7 +655,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded UV-sphere mesh, uniform segments; see DESIGN.md 4)",
             "config": arm_config(args, len(T), world, backend),
-            "build_ms": build_ms, "query_ms": query_ms,
+            "build_ms": build_ms, "query_ms": query_ms, "serial": serial,
             "roofline": roofline(args.mode, n, query_ms, clk["sm_mhz"] if clk else None, work, args.workload),
             "work_per_ray": work,
             "cpu_baseline": cpu, "e2e": e2e, "parity": parity,

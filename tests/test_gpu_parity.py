@@ -1156,3 +1156,31 @@ def test_sah_subtree_build_edge_cases(rsi, case):
     assert_parity(got, ref, S, E, case)
     if case == "outliers":
         assert got["hit"][:20].all() and (got["count"][20:40] == 2).all()
+
+
+def test_overlapped_steps_two_handles_two_streams(rsi):
+    """bench.py's overlapped steps: consecutive rebuild + intersect pairs
+    alternate between two handles and two streams with no host sync, so step
+    k+1's rebuild runs while step k's traversal is still in flight.  Every
+    step's outputs equal the oracle (all modes, every ray)."""
+    V, T, S, E, _ = synth.workload("sphere", 60_001, seed=17)
+    ref = oracle.run(V, T, S, E)
+    Vd, Td, Sd, Ed = to_dev(V, T, S, E)
+    hs = [rsi.rsi_build(Vd, Td, rsi.Options(deferred_status=True)) for _ in range(2)]
+    sts = [torch.cuda.Stream(), torch.cuda.Stream()]
+    modes = ("boolean", "barycentric", "intercept_count")
+    outs = [{m: rsi.alloc_outputs(len(S), m, DEV) for m in modes} for _ in range(6)]
+    torch.cuda.synchronize()
+    for k in range(6):
+        with torch.cuda.stream(sts[k % 2]):
+            rsi.rsi_rebuild(hs[k % 2], Vd, Td)
+            for m in modes:
+                rsi.rsi_intersect(hs[k % 2], Sd, Ed, m, out=outs[k][m])
+    torch.cuda.synchronize()
+    for h in hs:
+        rsi.rsi_build_status(h)
+        h.free()
+    for k in range(6):
+        got = {"hit": outs[k]["boolean"]["hit"].cpu().numpy(), "count": outs[k]["intercept_count"]["count"].cpu().numpy()}
+        got.update({f: v.cpu().numpy() for f, v in outs[k]["barycentric"].items()})
+        assert_parity(got, ref, S, E, f"step {k}")

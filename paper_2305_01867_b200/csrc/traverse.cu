@@ -190,17 +190,10 @@ __device__ __forceinline__ float ld_stream(const float* p) {
 // (reading R12).  `nonfinite` is set for the latter.
 // kNearFar: lx/hx become the offsets of each axis's NEAR / FAR plane (lo / hi
 // for inv >= 0, hi / lo for inv < 0) for the octant-selected quad slab test.
+// Ray setup from r.ox .. r.ez (already loaded); see load_ray.
 template <bool kNearFar = false>
-__device__ __forceinline__ bool load_ray(Ray& r, const float* __restrict__ S, const float* __restrict__ E,
-                                         int64_t i, bool& nonfinite, float qext = 0.0f, float lim_lo = 0.0f,
-                                         float lim_hi = INFINITY) {
-    // the segment stream is read once: do not let it displace tree nodes in L1
-    r.ox = ld_stream(S + 3 * i);
-    r.oy = ld_stream(S + 3 * i + 1);
-    r.oz = ld_stream(S + 3 * i + 2);
-    r.ex = ld_stream(E + 3 * i);
-    r.ey = ld_stream(E + 3 * i + 1);
-    r.ez = ld_stream(E + 3 * i + 2);
+__device__ __forceinline__ bool setup_ray(Ray& r, bool& nonfinite, float qext = 0.0f, float lim_lo = 0.0f,
+                                          float lim_hi = INFINITY) {
     nonfinite = !(isfinite(r.ox) && isfinite(r.oy) && isfinite(r.oz) && isfinite(r.ex) && isfinite(r.ey) &&
                   isfinite(r.ez));
     r.dx = r.ex - r.ox;
@@ -218,6 +211,41 @@ __device__ __forceinline__ bool load_ray(Ray& r, const float* __restrict__ S, co
         if (r.iz < 0.0f) { const float t = r.lz; r.lz = r.hz; r.hz = t; }
     }
     return !nonfinite && !(r.dx == 0.0f && r.dy == 0.0f && r.dz == 0.0f);
+}
+
+// Returns false for rays that cannot hit: zero length or a non-finite coordinate
+// (reading R12).  `nonfinite` is set for the latter.
+// kNearFar: lx/hx become the offsets of each axis's NEAR / FAR plane (lo / hi
+// for inv >= 0, hi / lo for inv < 0) for the octant-selected quad slab test.
+template <bool kNearFar = false>
+__device__ __forceinline__ bool load_ray(Ray& r, const float* __restrict__ S, const float* __restrict__ E,
+                                         int64_t i, bool& nonfinite, float qext = 0.0f, float lim_lo = 0.0f,
+                                         float lim_hi = INFINITY) {
+    // the segment stream is read once: do not let it displace tree nodes in L1
+    r.ox = ld_stream(S + 3 * i);
+    r.oy = ld_stream(S + 3 * i + 1);
+    r.oz = ld_stream(S + 3 * i + 2);
+    r.ex = ld_stream(E + 3 * i);
+    r.ey = ld_stream(E + 3 * i + 1);
+    r.ez = ld_stream(E + 3 * i + 2);
+    return setup_ray<kNearFar>(r, nonfinite, qext, lim_lo, lim_hi);
+}
+
+// Next-segment prefetch (RSI_RAY_PREFETCH): a lane claims the id of its NEXT
+// segment when it starts the current one and copies that segment's six floats
+// into its shared-memory column with cp.async (no registers held), so the
+// refill that starts it reads shared memory instead of waiting for HBM.
+// Measured and rejected (1e7 segments, query): sphere boolean 1.315 -> 1.347 ms,
+// barycentric 2.07 -> 2.20, intercept_count 3.31 -> 3.55; paper terrain
+// +6 / +9 / +11 % -- the 3 KB per CTA of columns come out of the L1 the
+// records live in, and the claim/commit logic adds spills (ray setup's HBM
+// wait, 7 % of the stall samples, is hidden by the other warps anyway).
+#ifndef RSI_RAY_PREFETCH
+#define RSI_RAY_PREFETCH 0
+#endif
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
 }
 
 // Conservative segment/box overlap on [0, tclip]; tnear is the (lowered) entry t.
@@ -1081,9 +1109,15 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), (MODE == MODE_BOOL ? RS
     // lanes without a segment take the next ids from the warp's chunk and set up
     // ---- 1. refill: lanes without a segment take the next ids from the warp's
     // chunk (one atomicAdd per kChunk segments per warp) and set them up
-    auto refill = [&]() {
-        unsigned want = __ballot_sync(FULL, ray < 0);
-        bool fresh = false;
+    constexpr bool kPf = RSI_RAY_PREFETCH && kQuad && !kStage;
+    __shared__ float s_nr[kPf ? 6 * kT : 1];
+    float* nr = s_nr + (kPf ? threadIdx.x : 0);  // this lane's column: S.xyz, E.xyz at stride kT
+    int nxt = -1;                                // kPf: the claimed next segment (data in flight to nr)
+    // lanes with no claimed segment take the next ids from the warp's chunk (one
+    // atomicAdd per kChunk segments per warp): kPf -- lanes without a next
+    // segment claim one and start its copy; else lanes without a segment
+    auto claim = [&](bool& fresh) {
+        unsigned want = __ballot_sync(FULL, kPf ? nxt < 0 : ray < 0);
         while (want && !exhausted) {
             if (cnext >= cend) {
                 unsigned long long base = 0;
@@ -1108,12 +1142,42 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), (MODE == MODE_BOOL ? RS
             const int rank = __popc(want & lt);
             const bool got = mine && rank < take;
             if (got) {
-                ray = cnext + rank;
-                fresh = true;
+                if (kPf) {
+                    nxt = cnext + rank;
+                    const float* sp3 = p.S + 3 * (int64_t)nxt;
+                    const float* ep3 = p.E + 3 * (int64_t)nxt;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        cp_async4(nr + c * kT, sp3 + c);
+                        cp_async4(nr + (3 + c) * kT, ep3 + c);
+                    }
+                    asm volatile("cp.async.commit_group;" ::: "memory");
+                } else {
+                    ray = cnext + rank;
+                    fresh = true;
+                }
             }
             want &= ~__ballot_sync(FULL, got);
             cnext += take;
         }
+    };
+    // ---- 1. refill: lanes without a segment start their claimed next one
+    // (kPf) or take the next ids from the warp's chunk, and set them up
+    auto refill = [&]() {
+        bool fresh = false;
+        if (kPf && ray < 0 && nxt >= 0) {
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            r.ox = nr[0];
+            r.oy = nr[kT];
+            r.oz = nr[2 * kT];
+            r.ex = nr[3 * kT];
+            r.ey = nr[4 * kT];
+            r.ez = nr[5 * kT];
+            ray = nxt;
+            nxt = -1;
+            fresh = true;
+        }
+        claim(fresh);
         if (fresh) {
             bool nonfinite;
             if (kQuad && kQcSmem) {
@@ -1121,7 +1185,8 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), (MODE == MODE_BOOL ? RS
                 qlim_lo = s_qc[1];
                 qlim_hi = s_qc[2];
             }
-            const bool ok = kQuad ? load_ray<true>(r, p.S, p.E, ray, nonfinite, qext, qlim_lo, qlim_hi)
+            const bool ok = kPf ? setup_ray<true>(r, nonfinite, qext, qlim_lo, qlim_hi)
+                          : kQuad ? load_ray<true>(r, p.S, p.E, ray, nonfinite, qext, qlim_lo, qlim_hi)
                                   : load_ray<false>(r, p.S, p.E, ray, nonfinite);
             if (nonfinite) st.add(ST_NONFINITE);
             ms.init();
@@ -1131,6 +1196,10 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), (MODE == MODE_BOOL ? RS
             node = ok ? root : -1;
         }
     };
+    if (kPf) {  // prologue: every lane claims its first segment
+        bool unused = false;
+        claim(unused);
+    }
     while (true) {
         refill();
         if (__ballot_sync(FULL, ray >= 0) == 0) break;  // no rays left for this warp

@@ -522,7 +522,7 @@ def main():
     stats = rsi.rsi_get_stats(h)
 
     # the other BASELINE.json configs (parity-test workloads), timed on this GPU
-    # for context: rays/s of rebuild + intersect per step, 3 warm-up + 3 timed steps
+    # for context: rays/s of rebuild + intersect per step, 3 warm-up + 10 timed steps
     other = {}
     if world == 1 and not args.no_configs:
         def one_config(name, mode, n_rays):
@@ -532,6 +532,7 @@ def main():
             # same step as the headline: rebuild + intersect, consecutive steps
             # overlapped on two handles / streams unless --no-overlap
             nh = 2 if args.overlap else 1
+            reps = 10  # timed steps (3 warm-ups)
             o2 = [rsi.alloc_outputs(n_rays, mode, dev) for _ in range(nh)]
             h2 = [rsi.rsi_build(V2d, T2d) for _ in range(nh)]
             st2 = [torch.cuda.Stream(dev) for _ in range(nh)] if args.overlap else [stream]
@@ -547,13 +548,13 @@ def main():
             a.record(stream)
             for st in st2:
                 st.wait_stream(stream)
-            for k in range(3):
+            for k in range(reps):
                 run(k)
             for st in st2:
                 stream.wait_stream(st)
             b.record(stream)
             torch.cuda.synchronize(dev)
-            ms3 = a.elapsed_time(b) / 3
+            ms3 = a.elapsed_time(b) / reps
             for hh in h2:
                 hh.free()
             return {"workload": f"{name} N_t={len(T2)}, N_r={n_rays}, {mode}", "value": n_rays / (ms3 * 1e-3),

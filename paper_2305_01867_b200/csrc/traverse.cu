@@ -157,8 +157,26 @@ struct Ray {
 // since 2^-21 / 4 = 2 * 2^-24), and axes whose |inv| falls outside
 // [lim_lo, lim_hi] are left unconstrained (conservative) so that s * inv stays
 // an exact normal float and no term can overflow.
+#ifndef RSI_SLAB_BF
+#define RSI_SLAB_BF 1  // branch-free ray setup (selects instead of the nested branches): sphere 1e7
+                       // boolean -0.7 %, intercept_count -2.5 %, barycentric 0; paper terrain +-1 %
+#endif
 __device__ __forceinline__ void slab_axis(float o, float d, float& inv, float& offlo, float& offhi,
                                           float qext = 0.0f, float lim_lo = 0.0f, float lim_hi = INFINITY) {
+    if (RSI_SLAB_BF) {  // the same values as the branches below, computed unconditionally
+        float r;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
+        const float ai = fabsf(r);
+        const float oinv = o * r;
+        const float slack = kSlack * fmaf(qext, ai, 1.0f + fabsf(oinv));
+        const float sg = r > 0.0f ? slack : -slack;
+        const float a = oinv + sg, b = oinv - sg;
+        const bool ok = fabsf(d) >= 1e-30f && ai >= lim_lo && ai <= lim_hi && ai > 0.0f && isfinite(a) && isfinite(b);
+        inv = ok ? r : 0.0f;
+        offlo = ok ? a : INFINITY;
+        offhi = ok ? b : -INFINITY;
+        return;
+    }
     if (fabsf(d) >= 1e-30f) {
         asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(inv) : "f"(d));
         const float ai = fabsf(inv);

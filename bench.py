@@ -406,6 +406,8 @@ def main():
     # a second handle for the overlapped steps (below); built once, rebuilt every step
     h_b = rsi.rsi_build(Vd, Td, rsi.Options(deferred_status=True)) if args.overlap else None
 
+    last_out = {}
+
     def timed(mode: str, steps: int, warmup: int, clocks: bool, overlap: bool = False):
         # N > 1: the gather of step k (NCCL, its own stream) overlaps the build +
         # traversal of step k+1; two output slots, each reused only after its
@@ -492,6 +494,8 @@ def main():
             ms = tm[0].item()
             if not overlap:
                 build_ms, query_ms = tm[1].item(), tm[2].item()
+        if world == 1 or peer is None:  # the last timed step's outputs (parity block below)
+            last_out[mode] = outs[(steps - 1) % len(outs)]
         return ms, build_ms, query_ms, (sampler.summary() if sampler else None), launches
 
     def timed_pair(mode: str, steps: int, warmup: int, clocks: bool):
@@ -534,7 +538,7 @@ def main():
             nh = 2 if args.overlap else 1
             reps = 10  # timed steps (3 warm-ups)
             o2 = [rsi.alloc_outputs(n_rays, mode, dev) for _ in range(nh)]
-            h2 = [rsi.rsi_build(V2d, T2d) for _ in range(nh)]
+            h2 = [rsi.rsi_build(V2d, T2d, rsi.Options(deferred_status=True)) for _ in range(nh)]
             st2 = [torch.cuda.Stream(dev) for _ in range(nh)] if args.overlap else [stream]
 
             def run(k):
@@ -556,6 +560,7 @@ def main():
             torch.cuda.synchronize(dev)
             ms3 = a.elapsed_time(b) / reps
             for hh in h2:
+                rsi.rsi_build_status(hh)
                 hh.free()
             return {"workload": f"{name} N_t={len(T2)}, N_r={n_rays}, {mode}", "value": n_rays / (ms3 * 1e-3),
                     "unit": UNIT, "ms_per_step": ms3}
@@ -638,9 +643,20 @@ def main():
         # three modes for the same rays of the timed workload (same kernels and
         # launch configuration as the timed steps)
         k = len(ref["hit"])
+        # the outputs the LAST TIMED STEP of each mode wrote (overlapped steps,
+        # full-size launch), sliced to the oracle's sample; a mode that was not
+        # timed (--no-extra-modes) is recomputed on the same handle
         got = gpu_outputs(h, Sd[:k], Ed[:k])
+        timed_src = []
+        for m, fields in (("boolean", ("hit",)), ("intercept_count", ("count",)),
+                          ("barycentric", ("tri", "t", "dist", "point"))):
+            if m in last_out:
+                got.update({f: last_out[m][f][:k].cpu().numpy() for f in fields})
+                timed_src.append(m)
         parity = {"bench": parity_report(got, ref, S[:k], E[:k], f"{args.workload} N_t={len(T)}, "
                                                                    f"first {k} rays of the timed workload")}
+        parity["bench"]["outputs"] = (f"last timed step's outputs of {', '.join(timed_src)}"
+                                      if timed_src else "recomputed on the timed handle")
         if not args.no_parity:  # the 1e6-triangle mesh of configs[4] (L2-sized tree)
             V1, T1, S1, E1 = workload_inputs("sphere1m", 20_000, 0)
             ref1 = oracle_run(V1, T1, S1, E1)

@@ -67,3 +67,19 @@ for nt in (20000, 40000):
     assert rsi.rsi_validate(h)["ok"]
     h.free()
 print("sanitize round-2 paths ok")
+# bench.py's overlapped steps: two handles on two streams, rebuild + intersect
+# alternating with no host sync (step k+1's build runs beside step k's walk)
+V2, T2, S2, E2, _ = synth.workload("sphere", 20000, seed=5)
+Vd, Td, Sd, Ed = (torch.from_numpy(a).to(dev) for a in (V2, T2, S2, E2))
+hs = [rsi.rsi_build(Vd, Td, rsi.Options(deferred_status=True)) for _ in range(2)]
+sts = [torch.cuda.Stream(), torch.cuda.Stream()]
+for k in range(4):
+    with torch.cuda.stream(sts[k % 2]):
+        rsi.rsi_rebuild(hs[k % 2], Vd, Td)
+        for m in ("boolean", "barycentric", "intercept_count"):
+            rsi.rsi_intersect(hs[k % 2], Sd, Ed, m)
+torch.cuda.synchronize()
+for h in hs:
+    rsi.rsi_build_status(h)
+    h.free()
+print("sanitize overlapped steps ok")

@@ -1,9 +1,9 @@
 #!/bin/bash
-# scratch A/B driver (GPU box): intercept_count at 8 CTAs / SM (64 registers)
+# scratch A/B driver (GPU box): rsi_test pipeline (H2D streams x slots)
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/ab_build.log 2>&1
-python - <<'PY' >> gpurun_out/ab_build.log 2>&1
-from paper_2305_01867_b200 import _build
-_build.build_variant("cm7", {"RSI_COUNT_MINB": 7})
-_build.build_variant("cm8", {"RSI_COUNT_MINB": 8})
-PY
-MODES=intercept_count bash tools/variants.sh "cm7 cm8 cm7 cm8" "sphere terrain paper_terrain" > gpurun_out/ab.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "rsi_test or sparse or pycuda" > gpurun_out/ab.log 2>&1
+for rep in 1 2; do
+for cfg in "1 2" "2 4" "2 3" "1 4" "2 6"; do
+  set -- $cfg
+  RSI_TEST_H2D=$1 RSI_TEST_SLOTS=$2 timeout 300 python tools/e2e_probe.py >> gpurun_out/ab.log 2>&1
+done; done

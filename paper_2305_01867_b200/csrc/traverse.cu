@@ -283,6 +283,12 @@ __device__ __forceinline__ bool slab(const Ray& r, float lox, float hix, float l
 // expression on absolute values with + for -): |fl(X) - X| <= ~10u M_X, so a
 // sign test on X is certain when |X| > 16u M_X (+ an underflow floor).
 // Returns MT_MISS / MT_HIT (with t and a bound et on |t - t_exact|) / MT_UNSURE.
+#ifndef RSI_MT_RCP
+#define RSI_MT_RCP 1
+#endif
+#ifndef RSI_FAST_NORM
+#define RSI_FAST_NORM 1  // |d| by one sqrt unless |d|^2 leaves [1e-30, 1e30] (then norm3df's scaling)
+#endif
 __device__ __forceinline__ int mt32(const Ray& r, const float4& A, const float4& B, const float4& C, float& t,
                                     float& et) {
     const float e1x = B.x - A.x, e1y = B.y - A.y, e1z = B.z - A.z;
@@ -320,8 +326,20 @@ __device__ __forceinline__ int mt32(const Ray& r, const float4& A, const float4&
     const float bz = fmaf(kFilt, Mdet + Mt, kTiny);
     if (z < -bz) return MT_MISS;
     if (nu > bu && nv > bv && w > bw && nt > bt && z > bz) {
+#if RSI_MT_RCP
+        // one approximate reciprocal instead of two IEEE divisions: rcp.approx
+        // (relative error <= 2^-23, see slab_axis) times nt adds <= 2.5u |t| <=
+        // 2.5u (a certified hit has 0 <= t <= 1) to t, covered by the constant
+        // term (3u -> 6u); the bound's own roundings (< 4u relative of a 12u
+        // term) by kTerr 12u -> 13u.  adet > 1e-30 here: a normal float.
+        float ra;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(adet));
+        t = nt * ra;
+        et = fmaf(13.0f * kU, (Mt + Mdet) * ra, 6.0f * kU);
+#else
         t = __fdiv_rn(nt, adet);
         et = kTerr * (Mt + Mdet) / adet + 3.0f * kU;
+#endif
         return MT_HIT;
     }
     return MT_UNSURE;
@@ -618,7 +636,15 @@ struct ModeState<MODE_BARY> {
             }
             tri[0] = id;
             if (t) t[0] = tt;
-            if (dist) dist[0] = tt * norm3df(r.dx, r.dy, r.dz);  // no overflow / underflow of |d|^2
+            if (dist) {
+#if RSI_FAST_NORM
+                const float d2 = fmaf(r.dx, r.dx, fmaf(r.dy, r.dy, r.dz * r.dz));
+                const float nd = (d2 >= 1e-30f && d2 <= 1e30f) ? sqrtf(d2) : norm3df(r.dx, r.dy, r.dz);
+                dist[0] = tt * nd;
+#else
+                dist[0] = tt * norm3df(r.dx, r.dy, r.dz);  // no overflow / underflow of |d|^2
+#endif
+            }
             if (point) {
                 point[0] = fmaf(tt, r.dx, r.ox);
                 point[1] = fmaf(tt, r.dy, r.oy);

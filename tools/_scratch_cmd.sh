@@ -1,9 +1,12 @@
 #!/bin/bash
-# scratch A/B driver (GPU box): rsi_test pipeline (H2D streams x slots)
+# scratch A/B driver (GPU box): approximate reciprocal in the MT hit path + fast |d|
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/ab_build.log 2>&1
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "rsi_test or sparse or pycuda" > gpurun_out/ab.log 2>&1
-for rep in 1 2; do
-for cfg in "1 2" "2 4" "2 3" "1 4" "2 6"; do
-  set -- $cfg
-  RSI_TEST_H2D=$1 RSI_TEST_SLOTS=$2 timeout 300 python tools/e2e_probe.py >> gpurun_out/ab.log 2>&1
-done; done
+timeout 900 python -m pytest tests -m gpu -q -x -p no:cacheprovider > gpurun_out/ab_pytest.log 2>&1
+tail -2 gpurun_out/ab_pytest.log > gpurun_out/ab.log
+python - <<'PY' >> gpurun_out/ab_build.log 2>&1
+from paper_2305_01867_b200 import _build
+_build.build_variant("mr1", {"RSI_MT_RCP": 1, "RSI_FAST_NORM": 1})
+_build.build_variant("mr0", {"RSI_MT_RCP": 0, "RSI_FAST_NORM": 0})
+PY
+MODES=barycentric,intercept_count bash tools/variants.sh "mr1 mr0 mr1 mr0" "sphere paper_terrain terrain" >> gpurun_out/ab.log 2>&1
+timeout 1200 python tools/parity_full.py > gpurun_out/parity_full_mr.json 2>&1

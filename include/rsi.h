@@ -33,6 +33,11 @@
  *     scratch (ray dispenser, overflow counters), which every call resets.
  *     rsi_free frees after the last call.  Work on distinct handles is not
  *     ordered.
+ *   - Pipelining (what bench.py does): a caller that rebuilds and queries every
+ *     step can alternate two handles (built with RSI_OPT_DEFERRED_STATUS) on
+ *     two streams, so that step k+1's rebuild runs in the SM slots step k's
+ *     traversal frees at its end; each handle's own calls stay in call order,
+ *     and rsi_build_status reports each handle's input checks afterwards.
  */
 #ifndef RSI_H_
 #define RSI_H_

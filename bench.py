@@ -70,7 +70,7 @@ FP32_LANES = 128
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     # 1.25e7 per GPU: --gpus 8 is exactly the north-star row N_t = 1e4, N_r = 1e8
@@ -108,7 +108,7 @@ class ClockSampler:
     def _run(self):
         try:
             p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                  "-i", str(self.index), "-lms", "100"], stdout=subprocess.PIPE, text=True)
+                                  "-i", str(self.index), "-lms", "20"], stdout=subprocess.PIPE, text=True)
         except OSError:
             return
         while not self._stop.is_set():

@@ -258,6 +258,10 @@ __device__ __forceinline__ bool load_ray(Ray& r, const float* __restrict__ S, co
 // +6 / +9 / +11 % -- the 3 KB per CTA of columns come out of the L1 the
 // records live in, and the claim/commit logic adds spills (ray setup's HBM
 // wait, 7 % of the stall samples, is hidden by the other warps anyway).
+#ifndef RSI_RAY_PF_L1
+#define RSI_RAY_PF_L1 1  // intercept_count: L1 prefetch of the chunk's next segments at each refill
+                         // (sphere -2 %, terrain -1 %; boolean +1 %, barycentric +2 %: count only)
+#endif
 #ifndef RSI_RAY_PREFETCH
 #define RSI_RAY_PREFETCH 0
 #endif
@@ -1226,6 +1230,17 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), (MODE == MODE_BOOL ? RS
             fresh = true;
         }
         claim(fresh);
+        if (RSI_RAY_PF_L1 && MODE == MODE_COUNT && !kPf && !exhausted && cnext < cend) {
+            // L1 prefetch of the 128-byte lines holding the chunk's next 32
+            // segments (start and end arrays): the refill that hands them out
+            // then finds them in L1.  Lanes 0..3 cover start, 4..7 end.
+            const int j1 = min(cnext + 32, cend);
+            const int a = lane & 3;
+            const float* base = lane < 4 ? p.S : p.E;
+            const uint64_t b0 = (reinterpret_cast<uint64_t>(base + 3 * (int64_t)cnext) & ~(uint64_t)127) + 128u * a;
+            const uint64_t b1 = reinterpret_cast<uint64_t>(base + 3 * (int64_t)j1);
+            if (lane < 8 && b0 < b1) asm volatile("prefetch.global.L1 [%0];" ::"l"(b0));
+        }
         if (fresh) {
             bool nonfinite;
             if (kQuad && kQcSmem) {

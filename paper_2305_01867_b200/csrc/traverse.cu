@@ -343,7 +343,7 @@ __device__ __forceinline__ int mt32(const Ray& r, const float4& A, const float4&
         float ra;
         asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(ra) : "f"(adet));
         t = nt * ra;
-        et = fmaf(13.0f * kU, (Mt + Mdet) * ra, 6.0f * kU);
+        et = fmaf(kTerr + kU, (Mt + Mdet) * ra, 6.0f * kU);
 #else
         t = __fdiv_rn(nt, adet);
         et = kTerr * (Mt + Mdet) / adet + 3.0f * kU;

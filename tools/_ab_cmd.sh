@@ -1,9 +1,9 @@
 #!/bin/bash
-# scratch A/B driver (GPU box): rsi_test short head chunk per mode
+# scratch A/B driver (GPU box): L2 prefetch of the chunk's next segments (boolean / barycentric)
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/ab_build.log 2>&1
-rm -f gpurun_out/ab.log
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "rsi_test or sparse or pycuda" > gpurun_out/ab.log 2>&1
-for rep in 1 2; do for head in 0 262144 131072 65536; do
-  RSI_TEST_HEAD=$head MODES=boolean,barycentric,intercept_count timeout 300 python tools/e2e_probe.py >> gpurun_out/ab.log 2>&1
-done; done
-RSI_TEST_HEAD=131072 timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "rsi_test or sparse or pycuda" >> gpurun_out/ab.log 2>&1
+python - <<'PY' >> gpurun_out/ab_build.log 2>&1
+from paper_2305_01867_b200 import _build
+_build.build_variant("p21", {"RSI_RAY_PF_L2": 1})
+_build.build_variant("p20", {"RSI_RAY_PF_L2": 0})
+PY
+MODES=boolean,barycentric bash tools/variants.sh "p21 p20 p21 p20" "sphere paper_terrain" > gpurun_out/ab.log 2>&1

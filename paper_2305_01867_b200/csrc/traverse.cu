@@ -115,7 +115,7 @@ constexpr int kCountCap = RSI_COUNT_CAP;
 #define RSI_BARY_MINB 8
 #endif
 #ifndef RSI_COUNT_MINB
-#define RSI_COUNT_MINB 7
+#define RSI_COUNT_MINB 7  // 72 registers; round 2: 8 CTAs +6..13 %, 6 CTAs +7..8 %
 #endif
 // k_trace block size: with the top-of-tree cache, one CTA per SM shares the
 // image (1024 threads at <= 64 registers for boolean, 768 at <= 80 otherwise)
@@ -1320,7 +1320,7 @@ __global__ void __launch_bounds__(trace_threads<MODE>(), (MODE == MODE_BOOL ? RS
                 const float inv3[3] = {r.ix, r.iy, r.iz};
                 const float scv[3] = {qa.w, qd.z, qd.w};  // grid steps s = 2^e
                 // octant masks: kept per ray, except for intercept_count (register
-                // pressure at 80 registers: derived from the sign of inv per visit)
+                // pressure at 72 registers: derived from the sign of inv per visit)
                 const uint32_t msk[3] = {
                     MODE == MODE_COUNT ? (uint32_t)(__float_as_int(r.ix) >> 31) : r.mx,
                     MODE == MODE_COUNT ? (uint32_t)(__float_as_int(r.iy) >> 31) : r.my,

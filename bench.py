@@ -144,22 +144,30 @@ def workload_inputs(name: str, n: int, rank: int):
     return V, T, S, E
 
 
+def host_cores() -> int:
+    """Host cores this process may run on (the oracle's thread count)."""
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return max(1, os.cpu_count() or 1)
+
+
 def cpu_baseline(V, T, S, E, target_s=20.0, sample=0):
     """The oracle (as it stands, with its ambiguity flags) on a bounded sample
     of the same workload.  Returns (cpu_baseline dict, oracle results on the
     sample) -- the results feed the parity report."""
     import oracle
-    cores = oracle.max_threads()
+    cores = host_cores()
     if sample <= 0:
         # calibrate with a small run, then size for ~target_s of CPU work
         n0 = 200
-        oracle.run(V, T, S[:n0], E[:n0])  # thread pool start-up outside the calibration
+        oracle.run(V, T, S[:n0], E[:n0], threads=cores)  # thread pool start-up outside the calibration
         t = time.perf_counter()
-        oracle.run(V, T, S[:n0], E[:n0])
+        oracle.run(V, T, S[:n0], E[:n0], threads=cores)
         dt = max(time.perf_counter() - t, 1e-3)
         sample = int(min(len(S), max(n0, n0 * target_s / dt)))
     t = time.perf_counter()
-    ref = oracle.run(V, T, S[:sample], E[:sample])
+    ref = oracle.run(V, T, S[:sample], E[:sample], threads=cores)
     dt = time.perf_counter() - t
     return ({"value": sample / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
              "sample": f"first {sample} rays of the workload x all {len(T)} triangles, all modes + ambiguity "
@@ -340,18 +348,20 @@ def run_reference(args, rank: int, world: int):
         return
     V, T, S, E = workload_inputs(args.workload, max(args.rays_per_gpu // 5, 20000), 0)
     import oracle
-    cores = oracle.max_threads()
+    # every host core this process may use: torchrun sets OMP_NUM_THREADS=1 per
+    # rank, but rank 0 is the only one working here
+    cores = host_cores()
     n0 = 100
-    oracle.run(V, T, S[:n0], E[:n0])  # thread pool start-up outside the calibration
+    oracle.run(V, T, S[:n0], E[:n0], threads=cores)  # thread pool start-up outside the calibration
     t = time.perf_counter()
-    oracle.run(V, T, S[:n0], E[:n0])
+    oracle.run(V, T, S[:n0], E[:n0], threads=cores)
     dt = max(time.perf_counter() - t, 1e-3)
     per_step = int(max(n0, min(len(S), n0 * 4.0 / dt)))   # ~4 s of CPU per step
     for i in range(args.warmup):
-        oracle.run(V, T, S[:per_step], E[:per_step])
+        oracle.run(V, T, S[:per_step], E[:per_step], threads=cores)
     t = time.perf_counter()
     for i in range(args.steps):
-        oracle.run(V, T, S[:per_step], E[:per_step])
+        oracle.run(V, T, S[:per_step], E[:per_step], threads=cores)
     el = time.perf_counter() - t
     value = per_step * args.steps / el
     sample = (f"first {per_step} rays of the workload per step x all {len(T)} triangles, "
